@@ -1,0 +1,197 @@
+/*
+ * scmoe.h -- C ABI of the B200-native ScMoE layer (LongCat-Flash shortcut-
+ * connected MoE with zero-computation experts).
+ *
+ * This is the drop-in boundary for the reference's hot path (moelab,
+ * /root/reference/proj/include/moelab).  Every entry point names the
+ * reference function it replaces.  Plain C: opaque handles, plain pointers
+ * and sizes, int status codes; no C++ or torch types.
+ *
+ * Two tiers:
+ *   - device tier: pointers are device pointers, calls are stream-ordered on
+ *     the context's stream and return as soon as the work is enqueued;
+ *   - host tier (suffix _host): pointers are host pointers, the call copies
+ *     inputs in, runs the device tier and copies results out before it
+ *     returns.  This is what the C++ compat headers (include/moelab_b200/)
+ *     and the reference-facing bindings use.
+ *
+ * Errors: a C ABI cannot throw, so the reference's exception taxonomy
+ * (common.hpp:11-33) is returned as a status code; scmoe_last_error(ctx)
+ * gives the message.  Host-checkable errors (ConfigError, DimensionError)
+ * are returned by the call itself.  Data-dependent errors found on the
+ * device by device-tier calls (StateError for an expert index out of range,
+ * blocks.hpp:375-377) are latched in the context and returned by the next
+ * scmoe_synchronize(ctx); host-tier calls always synchronize and return them
+ * directly.
+ *
+ * Thread safety: no global mutable state; one context per calling thread.
+ */
+#ifndef SCMOE_H
+#define SCMOE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SCMOE_OK = 0,
+    SCMOE_ERR_CONFIG = 1,    /* moelab::ConfigError    (common.hpp:21) */
+    SCMOE_ERR_DIMENSION = 2, /* moelab::DimensionError (common.hpp:13) */
+    SCMOE_ERR_STATE = 3,     /* moelab::StateError     (common.hpp:25) */
+    SCMOE_ERR_PARAMETER = 4, /* moelab::ParameterError (common.hpp:17) */
+    SCMOE_ERR_CUDA = 5,      /* device / driver failure (no reference equivalent) */
+    SCMOE_ERR_INTERNAL = 6
+} scmoe_status;
+
+/* Expert-bank storage precision. */
+typedef enum {
+    SCMOE_PREC_F32_EXACT = 0, /* fp32 weights in the reference layout; sequential-k SIMT
+                                 kernels, bitwise equal to moe_forward<float> */
+    SCMOE_PREC_BF16 = 1       /* bf16 weights, transposed K-major for the tcgen05 grouped
+                                 GEMM (fp32 accumulate); rel-L2 <= 2e-2 vs the oracle */
+} scmoe_precision;
+
+/* GammaMode (blocks.hpp:185): FfnOnly / All / Off. */
+typedef enum { SCMOE_GAMMA_FFN_ONLY = 0, SCMOE_GAMMA_ALL = 1, SCMOE_GAMMA_OFF = 2 } scmoe_gamma_mode;
+
+typedef struct scmoe_ctx scmoe_ctx;
+typedef struct scmoe_router scmoe_router;
+typedef struct scmoe_bank scmoe_bank;
+
+/* ---- context ------------------------------------------------------------ */
+int scmoe_ctx_create(int device, scmoe_ctx** out);
+int scmoe_ctx_destroy(scmoe_ctx* ctx);
+const char* scmoe_last_error(const scmoe_ctx* ctx);
+/* Use a caller-owned cudaStream_t (NULL restores the context's own stream). */
+int scmoe_set_stream(scmoe_ctx* ctx, void* cuda_stream);
+void* scmoe_get_stream(const scmoe_ctx* ctx);
+/* Waits for the stream; returns (and clears) any latched device-side error. */
+int scmoe_synchronize(scmoe_ctx* ctx);
+/* Number of kernels this context has launched (instrumentation). */
+uint64_t scmoe_kernel_launches(const scmoe_ctx* ctx);
+const char* scmoe_version(void);
+
+/* Device memory helpers for callers without their own allocator. */
+int scmoe_device_alloc(scmoe_ctx* ctx, size_t bytes, void** out);
+int scmoe_device_free(scmoe_ctx* ctx, void* p);
+int scmoe_copy_h2d(scmoe_ctx* ctx, void* dst_dev, const void* src_host, size_t bytes);
+int scmoe_copy_d2h(scmoe_ctx* ctx, void* dst_host, const void* src_dev, size_t bytes);
+
+/* ---- router: RouterState<float> (router.hpp:20-62) ------------------------ */
+/* Constructor + validate(); ConfigError exactly where RouterState throws. */
+int scmoe_router_create(scmoe_ctx* ctx, size_t d_model, size_t n_ffn, size_t n_zero,
+                        size_t top_k, size_t k_expected, double mu, double mu_decay,
+                        scmoe_router** out);
+int scmoe_router_destroy(scmoe_ctx* ctx, scmoe_router* r);
+/* w: [d_model, n_ffn+n_zero] row-major fp32 (RouterState::w). */
+int scmoe_router_set_weights_host(scmoe_ctx* ctx, scmoe_router* r, const float* w);
+int scmoe_router_set_weights(scmoe_ctx* ctx, scmoe_router* r, const float* w_dev);
+/* b: [E] doubles; ConfigError if a zero-expert bias is non-zero (router.hpp:59-60). */
+int scmoe_router_set_bias_host(scmoe_ctx* ctx, scmoe_router* r, const double* b);
+int scmoe_router_get_bias_host(scmoe_ctx* ctx, scmoe_router* r, double* b);
+int scmoe_router_set_mu(scmoe_ctx* ctx, scmoe_router* r, double mu, double mu_decay);
+int scmoe_router_get_mu(scmoe_ctx* ctx, scmoe_router* r, double* mu, double* mu_decay);
+/* tokens_routed [E] u64 and tokens_seen (router.hpp:30-31). */
+int scmoe_router_get_counters_host(scmoe_ctx* ctx, scmoe_router* r, uint64_t* tokens_routed,
+                                   uint64_t* tokens_seen);
+int scmoe_router_set_counters_host(scmoe_ctx* ctx, scmoe_router* r, const uint64_t* tokens_routed,
+                                   uint64_t tokens_seen);
+/* Device pointer to the router's [E] u64 counters (for EP all-reduce). */
+uint64_t* scmoe_router_counters_dev(scmoe_router* r);
+const double* scmoe_router_bias_dev(scmoe_router* r);
+
+/* route_topk (router.hpp:133-141): logits = x W (fp32, sequential k, no FMA),
+ * softmax_rows (tensor.hpp:174-192, glibc-expf port), biased top-K with
+ * lowest-index ties (router.hpp:90-104), unbiased gates.
+ *   x [T, d] fp32; indices [T*K] u32; gates [T*K] f64; ffn_count [T] u32;
+ *   probs [T, E] fp32 or NULL (router.hpp:139 probs_out). */
+int scmoe_route_topk(scmoe_ctx* ctx, scmoe_router* r, const float* x, size_t tokens,
+                     uint32_t* indices, double* gates, uint32_t* ffn_count, float* probs);
+int scmoe_route_topk_host(scmoe_ctx* ctx, scmoe_router* r, const float* x, size_t tokens,
+                          uint32_t* indices, double* gates, uint32_t* ffn_count, float* probs);
+/* route_from_probs (router.hpp:107-130) on given probabilities [T, E]. */
+int scmoe_route_from_probs_f32(scmoe_ctx* ctx, scmoe_router* r, const float* probs, size_t tokens,
+                               uint32_t* indices, double* gates, uint32_t* ffn_count);
+int scmoe_route_from_probs_f64(scmoe_ctx* ctx, scmoe_router* r, const double* probs, size_t tokens,
+                               uint32_t* indices, double* gates, uint32_t* ffn_count);
+int scmoe_route_from_probs_f32_host(scmoe_ctx* ctx, scmoe_router* r, const float* probs,
+                                    size_t tokens, uint32_t* indices, double* gates,
+                                    uint32_t* ffn_count);
+int scmoe_route_from_probs_f64_host(scmoe_ctx* ctx, scmoe_router* r, const double* probs,
+                                    size_t tokens, uint32_t* indices, double* gates,
+                                    uint32_t* ffn_count);
+/* accumulate_counters (router.hpp:144-150): slot-counted, zero experts included. */
+int scmoe_accumulate_counters(scmoe_ctx* ctx, scmoe_router* r, const uint32_t* indices,
+                              size_t tokens);
+int scmoe_accumulate_counters_host(scmoe_ctx* ctx, scmoe_router* r, const uint32_t* indices,
+                                   size_t tokens);
+/* bias_update (router.hpp:155-176).  StateError on an empty batch or counters
+ * that do not cover K slots per token.  delta [E] (host) may be NULL. */
+int scmoe_bias_update(scmoe_ctx* ctx, scmoe_router* r, double* delta);
+
+/* ---- expert bank: ExpertBank<float> (blocks.hpp:203-213) ------------------ */
+int scmoe_bank_create(scmoe_ctx* ctx, size_t n_ffn, size_t d_model, size_t inter,
+                      int precision, size_t segmentation_m, int gamma_mode, scmoe_bank** out);
+int scmoe_bank_destroy(scmoe_ctx* ctx, scmoe_bank* b);
+/* w_in [d, inter], w_out [inter, d] row-major fp32 (Parameter::value). */
+int scmoe_bank_set_expert_host(scmoe_ctx* ctx, scmoe_bank* b, size_t e, const float* w_in,
+                               const float* w_out);
+int scmoe_bank_set_expert(scmoe_ctx* ctx, scmoe_bank* b, size_t e, const float* w_in_dev,
+                          const float* w_out_dev);
+/* Synthetic weights generated on the device, bitwise equal to
+ * seeded_init<float>({d,inter}, Uniform, variance, CounterRng(seed).stream(stream0 + 2e))
+ * and stream(stream0 + 2e + 1) for w_out (rng.hpp:82-94). */
+int scmoe_bank_init_uniform(scmoe_ctx* ctx, scmoe_bank* b, uint64_t seed, uint64_t stream0,
+                            double variance);
+double scmoe_bank_gamma_ffn(const scmoe_bank* b);
+double scmoe_bank_gamma_zero(const scmoe_bank* b);
+size_t scmoe_bank_device_bytes(const scmoe_bank* b);
+
+/* moe_forward (blocks.hpp:372-394), optionally renormalised (moe_block
+ * renormalize=true, blocks.hpp:240-247) and with a fused residual
+ * out = residual + moe(x) (model.hpp:400).  x [T, d] fp32; indices/gates
+ * [T*K]; residual [T, d] or NULL; out [T, d] fp32. */
+int scmoe_moe_forward(scmoe_ctx* ctx, scmoe_bank* b, const float* x, size_t tokens,
+                      const uint32_t* indices, const double* gates, size_t top_k, size_t n_zero,
+                      int renormalize, const float* residual, float* out);
+int scmoe_moe_forward_host(scmoe_ctx* ctx, scmoe_bank* b, const float* x, size_t tokens,
+                           const uint32_t* indices, const double* gates, size_t top_k,
+                           size_t n_zero, int renormalize, const float* residual, float* out);
+
+/* Graph::rmsnorm forward (graph.hpp:322-335), fp32, eps as given (1e-6 default). */
+int scmoe_rmsnorm(scmoe_ctx* ctx, const float* x, const float* gain, size_t rows, size_t d,
+                  float eps, float* out);
+
+/* ScMoE layer, MoE branch of Model::build_layer (model.hpp:394-400):
+ *   hmoe = rmsnorm(a1, gain); probs = softmax(hmoe W_r); d = route_from_probs;
+ *   out = a3 + moe_block(hmoe, probs, d, bank, renormalize).
+ * gain may be NULL (unit gain).  indices/gates/ffn_count receive the routing. */
+int scmoe_layer_forward(scmoe_ctx* ctx, scmoe_router* r, scmoe_bank* b, const float* a1,
+                        const float* a3, const float* gain, size_t tokens, int renormalize,
+                        uint32_t* indices, double* gates, uint32_t* ffn_count, float* out);
+int scmoe_layer_forward_host(scmoe_ctx* ctx, scmoe_router* r, scmoe_bank* b, const float* a1,
+                             const float* a3, const float* gain, size_t tokens, int renormalize,
+                             uint32_t* indices, double* gates, uint32_t* ffn_count, float* out);
+
+/* ---- CounterRng (rng.hpp:15-64), host side, for synthetic inputs --------- */
+uint64_t scmoe_rng_stream_seed(uint64_t seed, uint64_t id);
+/* out[i] = (float) CounterRng(seed).normal_at(first + i)  (router.hpp:357-360) */
+void scmoe_rng_fill_normal_host(uint64_t seed, uint64_t first, size_t n, float* out, int threads);
+/* out[i] = seeded_init Uniform element first+i (rng.hpp:89-94), on the device. */
+int scmoe_rng_fill_uniform(scmoe_ctx* ctx, uint64_t seed, uint64_t first, size_t n,
+                           double variance, float* out_dev);
+
+/* ---- diagnostics ---------------------------------------------------------- */
+/* out[i] = device instantiation of the glibc-expf restatement used by the
+ * softmax and SiLU kernels (bit-exactness check against host libm). */
+int scmoe_debug_expf(scmoe_ctx* ctx, const float* in_dev, float* out_dev, size_t n);
+/* Same over the consecutive bit patterns first_bits, first_bits+1, ... */
+int scmoe_debug_expf_range(scmoe_ctx* ctx, uint32_t first_bits, float* out_dev, size_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SCMOE_H */

@@ -1,0 +1,449 @@
+/*
+ * scmoe_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain-C restatement of the reference's CPU algorithm for the ScMoE hot
+ * path (moelab, /root/reference/proj/include/moelab).  It is the checker the
+ * parity tests, __graft_entry__.smoke() and bench.py's cpu_baseline leg
+ * compare the CUDA path against.  Nothing in the product (libscmoe.so, the
+ * Python package, the compat headers) may link or call this file.
+ *
+ * Parity pin: every function below is checked in tests/test_oracle_*.py
+ * against (a) the golden vectors of the reference's own Catch2 tests
+ * (tests/test_router.cpp, tests/test_blocks.cpp, tests/test_core.cpp) and
+ * (b) the reference itself, compiled from its headers into
+ * oracle/_ref/libmoelab_ref.so by oracle/Makefile (oracle/ref_shim.cpp).
+ *
+ * Build flags matter: compile with -O2/-O3 and
+ * -ffp-contract=off and WITHOUT -march=native, exactly like the reference's
+ * CMake Release build.  Floating-point operations are written in the same
+ * order as the reference so results are bitwise identical.
+ *
+ * Error codes mirror the reference's exception taxonomy (common.hpp:11-33):
+ *   0 ok, 1 ConfigError, 2 DimensionError, 3 StateError, 4 ParameterError.
+ */
+#include <math.h>
+#include <stddef.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORC_OK 0
+#define ORC_CONFIG 1
+#define ORC_DIMENSION 2
+#define ORC_STATE 3
+#define ORC_PARAMETER 4
+
+#define ORC_NZ(x) ((x) > 0 ? (size_t)(x) : (size_t)1)
+
+/* ------------------------------------------------------------------------
+ * Counter RNG -- rng.hpp:15-64
+ * ---------------------------------------------------------------------- */
+
+/* rng.hpp:19-26 */
+uint64_t orc_mix64(uint64_t x) {
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdULL;
+    x ^= x >> 33;
+    x *= 0xc4ceb9fe1a85ec53ULL;
+    x ^= x >> 33;
+    return x;
+}
+
+/* rng.hpp:28-30 */
+uint64_t orc_hash2(uint64_t seed, uint64_t ctr) {
+    return orc_mix64(orc_mix64(seed + 0x9e3779b97f4a7c15ULL) ^ orc_mix64(ctr + 0xbf58476d1ce4e5b9ULL));
+}
+
+/* rng.hpp:35 -- CounterRng::stream(id) returns a generator seeded with this */
+uint64_t orc_stream_seed(uint64_t seed, uint64_t id) { return orc_hash2(seed, id ^ 0xa5a5a5a5a5a5a5a5ULL); }
+
+/* rng.hpp:40-42 */
+double orc_uniform01_at(uint64_t seed, uint64_t ctr) {
+    return ((double)(orc_hash2(seed, ctr) >> 11) + 1.0) * 0x1.0p-53;
+}
+
+/* rng.hpp:51-55 (Box-Muller on counters 2c, 2c+1) */
+double orc_normal_at(uint64_t seed, uint64_t ctr) {
+    const double u1 = orc_uniform01_at(seed, 2 * ctr);
+    const double u2 = orc_uniform01_at(seed, 2 * ctr + 1);
+    return sqrt(-2.0 * log(u1)) * cos(2.0 * 3.14159265358979323846 * u2);
+}
+
+/* router.hpp:357-360: x.data[i] = (S) batch_rng.normal_at(i), counters offset by `first` */
+void orc_fill_normal_f32(uint64_t seed, uint64_t first, uint64_t n, float* out) {
+    for (uint64_t i = 0; i < n; ++i) out[i] = (float)orc_normal_at(seed, first + i);
+}
+void orc_fill_normal_f64(uint64_t seed, uint64_t first, uint64_t n, double* out) {
+    for (uint64_t i = 0; i < n; ++i) out[i] = orc_normal_at(seed, first + i);
+}
+
+/* rng.hpp:89-94: Uniform init, element i drawn from counter i */
+int orc_seeded_uniform_f32(uint64_t seed, uint64_t first, uint64_t n, double variance, float* out) {
+    if (variance < 0.0) return ORC_PARAMETER;
+    if (variance == 0.0) {
+        memset(out, 0, n * sizeof(float));
+        return ORC_OK;
+    }
+    const double half_width = sqrt(3.0 * variance);
+    for (uint64_t i = 0; i < n; ++i) {
+        const double u = orc_uniform01_at(seed, first + i);
+        out[i] = (float)((2.0 * u - 1.0) * half_width);
+    }
+    return ORC_OK;
+}
+
+/* rng.hpp:95-111: TruncatedNormal init (64 rejection attempts per element) */
+int orc_seeded_tn_f64(uint64_t seed, uint64_t n, double variance, double* out) {
+    if (variance < 0.0) return ORC_PARAMETER;
+    if (variance == 0.0) {
+        memset(out, 0, n * sizeof(double));
+        return ORC_OK;
+    }
+    const double scale = sqrt(variance / 0.77374201465191098);
+    for (uint64_t i = 0; i < n; ++i) {
+        double z = 0.0;
+        int ok = 0;
+        for (uint64_t attempt = 0; attempt < 64; ++attempt) {
+            z = orc_normal_at(seed, (i << 6) | attempt);
+            if (z >= -2.0 && z <= 2.0) {
+                ok = 1;
+                break;
+            }
+        }
+        if (!ok) z = 0.0;
+        out[i] = z * scale;
+    }
+    return ORC_OK;
+}
+int orc_seeded_tn_f32(uint64_t seed, uint64_t n, double variance, float* out) {
+    if (variance < 0.0) return ORC_PARAMETER;
+    double* tmp = (double*)malloc(ORC_NZ(n) * sizeof(double));
+    int rc = orc_seeded_tn_f64(seed, n, variance, tmp);
+    for (uint64_t i = 0; i < n; ++i) out[i] = (float)tmp[i];
+    free(tmp);
+    return rc;
+}
+
+/* ------------------------------------------------------------------------
+ * Fixed-order kernels -- tensor.hpp:95-112 (mm_into), :174-192 (softmax_rows)
+ * Generated for S = float and S = double.
+ * ---------------------------------------------------------------------- */
+
+#define ORC_DEFINE_KERNELS(S, SUF, EXPF, SQRTF)                                                    \
+    /* tensor.hpp:95-112: c[i,j] = sum_p a[i,p]*b[p,j], p ascending, separate mul/add */           \
+    void orc_mm_##SUF(const S* a, const S* b, S* c, size_t m, size_t k, size_t n) {                \
+        for (size_t i = 0; i < m; ++i) {                                                           \
+            S* crow = c + i * n;                                                                   \
+            for (size_t j = 0; j < n; ++j) crow[j] = (S)0;                                         \
+            for (size_t p = 0; p < k; ++p) {                                                       \
+                const S av = a[i * k + p];                                                         \
+                const S* brow = b + p * n;                                                         \
+                for (size_t j = 0; j < n; ++j) crow[j] += av * brow[j];                            \
+            }                                                                                      \
+        }                                                                                          \
+    }                                                                                              \
+    /* tensor.hpp:174-192: row max, exp(in-mx), sequential sum, divide */                          \
+    void orc_softmax_rows_##SUF(const S* x, S* y, size_t rows, size_t cols) {                      \
+        for (size_t r = 0; r < rows; ++r) {                                                        \
+            const S* in = x + r * cols;                                                            \
+            S* out = y + r * cols;                                                                 \
+            S mx = in[0];                                                                          \
+            for (size_t j = 1; j < cols; ++j) mx = in[j] > mx ? in[j] : mx;                        \
+            S sum = (S)0;                                                                          \
+            for (size_t j = 0; j < cols; ++j) {                                                    \
+                out[j] = EXPF(in[j] - mx);                                                         \
+                sum += out[j];                                                                     \
+            }                                                                                      \
+            for (size_t j = 0; j < cols; ++j) out[j] /= sum;                                       \
+        }                                                                                          \
+    }                                                                                              \
+    /* graph.hpp:529-533: sign-branched logistic */                                                \
+    S orc_sigmoid_##SUF(S x) {                                                                     \
+        if (x >= (S)0) return (S)1 / ((S)1 + EXPF(-x));                                            \
+        const S e = EXPF(x);                                                                       \
+        return e / ((S)1 + e);                                                                     \
+    }                                                                                              \
+    /* graph.hpp:322-335: s2 += x*x (j ascending); inv = 1/sqrt(s2/d + eps); out = x*inv*g */      \
+    void orc_rmsnorm_##SUF(const S* x, const S* gain, size_t rows, size_t d, S eps, S* out) {      \
+        for (size_t r = 0; r < rows; ++r) {                                                        \
+            const S* xr = x + r * d;                                                               \
+            S s2 = (S)0;                                                                           \
+            for (size_t j = 0; j < d; ++j) s2 += xr[j] * xr[j];                                    \
+            const S inv = (S)1 / SQRTF(s2 / (S)d + eps);                                           \
+            for (size_t j = 0; j < d; ++j) out[r * d + j] = xr[j] * inv * gain[j];                 \
+        }                                                                                          \
+    }
+
+ORC_DEFINE_KERNELS(float, f32, expf, sqrtf)
+ORC_DEFINE_KERNELS(double, f64, exp, sqrt)
+
+float orc_expf(float x) { return expf(x); }
+/* libm expf over consecutive bit patterns (checker for the device port) */
+void orc_expf_range(uint32_t first_bits, size_t n, float* out) {
+    for (size_t i = 0; i < n; ++i) {
+        const uint32_t u = first_bits + (uint32_t)i;
+        float x;
+        memcpy(&x, &u, 4);
+        out[i] = expf(x);
+    }
+}
+
+/* ------------------------------------------------------------------------
+ * Router -- router.hpp:50-141
+ * ---------------------------------------------------------------------- */
+
+/* router.hpp:50-61 RouterState::validate */
+int orc_router_validate(size_t n_ffn, size_t n_zero, size_t top_k, size_t k_expected, double mu,
+                        const double* b) {
+    const size_t e = n_ffn + n_zero;
+    if (top_k > e) return ORC_CONFIG;
+    if (k_expected < 1 || k_expected > top_k) return ORC_CONFIG;
+    if (n_zero > 0 && k_expected >= top_k) return ORC_CONFIG;
+    if (n_zero < top_k - k_expected) return ORC_CONFIG;
+    if (mu < 0.0) return ORC_CONFIG;
+    if (b)
+        for (size_t i = n_ffn; i < e; ++i)
+            if (b[i] != 0.0) return ORC_CONFIG;
+    return ORC_OK;
+}
+
+/* router.hpp:90-104: K largest of double(p)+b, ordered (score desc, index asc).
+ * The comparator is a strict total order, so repeated arg-max extraction gives
+ * the same sequence as std::partial_sort. */
+#define ORC_DEFINE_SELECT(S, SUF)                                                                  \
+    void orc_select_topk_row_##SUF(const S* probs, const double* bias, size_t n_experts, size_t k, \
+                                   uint32_t* out_idx) {                                            \
+        unsigned char stack_taken[1024];                                                           \
+        unsigned char* taken = n_experts <= sizeof(stack_taken) ? stack_taken                      \
+                                                                : (unsigned char*)malloc(n_experts); \
+        memset(taken, 0, n_experts);                                                               \
+        for (size_t s = 0; s < k; ++s) {                                                           \
+            size_t best = (size_t)-1;                                                              \
+            double best_score = 0.0;                                                               \
+            for (size_t i = 0; i < n_experts; ++i) {                                               \
+                if (taken[i]) continue;                                                            \
+                const double sc = (double)probs[i] + bias[i];                                      \
+                if (best == (size_t)-1 || sc > best_score) {                                       \
+                    best = i;                                                                      \
+                    best_score = sc;                                                               \
+                }                                                                                  \
+            }                                                                                      \
+            taken[best] = 1;                                                                       \
+            out_idx[s] = (uint32_t)best;                                                           \
+        }                                                                                          \
+        if (taken != stack_taken) free(taken);                                                     \
+    }                                                                                              \
+    /* router.hpp:107-130 */                                                                       \
+    int orc_route_from_probs_##SUF(const S* probs, size_t t_count, size_t n_ffn, size_t n_zero,    \
+                                   size_t top_k, size_t k_expected, double mu, const double* bias, \
+                                   uint32_t* indices, double* gates, uint32_t* ffn_count) {        \
+        int rc = orc_router_validate(n_ffn, n_zero, top_k, k_expected, mu, bias);                  \
+        if (rc) return rc;                                                                         \
+        const size_t e = n_ffn + n_zero;                                                           \
+        for (size_t t = 0; t < t_count; ++t) {                                                     \
+            uint32_t* idx = indices + t * top_k;                                                   \
+            orc_select_topk_row_##SUF(probs + t * e, bias, e, top_k, idx);                         \
+            uint32_t ffn = 0;                                                                      \
+            for (size_t s = 0; s < top_k; ++s) {                                                   \
+                gates[t * top_k + s] = (double)probs[t * e + idx[s]];                              \
+                if (idx[s] < n_ffn) ++ffn;                                                         \
+            }                                                                                      \
+            ffn_count[t] = ffn;                                                                    \
+        }                                                                                          \
+        return ORC_OK;                                                                             \
+    }                                                                                              \
+    /* router.hpp:133-141: logits = mm(x, w); probs = softmax_rows(logits); route_from_probs */   \
+    int orc_route_topk_##SUF(const S* x, size_t t_count, size_t d, const S* w, size_t n_ffn,       \
+                             size_t n_zero, size_t top_k, size_t k_expected, double mu,            \
+                             const double* bias, uint32_t* indices, double* gates,                 \
+                             uint32_t* ffn_count, S* probs_out) {                                  \
+        const size_t e = n_ffn + n_zero;                                                           \
+        S* logits = (S*)malloc(ORC_NZ(t_count * e) * sizeof(S));                       \
+        S* probs = probs_out ? probs_out : (S*)malloc(ORC_NZ(t_count * e) * sizeof(S)); \
+        orc_mm_##SUF(x, w, logits, t_count, d, e);                                                 \
+        orc_softmax_rows_##SUF(logits, probs, t_count, e);                                         \
+        int rc = orc_route_from_probs_##SUF(probs, t_count, n_ffn, n_zero, top_k, k_expected, mu,  \
+                                            bias, indices, gates, ffn_count);                      \
+        free(logits);                                                                              \
+        if (!probs_out) free(probs);                                                               \
+        return rc;                                                                                 \
+    }
+
+ORC_DEFINE_SELECT(float, f32)
+ORC_DEFINE_SELECT(double, f64)
+
+/* router.hpp:144-150: slot-counted, zero experts included */
+void orc_accumulate_counters(const uint32_t* indices, size_t t_count, size_t top_k,
+                             uint64_t* tokens_routed, uint64_t* tokens_seen) {
+    for (size_t t = 0; t < t_count; ++t)
+        for (size_t s = 0; s < top_k; ++s) ++tokens_routed[indices[t * top_k + s]];
+    *tokens_seen += t_count;
+}
+
+/* router.hpp:155-176: PID-style bias controller tick */
+int orc_bias_update(size_t n_ffn, size_t n_zero, size_t top_k, size_t k_expected, double* mu,
+                    double mu_decay, double* b, uint64_t* tokens_routed, uint64_t* tokens_seen,
+                    double* delta) {
+    const size_t e = n_ffn + n_zero;
+    if (*tokens_seen == 0) return ORC_STATE;
+    const double t_all = (double)*tokens_seen;
+    uint64_t total = 0;
+    for (size_t i = 0; i < e; ++i) total += tokens_routed[i];
+    if (total != (uint64_t)top_k * *tokens_seen) return ORC_STATE;
+    const double target = (double)k_expected / ((double)top_k * (double)n_ffn);
+    for (size_t i = 0; i < e; ++i) delta[i] = 0.0;
+    for (size_t i = 0; i < n_ffn; ++i) {
+        const double load = (double)tokens_routed[i] / ((double)top_k * t_all);
+        delta[i] = *mu * (target - load);
+        b[i] += delta[i];
+    }
+    *mu *= mu_decay;
+    for (size_t i = 0; i < e; ++i) tokens_routed[i] = 0;
+    *tokens_seen = 0;
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------
+ * MoE -- blocks.hpp:226-394
+ *
+ * moe_forward (blocks.hpp:372-394) = index check, rebuilt probs[t,idx] =
+ * (S) gate, moe_block (:341-369) with renormalize=false.  Each expert row
+ * y = silu(x_t W_in[e]) W_out[e] depends only on its own token row (mm is
+ * row independent, tensor.hpp:95-112), so computing it per slot is bitwise
+ * the same as the reference's gathered sub-batch.  The combine follows
+ * moe_combine (:226-274): FFN slots in rank order out += (g_ffn*w)*y,
+ * zero slots zero_w += w, then out += (g_zero*zero_w)*x if zero_w != 0.
+ * `renorm` reproduces moe_block(..., renormalize=true) with probs equal to
+ * (S)gates at the selected entries (denominator in rank order, :240-247).
+ * ---------------------------------------------------------------------- */
+#define ORC_DEFINE_MOE(S, SUF)                                                                     \
+    void orc_expert_row_##SUF(const S* xrow, size_t d, const S* w_in, const S* w_out,              \
+                              size_t inter, S* h, S* y) {                                          \
+        orc_mm_##SUF(xrow, w_in, h, 1, d, inter);                                                  \
+        for (size_t i = 0; i < inter; ++i) h[i] = h[i] * orc_sigmoid_##SUF(h[i]);                  \
+        orc_mm_##SUF(h, w_out, y, 1, inter, d);                                                    \
+    }                                                                                              \
+    int orc_moe_forward_##SUF(const S* x, size_t t_count, size_t d, const uint32_t* indices,       \
+                              const double* gates, size_t top_k, size_t n_ffn, size_t n_zero,      \
+                              const S* const* w_in, const S* const* w_out, size_t inter,           \
+                              double gamma_ffn_d, double gamma_zero_d, int renorm, S* out) {       \
+        const size_t e_total = n_ffn + n_zero;                                                     \
+        for (size_t i = 0; i < t_count * top_k; ++i)                                               \
+            if (indices[i] >= e_total) return ORC_STATE;                                           \
+        const S gamma_ffn = (S)gamma_ffn_d, gamma_zero = (S)gamma_zero_d;                          \
+        S* h = (S*)malloc(ORC_NZ(inter) * sizeof(S));                                        \
+        S* y = (S*)malloc(ORC_NZ(d) * sizeof(S));                                                \
+        for (size_t t = 0; t < t_count; ++t) {                                                     \
+            S* orow = out + t * d;                                                                 \
+            const S* xrow = x + t * d;                                                             \
+            for (size_t j = 0; j < d; ++j) orow[j] = (S)0;                                         \
+            S denom = (S)1;                                                                        \
+            if (renorm) {                                                                          \
+                S s = (S)0;                                                                        \
+                for (size_t sl = 0; sl < top_k; ++sl) s += (S)gates[t * top_k + sl];              \
+                denom = s;                                                                         \
+            }                                                                                      \
+            S zero_w = (S)0;                                                                       \
+            for (size_t sl = 0; sl < top_k; ++sl) {                                                \
+                const uint32_t e = indices[t * top_k + sl];                                        \
+                const S w = (S)gates[t * top_k + sl] / denom;                                      \
+                if (e < n_ffn) {                                                                   \
+                    orc_expert_row_##SUF(xrow, d, w_in[e], w_out[e], inter, h, y);                 \
+                    const S coeff = gamma_ffn * w;                                                 \
+                    for (size_t j = 0; j < d; ++j) orow[j] += coeff * y[j];                        \
+                } else {                                                                           \
+                    zero_w += w;                                                                   \
+                }                                                                                  \
+            }                                                                                      \
+            if (zero_w != (S)0) {                                                                  \
+                const S coeff = gamma_zero * zero_w;                                               \
+                for (size_t j = 0; j < d; ++j) orow[j] += coeff * xrow[j];                         \
+            }                                                                                      \
+        }                                                                                          \
+        free(h);                                                                                   \
+        free(y);                                                                                   \
+        return ORC_OK;                                                                             \
+    }
+
+ORC_DEFINE_MOE(float, f32)
+ORC_DEFINE_MOE(double, f64)
+
+/* blocks.hpp:349-359: expert_tokens[e] ascending t, slot_row = position in it (-1 for zero). */
+void orc_permutation(const uint32_t* indices, size_t t_count, size_t top_k, size_t n_ffn,
+                     size_t n_zero, uint64_t* counts /*[n_ffn+n_zero]*/, int32_t* slot_row) {
+    for (size_t e = 0; e < n_ffn + n_zero; ++e) counts[e] = 0;
+    for (size_t t = 0; t < t_count; ++t)
+        for (size_t s = 0; s < top_k; ++s) {
+            const uint32_t e = indices[t * top_k + s];
+            slot_row[t * top_k + s] = e < n_ffn ? (int32_t)counts[e] : -1;
+            counts[e]++;
+        }
+}
+
+/* model.hpp:394-400 (ScMoE wiring, MoE branch): hmoe = rmsnorm(a1, g);
+ * probs = softmax(hmoe W_r); d = route_from_probs(probs); out = a3 + moe(hmoe). */
+int orc_scmoe_layer_f32(const float* a1, const float* a3, const float* gain, size_t t_count,
+                        size_t d, const float* w_router, size_t n_ffn, size_t n_zero, size_t top_k,
+                        size_t k_expected, double mu, const double* bias, const float* const* w_in,
+                        const float* const* w_out, size_t inter, double gamma_ffn,
+                        double gamma_zero, int renorm, uint32_t* indices, double* gates,
+                        uint32_t* ffn_count, float* out) {
+    const size_t e = n_ffn + n_zero;
+    float* hmoe = (float*)malloc(ORC_NZ(t_count * d) * sizeof(float));
+    float* moe = (float*)malloc(ORC_NZ(t_count * d) * sizeof(float));
+    float* probs = (float*)malloc(ORC_NZ(t_count * e) * sizeof(float));
+    orc_rmsnorm_f32(a1, gain, t_count, d, 1e-6f, hmoe);
+    int rc = orc_route_topk_f32(hmoe, t_count, d, w_router, n_ffn, n_zero, top_k, k_expected, mu,
+                                bias, indices, gates, ffn_count, probs);
+    if (!rc)
+        rc = orc_moe_forward_f32(hmoe, t_count, d, indices, gates, top_k, n_ffn, n_zero, w_in,
+                                 w_out, inter, gamma_ffn, gamma_zero, renorm, moe);
+    if (!rc)
+        for (size_t i = 0; i < t_count * d; ++i) out[i] = a3[i] + moe[i];
+    free(hmoe);
+    free(moe);
+    free(probs);
+    return rc;
+}
+
+/* router.hpp:349-369 simulate_bias_control, S = float, with the router
+ * projection given; mean/std per step out (RoutingDecision::mean_ffn/std_ffn,
+ * router.hpp:76-86). */
+int orc_simulate_bias_control_f32(const float* w, size_t d, size_t n_ffn, size_t n_zero,
+                                  size_t top_k, size_t k_expected, double* mu, double mu_decay,
+                                  double* b, uint64_t rng_seed, size_t batch_tokens, size_t steps,
+                                  double* mean_ffn, double* std_ffn) {
+    const size_t e = n_ffn + n_zero;
+    float* x = (float*)malloc(batch_tokens * d * sizeof(float));
+    uint32_t* idx = (uint32_t*)malloc(batch_tokens * top_k * sizeof(uint32_t));
+    double* gates = (double*)malloc(batch_tokens * top_k * sizeof(double));
+    uint32_t* cnt = (uint32_t*)malloc(batch_tokens * sizeof(uint32_t));
+    uint64_t* routed = (uint64_t*)calloc(e, sizeof(uint64_t));
+    double* delta = (double*)malloc(e * sizeof(double));
+    uint64_t seen = 0;
+    int rc = ORC_OK;
+    for (size_t step = 0; step < steps && !rc; ++step) {
+        const uint64_t s = orc_stream_seed(rng_seed, step);
+        orc_fill_normal_f32(s, 0, batch_tokens * d, x);
+        rc = orc_route_topk_f32(x, batch_tokens, d, w, n_ffn, n_zero, top_k, k_expected, *mu, b,
+                                idx, gates, cnt, NULL);
+        if (rc) break;
+        orc_accumulate_counters(idx, batch_tokens, top_k, routed, &seen);
+        double m = 0.0;
+        for (size_t t = 0; t < batch_tokens; ++t) m += cnt[t];
+        m /= (double)batch_tokens;
+        double v = 0.0;
+        for (size_t t = 0; t < batch_tokens; ++t) v += (cnt[t] - m) * (cnt[t] - m);
+        mean_ffn[step] = m;
+        std_ffn[step] = sqrt(v / (double)batch_tokens);
+        rc = orc_bias_update(n_ffn, n_zero, top_k, k_expected, mu, mu_decay, b, routed, &seen,
+                             delta);
+    }
+    free(x);
+    free(idx);
+    free(gates);
+    free(cnt);
+    free(routed);
+    free(delta);
+    return rc;
+}

@@ -1,0 +1,645 @@
+// capi.cu -- the extern "C" boundary (include/scmoe.h).
+//
+// Host-side validation reproduces the reference's checks and exception types
+// (router.hpp:45-61, :112, :157-162; blocks.hpp:237-238, :348, :375-377);
+// all numeric work is done by the CUDA kernels.  There is no CPU compute
+// path: without a device every entry point fails with SCMOE_ERR_CUDA.
+#include <cstring>
+#include <mutex>
+#include <thread>
+
+#include "internal.cuh"
+
+using namespace scmoe;
+
+namespace {
+
+template <typename F>
+int guarded(scmoe_ctx* c, F&& f) {
+    try {
+        f();
+        if (c) c->last_error.clear();
+        return SCMOE_OK;
+    } catch (const ScmoeError& e) {
+        if (c) c->last_error = e.msg;
+        return e.code;
+    } catch (const std::exception& e) {
+        if (c) c->last_error = e.what();
+        return SCMOE_ERR_INTERNAL;
+    }
+}
+
+// Host-tier staging buffers (distinct from the kernel workspace).
+struct Stage {
+    DevBuf bufs[12];
+};
+Stage& stage_of(scmoe_ctx* c) {
+    static thread_local std::vector<std::pair<scmoe_ctx*, Stage*>> table;
+    for (auto& kv : table)
+        if (kv.first == c) return *kv.second;
+    table.emplace_back(c, new Stage());
+    return *table.back().second;
+}
+
+template <typename T>
+T* upload(scmoe_ctx* c, DevBuf& b, const T* host, size_t n) {
+    T* d = b.get<T>(n);
+    if (n) SCMOE_CUDA(cudaMemcpyAsync(d, host, n * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+    return d;
+}
+template <typename T>
+void download(scmoe_ctx* c, T* host, const T* dev, size_t n) {
+    if (n) SCMOE_CUDA(cudaMemcpyAsync(host, dev, n * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+}
+
+void sync_and_check(scmoe_ctx* c) {
+    SCMOE_CUDA(cudaStreamSynchronize(c->stream));
+    int st = 0;
+    SCMOE_CUDA(cudaMemcpy(&st, c->dev_status, sizeof(int), cudaMemcpyDeviceToHost));
+    if (st != DEV_OK) {
+        SCMOE_CUDA(cudaMemset(c->dev_status, 0, sizeof(int)));
+        if (st == DEV_ERR_INDEX_RANGE) SCMOE_THROW(SCMOE_ERR_STATE, "moe_forward: expert index out of range");
+        if (st == DEV_ERR_COUNTERS)
+            SCMOE_THROW(SCMOE_ERR_STATE, "bias_update: counters do not cover top_k slots per token");
+        SCMOE_THROW(SCMOE_ERR_INTERNAL, "device reported an unknown error");
+    }
+}
+
+void validate_router(size_t n_ffn, size_t n_zero, size_t top_k, size_t k_expected, double mu) {
+    // RouterState::validate, router.hpp:50-61 (in its order)
+    const size_t e = n_ffn + n_zero;
+    if (top_k > e) SCMOE_THROW(SCMOE_ERR_CONFIG, "router: top_k exceeds expert count");
+    if (k_expected < 1 || k_expected > top_k)
+        SCMOE_THROW(SCMOE_ERR_CONFIG, "router: need 1 <= k_expected <= top_k");
+    if (n_zero > 0 && k_expected >= top_k)
+        SCMOE_THROW(SCMOE_ERR_CONFIG, "router: k_expected must be < top_k when zero experts exist");
+    if (n_zero < top_k - k_expected)
+        SCMOE_THROW(SCMOE_ERR_CONFIG, "router: too few zero experts to absorb top_k - k_expected slack");
+    if (mu < 0.0) SCMOE_THROW(SCMOE_ERR_CONFIG, "router: mu must be >= 0");
+}
+
+void require_ctx(scmoe_ctx* c) {
+    if (!c) throw ScmoeError{SCMOE_ERR_PARAMETER, "null context"};
+    SCMOE_CUDA(cudaSetDevice(c->device));
+}
+
+int tile_rows_for(const scmoe_bank* b) { return b->precision == SCMOE_PREC_BF16 ? 128 : 64; }
+
+// moe_forward on device pointers; x is the MoE input (hmoe), used by the
+// expert FFN and by the zero-expert identity term.
+void moe_forward_dev(scmoe_ctx* c, scmoe_bank* b, const float* x, const __nv_bfloat16* x_bf16,
+                     size_t T, const uint32_t* idx, const double* gates, size_t K, size_t n_zero,
+                     int renorm, const float* residual, float* out) {
+    const size_t n_ffn = b->n, d = b->d, I = b->inter, E = n_ffn + n_zero;
+    SCMOE_CHECK_ARG(K >= 1 && K <= 64, SCMOE_ERR_CONFIG, "moe_forward: top_k must be in [1, 64]");
+    Workspace& ws = c->ws;
+    PermResult pr = launch_permute(c, idx, T, K, n_ffn, E, tile_rows_for(b));
+    const float gf = (float)b->gamma_ffn(), gz = (float)b->gamma_zero();
+    if (b->precision == SCMOE_PREC_F32_EXACT) {
+        float* h = ws.h.get<float>(T * K * I + 1);
+        float* y = ws.y.get<float>(T * K * d + 1);
+        launch_seq_gemm(c, x, d, pr.row_token, b->w_in32, I, d * I, h, I, d, I, /*silu=*/1,
+                        pr.tiles, pr.n_tiles, pr.max_tiles);
+        launch_seq_gemm(c, h, I, nullptr, b->w_out32, d, I * d, y, d, I, d, /*silu=*/0, pr.tiles,
+                        pr.n_tiles, pr.max_tiles);
+        launch_combine_f32(c, x, y, idx, gates, pr.slot_pos, T, d, K, n_ffn, gf, gz, renorm,
+                           residual, out);
+    } else {
+        __nv_bfloat16* xb = const_cast<__nv_bfloat16*>(x_bf16);
+        if (!xb) {
+            // Caller passed fp32 only: make the bf16 GEMM operand copy once.
+            xb = ws.hmoe_bf16.get<__nv_bfloat16>(T * d);
+            launch_cast_bf16(c, x, T * d, xb);
+        }
+        __nv_bfloat16* xp = ws.xp.get<__nv_bfloat16>(T * K * d + 1);
+        __nv_bfloat16* h = ws.h.get<__nv_bfloat16>(T * K * I + 1);
+        __nv_bfloat16* y = ws.y.get<__nv_bfloat16>(T * K * d + 1);
+        launch_gather_bf16(c, xb, d, pr.row_token, pr.expert_base, n_ffn, T * K, xp);
+        launch_grouped_gemm_bf16(c, b->w1t, n_ffn, I, d, xp, T * K, h, /*silu=*/1, pr.tiles,
+                                 pr.n_tiles, pr.max_tiles, tile_rows_for(b));
+        launch_grouped_gemm_bf16(c, b->w2t, n_ffn, d, I, h, T * K, y, /*silu=*/0, pr.tiles,
+                                 pr.n_tiles, pr.max_tiles, tile_rows_for(b));
+        launch_combine_bf16(c, x, y, idx, gates, pr.slot_pos, T, d, K, n_ffn, gf, gz, renorm,
+                            residual, out);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* scmoe_version(void) { return "scmoe-b200 0.1 (sm_100a)"; }
+
+int scmoe_ctx_create(int device, scmoe_ctx** out) {
+    return guarded(nullptr, [&] {
+        if (!out) SCMOE_THROW(SCMOE_ERR_PARAMETER, "null out");
+        int n = 0;
+        SCMOE_CUDA(cudaGetDeviceCount(&n));
+        if (device < 0 || device >= n) SCMOE_THROW(SCMOE_ERR_CUDA, "no such CUDA device");
+        SCMOE_CUDA(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        SCMOE_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10)
+            SCMOE_THROW(SCMOE_ERR_CUDA, "libscmoe is built for sm_100a (B200); device is sm_" +
+                                            std::to_string(prop.major * 10 + prop.minor));
+        auto* c = new scmoe_ctx();
+        c->device = device;
+        c->num_sms = prop.multiProcessorCount;
+        SCMOE_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+        c->stream = c->own_stream;
+        SCMOE_CUDA(cudaMalloc(&c->dev_status, sizeof(int)));
+        SCMOE_CUDA(cudaMemset(c->dev_status, 0, sizeof(int)));
+        *out = c;
+    });
+}
+
+int scmoe_ctx_destroy(scmoe_ctx* c) {
+    if (!c) return SCMOE_OK;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    c->ws.release_all();
+    Stage& st = stage_of(c);
+    for (auto& b : st.bufs) b.release();
+    if (c->dev_status) cudaFree(c->dev_status);
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    delete c;
+    return SCMOE_OK;
+}
+
+const char* scmoe_last_error(const scmoe_ctx* c) { return c ? c->last_error.c_str() : "null context"; }
+
+int scmoe_set_stream(scmoe_ctx* c, void* s) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        c->stream = s ? static_cast<cudaStream_t>(s) : c->own_stream;
+    });
+}
+void* scmoe_get_stream(const scmoe_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int scmoe_synchronize(scmoe_ctx* c) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        sync_and_check(c);
+    });
+}
+uint64_t scmoe_kernel_launches(const scmoe_ctx* c) { return c ? c->launches : 0; }
+
+int scmoe_device_alloc(scmoe_ctx* c, size_t bytes, void** out) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        SCMOE_CUDA(cudaMalloc(out, bytes ? bytes : 16));
+    });
+}
+int scmoe_device_free(scmoe_ctx* c, void* p) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        SCMOE_CUDA(cudaFree(p));
+    });
+}
+int scmoe_copy_h2d(scmoe_ctx* c, void* dst, const void* src, size_t bytes) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        SCMOE_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
+    });
+}
+int scmoe_copy_d2h(scmoe_ctx* c, void* dst, const void* src, size_t bytes) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        SCMOE_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+        SCMOE_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+// ---- router ---------------------------------------------------------------
+
+int scmoe_router_create(scmoe_ctx* c, size_t d, size_t n_ffn, size_t n_zero, size_t top_k,
+                        size_t k_expected, double mu, double mu_decay, scmoe_router** out) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        validate_router(n_ffn, n_zero, top_k, k_expected, mu);
+        auto* r = new scmoe_router();
+        r->d = d;
+        r->n_ffn = n_ffn;
+        r->n_zero = n_zero;
+        r->top_k = top_k;
+        r->k_expected = k_expected;
+        r->mu = mu;
+        r->mu_decay = mu_decay;
+        const size_t E = r->E();
+        SCMOE_CUDA(cudaMalloc(&r->w, std::max<size_t>(d * E, 1) * sizeof(float)));
+        SCMOE_CUDA(cudaMalloc(&r->b, std::max<size_t>(E, 1) * sizeof(double)));
+        SCMOE_CUDA(cudaMalloc(&r->routed, std::max<size_t>(E, 1) * sizeof(uint64_t)));
+        SCMOE_CUDA(cudaMemset(r->w, 0, std::max<size_t>(d * E, 1) * sizeof(float)));
+        SCMOE_CUDA(cudaMemset(r->b, 0, std::max<size_t>(E, 1) * sizeof(double)));
+        SCMOE_CUDA(cudaMemset(r->routed, 0, std::max<size_t>(E, 1) * sizeof(uint64_t)));
+        *out = r;
+    });
+}
+
+int scmoe_router_destroy(scmoe_ctx* c, scmoe_router* r) {
+    if (!r) return SCMOE_OK;
+    if (c) cudaSetDevice(c->device);
+    cudaFree(r->w);
+    cudaFree(r->b);
+    cudaFree(r->routed);
+    delete r;
+    return SCMOE_OK;
+}
+
+int scmoe_router_set_weights_host(scmoe_ctx* c, scmoe_router* r, const float* w) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        SCMOE_CUDA(cudaMemcpy(r->w, w, r->d * r->E() * sizeof(float), cudaMemcpyHostToDevice));
+    });
+}
+int scmoe_router_set_weights(scmoe_ctx* c, scmoe_router* r, const float* w) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        SCMOE_CUDA(cudaMemcpyAsync(r->w, w, r->d * r->E() * sizeof(float), cudaMemcpyDeviceToDevice,
+                                   c->stream));
+    });
+}
+int scmoe_router_set_bias_host(scmoe_ctx* c, scmoe_router* r, const double* b) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        for (size_t i = r->n_ffn; i < r->E(); ++i)
+            if (b[i] != 0.0) SCMOE_THROW(SCMOE_ERR_CONFIG, "router: zero-expert bias must stay 0");
+        SCMOE_CUDA(cudaMemcpy(r->b, b, r->E() * sizeof(double), cudaMemcpyHostToDevice));
+    });
+}
+int scmoe_router_get_bias_host(scmoe_ctx* c, scmoe_router* r, double* b) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        SCMOE_CUDA(cudaStreamSynchronize(c->stream));
+        SCMOE_CUDA(cudaMemcpy(b, r->b, r->E() * sizeof(double), cudaMemcpyDeviceToHost));
+    });
+}
+int scmoe_router_set_mu(scmoe_ctx* c, scmoe_router* r, double mu, double mu_decay) {
+    return guarded(c, [&] {
+        if (mu < 0.0) SCMOE_THROW(SCMOE_ERR_CONFIG, "router: mu must be >= 0");
+        r->mu = mu;
+        r->mu_decay = mu_decay;
+    });
+}
+int scmoe_router_get_mu(scmoe_ctx* c, scmoe_router* r, double* mu, double* mu_decay) {
+    return guarded(c, [&] {
+        if (mu) *mu = r->mu;
+        if (mu_decay) *mu_decay = r->mu_decay;
+    });
+}
+int scmoe_router_get_counters_host(scmoe_ctx* c, scmoe_router* r, uint64_t* routed,
+                                   uint64_t* seen) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        SCMOE_CUDA(cudaStreamSynchronize(c->stream));
+        if (routed)
+            SCMOE_CUDA(cudaMemcpy(routed, r->routed, r->E() * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+        if (seen) *seen = r->tokens_seen;
+    });
+}
+int scmoe_router_set_counters_host(scmoe_ctx* c, scmoe_router* r, const uint64_t* routed,
+                                   uint64_t seen) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        SCMOE_CUDA(cudaStreamSynchronize(c->stream));
+        SCMOE_CUDA(cudaMemcpy(r->routed, routed, r->E() * sizeof(uint64_t), cudaMemcpyHostToDevice));
+        r->tokens_seen = seen;
+    });
+}
+uint64_t* scmoe_router_counters_dev(scmoe_router* r) { return r ? r->routed : nullptr; }
+const double* scmoe_router_bias_dev(scmoe_router* r) { return r ? r->b : nullptr; }
+
+int scmoe_route_topk(scmoe_ctx* c, scmoe_router* r, const float* x, size_t T, uint32_t* idx,
+                     double* gates, uint32_t* ffn_count, float* probs) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        validate_router(r->n_ffn, r->n_zero, r->top_k, r->k_expected, r->mu);
+        if (T == 0) return;
+        const size_t E = r->E();
+        float* logits = c->ws.logits.get<float>(T * E);
+        // router.hpp:136 -- one group, row tiles of 64 tokens
+        const size_t ntile = ceil_div(T, 64);
+        TokenTile* td = c->ws.misc.get<TokenTile>(ntile);
+        launch_row_tiles(c, T, 64, td);
+        launch_seq_gemm(c, x, r->d, nullptr, r->w, E, 0, logits, E, r->d, E, 0, td, nullptr, ntile);
+        launch_softmax_topk(c, logits, T, E, r->top_k, r->n_ffn, r->b, idx, gates, ffn_count, probs);
+    });
+}
+
+int scmoe_route_topk_host(scmoe_ctx* c, scmoe_router* r, const float* x, size_t T, uint32_t* idx,
+                          double* gates, uint32_t* ffn_count, float* probs) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        Stage& s = stage_of(c);
+        const size_t K = r->top_k, E = r->E();
+        const float* xd = upload(c, s.bufs[0], x, T * r->d);
+        uint32_t* di = s.bufs[1].get<uint32_t>(T * K);
+        double* dg = s.bufs[2].get<double>(T * K);
+        uint32_t* dc = s.bufs[3].get<uint32_t>(T);
+        float* dp = probs ? s.bufs[4].get<float>(T * E) : nullptr;
+        int rc = scmoe_route_topk(c, r, xd, T, di, dg, dc, dp);
+        if (rc) throw ScmoeError{rc, c->last_error};
+        download(c, idx, di, T * K);
+        download(c, gates, dg, T * K);
+        download(c, ffn_count, dc, T);
+        if (probs) download(c, probs, dp, T * E);
+        sync_and_check(c);
+    });
+}
+
+#define ROUTE_FROM_PROBS(S, SUF)                                                                   \
+    int scmoe_route_from_probs_##SUF(scmoe_ctx* c, scmoe_router* r, const S* probs, size_t T,      \
+                                     uint32_t* idx, double* gates, uint32_t* ffn_count) {          \
+        return guarded(c, [&] {                                                                    \
+            require_ctx(c);                                                                        \
+            validate_router(r->n_ffn, r->n_zero, r->top_k, r->k_expected, r->mu);                  \
+            launch_topk_from_probs_##SUF(c, probs, T, r->E(), r->top_k, r->n_ffn, r->b, idx,       \
+                                         gates, ffn_count);                                        \
+        });                                                                                        \
+    }                                                                                              \
+    int scmoe_route_from_probs_##SUF##_host(scmoe_ctx* c, scmoe_router* r, const S* probs,         \
+                                            size_t T, uint32_t* idx, double* gates,                \
+                                            uint32_t* ffn_count) {                                 \
+        return guarded(c, [&] {                                                                    \
+            require_ctx(c);                                                                        \
+            Stage& s = stage_of(c);                                                                \
+            const size_t K = r->top_k;                                                             \
+            const S* pd = upload(c, s.bufs[0], probs, T * r->E());                                 \
+            uint32_t* di = s.bufs[1].get<uint32_t>(T * K);                                         \
+            double* dg = s.bufs[2].get<double>(T * K);                                             \
+            uint32_t* dc = s.bufs[3].get<uint32_t>(T);                                             \
+            int rc = scmoe_route_from_probs_##SUF(c, r, pd, T, di, dg, dc);                        \
+            if (rc) throw ScmoeError{rc, c->last_error};                                           \
+            download(c, idx, di, T * K);                                                           \
+            download(c, gates, dg, T * K);                                                         \
+            download(c, ffn_count, dc, T);                                                         \
+            sync_and_check(c);                                                                     \
+        });                                                                                        \
+    }
+ROUTE_FROM_PROBS(float, f32)
+ROUTE_FROM_PROBS(double, f64)
+
+int scmoe_accumulate_counters(scmoe_ctx* c, scmoe_router* r, const uint32_t* idx, size_t T) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        launch_accumulate(c, idx, T * r->top_k, r->E(), r->routed);
+        r->tokens_seen += T;
+    });
+}
+int scmoe_accumulate_counters_host(scmoe_ctx* c, scmoe_router* r, const uint32_t* idx, size_t T) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        Stage& s = stage_of(c);
+        const uint32_t* di = upload(c, s.bufs[1], idx, T * r->top_k);
+        int rc = scmoe_accumulate_counters(c, r, di, T);
+        if (rc) throw ScmoeError{rc, c->last_error};
+        sync_and_check(c);
+    });
+}
+
+int scmoe_bias_update(scmoe_ctx* c, scmoe_router* r, double* delta) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        if (r->tokens_seen == 0) SCMOE_THROW(SCMOE_ERR_STATE, "bias_update: empty batch");
+        double* dd = c->ws.misc.get<double>(r->E());
+        launch_bias_update(c, r, dd);
+        sync_and_check(c);  // StateError on counter mismatch (router.hpp:161-162)
+        if (delta) SCMOE_CUDA(cudaMemcpy(delta, dd, r->E() * sizeof(double), cudaMemcpyDeviceToHost));
+        r->mu *= r->mu_decay;  // router.hpp:172
+        r->tokens_seen = 0;
+    });
+}
+
+// ---- bank -----------------------------------------------------------------
+
+int scmoe_bank_create(scmoe_ctx* c, size_t n, size_t d, size_t inter, int precision, size_t m,
+                      int gamma_mode, scmoe_bank** out) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        if (m < 1) SCMOE_THROW(SCMOE_ERR_PARAMETER, "variance_gamma: m must be >= 1");
+        if (precision != SCMOE_PREC_F32_EXACT && precision != SCMOE_PREC_BF16)
+            SCMOE_THROW(SCMOE_ERR_PARAMETER, "bank: unknown precision");
+        if (gamma_mode < 0 || gamma_mode > 2) SCMOE_THROW(SCMOE_ERR_PARAMETER, "unknown gamma mode");
+        if (precision == SCMOE_PREC_BF16) {
+            if (d % 64 != 0 || inter % 128 != 0 || d % 128 != 0)
+                SCMOE_THROW(SCMOE_ERR_DIMENSION,
+                            "bank: bf16 tensor-core path needs d % 128 == 0 and inter % 128 == 0");
+        }
+        auto* b = new scmoe_bank();
+        b->n = n;
+        b->d = d;
+        b->inter = inter;
+        b->m = m;
+        b->precision = precision;
+        b->gamma_mode = gamma_mode;
+        const size_t per = d * inter;
+        if (precision == SCMOE_PREC_F32_EXACT) {
+            SCMOE_CUDA(cudaMalloc(&b->w_in32, std::max<size_t>(n * per, 1) * sizeof(float)));
+            SCMOE_CUDA(cudaMalloc(&b->w_out32, std::max<size_t>(n * per, 1) * sizeof(float)));
+            SCMOE_CUDA(cudaMemset(b->w_in32, 0, std::max<size_t>(n * per, 1) * sizeof(float)));
+            SCMOE_CUDA(cudaMemset(b->w_out32, 0, std::max<size_t>(n * per, 1) * sizeof(float)));
+        } else {
+            SCMOE_CUDA(cudaMalloc(&b->w1t, std::max<size_t>(n * per, 1) * sizeof(__nv_bfloat16)));
+            SCMOE_CUDA(cudaMalloc(&b->w2t, std::max<size_t>(n * per, 1) * sizeof(__nv_bfloat16)));
+            SCMOE_CUDA(cudaMemset(b->w1t, 0, std::max<size_t>(n * per, 1) * sizeof(__nv_bfloat16)));
+            SCMOE_CUDA(cudaMemset(b->w2t, 0, std::max<size_t>(n * per, 1) * sizeof(__nv_bfloat16)));
+        }
+        *out = b;
+    });
+}
+
+int scmoe_bank_destroy(scmoe_ctx* c, scmoe_bank* b) {
+    if (!b) return SCMOE_OK;
+    if (c) cudaSetDevice(c->device);
+    cudaFree(b->w_in32);
+    cudaFree(b->w_out32);
+    cudaFree(b->w1t);
+    cudaFree(b->w2t);
+    delete b;
+    return SCMOE_OK;
+}
+
+int scmoe_bank_set_expert(scmoe_ctx* c, scmoe_bank* b, size_t e, const float* w_in,
+                          const float* w_out) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        if (e >= b->n) SCMOE_THROW(SCMOE_ERR_DIMENSION, "bank: expert index out of range");
+        const size_t per = b->d * b->inter;
+        if (b->precision == SCMOE_PREC_F32_EXACT) {
+            SCMOE_CUDA(cudaMemcpyAsync(b->w_in32 + e * per, w_in, per * sizeof(float),
+                                       cudaMemcpyDeviceToDevice, c->stream));
+            SCMOE_CUDA(cudaMemcpyAsync(b->w_out32 + e * per, w_out, per * sizeof(float),
+                                       cudaMemcpyDeviceToDevice, c->stream));
+        } else {
+            // w_in [d, I] -> w1t [I, d];  w_out [I, d] -> w2t [d, I]
+            launch_f32_to_bf16_t(c, w_in, b->d, b->inter, b->w1t + e * per);
+            launch_f32_to_bf16_t(c, w_out, b->inter, b->d, b->w2t + e * per);
+        }
+    });
+}
+
+int scmoe_bank_set_expert_host(scmoe_ctx* c, scmoe_bank* b, size_t e, const float* w_in,
+                               const float* w_out) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        Stage& s = stage_of(c);
+        const size_t per = b->d * b->inter;
+        const float* di = upload(c, s.bufs[8], w_in, per);
+        const float* dout = upload(c, s.bufs[9], w_out, per);
+        int rc = scmoe_bank_set_expert(c, b, e, di, dout);
+        if (rc) throw ScmoeError{rc, c->last_error};
+        SCMOE_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int scmoe_bank_init_uniform(scmoe_ctx* c, scmoe_bank* b, uint64_t seed, uint64_t stream0,
+                            double variance) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        if (variance < 0.0) SCMOE_THROW(SCMOE_ERR_PARAMETER, "seeded_init: variance must be >= 0");
+        const double hw = std::sqrt(3.0 * variance);
+        const size_t per = b->d * b->inter;
+        for (size_t e = 0; e < b->n; ++e) {
+            const uint64_t s_in = scmoe_rng_stream_seed(seed, stream0 + 2 * e);
+            const uint64_t s_out = scmoe_rng_stream_seed(seed, stream0 + 2 * e + 1);
+            if (b->precision == SCMOE_PREC_F32_EXACT) {
+                launch_uniform_init(c, s_in, 0, per, hw, b->w_in32 + e * per);
+                launch_uniform_init(c, s_out, 0, per, hw, b->w_out32 + e * per);
+            } else {
+                launch_uniform_init_bf16_t(c, s_in, b->d, b->inter, hw, b->w1t + e * per);
+                launch_uniform_init_bf16_t(c, s_out, b->inter, b->d, hw, b->w2t + e * per);
+            }
+        }
+        SCMOE_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+double scmoe_bank_gamma_ffn(const scmoe_bank* b) { return b ? b->gamma_ffn() : 0.0; }
+double scmoe_bank_gamma_zero(const scmoe_bank* b) { return b ? b->gamma_zero() : 0.0; }
+size_t scmoe_bank_device_bytes(const scmoe_bank* b) {
+    if (!b) return 0;
+    const size_t per = b->d * b->inter * b->n * 2;
+    return b->precision == SCMOE_PREC_F32_EXACT ? per * 4 : per * 2;
+}
+
+// ---- MoE forward / layer ---------------------------------------------------
+
+int scmoe_moe_forward(scmoe_ctx* c, scmoe_bank* b, const float* x, size_t T, const uint32_t* idx,
+                      const double* gates, size_t K, size_t n_zero, int renorm,
+                      const float* residual, float* out) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        if (T == 0) return;
+        launch_check_indices(c, idx, T * K, b->n + n_zero);
+        moe_forward_dev(c, b, x, nullptr, T, idx, gates, K, n_zero, renorm, residual, out);
+    });
+}
+
+int scmoe_moe_forward_host(scmoe_ctx* c, scmoe_bank* b, const float* x, size_t T,
+                           const uint32_t* idx, const double* gates, size_t K, size_t n_zero,
+                           int renorm, const float* residual, float* out) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        // blocks.hpp:375-377 -- index range check before any work
+        for (size_t i = 0; i < T * K; ++i)
+            if (idx[i] >= b->n + n_zero) SCMOE_THROW(SCMOE_ERR_STATE, "moe_forward: expert index out of range");
+        if (T == 0) return;
+        Stage& s = stage_of(c);
+        const float* xd = upload(c, s.bufs[0], x, T * b->d);
+        const uint32_t* di = upload(c, s.bufs[1], idx, T * K);
+        const double* dg = upload(c, s.bufs[2], gates, T * K);
+        const float* dr = residual ? upload(c, s.bufs[3], residual, T * b->d) : nullptr;
+        float* dout = s.bufs[4].get<float>(T * b->d);
+        int rc = scmoe_moe_forward(c, b, xd, T, di, dg, K, n_zero, renorm, dr, dout);
+        if (rc) throw ScmoeError{rc, c->last_error};
+        download(c, out, dout, T * b->d);
+        sync_and_check(c);
+    });
+}
+
+int scmoe_rmsnorm(scmoe_ctx* c, const float* x, const float* gain, size_t rows, size_t d, float eps,
+                  float* out) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        launch_rmsnorm(c, x, gain, rows, d, eps, out, nullptr);
+    });
+}
+
+int scmoe_layer_forward(scmoe_ctx* c, scmoe_router* r, scmoe_bank* b, const float* a1,
+                        const float* a3, const float* gain, size_t T, int renorm, uint32_t* idx,
+                        double* gates, uint32_t* ffn_count, float* out) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        if (r->d != b->d) SCMOE_THROW(SCMOE_ERR_DIMENSION, "layer: router/bank width mismatch");
+        if (r->n_ffn != b->n) SCMOE_THROW(SCMOE_ERR_DIMENSION, "moe_block: decision/bank FFN count mismatch");
+        validate_router(r->n_ffn, r->n_zero, r->top_k, r->k_expected, r->mu);
+        if (T == 0) return;
+        const size_t d = r->d, E = r->E(), K = r->top_k;
+        Workspace& ws = c->ws;
+        float* hmoe = ws.hmoe.get<float>(T * d);
+        __nv_bfloat16* hb =
+            b->precision == SCMOE_PREC_BF16 ? ws.hmoe_bf16.get<__nv_bfloat16>(T * d) : nullptr;
+        launch_rmsnorm(c, a1, gain, T, d, 1e-6f, hmoe, hb);
+        float* logits = ws.logits.get<float>(T * E);
+        const size_t ntile = ceil_div(T, 64);
+        TokenTile* td = ws.misc.get<TokenTile>(ntile);
+        launch_row_tiles(c, T, 64, td);
+        launch_seq_gemm(c, hmoe, d, nullptr, r->w, E, 0, logits, E, d, E, 0, td, nullptr, ntile);
+        launch_softmax_topk(c, logits, T, E, K, r->n_ffn, r->b, idx, gates, ffn_count, nullptr);
+        moe_forward_dev(c, b, hmoe, hb, T, idx, gates, K, r->n_zero, renorm, a3, out);
+    });
+}
+
+int scmoe_layer_forward_host(scmoe_ctx* c, scmoe_router* r, scmoe_bank* b, const float* a1,
+                             const float* a3, const float* gain, size_t T, int renorm,
+                             uint32_t* idx, double* gates, uint32_t* ffn_count, float* out) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        if (T == 0) return;
+        Stage& s = stage_of(c);
+        const size_t d = r->d, K = r->top_k;
+        const float* da1 = upload(c, s.bufs[0], a1, T * d);
+        const float* da3 = a3 ? upload(c, s.bufs[5], a3, T * d) : nullptr;
+        const float* dg = gain ? upload(c, s.bufs[6], gain, d) : nullptr;
+        uint32_t* di = s.bufs[1].get<uint32_t>(T * K);
+        double* dgt = s.bufs[2].get<double>(T * K);
+        uint32_t* dc = s.bufs[3].get<uint32_t>(T);
+        float* dout = s.bufs[4].get<float>(T * d);
+        int rc = scmoe_layer_forward(c, r, b, da1, da3, dg, T, renorm, di, dgt, dc, dout);
+        if (rc) throw ScmoeError{rc, c->last_error};
+        if (idx) download(c, idx, di, T * K);
+        if (gates) download(c, gates, dgt, T * K);
+        if (ffn_count) download(c, ffn_count, dc, T);
+        download(c, out, dout, T * d);
+        sync_and_check(c);
+    });
+}
+
+int scmoe_rng_fill_uniform(scmoe_ctx* c, uint64_t seed, uint64_t first, size_t n, double variance,
+                           float* out) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        if (variance < 0.0) SCMOE_THROW(SCMOE_ERR_PARAMETER, "seeded_init: variance must be >= 0");
+        if (variance == 0.0) {
+            SCMOE_CUDA(cudaMemsetAsync(out, 0, n * sizeof(float), c->stream));
+            return;
+        }
+        launch_uniform_init(c, seed, first, n, std::sqrt(3.0 * variance), out);
+    });
+}
+
+int scmoe_debug_expf(scmoe_ctx* c, const float* in, float* out, size_t n) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        launch_debug_expf(c, in, out, n);
+    });
+}
+
+int scmoe_debug_expf_range(scmoe_ctx* c, uint32_t first, float* out, size_t n) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        launch_debug_expf_range(c, first, out, n);
+    });
+}
+
+}  // extern "C"

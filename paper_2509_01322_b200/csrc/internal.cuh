@@ -1,0 +1,192 @@
+// internal.cuh -- shared state and helpers of libscmoe (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/scmoe.h"
+
+// ---------------------------------------------------------------------------
+// Status plumbing.  The C ABI maps the reference's exceptions to codes
+// (common.hpp:11-33); ScmoeError carries one through the C++ implementation.
+// ---------------------------------------------------------------------------
+struct ScmoeError {
+    int code;
+    std::string msg;
+};
+
+#define SCMOE_THROW(code, msg) throw ScmoeError{(code), (msg)}
+#define SCMOE_CHECK_ARG(cond, code, msg) \
+    do {                                 \
+        if (!(cond)) SCMOE_THROW(code, msg); \
+    } while (0)
+#define SCMOE_CUDA(expr)                                                                      \
+    do {                                                                                      \
+        cudaError_t _e = (expr);                                                              \
+        if (_e != cudaSuccess)                                                                \
+            SCMOE_THROW(SCMOE_ERR_CUDA, std::string(#expr " failed: ") + cudaGetErrorString(_e)); \
+    } while (0)
+
+// Device-side latched errors (written by kernels that validate data).
+enum : int { DEV_OK = 0, DEV_ERR_INDEX_RANGE = 1, DEV_ERR_COUNTERS = 2 };
+
+// ---------------------------------------------------------------------------
+// Grow-only device workspace.
+// ---------------------------------------------------------------------------
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    template <typename T>
+    T* get(size_t n) {
+        size_t need = n * sizeof(T);
+        if (need == 0) need = 16;
+        if (need > bytes) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            bytes = 0;
+            // round up to 2 MiB so repeated growth is rare
+            size_t cap = (need + (2u << 20) - 1) & ~size_t((2u << 20) - 1);
+            SCMOE_CUDA(cudaMalloc(&p, cap));
+            bytes = cap;
+        }
+        return static_cast<T*>(p);
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+};
+
+struct Workspace {
+    DevBuf logits, probs, hmoe, hmoe_bf16, idx, gates, ffn_count;
+    DevBuf rank_in_block, block_counts, expert_count, expert_base, slot_pos, row_token;
+    DevBuf tiles, n_tiles, xp, h, y, in_copy, out_copy, misc;
+    void release_all() {
+        DevBuf* all[] = {&logits, &probs, &hmoe, &hmoe_bf16, &idx, &gates, &ffn_count,
+                         &rank_in_block, &block_counts, &expert_count, &expert_base, &slot_pos,
+                         &row_token, &tiles, &n_tiles, &xp, &h, &y, &in_copy, &out_copy, &misc};
+        for (DevBuf* b : all) b->release();
+    }
+};
+
+struct scmoe_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    std::string last_error;
+    int* dev_status = nullptr;  // latched device-side error
+    uint64_t launches = 0;
+    Workspace ws;
+};
+
+struct scmoe_router {
+    size_t d = 0, n_ffn = 0, n_zero = 0, top_k = 0, k_expected = 0;
+    double mu = 0.0, mu_decay = 1.0;
+    uint64_t tokens_seen = 0;  // host mirror of RouterState::tokens_seen
+    float* w = nullptr;         // [d, E] fp32
+    double* b = nullptr;        // [E]
+    uint64_t* routed = nullptr; // [E]
+    size_t E() const { return n_ffn + n_zero; }
+};
+
+struct scmoe_bank {
+    size_t n = 0, d = 0, inter = 0, m = 1;
+    int precision = SCMOE_PREC_F32_EXACT;
+    int gamma_mode = SCMOE_GAMMA_FFN_ONLY;
+    float* w_in32 = nullptr;          // [n][d][inter]   (F32_EXACT)
+    float* w_out32 = nullptr;         // [n][inter][d]
+    __nv_bfloat16* w1t = nullptr;     // [n][inter][d]   (BF16, K-major for GEMM1)
+    __nv_bfloat16* w2t = nullptr;     // [n][d][inter]   (BF16, K-major for GEMM2)
+    double gamma_ffn() const { return gamma_mode == SCMOE_GAMMA_OFF ? 1.0 : (double)m; }
+    double gamma_zero() const { return gamma_mode == SCMOE_GAMMA_ALL ? (double)m : 1.0; }
+};
+
+// One GEMM work tile: rows [pos, pos+count) of expert `e` in the permuted order.
+struct TokenTile {
+    int e, pos, count, pad;
+};
+
+// ---------------------------------------------------------------------------
+// Kernel launchers (defined in the .cu files).
+// ---------------------------------------------------------------------------
+namespace scmoe {
+
+constexpr int kPermTokensPerBlock = 256;
+
+void launch_rmsnorm(scmoe_ctx* c, const float* x, const float* gain, size_t rows, size_t d,
+                    float eps, float* out, __nv_bfloat16* out_bf16);
+// C[rows, n] = A[rows, k] B[k, n], sequential k (router.hpp:136 / tensor.hpp:95-112).
+void launch_seq_gemm(scmoe_ctx* c, const float* A, size_t lda, const int* a_rows,
+                     const float* B, size_t ldb, size_t b_group_stride, float* C, size_t ldc,
+                     size_t K, size_t N, int silu, const TokenTile* tiles, const int* n_tiles_dev,
+                     size_t max_tiles);
+void launch_softmax_topk(scmoe_ctx* c, const float* logits, size_t T, size_t E, size_t K,
+                         size_t n_ffn, const double* bias, uint32_t* idx, double* gates,
+                         uint32_t* ffn_count, float* probs_out);
+void launch_topk_from_probs_f32(scmoe_ctx* c, const float* probs, size_t T, size_t E, size_t K,
+                                size_t n_ffn, const double* bias, uint32_t* idx, double* gates,
+                                uint32_t* ffn_count);
+void launch_topk_from_probs_f64(scmoe_ctx* c, const double* probs, size_t T, size_t E, size_t K,
+                                size_t n_ffn, const double* bias, uint32_t* idx, double* gates,
+                                uint32_t* ffn_count);
+
+struct PermResult {
+    int* slot_pos;      // [T*K], -1 for zero experts
+    int* row_token;     // [T*K] upper bound; first total entries valid
+    int* expert_base;   // [n_ffn+1]
+    int* expert_count;  // [E]
+    TokenTile* tiles;   // [max_tiles]
+    int* n_tiles;       // device scalar
+    size_t max_tiles;
+};
+PermResult launch_permute(scmoe_ctx* c, const uint32_t* idx, size_t T, size_t K, size_t n_ffn,
+                          size_t E, int tile_rows);
+void launch_gather_bf16(scmoe_ctx* c, const __nv_bfloat16* src, size_t d, const int* row_token,
+                        const int* expert_base, size_t n_ffn, size_t max_rows,
+                        __nv_bfloat16* dst);
+void launch_combine_f32(scmoe_ctx* c, const float* x, const float* y, const uint32_t* idx,
+                        const double* gates, const int* slot_pos, size_t T, size_t d, size_t K,
+                        size_t n_ffn, float gamma_ffn, float gamma_zero, int renorm,
+                        const float* residual, float* out);
+void launch_combine_bf16(scmoe_ctx* c, const float* x, const __nv_bfloat16* y,
+                         const uint32_t* idx, const double* gates, const int* slot_pos, size_t T,
+                         size_t d, size_t K, size_t n_ffn, float gamma_ffn, float gamma_zero,
+                         int renorm, const float* residual, float* out);
+void launch_check_indices(scmoe_ctx* c, const uint32_t* idx, size_t n, size_t E);
+void launch_accumulate(scmoe_ctx* c, const uint32_t* idx, size_t n, size_t E, uint64_t* routed);
+void launch_bias_update(scmoe_ctx* c, scmoe_router* r, double* delta_dev);
+void launch_uniform_init(scmoe_ctx* c, uint64_t seed, uint64_t first, size_t n,
+                         double half_width, float* out);
+void launch_uniform_init_bf16_t(scmoe_ctx* c, uint64_t seed, size_t rows, size_t cols,
+                                double half_width, __nv_bfloat16* out_t);
+void launch_debug_expf(scmoe_ctx* c, const float* in, float* out, size_t n);
+void launch_debug_expf_range(scmoe_ctx* c, uint32_t first, float* out, size_t n);
+void launch_cast_bf16(scmoe_ctx* c, const float* src, size_t n, __nv_bfloat16* dst);
+void launch_row_tiles(scmoe_ctx* c, size_t rows, int tile_rows, TokenTile* tiles);
+void launch_f32_to_bf16_t(scmoe_ctx* c, const float* src, size_t rows, size_t cols,
+                          __nv_bfloat16* dst_t);
+
+// tcgen05 grouped GEMM (gemm_sm100.cu).  D^T = W x X^T per expert tile:
+//   out[pos, m] = epi( sum_k W[e][m][k] * X[pos][k] ),  epi = silu or identity,
+// W: [n][M][K] bf16 (K-major), X: [rows][K] bf16, out: [rows][M] bf16.
+void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_experts,
+                              size_t M, size_t K, const __nv_bfloat16* X, size_t x_rows,
+                              __nv_bfloat16* out, int silu, const TokenTile* tiles,
+                              const int* n_tiles_dev, size_t max_tiles, int tile_rows);
+
+}  // namespace scmoe
+
+#define SCMOE_LAUNCH_CHECK(c)                                                               \
+    do {                                                                                    \
+        (c)->launches++;                                                                    \
+        cudaError_t _e = cudaGetLastError();                                                \
+        if (_e != cudaSuccess)                                                              \
+            SCMOE_THROW(SCMOE_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+    } while (0)
+
+static inline size_t ceil_div(size_t a, size_t b) { return (a + b - 1) / b; }

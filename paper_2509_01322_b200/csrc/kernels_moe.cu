@@ -1,0 +1,530 @@
+// kernels_moe.cu -- permutation / histogram, row gather, combine, routing
+// counters, bias controller, and weight preparation.
+//
+// Permutation follows moe_block (blocks.hpp:349-359): the tokens of expert e
+// are listed in ascending token order and slot (t, s) gets its position in
+// that list.  On the device the order is made deterministic without sorting:
+// each block of 256 tokens builds, per expert, a 256-bit mask of the tokens
+// that chose it (atomicOr is order independent), a slot's in-block rank is a
+// popcount below its bit, and block offsets come from a scan over blocks.
+#include "internal.cuh"
+#include "libm_port.h"
+
+namespace scmoe {
+
+constexpr int kTB = kPermTokensPerBlock;  // tokens per permutation block
+constexpr int kMaskWords = kTB / 32;
+
+// Pass 1: in-block ranks and per-(block, expert) counts for all E experts.
+__global__ void __launch_bounds__(kTB) perm_hist_kernel(const uint32_t* __restrict__ idx, int T,
+                                                        int K, int E, int* __restrict__ rank_in_block,
+                                                        int* __restrict__ block_counts,
+                                                        int* __restrict__ dev_status) {
+    extern __shared__ uint32_t masks[];  // [E][kMaskWords]
+    for (int i = threadIdx.x; i < E * kMaskWords; i += blockDim.x) masks[i] = 0;
+    __syncthreads();
+    const int tl = threadIdx.x;
+    const int t = blockIdx.x * kTB + tl;
+    const int word = tl >> 5;
+    const uint32_t bit = 1u << (tl & 31);
+    if (t < T) {
+        for (int s = 0; s < K; ++s) {
+            const uint32_t e = idx[(size_t)t * K + s];
+            if (e >= (uint32_t)E) {
+                atomicExch(dev_status, DEV_ERR_INDEX_RANGE);
+                continue;
+            }
+            atomicOr(&masks[e * kMaskWords + word], bit);
+        }
+    }
+    __syncthreads();
+    if (t < T) {
+        for (int s = 0; s < K; ++s) {
+            const uint32_t e = idx[(size_t)t * K + s];
+            if (e >= (uint32_t)E) {
+                rank_in_block[(size_t)t * K + s] = 0;
+                continue;
+            }
+            const uint32_t* m = masks + e * kMaskWords;
+            int r = __popc(m[word] & (bit - 1u));
+            for (int w = 0; w < word; ++w) r += __popc(m[w]);
+            rank_in_block[(size_t)t * K + s] = r;
+        }
+    }
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        int cnt = 0;
+#pragma unroll
+        for (int w = 0; w < kMaskWords; ++w) cnt += __popc(masks[e * kMaskWords + w]);
+        block_counts[(size_t)blockIdx.x * E + e] = cnt;
+    }
+}
+
+// Block-wide exclusive scan helper (blockDim.x == 1024).
+__device__ int block_exclusive_scan(int v, int* total) {
+    __shared__ int warp_sums[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        int w = warp_sums[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        warp_sums[lane] = w;
+    }
+    __syncthreads();
+    const int excl = x - v + (warp > 0 ? warp_sums[warp - 1] : 0);
+    *total = warp_sums[31];
+    __syncthreads();
+    return excl;
+}
+
+// Pass 2 (one block of 1024 threads): per-expert block offsets, expert
+// totals, FFN expert bases (exclusive scan) and the GEMM token-tile list.
+__global__ void __launch_bounds__(1024) perm_scan_kernel(int nblk, int E, int n_ffn,
+                                                         int tile_rows, int* __restrict__ block_counts,
+                                                         int* __restrict__ expert_count,
+                                                         int* __restrict__ expert_base,
+                                                         TokenTile* __restrict__ tiles,
+                                                         int* __restrict__ n_tiles) {
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        int run = 0;
+        for (int b = 0; b < nblk; ++b) {
+            const int cnt = block_counts[(size_t)b * E + e];
+            block_counts[(size_t)b * E + e] = run;
+            run += cnt;
+        }
+        expert_count[e] = run;
+    }
+    __syncthreads();
+    // Chunked scan over the FFN experts: thread i owns experts [i*per, (i+1)*per).
+    const int per = (n_ffn + blockDim.x - 1) / blockDim.x;
+    const int e0 = threadIdx.x * per, e1 = min(n_ffn, e0 + per);
+    int my_rows = 0, my_tiles = 0;
+    for (int e = e0; e < e1; ++e) {
+        my_rows += expert_count[e];
+        my_tiles += (expert_count[e] + tile_rows - 1) / tile_rows;
+    }
+    int total_rows, total_tiles;
+    int row_base = block_exclusive_scan(my_rows, &total_rows);
+    int tile_base = block_exclusive_scan(my_tiles, &total_tiles);
+    for (int e = e0; e < e1; ++e) {
+        expert_base[e] = row_base;
+        const int cnt = expert_count[e];
+        for (int r = 0; r < cnt; r += tile_rows) {
+            TokenTile tt;
+            tt.e = e;
+            tt.pos = row_base + r;
+            tt.count = min(tile_rows, cnt - r);
+            tt.pad = 0;
+            tiles[tile_base++] = tt;
+        }
+        row_base += cnt;
+    }
+    if (threadIdx.x == 0) {
+        expert_base[n_ffn] = total_rows;
+        *n_tiles = total_tiles;
+    }
+}
+
+// Pass 3: slot -> permuted row position, and row -> source token.
+__global__ void perm_scatter_kernel(const uint32_t* __restrict__ idx, int T, int K, int E,
+                                    int n_ffn, const int* __restrict__ rank_in_block,
+                                    const int* __restrict__ block_offsets,
+                                    const int* __restrict__ expert_base, int* __restrict__ slot_pos,
+                                    int* __restrict__ row_token) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (size_t)T * K) return;
+    const int t = (int)(i / K);
+    const uint32_t e = idx[i];
+    if (e >= (uint32_t)n_ffn) {
+        slot_pos[i] = -1;
+        return;
+    }
+    const int b = t / kTB;
+    const int pos = expert_base[e] + block_offsets[(size_t)b * E + e] + rank_in_block[i];
+    slot_pos[i] = pos;
+    row_token[pos] = t;
+}
+
+PermResult launch_permute(scmoe_ctx* c, const uint32_t* idx, size_t T, size_t K, size_t n_ffn,
+                          size_t E, int tile_rows) {
+    Workspace& ws = c->ws;
+    const size_t nblk = ceil_div(std::max<size_t>(T, 1), kTB);
+    PermResult pr;
+    int* rank = ws.rank_in_block.get<int>(T * K);
+    int* bcounts = ws.block_counts.get<int>(nblk * E);
+    pr.expert_count = ws.expert_count.get<int>(E);
+    pr.expert_base = ws.expert_base.get<int>(n_ffn + 1);
+    pr.slot_pos = ws.slot_pos.get<int>(T * K);
+    pr.row_token = ws.row_token.get<int>(T * K);
+    pr.max_tiles = ceil_div(T * K, tile_rows) + n_ffn;
+    pr.tiles = ws.tiles.get<TokenTile>(pr.max_tiles);
+    pr.n_tiles = ws.n_tiles.get<int>(1);
+    const size_t smem = E * kMaskWords * sizeof(uint32_t);
+    SCMOE_CHECK_ARG(smem <= 200 * 1024, SCMOE_ERR_CONFIG, "permute: too many experts");
+    if (smem > 48 * 1024)
+        SCMOE_CUDA(cudaFuncSetAttribute(perm_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+    if (T > 0) {
+        perm_hist_kernel<<<nblk, kTB, smem, c->stream>>>(idx, (int)T, (int)K, (int)E, rank, bcounts,
+                                                         c->dev_status);
+        SCMOE_LAUNCH_CHECK(c);
+    } else {
+        SCMOE_CUDA(cudaMemsetAsync(bcounts, 0, nblk * E * sizeof(int), c->stream));
+    }
+    perm_scan_kernel<<<1, 1024, 0, c->stream>>>((int)nblk, (int)E, (int)n_ffn, tile_rows, bcounts,
+                                                pr.expert_count, pr.expert_base, pr.tiles,
+                                                pr.n_tiles);
+    SCMOE_LAUNCH_CHECK(c);
+    if (T > 0) {
+        perm_scatter_kernel<<<ceil_div(T * K, 256), 256, 0, c->stream>>>(
+            idx, (int)T, (int)K, (int)E, (int)n_ffn, rank, bcounts, pr.expert_base, pr.slot_pos,
+            pr.row_token);
+        SCMOE_LAUNCH_CHECK(c);
+    }
+    return pr;
+}
+
+// Row gather into the permuted order: dst[pos] = src[row_token[pos]] (bf16,
+// 16-byte vectors; one warp per row).  Rows past the total are skipped.
+__global__ void gather_bf16_kernel(const __nv_bfloat16* __restrict__ src, int d,
+                                   const int* __restrict__ row_token,
+                                   const int* __restrict__ total_rows, int max_rows,
+                                   __nv_bfloat16* __restrict__ dst) {
+    const int total = *total_rows;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int vec = d / 8;
+    for (int pos = warp; pos < total && pos < max_rows; pos += nwarps) {
+        const uint4* s = reinterpret_cast<const uint4*>(src + (size_t)row_token[pos] * d);
+        uint4* o = reinterpret_cast<uint4*>(dst + (size_t)pos * d);
+        for (int v = lane; v < vec; v += 32) o[v] = s[v];
+    }
+}
+
+void launch_gather_bf16(scmoe_ctx* c, const __nv_bfloat16* src, size_t d, const int* row_token,
+                        const int* expert_base, size_t n_ffn, size_t max_rows,
+                        __nv_bfloat16* dst) {
+    if (max_rows == 0) return;
+    SCMOE_CHECK_ARG(d % 8 == 0, SCMOE_ERR_DIMENSION, "gather: d must be a multiple of 8");
+    const int blocks = c->num_sms * 8;
+    gather_bf16_kernel<<<blocks, 256, 0, c->stream>>>(src, (int)d, row_token, expert_base + n_ffn,
+                                                      (int)max_rows, dst);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
+// ---------------------------------------------------------------------------
+// Combine -- moe_combine forward (blocks.hpp:226-274) + residual
+// (model.hpp:400).  One block per token, threads over columns.  For slots in
+// rank order: FFN out += (g_ffn*w)*y[pos]; zero zero_w += w; then
+// out += (g_zero*zero_w)*x when zero_w != 0; finally out = residual + out.
+// w = (float)gate / denom with denom = 1 or the rank-order gate sum.
+// ---------------------------------------------------------------------------
+template <typename Y>
+__device__ __forceinline__ float load_y(const Y* p);
+template <>
+__device__ __forceinline__ float load_y<float>(const float* p) {
+    return *p;
+}
+template <>
+__device__ __forceinline__ float load_y<__nv_bfloat16>(const __nv_bfloat16* p) {
+    return __bfloat162float(*p);
+}
+
+constexpr int kMaxK = 64;
+
+template <typename Y>
+__global__ void __launch_bounds__(256) combine_kernel(
+    const float* __restrict__ x, const Y* __restrict__ y, const uint32_t* __restrict__ idx,
+    const double* __restrict__ gates, const int* __restrict__ slot_pos, int d, int K, int n_ffn,
+    float gamma_ffn, float gamma_zero, int renorm, const float* __restrict__ residual,
+    float* __restrict__ out) {
+    __shared__ float coeff[kMaxK];
+    __shared__ int rowpos[kMaxK];
+    __shared__ int nffn, use_zero;
+    __shared__ float zcoeff;
+    const int t = blockIdx.x;
+    if (threadIdx.x == 0) {
+        float denom = 1.0f;
+        if (renorm) {
+            float s = 0.0f;
+            for (int sl = 0; sl < K; ++sl) s = __fadd_rn(s, (float)gates[(size_t)t * K + sl]);
+            denom = s;
+        }
+        float zero_w = 0.0f;
+        int n = 0;
+        for (int sl = 0; sl < K; ++sl) {
+            const uint32_t e = idx[(size_t)t * K + sl];
+            const float w = __fdiv_rn((float)gates[(size_t)t * K + sl], denom);
+            if (e < (uint32_t)n_ffn) {
+                coeff[n] = __fmul_rn(gamma_ffn, w);
+                rowpos[n] = slot_pos[(size_t)t * K + sl];
+                ++n;
+            } else {
+                zero_w = __fadd_rn(zero_w, w);
+            }
+        }
+        nffn = n;
+        // zero_w == 0 skips the identity term entirely (blocks.hpp:266)
+        use_zero = zero_w != 0.0f;
+        zcoeff = __fmul_rn(gamma_zero, zero_w);
+    }
+    __syncthreads();
+    const int n = nffn;
+    const float zc = zcoeff;
+    const bool uz = use_zero != 0;
+    const float* xr = x + (size_t)t * d;
+    float* orow = out + (size_t)t * d;
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+        float acc = 0.0f;
+        for (int s = 0; s < n; ++s)
+            acc = __fadd_rn(acc, __fmul_rn(coeff[s], load_y(y + (size_t)rowpos[s] * d + j)));
+        if (uz) acc = __fadd_rn(acc, __fmul_rn(zc, xr[j]));
+        if (residual) acc = __fadd_rn(residual[(size_t)t * d + j], acc);
+        orow[j] = acc;
+    }
+}
+
+template <typename Y>
+static void launch_combine_impl(scmoe_ctx* c, const float* x, const Y* y, const uint32_t* idx,
+                                const double* gates, const int* slot_pos, size_t T, size_t d,
+                                size_t K, size_t n_ffn, float gamma_ffn, float gamma_zero,
+                                int renorm, const float* residual, float* out) {
+    if (T == 0) return;
+    SCMOE_CHECK_ARG(K <= kMaxK, SCMOE_ERR_CONFIG, "combine: top_k too large");
+    combine_kernel<Y><<<T, 256, 0, c->stream>>>(x, y, idx, gates, slot_pos, (int)d, (int)K,
+                                                (int)n_ffn, gamma_ffn, gamma_zero, renorm,
+                                                residual, out);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
+void launch_combine_f32(scmoe_ctx* c, const float* x, const float* y, const uint32_t* idx,
+                        const double* gates, const int* slot_pos, size_t T, size_t d, size_t K,
+                        size_t n_ffn, float gamma_ffn, float gamma_zero, int renorm,
+                        const float* residual, float* out) {
+    launch_combine_impl<float>(c, x, y, idx, gates, slot_pos, T, d, K, n_ffn, gamma_ffn,
+                               gamma_zero, renorm, residual, out);
+}
+void launch_combine_bf16(scmoe_ctx* c, const float* x, const __nv_bfloat16* y,
+                         const uint32_t* idx, const double* gates, const int* slot_pos, size_t T,
+                         size_t d, size_t K, size_t n_ffn, float gamma_ffn, float gamma_zero,
+                         int renorm, const float* residual, float* out) {
+    launch_combine_impl<__nv_bfloat16>(c, x, y, idx, gates, slot_pos, T, d, K, n_ffn, gamma_ffn,
+                                       gamma_zero, renorm, residual, out);
+}
+
+// ---------------------------------------------------------------------------
+// Index validation (blocks.hpp:375-377) and counters (router.hpp:144-150).
+// ---------------------------------------------------------------------------
+__global__ void check_indices_kernel(const uint32_t* __restrict__ idx, size_t n, uint32_t E,
+                                     int* __restrict__ dev_status) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && idx[i] >= E) atomicExch(dev_status, DEV_ERR_INDEX_RANGE);
+}
+
+void launch_check_indices(scmoe_ctx* c, const uint32_t* idx, size_t n, size_t E) {
+    if (n == 0) return;
+    check_indices_kernel<<<ceil_div(n, 256), 256, 0, c->stream>>>(idx, n, (uint32_t)E,
+                                                                 c->dev_status);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
+__global__ void accumulate_kernel(const uint32_t* __restrict__ idx, size_t n, uint32_t E,
+                                  unsigned long long* __restrict__ routed,
+                                  int* __restrict__ dev_status) {
+    extern __shared__ unsigned int hist[];
+    for (uint32_t e = threadIdx.x; e < E; e += blockDim.x) hist[e] = 0;
+    __syncthreads();
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t e = idx[i];
+        if (e < E)
+            atomicAdd(&hist[e], 1u);
+        else
+            atomicExch(dev_status, DEV_ERR_INDEX_RANGE);
+    }
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < E; e += blockDim.x)
+        if (hist[e]) atomicAdd(&routed[e], (unsigned long long)hist[e]);
+}
+
+void launch_accumulate(scmoe_ctx* c, const uint32_t* idx, size_t n, size_t E, uint64_t* routed) {
+    if (n == 0) return;
+    const int blocks = (int)std::min<size_t>(ceil_div(n, 1024), (size_t)c->num_sms * 2);
+    accumulate_kernel<<<blocks, 1024, E * sizeof(unsigned int), c->stream>>>(
+        idx, n, (uint32_t)E, reinterpret_cast<unsigned long long*>(routed), c->dev_status);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
+// bias_update (router.hpp:155-176), double arithmetic with explicit rounding
+// so nothing is contracted: load = T_i / (K*T_all); delta = mu*(target-load);
+// b += delta; counters reset.  Counter coverage is validated first.
+__global__ void bias_update_kernel(int n_ffn, int E, int top_k, int k_expected, double mu,
+                                   unsigned long long tokens_seen, double* __restrict__ b,
+                                   unsigned long long* __restrict__ routed,
+                                   double* __restrict__ delta, int* __restrict__ dev_status) {
+    __shared__ unsigned long long total;
+    if (threadIdx.x == 0) {
+        unsigned long long s = 0;
+        for (int i = 0; i < E; ++i) s += routed[i];
+        total = s;
+    }
+    __syncthreads();
+    if (total != (unsigned long long)top_k * tokens_seen) {
+        if (threadIdx.x == 0) atomicExch(dev_status, DEV_ERR_COUNTERS);
+        return;
+    }
+    const double t_all = (double)tokens_seen;
+    const double target = __ddiv_rn((double)k_expected, __dmul_rn((double)top_k, (double)n_ffn));
+    for (int i = threadIdx.x; i < E; i += blockDim.x) {
+        double dl = 0.0;
+        if (i < n_ffn) {
+            const double load = __ddiv_rn((double)routed[i], __dmul_rn((double)top_k, t_all));
+            dl = __dmul_rn(mu, __dsub_rn(target, load));
+            b[i] = __dadd_rn(b[i], dl);
+        }
+        if (delta) delta[i] = dl;
+        routed[i] = 0;
+    }
+}
+
+void launch_bias_update(scmoe_ctx* c, scmoe_router* r, double* delta_dev) {
+    bias_update_kernel<<<1, 256, 0, c->stream>>>((int)r->n_ffn, (int)r->E(), (int)r->top_k,
+                                                 (int)r->k_expected, r->mu,
+                                                 (unsigned long long)r->tokens_seen, r->b,
+                                                 reinterpret_cast<unsigned long long*>(r->routed),
+                                                 delta_dev, c->dev_status);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
+// ---------------------------------------------------------------------------
+// Synthetic weights: seeded_init Uniform (rng.hpp:89-94) on the device,
+// bitwise equal to the host: u = ((h >> 11) + 1) * 2^-53 is exact, then
+// (2u - 1) * half_width with separately rounded double ops.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t d_mix64(uint64_t x) {
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdULL;
+    x ^= x >> 33;
+    x *= 0xc4ceb9fe1a85ec53ULL;
+    x ^= x >> 33;
+    return x;
+}
+__device__ __forceinline__ float d_uniform_init(uint64_t seed_mix, uint64_t ctr, double hw) {
+    const uint64_t h = d_mix64(seed_mix ^ d_mix64(ctr + 0xbf58476d1ce4e5b9ULL));
+    const double u = __dmul_rn((double)(h >> 11) + 1.0, 0x1.0p-53);
+    return (float)__dmul_rn(__dsub_rn(__dmul_rn(2.0, u), 1.0), hw);
+}
+
+__global__ void uniform_init_kernel(uint64_t seed_mix, uint64_t first, size_t n, double hw,
+                                    float* __restrict__ out) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x)
+        out[i] = d_uniform_init(seed_mix, first + i, hw);
+}
+
+static uint64_t host_mix64(uint64_t x) {
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdULL;
+    x ^= x >> 33;
+    x *= 0xc4ceb9fe1a85ec53ULL;
+    x ^= x >> 33;
+    return x;
+}
+
+void launch_uniform_init(scmoe_ctx* c, uint64_t seed, uint64_t first, size_t n, double half_width,
+                         float* out) {
+    if (n == 0) return;
+    const uint64_t seed_mix = host_mix64(seed + 0x9e3779b97f4a7c15ULL);
+    uniform_init_kernel<<<c->num_sms * 16, 256, 0, c->stream>>>(seed_mix, first, n, half_width, out);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
+// Uniform init of a [rows, cols] row-major matrix, written transposed as
+// bf16 [cols, rows] (the K-major layout the tcgen05 GEMM reads).
+__global__ void uniform_init_bf16_t_kernel(uint64_t seed_mix, int rows, int cols, double hw,
+                                           __nv_bfloat16* __restrict__ out_t) {
+    __shared__ float tile[32][33];
+    const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int r = r0 + i, cc = c0 + threadIdx.x;
+        if (r < rows && cc < cols)
+            tile[i][threadIdx.x] = d_uniform_init(seed_mix, (uint64_t)r * cols + cc, hw);
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int cc = c0 + i, r = r0 + threadIdx.x;
+        if (r < rows && cc < cols)
+            out_t[(size_t)cc * rows + r] = __float2bfloat16_rn(tile[threadIdx.x][i]);
+    }
+}
+
+void launch_uniform_init_bf16_t(scmoe_ctx* c, uint64_t seed, size_t rows, size_t cols,
+                                double half_width, __nv_bfloat16* out_t) {
+    const uint64_t seed_mix = host_mix64(seed + 0x9e3779b97f4a7c15ULL);
+    dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32));
+    uniform_init_bf16_t_kernel<<<grid, dim3(32, 8), 0, c->stream>>>(seed_mix, (int)rows, (int)cols,
+                                                                   half_width, out_t);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
+__global__ void f32_to_bf16_t_kernel(const float* __restrict__ src, int rows, int cols,
+                                     __nv_bfloat16* __restrict__ dst_t) {
+    __shared__ float tile[32][33];
+    const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int r = r0 + i, cc = c0 + threadIdx.x;
+        if (r < rows && cc < cols) tile[i][threadIdx.x] = src[(size_t)r * cols + cc];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int cc = c0 + i, r = r0 + threadIdx.x;
+        if (r < rows && cc < cols) dst_t[(size_t)cc * rows + r] = __float2bfloat16_rn(tile[threadIdx.x][i]);
+    }
+}
+
+void launch_f32_to_bf16_t(scmoe_ctx* c, const float* src, size_t rows, size_t cols,
+                          __nv_bfloat16* dst_t) {
+    dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32));
+    f32_to_bf16_t_kernel<<<grid, dim3(32, 8), 0, c->stream>>>(src, (int)rows, (int)cols, dst_t);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
+__global__ void cast_bf16_kernel(const float* __restrict__ src, size_t n,
+                                 __nv_bfloat16* __restrict__ dst) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x)
+        dst[i] = __float2bfloat16_rn(src[i]);
+}
+
+void launch_cast_bf16(scmoe_ctx* c, const float* src, size_t n, __nv_bfloat16* dst) {
+    if (n == 0) return;
+    cast_bf16_kernel<<<c->num_sms * 8, 256, 0, c->stream>>>(src, n, dst);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
+// One group, consecutive row tiles (router projection, router.hpp:136).
+__global__ void row_tiles_kernel(int rows, int tile_rows, TokenTile* __restrict__ tiles) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n = (rows + tile_rows - 1) / tile_rows;
+    if (i < n) tiles[i] = TokenTile{0, i * tile_rows, min(tile_rows, rows - i * tile_rows), 0};
+}
+
+void launch_row_tiles(scmoe_ctx* c, size_t rows, int tile_rows, TokenTile* tiles) {
+    const size_t n = ceil_div(rows, tile_rows);
+    if (n == 0) return;
+    row_tiles_kernel<<<ceil_div(n, 256), 256, 0, c->stream>>>((int)rows, tile_rows, tiles);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
+}  // namespace scmoe

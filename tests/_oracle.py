@@ -1,0 +1,210 @@
+"""ctypes access to the parity checkers (TEST INFRASTRUCTURE).
+
+    ORC  oracle/liboracle.so          C restatement (oracle/scmoe_oracle.c)
+    REF  oracle/_ref/libmoelab_ref.so the reference's own templates (ref_shim.cpp)
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+legs may use this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ORACLE_DIR = os.path.join(ROOT, "oracle")
+ORC_PATH = os.path.join(ORACLE_DIR, "liboracle.so")
+REF_PATH = os.path.join(ORACLE_DIR, "_ref", "libmoelab_ref.so")
+
+_P = C.c_void_p
+_SZ = C.c_size_t
+_U64 = C.c_uint64
+_D = C.c_double
+
+ERR = {0: None, 1: "ConfigError", 2: "DimensionError", 3: "StateError", 4: "ParameterError"}
+
+
+def build_oracle():
+    if not os.path.exists(ORC_PATH) or (
+            os.path.exists("/root/reference") and not os.path.exists(REF_PATH)):
+        subprocess.run(["make", "-s", "-C", ORACLE_DIR], check=True)
+
+
+def _load(path, protos):
+    L = C.CDLL(path)
+    for name, (res, args) in protos.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    return L
+
+
+_ORC_PROTOS = {
+    "orc_hash2": (_U64, [_U64, _U64]),
+    "orc_stream_seed": (_U64, [_U64, _U64]),
+    "orc_normal_at": (_D, [_U64, _U64]),
+    "orc_fill_normal_f32": (None, [_U64, _U64, _U64, _P]),
+    "orc_fill_normal_f64": (None, [_U64, _U64, _U64, _P]),
+    "orc_seeded_uniform_f32": (C.c_int, [_U64, _U64, _U64, _D, _P]),
+    "orc_seeded_tn_f64": (C.c_int, [_U64, _U64, _D, _P]),
+    "orc_seeded_tn_f32": (C.c_int, [_U64, _U64, _D, _P]),
+    "orc_mm_f32": (None, [_P, _P, _P, _SZ, _SZ, _SZ]),
+    "orc_mm_f64": (None, [_P, _P, _P, _SZ, _SZ, _SZ]),
+    "orc_softmax_rows_f32": (None, [_P, _P, _SZ, _SZ]),
+    "orc_softmax_rows_f64": (None, [_P, _P, _SZ, _SZ]),
+    "orc_rmsnorm_f32": (None, [_P, _P, _SZ, _SZ, C.c_float, _P]),
+    "orc_expf": (C.c_float, [C.c_float]),
+    "orc_expf_range": (None, [C.c_uint32, _SZ, _P]),
+    "orc_router_validate": (C.c_int, [_SZ, _SZ, _SZ, _SZ, _D, _P]),
+    "orc_select_topk_row_f32": (None, [_P, _P, _SZ, _SZ, _P]),
+    "orc_select_topk_row_f64": (None, [_P, _P, _SZ, _SZ, _P]),
+    "orc_route_from_probs_f32": (C.c_int, [_P, _SZ, _SZ, _SZ, _SZ, _SZ, _D, _P, _P, _P, _P]),
+    "orc_route_from_probs_f64": (C.c_int, [_P, _SZ, _SZ, _SZ, _SZ, _SZ, _D, _P, _P, _P, _P]),
+    "orc_route_topk_f32": (C.c_int, [_P, _SZ, _SZ, _P, _SZ, _SZ, _SZ, _SZ, _D, _P, _P, _P, _P,
+                                     _P]),
+    "orc_route_topk_f64": (C.c_int, [_P, _SZ, _SZ, _P, _SZ, _SZ, _SZ, _SZ, _D, _P, _P, _P, _P,
+                                     _P]),
+    "orc_accumulate_counters": (None, [_P, _SZ, _SZ, _P, _P]),
+    "orc_bias_update": (C.c_int, [_SZ, _SZ, _SZ, _SZ, _P, _D, _P, _P, _P, _P]),
+    "orc_moe_forward_f32": (C.c_int, [_P, _SZ, _SZ, _P, _P, _SZ, _SZ, _SZ, _P, _P, _SZ, _D, _D,
+                                      C.c_int, _P]),
+    "orc_moe_forward_f64": (C.c_int, [_P, _SZ, _SZ, _P, _P, _SZ, _SZ, _SZ, _P, _P, _SZ, _D, _D,
+                                      C.c_int, _P]),
+    "orc_permutation": (None, [_P, _SZ, _SZ, _SZ, _SZ, _P, _P]),
+    "orc_scmoe_layer_f32": (C.c_int, [_P, _P, _P, _SZ, _SZ, _P, _SZ, _SZ, _SZ, _SZ, _D, _P, _P,
+                                      _P, _SZ, _D, _D, C.c_int, _P, _P, _P, _P]),
+    "orc_simulate_bias_control_f32": (C.c_int, [_P, _SZ, _SZ, _SZ, _SZ, _SZ, _P, _D, _P, _U64,
+                                                _SZ, _SZ, _P, _P]),
+}
+
+_REF_PROTOS = {
+    "ref_hash2": (_U64, [_U64, _U64]),
+    "ref_stream_seed": (_U64, [_U64, _U64]),
+    "ref_normal_at": (_D, [_U64, _U64]),
+    "ref_seeded_init_f32": (C.c_int, [_U64, _U64, C.c_int, _D, _P]),
+    "ref_seeded_init_f64": (C.c_int, [_U64, _U64, C.c_int, _D, _P]),
+    "ref_mm_f32": (C.c_int, [_P, _P, _P, _SZ, _SZ, _SZ]),
+    "ref_softmax_rows_f32": (C.c_int, [_P, _P, _SZ, _SZ]),
+    "ref_expf": (C.c_float, [C.c_float]),
+    "ref_route_topk_f32": (C.c_int, [_P, _SZ, _SZ, _P, _SZ, _SZ, _SZ, _SZ, _D, _P, _P, _P, _P, _P,
+                                     C.c_int]),
+    "ref_route_from_probs_f32": (C.c_int, [_P, _SZ, _SZ, _SZ, _SZ, _SZ, _D, _P, _P, _P, _P]),
+    "ref_route_from_probs_f64": (C.c_int, [_P, _SZ, _SZ, _SZ, _SZ, _SZ, _D, _P, _P, _P, _P]),
+    "ref_bias_update": (C.c_int, [_SZ, _SZ, _SZ, _SZ, _P, _D, _P, _P, _P, _P]),
+    "ref_accumulate_counters": (C.c_int, [_P, _SZ, _SZ, _SZ, _SZ, _P, _P]),
+    "ref_moe_forward_f32": (C.c_int, [_P, _SZ, _SZ, _P, _P, _SZ, _SZ, _SZ, _P, _P, _SZ, _SZ,
+                                      C.c_int, _P, C.c_int]),
+    "ref_moe_forward_f64": (C.c_int, [_P, _SZ, _SZ, _P, _P, _SZ, _SZ, _SZ, _P, _P, _SZ, _SZ,
+                                      C.c_int, _P, C.c_int]),
+    "ref_rmsnorm_f32": (C.c_int, [_P, _P, _SZ, _SZ, _P]),
+    "ref_simulate_bias_control_f32": (C.c_int, [_P, _SZ, _SZ, _SZ, _SZ, _SZ, _P, _D, _P, _U64,
+                                                _SZ, _SZ, _P, _P]),
+}
+
+_orc = None
+_ref = None
+
+
+def orc():
+    global _orc
+    if _orc is None:
+        build_oracle()
+        _orc = _load(ORC_PATH, _ORC_PROTOS)
+    return _orc
+
+
+def ref_available() -> bool:
+    if os.path.exists("/root/reference"):
+        build_oracle()
+    return os.path.exists(REF_PATH)
+
+
+def ref():
+    global _ref
+    if _ref is None:
+        build_oracle()
+        _ref = _load(REF_PATH, _REF_PROTOS)
+    return _ref
+
+
+def ptr(a):
+    return None if a is None else a.ctypes.data_as(_P)
+
+
+def ptr_array(arrs):
+    """float* const* from a list of numpy arrays (None -> NULL)."""
+    arr = (_P * len(arrs))()
+    for i, a in enumerate(arrs):
+        arr[i] = None if a is None else a.ctypes.data
+    return arr
+
+
+# ---- synthetic recipe ---------------------------------------
+def normal_f32(seed: int, n: int, first: int = 0) -> np.ndarray:
+    out = np.empty(n, np.float32)
+    orc().orc_fill_normal_f32(seed, first, n, ptr(out))
+    return out
+
+
+def normal_f64(seed: int, n: int, first: int = 0) -> np.ndarray:
+    out = np.empty(n, np.float64)
+    orc().orc_fill_normal_f64(seed, first, n, ptr(out))
+    return out
+
+
+def uniform_f32(seed: int, n: int, variance: float, first: int = 0) -> np.ndarray:
+    out = np.empty(n, np.float32)
+    rc = orc().orc_seeded_uniform_f32(seed, first, n, variance, ptr(out))
+    assert rc == 0
+    return out
+
+
+def stream_seed(seed: int, sid: int) -> int:
+    return int(orc().orc_stream_seed(seed, sid))
+
+
+def bf16_round(a: np.ndarray) -> np.ndarray:
+    """Round fp32 to bf16 (RNE) and widen back to fp32."""
+    u = np.ascontiguousarray(a, np.float32).view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    return r.astype(np.uint32).view(np.float32)
+
+
+# ---- oracle calls -----------------------------------------------------------
+def orc_route_topk(x, w, n_ffn, n_zero, k, ke, mu=0.0, bias=None, want_probs=False):
+    x = np.ascontiguousarray(x, np.float32)
+    w = np.ascontiguousarray(w, np.float32)
+    T, d = x.shape
+    E = n_ffn + n_zero
+    b = np.zeros(E) if bias is None else np.ascontiguousarray(bias, np.float64)
+    idx = np.empty(T * k, np.uint32)
+    g = np.empty(T * k, np.float64)
+    c = np.empty(T, np.uint32)
+    probs = np.empty((T, E), np.float32) if want_probs else None
+    rc = orc().orc_route_topk_f32(ptr(x), T, d, ptr(w), n_ffn, n_zero, k, ke, mu, ptr(b),
+                                  ptr(idx), ptr(g), ptr(c), ptr(probs))
+    return rc, idx, g, c, probs
+
+
+def orc_moe_forward(x, idx, gates, k, n_ffn, n_zero, w_in, w_out, gamma_ffn=1.0,
+                    gamma_zero=1.0, renorm=False):
+    x = np.ascontiguousarray(x, np.float32)
+    T, d = x.shape
+    I = next(w for w in w_in if w is not None).shape[1]
+    out = np.empty((T, d), np.float32)
+    w_in = [None if w is None else np.ascontiguousarray(w, np.float32) for w in w_in]
+    w_out = [None if w is None else np.ascontiguousarray(w, np.float32) for w in w_out]
+    rc = orc().orc_moe_forward_f32(ptr(x), T, d, ptr(np.ascontiguousarray(idx, np.uint32)),
+                                   ptr(np.ascontiguousarray(gates, np.float64)), k, n_ffn, n_zero,
+                                   ptr_array(w_in), ptr_array(w_out), I, gamma_ffn, gamma_zero,
+                                   int(renorm), ptr(out))
+    return rc, out
+
+
+def rel_l2(a, b) -> float:
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))

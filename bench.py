@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""ScMoE layer benchmark (BASELINE.json metric: ScMoE layer tokens/sec).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config prefill|decode]
+
+N=1 workload = BASELINE config 2 ("prefill"): one LongCat-Flash-shape MoE
+layer (d=6144, 512 FFN experts with inter 2048 + 256 zero experts, top-12,
+K_e=8), 8192 tokens, bf16 expert GEMMs on tcgen05, exact fp32 router.  A step
+is one full ScMoE MoE-branch forward through the C ABI
+(scmoe_layer_forward: rmsnorm -> exact router -> permutation -> grouped GEMM1
+(+SiLU) -> grouped GEMM2 -> combine with zero-expert identity + residual).
+
+For N>1 (torchrun, one process per GPU) every rank runs the same layer on its
+own 8192-token shard with the full expert set resident (replicated experts,
+token-sharded; no data-path collective) -> "scaling": "weak".
+
+`value` is device-timed (CUDA events on the layer's stream, inputs resident in
+HBM, inputs + weights larger than L2); `e2e` is the same metric through the
+host tier (scmoe_layer_forward_host) with pinned host buffers, H2D of the
+step's inputs and D2H of its outputs inside the timed region.
+`--impl reference` times the reference's own CPU code (oracle/_ref, compiled
+from /root/reference headers; the C restatement when absent) on this host's
+cores on a bounded token sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ScMoE layer tokens/sec"
+D, N_FFN, N_ZERO, TOPK, KE, INTER = 6144, 512, 256, 12, 8, 2048
+CONFIGS = {
+    "prefill": dict(tokens=8192, workload="LongCat-Flash ScMoE MoE layer prefill (BASELINE config 2)"),
+    "decode": dict(tokens=256, workload="LongCat-Flash ScMoE MoE layer decode step (BASELINE config 3)"),
+}
+SEED_W, SEED_X = 5, 99
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v: float, ws: int) -> float:
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            self.p.wait()
+
+    def summary(self):
+        self.f.flush()
+        rows = [r.split(", ") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        rows = [r for r in rows if len(r) >= 9]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows]
+        mx = max(float(r[2]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.strip() == "Active"})
+        loaded = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows)}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle/_ref = the reference's own code) on a bounded sample
+# ---------------------------------------------------------------------------
+def reference_cpu_sample(route_tokens=64, moe_tokens=16, threads=None, log_fn=log):
+    """tokens/s of the reference's route_topk + moe_forward at the LongCat
+    shape on this host, token-sharded over `threads` (bitwise identical to a
+    monolithic call).  Only the experts the sample hits are materialised."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import _oracle as O
+    from concurrent.futures import ThreadPoolExecutor
+    from _oracle import ptr, ptr_array
+
+    threads = threads or os.cpu_count() or 1
+    kind = "reference" if O.ref_available() else "port"
+    E = N_FFN + N_ZERO
+    x = O.normal_f32(O.stream_seed(SEED_X, 0), route_tokens * D).reshape(route_tokens, D)
+    w = O.uniform_f32(O.stream_seed(SEED_W, 0), D * E, 1.0 / D).reshape(D, E)
+    idx = np.empty(route_tokens * TOPK, np.uint32)
+    g = np.empty(route_tokens * TOPK)
+    cnt = np.empty(route_tokens, np.uint32)
+    b = np.zeros(E)
+    t0 = time.perf_counter()
+    if kind == "reference":
+        rc = O.ref().ref_route_topk_f32(ptr(x), route_tokens, D, ptr(w), N_FFN, N_ZERO, TOPK, KE,
+                                        0.0, ptr(b), ptr(idx), ptr(g), ptr(cnt), None, threads)
+    else:
+        rc = O.orc().orc_route_topk_f32(ptr(x), route_tokens, D, ptr(w), N_FFN, N_ZERO, TOPK, KE,
+                                        0.0, ptr(b), ptr(idx), ptr(g), ptr(cnt), None)
+    t_route = time.perf_counter() - t0
+    assert rc == 0
+    mi = idx[:moe_tokens * TOPK]
+    hit = sorted({int(e) for e in mi if e < N_FFN})
+
+    def gen(e):
+        a = np.empty(D * INTER, np.float32)
+        bb = np.empty(D * INTER, np.float32)
+        O.orc().orc_seeded_uniform_f32(O.stream_seed(SEED_W, 100 + 2 * e), 0, D * INTER, 1.0 / D, ptr(a))
+        O.orc().orc_seeded_uniform_f32(O.stream_seed(SEED_W, 101 + 2 * e), 0, D * INTER, 1.0 / D, ptr(bb))
+        return e, a, bb
+
+    w_in = [None] * N_FFN
+    w_out = [None] * N_FFN
+    with ThreadPoolExecutor(threads) as ex:
+        for e, a, bb in ex.map(gen, hit):
+            w_in[e], w_out[e] = a, bb
+    out = np.empty((moe_tokens, D), np.float32)
+    t0 = time.perf_counter()
+    if kind == "reference":
+        rc = O.ref().ref_moe_forward_f32(ptr(x[:moe_tokens]), moe_tokens, D, ptr(mi), ptr(g), TOPK,
+                                         N_FFN, N_ZERO, ptr_array(w_in), ptr_array(w_out), INTER, 1,
+                                         0, ptr(out), min(threads, moe_tokens))
+        used = max(min(threads, moe_tokens), min(threads, route_tokens))
+    else:
+        rc = O.orc().orc_moe_forward_f32(ptr(x[:moe_tokens]), moe_tokens, D, ptr(mi), ptr(g),
+                                         TOPK, N_FFN, N_ZERO, ptr_array(w_in), ptr_array(w_out),
+                                         INTER, 1.0, 1.0, 0, ptr(out))
+        used = 1
+    t_moe = time.perf_counter() - t0
+    assert rc == 0
+    per_token = t_route / route_tokens + t_moe / moe_tokens
+    value = 1.0 / per_token
+    sample = (f"route_topk on {route_tokens} tokens ({t_route:.2f}s) + moe_forward on "
+              f"{moe_tokens} tokens ({t_moe:.2f}s, {len(hit)} experts materialised), LongCat "
+              f"shape fp32, token-sharded over {used} threads")
+    log_fn("cpu reference:", sample, f"-> {value:.2f} tok/s")
+    return {"value": value, "unit": "tokens/s", "cores": used, "kind": kind, "sample": sample}
+
+
+def run_reference_arm(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    vals = []
+    base = None
+    for i in range(args.warmup + args.steps):
+        r = reference_cpu_sample(route_tokens=32, moe_tokens=8)
+        if i >= args.warmup:
+            vals.append(r["value"])
+            base = r
+    v = statistics.mean(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (CounterRng normal inputs, seeded_init Uniform weights)",
+        "config": {"workload": cfg["workload"], "tokens": cfg["tokens"], "d_model": D,
+                   "n_ffn": N_FFN, "n_zero": N_ZERO, "top_k": TOPK, "inter": INTER,
+                   "parallelism": f"cpu x{base['cores']}"},
+        "cpu_baseline": {**base, "value": v},
+        "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+def gemm_algorithmic_bytes(idx: np.ndarray, T: int):
+    """Algorithmic bytes of the two grouped-GEMM launches of one step: the
+    bf16 weights of every hit expert once + activations in/out once."""
+    ffn = idx[idx < N_FFN]
+    S = int(ffn.size)
+    n_hit = int(np.unique(ffn).size)
+    w_bytes = n_hit * D * INTER * 2
+    g1 = w_bytes + S * D * 2 + S * INTER * 2
+    g2 = w_bytes + S * INTER * 2 + S * D * 2
+    flops = 2 * 2 * S * D * INTER
+    return g1, g2, S, n_hit, flops
+
+
+def run_b200(args):
+    import torch
+    ws, rank, local = dist_init()
+    torch.cuda.set_device(local)
+    import paper_2509_01322_b200 as P
+    from paper_2509_01322_b200.layer import LONGCAT, DeviceLayer
+
+    cfg = CONFIGS[args.config]
+    T = args.tokens or cfg["tokens"]
+    ctx = P.Context(local)
+    stream = torch.cuda.Stream()
+    ctx.set_stream(stream.cuda_stream)
+    t0 = time.time()
+    layer = DeviceLayer(ctx, LONGCAT, seed=SEED_W)
+    # inputs: a1 (shortcut stream) and a3 (dense-branch output / residual)
+    a1_h = P.fill_normal(P.stream_seed(SEED_X, rank), T * D, threads=os.cpu_count() or 8)
+    a3_h = P.fill_normal(P.stream_seed(SEED_X + 1, rank), T * D, threads=os.cpu_count() or 8)
+    a1 = torch.from_numpy(a1_h).cuda()
+    a3 = torch.from_numpy(a3_h).cuda()
+    idx = torch.empty(T * TOPK, dtype=torch.int32, device="cuda")
+    gates = torch.empty(T * TOPK, dtype=torch.float64, device="cuda")
+    cnt = torch.empty(T, dtype=torch.int32, device="cuda")
+    out = torch.empty(T, D, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    log(f"[rank {rank}] setup {time.time() - t0:.1f}s; bank {layer.bank_bytes() / 1e9:.2f} GB")
+
+    def step():
+        layer.forward(a1.data_ptr(), a3.data_ptr(), None, T, idx.data_ptr(), gates.data_ptr(),
+                      cnt.data_ptr(), out.data_ptr())
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+        ctx.synchronize()
+    idx_h = idx.cpu().numpy().view(np.uint32)
+    g1b, g2b, S, n_hit, flops = gemm_algorithmic_bytes(idx_h, T)
+    ffn_mean = float(cnt.cpu().numpy().mean())
+
+    # ---- timed region: device events on the layer's stream -----------------
+    ctx.profile(True)
+    ctx.profile_flush()
+    l0 = ctx.kernel_launches()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    barrier(ws)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+            for _ in range(args.steps):
+                step()
+            ev1.record(stream)
+        ev1.synchronize()
+    torch.cuda.synchronize()
+    barrier(ws)
+    launches = ctx.kernel_launches() - l0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    stages = ctx.profile_flush()
+    ctx.profile(False)
+    ms_max = max_over_ranks(ms, ws)
+    value = T * ws / (ms_max / 1e3)
+
+    # ---- e2e through the host tier (pinned buffers, copies in the region) --
+    a1_p = torch.empty(T, D, dtype=torch.float32).pin_memory()
+    a3_p = torch.empty(T, D, dtype=torch.float32).pin_memory()
+    a1_p.copy_(torch.from_numpy(a1_h.reshape(T, D)))
+    a3_p.copy_(torch.from_numpy(a3_h.reshape(T, D)))
+    out_p = torch.empty(T, D, dtype=torch.float32).pin_memory()
+    idx_p = torch.empty(T * TOPK, dtype=torch.int32).pin_memory()
+    gat_p = torch.empty(T * TOPK, dtype=torch.float64).pin_memory()
+    cnt_p = torch.empty(T, dtype=torch.int32).pin_memory()
+    host = [a.numpy() for a in (a1_p, a3_p, idx_p, gat_p, cnt_p, out_p)]
+    e_steps = max(1, min(args.steps, 5))
+    layer.forward_host(host[0], host[1], None, T, host[2], host[3], host[4], host[5])
+    barrier(ws)
+    with torch.cuda.stream(stream):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e_steps):
+            layer.forward_host(host[0], host[1], None, T, host[2], host[3], host[4], host[5])
+        e1.record(stream)
+        e1.synchronize()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e_steps, ws)
+    e2e_val = T * ws / (e2e_ms / 1e3)
+    h2d = 2 * T * D * 4
+    d2h = T * D * 4 + T * TOPK * (4 + 8) + T * 4
+
+    if rank != 0:
+        return
+    peaks = measured_peaks()
+    hbm_peak = peaks["hbm_gbs"] if peaks else 6650.0
+    g1 = stages.get("gemm1_tcgen05", (0.0, 1))
+    g2 = stages.get("gemm2_tcgen05", (0.0, 1))
+    t_gemm = (g1[0] + g2[0]) / max(1, g1[1])  # per step (one launch each per step)
+    achieved = (g1b + g2b) / (t_gemm / 1e3) / 1e9 if t_gemm > 0 else None
+    per_stage = {k: round(v[0] / v[1], 4) for k, v in stages.items()}
+    cpu = None
+    if ws == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = reference_cpu_sample()
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "reference",
+                   "sample": f"failed: {e}"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (CounterRng normal inputs, seeded_init Uniform weights, random-init)",
+        "config": {"workload": cfg["workload"], "tokens_per_gpu": T, "d_model": D, "n_ffn": N_FFN,
+                   "n_zero": N_ZERO, "top_k": TOPK, "k_expected": KE, "inter": INTER,
+                   "router": "exact fp32 (bit-exact vs reference)", "expert_gemm": "bf16 tcgen05",
+                   "parallelism": f"replicated experts, token-sharded x{ws}",
+                   "l2": "inputs + weights (25.8 GB) larger than L2 every step",
+                   "mean_ffn_per_token": ffn_mean, "ffn_slots": S, "experts_hit": n_hit},
+        "e2e": {"value": e2e_val, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+        "gpu_launches": launches,
+        "roofline": {"kernel": "grouped_gemm_bf16 (GEMM1+GEMM2)", "bound": "hbm",
+                     "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": (achieved / hbm_peak) if achieved else None, "traffic": None,
+                     "algorithmic_bytes_per_step": g1b + g2b, "ms_per_step": t_gemm,
+                     "tflops": flops / (t_gemm / 1e3) / 1e12 if t_gemm > 0 else None,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},
+        "stages_ms": per_stage,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="prefill", choices=sorted(CONFIGS))
+    ap.add_argument("--tokens", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -185,6 +185,13 @@ int scmoe_rng_fill_uniform(scmoe_ctx* ctx, uint64_t seed, uint64_t first, size_t
                            double variance, float* out_dev);
 
 /* ---- diagnostics ---------------------------------------------------------- */
+/* Per-stage timing with CUDA events on the context's stream (off by default).
+ * flush() waits for the stream and aggregates by stage name; entry(i) reads
+ * one aggregate (name valid until the next flush). */
+int scmoe_profile_enable(scmoe_ctx* ctx, int on);
+int scmoe_profile_flush(scmoe_ctx* ctx, int* n_entries);
+int scmoe_profile_entry(scmoe_ctx* ctx, int i, const char** name, double* total_ms,
+                        uint64_t* launches);
 /* out[i] = device instantiation of the glibc-expf restatement used by the
  * softmax and SiLU kernels (bit-exactness check against host libm). */
 int scmoe_debug_expf(scmoe_ctx* ctx, const float* in_dev, float* out_dev, size_t n);

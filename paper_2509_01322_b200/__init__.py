@@ -136,6 +136,10 @@ _PROTOS = {
     "scmoe_rng_stream_seed": (_U64, [_U64, _U64]),
     "scmoe_rng_fill_normal_host": (None, [_U64, _U64, _SZ, _P, C.c_int]),
     "scmoe_rng_fill_uniform": (C.c_int, [_P, _U64, _U64, _SZ, C.c_double, _P]),
+    "scmoe_profile_enable": (C.c_int, [_P, C.c_int]),
+    "scmoe_profile_flush": (C.c_int, [_P, C.POINTER(C.c_int)]),
+    "scmoe_profile_entry": (C.c_int, [_P, C.c_int, C.POINTER(C.c_char_p), C.POINTER(C.c_double),
+                                      C.POINTER(_U64)]),
     "scmoe_debug_expf": (C.c_int, [_P, _P, _P, _SZ]),
     "scmoe_debug_expf_range": (C.c_int, [_P, C.c_uint32, _P, _SZ]),
 }
@@ -192,6 +196,21 @@ class Context:
 
     def kernel_launches(self) -> int:
         return int(lib().scmoe_kernel_launches(self._h))
+
+    def profile(self, on: bool = True):
+        self._check(lib().scmoe_profile_enable(self._h, int(on)))
+
+    def profile_flush(self) -> dict:
+        """{stage: (total_ms, launches)} since the last flush (syncs the stream)."""
+        n = C.c_int()
+        self._check(lib().scmoe_profile_flush(self._h, C.byref(n)))
+        out = {}
+        for i in range(n.value):
+            name, ms, cnt = C.c_char_p(), C.c_double(), _U64()
+            self._check(lib().scmoe_profile_entry(self._h, i, C.byref(name), C.byref(ms),
+                                                  C.byref(cnt)))
+            out[name.value.decode()] = (ms.value, int(cnt.value))
+        return out
 
     def close(self):
         if self._h:

@@ -93,17 +93,17 @@ void moe_forward_dev(scmoe_ctx* c, scmoe_bank* b, const float* x, const __nv_bfl
     const size_t n_ffn = b->n, d = b->d, I = b->inter, E = n_ffn + n_zero;
     SCMOE_CHECK_ARG(K >= 1 && K <= 64, SCMOE_ERR_CONFIG, "moe_forward: top_k must be in [1, 64]");
     Workspace& ws = c->ws;
-    PermResult pr = launch_permute(c, idx, T, K, n_ffn, E, tile_rows_for(b));
+    PermResult pr; { ProfScope _p(c, "permute"); pr = launch_permute(c, idx, T, K, n_ffn, E, tile_rows_for(b)); }
     const float gf = (float)b->gamma_ffn(), gz = (float)b->gamma_zero();
     if (b->precision == SCMOE_PREC_F32_EXACT) {
         float* h = ws.h.get<float>(T * K * I + 1);
         float* y = ws.y.get<float>(T * K * d + 1);
-        launch_seq_gemm(c, x, d, pr.row_token, b->w_in32, I, d * I, h, I, d, I, /*silu=*/1,
-                        pr.tiles, pr.n_tiles, pr.max_tiles);
-        launch_seq_gemm(c, h, I, nullptr, b->w_out32, d, I * d, y, d, I, d, /*silu=*/0, pr.tiles,
-                        pr.n_tiles, pr.max_tiles);
-        launch_combine_f32(c, x, y, idx, gates, pr.slot_pos, T, d, K, n_ffn, gf, gz, renorm,
-                           residual, out);
+        { ProfScope _p(c, "expert_gemm1_f32"); launch_seq_gemm(c, x, d, pr.row_token, b->w_in32, I, d * I, h, I, d, I, /*silu=*/1,
+                        pr.tiles, pr.n_tiles, pr.max_tiles); }
+        { ProfScope _p(c, "expert_gemm2_f32"); launch_seq_gemm(c, h, I, nullptr, b->w_out32, d, I * d, y, d, I, d, /*silu=*/0, pr.tiles,
+                        pr.n_tiles, pr.max_tiles); }
+        { ProfScope _p(c, "combine"); launch_combine_f32(c, x, y, idx, gates, pr.slot_pos, T, d, K, n_ffn, gf, gz, renorm,
+                           residual, out); }
     } else {
         __nv_bfloat16* xb = const_cast<__nv_bfloat16*>(x_bf16);
         if (!xb) {
@@ -114,13 +114,13 @@ void moe_forward_dev(scmoe_ctx* c, scmoe_bank* b, const float* x, const __nv_bfl
         __nv_bfloat16* xp = ws.xp.get<__nv_bfloat16>(T * K * d + 1);
         __nv_bfloat16* h = ws.h.get<__nv_bfloat16>(T * K * I + 1);
         __nv_bfloat16* y = ws.y.get<__nv_bfloat16>(T * K * d + 1);
-        launch_gather_bf16(c, xb, d, pr.row_token, pr.expert_base, n_ffn, T * K, xp);
-        launch_grouped_gemm_bf16(c, b->w1t, n_ffn, I, d, xp, T * K, h, /*silu=*/1, pr.tiles,
-                                 pr.n_tiles, pr.max_tiles, tile_rows_for(b));
-        launch_grouped_gemm_bf16(c, b->w2t, n_ffn, d, I, h, T * K, y, /*silu=*/0, pr.tiles,
-                                 pr.n_tiles, pr.max_tiles, tile_rows_for(b));
-        launch_combine_bf16(c, x, y, idx, gates, pr.slot_pos, T, d, K, n_ffn, gf, gz, renorm,
-                            residual, out);
+        { ProfScope _p(c, "gather"); launch_gather_bf16(c, xb, d, pr.row_token, pr.expert_base, n_ffn, T * K, xp); }
+        { ProfScope _p(c, "gemm1_tcgen05"); launch_grouped_gemm_bf16(c, b->w1t, n_ffn, I, d, xp, T * K, h, /*silu=*/1, pr.tiles,
+                                 pr.n_tiles, pr.max_tiles, tile_rows_for(b)); }
+        { ProfScope _p(c, "gemm2_tcgen05"); launch_grouped_gemm_bf16(c, b->w2t, n_ffn, d, I, h, T * K, y, /*silu=*/0, pr.tiles,
+                                 pr.n_tiles, pr.max_tiles, tile_rows_for(b)); }
+        { ProfScope _p(c, "combine"); launch_combine_bf16(c, x, y, idx, gates, pr.slot_pos, T, d, K, n_ffn, gf, gz, renorm,
+                            residual, out); }
     }
 }
 
@@ -321,8 +321,8 @@ int scmoe_route_topk(scmoe_ctx* c, scmoe_router* r, const float* x, size_t T, ui
         const size_t ntile = ceil_div(T, 64);
         TokenTile* td = c->ws.misc.get<TokenTile>(ntile);
         launch_row_tiles(c, T, 64, td);
-        launch_seq_gemm(c, x, r->d, nullptr, r->w, E, 0, logits, E, r->d, E, 0, td, nullptr, ntile);
-        launch_softmax_topk(c, logits, T, E, r->top_k, r->n_ffn, r->b, idx, gates, ffn_count, probs);
+        { ProfScope _p(c, "router_gemm"); launch_seq_gemm(c, x, r->d, nullptr, r->w, E, 0, logits, E, r->d, E, 0, td, nullptr, ntile); }
+        { ProfScope _p(c, "softmax_topk"); launch_softmax_topk(c, logits, T, E, r->top_k, r->n_ffn, r->b, idx, gates, ffn_count, probs); }
     });
 }
 
@@ -579,13 +579,13 @@ int scmoe_layer_forward(scmoe_ctx* c, scmoe_router* r, scmoe_bank* b, const floa
         float* hmoe = ws.hmoe.get<float>(T * d);
         __nv_bfloat16* hb =
             b->precision == SCMOE_PREC_BF16 ? ws.hmoe_bf16.get<__nv_bfloat16>(T * d) : nullptr;
-        launch_rmsnorm(c, a1, gain, T, d, 1e-6f, hmoe, hb);
+        { ProfScope _p(c, "rmsnorm"); launch_rmsnorm(c, a1, gain, T, d, 1e-6f, hmoe, hb); }
         float* logits = ws.logits.get<float>(T * E);
         const size_t ntile = ceil_div(T, 64);
         TokenTile* td = ws.misc.get<TokenTile>(ntile);
         launch_row_tiles(c, T, 64, td);
-        launch_seq_gemm(c, hmoe, d, nullptr, r->w, E, 0, logits, E, d, E, 0, td, nullptr, ntile);
-        launch_softmax_topk(c, logits, T, E, K, r->n_ffn, r->b, idx, gates, ffn_count, nullptr);
+        { ProfScope _p(c, "router_gemm"); launch_seq_gemm(c, hmoe, d, nullptr, r->w, E, 0, logits, E, d, E, 0, td, nullptr, ntile); }
+        { ProfScope _p(c, "softmax_topk"); launch_softmax_topk(c, logits, T, E, K, r->n_ffn, r->b, idx, gates, ffn_count, nullptr); }
         moe_forward_dev(c, b, hmoe, hb, T, idx, gates, K, r->n_zero, renorm, a3, out);
     });
 }
@@ -632,6 +632,47 @@ int scmoe_debug_expf(scmoe_ctx* c, const float* in, float* out, size_t n) {
     return guarded(c, [&] {
         require_ctx(c);
         launch_debug_expf(c, in, out, n);
+    });
+}
+
+int scmoe_profile_enable(scmoe_ctx* c, int on) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        c->prof.on = on != 0;
+    });
+}
+
+int scmoe_profile_flush(scmoe_ctx* c, int* n_entries) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        SCMOE_CUDA(cudaStreamSynchronize(c->stream));
+        Profiler& p = c->prof;
+        p.agg.clear();
+        for (size_t i = 0; i < p.used; ++i) {
+            float ms = 0.f;
+            SCMOE_CUDA(cudaEventElapsedTime(&ms, p.recs[i].a, p.recs[i].b));
+            ProfAgg* a = nullptr;
+            for (auto& x : p.agg)
+                if (x.name == p.recs[i].name) a = &x;
+            if (!a) {
+                p.agg.push_back(ProfAgg{p.recs[i].name, 0.0, 0});
+                a = &p.agg.back();
+            }
+            a->ms += ms;
+            a->count++;
+        }
+        p.used = 0;
+        if (n_entries) *n_entries = (int)p.agg.size();
+    });
+}
+
+int scmoe_profile_entry(scmoe_ctx* c, int i, const char** name, double* total_ms,
+                        uint64_t* launches) {
+    return guarded(c, [&] {
+        if (i < 0 || (size_t)i >= c->prof.agg.size()) SCMOE_THROW(SCMOE_ERR_PARAMETER, "no such entry");
+        if (name) *name = c->prof.agg[i].name.c_str();
+        if (total_ms) *total_ms = c->prof.agg[i].ms;
+        if (launches) *launches = c->prof.agg[i].count;
     });
 }
 

@@ -73,6 +73,24 @@ struct Workspace {
     }
 };
 
+// Optional per-kernel timing: CUDA events recorded on the launching stream
+// around each named stage (scmoe_profile_* in the ABI).
+struct ProfRec {
+    const char* name;
+    cudaEvent_t a, b;
+};
+struct ProfAgg {
+    std::string name;
+    double ms = 0.0;
+    uint64_t count = 0;
+};
+struct Profiler {
+    bool on = false;
+    std::vector<ProfRec> recs;
+    size_t used = 0;
+    std::vector<ProfAgg> agg;
+};
+
 struct scmoe_ctx {
     int device = 0;
     int num_sms = 148;
@@ -82,6 +100,29 @@ struct scmoe_ctx {
     int* dev_status = nullptr;  // latched device-side error
     uint64_t launches = 0;
     Workspace ws;
+    Profiler prof;
+};
+
+// RAII stage timer; a no-op unless profiling is enabled on the context.
+struct ProfScope {
+    scmoe_ctx* c;
+    size_t i = SIZE_MAX;
+    ProfScope(scmoe_ctx* ctx, const char* name) : c(ctx) {
+        if (!c->prof.on) return;
+        Profiler& p = c->prof;
+        if (p.used == p.recs.size()) {
+            ProfRec r{name, nullptr, nullptr};
+            cudaEventCreate(&r.a);
+            cudaEventCreate(&r.b);
+            p.recs.push_back(r);
+        }
+        i = p.used++;
+        p.recs[i].name = name;
+        cudaEventRecord(p.recs[i].a, c->stream);
+    }
+    ~ProfScope() {
+        if (i != SIZE_MAX) cudaEventRecord(c->prof.recs[i].b, c->stream);
+    }
 };
 
 struct scmoe_router {

@@ -1,0 +1,90 @@
+"""Device-tier ScMoE layer: router + expert bank resident in HBM, inputs and
+outputs as device pointers (e.g. torch CUDA tensors' data_ptr()).
+
+This is the serving/benchmark entry point; the reference-shaped API in
+``paper_2509_01322_b200`` (route_topk, moe_forward, ...) is the host tier.
+Synthetic weights follow SURVEY.md 8(d): router W_r = seeded_init Uniform
+(variance 1/d) of CounterRng(seed).stream(0); expert e's w_in / w_out =
+seeded_init Uniform of stream(100 + 2e) / stream(101 + 2e), generated on the
+device bit-for-bit as the reference's rng.hpp would on the host.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+from . import (PREC_BF16, Context, GammaMode, _P, lib)
+
+
+@dataclass
+class LayerShape:
+    d: int = 6144
+    n_ffn: int = 512
+    n_zero: int = 256
+    top_k: int = 12
+    k_expected: int = 8
+    inter: int = 2048
+    m: int = 1
+    gamma_mode: int = int(GammaMode.FfnOnly)
+    precision: int = PREC_BF16
+
+    @property
+    def E(self) -> int:
+        return self.n_ffn + self.n_zero
+
+
+LONGCAT = LayerShape()
+TINY = LayerShape(d=256, n_ffn=8, n_zero=4, top_k=2, k_expected=1, inter=128, precision=0)
+
+
+class DeviceLayer:
+    def __init__(self, ctx: Context, shape: LayerShape, seed: int = 5, mu: float = 0.0,
+                 mu_decay: float = 1.0):
+        self.ctx, self.shape = ctx, shape
+        L = lib()
+        s = shape
+        self.router = _P()
+        ctx._check(L.scmoe_router_create(ctx.handle, s.d, s.n_ffn, s.n_zero, s.top_k,
+                                         s.k_expected, mu, mu_decay, C.byref(self.router)))
+        # router weights: generated on the device into a scratch buffer
+        wbuf = _P()
+        nbytes = s.d * s.E * 4
+        ctx._check(L.scmoe_device_alloc(ctx.handle, nbytes, C.byref(wbuf)))
+        sd = int(L.scmoe_rng_stream_seed(seed, 0))
+        ctx._check(L.scmoe_rng_fill_uniform(ctx.handle, sd, 0, s.d * s.E, 1.0 / s.d, wbuf))
+        ctx._check(L.scmoe_router_set_weights(ctx.handle, self.router, wbuf))
+        ctx.synchronize()
+        ctx._check(L.scmoe_device_free(ctx.handle, wbuf))
+        self.bank = _P()
+        ctx._check(L.scmoe_bank_create(ctx.handle, s.n_ffn, s.d, s.inter, s.precision, s.m,
+                                       s.gamma_mode, C.byref(self.bank)))
+        ctx._check(L.scmoe_bank_init_uniform(ctx.handle, self.bank, seed, 100, 1.0 / s.d))
+
+    def bank_bytes(self) -> int:
+        return int(lib().scmoe_bank_device_bytes(self.bank))
+
+    def forward(self, a1: int, a3: int, gain: Optional[int], tokens: int, idx: int, gates: int,
+                ffn_count: int, out: int, renormalize: bool = False):
+        """Device pointers; stream-ordered on the context's stream."""
+        self.ctx._check(lib().scmoe_layer_forward(self.ctx.handle, self.router, self.bank, a1, a3,
+                                                  gain, tokens, int(renormalize), idx, gates,
+                                                  ffn_count, out))
+
+    def forward_host(self, a1, a3, gain, tokens: int, idx, gates, ffn_count, out,
+                     renormalize: bool = False):
+        """Host (ideally pinned) numpy buffers; copies in, runs, copies out."""
+        p = lambda a: None if a is None else a.ctypes.data_as(_P)  # noqa: E731
+        self.ctx._check(lib().scmoe_layer_forward_host(self.ctx.handle, self.router, self.bank,
+                                                       p(a1), p(a3), p(gain), tokens,
+                                                       int(renormalize), p(idx), p(gates),
+                                                       p(ffn_count), p(out)))
+
+    def close(self):
+        L = lib()
+        if self.bank:
+            L.scmoe_bank_destroy(self.ctx.handle, self.bank)
+            self.bank = _P()
+        if self.router:
+            L.scmoe_router_destroy(self.ctx.handle, self.router)
+            self.router = _P()

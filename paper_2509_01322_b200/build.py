@@ -70,7 +70,7 @@ def check_sass(lib: str = LIB) -> dict:
     # The plain sequential-k GEMM (router projection, fp32 W_out GEMM) must be
     # pure FMUL + FADD.  The SiLU instantiation's only FFMAs come from the
     # correctly rounded IEEE division (__fdiv_rn) inside the logistic.
-    seq = [n for n in summary if "seq_gemm_kernelILb0" in n]
+    seq = [n for n in summary if re.search(r"seq_gemm_kernel.*Lb0EE", n)]
     assert seq, "seq_gemm kernel missing from SASS"
     for n in seq:
         assert summary[n]["FFMA"] == 0, f"{n}: FFMA found in exact-order kernel"

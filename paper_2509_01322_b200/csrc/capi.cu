@@ -83,7 +83,9 @@ void require_ctx(scmoe_ctx* c) {
     SCMOE_CUDA(cudaSetDevice(c->device));
 }
 
-int tile_rows_for(const scmoe_bank* b) { return b->precision == SCMOE_PREC_BF16 ? 128 : 64; }
+int tile_rows_for(const scmoe_bank* b) {
+    return b->precision == SCMOE_PREC_BF16 ? grouped_gemm_tile_rows() : 64;
+}
 
 // moe_forward on device pointers; x is the MoE input (hmoe), used by the
 // expert FFN and by the zero-expert identity term.
@@ -99,9 +101,9 @@ void moe_forward_dev(scmoe_ctx* c, scmoe_bank* b, const float* x, const __nv_bfl
         float* h = ws.h.get<float>(T * K * I + 1);
         float* y = ws.y.get<float>(T * K * d + 1);
         { ProfScope _p(c, "expert_gemm1_f32"); launch_seq_gemm(c, x, d, pr.row_token, b->w_in32, I, d * I, h, I, d, I, /*silu=*/1,
-                        pr.tiles, pr.n_tiles, pr.max_tiles); }
+                        pr.tiles, pr.n_tiles, pr.max_tiles, 64); }
         { ProfScope _p(c, "expert_gemm2_f32"); launch_seq_gemm(c, h, I, nullptr, b->w_out32, d, I * d, y, d, I, d, /*silu=*/0, pr.tiles,
-                        pr.n_tiles, pr.max_tiles); }
+                        pr.n_tiles, pr.max_tiles, 64); }
         { ProfScope _p(c, "combine"); launch_combine_f32(c, x, y, idx, gates, pr.slot_pos, T, d, K, n_ffn, gf, gz, renorm,
                            residual, out); }
     } else {
@@ -122,6 +124,22 @@ void moe_forward_dev(scmoe_ctx* c, scmoe_bank* b, const float* x, const __nv_bfl
         { ProfScope _p(c, "combine"); launch_combine_bf16(c, x, y, idx, gates, pr.slot_pos, T, d, K, n_ffn, gf, gz, renorm,
                             residual, out); }
     }
+}
+
+// router.hpp:136 logits = mm(x, W_r): one group, row tiles sized for the batch.
+void route_logits(scmoe_ctx* c, scmoe_router* r, const float* x, size_t T, float* logits) {
+    const size_t E = r->E();
+    if (router_slab_ok(T, r->d, E, c->num_sms)) {
+        ProfScope _p(c, "router_gemm");
+        launch_router_slab(c, x, r->w, logits, T, r->d, E);
+        return;
+    }
+    const int tr = seq_gemm_tile_rows(T, E, c->num_sms);
+    const size_t ntile = ceil_div(T, tr);
+    TokenTile* td = c->ws.tiles_router.get<TokenTile>(ntile);
+    launch_row_tiles(c, T, tr, td);
+    ProfScope _p(c, "router_gemm");
+    launch_seq_gemm(c, x, r->d, nullptr, r->w, E, 0, logits, E, r->d, E, 0, td, nullptr, ntile, tr);
 }
 
 }  // namespace
@@ -318,10 +336,7 @@ int scmoe_route_topk(scmoe_ctx* c, scmoe_router* r, const float* x, size_t T, ui
         const size_t E = r->E();
         float* logits = c->ws.logits.get<float>(T * E);
         // router.hpp:136 -- one group, row tiles of 64 tokens
-        const size_t ntile = ceil_div(T, 64);
-        TokenTile* td = c->ws.misc.get<TokenTile>(ntile);
-        launch_row_tiles(c, T, 64, td);
-        { ProfScope _p(c, "router_gemm"); launch_seq_gemm(c, x, r->d, nullptr, r->w, E, 0, logits, E, r->d, E, 0, td, nullptr, ntile); }
+        route_logits(c, r, x, T, logits);
         { ProfScope _p(c, "softmax_topk"); launch_softmax_topk(c, logits, T, E, r->top_k, r->n_ffn, r->b, idx, gates, ffn_count, probs); }
     });
 }
@@ -581,10 +596,7 @@ int scmoe_layer_forward(scmoe_ctx* c, scmoe_router* r, scmoe_bank* b, const floa
             b->precision == SCMOE_PREC_BF16 ? ws.hmoe_bf16.get<__nv_bfloat16>(T * d) : nullptr;
         { ProfScope _p(c, "rmsnorm"); launch_rmsnorm(c, a1, gain, T, d, 1e-6f, hmoe, hb); }
         float* logits = ws.logits.get<float>(T * E);
-        const size_t ntile = ceil_div(T, 64);
-        TokenTile* td = ws.misc.get<TokenTile>(ntile);
-        launch_row_tiles(c, T, 64, td);
-        { ProfScope _p(c, "router_gemm"); launch_seq_gemm(c, hmoe, d, nullptr, r->w, E, 0, logits, E, d, E, 0, td, nullptr, ntile); }
+        route_logits(c, r, hmoe, T, logits);
         { ProfScope _p(c, "softmax_topk"); launch_softmax_topk(c, logits, T, E, K, r->n_ffn, r->b, idx, gates, ffn_count, nullptr); }
         moe_forward_dev(c, b, hmoe, hb, T, idx, gates, K, r->n_zero, renorm, a3, out);
     });

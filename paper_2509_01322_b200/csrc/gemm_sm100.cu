@@ -5,20 +5,29 @@
 // Orientation ("SwapAB", SURVEY.md 7 hard part 2): the expert weights are
 // the MMA's M side and the tokens routed to the expert its N side,
 //     D[m, j] = sum_k W[e][m][k] * X[pos0 + j][k]       (M = weight rows)
-// so an expert with ~128 tokens fills one N=128 tile instead of padding a
-// 128-row token tile.  W is stored K-major ([e][M][K] bf16: w_in^T for GEMM1,
-// w_out^T for GEMM2) and X/H are token-major rows ([rows][K] bf16), so both
-// operands are K-major 128-byte-swizzled TMA tiles.
+// W is stored K-major ([e][M][K] bf16: w_in^T for GEMM1, w_out^T for GEMM2)
+// and X/H are token-major rows ([rows][K] bf16), so both operands are
+// K-major 128-byte-swizzled TMA tiles.
 //
-// Work unit = (token tile of one expert, block of 256 weight rows).  Each
-// CTA (one per SM, persistent) runs three roles:
-//   warp 0      TMA producer: A (2 x 128-row weight slabs) + B (128 token
-//               rows) per 64-wide K block into a 4-stage smem ring;
+// A token tile holds up to 256 tokens of one expert, so at the LongCat
+// prefill shape (98..163 tokens per expert) every expert's weights are
+// streamed from HBM exactly once per GEMM.  The MMA's N is chosen per tile at
+// run time (tokens rounded up to 16), so short tiles (decode: ~4 tokens per
+// expert) issue N=16 MMAs and load only the token rows they use.
+//
+// Work unit = (token tile, block of 256 weight rows).  Each CTA (one per SM,
+// persistent, static round-robin over units) runs three roles:
+//   warp 0      TMA producer: per 64-wide K block, two 128-row weight slabs
+//               and one or two 128-row token boxes into a 3-stage smem ring;
 //   warp 1      MMA issuer: one elected lane issues tcgen05.mma
-//               (M=128, N=128, K=16) into two TMEM accumulators of 128
-//               columns, double-buffered across units (4 x 128 = 512 cols);
-//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers, optional SiLU,
-//               bf16 store of out[pos0 + j][m] (token-major rows again).
+//               (M=128, N=16..256, K=16) into two TMEM accumulators (one per
+//               weight slab, 256 columns each);
+//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers, optional SiLU, bf16
+//               store of out[pos0 + j][m] (token-major rows again).
+// The accumulators fill all 512 TMEM columns, so the epilogue of unit i and
+// the MMAs of unit i+1 do not overlap; the TMA producer keeps streaming the
+// next unit's weights into free stages meanwhile, which is what matters for
+// this HBM-bound kernel (the epilogue is ~2% of a unit).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -31,17 +40,16 @@ namespace {
 constexpr int BK = 64;          // K elements per stage (128 B rows, SWIZZLE_128B)
 constexpr int SLABS = 2;        // 128-row weight slabs per unit (BM = 256)
 constexpr int BM = 128 * SLABS;
-constexpr int NT = 128;         // token columns per tile
-constexpr int STAGES = 4;
-constexpr int ACC_BUFS = 2;
+constexpr int NT = 256;         // max token columns per tile
+constexpr int STAGES = 3;
 constexpr int A_SLAB_BYTES = 128 * BK * 2;        // 16 KB
-constexpr int B_BYTES = NT * BK * 2;              // 16 KB
-constexpr int STAGE_BYTES = SLABS * A_SLAB_BYTES + B_BYTES;
+constexpr int B_HALF_BYTES = 128 * BK * 2;        // 16 KB per 128 token rows
+constexpr int STAGE_BYTES = SLABS * A_SLAB_BYTES + 2 * B_HALF_BYTES;  // 64 KB
 constexpr int TMEM_COLS = 512;
 constexpr int NUM_THREADS = 192;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 
-static_assert(ACC_BUFS * SLABS * NT <= TMEM_COLS, "TMEM overflow");
+static_assert(SLABS * NT <= TMEM_COLS, "TMEM overflow");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -68,13 +76,27 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// 2-D TMA load with an L2 cache-policy hint (weights are streamed once:
+// evict-first; activations are re-read by the other weight blocks of the
+// same tile: evict-last).
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst,
-                                            int c0, int c1) {
+                                            int c0, int c1, uint64_t policy) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
         : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
 }
 
 // K-major, 128B-swizzled UMMA shared-memory descriptor (cute::UMMA::SmemDescriptor):
@@ -108,12 +130,15 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
         : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
     asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+        "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
           "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-          "=r"(v[14]), "=r"(v[15])
+          "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+          "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+          "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -137,8 +162,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
-    uint64_t* tempty = tfull + ACC_BUFS;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + ACC_BUFS);
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -151,10 +176,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        for (int a = 0; a < ACC_BUFS; ++a) {
-            mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4);
-        }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, 4);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_w)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_x)) : "memory");
@@ -173,22 +196,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (warp == 0) {
         // ===== TMA producer =====
         if (lane == 0) {
+            const uint64_t pol_w = policy_evict_first();
+            const uint64_t pol_x = policy_evict_last();
             int stage = 0;
             uint32_t phase = 0;
             for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
                 const TokenTile tile = args.tiles[u / mblocks];
                 const int mb = u % mblocks;
                 const int wrow = tile.e * args.M + mb * BM;
+                const bool two = tile.count > 128;
+                const uint32_t bytes = SLABS * A_SLAB_BYTES + (two ? 2 : 1) * B_HALF_BYTES;
                 for (int kb = 0; kb < kblocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     unsigned char* sbase = smem + stage * STAGE_BYTES;
-                    mbar_expect_tx(&full[stage], STAGE_BYTES);
+                    mbar_expect_tx(&full[stage], bytes);
 #pragma unroll
                     for (int s = 0; s < SLABS; ++s)
                         tma_load_2d(&map_w, &full[stage], sbase + s * A_SLAB_BYTES, kb * BK,
-                                    wrow + s * 128);
-                    tma_load_2d(&map_x, &full[stage], sbase + SLABS * A_SLAB_BYTES, kb * BK,
-                                tile.pos);
+                                    wrow + s * 128, pol_w);
+                    unsigned char* bbase = sbase + SLABS * A_SLAB_BYTES;
+                    tma_load_2d(&map_x, &full[stage], bbase, kb * BK, tile.pos, pol_x);
+                    if (two)
+                        tma_load_2d(&map_x, &full[stage], bbase + B_HALF_BYTES, kb * BK,
+                                    tile.pos + 128, pol_x);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -198,16 +228,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
     } else if (warp == 1) {
         // ===== MMA issuer =====
-        constexpr uint32_t idesc = make_idesc(128, NT);
         int stage = 0;
         uint32_t phase = 0;
         int local = 0;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++local) {
-            const int acc = local & 1;
-            const uint32_t acc_phase = (local >> 1) & 1;
-            mbar_wait(&tempty[acc], acc_phase ^ 1);
+            const TokenTile tile = args.tiles[u / mblocks];
+            const int n_eff = max(16, (tile.count + 15) & ~15);
+            const uint32_t idesc = make_idesc(128, n_eff);
+            mbar_wait(tempty, (local & 1) ^ 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t d_base = tmem_base + acc * (SLABS * NT);
             for (int kb = 0; kb < kblocks; ++kb) {
                 mbar_wait(&full[stage], phase);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -220,7 +249,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                         for (int s = 0; s < SLABS; ++s) {
                             const uint64_t adesc = make_desc_sw128(sbase + s * A_SLAB_BYTES + k * 32);
-                            mma_bf16(d_base + s * NT, adesc, bdesc, idesc, (kb | k) != 0);
+                            mma_bf16(tmem_base + s * NT, adesc, bdesc, idesc, (kb | k) != 0);
                         }
                     }
                     mma_commit(&empty[stage]);
@@ -231,7 +260,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     phase ^= 1;
                 }
             }
-            if (lane == 0) mma_commit(&tfull[acc]);
+            if (lane == 0) mma_commit(tfull);
             __syncwarp();
         }
     } else {
@@ -241,33 +270,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++local) {
             const TokenTile tile = args.tiles[u / mblocks];
             const int mb = u % mblocks;
-            const int acc = local & 1;
-            const uint32_t acc_phase = (local >> 1) & 1;
-            mbar_wait(&tfull[acc], acc_phase);
+            mbar_wait(tfull, local & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
             for (int s = 0; s < SLABS; ++s) {
                 const int m = mb * BM + s * 128 + quad * 32 + lane;
-                const uint32_t taddr =
-                    tmem_base + ((uint32_t)(quad * 32) << 16) + acc * (SLABS * NT) + s * NT;
-                for (int j0 = 0; j0 < NT; j0 += 16) {
-                    if (j0 >= tile.count) break;
-                    uint32_t v[16];
-                    tmem_ld16(taddr + j0, v);
+                const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + s * NT;
+                __nv_bfloat16* optr = args.out + (size_t)tile.pos * args.M + m;
+                for (int j0 = 0; j0 < tile.count; j0 += 32) {
+                    uint32_t v[32];
+                    tmem_ld32(taddr + j0, v);
+                    const int jn = min(32, tile.count - j0);
 #pragma unroll
-                    for (int jj = 0; jj < 16; ++jj) {
-                        const int j = j0 + jj;
-                        if (j < tile.count) {
+                    for (int jj = 0; jj < 32; ++jj) {
+                        if (jj < jn) {
                             float f = __uint_as_float(v[jj]);
                             if (args.silu) f = silu_fast(f);
-                            args.out[(size_t)(tile.pos + j) * args.M + m] = __float2bfloat16_rn(f);
+                            optr[(size_t)(j0 + jj) * args.M] = __float2bfloat16_rn(f);
                         }
                     }
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) mbar_arrive(tempty);
         }
     }
 
@@ -310,6 +336,8 @@ CUtensorMap make_map_2d(const void* base, uint64_t rows, uint64_t cols, uint32_t
 
 }  // namespace
 
+int grouped_gemm_tile_rows() { return NT; }
+
 void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_experts, size_t M,
                               size_t K, const __nv_bfloat16* X, size_t x_rows,
                               __nv_bfloat16* out, int silu, const TokenTile* tiles,
@@ -319,7 +347,7 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
     SCMOE_CHECK_ARG(M % BM == 0 && K % BK == 0, SCMOE_ERR_DIMENSION,
                     "gemm: M must be a multiple of 256 and K of 64");
     const CUtensorMap mw = make_map_2d(W, n_experts * M, K, 128, BK);
-    const CUtensorMap mx = make_map_2d(X, std::max<size_t>(x_rows, 1), K, NT, BK);
+    const CUtensorMap mx = make_map_2d(X, std::max<size_t>(x_rows, 1), K, 128, BK);
     static bool attr_set = false;
     if (!attr_set) {
         SCMOE_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel,

@@ -64,11 +64,12 @@ struct DevBuf {
 struct Workspace {
     DevBuf logits, probs, hmoe, hmoe_bf16, idx, gates, ffn_count;
     DevBuf rank_in_block, block_counts, expert_count, expert_base, slot_pos, row_token;
-    DevBuf tiles, n_tiles, xp, h, y, in_copy, out_copy, misc;
+    DevBuf tiles, n_tiles, xp, h, y, in_copy, out_copy, misc, tiles_router;
     void release_all() {
         DevBuf* all[] = {&logits, &probs, &hmoe, &hmoe_bf16, &idx, &gates, &ffn_count,
                          &rank_in_block, &block_counts, &expert_count, &expert_base, &slot_pos,
-                         &row_token, &tiles, &n_tiles, &xp, &h, &y, &in_copy, &out_copy, &misc};
+                         &row_token, &tiles, &n_tiles, &xp, &h, &y, &in_copy, &out_copy, &misc,
+                         &tiles_router};
         for (DevBuf* b : all) b->release();
     }
 };
@@ -165,7 +166,12 @@ void launch_rmsnorm(scmoe_ctx* c, const float* x, const float* gain, size_t rows
 void launch_seq_gemm(scmoe_ctx* c, const float* A, size_t lda, const int* a_rows,
                      const float* B, size_t ldb, size_t b_group_stride, float* C, size_t ldc,
                      size_t K, size_t N, int silu, const TokenTile* tiles, const int* n_tiles_dev,
-                     size_t max_tiles);
+                     size_t max_tiles, int tile_rows);
+int seq_gemm_tile_rows(size_t rows, size_t N, int num_sms);
+// Router projection with one CTA per 56-token slab x all experts (E <= 768).
+bool router_slab_ok(size_t T, size_t K, size_t E, int num_sms);
+void launch_router_slab(scmoe_ctx* c, const float* X, const float* W, float* logits, size_t T,
+                        size_t K, size_t E);
 void launch_softmax_topk(scmoe_ctx* c, const float* logits, size_t T, size_t E, size_t K,
                          size_t n_ffn, const double* bias, uint32_t* idx, double* gates,
                          uint32_t* ffn_count, float* probs_out);
@@ -215,6 +221,7 @@ void launch_f32_to_bf16_t(scmoe_ctx* c, const float* src, size_t rows, size_t co
 // tcgen05 grouped GEMM (gemm_sm100.cu).  D^T = W x X^T per expert tile:
 //   out[pos, m] = epi( sum_k W[e][m][k] * X[pos][k] ),  epi = silu or identity,
 // W: [n][M][K] bf16 (K-major), X: [rows][K] bf16, out: [rows][M] bf16.
+int grouped_gemm_tile_rows();
 void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_experts,
                               size_t M, size_t K, const __nv_bfloat16* X, size_t x_rows,
                               __nv_bfloat16* out, int silu, const TokenTile* tiles,

@@ -315,10 +315,96 @@ void launch_combine_f32(scmoe_ctx* c, const float* x, const float* y, const uint
     launch_combine_impl<float>(c, x, y, idx, gates, slot_pos, T, d, K, n_ffn, gamma_ffn,
                                gamma_zero, renorm, residual, out);
 }
+// bf16 expert rows, 8 columns per thread per step (16-byte Y loads, 2x float4
+// for x / residual / out).  Same per-element operation order as above.
+__global__ void __launch_bounds__(256) combine_bf16_vec8_kernel(
+    const float* __restrict__ x, const __nv_bfloat16* __restrict__ y,
+    const uint32_t* __restrict__ idx, const double* __restrict__ gates,
+    const int* __restrict__ slot_pos, int d, int K, int n_ffn, float gamma_ffn, float gamma_zero,
+    int renorm, const float* __restrict__ residual, float* __restrict__ out) {
+    __shared__ float coeff[kMaxK];
+    __shared__ int rowpos[kMaxK];
+    __shared__ int nffn, use_zero;
+    __shared__ float zcoeff;
+    const int t = blockIdx.x;
+    if (threadIdx.x == 0) {
+        float denom = 1.0f;
+        if (renorm) {
+            float s = 0.0f;
+            for (int sl = 0; sl < K; ++sl) s = __fadd_rn(s, (float)gates[(size_t)t * K + sl]);
+            denom = s;
+        }
+        float zero_w = 0.0f;
+        int n = 0;
+        for (int sl = 0; sl < K; ++sl) {
+            const uint32_t e = idx[(size_t)t * K + sl];
+            const float w = __fdiv_rn((float)gates[(size_t)t * K + sl], denom);
+            if (e < (uint32_t)n_ffn) {
+                coeff[n] = __fmul_rn(gamma_ffn, w);
+                rowpos[n] = slot_pos[(size_t)t * K + sl];
+                ++n;
+            } else {
+                zero_w = __fadd_rn(zero_w, w);
+            }
+        }
+        nffn = n;
+        use_zero = zero_w != 0.0f;
+        zcoeff = __fmul_rn(gamma_zero, zero_w);
+    }
+    __syncthreads();
+    const int n = nffn;
+    const float zc = zcoeff;
+    const bool uz = use_zero != 0;
+    const int d8 = d / 8;
+    for (int v = threadIdx.x; v < d8; v += blockDim.x) {
+        float acc[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
+        for (int s = 0; s < n; ++s) {
+            const uint4 raw = reinterpret_cast<const uint4*>(y + (size_t)rowpos[s] * d)[v];
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float2 f = __bfloat1622float2(h[q]);
+                acc[2 * q] = __fadd_rn(acc[2 * q], __fmul_rn(coeff[s], f.x));
+                acc[2 * q + 1] = __fadd_rn(acc[2 * q + 1], __fmul_rn(coeff[s], f.y));
+            }
+        }
+        if (uz) {
+            const float4* xr = reinterpret_cast<const float4*>(x + (size_t)t * d) + 2 * v;
+            const float4 a = xr[0], b = xr[1];
+            const float xv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[q] = __fadd_rn(acc[q], __fmul_rn(zc, xv[q]));
+        }
+        if (residual) {
+            const float4* rr = reinterpret_cast<const float4*>(residual + (size_t)t * d) + 2 * v;
+            const float4 a = rr[0], b = rr[1];
+            const float rv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[q] = __fadd_rn(rv[q], acc[q]);
+        }
+        float4* o = reinterpret_cast<float4*>(out + (size_t)t * d) + 2 * v;
+        o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    }
+}
+
 void launch_combine_bf16(scmoe_ctx* c, const float* x, const __nv_bfloat16* y,
                          const uint32_t* idx, const double* gates, const int* slot_pos, size_t T,
                          size_t d, size_t K, size_t n_ffn, float gamma_ffn, float gamma_zero,
                          int renorm, const float* residual, float* out) {
+    const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(out) |
+                           reinterpret_cast<uintptr_t>(residual) | reinterpret_cast<uintptr_t>(y)) &
+                          15) == 0;
+    if (d % 8 == 0 && aligned && T > 0) {
+        SCMOE_CHECK_ARG(K <= kMaxK, SCMOE_ERR_CONFIG, "combine: top_k too large");
+        combine_bf16_vec8_kernel<<<T, 256, 0, c->stream>>>(x, y, idx, gates, slot_pos, (int)d,
+                                                           (int)K, (int)n_ffn, gamma_ffn,
+                                                           gamma_zero, renorm, residual, out);
+        SCMOE_LAUNCH_CHECK(c);
+        return;
+    }
     launch_combine_impl<__nv_bfloat16>(c, x, y, idx, gates, slot_pos, T, d, K, n_ffn, gamma_ffn,
                                        gamma_zero, renorm, residual, out);
 }

@@ -14,9 +14,11 @@
 namespace scmoe {
 
 // ---------------------------------------------------------------------------
-// rmsnorm forward -- graph.hpp:322-335.  One warp per row; the sum of squares
-// is a strictly sequential chain in j (lane 0), the products are computed by
-// all lanes.  out = (x * inv) * gain, left to right.
+// rmsnorm forward -- graph.hpp:322-335.  One warp per row.  All lanes load the
+// row chunk (16-byte vectors, all loads in flight at once) and square it into
+// shared memory; lane 0 then runs the reference's strictly sequential sum of
+// squares in j order (float4 shared reads issued ahead of the add chain).
+// out = (x * inv) * gain, left to right; optional bf16 copy for the GEMMs.
 // ---------------------------------------------------------------------------
 constexpr int kNormChunk = 1024;
 
@@ -24,33 +26,85 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
                                                       const float* __restrict__ gain, int rows,
                                                       int d, float eps, float* __restrict__ out,
                                                       __nv_bfloat16* __restrict__ out_bf16) {
-    __shared__ float sq[8][kNormChunk];
+    __shared__ __align__(16) float sq[8][kNormChunk];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int row = blockIdx.x * 8 + warp;
     if (row >= rows) return;
     const float* xr = x + (size_t)row * d;
+    const bool vec = (d % 4 == 0) && ((reinterpret_cast<uintptr_t>(xr) & 15) == 0);
     float s2 = 0.0f;
     for (int j0 = 0; j0 < d; j0 += kNormChunk) {
         const int n = min(kNormChunk, d - j0);
-        for (int j = lane; j < n; j += 32) {
-            const float v = xr[j0 + j];
-            sq[warp][j] = __fmul_rn(v, v);
+        if (vec && n == kNormChunk) {
+            const float4* src = reinterpret_cast<const float4*>(xr + j0);
+            float4 v[kNormChunk / 128];
+#pragma unroll
+            for (int i = 0; i < kNormChunk / 128; ++i) v[i] = src[lane + 32 * i];
+#pragma unroll
+            for (int i = 0; i < kNormChunk / 128; ++i) {
+                float4 q;
+                q.x = __fmul_rn(v[i].x, v[i].x);
+                q.y = __fmul_rn(v[i].y, v[i].y);
+                q.z = __fmul_rn(v[i].z, v[i].z);
+                q.w = __fmul_rn(v[i].w, v[i].w);
+                reinterpret_cast<float4*>(sq[warp])[lane + 32 * i] = q;
+            }
+        } else {
+            for (int j = lane; j < n; j += 32) {
+                const float v = xr[j0 + j];
+                sq[warp][j] = __fmul_rn(v, v);
+            }
         }
         __syncwarp();
         if (lane == 0) {
-#pragma unroll 8
-            for (int j = 0; j < n; ++j) s2 = __fadd_rn(s2, sq[warp][j]);
+            int j = 0;
+            const float4* q4 = reinterpret_cast<const float4*>(sq[warp]);
+            for (; j + 16 <= n; j += 16) {
+                const float4 a = q4[j / 4], b = q4[j / 4 + 1], c = q4[j / 4 + 2], e = q4[j / 4 + 3];
+                s2 = __fadd_rn(s2, a.x); s2 = __fadd_rn(s2, a.y);
+                s2 = __fadd_rn(s2, a.z); s2 = __fadd_rn(s2, a.w);
+                s2 = __fadd_rn(s2, b.x); s2 = __fadd_rn(s2, b.y);
+                s2 = __fadd_rn(s2, b.z); s2 = __fadd_rn(s2, b.w);
+                s2 = __fadd_rn(s2, c.x); s2 = __fadd_rn(s2, c.y);
+                s2 = __fadd_rn(s2, c.z); s2 = __fadd_rn(s2, c.w);
+                s2 = __fadd_rn(s2, e.x); s2 = __fadd_rn(s2, e.y);
+                s2 = __fadd_rn(s2, e.z); s2 = __fadd_rn(s2, e.w);
+            }
+            for (; j < n; ++j) s2 = __fadd_rn(s2, sq[warp][j]);
         }
         __syncwarp();
     }
     s2 = __shfl_sync(0xffffffffu, s2, 0);
     const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(s2, (float)d), eps)));
     float* orow = out + (size_t)row * d;
-    for (int j = lane; j < d; j += 32) {
-        const float g = gain ? gain[j] : 1.0f;
-        const float v = __fmul_rn(__fmul_rn(xr[j], inv), g);
-        orow[j] = v;
-        if (out_bf16) out_bf16[(size_t)row * d + j] = __float2bfloat16_rn(v);
+    if (vec) {
+        const float4* src = reinterpret_cast<const float4*>(xr);
+        float4* dst = reinterpret_cast<float4*>(orow);
+        for (int j4 = lane; j4 < d / 4; j4 += 32) {
+            const float4 v = src[j4];
+            float4 g = gain ? reinterpret_cast<const float4*>(gain)[j4] : make_float4(1.f, 1.f, 1.f, 1.f);
+            float4 o;
+            o.x = __fmul_rn(__fmul_rn(v.x, inv), g.x);
+            o.y = __fmul_rn(__fmul_rn(v.y, inv), g.y);
+            o.z = __fmul_rn(__fmul_rn(v.z, inv), g.z);
+            o.w = __fmul_rn(__fmul_rn(v.w, inv), g.w);
+            dst[j4] = o;
+            if (out_bf16) {
+                __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y);
+                __nv_bfloat162 hi = __floats2bfloat162_rn(o.z, o.w);
+                uint2 pk;
+                pk.x = *reinterpret_cast<uint32_t*>(&lo);
+                pk.y = *reinterpret_cast<uint32_t*>(&hi);
+                reinterpret_cast<uint2*>(out_bf16 + (size_t)row * d)[j4] = pk;
+            }
+        }
+    } else {
+        for (int j = lane; j < d; j += 32) {
+            const float g = gain ? gain[j] : 1.0f;
+            const float v = __fmul_rn(__fmul_rn(xr[j], inv), g);
+            orow[j] = v;
+            if (out_bf16) out_bf16[(size_t)row * d + j] = __float2bfloat16_rn(v);
+        }
     }
 }
 
@@ -65,158 +119,362 @@ void launch_rmsnorm(scmoe_ctx* c, const float* x, const float* gain, size_t rows
 // ---------------------------------------------------------------------------
 // Sequential-k GEMM -- tensor.hpp:95-112 (mm_into).  Each output element is
 // c = 0; for p ascending: c = c + a[p]*b[p] with both operations rounded.
-// Tiles of 64 rows x 64 columns, 256 threads, 4x4 outputs per thread, K
-// staged through shared memory in chunks of 32.  Rows can be indirected
+// A CTA owns TM rows x TN columns; each thread RM x RN outputs (independent
+// chains, so the 4-cycle FADD latency is covered by ILP).  K is staged
+// through shared memory in chunks of KC with a register-staged double
+// buffer: the next chunk's global loads are issued before the current
+// chunk's arithmetic and stored to shared memory after it, so load latency
+// hides behind ~RM*RN*2*KC instructions per thread.  Rows can be indirected
 // (a_rows) and grouped (tiles: expert, first row, row count), which serves
 // both the router projection (one group) and the fp32 expert FFN.
 // ---------------------------------------------------------------------------
-constexpr int kSeqTM = 64, kSeqTN = 64, kSeqKC = 32, kSeqPad = 4;
+constexpr int kSeqKC = 32, kSeqPad = 4;
 
-template <bool kSilu>
-__global__ void __launch_bounds__(256) seq_gemm_kernel(
+template <int TM, int TN, int RM, int RN, bool kSilu>
+__global__ void __launch_bounds__((TM / RM) * (TN / RN)) seq_gemm_kernel(
     const float* __restrict__ A, size_t lda, const int* __restrict__ a_rows,
     const float* __restrict__ B, size_t ldb, size_t b_group_stride, float* __restrict__ C,
     size_t ldc, int K, int N, const TokenTile* __restrict__ tiles, const int* __restrict__ n_tiles_dev,
     int n_tiles_host) {
-    __shared__ __align__(16) float As[2][kSeqKC][kSeqTM + kSeqPad];
-    __shared__ __align__(16) float Bs[2][kSeqKC][kSeqTN + kSeqPad];
+    constexpr int NT = (TM / RM) * (TN / RN);
+    constexpr int TX = TN / RN;             // threads along N
+    constexpr int A4 = TM * kSeqKC / 4;     // float4 per A chunk
+    constexpr int B4 = kSeqKC * TN / 4;     // float4 per B chunk
+    constexpr int AL = (A4 + NT - 1) / NT;  // per-thread loads
+    constexpr int BL = (B4 + NT - 1) / NT;
+    static_assert(RM == 2 || RM == 4, "RM");
+    static_assert(RN == 4, "RN");
+    __shared__ __align__(16) float As[2][kSeqKC][TM + kSeqPad];
+    __shared__ __align__(16) float Bs[2][kSeqKC][TN + kSeqPad];
 
     const int n_tiles = n_tiles_dev ? *n_tiles_dev : n_tiles_host;
-    const int col0 = blockIdx.x * kSeqTN;
+    const int col0 = blockIdx.x * TN;
     const int tid = threadIdx.x;
-    const int ty = tid >> 4, tx = tid & 15;
+    const int ty = tid / TX, tx = tid % TX;
 
     for (int tile_id = blockIdx.y; tile_id < n_tiles; tile_id += gridDim.y) {
         const TokenTile tile = tiles[tile_id];
         const float* Bg = B + (size_t)tile.e * b_group_stride;
-        // Row sources for the A loader: thread loads rows (tid>>3) and (tid>>3)+32.
-        const int lr0 = tid >> 3, lk4 = tid & 7;
-        const float* arow[2];
+        // A loader: element i -> row i / (KC/4), k4 = i % (KC/4)
+        const float* arow[AL];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int r = lr0 + 32 * h;
-            if (r < tile.count) {
+        for (int l = 0; l < AL; ++l) {
+            const int i = tid + l * NT;
+            const int r = i / (kSeqKC / 4);
+            arow[l] = nullptr;
+            if (i < A4 && r < tile.count) {
                 const int src = a_rows ? a_rows[tile.pos + r] : tile.pos + r;
-                arow[h] = A + (size_t)src * lda;
-            } else {
-                arow[h] = nullptr;
+                arow[l] = A + (size_t)src * lda;
             }
         }
-        // B loader: 32 rows x 64 cols = 512 float4, 2 per thread.
-        const int bk = tid >> 4, bc4 = tid & 15;
-
-        float acc[4][4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
-
-        auto load_stage = [&](int buf, int k0) {
+        float4 ra[AL], rb[BL];
+        auto load_regs = [&](int k0) {
             const int kc = min(kSeqKC, K - k0);
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int l = 0; l < AL; ++l) {
+                const int i = tid + l * NT;
+                const int kk = 4 * (i % (kSeqKC / 4));
                 float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                const int kk = 4 * lk4;
-                if (arow[h]) {
-                    if (kk + 3 < kc) {
-                        v = *reinterpret_cast<const float4*>(arow[h] + k0 + kk);
+                if (arow[l]) {
+                    const float* s = arow[l] + k0 + kk;
+                    if (kk + 3 < kc && ((reinterpret_cast<uintptr_t>(s) & 15) == 0)) {
+                        v = *reinterpret_cast<const float4*>(s);
                     } else {
-                        if (kk + 0 < kc) v.x = arow[h][k0 + kk + 0];
-                        if (kk + 1 < kc) v.y = arow[h][k0 + kk + 1];
-                        if (kk + 2 < kc) v.z = arow[h][k0 + kk + 2];
+                        if (kk + 0 < kc) v.x = s[0];
+                        if (kk + 1 < kc) v.y = s[1];
+                        if (kk + 2 < kc) v.z = s[2];
+                        if (kk + 3 < kc) v.w = s[3];
                     }
                 }
-                const int r = lr0 + 32 * h;
-                As[buf][kk + 0][r] = v.x;
-                As[buf][kk + 1][r] = v.y;
-                As[buf][kk + 2][r] = v.z;
-                As[buf][kk + 3][r] = v.w;
+                ra[l] = v;
             }
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int k = bk + 16 * h;
-                const int col = col0 + 4 * bc4;
+            for (int l = 0; l < BL; ++l) {
+                const int i = tid + l * NT;
+                const int k = i / (TN / 4), c4 = i % (TN / 4);
+                const int col = col0 + 4 * c4;
                 float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (k < kc) {
-                    const float* src = Bg + (size_t)(k0 + k) * ldb + col;
-                    if (col + 3 < N && (((uintptr_t)src & 15) == 0)) {
-                        v = *reinterpret_cast<const float4*>(src);
+                if (i < B4 && k < kc) {
+                    const float* s = Bg + (size_t)(k0 + k) * ldb + col;
+                    if (col + 3 < N && ((reinterpret_cast<uintptr_t>(s) & 15) == 0)) {
+                        v = *reinterpret_cast<const float4*>(s);
                     } else {
-                        if (col + 0 < N) v.x = src[0];
-                        if (col + 1 < N) v.y = src[1];
-                        if (col + 2 < N) v.z = src[2];
-                        if (col + 3 < N) v.w = src[3];
+                        if (col + 0 < N) v.x = s[0];
+                        if (col + 1 < N) v.y = s[1];
+                        if (col + 2 < N) v.z = s[2];
+                        if (col + 3 < N) v.w = s[3];
                     }
                 }
-                *reinterpret_cast<float4*>(&Bs[buf][k][4 * bc4]) = v;
+                rb[l] = v;
+            }
+        };
+        auto store_smem = [&](int buf) {
+#pragma unroll
+            for (int l = 0; l < AL; ++l) {
+                const int i = tid + l * NT;
+                if (i < A4) {
+                    const int r = i / (kSeqKC / 4), kk = 4 * (i % (kSeqKC / 4));
+                    As[buf][kk + 0][r] = ra[l].x;
+                    As[buf][kk + 1][r] = ra[l].y;
+                    As[buf][kk + 2][r] = ra[l].z;
+                    As[buf][kk + 3][r] = ra[l].w;
+                }
+            }
+#pragma unroll
+            for (int l = 0; l < BL; ++l) {
+                const int i = tid + l * NT;
+                if (i < B4) {
+                    const int k = i / (TN / 4), c4 = i % (TN / 4);
+                    *reinterpret_cast<float4*>(&Bs[buf][k][4 * c4]) = rb[l];
+                }
             }
         };
 
+        float acc[RM][RN];
+#pragma unroll
+        for (int i = 0; i < RM; ++i)
+#pragma unroll
+            for (int j = 0; j < RN; ++j) acc[i][j] = 0.0f;
+
         int buf = 0;
-        load_stage(0, 0);
+        load_regs(0);
+        store_smem(0);
         __syncthreads();
         for (int k0 = 0; k0 < K; k0 += kSeqKC) {
             const int kc = min(kSeqKC, K - k0);
-            if (k0 + kSeqKC < K) load_stage(buf ^ 1, k0 + kSeqKC);
+            const bool more = k0 + kSeqKC < K;
+            if (more) load_regs(k0 + kSeqKC);
             if (kc == kSeqKC) {
 #pragma unroll 8
                 for (int k = 0; k < kSeqKC; ++k) {
-                    const float4 a = *reinterpret_cast<const float4*>(&As[buf][k][4 * ty]);
-                    const float4 b = *reinterpret_cast<const float4*>(&Bs[buf][k][4 * tx]);
-                    const float av[4] = {a.x, a.y, a.z, a.w};
+                    float av[RM];
+                    if constexpr (RM == 4) {
+                        const float4 a = *reinterpret_cast<const float4*>(&As[buf][k][RM * ty]);
+                        av[0] = a.x; av[1] = a.y; av[2] = a.z; av[3] = a.w;
+                    } else {
+                        const float2 a = *reinterpret_cast<const float2*>(&As[buf][k][RM * ty]);
+                        av[0] = a.x; av[1] = a.y;
+                    }
+                    const float4 b = *reinterpret_cast<const float4*>(&Bs[buf][k][RN * tx]);
                     const float bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-                    for (int i = 0; i < 4; ++i)
+                    for (int i = 0; i < RM; ++i)
 #pragma unroll
-                        for (int j = 0; j < 4; ++j)
+                        for (int j = 0; j < RN; ++j)
                             acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(av[i], bv[j]));
                 }
             } else {
                 for (int k = 0; k < kc; ++k) {
-                    const float4 a = *reinterpret_cast<const float4*>(&As[buf][k][4 * ty]);
-                    const float4 b = *reinterpret_cast<const float4*>(&Bs[buf][k][4 * tx]);
-                    const float av[4] = {a.x, a.y, a.z, a.w};
-                    const float bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-                    for (int i = 0; i < 4; ++i)
+                    for (int i = 0; i < RM; ++i)
 #pragma unroll
-                        for (int j = 0; j < 4; ++j)
-                            acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(av[i], bv[j]));
+                        for (int j = 0; j < RN; ++j)
+                            acc[i][j] = __fadd_rn(acc[i][j],
+                                                  __fmul_rn(As[buf][k][RM * ty + i], Bs[buf][k][RN * tx + j]));
                 }
             }
+            if (more) store_smem(buf ^ 1);
             __syncthreads();
             buf ^= 1;
         }
         // Epilogue.
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int r = 4 * ty + i;
+        for (int i = 0; i < RM; ++i) {
+            const int r = RM * ty + i;
             if (r >= tile.count) continue;
             float* crow = C + (size_t)(tile.pos + r) * ldc;
+            const int col = col0 + RN * tx;
+            if (!kSilu && col + 3 < N && ((reinterpret_cast<uintptr_t>(crow + col) & 15) == 0)) {
+                *reinterpret_cast<float4*>(crow + col) =
+                    make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+            } else {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int col = col0 + 4 * tx + j;
-                if (col < N) crow[col] = kSilu ? scmoe_siluf(acc[i][j]) : acc[i][j];
+                for (int j = 0; j < RN; ++j)
+                    if (col + j < N) crow[col + j] = kSilu ? scmoe_siluf(acc[i][j]) : acc[i][j];
             }
         }
         __syncthreads();
     }
 }
 
+// ---------------------------------------------------------------------------
+// Router projection, large batches: one CTA per 56-token slab covering all
+// E <= 768 expert columns (8 token groups x 96 expert groups = 768 threads,
+// 7 x 8 independent sequential chains per thread).  With T=8192 this is 147
+// CTAs -- a single wave on 148 SMs -- instead of 3.5 waves of 64x64 tiles.
+// Same arithmetic as seq_gemm_kernel: per output c = 0; c = c + x*w in k order.
+// ---------------------------------------------------------------------------
+constexpr int kSlabTok = 7, kSlabExp = 8, kSlabTG = 8, kSlabEG = 96;
+constexpr int kSlabRows = kSlabTok * kSlabTG;          // 56
+constexpr int kSlabThreads = kSlabTG * kSlabEG;        // 768
+constexpr int kSlabKC = 16;
+constexpr int kSlabXStride = kSlabTG * 8;              // 64: group g at columns [8g, 8g+7)
+
+__global__ void __launch_bounds__(kSlabThreads, 1) router_slab_kernel(
+    const float* __restrict__ X, const float* __restrict__ W, float* __restrict__ logits, int T,
+    int K, int E) {
+    extern __shared__ __align__(16) float slab_smem[];
+    auto xs = reinterpret_cast<float(*)[kSlabKC][kSlabXStride]>(slab_smem);
+    auto ws = reinterpret_cast<float(*)[kSlabKC][kSlabEG * kSlabExp]>(
+        slab_smem + 2 * kSlabKC * kSlabXStride);
+    const int tid = threadIdx.x;
+    const int tg = tid / kSlabEG, eg = tid % kSlabEG;
+    const int row0 = blockIdx.x * kSlabRows;
+    const int nrows = min(kSlabRows, T - row0);
+    if (nrows <= 0) return;
+    const int Ew = kSlabEG * kSlabExp;  // padded width 768
+    // Both chunks go global -> shared with cp.async (nothing held in
+    // registers across the arithmetic): W (KC x 768 floats, 4 x 16 B per
+    // thread) straight into ws, X (56 rows x 16 k) raw into xraw, transposed
+    // into xs after the chunk's arithmetic.
+    auto xraw = reinterpret_cast<float(*)[kSlabRows][kSlabKC]>(
+        slab_smem + 2 * kSlabKC * (kSlabXStride + kSlabEG * kSlabExp));
+    auto load = [&](int k0, int buf) {
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            const int i = tid + l * kSlabThreads;
+            const int k = i / (Ew / 4), c4 = i % (Ew / 4);
+            const int col = 4 * c4;
+            const bool ok = (k0 + k < K) && (col + 3 < E);
+            const float* s = ok ? W + (size_t)(k0 + k) * E + col : W;
+            const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&ws[buf][k][col]));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(s),
+                         "r"(ok ? 16 : 0)
+                         : "memory");
+        }
+        if (tid < kSlabRows * kSlabKC / 4) {
+            const int r = tid / (kSlabKC / 4), k4 = tid % (kSlabKC / 4);
+            const bool ok = r < nrows;
+            const float* s = ok ? X + (size_t)(row0 + r) * K + k0 + 4 * k4 : X;
+            const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&xraw[buf][r][4 * k4]));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(s),
+                         "r"(ok ? 16 : 0)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    // Waits for this thread's copies, publishes them block-wide, transposes X.
+    auto store = [&](int buf) {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+        if (tid < kSlabRows * kSlabKC / 4) {
+            const int r = tid / (kSlabKC / 4), k4 = tid % (kSlabKC / 4);
+            const int col = 8 * (r / kSlabTok) + r % kSlabTok;
+            const float4 v = *reinterpret_cast<const float4*>(&xraw[buf][r][4 * k4]);
+            xs[buf][4 * k4 + 0][col] = v.x;
+            xs[buf][4 * k4 + 1][col] = v.y;
+            xs[buf][4 * k4 + 2][col] = v.z;
+            xs[buf][4 * k4 + 3][col] = v.w;
+        }
+    };
+    float acc[kSlabTok][kSlabExp];
+#pragma unroll
+    for (int i = 0; i < kSlabTok; ++i)
+#pragma unroll
+        for (int j = 0; j < kSlabExp; ++j) acc[i][j] = 0.0f;
+
+    int buf = 0;
+    load(0, 0);
+    store(0);
+    __syncthreads();
+    for (int k0 = 0; k0 < K; k0 += kSlabKC) {
+        const bool more = k0 + kSlabKC < K;
+        if (more) load(k0 + kSlabKC, buf ^ 1);
+#pragma unroll 4
+        for (int k = 0; k < kSlabKC; ++k) {
+            const float4 a03 = *reinterpret_cast<const float4*>(&xs[buf][k][8 * tg]);
+            const float2 a45 = *reinterpret_cast<const float2*>(&xs[buf][k][8 * tg + 4]);
+            const float a6 = xs[buf][k][8 * tg + 6];
+            const float4 b03 = *reinterpret_cast<const float4*>(&ws[buf][k][8 * eg]);
+            const float4 b47 = *reinterpret_cast<const float4*>(&ws[buf][k][8 * eg + 4]);
+            const float av[7] = {a03.x, a03.y, a03.z, a03.w, a45.x, a45.y, a6};
+            const float bv[8] = {b03.x, b03.y, b03.z, b03.w, b47.x, b47.y, b47.z, b47.w};
+#pragma unroll
+            for (int i = 0; i < kSlabTok; ++i)
+#pragma unroll
+                for (int j = 0; j < kSlabExp; ++j)
+                    acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(av[i], bv[j]));
+        }
+        if (more) store(buf ^ 1);
+        __syncthreads();
+        buf ^= 1;
+    }
+#pragma unroll
+    for (int i = 0; i < kSlabTok; ++i) {
+        const int r = kSlabTok * tg + i;
+        if (r >= nrows) continue;
+        float* dst = logits + (size_t)(row0 + r) * E + 8 * eg;
+        if (8 * eg + 7 < E) {
+            reinterpret_cast<float4*>(dst)[0] = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+            reinterpret_cast<float4*>(dst)[1] = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < kSlabExp; ++j)
+                if (8 * eg + j < E) dst[j] = acc[i][j];
+        }
+    }
+}
+
+bool router_slab_ok(size_t T, size_t K, size_t E, int num_sms) {
+    // full-width slab needs E <= 768, E and K multiples of 4 (float4 rows), and
+    // enough tokens to fill most SMs (otherwise the 16/64-row tiles spread better)
+    return E <= (size_t)kSlabEG * kSlabExp && E % 4 == 0 && K % kSlabKC == 0 &&
+           ceil_div(T, kSlabRows) >= (size_t)num_sms * 3 / 4;
+}
+
+void launch_router_slab(scmoe_ctx* c, const float* X, const float* W, float* logits, size_t T,
+                        size_t K, size_t E) {
+    constexpr size_t smem =
+        sizeof(float) * 2 * (kSlabKC * (kSlabXStride + kSlabEG * kSlabExp) + kSlabRows * kSlabKC);
+    static bool attr = false;
+    if (!attr) {
+        SCMOE_CUDA(cudaFuncSetAttribute(router_slab_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    router_slab_kernel<<<ceil_div(T, kSlabRows), kSlabThreads, smem, c->stream>>>(
+        X, W, logits, (int)T, (int)K, (int)E);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
+template <int TM, int TN, int RM, int RN>
+static void seq_gemm_dispatch(scmoe_ctx* c, const float* A, size_t lda, const int* a_rows,
+                              const float* B, size_t ldb, size_t b_group_stride, float* C,
+                              size_t ldc, size_t K, size_t N, int silu, const TokenTile* tiles,
+                              const int* n_tiles_dev, size_t max_tiles) {
+    constexpr int NT = (TM / RM) * (TN / RN);
+    dim3 grid((unsigned)ceil_div(N, TN), (unsigned)std::min<size_t>(max_tiles, 65535));
+    if (silu)
+        seq_gemm_kernel<TM, TN, RM, RN, true><<<grid, NT, 0, c->stream>>>(
+            A, lda, a_rows, B, ldb, b_group_stride, C, ldc, (int)K, (int)N, tiles, n_tiles_dev,
+            (int)max_tiles);
+    else
+        seq_gemm_kernel<TM, TN, RM, RN, false><<<grid, NT, 0, c->stream>>>(
+            A, lda, a_rows, B, ldb, b_group_stride, C, ldc, (int)K, (int)N, tiles, n_tiles_dev,
+            (int)max_tiles);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
+int seq_gemm_tile_rows(size_t rows, size_t N, int num_sms) {
+    // Large config (64 x 64 tiles, 4x4 per thread) when it gives >= 4 CTAs per
+    // SM; otherwise 16-row tiles (2x4 per thread) so small batches (decode)
+    // still spread over every SM.
+    return ceil_div(rows, 64) * ceil_div(N, 64) >= (size_t)num_sms * 4 ? 64 : 16;
+}
+
 void launch_seq_gemm(scmoe_ctx* c, const float* A, size_t lda, const int* a_rows, const float* B,
                      size_t ldb, size_t b_group_stride, float* C, size_t ldc, size_t K, size_t N,
-                     int silu, const TokenTile* tiles, const int* n_tiles_dev, size_t max_tiles) {
+                     int silu, const TokenTile* tiles, const int* n_tiles_dev, size_t max_tiles,
+                     int tile_rows) {
     if (max_tiles == 0 || N == 0) return;
-    dim3 grid((unsigned)ceil_div(N, kSeqTN), (unsigned)std::min<size_t>(max_tiles, 65535));
-    if (silu)
-        seq_gemm_kernel<true><<<grid, 256, 0, c->stream>>>(A, lda, a_rows, B, ldb, b_group_stride,
-                                                           C, ldc, (int)K, (int)N, tiles,
-                                                           n_tiles_dev, (int)max_tiles);
+    if (tile_rows == 64)
+        seq_gemm_dispatch<64, 64, 4, 4>(c, A, lda, a_rows, B, ldb, b_group_stride, C, ldc, K, N,
+                                        silu, tiles, n_tiles_dev, max_tiles);
+    else if (tile_rows == 16)
+        seq_gemm_dispatch<16, 64, 2, 4>(c, A, lda, a_rows, B, ldb, b_group_stride, C, ldc, K, N,
+                                        silu, tiles, n_tiles_dev, max_tiles);
     else
-        seq_gemm_kernel<false><<<grid, 256, 0, c->stream>>>(A, lda, a_rows, B, ldb, b_group_stride,
-                                                            C, ldc, (int)K, (int)N, tiles,
-                                                            n_tiles_dev, (int)max_tiles);
-    SCMOE_LAUNCH_CHECK(c);
+        SCMOE_THROW(SCMOE_ERR_INTERNAL, "seq_gemm: unsupported tile rows");
 }
 
 // ---------------------------------------------------------------------------

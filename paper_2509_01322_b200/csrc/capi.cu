@@ -113,13 +113,22 @@ void moe_forward_dev(scmoe_ctx* c, scmoe_bank* b, const float* x, const __nv_bfl
             xb = ws.hmoe_bf16.get<__nv_bfloat16>(T * d);
             launch_cast_bf16(c, x, T * d, xb);
         }
-        __nv_bfloat16* xp = ws.xp.get<__nv_bfloat16>(T * K * d + 1);
         __nv_bfloat16* h = ws.h.get<__nv_bfloat16>(T * K * I + 1);
         __nv_bfloat16* y = ws.y.get<__nv_bfloat16>(T * K * d + 1);
-        { ProfScope _p(c, "gather"); launch_gather_bf16(c, xb, d, pr.row_token, pr.expert_base, n_ffn, T * K, xp); }
-        { ProfScope _p(c, "gemm1_tcgen05"); launch_grouped_gemm_bf16(c, b->w1t, n_ffn, I, d, xp, T * K, h, /*silu=*/1, pr.tiles,
-                                 pr.n_tiles, pr.max_tiles, tile_rows_for(b)); }
-        { ProfScope _p(c, "gemm2_tcgen05"); launch_grouped_gemm_bf16(c, b->w2t, n_ffn, d, I, h, T * K, y, /*silu=*/0, pr.tiles,
+        if (c->gemm1_gather) {
+            // GEMM1 gathers its token rows straight from x (TMA tile::gather4);
+            // x (T x d bf16) stays L2-resident, no permuted copy is written.
+            ProfScope _p(c, "gemm1_tcgen05");
+            launch_grouped_gemm_bf16(c, b->w1t, n_ffn, I, d, xb, T, pr.row_token, h, /*silu=*/1,
+                                     pr.tiles, pr.n_tiles, pr.max_tiles, tile_rows_for(b));
+        } else {
+            __nv_bfloat16* xp = ws.xp.get<__nv_bfloat16>(T * K * d + 1);
+            { ProfScope _p(c, "gather"); launch_gather_bf16(c, xb, d, pr.row_token, pr.expert_base, n_ffn, T * K, xp); }
+            ProfScope _p(c, "gemm1_tcgen05");
+            launch_grouped_gemm_bf16(c, b->w1t, n_ffn, I, d, xp, T * K, nullptr, h, /*silu=*/1,
+                                     pr.tiles, pr.n_tiles, pr.max_tiles, tile_rows_for(b));
+        }
+        { ProfScope _p(c, "gemm2_tcgen05"); launch_grouped_gemm_bf16(c, b->w2t, n_ffn, d, I, h, T * K, nullptr, y, /*silu=*/0, pr.tiles,
                                  pr.n_tiles, pr.max_tiles, tile_rows_for(b)); }
         { ProfScope _p(c, "combine"); launch_combine_bf16(c, x, y, idx, gates, pr.slot_pos, T, d, K, n_ffn, gf, gz, renorm,
                             residual, out); }
@@ -163,6 +172,7 @@ int scmoe_ctx_create(int device, scmoe_ctx** out) {
         auto* c = new scmoe_ctx();
         c->device = device;
         c->num_sms = prop.multiProcessorCount;
+        if (const char* g = getenv("SCMOE_GEMM1_GATHER")) c->gemm1_gather = atoi(g) != 0;
         SCMOE_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
         c->stream = c->own_stream;
         SCMOE_CUDA(cudaMalloc(&c->dev_status, sizeof(int)));

@@ -66,14 +66,26 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
     asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
+    return ok != 0;
+}
+// Waits for the barrier phase; a watchdog turns a never-completing phase
+// (e.g. a TMA byte-count mismatch) into a trap after ~2^33 cycles instead of
+// an indefinitely hung GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    if (mbar_try(bar, parity)) return;
+    const long long t0 = clock64();
+    while (!mbar_try(bar, parity)) {
+        if (clock64() - t0 > (1ll << 33)) __trap();
+    }
 }
 
 // 2-D TMA load with an L2 cache-policy hint (weights are streamed once:
@@ -85,6 +97,18 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
         " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
+        : "memory");
+}
+
+// Row gather (tile::gather4): 4 rows r0..r3, 64 columns from c0, into 512 B of
+// 128B-swizzled shared memory (same layout as 4 rows of a tiled box).
+__device__ __forceinline__ void tma_gather4(const CUtensorMap* map, uint64_t* bar, void* dst, int c0,
+                                            int r0, int r1, int r2, int r3, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        ".L2::cache_hint [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+        "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
 
@@ -148,6 +172,7 @@ __device__ __forceinline__ float silu_fast(float v) { return __fdividef(v, 1.0f 
 struct GemmArgs {
     const TokenTile* tiles;
     const int* n_tiles;
+    const int* x_rows;   // gather mode: permuted row -> source row of X (nullptr: X is permuted)
     __nv_bfloat16* out;  // [rows][M]
     int M, K;            // weight rows per expert, reduction length
     int silu;
@@ -194,35 +219,67 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        // ===== TMA producer =====
-        if (lane == 0) {
-            const uint64_t pol_w = policy_evict_first();
-            const uint64_t pol_x = policy_evict_last();
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-                const TokenTile tile = args.tiles[u / mblocks];
-                const int mb = u % mblocks;
-                const int wrow = tile.e * args.M + mb * BM;
-                const bool two = tile.count > 128;
-                const uint32_t bytes = SLABS * A_SLAB_BYTES + (two ? 2 : 1) * B_HALF_BYTES;
-                for (int kb = 0; kb < kblocks; ++kb) {
-                    mbar_wait(&empty[stage], phase ^ 1);
-                    unsigned char* sbase = smem + stage * STAGE_BYTES;
+        // ===== TMA producer (whole warp: lane 0 loads the weights, every lane
+        // issues row gathers in gather mode) =====
+        const uint64_t pol_w = policy_evict_first();
+        const uint64_t pol_x = policy_evict_last();
+        const bool gather = args.x_rows != nullptr;
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+            const TokenTile tile = args.tiles[u / mblocks];
+            const int mb = u % mblocks;
+            // blocked weight layout (wblk_index): each (128-row, 64-col) tile is
+            // 128 contiguous 64-element rows of the 2-D view the map describes
+            const int ebase = tile.e * (args.M / 128) * kblocks * 128;
+            const int n_eff = max(16, (tile.count + 15) & ~15);
+            // gather mode: this lane's two groups of 4 source rows (padding rows
+            // repeat the tile's last row; their columns are never stored)
+            int rows[8];
+            const int ngroups = n_eff / 4;
+            if (gather) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int j = min(4 * (lane + 32 * h) + q, tile.count - 1);
+                        rows[4 * h + q] = args.x_rows[tile.pos + j];
+                    }
+            }
+            const bool two = tile.count > 128;
+            const uint32_t bytes = SLABS * A_SLAB_BYTES +
+                                   (gather ? (uint32_t)n_eff * BK * 2 : (two ? 2u : 1u) * B_HALF_BYTES);
+            for (int kb = 0; kb < kblocks; ++kb) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                unsigned char* sbase = smem + stage * STAGE_BYTES;
+                unsigned char* bbase = sbase + SLABS * A_SLAB_BYTES;
+                if (lane == 0) {
                     mbar_expect_tx(&full[stage], bytes);
 #pragma unroll
                     for (int s = 0; s < SLABS; ++s)
-                        tma_load_2d(&map_w, &full[stage], sbase + s * A_SLAB_BYTES, kb * BK,
-                                    wrow + s * 128, pol_w);
-                    unsigned char* bbase = sbase + SLABS * A_SLAB_BYTES;
-                    tma_load_2d(&map_x, &full[stage], bbase, kb * BK, tile.pos, pol_x);
-                    if (two)
-                        tma_load_2d(&map_x, &full[stage], bbase + B_HALF_BYTES, kb * BK,
-                                    tile.pos + 128, pol_x);
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
+                        tma_load_2d(&map_w, &full[stage], sbase + s * A_SLAB_BYTES, 0,
+                                    ebase + ((mb * SLABS + s) * kblocks + kb) * 128, pol_w);
+                    if (!gather) {
+                        tma_load_2d(&map_x, &full[stage], bbase, kb * BK, tile.pos, pol_x);
+                        if (two)
+                            tma_load_2d(&map_x, &full[stage], bbase + B_HALF_BYTES, kb * BK,
+                                        tile.pos + 128, pol_x);
                     }
+                }
+                __syncwarp();  // expect_tx is posted before any gather can complete
+                if (gather) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int g = lane + 32 * h;
+                        if (g < ngroups)
+                            tma_gather4(&map_x, &full[stage], bbase + g * 4 * BK * 2, kb * BK,
+                                        rows[4 * h], rows[4 * h + 1], rows[4 * h + 2],
+                                        rows[4 * h + 3], pol_x);
+                    }
+                }
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
                 }
             }
         }
@@ -339,15 +396,18 @@ CUtensorMap make_map_2d(const void* base, uint64_t rows, uint64_t cols, uint32_t
 int grouped_gemm_tile_rows() { return NT; }
 
 void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_experts, size_t M,
-                              size_t K, const __nv_bfloat16* X, size_t x_rows,
+                              size_t K, const __nv_bfloat16* X, size_t x_rows, const int* x_row_ids,
                               __nv_bfloat16* out, int silu, const TokenTile* tiles,
                               const int* n_tiles_dev, size_t max_tiles, int tile_rows) {
     if (max_tiles == 0 || n_experts == 0) return;
     SCMOE_CHECK_ARG(tile_rows == NT, SCMOE_ERR_INTERNAL, "gemm: tile rows must equal NT");
     SCMOE_CHECK_ARG(M % BM == 0 && K % BK == 0, SCMOE_ERR_DIMENSION,
                     "gemm: M must be a multiple of 256 and K of 64");
-    const CUtensorMap mw = make_map_2d(W, n_experts * M, K, 128, BK);
-    const CUtensorMap mx = make_map_2d(X, std::max<size_t>(x_rows, 1), K, 128, BK);
+    // W in the blocked layout (internal.cuh wblk_index): a 2-D view of rows of BK elements
+    const CUtensorMap mw = make_map_2d(W, n_experts * M * K / BK, BK, 128, BK);
+    // X: tiled boxes of 128 permuted rows, or single-row boxes for tile::gather4
+    const CUtensorMap mx =
+        make_map_2d(X, std::max<size_t>(x_rows, 1), K, x_row_ids ? 1 : 128, BK);
     static bool attr_set = false;
     if (!attr_set) {
         SCMOE_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel,
@@ -357,6 +417,7 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
     GemmArgs a;
     a.tiles = tiles;
     a.n_tiles = n_tiles_dev;
+    a.x_rows = x_row_ids;
     a.out = out;
     a.M = (int)M;
     a.K = (int)K;

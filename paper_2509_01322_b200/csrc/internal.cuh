@@ -102,6 +102,7 @@ struct scmoe_ctx {
     uint64_t launches = 0;
     Workspace ws;
     Profiler prof;
+    bool gemm1_gather = true;  // GEMM1 B operand via TMA gather4 (SCMOE_GEMM1_GATHER=0: gather kernel)
 };
 
 // RAII stage timer; a no-op unless profiling is enabled on the context.
@@ -147,6 +148,15 @@ struct scmoe_bank {
     double gamma_ffn() const { return gamma_mode == SCMOE_GAMMA_OFF ? 1.0 : (double)m; }
     double gamma_zero() const { return gamma_mode == SCMOE_GAMMA_ALL ? (double)m : 1.0; }
 };
+
+// Blocked K-major layout of one expert's bf16 weight matrix W[M][K] (the
+// tcgen05 GEMM's A operand): 128-row x 64-column tiles stored contiguously,
+// tile (m/128, k/64) at ((m/128) * K/64 + k/64) * 8192 elements, row-major
+// inside (128 B rows).  Every TMA box the GEMM loads is then one contiguous
+// 16 KB read.  Requires M % 128 == 0 and K % 64 == 0.
+__host__ __device__ __forceinline__ size_t wblk_index(size_t m, size_t k, size_t K) {
+    return (((m >> 7) * (K >> 6) + (k >> 6)) << 13) + ((m & 127) << 6) + (k & 63);
+}
 
 // One GEMM work tile: rows [pos, pos+count) of expert `e` in the permuted order.
 struct TokenTile {
@@ -224,7 +234,8 @@ void launch_f32_to_bf16_t(scmoe_ctx* c, const float* src, size_t rows, size_t co
 int grouped_gemm_tile_rows();
 void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_experts,
                               size_t M, size_t K, const __nv_bfloat16* X, size_t x_rows,
-                              __nv_bfloat16* out, int silu, const TokenTile* tiles,
+                              const int* x_row_ids, __nv_bfloat16* out, int silu,
+                              const TokenTile* tiles,
                               const int* n_tiles_dev, size_t max_tiles, int tile_rows);
 
 }  // namespace scmoe

@@ -551,7 +551,7 @@ __global__ void uniform_init_bf16_t_kernel(uint64_t seed_mix, int rows, int cols
     for (int i = threadIdx.y; i < 32; i += blockDim.y) {
         const int cc = c0 + i, r = r0 + threadIdx.x;
         if (r < rows && cc < cols)
-            out_t[(size_t)cc * rows + r] = __float2bfloat16_rn(tile[threadIdx.x][i]);
+            out_t[wblk_index(cc, r, rows)] = __float2bfloat16_rn(tile[threadIdx.x][i]);
     }
 }
 
@@ -575,7 +575,7 @@ __global__ void f32_to_bf16_t_kernel(const float* __restrict__ src, int rows, in
     __syncthreads();
     for (int i = threadIdx.y; i < 32; i += blockDim.y) {
         const int cc = c0 + i, r = r0 + threadIdx.x;
-        if (r < rows && cc < cols) dst_t[(size_t)cc * rows + r] = __float2bfloat16_rn(tile[threadIdx.x][i]);
+        if (r < rows && cc < cols) dst_t[wblk_index(cc, r, rows)] = __float2bfloat16_rn(tile[threadIdx.x][i]);
     }
 }
 

@@ -265,47 +265,74 @@ def run_b200(args):
     a3_h = P.fill_normal(P.stream_seed(SEED_X + 1, rank), T * D, threads=os.cpu_count() or 8)
     a1 = torch.from_numpy(a1_h).cuda()
     a3 = torch.from_numpy(a3_h).cuda()
-    idx = torch.empty(T * TOPK, dtype=torch.int32, device="cuda")
-    gates = torch.empty(T * TOPK, dtype=torch.float64, device="cuda")
-    cnt = torch.empty(T, dtype=torch.int32, device="cuda")
-    out = torch.empty(T, D, dtype=torch.float32, device="cuda")
+    # two output sets: consecutive micro-batches of the pipelined schedule must not alias
+    sets = [dict(idx=torch.empty(T * TOPK, dtype=torch.int32, device="cuda"),
+                 gates=torch.empty(T * TOPK, dtype=torch.float64, device="cuda"),
+                 cnt=torch.empty(T, dtype=torch.int32, device="cuda"),
+                 out=torch.empty(T, D, dtype=torch.float32, device="cuda")) for _ in range(2)]
     torch.cuda.synchronize()
     log(f"[rank {rank}] setup {time.time() - t0:.1f}s; bank {layer.bank_bytes() / 1e9:.2f} GB")
 
-    def step():
-        layer.forward(a1.data_ptr(), a3.data_ptr(), None, T, idx.data_ptr(), gates.data_ptr(),
-                      cnt.data_ptr(), out.data_ptr())
+    def step(s):
+        b = sets[s & 1]
+        layer.forward(a1.data_ptr(), a3.data_ptr(), None, T, b["idx"].data_ptr(),
+                      b["gates"].data_ptr(), b["cnt"].data_ptr(), b["out"].data_ptr())
 
-    with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            step()
-        ctx.synchronize()
-    idx_h = idx.cpu().numpy().view(np.uint32)
-    g1b, g2b, S, n_hit, flops = gemm_algorithmic_bytes(idx_h, T)
-    ffn_mean = float(cnt.cpu().numpy().mean())
+    def batches(n):
+        sel = [sets[i & 1] for i in range(n)]
+        layer.forward_batches([a1.data_ptr()] * n, [a3.data_ptr()] * n, None, T,
+                              [b["idx"].data_ptr() for b in sel],
+                              [b["gates"].data_ptr() for b in sel],
+                              [b["cnt"].data_ptr() for b in sel],
+                              [b["out"].data_ptr() for b in sel])
 
-    # ---- timed region: device events on the layer's stream -----------------
-    ctx.profile(True)
-    ctx.profile_flush()
-    l0 = ctx.kernel_launches()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    barrier(ws)
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    def timed(fn, n):
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        barrier(ws)
+        torch.cuda.synchronize()
         with torch.cuda.stream(stream):
             ev0.record(stream)
-            for _ in range(args.steps):
-                step()
+            fn(n)
             ev1.record(stream)
         ev1.synchronize()
-    torch.cuda.synchronize()
-    barrier(ws)
+        torch.cuda.synchronize()
+        barrier(ws)
+        return ev0.elapsed_time(ev1) / n
+
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup):
+            step(i)
+        ctx.synchronize()
+    idx_h = sets[0]["idx"].cpu().numpy().view(np.uint32)
+    g1b, g2b, S, n_hit, flops = gemm_algorithmic_bytes(idx_h, T)
+    ffn_mean = float(sets[0]["cnt"].cpu().numpy().mean())
+
+    # ---- serial schedule: one batch after the other (per-batch latency) ----
+    ctx.profile(True)
+    ctx.profile_flush()
+    ms_serial = timed(lambda n: [step(i) for i in range(n)], args.steps)
+    stages_serial = ctx.profile_flush()
+
+    # ---- pipelined schedule (headline): front half of batch i+1 under the
+    # expert GEMMs of batch i; device-timed over K batches -------------------
+    pipelined = args.schedule == "pipelined"
+    if pipelined:
+        with torch.cuda.stream(stream):
+            batches(max(args.warmup, 2))
+        ctx.synchronize()
+    ctx.profile_flush()
+    l0 = ctx.kernel_launches()
+    with ClockSampler(local) as clk:
+        if pipelined:
+            ms = timed(batches, args.steps)
+        else:
+            ms = timed(lambda n: [step(i) for i in range(n)], args.steps)
     launches = ctx.kernel_launches() - l0
-    ms = ev0.elapsed_time(ev1) / args.steps
     stages = ctx.profile_flush()
     ctx.profile(False)
     ms_max = max_over_ranks(ms, ws)
+    ms_serial_max = max_over_ranks(ms_serial, ws)
     value = T * ws / (ms_max / 1e3)
 
     # ---- e2e through the host tier (pinned buffers, copies in the region) --
@@ -320,16 +347,9 @@ def run_b200(args):
     host = [a.numpy() for a in (a1_p, a3_p, idx_p, gat_p, cnt_p, out_p)]
     e_steps = max(1, min(args.steps, 5))
     layer.forward_host(host[0], host[1], None, T, host[2], host[3], host[4], host[5])
-    barrier(ws)
-    with torch.cuda.stream(stream):
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(e_steps):
-            layer.forward_host(host[0], host[1], None, T, host[2], host[3], host[4], host[5])
-        e1.record(stream)
-        e1.synchronize()
-    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e_steps, ws)
+    e2e_ms = timed(lambda n: [layer.forward_host(host[0], host[1], None, T, host[2], host[3],
+                                                 host[4], host[5]) for _ in range(n)], e_steps)
+    e2e_ms = max_over_ranks(e2e_ms, ws)
     e2e_val = T * ws / (e2e_ms / 1e3)
     h2d = 2 * T * D * 4
     d2h = T * D * 4 + T * TOPK * (4 + 8) + T * 4
@@ -338,11 +358,15 @@ def run_b200(args):
         return
     peaks = measured_peaks()
     hbm_peak = peaks["hbm_gbs"] if peaks else 6650.0
-    g1 = stages.get("gemm1_tcgen05", (0.0, 1))
-    g2 = stages.get("gemm2_tcgen05", (0.0, 1))
-    t_gemm = (g1[0] + g2[0]) / max(1, g1[1])  # per step (one launch each per step)
-    achieved = (g1b + g2b) / (t_gemm / 1e3) / 1e9 if t_gemm > 0 else None
-    per_stage = {k: round(v[0] / v[1], 4) for k, v in stages.items()}
+
+    def gemm_roofline(st):
+        g1 = st.get("gemm1_tcgen05", (0.0, 1))
+        g2 = st.get("gemm2_tcgen05", (0.0, 1))
+        t = (g1[0] + g2[0]) / max(1, g1[1])  # per step (one launch of each per step)
+        return t, ((g1b + g2b) / (t / 1e3) / 1e9 if t > 0 else None)
+
+    t_gemm, achieved = gemm_roofline(stages)
+    t_gemm_serial, achieved_serial = gemm_roofline(stages_serial)
     cpu = None
     if ws == 1 and not args.no_cpu_baseline:
         try:
@@ -358,19 +382,25 @@ def run_b200(args):
         "config": {"workload": cfg["workload"], "tokens_per_gpu": T, "d_model": D, "n_ffn": N_FFN,
                    "n_zero": N_ZERO, "top_k": TOPK, "k_expected": KE, "inter": INTER,
                    "router": "exact fp32 (bit-exact vs reference)", "expert_gemm": "bf16 tcgen05",
+                   "schedule": ("pipelined micro-batches: front half (rmsnorm, exact router, "
+                                "top-K, permute) of batch i+1 on the FP32 pipes under the "
+                                "HBM-bound expert GEMMs of batch i (2 streams)") if pipelined
+                   else "serial", "serial_ms_per_batch": ms_serial_max,
                    "parallelism": f"replicated experts, token-sharded x{ws}",
                    "l2": "inputs + weights (25.8 GB) larger than L2 every step",
                    "mean_ffn_per_token": ffn_mean, "ffn_slots": S, "experts_hit": n_hit},
         "e2e": {"value": e2e_val, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "gpu_launches": launches,
-        "roofline": {"kernel": "grouped_gemm_bf16 (GEMM1+GEMM2)", "bound": "hbm",
+        "roofline": {"kernel": "grouped_gemm_bf16 (GEMM1+GEMM2, tcgen05)", "bound": "hbm",
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": (achieved / hbm_peak) if achieved else None, "traffic": None,
                      "algorithmic_bytes_per_step": g1b + g2b, "ms_per_step": t_gemm,
+                     "achieved_serial": achieved_serial, "ms_per_step_serial": t_gemm_serial,
                      "tflops": flops / (t_gemm / 1e3) / 1e12 if t_gemm > 0 else None,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},
-        "stages_ms": per_stage,
+        "stages_ms": {k: round(v[0] / v[1], 4) for k, v in stages.items()},
+        "stages_ms_serial": {k: round(v[0] / v[1], 4) for k, v in stages_serial.items()},
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
     }
@@ -386,6 +416,7 @@ def main():
     ap.add_argument("--config", default="prefill", choices=sorted(CONFIGS))
     ap.add_argument("--tokens", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--schedule", default="pipelined", choices=["pipelined", "serial"])
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)

@@ -172,6 +172,17 @@ int scmoe_rmsnorm(scmoe_ctx* ctx, const float* x, const float* gain, size_t rows
 int scmoe_layer_forward(scmoe_ctx* ctx, scmoe_router* r, scmoe_bank* b, const float* a1,
                         const float* a3, const float* gain, size_t tokens, int renormalize,
                         uint32_t* indices, double* gates, uint32_t* ffn_count, float* out);
+/* Pipelined form for a stream of micro-batches (serving / the paper's
+ * two-batch overlap): batch i+1's front half (rmsnorm, exact router, top-K,
+ * permutation) runs on the tensor-core-idle FP32 pipes while batch i's
+ * expert GEMMs stream weights from HBM.  Results are identical to n calls of
+ * scmoe_layer_forward; arrays hold one device pointer per batch (a3 may be
+ * NULL).  Stream-ordered on the context's stream. */
+int scmoe_layer_forward_batches(scmoe_ctx* ctx, scmoe_router* r, scmoe_bank* b, size_t n_batches,
+                                const float* const* a1, const float* const* a3, const float* gain,
+                                size_t tokens, int renormalize, uint32_t* const* indices,
+                                double* const* gates, uint32_t* const* ffn_count,
+                                float* const* out);
 int scmoe_layer_forward_host(scmoe_ctx* ctx, scmoe_router* r, scmoe_bank* b, const float* a1,
                              const float* a3, const float* gain, size_t tokens, int renormalize,
                              uint32_t* indices, double* gates, uint32_t* ffn_count, float* out);

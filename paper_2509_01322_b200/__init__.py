@@ -133,6 +133,8 @@ _PROTOS = {
     "scmoe_layer_forward": (C.c_int, [_P, _P, _P, _P, _P, _P, _SZ, C.c_int, _P, _P, _P, _P]),
     "scmoe_layer_forward_host": (C.c_int, [_P, _P, _P, _P, _P, _P, _SZ, C.c_int, _P, _P, _P,
                                            _P]),
+    "scmoe_layer_forward_batches": (C.c_int, [_P, _P, _P, _SZ, _P, _P, _P, _SZ, C.c_int, _P, _P,
+                                              _P, _P]),
     "scmoe_rng_stream_seed": (_U64, [_U64, _U64]),
     "scmoe_rng_fill_normal_host": (None, [_U64, _U64, _SZ, _P, C.c_int]),
     "scmoe_rng_fill_uniform": (C.c_int, [_P, _U64, _U64, _SZ, C.c_double, _P]),

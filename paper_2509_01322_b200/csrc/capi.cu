@@ -87,68 +87,154 @@ int tile_rows_for(const scmoe_bank* b) {
     return b->precision == SCMOE_PREC_BF16 ? grouped_gemm_tile_rows() : 64;
 }
 
-// moe_forward on device pointers; x is the MoE input (hmoe), used by the
-// expert FFN and by the zero-expert identity term.
-void moe_forward_dev(scmoe_ctx* c, scmoe_bank* b, const float* x, const __nv_bfloat16* x_bf16,
-                     size_t T, const uint32_t* idx, const double* gates, size_t K, size_t n_zero,
-                     int renorm, const float* residual, float* out) {
-    const size_t n_ffn = b->n, d = b->d, I = b->inter, E = n_ffn + n_zero;
+// The MoE block is split into a front half (permutation, and the row gather
+// of the bf16 operand) and a back half (expert GEMMs, combine) so a pipelined
+// caller can run the front of batch i+1 beside the back of batch i.  The
+// permutation result travels between the halves inside the workspace.
+void moe_front(scmoe_ctx* c, scmoe_bank* b, const float* x, const __nv_bfloat16* x_bf16,
+               size_t T, const uint32_t* idx, size_t K, size_t n_zero) {
+    const size_t n_ffn = b->n, d = b->d, E = n_ffn + n_zero;
     SCMOE_CHECK_ARG(K >= 1 && K <= 64, SCMOE_ERR_CONFIG, "moe_forward: top_k must be in [1, 64]");
     Workspace& ws = c->ws;
-    PermResult pr; { ProfScope _p(c, "permute"); pr = launch_permute(c, idx, T, K, n_ffn, E, tile_rows_for(b)); }
-    const float gf = (float)b->gamma_ffn(), gz = (float)b->gamma_zero();
-    if (b->precision == SCMOE_PREC_F32_EXACT) {
-        float* h = ws.h.get<float>(T * K * I + 1);
-        float* y = ws.y.get<float>(T * K * d + 1);
-        { ProfScope _p(c, "expert_gemm1_f32"); launch_seq_gemm(c, x, d, pr.row_token, b->w_in32, I, d * I, h, I, d, I, /*silu=*/1,
-                        pr.tiles, pr.n_tiles, pr.max_tiles, 64); }
-        { ProfScope _p(c, "expert_gemm2_f32"); launch_seq_gemm(c, h, I, nullptr, b->w_out32, d, I * d, y, d, I, d, /*silu=*/0, pr.tiles,
-                        pr.n_tiles, pr.max_tiles, 64); }
-        { ProfScope _p(c, "combine"); launch_combine_f32(c, x, y, idx, gates, pr.slot_pos, T, d, K, n_ffn, gf, gz, renorm,
-                           residual, out); }
-    } else {
+    PermResult pr;
+    {
+        ProfScope _p(c, "permute");
+        pr = launch_permute(c, idx, T, K, n_ffn, E, tile_rows_for(b));
+    }
+    static_assert(sizeof(PermResult) <= sizeof(ws.pr_blob), "perm blob");
+    memcpy(ws.pr_blob, &pr, sizeof(pr));
+    if (b->precision == SCMOE_PREC_BF16) {
         __nv_bfloat16* xb = const_cast<__nv_bfloat16*>(x_bf16);
         if (!xb) {
             // Caller passed fp32 only: make the bf16 GEMM operand copy once.
             xb = ws.hmoe_bf16.get<__nv_bfloat16>(T * d);
             launch_cast_bf16(c, x, T * d, xb);
         }
-        __nv_bfloat16* h = ws.h.get<__nv_bfloat16>(T * K * I + 1);
-        __nv_bfloat16* y = ws.y.get<__nv_bfloat16>(T * K * d + 1);
-        if (c->gemm1_gather) {
-            // GEMM1 gathers its token rows straight from x (TMA tile::gather4);
-            // x (T x d bf16) stays L2-resident, no permuted copy is written.
-            ProfScope _p(c, "gemm1_tcgen05");
-            launch_grouped_gemm_bf16(c, b->w1t, n_ffn, I, d, xb, T, pr.row_token, h, /*silu=*/1,
-                                     pr.tiles, pr.n_tiles, pr.max_tiles, tile_rows_for(b));
-        } else {
+        if (!c->gemm1_gather) {
             __nv_bfloat16* xp = ws.xp.get<__nv_bfloat16>(T * K * d + 1);
-            { ProfScope _p(c, "gather"); launch_gather_bf16(c, xb, d, pr.row_token, pr.expert_base, n_ffn, T * K, xp); }
-            ProfScope _p(c, "gemm1_tcgen05");
-            launch_grouped_gemm_bf16(c, b->w1t, n_ffn, I, d, xp, T * K, nullptr, h, /*silu=*/1,
-                                     pr.tiles, pr.n_tiles, pr.max_tiles, tile_rows_for(b));
+            ProfScope _p(c, "gather");
+            launch_gather_bf16(c, xb, d, pr.row_token, pr.expert_base, n_ffn, T * K, xp);
         }
-        { ProfScope _p(c, "gemm2_tcgen05"); launch_grouped_gemm_bf16(c, b->w2t, n_ffn, d, I, h, T * K, nullptr, y, /*silu=*/0, pr.tiles,
-                                 pr.n_tiles, pr.max_tiles, tile_rows_for(b)); }
-        { ProfScope _p(c, "combine"); launch_combine_bf16(c, x, y, idx, gates, pr.slot_pos, T, d, K, n_ffn, gf, gz, renorm,
-                            residual, out); }
     }
 }
 
-// router.hpp:136 logits = mm(x, W_r): one group, row tiles sized for the batch.
+void moe_back(scmoe_ctx* c, scmoe_bank* b, const float* x, size_t T, const uint32_t* idx,
+              const double* gates, size_t K, int renorm, const float* residual, float* out) {
+    const size_t n_ffn = b->n, d = b->d, I = b->inter;
+    Workspace& ws = c->ws;
+    PermResult pr;
+    memcpy(&pr, ws.pr_blob, sizeof(pr));
+    const float gf = (float)b->gamma_ffn(), gz = (float)b->gamma_zero();
+    if (b->precision == SCMOE_PREC_F32_EXACT) {
+        float* h = ws.h.get<float>(T * K * I + 1);
+        float* y = ws.y.get<float>(T * K * d + 1);
+        {
+            ProfScope _p(c, "expert_gemm1_f32");
+            launch_seq_gemm(c, x, d, pr.row_token, b->w_in32, I, d * I, h, I, d, I, /*silu=*/1,
+                            pr.tiles, pr.n_tiles, pr.max_tiles, 64);
+        }
+        {
+            ProfScope _p(c, "expert_gemm2_f32");
+            launch_seq_gemm(c, h, I, nullptr, b->w_out32, d, I * d, y, d, I, d, /*silu=*/0,
+                            pr.tiles, pr.n_tiles, pr.max_tiles, 64);
+        }
+        ProfScope _p(c, "combine");
+        launch_combine_f32(c, x, y, idx, gates, pr.slot_pos, T, d, K, n_ffn, gf, gz, renorm,
+                           residual, out);
+    } else {
+        __nv_bfloat16* h = ws.h.get<__nv_bfloat16>(T * K * I + 1);
+        __nv_bfloat16* y = ws.y.get<__nv_bfloat16>(T * K * d + 1);
+        if (c->gemm1_gather) {
+            // GEMM1 gathers its token rows straight from x (TMA tile::gather4).
+            ProfScope _p(c, "gemm1_tcgen05");
+            launch_grouped_gemm_bf16(c, b->w1t, n_ffn, I, d, ws.hmoe_bf16.get<__nv_bfloat16>(T * d),
+                                     T, pr.row_token, h, /*silu=*/1, pr.tiles, pr.n_tiles,
+                                     pr.max_tiles, tile_rows_for(b));
+        } else {
+            ProfScope _p(c, "gemm1_tcgen05");
+            launch_grouped_gemm_bf16(c, b->w1t, n_ffn, I, d, ws.xp.get<__nv_bfloat16>(T * K * d + 1),
+                                     T * K, nullptr, h, /*silu=*/1, pr.tiles, pr.n_tiles,
+                                     pr.max_tiles, tile_rows_for(b));
+        }
+        {
+            ProfScope _p(c, "gemm2_tcgen05");
+            launch_grouped_gemm_bf16(c, b->w2t, n_ffn, d, I, h, T * K, nullptr, y, /*silu=*/0,
+                                     pr.tiles, pr.n_tiles, pr.max_tiles, tile_rows_for(b));
+        }
+        ProfScope _p(c, "combine");
+        launch_combine_bf16(c, x, y, idx, gates, pr.slot_pos, T, d, K, n_ffn, gf, gz, renorm,
+                            residual, out);
+    }
+}
+
+// moe_forward on device pointers; x is the MoE input (hmoe), used by the
+// expert FFN and by the zero-expert identity term.
+void moe_forward_dev(scmoe_ctx* c, scmoe_bank* b, const float* x, const __nv_bfloat16* x_bf16,
+                     size_t T, const uint32_t* idx, const double* gates, size_t K, size_t n_zero,
+                     int renorm, const float* residual, float* out) {
+    moe_front(c, b, x, x_bf16, T, idx, K, n_zero);
+    moe_back(c, b, x, T, idx, gates, K, renorm, residual, out);
+}
+
+// router.hpp:136 logits = mm(x, W_r).  Kernel choice: the full-width slab
+// kernel (1 CTA/SM, single wave) when the batch fills the GPU; the lean
+// kernel inside pipelined calls (it co-resides with the grouped GEMM); the
+// 64/16-row tiled kernel otherwise (small batches, E > 768).
 void route_logits(scmoe_ctx* c, scmoe_router* r, const float* x, size_t T, float* logits) {
     const size_t E = r->E();
-    if (router_slab_ok(T, r->d, E, c->num_sms)) {
-        ProfScope _p(c, "router_gemm");
-        launch_router_slab(c, x, r->w, logits, T, r->d, E);
-        return;
+    int v = c->router_variant;
+    if (v == 2 && !router_lean_ok(r->d, E)) v = 0;
+    if (v == 1 && !router_slab_ok(T, r->d, E, 0)) v = 0;
+    if (v == 0) {
+        if (c->overlapped && router_lean_ok(r->d, E) && T >= 512)
+            v = 2;
+        else if (router_slab_ok(T, r->d, E, c->num_sms))
+            v = 1;
+        else
+            v = 3;
     }
-    const int tr = seq_gemm_tile_rows(T, E, c->num_sms);
-    const size_t ntile = ceil_div(T, tr);
-    TokenTile* td = c->ws.tiles_router.get<TokenTile>(ntile);
-    launch_row_tiles(c, T, tr, td);
     ProfScope _p(c, "router_gemm");
-    launch_seq_gemm(c, x, r->d, nullptr, r->w, E, 0, logits, E, r->d, E, 0, td, nullptr, ntile, tr);
+    if (v == 1) {
+        launch_router_slab(c, x, r->w, logits, T, r->d, E);
+    } else if (v == 2) {
+        launch_router_lean(c, x, r->w, logits, T, r->d, E);
+    } else {
+        const int tr = seq_gemm_tile_rows(T, E, c->num_sms);
+        const size_t ntile = ceil_div(T, tr);
+        TokenTile* td = c->ws.tiles_router.get<TokenTile>(ntile);
+        launch_row_tiles(c, T, tr, td);
+        launch_seq_gemm(c, x, r->d, nullptr, r->w, E, 0, logits, E, r->d, E, 0, td, nullptr, ntile,
+                        tr);
+    }
+}
+
+// Front half of the ScMoE MoE branch (model.hpp:394-397): rmsnorm, router,
+// softmax + top-K, permutation (+ gather).
+void layer_front(scmoe_ctx* c, scmoe_router* r, scmoe_bank* b, const float* a1, const float* gain,
+                 size_t T, uint32_t* idx, double* gates, uint32_t* ffn_count) {
+    const size_t d = r->d, E = r->E(), K = r->top_k;
+    Workspace& ws = c->ws;
+    float* hmoe = ws.hmoe.get<float>(T * d);
+    __nv_bfloat16* hb =
+        b->precision == SCMOE_PREC_BF16 ? ws.hmoe_bf16.get<__nv_bfloat16>(T * d) : nullptr;
+    {
+        ProfScope _p(c, "rmsnorm");
+        launch_rmsnorm(c, a1, gain, T, d, 1e-6f, hmoe, hb);
+    }
+    float* logits = ws.logits.get<float>(T * E);
+    route_logits(c, r, hmoe, T, logits);
+    {
+        ProfScope _p(c, "softmax_topk");
+        launch_softmax_topk(c, logits, T, E, K, r->n_ffn, r->b, idx, gates, ffn_count, nullptr);
+    }
+    moe_front(c, b, hmoe, hb, T, idx, K, r->n_zero);
+}
+
+void check_layer_args(scmoe_router* r, scmoe_bank* b) {
+    if (r->d != b->d) SCMOE_THROW(SCMOE_ERR_DIMENSION, "layer: router/bank width mismatch");
+    if (r->n_ffn != b->n)
+        SCMOE_THROW(SCMOE_ERR_DIMENSION, "moe_block: decision/bank FFN count mismatch");
+    validate_router(r->n_ffn, r->n_zero, r->top_k, r->k_expected, r->mu);
 }
 
 }  // namespace
@@ -173,6 +259,10 @@ int scmoe_ctx_create(int device, scmoe_ctx** out) {
         c->device = device;
         c->num_sms = prop.multiProcessorCount;
         if (const char* g = getenv("SCMOE_GEMM1_GATHER")) c->gemm1_gather = atoi(g) != 0;
+        if (const char* v = getenv("SCMOE_ROUTER")) {
+            const std::string sv(v);
+            c->router_variant = sv == "slab" ? 1 : sv == "lean" ? 2 : sv == "tiled" ? 3 : 0;
+        }
         SCMOE_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
         c->stream = c->own_stream;
         SCMOE_CUDA(cudaMalloc(&c->dev_status, sizeof(int)));
@@ -186,6 +276,20 @@ int scmoe_ctx_destroy(scmoe_ctx* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     c->ws.release_all();
+    c->ws_alt.release_all();
+    if (c->s_front) {
+        cudaStreamDestroy(c->s_front);
+        cudaStreamDestroy(c->s_back);
+        for (int i = 0; i < 2; ++i) {
+            cudaEventDestroy(c->ev_front[i]);
+            cudaEventDestroy(c->ev_back[i]);
+        }
+        cudaEventDestroy(c->ev_join);
+    }
+    for (auto& rec : c->prof.recs) {
+        cudaEventDestroy(rec.a);
+        cudaEventDestroy(rec.b);
+    }
     Stage& st = stage_of(c);
     for (auto& b : st.bufs) b.release();
     if (c->dev_status) cudaFree(c->dev_status);
@@ -595,20 +699,65 @@ int scmoe_layer_forward(scmoe_ctx* c, scmoe_router* r, scmoe_bank* b, const floa
                         double* gates, uint32_t* ffn_count, float* out) {
     return guarded(c, [&] {
         require_ctx(c);
-        if (r->d != b->d) SCMOE_THROW(SCMOE_ERR_DIMENSION, "layer: router/bank width mismatch");
-        if (r->n_ffn != b->n) SCMOE_THROW(SCMOE_ERR_DIMENSION, "moe_block: decision/bank FFN count mismatch");
-        validate_router(r->n_ffn, r->n_zero, r->top_k, r->k_expected, r->mu);
+        check_layer_args(r, b);
         if (T == 0) return;
-        const size_t d = r->d, E = r->E(), K = r->top_k;
-        Workspace& ws = c->ws;
-        float* hmoe = ws.hmoe.get<float>(T * d);
-        __nv_bfloat16* hb =
-            b->precision == SCMOE_PREC_BF16 ? ws.hmoe_bf16.get<__nv_bfloat16>(T * d) : nullptr;
-        { ProfScope _p(c, "rmsnorm"); launch_rmsnorm(c, a1, gain, T, d, 1e-6f, hmoe, hb); }
-        float* logits = ws.logits.get<float>(T * E);
-        route_logits(c, r, hmoe, T, logits);
-        { ProfScope _p(c, "softmax_topk"); launch_softmax_topk(c, logits, T, E, K, r->n_ffn, r->b, idx, gates, ffn_count, nullptr); }
-        moe_forward_dev(c, b, hmoe, hb, T, idx, gates, K, r->n_zero, renorm, a3, out);
+        layer_front(c, r, b, a1, gain, T, idx, gates, ffn_count);
+        moe_back(c, b, c->ws.hmoe.get<float>(T * r->d), T, idx, gates, r->top_k, renorm, a3, out);
+    });
+}
+
+int scmoe_layer_forward_batches(scmoe_ctx* c, scmoe_router* r, scmoe_bank* b, size_t n_batches,
+                                const float* const* a1, const float* const* a3, const float* gain,
+                                size_t T, int renorm, uint32_t* const* idx, double* const* gates,
+                                uint32_t* const* ffn_count, float* const* out) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        check_layer_args(r, b);
+        if (T == 0 || n_batches == 0) return;
+        if (!c->s_front) {
+            SCMOE_CUDA(cudaStreamCreateWithFlags(&c->s_front, cudaStreamNonBlocking));
+            SCMOE_CUDA(cudaStreamCreateWithFlags(&c->s_back, cudaStreamNonBlocking));
+            for (int i = 0; i < 2; ++i) {
+                SCMOE_CUDA(cudaEventCreateWithFlags(&c->ev_front[i], cudaEventDisableTiming));
+                SCMOE_CUDA(cudaEventCreateWithFlags(&c->ev_back[i], cudaEventDisableTiming));
+            }
+            SCMOE_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+        }
+        cudaStream_t user = c->stream;
+        SCMOE_CUDA(cudaEventRecord(c->ev_join, user));
+        SCMOE_CUDA(cudaStreamWaitEvent(c->s_front, c->ev_join, 0));
+        SCMOE_CUDA(cudaStreamWaitEvent(c->s_back, c->ev_join, 0));
+        c->overlapped = true;
+        int slot = 0;  // c->ws holds slot `slot`'s buffers, c->ws_alt the other's
+        struct Restore {
+            scmoe_ctx* c;
+            cudaStream_t user;
+            int* slot;
+            ~Restore() {
+                if (*slot) std::swap(c->ws, c->ws_alt);
+                c->stream = user;
+                c->overlapped = false;
+            }
+        } restore{c, user, &slot};
+        for (size_t i = 0; i < n_batches; ++i) {
+            const int want = (int)(i & 1);
+            if (want != slot) {
+                std::swap(c->ws, c->ws_alt);
+                slot = want;
+            }
+            // front(i) reuses the buffers of batch i-2: wait for its back half
+            c->stream = c->s_front;
+            if (i >= 2) SCMOE_CUDA(cudaStreamWaitEvent(c->s_front, c->ev_back[slot], 0));
+            layer_front(c, r, b, a1[i], gain, T, idx[i], gates[i], ffn_count[i]);
+            SCMOE_CUDA(cudaEventRecord(c->ev_front[slot], c->s_front));
+            c->stream = c->s_back;
+            SCMOE_CUDA(cudaStreamWaitEvent(c->s_back, c->ev_front[slot], 0));
+            moe_back(c, b, c->ws.hmoe.get<float>(T * r->d), T, idx[i], gates[i], r->top_k, renorm,
+                     a3 ? a3[i] : nullptr, out[i]);
+            SCMOE_CUDA(cudaEventRecord(c->ev_back[slot], c->s_back));
+        }
+        // the caller's stream resumes after the last back half (s_back is in order)
+        SCMOE_CUDA(cudaStreamWaitEvent(user, c->ev_back[(n_batches - 1) & 1], 0));
     });
 }
 

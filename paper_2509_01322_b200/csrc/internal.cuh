@@ -65,6 +65,7 @@ struct Workspace {
     DevBuf logits, probs, hmoe, hmoe_bf16, idx, gates, ffn_count;
     DevBuf rank_in_block, block_counts, expert_count, expert_base, slot_pos, row_token;
     DevBuf tiles, n_tiles, xp, h, y, in_copy, out_copy, misc, tiles_router;
+    unsigned char pr_blob[64] = {};  // permutation result carried from moe_front to moe_back
     void release_all() {
         DevBuf* all[] = {&logits, &probs, &hmoe, &hmoe_bf16, &idx, &gates, &ffn_count,
                          &rank_in_block, &block_counts, &expert_count, &expert_base, &slot_pos,
@@ -102,7 +103,16 @@ struct scmoe_ctx {
     uint64_t launches = 0;
     Workspace ws;
     Profiler prof;
-    bool gemm1_gather = true;  // GEMM1 B operand via TMA gather4 (SCMOE_GEMM1_GATHER=0: gather kernel)
+    bool gemm1_gather = false;  // GEMM1 B operand via TMA gather4 (SCMOE_GEMM1_GATHER=1)
+    // router projection kernel: 0 auto, 1 slab (56 tokens x E, 1 CTA/SM),
+    // 2 lean (co-resides with the GEMM), 3 tiled (64/16-row tiles); SCMOE_ROUTER
+    int router_variant = 0;
+    bool overlapped = false;    // inside a pipelined multi-batch call
+    // pipelined multi-batch execution (scmoe_layer_forward_batches)
+    cudaStream_t s_front = nullptr, s_back = nullptr;
+    cudaEvent_t ev_front[2] = {nullptr, nullptr}, ev_back[2] = {nullptr, nullptr};
+    cudaEvent_t ev_join = nullptr;
+    Workspace ws_alt;
 };
 
 // RAII stage timer; a no-op unless profiling is enabled on the context.
@@ -180,6 +190,10 @@ void launch_seq_gemm(scmoe_ctx* c, const float* A, size_t lda, const int* a_rows
 int seq_gemm_tile_rows(size_t rows, size_t N, int num_sms);
 // Router projection with one CTA per 56-token slab x all experts (E <= 768).
 bool router_slab_ok(size_t T, size_t K, size_t E, int num_sms);
+// Router projection sized to co-reside with the grouped GEMM (28-token slabs).
+bool router_lean_ok(size_t K, size_t E);
+void launch_router_lean(scmoe_ctx* c, const float* X, const float* W, float* logits, size_t T,
+                        size_t K, size_t E);
 void launch_router_slab(scmoe_ctx* c, const float* X, const float* W, float* logits, size_t T,
                         size_t K, size_t E);
 void launch_softmax_topk(scmoe_ctx* c, const float* logits, size_t T, size_t E, size_t K,

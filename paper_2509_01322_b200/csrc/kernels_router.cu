@@ -415,6 +415,137 @@ __global__ void __launch_bounds__(kSlabThreads, 1) router_slab_kernel(
     }
 }
 
+// ---------------------------------------------------------------------------
+// Router projection, "lean" variant sized to co-reside with the persistent
+// grouped GEMM on every SM (GEMM: 192 threads, ~194 KB smem; this kernel:
+// 512 threads x <= 64 registers, ~26 KB smem), so the FP32-pipe-bound router
+// of the next micro-batch runs underneath the HBM-bound expert GEMMs of the
+// current one.  CTA = 28 tokens x all E <= 768 experts (4 token groups x 128
+// expert groups, 7 x 6 chains per thread); K staged 4 rows at a time, W by a
+// double-buffered cp.async ring, X (raw rows) by a 4-deep ring.
+// ---------------------------------------------------------------------------
+constexpr int kLeanTok = 7, kLeanExp = 6, kLeanTG = 4, kLeanEG = 128;
+constexpr int kLeanRows = kLeanTok * kLeanTG;     // 28
+constexpr int kLeanThreads = kLeanTG * kLeanEG;   // 512
+constexpr int kLeanKC = 4;
+constexpr int kLeanW = kLeanEG * kLeanExp;        // 768
+constexpr int kLeanXS = 32;                       // xs row: group g at [8g, 8g+7)
+constexpr int kLeanXStages = 4;
+
+__global__ void __launch_bounds__(kLeanThreads, 2) router_lean_kernel(
+    const float* __restrict__ X, const float* __restrict__ W, float* __restrict__ logits, int T,
+    int K, int E) {
+    __shared__ __align__(16) float ws[2][kLeanKC][kLeanW];
+    __shared__ __align__(16) float xraw[kLeanXStages][kLeanRows][kLeanKC];
+    __shared__ __align__(16) float xs[2][kLeanKC][kLeanXS];
+    const int tid = threadIdx.x;
+    const int tg = tid / kLeanEG, eg = tid % kLeanEG;
+    const int nchunks = K / kLeanKC;
+
+    for (int slab = blockIdx.x; slab * kLeanRows < T; slab += gridDim.x) {
+        const int row0 = slab * kLeanRows;
+        const int nrows = min(kLeanRows, T - row0);
+        // W chunk: 4 x 768 floats = 768 float4 -> 1.5 per thread (threads 0..255 do 2)
+        auto load_w = [&](int chunk, int buf) {
+            const int k0 = chunk * kLeanKC;
+            for (int i = tid; i < kLeanKC * kLeanW / 4; i += kLeanThreads) {
+                const int k = i / (kLeanW / 4), col = 4 * (i % (kLeanW / 4));
+                const bool ok = col + 3 < E;
+                const float* s = ok ? W + (size_t)(k0 + k) * E + col : W;
+                const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&ws[buf][k][col]));
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(s),
+                             "r"(ok ? 16 : 0)
+                             : "memory");
+            }
+        };
+        auto load_x = [&](int chunk) {
+            if (tid < kLeanRows && chunk < nchunks) {
+                const bool ok = tid < nrows;
+                const float* s = ok ? X + (size_t)(row0 + tid) * K + chunk * kLeanKC : X;
+                const uint32_t dst = static_cast<uint32_t>(
+                    __cvta_generic_to_shared(&xraw[chunk % kLeanXStages][tid][0]));
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(s),
+                             "r"(ok ? 16 : 0)
+                             : "memory");
+            }
+        };
+        float acc[kLeanTok][kLeanExp];
+#pragma unroll
+        for (int i = 0; i < kLeanTok; ++i)
+#pragma unroll
+            for (int j = 0; j < kLeanExp; ++j) acc[i][j] = 0.0f;
+
+        // prologue: X chunks 0..2, W chunk 0
+        load_x(0);
+        load_x(1);
+        load_x(2);
+        load_w(0, 0);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+        if (tid < kLeanRows * kLeanKC) {
+            const int r = tid / kLeanKC, k = tid % kLeanKC;
+            xs[0][k][8 * (r / kLeanTok) + r % kLeanTok] = xraw[0][r][k];
+        }
+        __syncthreads();
+        for (int ch = 0; ch < nchunks; ++ch) {
+            const int buf = ch & 1;
+            const bool more = ch + 1 < nchunks;
+            // two groups: W(ch+1) (needed next iteration), then X(ch+3); the
+            // wait below leaves only the newest group (X(ch+3)) in flight
+            if (more) load_w(ch + 1, buf ^ 1);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            load_x(ch + 3);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+#pragma unroll
+            for (int k = 0; k < kLeanKC; ++k) {
+                const float4 a03 = *reinterpret_cast<const float4*>(&xs[buf][k][8 * tg]);
+                const float2 a45 = *reinterpret_cast<const float2*>(&xs[buf][k][8 * tg + 4]);
+                const float a6 = xs[buf][k][8 * tg + 6];
+                const float2 b01 = *reinterpret_cast<const float2*>(&ws[buf][k][kLeanExp * eg]);
+                const float2 b23 = *reinterpret_cast<const float2*>(&ws[buf][k][kLeanExp * eg + 2]);
+                const float2 b45 = *reinterpret_cast<const float2*>(&ws[buf][k][kLeanExp * eg + 4]);
+                const float av[7] = {a03.x, a03.y, a03.z, a03.w, a45.x, a45.y, a6};
+                const float bv[6] = {b01.x, b01.y, b23.x, b23.y, b45.x, b45.y};
+#pragma unroll
+                for (int i = 0; i < kLeanTok; ++i)
+#pragma unroll
+                    for (int j = 0; j < kLeanExp; ++j)
+                        acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(av[i], bv[j]));
+            }
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+            __syncthreads();
+            if (more && tid < kLeanRows * kLeanKC) {
+                const int r = tid / kLeanKC, k = tid % kLeanKC;
+                xs[buf ^ 1][k][8 * (r / kLeanTok) + r % kLeanTok] =
+                    xraw[(ch + 1) % kLeanXStages][r][k];
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int i = 0; i < kLeanTok; ++i) {
+            const int r = kLeanTok * tg + i;
+            if (r >= nrows) continue;
+            float* dst = logits + (size_t)(row0 + r) * E + kLeanExp * eg;
+#pragma unroll
+            for (int j = 0; j < kLeanExp; ++j)
+                if (kLeanExp * eg + j < E) dst[j] = acc[i][j];
+        }
+    }
+}
+
+bool router_lean_ok(size_t K, size_t E) {
+    return E <= (size_t)kLeanW && E % 4 == 0 && K % kLeanKC == 0;
+}
+
+void launch_router_lean(scmoe_ctx* c, const float* X, const float* W, float* logits, size_t T,
+                        size_t K, size_t E) {
+    const size_t slabs = ceil_div(T, kLeanRows);
+    const int grid = (int)std::min<size_t>(slabs, (size_t)c->num_sms * 2);
+    router_lean_kernel<<<grid, kLeanThreads, 0, c->stream>>>(X, W, logits, (int)T, (int)K, (int)E);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
 bool router_slab_ok(size_t T, size_t K, size_t E, int num_sms) {
     // full-width slab needs E <= 768, E and K multiples of 4 (float4 rows), and
     // enough tokens to fill most SMs (otherwise the 16/64-row tiles spread better)

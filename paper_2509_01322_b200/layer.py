@@ -71,6 +71,17 @@ class DeviceLayer:
                                                   gain, tokens, int(renormalize), idx, gates,
                                                   ffn_count, out))
 
+    def forward_batches(self, a1s, a3s, gain: Optional[int], tokens: int, idxs, gatess, cnts,
+                        outs, renormalize: bool = False):
+        """Pipelined micro-batches (scmoe_layer_forward_batches): lists of device
+        pointers, one per batch.  Buffers of consecutive batches must not alias."""
+        n = len(a1s)
+        arr = lambda xs: (C.c_void_p * n)(*xs)  # noqa: E731
+        self.ctx._check(lib().scmoe_layer_forward_batches(
+            self.ctx.handle, self.router, self.bank, n, arr(a1s),
+            arr(a3s) if a3s is not None else None, gain, tokens, int(renormalize), arr(idxs),
+            arr(gatess), arr(cnts), arr(outs)))
+
     def forward_host(self, a1, a3, gain, tokens: int, idx, gates, ffn_count, out,
                      renormalize: bool = False):
         """Host (ideally pinned) numpy buffers; copies in, runs, copies out."""

@@ -416,7 +416,9 @@ def main():
     ap.add_argument("--config", default="prefill", choices=sorted(CONFIGS))
     ap.add_argument("--tokens", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--schedule", default="pipelined", choices=["pipelined", "serial"])
+    # pipelined = scmoe_layer_forward_batches; measured slower than serial on B200 in round 1
+    # (router and GEMM contend for shared-memory bandwidth), so serial is the default
+    ap.add_argument("--schedule", default="serial", choices=["pipelined", "serial"])
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)

@@ -47,7 +47,9 @@ constexpr int B_HALF_BYTES = 128 * BK * 2;        // 16 KB per 128 token rows
 constexpr int STAGE_BYTES = SLABS * A_SLAB_BYTES + 2 * B_HALF_BYTES;  // 64 KB
 constexpr int TMEM_COLS = 512;
 constexpr int NUM_THREADS = 192;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int EPI_STAGE_BYTES = 4 * 32 * 80;  // epilogue transpose buffers (4 warps)
+constexpr int SMEM_BYTES =
+    STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + EPI_STAGE_BYTES;
 
 static_assert(SLABS * NT <= TMEM_COLS, "TMEM overflow");
 
@@ -176,6 +178,7 @@ struct GemmArgs {
     __nv_bfloat16* out;  // [rows][M]
     int M, K;            // weight rows per expert, reduction length
     int silu;
+    int debug;           // bit 0: skip epilogue stores (timing experiments only)
 };
 
 __global__ void __launch_bounds__(NUM_THREADS, 1)
@@ -323,6 +326,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     } else {
         // ===== epilogue (warps 2..5) =====
         const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+        // Per-warp 32 tokens x 32 rows bf16 transpose buffer (80 B row pitch:
+        // 16-byte reads of 8 consecutive lanes hit distinct banks).
+        unsigned char* stage_base = smem + STAGES * STAGE_BYTES + 256 + (warp - 2) * 32 * 80;
         int local = 0;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++local) {
             const TokenTile tile = args.tiles[u / mblocks];
@@ -331,21 +337,32 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
             for (int s = 0; s < SLABS; ++s) {
-                const int m = mb * BM + s * 128 + quad * 32 + lane;
+                const int m0 = mb * BM + s * 128 + quad * 32;  // this warp's 32 rows
                 const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + s * NT;
-                __nv_bfloat16* optr = args.out + (size_t)tile.pos * args.M + m;
                 for (int j0 = 0; j0 < tile.count; j0 += 32) {
                     uint32_t v[32];
-                    tmem_ld32(taddr + j0, v);
-                    const int jn = min(32, tile.count - j0);
+                    tmem_ld32(taddr + j0, v);  // v[jj] = D[m0 + lane][j0 + jj]
 #pragma unroll
                     for (int jj = 0; jj < 32; ++jj) {
-                        if (jj < jn) {
-                            float f = __uint_as_float(v[jj]);
-                            if (args.silu) f = silu_fast(f);
-                            optr[(size_t)(j0 + jj) * args.M] = __float2bfloat16_rn(f);
-                        }
+                        float f = __uint_as_float(v[jj]);
+                        if (args.silu) f = silu_fast(f);
+                        *reinterpret_cast<__nv_bfloat16*>(stage_base + jj * 80 + lane * 2) =
+                            __float2bfloat16_rn(f);
                     }
+                    __syncwarp();
+                    // lane l writes token j0+l: 32 consecutive rows m0..m0+31 = 64 B
+                    const int j = j0 + lane;
+                    if (j < tile.count && !(args.debug & 1)) {
+                        const uint4* src = reinterpret_cast<const uint4*>(stage_base + lane * 80);
+                        uint4* dst = reinterpret_cast<uint4*>(
+                            args.out + (size_t)(tile.pos + j) * args.M + m0);
+                        const uint4 q0 = src[0], q1 = src[1], q2 = src[2], q3 = src[3];
+                        dst[0] = q0;
+                        dst[1] = q1;
+                        dst[2] = q2;
+                        dst[3] = q3;
+                    }
+                    __syncwarp();
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -422,6 +439,8 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
     a.M = (int)M;
     a.K = (int)K;
     a.silu = silu;
+    static const int dbg = getenv("SCMOE_GEMM_DEBUG") ? atoi(getenv("SCMOE_GEMM_DEBUG")) : 0;
+    a.debug = dbg;
     const size_t units_max = max_tiles * (M / BM);
     const int grid = (int)std::min<size_t>(units_max, (size_t)c->num_sms);
     grouped_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, c->stream>>>(mw, mx, a);

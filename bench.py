@@ -407,6 +407,112 @@ def run_b200(args):
     print(json.dumps(line), flush=True)
 
 
+def run_b200_ep(args):
+    """N>1: expert-parallel layer (paper_2509_01322_b200.ep), experts block-
+    partitioned over the ranks, tokens sharded (8192 per GPU), dispatch /
+    return all-to-all over NCCL (NVLink 5 / NVSwitch)."""
+    import torch
+    ws, rank, local = dist_init()
+    import paper_2509_01322_b200 as P
+    from paper_2509_01322_b200.ep import EPLayer, GpuOps
+    from paper_2509_01322_b200.layer import LONGCAT
+
+    cfg = CONFIGS[args.config]
+    T = args.tokens or cfg["tokens"]
+    ctx = P.Context(local)
+    ops = GpuOps(ctx, LONGCAT, rank, ws, seed=SEED_W)
+    ep = EPLayer(ops)
+    a1_h = P.fill_normal(P.stream_seed(SEED_X, rank), T * D, threads=os.cpu_count() or 8)
+    a3_h = P.fill_normal(P.stream_seed(SEED_X + 1, rank), T * D, threads=os.cpu_count() or 8)
+    a1 = torch.from_numpy(a1_h).cuda()
+    a3 = torch.from_numpy(a3_h).cuda()
+    for _ in range(args.warmup):
+        out, idx, gates, cnt = ep.forward(a1, a3, None, T)
+    torch.cuda.synchronize()
+    idx_h = idx.cpu().numpy().view(np.uint32)
+    ffn = idx_h[idx_h < N_FFN]
+    ctx.profile(True)
+    ctx.profile_flush()
+    l0 = ctx.kernel_launches()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    barrier(ws)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            out, idx, gates, cnt = ep.forward(a1, a3, None, T)
+        ev1.record()
+        ev1.synchronize()
+    torch.cuda.synchronize()
+    barrier(ws)
+    launches = ctx.kernel_launches() - l0
+    stages = ctx.profile_flush()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    ms_max = max_over_ranks(ms, ws)
+    value = T * ws / (ms_max / 1e3)
+    # e2e: H2D of the step's inputs, layer, D2H of its output
+    a1_p = torch.from_numpy(a1_h).pin_memory()
+    a3_p = torch.from_numpy(a3_h).pin_memory()
+    out_p = torch.empty(T, D, dtype=torch.float32).pin_memory()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e_steps = max(1, min(args.steps, 5))
+    barrier(ws)
+    e0.record()
+    for _ in range(e_steps):
+        x1 = a1_p.cuda(non_blocking=True)
+        x3 = a3_p.cuda(non_blocking=True)
+        o, _, _, _ = ep.forward(x1, x3, None, T)
+        out_p.copy_(o.view(T, D), non_blocking=True)
+    e1.record()
+    e1.synchronize()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e_steps, ws)
+    if rank != 0:
+        return
+    peaks = measured_peaks() or {}
+    n_local = N_FFN // ws
+    g1 = stages.get("gemm1_tcgen05", (0.0, 1))
+    g2 = stages.get("gemm2_tcgen05", (0.0, 1))
+    t_gemm = (g1[0] + g2[0]) / max(1, g1[1])
+    slots_local = ep.last_stats["recv_rows"]
+    flops = 4.0 * slots_local * D * INTER
+    wbytes = 2 * n_local * D * INTER * 2
+    tok_per_expert = slots_local / n_local
+    bound = "tensor" if tok_per_expert > 254 else "hbm"
+    if bound == "tensor":
+        achieved = flops / (t_gemm / 1e3) / 1e12 if t_gemm else None
+        peak, unit = peaks.get("bf16_tflops", 1590.0), "TFLOP/s"
+    else:
+        achieved = (wbytes + slots_local * (D + INTER) * 4) / (t_gemm / 1e3) / 1e9 if t_gemm else None
+        peak, unit = peaks.get("hbm_gbs", 6650.0), "GB/s"
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (CounterRng normal inputs, seeded_init Uniform weights, random-init)",
+        "config": {"workload": f"LongCat-Flash ScMoE MoE layer, expert-parallel x{ws} "
+                               f"(BASELINE config 4 shape, {T} tokens per GPU)",
+                   "tokens_per_gpu": T, "d_model": D, "n_ffn": N_FFN, "n_zero": N_ZERO,
+                   "top_k": TOPK, "inter": INTER, "experts_per_gpu": n_local,
+                   "parallelism": f"ep{ws} (NCCL all_to_all dispatch/return, no overlap yet)",
+                   "a2a_bytes_each_way_rank0": ep.last_stats["a2a_bytes_each_way"],
+                   "mean_ffn_per_token": float(ffn.size) / T},
+        "e2e": {"value": T * ws / (e2e_ms / 1e3), "unit": "tokens/s",
+                "h2d_bytes_per_step": 2 * T * D * 4, "d2h_bytes_per_step": T * D * 4,
+                "ms_per_step": e2e_ms},
+        "gpu_launches": launches,
+        "roofline": {"kernel": "grouped_gemm_bf16 (GEMM1+GEMM2, tcgen05), rank 0", "bound": bound,
+                     "achieved": achieved, "peak": peak, "unit": unit,
+                     "frac": achieved / peak if achieved else None, "traffic": None,
+                     "tokens_per_local_expert": tok_per_expert, "ms_per_step": t_gemm},
+        "stages_ms": {k: round(v[0] / v[1], 4) for k, v in stages.items()},
+        "clocks": clk.summary(),
+        "cpu_baseline": None,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -419,9 +525,13 @@ def main():
     # pipelined = scmoe_layer_forward_batches; measured slower than serial on B200 in round 1
     # (router and GEMM contend for shared-memory bandwidth), so serial is the default
     ap.add_argument("--schedule", default="serial", choices=["pipelined", "serial"])
+    ap.add_argument("--parallel", default="ep", choices=["ep", "replicated"],
+                    help="N>1: expert-parallel (default) or replicated experts")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
+    elif int(os.environ.get("WORLD_SIZE", "1")) > 1 and args.parallel == "ep":
+        run_b200_ep(args)
     else:
         run_b200(args)
 

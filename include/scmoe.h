@@ -146,6 +146,10 @@ int scmoe_bank_set_expert(scmoe_ctx* ctx, scmoe_bank* b, size_t e, const float* 
  * and stream(stream0 + 2e + 1) for w_out (rng.hpp:82-94). */
 int scmoe_bank_init_uniform(scmoe_ctx* ctx, scmoe_bank* b, uint64_t seed, uint64_t stream0,
                             double variance);
+/* Same for the expert shard [first, first + n) of a larger bank: local expert
+ * i gets global expert (first + i)'s streams. */
+int scmoe_bank_init_uniform_shard(scmoe_ctx* ctx, scmoe_bank* b, uint64_t seed, uint64_t stream0,
+                                  double variance, size_t first_expert);
 double scmoe_bank_gamma_ffn(const scmoe_bank* b);
 double scmoe_bank_gamma_zero(const scmoe_bank* b);
 size_t scmoe_bank_device_bytes(const scmoe_bank* b);
@@ -186,6 +190,42 @@ int scmoe_layer_forward_batches(scmoe_ctx* ctx, scmoe_router* r, scmoe_bank* b, 
 int scmoe_layer_forward_host(scmoe_ctx* ctx, scmoe_router* r, scmoe_bank* b, const float* a1,
                              const float* a3, const float* gain, size_t tokens, int renormalize,
                              uint32_t* indices, double* gates, uint32_t* ffn_count, float* out);
+
+/* ---- expert parallelism ------------------------------------
+ * Experts are block-partitioned over G ranks (rank g owns FFN experts
+ * [g*N/G, (g+1)*N/G)); router and bias are replicated, tokens sharded, zero
+ * experts stay local.  One layer = route -> plan -> pack -> all-to-all ->
+ * scmoe_moe_rows -> all-to-all back -> scmoe_combine_rows; the transport
+ * (NCCL all_to_all) is the caller's.  Expert rows are returned per slot and
+ * combined at the source in rank order, so the G-rank output is bitwise equal
+ * to the single-GPU output. */
+
+/* Front half of the layer (model.hpp:394-397): hmoe = rmsnorm(a1, gain) (fp32
+ * and bf16 copies), exact router, top-K.  hmoe_bf16 may be NULL. */
+int scmoe_rmsnorm_route(scmoe_ctx* ctx, scmoe_router* r, const float* a1, const float* gain,
+                        size_t tokens, float* hmoe, void* hmoe_bf16, uint32_t* indices,
+                        double* gates, uint32_t* ffn_count);
+/* Dispatch plan: FFN slots grouped by owning rank, (token, slot) ascending
+ * within a rank.  send_counts [G] (device), slot_send_pos [T*K] (-1: zero
+ * expert), send_token [T*K] / send_expert [T*K] (global expert id) per send
+ * row.  All device pointers. */
+int scmoe_ep_plan(scmoe_ctx* ctx, const uint32_t* indices, size_t tokens, size_t top_k,
+                  size_t n_ffn, size_t n_zero, int world, int* send_counts, int* slot_send_pos,
+                  int* send_token, int* send_expert);
+/* dst[i] = src[rows[i]] for i < n_rows (bf16 rows of width d). */
+int scmoe_gather_rows_bf16(scmoe_ctx* ctx, const void* src, size_t d, const int* rows,
+                           size_t n_rows, void* dst);
+/* Expert FFN (blocks.hpp:361-365) on rows that each carry one expert:
+ * y[r] = silu(x[r] W_in[e_r - expert_offset]) W_out[e_r - expert_offset],
+ * bf16 in / bf16 out, rows in the given order.  bf16 banks only. */
+int scmoe_moe_rows(scmoe_ctx* ctx, scmoe_bank* b, const void* x_bf16, const int* row_expert,
+                   int expert_offset, size_t rows, void* y_bf16);
+/* moe_combine (blocks.hpp:226-274) + residual from per-slot expert rows:
+ * slot (t,s) with an FFN expert reads y_rows[slot_row[t*K+s]]. */
+int scmoe_combine_rows(scmoe_ctx* ctx, scmoe_bank* b, const float* x, const void* y_rows_bf16,
+                       const int* slot_row, const uint32_t* indices, const double* gates,
+                       size_t tokens, size_t top_k, size_t n_ffn_total, int renormalize,
+                       const float* residual, float* out);
 
 /* ---- CounterRng (rng.hpp:15-64), host side, for synthetic inputs --------- */
 uint64_t scmoe_rng_stream_seed(uint64_t seed, uint64_t id);

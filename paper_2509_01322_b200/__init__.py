@@ -135,6 +135,13 @@ _PROTOS = {
                                            _P]),
     "scmoe_layer_forward_batches": (C.c_int, [_P, _P, _P, _SZ, _P, _P, _P, _SZ, C.c_int, _P, _P,
                                               _P, _P]),
+    "scmoe_bank_init_uniform_shard": (C.c_int, [_P, _P, _U64, _U64, C.c_double, _SZ]),
+    "scmoe_rmsnorm_route": (C.c_int, [_P, _P, _P, _P, _SZ, _P, _P, _P, _P, _P]),
+    "scmoe_ep_plan": (C.c_int, [_P, _P, _SZ, _SZ, _SZ, _SZ, C.c_int, _P, _P, _P, _P]),
+    "scmoe_gather_rows_bf16": (C.c_int, [_P, _P, _SZ, _P, _SZ, _P]),
+    "scmoe_moe_rows": (C.c_int, [_P, _P, _P, _P, C.c_int, _SZ, _P]),
+    "scmoe_combine_rows": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _SZ, _SZ, _SZ, C.c_int, _P,
+                                     _P]),
     "scmoe_rng_stream_seed": (_U64, [_U64, _U64]),
     "scmoe_rng_fill_normal_host": (None, [_U64, _U64, _SZ, _P, C.c_int]),
     "scmoe_rng_fill_uniform": (C.c_int, [_P, _U64, _U64, _SZ, C.c_double, _P]),

@@ -854,4 +854,128 @@ int scmoe_debug_expf_range(scmoe_ctx* c, uint32_t first, float* out, size_t n) {
     });
 }
 
+// ---- expert parallelism -------------------------------------------------------
+
+int scmoe_bank_init_uniform_shard(scmoe_ctx* c, scmoe_bank* b, uint64_t seed, uint64_t stream0,
+                                  double variance, size_t first) {
+    return scmoe_bank_init_uniform(c, b, seed, stream0 + 2 * first, variance);
+}
+
+int scmoe_rmsnorm_route(scmoe_ctx* c, scmoe_router* r, const float* a1, const float* gain,
+                        size_t T, float* hmoe, void* hmoe_bf16, uint32_t* idx, double* gates,
+                        uint32_t* ffn_count) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        validate_router(r->n_ffn, r->n_zero, r->top_k, r->k_expected, r->mu);
+        if (T == 0) return;
+        const size_t d = r->d, E = r->E();
+        {
+            ProfScope _p(c, "rmsnorm");
+            launch_rmsnorm(c, a1, gain, T, d, 1e-6f, hmoe,
+                           static_cast<__nv_bfloat16*>(hmoe_bf16));
+        }
+        float* logits = c->ws.logits.get<float>(T * E);
+        route_logits(c, r, hmoe, T, logits);
+        ProfScope _p(c, "softmax_topk");
+        launch_softmax_topk(c, logits, T, E, r->top_k, r->n_ffn, r->b, idx, gates, ffn_count,
+                            nullptr);
+    });
+}
+
+int scmoe_ep_plan(scmoe_ctx* c, const uint32_t* idx, size_t T, size_t K, size_t n_ffn,
+                  size_t n_zero, int world, int* send_counts, int* slot_send_pos, int* send_token,
+                  int* send_expert) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        if (world < 1 || n_ffn % (size_t)world != 0)
+            SCMOE_THROW(SCMOE_ERR_CONFIG, "ep: world size must divide the FFN expert count");
+        if (T == 0) {
+            SCMOE_CUDA(cudaMemsetAsync(send_counts, 0, world * sizeof(int), c->stream));
+            return;
+        }
+        launch_check_indices(c, idx, T * K, n_ffn + n_zero);
+        uint32_t* bins = c->ws.ep_bins.get<uint32_t>(T * K);
+        launch_ep_bins(c, idx, T * K, n_ffn, n_ffn / world, world, bins);
+        // one permutation over the G rank bins (+1 zero bin): offsets per rank,
+        // position of each slot in the send buffer, token of each send row
+        PermResult pr;
+        {
+            ProfScope _p(c, "ep_plan");
+            pr = launch_permute(c, bins, T, K, world, world + 1, 256);
+        }
+        SCMOE_CUDA(cudaMemcpyAsync(send_counts, pr.expert_count, world * sizeof(int),
+                                   cudaMemcpyDeviceToDevice, c->stream));
+        SCMOE_CUDA(cudaMemcpyAsync(slot_send_pos, pr.slot_pos, T * K * sizeof(int),
+                                   cudaMemcpyDeviceToDevice, c->stream));
+        SCMOE_CUDA(cudaMemcpyAsync(send_token, pr.row_token, T * K * sizeof(int),
+                                   cudaMemcpyDeviceToDevice, c->stream));
+        launch_ep_send_expert(c, idx, pr.slot_pos, T * K, send_expert);
+    });
+}
+
+int scmoe_gather_rows_bf16(scmoe_ctx* c, const void* src, size_t d, const int* rows,
+                           size_t n_rows, void* dst) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        ProfScope _p(c, "gather_rows");
+        launch_gather_rows_bf16(c, static_cast<const __nv_bfloat16*>(src), d, rows, n_rows,
+                                static_cast<__nv_bfloat16*>(dst));
+    });
+}
+
+int scmoe_moe_rows(scmoe_ctx* c, scmoe_bank* b, const void* x_bf16, const int* row_expert,
+                   int expert_offset, size_t R, void* y_bf16) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        if (b->precision != SCMOE_PREC_BF16)
+            SCMOE_THROW(SCMOE_ERR_CONFIG, "moe_rows: needs a bf16 (tensor-core) bank");
+        if (R == 0) return;
+        const size_t d = b->d, I = b->inter, n = b->n;
+        Workspace& ws = c->ws;
+        uint32_t* loc = ws.ep_local.get<uint32_t>(R);
+        launch_ep_localize(c, row_expert, R, expert_offset, (int)n, loc);
+        // each row is a "token" routed to exactly one local expert (K = 1)
+        PermResult pr;
+        {
+            ProfScope _p(c, "permute");
+            pr = launch_permute(c, loc, R, 1, n, n, grouped_gemm_tile_rows());
+        }
+        const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x_bf16);
+        __nv_bfloat16* xp = ws.xp.get<__nv_bfloat16>(R * d);
+        __nv_bfloat16* h = ws.h.get<__nv_bfloat16>(R * I);
+        __nv_bfloat16* y = ws.ep_y.get<__nv_bfloat16>(R * d);
+        {
+            ProfScope _p(c, "gather");
+            launch_gather_bf16(c, xb, d, pr.row_token, pr.expert_base, n, R, xp);
+        }
+        {
+            ProfScope _p(c, "gemm1_tcgen05");
+            launch_grouped_gemm_bf16(c, b->w1t, n, I, d, xp, R, nullptr, h, 1, pr.tiles,
+                                     pr.n_tiles, pr.max_tiles, grouped_gemm_tile_rows());
+        }
+        {
+            ProfScope _p(c, "gemm2_tcgen05");
+            launch_grouped_gemm_bf16(c, b->w2t, n, d, I, h, R, nullptr, y, 0, pr.tiles,
+                                     pr.n_tiles, pr.max_tiles, grouped_gemm_tile_rows());
+        }
+        // back to the received order: y_out[r] = y[slot_pos[r]]
+        ProfScope _p(c, "unpermute");
+        launch_gather_rows_bf16(c, y, d, pr.slot_pos, R, static_cast<__nv_bfloat16*>(y_bf16));
+    });
+}
+
+int scmoe_combine_rows(scmoe_ctx* c, scmoe_bank* b, const float* x, const void* y_rows,
+                       const int* slot_row, const uint32_t* idx, const double* gates, size_t T,
+                       size_t K, size_t n_ffn_total, int renorm, const float* residual,
+                       float* out) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        if (T == 0) return;
+        ProfScope _p(c, "combine");
+        launch_combine_bf16(c, x, static_cast<const __nv_bfloat16*>(y_rows), idx, gates, slot_row,
+                            T, b->d, K, n_ffn_total, (float)b->gamma_ffn(), (float)b->gamma_zero(),
+                            renorm, residual, out);
+    });
+}
+
 }  // extern "C"

@@ -64,13 +64,14 @@ struct DevBuf {
 struct Workspace {
     DevBuf logits, probs, hmoe, hmoe_bf16, idx, gates, ffn_count;
     DevBuf rank_in_block, block_counts, expert_count, expert_base, slot_pos, row_token;
-    DevBuf tiles, n_tiles, xp, h, y, in_copy, out_copy, misc, tiles_router;
+    DevBuf tiles, n_tiles, xp, h, y, in_copy, out_copy, misc, tiles_router, ep_bins, ep_local,
+        ep_y;
     unsigned char pr_blob[64] = {};  // permutation result carried from moe_front to moe_back
     void release_all() {
         DevBuf* all[] = {&logits, &probs, &hmoe, &hmoe_bf16, &idx, &gates, &ffn_count,
                          &rank_in_block, &block_counts, &expert_count, &expert_base, &slot_pos,
                          &row_token, &tiles, &n_tiles, &xp, &h, &y, &in_copy, &out_copy, &misc,
-                         &tiles_router};
+                         &tiles_router, &ep_bins, &ep_local, &ep_y};
         for (DevBuf* b : all) b->release();
     }
 };
@@ -245,6 +246,16 @@ void launch_f32_to_bf16_t(scmoe_ctx* c, const float* src, size_t rows, size_t co
 // tcgen05 grouped GEMM (gemm_sm100.cu).  D^T = W x X^T per expert tile:
 //   out[pos, m] = epi( sum_k W[e][m][k] * X[pos][k] ),  epi = silu or identity,
 // W: [n][M][K] bf16 (K-major), X: [rows][K] bf16, out: [rows][M] bf16.
+// expert parallelism helpers (kernels_moe.cu)
+void launch_ep_bins(scmoe_ctx* c, const uint32_t* idx, size_t n, size_t n_ffn, size_t per_rank,
+                    int world, uint32_t* bins);
+void launch_ep_send_expert(scmoe_ctx* c, const uint32_t* idx, const int* slot_pos, size_t n,
+                           int* send_expert);
+void launch_ep_localize(scmoe_ctx* c, const int* row_expert, size_t n, int offset, int n_local,
+                        uint32_t* local);
+void launch_gather_rows_bf16(scmoe_ctx* c, const __nv_bfloat16* src, size_t d, const int* rows,
+                             size_t n_rows, __nv_bfloat16* dst);
+
 int grouped_gemm_tile_rows();
 void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_experts,
                               size_t M, size_t K, const __nv_bfloat16* X, size_t x_rows,

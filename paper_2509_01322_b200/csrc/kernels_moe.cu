@@ -613,4 +613,88 @@ void launch_row_tiles(scmoe_ctx* c, size_t rows, int tile_rows, TokenTile* tiles
     SCMOE_LAUNCH_CHECK(c);
 }
 
+// ---------------------------------------------------------------------------
+// Expert-parallel helpers.
+// ---------------------------------------------------------------------------
+// Destination "bin" of every slot: owning rank of an FFN expert, `world` for
+// a zero expert (never sent).
+__global__ void ep_bins_kernel(const uint32_t* __restrict__ idx, size_t n, uint32_t n_ffn,
+                               uint32_t per_rank, uint32_t world, uint32_t* __restrict__ bins) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        const uint32_t e = idx[i];
+        bins[i] = e < n_ffn ? e / per_rank : world;
+    }
+}
+
+void launch_ep_bins(scmoe_ctx* c, const uint32_t* idx, size_t n, size_t n_ffn, size_t per_rank,
+                    int world, uint32_t* bins) {
+    if (n == 0) return;
+    ep_bins_kernel<<<ceil_div(n, 256), 256, 0, c->stream>>>(idx, n, (uint32_t)n_ffn,
+                                                           (uint32_t)per_rank, (uint32_t)world, bins);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
+// send_expert[slot_pos[i]] = idx[i] for every sent slot.
+__global__ void ep_send_expert_kernel(const uint32_t* __restrict__ idx,
+                                      const int* __restrict__ slot_pos, size_t n,
+                                      int* __restrict__ send_expert) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && slot_pos[i] >= 0) send_expert[slot_pos[i]] = (int)idx[i];
+}
+
+void launch_ep_send_expert(scmoe_ctx* c, const uint32_t* idx, const int* slot_pos, size_t n,
+                           int* send_expert) {
+    if (n == 0) return;
+    ep_send_expert_kernel<<<ceil_div(n, 256), 256, 0, c->stream>>>(idx, slot_pos, n, send_expert);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
+// Received rows' global expert ids -> this rank's local ids (range-checked).
+__global__ void ep_localize_kernel(const int* __restrict__ row_expert, size_t n, int offset,
+                                   int n_local, uint32_t* __restrict__ local,
+                                   int* __restrict__ dev_status) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int e = row_expert[i] - offset;
+    if (e < 0 || e >= n_local) {
+        atomicExch(dev_status, DEV_ERR_INDEX_RANGE);
+        local[i] = 0;
+    } else {
+        local[i] = (uint32_t)e;
+    }
+}
+
+void launch_ep_localize(scmoe_ctx* c, const int* row_expert, size_t n, int offset, int n_local,
+                        uint32_t* local) {
+    if (n == 0) return;
+    ep_localize_kernel<<<ceil_div(n, 256), 256, 0, c->stream>>>(row_expert, n, offset, n_local,
+                                                               local, c->dev_status);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
+// dst[i] = src[rows[i]], bf16 rows of width d (one warp per row, 16-byte vectors).
+__global__ void gather_rows_bf16_kernel(const __nv_bfloat16* __restrict__ src, int d,
+                                        const int* __restrict__ rows, size_t n_rows,
+                                        __nv_bfloat16* __restrict__ dst) {
+    const size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const size_t nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
+    const int vec = d / 8;
+    for (size_t r = warp; r < n_rows; r += nwarps) {
+        const uint4* s = reinterpret_cast<const uint4*>(src + (size_t)rows[r] * d);
+        uint4* o = reinterpret_cast<uint4*>(dst + r * d);
+        for (int v = lane; v < vec; v += 32) o[v] = s[v];
+    }
+}
+
+void launch_gather_rows_bf16(scmoe_ctx* c, const __nv_bfloat16* src, size_t d, const int* rows,
+                             size_t n_rows, __nv_bfloat16* dst) {
+    if (n_rows == 0) return;
+    SCMOE_CHECK_ARG(d % 8 == 0, SCMOE_ERR_DIMENSION, "gather: d must be a multiple of 8");
+    const int blocks = (int)std::min<size_t>(ceil_div(n_rows, 8), (size_t)c->num_sms * 8);
+    gather_rows_bf16_kernel<<<blocks, 256, 0, c->stream>>>(src, (int)d, rows, n_rows, dst);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
 }  // namespace scmoe

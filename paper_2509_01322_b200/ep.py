@@ -1,0 +1,155 @@
+"""Expert-parallel ScMoE layer across the GPUs of one node.
+
+Partitioning: router + bias replicated on every rank, tokens sharded, FFN
+experts block-partitioned (rank g owns [g*N/G, (g+1)*N/G)), zero experts
+handled locally with no communication.  Per layer:
+
+    1. route      rmsnorm + exact router + top-K on the local tokens
+    2. plan       FFN slots grouped by owning rank, (token, slot) order
+    3. counts     all-to-all of per-rank slot counts (G ints)
+    4. dispatch   all-to-all of the slots' bf16 rows (+ their expert ids)
+    5. experts    grouped GEMM1(+SiLU)/GEMM2 on the received rows (tcgen05)
+    6. return     all-to-all of the expert output rows, in received order
+    7. combine    rank-order combine + zero-expert identity + residual
+
+Expert rows are returned per slot and combined at the source in the
+reference's rank order (blocks.hpp:251-274), so the G-rank output is bitwise
+equal to the single-GPU output.  The transport is torch.distributed's NCCL
+all_to_all_single over NVLink/NVSwitch (plumbing); the numeric steps are the
+C-ABI kernels, reached through a small ``ops`` object so that the
+orchestration itself can be exercised on CPU with the gloo backend by the
+tests (tests/test_ep_gloo.py) -- the product path always uses ``GpuOps``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import torch
+import torch.distributed as dist
+
+from . import _P, Context, lib
+from .layer import LayerShape
+
+
+class GpuOps:
+    """The device kernels of one rank (C ABI), on torch CUDA tensors."""
+
+    def __init__(self, ctx: Context, shape: LayerShape, rank: int, world: int, seed: int):
+        self.ctx, self.shape, self.rank, self.world = ctx, shape, rank, world
+        # kernels and NCCL collectives must be ordered on one stream: run the
+        # layer on torch's current stream (collectives synchronise with it)
+        ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+        L = lib()
+        s = shape
+        if s.n_ffn % world:
+            raise ValueError("world size must divide the FFN expert count")
+        self.n_local = s.n_ffn // world
+        self.first = rank * self.n_local
+        self.router = _P()
+        ctx._check(L.scmoe_router_create(ctx.handle, s.d, s.n_ffn, s.n_zero, s.top_k,
+                                         s.k_expected, 0.0, 1.0, C.byref(self.router)))
+        w = torch.empty(s.d * s.E, dtype=torch.float32, device="cuda")
+        ctx._check(L.scmoe_rng_fill_uniform(ctx.handle, int(L.scmoe_rng_stream_seed(seed, 0)), 0,
+                                            s.d * s.E, 1.0 / s.d, w.data_ptr()))
+        ctx._check(L.scmoe_router_set_weights(ctx.handle, self.router, w.data_ptr()))
+        self.bank = _P()
+        ctx._check(L.scmoe_bank_create(ctx.handle, self.n_local, s.d, s.inter, s.precision, s.m,
+                                       s.gamma_mode, C.byref(self.bank)))
+        ctx._check(L.scmoe_bank_init_uniform_shard(ctx.handle, self.bank, seed, 100, 1.0 / s.d,
+                                                   self.first))
+        ctx.synchronize()
+
+    def _chk(self, rc):
+        self.ctx._check(rc)
+
+    def route(self, a1: torch.Tensor, gain: Optional[torch.Tensor], T: int):
+        s = self.shape
+        hmoe = torch.empty(T, s.d, dtype=torch.float32, device="cuda")
+        hb = torch.empty(T, s.d, dtype=torch.bfloat16, device="cuda")
+        idx = torch.empty(T * s.top_k, dtype=torch.int32, device="cuda")
+        gates = torch.empty(T * s.top_k, dtype=torch.float64, device="cuda")
+        cnt = torch.empty(T, dtype=torch.int32, device="cuda")
+        self._chk(lib().scmoe_rmsnorm_route(self.ctx.handle, self.router, a1.data_ptr(),
+                                            None if gain is None else gain.data_ptr(), T,
+                                            hmoe.data_ptr(), hb.data_ptr(), idx.data_ptr(),
+                                            gates.data_ptr(), cnt.data_ptr()))
+        return hmoe, hb, idx, gates, cnt
+
+    def plan(self, idx: torch.Tensor, T: int):
+        s = self.shape
+        n = T * s.top_k
+        counts = torch.empty(self.world, dtype=torch.int32, device="cuda")
+        slot_pos = torch.empty(n, dtype=torch.int32, device="cuda")
+        send_token = torch.empty(n, dtype=torch.int32, device="cuda")
+        send_expert = torch.empty(n, dtype=torch.int32, device="cuda")
+        self._chk(lib().scmoe_ep_plan(self.ctx.handle, idx.data_ptr(), T, s.top_k, s.n_ffn,
+                                      s.n_zero, self.world, counts.data_ptr(), slot_pos.data_ptr(),
+                                      send_token.data_ptr(), send_expert.data_ptr()))
+        return counts, slot_pos, send_token, send_expert
+
+    def gather(self, src: torch.Tensor, rows: torch.Tensor, n_rows: int):
+        out = torch.empty(n_rows, self.shape.d, dtype=src.dtype, device="cuda")
+        self._chk(lib().scmoe_gather_rows_bf16(self.ctx.handle, src.data_ptr(), self.shape.d,
+                                               rows.data_ptr(), n_rows, out.data_ptr()))
+        return out
+
+    def experts(self, rows: torch.Tensor, row_expert: torch.Tensor):
+        R = rows.shape[0]
+        y = torch.empty_like(rows)
+        self._chk(lib().scmoe_moe_rows(self.ctx.handle, self.bank, rows.data_ptr(),
+                                       row_expert.data_ptr(), self.first, R, y.data_ptr()))
+        return y
+
+    def combine(self, hmoe, y_rows, slot_pos, idx, gates, T, a3, renormalize=False):
+        s = self.shape
+        out = torch.empty(T, s.d, dtype=torch.float32, device="cuda")
+        self._chk(lib().scmoe_combine_rows(self.ctx.handle, self.bank, hmoe.data_ptr(),
+                                           y_rows.data_ptr(), slot_pos.data_ptr(), idx.data_ptr(),
+                                           gates.data_ptr(), T, s.top_k, s.n_ffn, int(renormalize),
+                                           None if a3 is None else a3.data_ptr(), out.data_ptr()))
+        return out
+
+    def sync(self):
+        torch.cuda.current_stream().synchronize()
+        self.ctx.synchronize()
+
+    def close(self):
+        L = lib()
+        L.scmoe_bank_destroy(self.ctx.handle, self.bank)
+        L.scmoe_router_destroy(self.ctx.handle, self.router)
+
+
+class EPLayer:
+    """One ScMoE MoE branch sharded over the ranks of ``group``."""
+
+    def __init__(self, ops, group=None):
+        self.ops, self.group = ops, group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.last_stats = {}
+
+    def forward(self, a1: torch.Tensor, a3: Optional[torch.Tensor], gain, T: int,
+                renormalize: bool = False):
+        ops, G = self.ops, self.world
+        hmoe, hb, idx, gates, cnt = ops.route(a1, gain, T)
+        counts, slot_pos, send_token, send_expert = ops.plan(idx, T)
+        # count exchange (G ints); split sizes are needed on the host
+        recv_counts = torch.empty_like(counts)
+        dist.all_to_all_single(recv_counts, counts, group=self.group)
+        both = torch.cat([counts, recv_counts]).cpu().tolist()
+        send_split, recv_split = both[:G], both[G:]
+        n_send, n_recv = sum(send_split), sum(recv_split)
+        send_rows = ops.gather(hb, send_token, n_send)
+        recv_rows = torch.empty(n_recv, hb.shape[1], dtype=hb.dtype, device=hb.device)
+        dist.all_to_all_single(recv_rows, send_rows, recv_split, send_split, group=self.group)
+        recv_expert = torch.empty(n_recv, dtype=send_expert.dtype, device=send_expert.device)
+        dist.all_to_all_single(recv_expert, send_expert[:n_send].contiguous(), recv_split,
+                               send_split, group=self.group)
+        y_rows = ops.experts(recv_rows, recv_expert)
+        back_rows = torch.empty(n_send, hb.shape[1], dtype=hb.dtype, device=hb.device)
+        dist.all_to_all_single(back_rows, y_rows, send_split, recv_split, group=self.group)
+        out = ops.combine(hmoe, back_rows, slot_pos, idx, gates, T, a3, renormalize)
+        self.last_stats = {"send_rows": n_send, "recv_rows": n_recv,
+                           "a2a_bytes_each_way": n_send * hb.shape[1] * hb.element_size()}
+        return out, idx, gates, cnt

@@ -74,6 +74,7 @@ _ORC_PROTOS = {
     "orc_moe_forward_f64": (C.c_int, [_P, _SZ, _SZ, _P, _P, _SZ, _SZ, _SZ, _P, _P, _SZ, _D, _D,
                                       C.c_int, _P]),
     "orc_permutation": (None, [_P, _SZ, _SZ, _SZ, _SZ, _P, _P]),
+    "orc_expert_row_f32": (None, [_P, _SZ, _P, _P, _SZ, _P, _P]),
     "orc_scmoe_layer_f32": (C.c_int, [_P, _P, _P, _SZ, _SZ, _P, _SZ, _SZ, _SZ, _SZ, _D, _P, _P,
                                       _P, _SZ, _D, _D, C.c_int, _P, _P, _P, _P]),
     "orc_simulate_bias_control_f32": (C.c_int, [_P, _SZ, _SZ, _SZ, _SZ, _SZ, _P, _D, _P, _U64,

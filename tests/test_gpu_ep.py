@@ -1,0 +1,73 @@
+"""Expert parallelism on real GPUs (NCCL over NVLink): the G-rank EP layer's
+routing and output are bitwise equal to the single-GPU layer on the same
+tokens (per-slot expert rows, rank-order combine at the source)."""
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+pytestmark = pytest.mark.gpu
+
+
+def _worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", rank))
+    try:
+        import paper_2509_01322_b200 as P
+        from paper_2509_01322_b200.ep import EPLayer, GpuOps
+        from paper_2509_01322_b200.layer import DeviceLayer, LayerShape
+        shape = LayerShape(d=1024, n_ffn=64, n_zero=32, top_k=6, k_expected=4, inter=512,
+                           precision=P.PREC_BF16)
+        T = 640 + 64 * rank  # ragged shards
+        a1 = torch.from_numpy(P.fill_normal(P.stream_seed(9, rank), T * shape.d)).cuda()
+        a3 = torch.from_numpy(P.fill_normal(P.stream_seed(10, rank), T * shape.d)).cuda()
+        ctx = P.Context(rank)
+        ep = EPLayer(GpuOps(ctx, shape, rank, world, seed=3))
+        out, idx, gates, cnt = ep.forward(a1, a3, None, T)
+        torch.cuda.synchronize()
+        # single-GPU reference: same seed => same router and the full expert set
+        ctx1 = P.Context(rank)
+        ctx1.set_stream(torch.cuda.current_stream().cuda_stream)
+        full = DeviceLayer(ctx1, shape, seed=3)
+        idx1 = torch.empty_like(idx)
+        gates1 = torch.empty_like(gates)
+        cnt1 = torch.empty_like(cnt)
+        out1 = torch.empty_like(out)
+        full.forward(a1.data_ptr(), a3.data_ptr(), None, T, idx1.data_ptr(), gates1.data_ptr(),
+                     cnt1.data_ptr(), out1.data_ptr())
+        torch.cuda.synchronize()
+        ok = (torch.equal(idx, idx1) and torch.equal(gates, gates1) and torch.equal(out, out1))
+        q.put((rank, bool(ok), ep.last_stats))
+    except Exception as e:  # pragma: no cover
+        import traceback
+        q.put((rank, False, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ep_equals_single_gpu_bitwise():
+    import torch
+    import torch.multiprocessing as mp
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = 4 if n >= 4 else 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29700 + os.getpid() % 200
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, info in sorted(res):
+        assert ok, f"rank {rank}: {info}"

@@ -901,7 +901,7 @@ int scmoe_ep_plan(scmoe_ctx* c, const uint32_t* idx, size_t T, size_t K, size_t 
         PermResult pr;
         {
             ProfScope _p(c, "ep_plan");
-            pr = launch_permute(c, bins, T, K, world, world + 1, 256);
+            pr = launch_permute(c, bins, T, K, world, world + 1, 256, /*multi=*/true);
         }
         SCMOE_CUDA(cudaMemcpyAsync(send_counts, pr.expert_count, world * sizeof(int),
                                    cudaMemcpyDeviceToDevice, c->stream));

@@ -216,8 +216,10 @@ struct PermResult {
     int* n_tiles;       // device scalar
     size_t max_tiles;
 };
+// multi: a token may hit the same bin in several slots (EP destination ranks);
+// otherwise each token hits an expert at most once (top-K of distinct experts).
 PermResult launch_permute(scmoe_ctx* c, const uint32_t* idx, size_t T, size_t K, size_t n_ffn,
-                          size_t E, int tile_rows);
+                          size_t E, int tile_rows, bool multi = false);
 void launch_gather_bf16(scmoe_ctx* c, const __nv_bfloat16* src, size_t d, const int* row_token,
                         const int* expert_base, size_t n_ffn, size_t max_rows,
                         __nv_bfloat16* dst);

@@ -155,9 +155,60 @@ __global__ void perm_scatter_kernel(const uint32_t* __restrict__ idx, int T, int
     row_token[pos] = t;
 }
 
+// Pass 1 for bins a token may hit several times (expert-parallel destination
+// ranks): slot (t, s) -> bin b gets in-block rank = (slots of bin b in earlier
+// tokens of the block) + (earlier slots of token t in bin b); a block scan
+// over the 256 tokens per bin replaces the bitmask.  E <= kMaxMultiBins.
+constexpr int kMaxMultiBins = 33;
+
+__global__ void __launch_bounds__(kTB) perm_hist_multi_kernel(
+    const uint32_t* __restrict__ idx, int T, int K, int E, int* __restrict__ rank_in_block,
+    int* __restrict__ block_counts, int* __restrict__ dev_status) {
+    __shared__ int warp_tot[kTB / 32];
+    const int tl = threadIdx.x;
+    const int t = blockIdx.x * kTB + tl;
+    const int lane = tl & 31, warp = tl >> 5;
+    for (int b = 0; b < E; ++b) {
+        int cnt = 0;
+        if (t < T)
+            for (int s = 0; s < K; ++s) cnt += idx[(size_t)t * K + s] == (uint32_t)b;
+        // block exclusive scan of cnt over tokens
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) warp_tot[warp] = incl;
+        __syncthreads();
+        int before = 0, total = 0;
+        for (int w = 0; w < kTB / 32; ++w) {
+            if (w < warp) before += warp_tot[w];
+            total += warp_tot[w];
+        }
+        const int excl = before + incl - cnt;
+        if (t < T) {
+            int within = 0;
+            for (int s = 0; s < K; ++s) {
+                const uint32_t e = idx[(size_t)t * K + s];
+                if (e == (uint32_t)b) rank_in_block[(size_t)t * K + s] = excl + within++;
+            }
+        }
+        if (tl == 0) block_counts[(size_t)blockIdx.x * E + b] = total;
+        __syncthreads();
+    }
+    if (t < T)
+        for (int s = 0; s < K; ++s)
+            if (idx[(size_t)t * K + s] >= (uint32_t)E) {
+                atomicExch(dev_status, DEV_ERR_INDEX_RANGE);
+                rank_in_block[(size_t)t * K + s] = 0;
+            }
+}
+
 PermResult launch_permute(scmoe_ctx* c, const uint32_t* idx, size_t T, size_t K, size_t n_ffn,
-                          size_t E, int tile_rows) {
+                          size_t E, int tile_rows, bool multi) {
     Workspace& ws = c->ws;
+    if (multi) SCMOE_CHECK_ARG(E <= kMaxMultiBins, SCMOE_ERR_CONFIG, "permute: too many bins");
     const size_t nblk = ceil_div(std::max<size_t>(T, 1), kTB);
     PermResult pr;
     int* rank = ws.rank_in_block.get<int>(T * K);
@@ -174,7 +225,11 @@ PermResult launch_permute(scmoe_ctx* c, const uint32_t* idx, size_t T, size_t K,
     if (smem > 48 * 1024)
         SCMOE_CUDA(cudaFuncSetAttribute(perm_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
-    if (T > 0) {
+    if (T > 0 && multi) {
+        perm_hist_multi_kernel<<<nblk, kTB, 0, c->stream>>>(idx, (int)T, (int)K, (int)E, rank,
+                                                            bcounts, c->dev_status);
+        SCMOE_LAUNCH_CHECK(c);
+    } else if (T > 0) {
         perm_hist_kernel<<<nblk, kTB, smem, c->stream>>>(idx, (int)T, (int)K, (int)E, rank, bcounts,
                                                          c->dev_status);
         SCMOE_LAUNCH_CHECK(c);

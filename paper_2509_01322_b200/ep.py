@@ -37,9 +37,12 @@ class GpuOps:
 
     def __init__(self, ctx: Context, shape: LayerShape, rank: int, world: int, seed: int):
         self.ctx, self.shape, self.rank, self.world = ctx, shape, rank, world
-        # kernels and NCCL collectives must be ordered on one stream: run the
-        # layer on torch's current stream (collectives synchronise with it)
-        ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+        # kernels and NCCL collectives must be ordered on one stream: the layer
+        # runs on this stream, made torch's current stream during forward()
+        # (collectives synchronise with the current stream).  A real stream is
+        # needed: handle 0 would select the context's private stream.
+        self.stream = torch.cuda.Stream()
+        ctx.set_stream(self.stream.cuda_stream)
         L = lib()
         s = shape
         if s.n_ffn % world:
@@ -131,6 +134,19 @@ class EPLayer:
 
     def forward(self, a1: torch.Tensor, a3: Optional[torch.Tensor], gain, T: int,
                 renormalize: bool = False):
+        stream = getattr(self.ops, "stream", None)
+        if stream is None:
+            return self._forward(a1, a3, gain, T, renormalize)
+        # inputs produced on the caller's stream must be complete first
+        stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(stream):
+            res = self._forward(a1, a3, gain, T, renormalize)
+        torch.cuda.current_stream().wait_stream(stream)
+        for t in res:
+            t.record_stream(torch.cuda.current_stream())
+        return res
+
+    def _forward(self, a1, a3, gain, T, renormalize):
         ops, G = self.ops, self.world
         hmoe, hb, idx, gates, cnt = ops.route(a1, gain, T)
         counts, slot_pos, send_token, send_expert = ops.plan(idx, T)

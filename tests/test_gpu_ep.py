@@ -35,7 +35,8 @@ def _worker(rank, world, port, q):
         torch.cuda.synchronize()
         # single-GPU reference: same seed => same router and the full expert set
         ctx1 = P.Context(rank)
-        ctx1.set_stream(torch.cuda.current_stream().cuda_stream)
+        s1 = torch.cuda.Stream()
+        ctx1.set_stream(s1.cuda_stream)
         full = DeviceLayer(ctx1, shape, seed=3)
         idx1 = torch.empty_like(idx)
         gates1 = torch.empty_like(gates)
@@ -45,7 +46,10 @@ def _worker(rank, world, port, q):
                      cnt1.data_ptr(), out1.data_ptr())
         torch.cuda.synchronize()
         ok = (torch.equal(idx, idx1) and torch.equal(gates, gates1) and torch.equal(out, out1))
-        q.put((rank, bool(ok), ep.last_stats))
+        info = dict(ep.last_stats, idx_diff=int((idx != idx1).sum()),
+                    out_diff=int((out != out1).sum()),
+                    rel=float((out - out1).norm() / out1.norm()))
+        q.put((rank, bool(ok), info))
     except Exception as e:  # pragma: no cover
         import traceback
         q.put((rank, False, traceback.format_exc()))
@@ -53,13 +57,13 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_ep_equals_single_gpu_bitwise():
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_ep_equals_single_gpu_bitwise(world):
     import torch
     import torch.multiprocessing as mp
     n = torch.cuda.device_count()
-    if n < 2:
-        pytest.skip("needs >= 2 GPUs")
-    world = 4 if n >= 4 else 2
+    if n < world:
+        pytest.skip(f"needs >= {world} GPUs")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = 29700 + os.getpid() % 200

@@ -41,7 +41,7 @@ TINY = LayerShape(d=256, n_ffn=8, n_zero=4, top_k=2, k_expected=1, inter=128, pr
 class DeviceLayer:
     def __init__(self, ctx: Context, shape: LayerShape, seed: int = 5, mu: float = 0.0,
                  mu_decay: float = 1.0):
-        self.ctx, self.shape = ctx, shape
+        self.ctx, self.shape, self.seed = ctx, shape, seed
         L = lib()
         s = shape
         self.router = _P()
@@ -70,6 +70,54 @@ class DeviceLayer:
         self.ctx._check(lib().scmoe_layer_forward(self.ctx.handle, self.router, self.bank, a1, a3,
                                                   gain, tokens, int(renormalize), idx, gates,
                                                   ffn_count, out))
+
+    # ---- PID controller (router.hpp:144-176, model.hpp:235-244) ------------
+    def accumulate(self, idx: int, tokens: int):
+        """accumulate_counters on the device (indices as a device pointer)."""
+        self.ctx._check(lib().scmoe_accumulate_counters(self.ctx.handle, self.router, idx, tokens))
+
+    def bias_update(self):
+        """bias_update; returns the applied deltas (numpy)."""
+        import numpy as np
+        delta = np.empty(self.shape.E, np.float64)
+        self.ctx._check(lib().scmoe_bias_update(self.ctx.handle, self.router,
+                                                delta.ctypes.data_as(_P)))
+        return delta
+
+    def tokens_seen(self) -> int:
+        seen = C.c_uint64()
+        self.ctx._check(lib().scmoe_router_get_counters_host(self.ctx.handle, self.router, None,
+                                                             C.byref(seen)))
+        return int(seen.value)
+
+    def bias(self):
+        import numpy as np
+        b = np.empty(self.shape.E, np.float64)
+        self.ctx._check(lib().scmoe_router_get_bias_host(self.ctx.handle, self.router,
+                                                         b.ctypes.data_as(_P)))
+        return b
+
+    def counters(self):
+        import numpy as np
+        r = np.empty(self.shape.E, np.uint64)
+        seen = C.c_uint64()
+        self.ctx._check(lib().scmoe_router_get_counters_host(self.ctx.handle, self.router,
+                                                             r.ctypes.data_as(_P), C.byref(seen)))
+        return r, int(seen.value)
+
+    def router_weights(self):
+        """The router projection [d, E] (host copy), e.g. for an oracle check."""
+        import numpy as np
+        s = self.shape
+        w = np.empty(s.d * s.E, np.float32)
+        L = lib()
+        sd = int(L.scmoe_rng_stream_seed(self.seed, 0))
+        dev = _P()
+        self.ctx._check(L.scmoe_device_alloc(self.ctx.handle, w.nbytes, C.byref(dev)))
+        self.ctx._check(L.scmoe_rng_fill_uniform(self.ctx.handle, sd, 0, w.size, 1.0 / s.d, dev))
+        self.ctx._check(L.scmoe_copy_d2h(self.ctx.handle, w.ctypes.data_as(_P), dev, w.nbytes))
+        L.scmoe_device_free(self.ctx.handle, dev)
+        return w.reshape(s.d, s.E)
 
     def forward_batches(self, a1s, a3s, gain: Optional[int], tokens: int, idxs, gatess, cnts,
                         outs, renormalize: bool = False):

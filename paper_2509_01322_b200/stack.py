@@ -1,0 +1,66 @@
+"""A stack of ScMoE MoE branches with PID-controlled expert bias
+(BASELINE config 5).
+
+Each step feeds x through L layers -- layer l computes
+out = x + moe(rmsnorm(x)) with its own router, controller state and expert
+bank (model.hpp:394-400 with the dense branch the identity) -- accumulates
+every layer's slot counters (Model::accumulate_routing, model.hpp:235-238)
+and ticks every layer's controller (Model::update_biases, model.hpp:241-244:
+only layers with tokens_seen > 0).  Everything runs on the device; the host
+only sequences calls and records statistics.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import List
+
+import numpy as np
+import torch
+
+from . import Context
+from .layer import DeviceLayer, LayerShape
+
+
+@dataclass
+class StackTrace:
+    mean_ffn: List[List[float]] = field(default_factory=list)  # [step][layer]
+    std_ffn: List[List[float]] = field(default_factory=list)
+
+
+class ScMoEStack:
+    def __init__(self, ctx: Context, shape: LayerShape, n_layers: int, seed: int, mu: float,
+                 mu_decay: float):
+        self.ctx, self.shape = ctx, shape
+        self.layers = [DeviceLayer(ctx, shape, seed=seed + 1000 * l, mu=mu, mu_decay=mu_decay)
+                       for l in range(n_layers)]
+        self.trace = StackTrace()
+
+    def step(self, x: torch.Tensor, T: int, keep_inputs: bool = False):
+        """One training-style step: forward through every layer, count, tick.
+        Returns the per-layer routing indices (device) and, if requested, the
+        per-layer inputs (for teacher-forced checking)."""
+        s = self.shape
+        inputs, idxs = [], []
+        means, stds = [], []
+        for layer in self.layers:
+            if keep_inputs:
+                inputs.append(x.clone())
+            idx = torch.empty(T * s.top_k, dtype=torch.int32, device=x.device)
+            gates = torch.empty(T * s.top_k, dtype=torch.float64, device=x.device)
+            cnt = torch.empty(T, dtype=torch.int32, device=x.device)
+            out = torch.empty_like(x)
+            layer.forward(x.data_ptr(), x.data_ptr(), None, T, idx.data_ptr(), gates.data_ptr(),
+                          cnt.data_ptr(), out.data_ptr())
+            layer.accumulate(idx.data_ptr(), T)
+            self.ctx.synchronize()
+            c = cnt.cpu().numpy().astype(np.float64)
+            means.append(float(c.mean()))
+            stds.append(float(c.std()))
+            idxs.append(idx)
+            x = out
+        for layer in self.layers:
+            if layer.tokens_seen() > 0:
+                layer.bias_update()
+        self.trace.mean_ffn.append(means)
+        self.trace.std_ffn.append(stds)
+        return idxs, inputs, x

@@ -1,0 +1,194 @@
+// The reference's own unit-test cases for the hot path (tests/test_router.cpp,
+// tests/test_blocks.cpp), restated against the C++ drop-in header
+// include/moelab_b200/moelab.hpp so they run on the B200 through libscmoe.
+// Same inputs, same expectations; a tiny CHECK shim replaces Catch2.
+// Exit status = number of failed checks.
+#include <cmath>
+#include <cstdio>
+
+#include "moelab_b200/moelab.hpp"
+
+using namespace moelab;
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond)                                                          \
+    do {                                                                     \
+        if (cond) {                                                          \
+            ++g_pass;                                                        \
+        } else {                                                             \
+            ++g_fail;                                                        \
+            std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);       \
+        }                                                                    \
+    } while (0)
+#define CHECK_THROWS_AS(expr, T)                                             \
+    do {                                                                     \
+        bool thrown = false;                                                 \
+        try {                                                                \
+            (void)(expr);                                                    \
+        } catch (const T&) {                                                 \
+            thrown = true;                                                   \
+        }                                                                    \
+        CHECK(thrown);                                                       \
+    } while (0)
+
+static RouterState<double> make_state(std::size_t n, std::size_t z, std::size_t k, std::size_t ke,
+                                      double mu = 0.1, double decay = 1.0) {
+    return RouterState<double>(Tensor<double>{}, n, z, k, ke, mu, decay);
+}
+
+static void selection_is_biased_gates_are_not() {  // test_router.cpp:26-51
+    auto st = make_state(2, 1, 2, 1);
+    auto d = route_from_probs(Tensor<double>::row({0.5, 0.3, 0.2}), st);
+    CHECK((d.indices == std::vector<std::uint32_t>{0, 1}));
+    CHECK((d.gates == std::vector<double>{0.5, 0.3}));
+    CHECK((d.ffn_count == std::vector<std::uint32_t>{2}));
+    st.b = {-0.4, 0.0, 0.0};
+    d = route_from_probs(Tensor<double>::row({0.5, 0.3, 0.2}), st);
+    CHECK((d.indices == std::vector<std::uint32_t>{1, 2}));
+    CHECK((d.gates == std::vector<double>{0.3, 0.2}));
+    CHECK((d.ffn_count == std::vector<std::uint32_t>{1}));
+    st.b = {0.0, 1e9, 0.0};
+    d = route_from_probs(Tensor<double>::row({0.5, 0.3, 0.2}), st);
+    CHECK(d.indices[0] == 1 && d.gates[0] == 0.3);
+    st.b = {0.0, 0.0, 0.0};
+    d = route_from_probs(Tensor<double>::row({0.4, 0.4, 0.2}), st);
+    CHECK((d.indices == std::vector<std::uint32_t>{0, 1}));
+}
+
+static void config_errors() {  // test_router.cpp:88-92
+    CHECK_THROWS_AS(make_state(2, 1, 4, 1), ConfigError);
+    CHECK_THROWS_AS(make_state(2, 0, 2, 1), ConfigError);
+    CHECK_THROWS_AS(make_state(2, 1, 2, 2), ConfigError);
+}
+
+static void bias_update_rules() {  // test_router.cpp:94-134
+    {
+        auto st = make_state(2, 1, 2, 1, 0.1);
+        st.tokens_routed = {50, 50, 100};
+        st.tokens_seen = 100;
+        auto delta = bias_update(st);
+        CHECK(delta[0] == 0.0 && delta[1] == 0.0 && delta[2] == 0.0);
+    }
+    {
+        auto st = make_state(2, 1, 2, 1, 0.1);
+        st.tokens_routed = {80, 70, 50};
+        st.tokens_seen = 100;
+        auto delta = bias_update(st);
+        CHECK(std::fabs(delta[0] + 0.015) < 1e-15);
+        CHECK(std::fabs(delta[1] + 0.010) < 1e-15);
+        CHECK(delta[2] == 0.0);
+        CHECK(std::fabs(st.b[0] + 0.015) < 1e-15);
+        CHECK(st.b[2] == 0.0);
+        CHECK(st.tokens_seen == 0 && st.tokens_routed[0] == 0);
+    }
+    {
+        auto st = make_state(2, 1, 2, 1, 0.1, 0.5);
+        st.tokens_routed = {50, 50, 100};
+        st.tokens_seen = 100;
+        bias_update(st);
+        CHECK(std::fabs(st.mu - 0.05) < 1e-15);
+    }
+    {
+        auto st = make_state(2, 1, 2, 1);
+        CHECK_THROWS_AS(bias_update(st), StateError);
+    }
+    {
+        auto st = make_state(2, 1, 2, 1);
+        st.tokens_routed = {10, 10, 10};
+        st.tokens_seen = 100;
+        CHECK_THROWS_AS(bias_update(st), StateError);
+    }
+}
+
+struct BankFixture {  // test_blocks.cpp:214-248 (fp32, Uniform init)
+    std::vector<Parameter<float>> store;
+    ExpertBank<float> bank;
+    BankFixture(std::size_t n, std::size_t d, std::size_t inter, std::uint64_t seed) {
+        store.reserve(2 * n);
+        for (std::size_t e = 0; e < n; ++e) {
+            store.emplace_back("in", seeded_init<float>({d, inter}, InitDistribution::Uniform,
+                                                         1.0 / d, CounterRng(seed).stream(2 * e)));
+            store.emplace_back("out", seeded_init<float>({inter, d}, InitDistribution::Uniform,
+                                                          1.0 / d, CounterRng(seed).stream(2 * e + 1)));
+        }
+        for (std::size_t e = 0; e < n; ++e) {
+            bank.w_in.push_back(&store[2 * e]);
+            bank.w_out.push_back(&store[2 * e + 1]);
+        }
+    }
+};
+
+static Tensor<float> random_tensor(std::vector<std::size_t> shape, std::uint64_t seed) {
+    CounterRng rng(seed);
+    Tensor<float> t(std::move(shape));
+    for (std::size_t i = 0; i < t.numel(); ++i) t.data[i] = static_cast<float>(rng.normal_at(i));
+    return t;
+}
+
+static void moe_cases() {  // test_blocks.cpp:250-304
+    BankFixture fx(2, 8, 4, 7);
+    {
+        const Tensor<float> x = random_tensor({3, 8}, 11);
+        RoutingDecision d;
+        d.top_k = 1;
+        d.n_ffn = 2;
+        d.indices = {2, 3, 2};
+        d.gates = {1.0, 1.0, 1.0};
+        d.ffn_count = {0, 0, 0};
+        Tensor<float> out = moe_forward(x, d, fx.bank, 2);
+        bool same = true;
+        for (std::size_t i = 0; i < x.numel(); ++i) same = same && out.data[i] == x.data[i];
+        CHECK(same);  // zero-expert identity is bitwise
+    }
+    {
+        const Tensor<float> x = random_tensor({1, 8}, 12);
+        RoutingDecision d;
+        d.top_k = 2;
+        d.n_ffn = 2;
+        d.indices = {2, 3};
+        d.gates = {0.25, 0.5};
+        d.ffn_count = {0};
+        Tensor<float> out = moe_forward(x, d, fx.bank, 2);
+        bool close = true;
+        for (std::size_t i = 0; i < x.numel(); ++i)
+            close = close && std::fabs(out.data[i] - 0.75f * x.data[i]) < 1e-6f;
+        CHECK(close);
+    }
+    {
+        const Tensor<float> x = random_tensor({1, 8}, 14);
+        RoutingDecision d;
+        d.top_k = 1;
+        d.n_ffn = 2;
+        d.indices = {4};
+        d.gates = {1.0};
+        d.ffn_count = {0};
+        CHECK_THROWS_AS(moe_forward(x, d, fx.bank, 1), StateError);
+    }
+}
+
+static void closed_loop_controller() {  // test_router.cpp:269-283 (fp32 router)
+    RouterState<float> st(seeded_init<float>({64, 24}, InitDistribution::TruncatedNormal,
+                                             1.0 / 64, CounterRng(7)),
+                          16, 8, 6, 4, 0.05, 0.999);
+    auto trace = simulate_bias_control(st, 64, 512, 220, CounterRng(99));
+    double tail = 0.0;
+    for (std::size_t i = trace.mean_ffn.size() - 60; i < trace.mean_ffn.size(); ++i)
+        tail += trace.mean_ffn[i];
+    tail /= 60.0;
+    CHECK(std::fabs(tail - 4.0) / 4.0 < 0.05);
+    CHECK(trace.std_ffn.back() > 0.25);
+    bool zero_fixed = true;
+    for (std::size_t i = 16; i < 24; ++i) zero_fixed = zero_fixed && st.b[i] == 0.0;
+    CHECK(zero_fixed);
+    std::printf("closed loop: tail mean %.4f (target 4)\n", tail);
+}
+
+int main() {
+    selection_is_biased_gates_are_not();
+    config_errors();
+    bias_update_rules();
+    moe_cases();
+    closed_loop_controller();
+    std::printf("compat: %d passed, %d failed\n", g_pass, g_fail);
+    return g_fail;
+}

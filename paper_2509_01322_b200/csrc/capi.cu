@@ -29,17 +29,10 @@ int guarded(scmoe_ctx* c, F&& f) {
     }
 }
 
-// Host-tier staging buffers (distinct from the kernel workspace).
-struct Stage {
-    DevBuf bufs[12];
-};
-Stage& stage_of(scmoe_ctx* c) {
-    static thread_local std::vector<std::pair<scmoe_ctx*, Stage*>> table;
-    for (auto& kv : table)
-        if (kv.first == c) return *kv.second;
-    table.emplace_back(c, new Stage());
-    return *table.back().second;
-}
+// Host-tier staging buffers (distinct from the kernel workspace), owned by the
+// context so that destroying it never depends on thread/static teardown order.
+using Stage = HostStage;
+Stage& stage_of(scmoe_ctx* c) { return c->stage; }
 
 template <typename T>
 T* upload(scmoe_ctx* c, DevBuf& b, const T* host, size_t n) {

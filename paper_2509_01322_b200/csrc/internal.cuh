@@ -94,7 +94,12 @@ struct Profiler {
     std::vector<ProfAgg> agg;
 };
 
+struct HostStage {
+    DevBuf bufs[12];
+};
+
 struct scmoe_ctx {
+    HostStage stage;  // host-tier (_host) staging buffers
     int device = 0;
     int num_sms = 148;
     cudaStream_t own_stream = nullptr;

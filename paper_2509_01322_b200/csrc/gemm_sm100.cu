@@ -40,16 +40,22 @@ namespace {
 constexpr int BK = 64;          // K elements per stage (128 B rows, SWIZZLE_128B)
 constexpr int SLABS = 2;        // 128-row weight slabs per unit (BM = 256)
 constexpr int BM = 128 * SLABS;
-constexpr int NT = 256;         // max token columns per tile
-constexpr int STAGES = 3;
+constexpr int NT = 192;         // max token columns per tile
+// Separate rings: weights come from HBM (deep ring, most bytes in flight),
+// token rows from L2 (shallow ring).
+constexpr int A_STAGES = 4;
+constexpr int B_STAGES = 3;
 constexpr int A_SLAB_BYTES = 128 * BK * 2;        // 16 KB
-constexpr int B_HALF_BYTES = 128 * BK * 2;        // 16 KB per 128 token rows
-constexpr int STAGE_BYTES = SLABS * A_SLAB_BYTES + 2 * B_HALF_BYTES;  // 64 KB
+constexpr int B_HALF_BYTES = 128 * BK * 2;        // 16 KB per 128 token rows (first box)
+constexpr int A_STAGE_BYTES = SLABS * A_SLAB_BYTES;   // 32 KB
+constexpr int B_STAGE_BYTES = NT * BK * 2;            // 24 KB (up to NT tokens)
+constexpr int RING_BYTES = A_STAGES * A_STAGE_BYTES + B_STAGES * B_STAGE_BYTES;  // 192 KB
 constexpr int TMEM_COLS = 512;
-constexpr int NUM_THREADS = 192;
-constexpr int EPI_STAGE_BYTES = 4 * 32 * 80;  // epilogue transpose buffers (4 warps)
-constexpr int SMEM_BYTES =
-    STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + EPI_STAGE_BYTES;
+constexpr int EPI_WARPS = 4 * SLABS;             // one per (TMEM lane quadrant, slab)
+constexpr int EPI_WARP0 = 3;                     // warps 0: W producer, 1: MMA, 2: X producer
+constexpr int NUM_THREADS = 32 * (EPI_WARP0 + EPI_WARPS);
+constexpr int EPI_STAGE_BYTES = EPI_WARPS * 32 * 80;  // epilogue transpose buffers
+constexpr int SMEM_BYTES = RING_BYTES + 1024 /*align*/ + 256 /*barriers*/ + EPI_STAGE_BYTES;
 
 static_assert(SLABS * NT <= TMEM_COLS, "TMEM overflow");
 
@@ -99,18 +105,6 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
         " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
-        : "memory");
-}
-
-// Row gather (tile::gather4): 4 rows r0..r3, 64 columns from c0, into 512 B of
-// 128B-swizzled shared memory (same layout as 4 rows of a tiled box).
-__device__ __forceinline__ void tma_gather4(const CUtensorMap* map, uint64_t* bar, void* dst, int c0,
-                                            int r0, int r1, int r2, int r3, uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-        ".L2::cache_hint [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
-        "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
 
@@ -175,6 +169,7 @@ struct GemmArgs {
     const TokenTile* tiles;
     const int* n_tiles;
     const int* x_rows;   // gather mode: permuted row -> source row of X (nullptr: X is permuted)
+    const __nv_bfloat16* x;  // X base (gather mode reads rows directly)
     __nv_bfloat16* out;  // [rows][M]
     int M, K;            // weight rows per expert, reduction length
     int silu;
@@ -187,9 +182,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-    uint64_t* empty = full + STAGES;
-    uint64_t* tfull = empty + STAGES;
+    // smem: weight ring [A_STAGES][SLABS][16 KB] | token ring [B_STAGES][2][16 KB] |
+    //       barriers | epilogue transpose buffers
+    unsigned char* a_ring = smem;
+    unsigned char* b_ring = smem + A_STAGES * A_STAGE_BYTES;
+    uint64_t* a_full = reinterpret_cast<uint64_t*>(smem + RING_BYTES);
+    uint64_t* a_empty = a_full + A_STAGES;
+    uint64_t* b_full = a_empty + A_STAGES;
+    uint64_t* b_empty = b_full + B_STAGES;
+    uint64_t* tfull = b_empty + B_STAGES;
     uint64_t* tempty = tfull + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
 
@@ -200,12 +201,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int n_units = (*args.n_tiles) * mblocks;
 
     if (warp == 0 && lane == 0) {
-        for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+        for (int s = 0; s < A_STAGES; ++s) {
+            mbar_init(&a_full[s], 1);
+            mbar_init(&a_empty[s], 1);
+        }
+        for (int s = 0; s < B_STAGES; ++s) {
+            // gather mode: the 32 producer lanes each arrive once per stage
+            mbar_init(&b_full[s], args.x_rows ? 32 : 1);
+            mbar_init(&b_empty[s], 1);
         }
         mbar_init(tfull, 1);
-        mbar_init(tempty, 4);
+        mbar_init(tempty, EPI_WARPS);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_w)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_x)) : "memory");
@@ -222,74 +228,110 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        // ===== TMA producer (whole warp: lane 0 loads the weights, every lane
-        // issues row gathers in gather mode) =====
-        const uint64_t pol_w = policy_evict_first();
+        // ===== weight producer: streams W from HBM, A_STAGES deep =====
+        if (lane == 0) {
+            const uint64_t pol_w = policy_evict_first();
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+                const TokenTile tile = args.tiles[u / mblocks];
+                const int mb = u % mblocks;
+                // blocked weight layout (wblk_index): each (128-row, 64-col) tile is
+                // 128 contiguous 64-element rows of the 2-D view the map describes
+                const int ebase = tile.e * (args.M / 128) * kblocks * 128;
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&a_empty[stage], phase ^ 1);
+                    unsigned char* abase = a_ring + stage * A_STAGE_BYTES;
+                    mbar_expect_tx(&a_full[stage], A_STAGE_BYTES);
+#pragma unroll
+                    for (int s = 0; s < SLABS; ++s)
+                        tma_load_2d(&map_w, &a_full[stage], abase + s * A_SLAB_BYTES, 0,
+                                    ebase + ((mb * SLABS + s) * kblocks + kb) * 128, pol_w);
+                    if (++stage == A_STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 2) {
+        // ===== token producer: the tile's rows of X (L2-resident), B_STAGES
+        // deep; lane 0 issues tiled boxes, or every lane issues row gathers =====
         const uint64_t pol_x = policy_evict_last();
         const bool gather = args.x_rows != nullptr;
         int stage = 0;
         uint32_t phase = 0;
+        int pending = -1;  // gather mode: stage whose copies are in flight, not yet published
+        constexpr int kRowsPerLane = (NT + 31) / 32;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             const TokenTile tile = args.tiles[u / mblocks];
-            const int mb = u % mblocks;
-            // blocked weight layout (wblk_index): each (128-row, 64-col) tile is
-            // 128 contiguous 64-element rows of the 2-D view the map describes
-            const int ebase = tile.e * (args.M / 128) * kblocks * 128;
             const int n_eff = max(16, (tile.count + 15) & ~15);
-            // gather mode: this lane's two groups of 4 source rows (padding rows
-            // repeat the tile's last row; their columns are never stored)
-            int rows[8];
-            const int ngroups = n_eff / 4;
+            // gather mode: this lane's rows r = lane + 32 i (padding rows repeat
+            // the tile's last token; their columns are never stored)
+            const __nv_bfloat16* src[kRowsPerLane];
             if (gather) {
 #pragma unroll
-                for (int h = 0; h < 2; ++h)
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int j = min(4 * (lane + 32 * h) + q, tile.count - 1);
-                        rows[4 * h + q] = args.x_rows[tile.pos + j];
-                    }
+                for (int i = 0; i < kRowsPerLane; ++i) {
+                    const int r = lane + 32 * i;
+                    src[i] = r < n_eff ? args.x + (size_t)args.x_rows[tile.pos + min(r, tile.count - 1)] *
+                                                      args.K
+                                       : nullptr;
+                }
             }
-            const bool two = tile.count > 128;
-            const uint32_t bytes = SLABS * A_SLAB_BYTES +
-                                   (gather ? (uint32_t)n_eff * BK * 2 : (two ? 2u : 1u) * B_HALF_BYTES);
+            // tiled mode: boxes of 64 rows, as many as the tile needs
+            const int nbox = (n_eff + 63) / 64;
             for (int kb = 0; kb < kblocks; ++kb) {
-                mbar_wait(&empty[stage], phase ^ 1);
-                unsigned char* sbase = smem + stage * STAGE_BYTES;
-                unsigned char* bbase = sbase + SLABS * A_SLAB_BYTES;
-                if (lane == 0) {
-                    mbar_expect_tx(&full[stage], bytes);
-#pragma unroll
-                    for (int s = 0; s < SLABS; ++s)
-                        tma_load_2d(&map_w, &full[stage], sbase + s * A_SLAB_BYTES, 0,
-                                    ebase + ((mb * SLABS + s) * kblocks + kb) * 128, pol_w);
-                    if (!gather) {
-                        tma_load_2d(&map_x, &full[stage], bbase, kb * BK, tile.pos, pol_x);
-                        if (two)
-                            tma_load_2d(&map_x, &full[stage], bbase + B_HALF_BYTES, kb * BK,
-                                        tile.pos + 128, pol_x);
+                mbar_wait(&b_empty[stage], phase ^ 1);
+                unsigned char* bbase = b_ring + stage * B_STAGE_BYTES;
+                if (!gather) {
+                    if (lane == 0) {
+                        mbar_expect_tx(&b_full[stage], (uint32_t)nbox * 64 * BK * 2);
+                        for (int bx = 0; bx < nbox; ++bx)
+                            tma_load_2d(&map_x, &b_full[stage], bbase + bx * 64 * BK * 2, kb * BK,
+                                        tile.pos + 64 * bx, pol_x);
                     }
-                }
-                __syncwarp();  // expect_tx is posted before any gather can complete
-                if (gather) {
+                } else {
+                    // 16-byte cp.async per (row, chunk) into the 128B-swizzled
+                    // K-major layout the UMMA descriptor expects: chunk c of row r
+                    // lands at chunk position c ^ (r & 7)
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int g = lane + 32 * h;
-                        if (g < ngroups)
-                            tma_gather4(&map_x, &full[stage], bbase + g * 4 * BK * 2, kb * BK,
-                                        rows[4 * h], rows[4 * h + 1], rows[4 * h + 2],
-                                        rows[4 * h + 3], pol_x);
+                    for (int i = 0; i < kRowsPerLane; ++i) {
+                        if (!src[i]) continue;
+                        const int r = lane + 32 * i;
+                        const unsigned char* g =
+                            reinterpret_cast<const unsigned char*>(src[i] + kb * BK);
+                        const uint32_t d = smem_u32(bbase + r * 128);
+#pragma unroll
+                        for (int cc = 0; cc < 8; ++cc)
+                            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                                             d + ((cc ^ (r & 7)) << 4)),
+                                         "l"(g + cc * 16)
+                                         : "memory");
                     }
+                    asm volatile("cp.async.commit_group;" ::: "memory");
+                    // publish the previous stage once its copies have landed
+                    if (pending >= 0) {
+                        asm volatile("cp.async.wait_group 1;" ::: "memory");
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        mbar_arrive(&b_full[pending]);
+                    }
+                    pending = stage;
                 }
-                if (++stage == STAGES) {
+                if (++stage == B_STAGES) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
         }
+        if (gather && pending >= 0) {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive(&b_full[pending]);
+        }
     } else if (warp == 1) {
         // ===== MMA issuer =====
-        int stage = 0;
-        uint32_t phase = 0;
+        int as = 0, bs = 0;
+        uint32_t aph = 0, bph = 0;
         int local = 0;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++local) {
             const TokenTile tile = args.tiles[u / mblocks];
@@ -298,45 +340,51 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_wait(tempty, (local & 1) ^ 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             for (int kb = 0; kb < kblocks; ++kb) {
-                mbar_wait(&full[stage], phase);
+                mbar_wait(&a_full[as], aph);
+                mbar_wait(&b_full[bs], bph);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 if (lane == 0) {
-                    const uint32_t sbase = smem_u32(smem + stage * STAGE_BYTES);
-                    const uint32_t bbase = sbase + SLABS * A_SLAB_BYTES;
+                    const uint32_t abase = smem_u32(a_ring + as * A_STAGE_BYTES);
+                    const uint32_t bbase = smem_u32(b_ring + bs * B_STAGE_BYTES);
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k) {
                         const uint64_t bdesc = make_desc_sw128(bbase + k * 32);
 #pragma unroll
                         for (int s = 0; s < SLABS; ++s) {
-                            const uint64_t adesc = make_desc_sw128(sbase + s * A_SLAB_BYTES + k * 32);
+                            const uint64_t adesc = make_desc_sw128(abase + s * A_SLAB_BYTES + k * 32);
                             mma_bf16(tmem_base + s * NT, adesc, bdesc, idesc, (kb | k) != 0);
                         }
                     }
-                    mma_commit(&empty[stage]);
+                    mma_commit(&a_empty[as]);
+                    mma_commit(&b_empty[bs]);
                 }
                 __syncwarp();
-                if (++stage == STAGES) {
-                    stage = 0;
-                    phase ^= 1;
+                if (++as == A_STAGES) {
+                    as = 0;
+                    aph ^= 1;
+                }
+                if (++bs == B_STAGES) {
+                    bs = 0;
+                    bph ^= 1;
                 }
             }
             if (lane == 0) mma_commit(tfull);
             __syncwarp();
         }
     } else {
-        // ===== epilogue (warps 2..5) =====
+        // ===== epilogue (warps 3..10: one warp per TMEM lane quadrant and slab) =====
         const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+        const int s = (warp - EPI_WARP0) >> 2;  // weight slab this warp drains
         // Per-warp 32 tokens x 32 rows bf16 transpose buffer (80 B row pitch:
         // 16-byte reads of 8 consecutive lanes hit distinct banks).
-        unsigned char* stage_base = smem + STAGES * STAGE_BYTES + 256 + (warp - 2) * 32 * 80;
+        unsigned char* stage_base = smem + RING_BYTES + 256 + (warp - EPI_WARP0) * 32 * 80;
         int local = 0;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++local) {
             const TokenTile tile = args.tiles[u / mblocks];
             const int mb = u % mblocks;
             mbar_wait(tfull, local & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll
-            for (int s = 0; s < SLABS; ++s) {
+            {
                 const int m0 = mb * BM + s * 128 + quad * 32;  // this warp's 32 rows
                 const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + s * NT;
                 for (int j0 = 0; j0 < tile.count; j0 += 32) {
@@ -424,7 +472,7 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
     const CUtensorMap mw = make_map_2d(W, n_experts * M * K / BK, BK, 128, BK);
     // X: tiled boxes of 128 permuted rows, or single-row boxes for tile::gather4
     const CUtensorMap mx =
-        make_map_2d(X, std::max<size_t>(x_rows, 1), K, x_row_ids ? 1 : 128, BK);
+        make_map_2d(X, std::max<size_t>(x_rows, 1), K, x_row_ids ? 1 : 64, BK);
     static bool attr_set = false;
     if (!attr_set) {
         SCMOE_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel,
@@ -435,6 +483,7 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
     a.tiles = tiles;
     a.n_tiles = n_tiles_dev;
     a.x_rows = x_row_ids;
+    a.x = X;
     a.out = out;
     a.M = (int)M;
     a.K = (int)K;

@@ -9,25 +9,28 @@
 // and X/H are token-major rows ([rows][K] bf16), so both operands are
 // K-major 128-byte-swizzled TMA tiles.
 //
-// A token tile holds up to 256 tokens of one expert, so at the LongCat
+// A token tile holds up to NT=192 tokens of one expert, so at the LongCat
 // prefill shape (98..163 tokens per expert) every expert's weights are
 // streamed from HBM exactly once per GEMM.  The MMA's N is chosen per tile at
 // run time (tokens rounded up to 16), so short tiles (decode: ~4 tokens per
-// expert) issue N=16 MMAs and load only the token rows they use.
+// expert) issue N=16 MMAs and load only the token rows they use.  Weights are
+// stored in a blocked layout (internal.cuh wblk_index) so every weight TMA box
+// is one contiguous 16 KB read.
 //
 // Work unit = (token tile, block of 256 weight rows).  Each CTA (one per SM,
-// persistent, static round-robin over units) runs three roles:
-//   warp 0      TMA producer: per 64-wide K block, two 128-row weight slabs
-//               and one or two 128-row token boxes into a 3-stage smem ring;
+// persistent, static round-robin over units) runs four roles:
+//   warp 0      weight producer: per 64-wide K block two 128-row slabs into a
+//               4-stage ring (HBM stream, the bytes that must be in flight);
+//   warp 2      token producer: the tile's token rows into a 3-stage ring
+//               (64-row TMA boxes; or cp.async row gathers, SCMOE_GEMM1_GATHER);
 //   warp 1      MMA issuer: one elected lane issues tcgen05.mma
-//               (M=128, N=16..256, K=16) into two TMEM accumulators (one per
-//               weight slab, 256 columns each);
-//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers, optional SiLU, bf16
-//               store of out[pos0 + j][m] (token-major rows again).
-// The accumulators fill all 512 TMEM columns, so the epilogue of unit i and
-// the MMAs of unit i+1 do not overlap; the TMA producer keeps streaming the
-// next unit's weights into free stages meanwhile, which is what matters for
-// this HBM-bound kernel (the epilogue is ~2% of a unit).
+//               (M=128, N=16..192, K=16) into two TMEM accumulators (one per
+//               weight slab);
+//   warps 3-10  epilogue, one per (TMEM lane quadrant, slab): tcgen05.ld ->
+//               registers, optional SiLU, bf16, per-warp smem transpose, 64-byte
+//               token-row stores of out[pos0 + j][m].
+// The accumulators are single-buffered (2 x 192 columns); while the epilogue
+// drains them the producers keep streaming the next unit into free stages.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 

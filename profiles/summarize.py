@@ -55,7 +55,8 @@ def full_metrics(rep):
         name = r[h.index("Kernel Name")].split("(")[0].split("::")[-1].split("<")[0]
         vals = []
         for key, label in METRICS:
-            cands = [i for i, k in enumerate(h) if k == key or k.endswith("." + key)]
+            cands = [i for i, k in enumerate(h) if k == key] + \
+                    [i for i, k in enumerate(h) if k.endswith("." + key) and r[i].strip()]
             if cands:
                 i = cands[0]
                 vals.append(f"{r[i]} {units[i]}".strip())

@@ -53,6 +53,27 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+_JSON_FD = None
+
+
+def emit(line: dict):
+    """The one JSON line on stdout (libraries' banners are routed to stderr)."""
+    data = (json.dumps(line) + "\n").encode()
+    if _JSON_FD is not None:
+        os.write(_JSON_FD, data)
+    else:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+
+
+def stdout_to_stderr():
+    """Keep fd 1 for the JSON line only: NCCL prints its version banner on stdout."""
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
+
+
 # ---------------------------------------------------------------------------
 # distributed plumbing
 # ---------------------------------------------------------------------------
@@ -228,7 +249,7 @@ def run_reference_arm(args):
         "cpu_baseline": {**base, "value": v},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ---------------------------------------------------------------------------
@@ -405,7 +426,7 @@ def run_b200(args):
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def run_b200_ep(args):
@@ -427,8 +448,9 @@ def run_b200_ep(args):
     a3_h = P.fill_normal(P.stream_seed(SEED_X + 1, rank), T * D, threads=os.cpu_count() or 8)
     a1 = torch.from_numpy(a1_h).cuda()
     a3 = torch.from_numpy(a3_h).cuda()
+    chunks = args.ep_chunks
     for _ in range(args.warmup):
-        out, idx, gates, cnt = ep.forward(a1, a3, None, T)
+        out, idx, gates, cnt = ep.forward(a1, a3, None, T, chunks=chunks)
     torch.cuda.synchronize()
     idx_h = idx.cpu().numpy().view(np.uint32)
     ffn = idx_h[idx_h < N_FFN]
@@ -442,7 +464,7 @@ def run_b200_ep(args):
     with ClockSampler(local) as clk:
         ev0.record()
         for _ in range(args.steps):
-            out, idx, gates, cnt = ep.forward(a1, a3, None, T)
+            out, idx, gates, cnt = ep.forward(a1, a3, None, T, chunks=chunks)
         ev1.record()
         ev1.synchronize()
     torch.cuda.synchronize()
@@ -464,7 +486,7 @@ def run_b200_ep(args):
     for _ in range(e_steps):
         x1 = a1_p.cuda(non_blocking=True)
         x3 = a3_p.cuda(non_blocking=True)
-        o, _, _, _ = ep.forward(x1, x3, None, T)
+        o, _, _, _ = ep.forward(x1, x3, None, T, chunks=chunks)
         out_p.copy_(o.view(T, D), non_blocking=True)
     e1.record()
     e1.synchronize()
@@ -496,7 +518,9 @@ def run_b200_ep(args):
                                f"(BASELINE config 4 shape, {T} tokens per GPU)",
                    "tokens_per_gpu": T, "d_model": D, "n_ffn": N_FFN, "n_zero": N_ZERO,
                    "top_k": TOPK, "inter": INTER, "experts_per_gpu": n_local,
-                   "parallelism": f"ep{ws} (NCCL all_to_all dispatch/return, no overlap yet)",
+                   "parallelism": f"ep{ws} (NCCL all_to_all dispatch/return, {chunks}-chunk "
+                                  "software pipeline overlapping routing / expert GEMMs with "
+                                  "the all-to-alls)",
                    "a2a_bytes_each_way_rank0": ep.last_stats["a2a_bytes_each_way"],
                    "mean_ffn_per_token": float(ffn.size) / T},
         "e2e": {"value": T * ws / (e2e_ms / 1e3), "unit": "tokens/s",
@@ -511,7 +535,7 @@ def run_b200_ep(args):
         "clocks": clk.summary(),
         "cpu_baseline": None,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def main():
@@ -528,7 +552,10 @@ def main():
     ap.add_argument("--schedule", default="serial", choices=["pipelined", "serial"])
     ap.add_argument("--parallel", default="ep", choices=["ep", "replicated"],
                     help="N>1: expert-parallel (default) or replicated experts")
+    ap.add_argument("--ep-chunks", type=int, default=2,
+                    help="EP software-pipeline depth (token chunks per step)")
     args = ap.parse_args()
+    stdout_to_stderr()
     if args.impl == "reference":
         run_reference_arm(args)
     elif int(os.environ.get("WORLD_SIZE", "1")) > 1 and args.parallel == "ep":

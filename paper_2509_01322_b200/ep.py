@@ -133,22 +133,30 @@ class EPLayer:
         self.last_stats = {}
 
     def forward(self, a1: torch.Tensor, a3: Optional[torch.Tensor], gain, T: int,
-                renormalize: bool = False):
+                renormalize: bool = False, chunks: int = 1):
+        """chunks > 1 splits the tokens into micro-chunks processed as a
+        software pipeline: chunk c+1's routing runs while chunk
+        c's rows are in flight, chunk c's expert GEMMs while chunk c+1's rows
+        are in flight, and so on.  Results are bitwise identical to chunks=1
+        (every step is per-token independent)."""
         stream = getattr(self.ops, "stream", None)
         if stream is None:
-            return self._forward(a1, a3, gain, T, renormalize)
+            return self._forward(a1, a3, gain, T, renormalize, chunks)
         # inputs produced on the caller's stream must be complete first
         stream.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(stream):
-            res = self._forward(a1, a3, gain, T, renormalize)
+            res = self._forward(a1, a3, gain, T, renormalize, chunks)
         torch.cuda.current_stream().wait_stream(stream)
         for t in res:
             t.record_stream(torch.cuda.current_stream())
         return res
 
-    def _forward(self, a1, a3, gain, T, renormalize):
+    # -- pipeline stages (all on the current stream; collectives async) -------
+    def _dispatch(self, a1, gain, t0, t1):
         ops, G = self.ops, self.world
-        hmoe, hb, idx, gates, cnt = ops.route(a1, gain, T)
+        T = t1 - t0
+        a1c = a1.reshape(-1)[t0 * self.d:t1 * self.d]
+        hmoe, hb, idx, gates, cnt = ops.route(a1c, gain, T)
         counts, slot_pos, send_token, send_expert = ops.plan(idx, T)
         # count exchange (G ints); split sizes are needed on the host
         recv_counts = torch.empty_like(counts)
@@ -158,14 +166,51 @@ class EPLayer:
         n_send, n_recv = sum(send_split), sum(recv_split)
         send_rows = ops.gather(hb, send_token, n_send)
         recv_rows = torch.empty(n_recv, hb.shape[1], dtype=hb.dtype, device=hb.device)
-        dist.all_to_all_single(recv_rows, send_rows, recv_split, send_split, group=self.group)
+        w_rows = dist.all_to_all_single(recv_rows, send_rows, recv_split, send_split,
+                                        group=self.group, async_op=True)
         recv_expert = torch.empty(n_recv, dtype=send_expert.dtype, device=send_expert.device)
-        dist.all_to_all_single(recv_expert, send_expert[:n_send].contiguous(), recv_split,
-                               send_split, group=self.group)
-        y_rows = ops.experts(recv_rows, recv_expert)
-        back_rows = torch.empty(n_send, hb.shape[1], dtype=hb.dtype, device=hb.device)
-        dist.all_to_all_single(back_rows, y_rows, send_split, recv_split, group=self.group)
-        out = ops.combine(hmoe, back_rows, slot_pos, idx, gates, T, a3, renormalize)
-        self.last_stats = {"send_rows": n_send, "recv_rows": n_recv,
-                           "a2a_bytes_each_way": n_send * hb.shape[1] * hb.element_size()}
-        return out, idx, gates, cnt
+        w_exp = dist.all_to_all_single(recv_expert, send_expert[:n_send].contiguous(), recv_split,
+                                       send_split, group=self.group, async_op=True)
+        return dict(t0=t0, T=T, hmoe=hmoe, idx=idx, gates=gates, cnt=cnt, slot_pos=slot_pos,
+                    send_split=send_split, recv_split=recv_split, n_send=n_send, n_recv=n_recv,
+                    recv_rows=recv_rows, recv_expert=recv_expert, waits=[w_rows, w_exp],
+                    keep=[send_rows], width=hb.shape[1], dtype=hb.dtype)
+
+    def _experts(self, st):
+        for w in st.pop("waits"):
+            w.wait()
+        y_rows = self.ops.experts(st["recv_rows"], st["recv_expert"])
+        back = torch.empty(st["n_send"], st["width"], dtype=st["dtype"], device=y_rows.device)
+        st["w_back"] = dist.all_to_all_single(back, y_rows, st["send_split"], st["recv_split"],
+                                              group=self.group, async_op=True)
+        st["back"] = back
+        st["keep"].append(y_rows)
+
+    def _combine(self, st, a3, renormalize):
+        st.pop("w_back").wait()
+        a3c = None if a3 is None else a3.view(-1)[st["t0"] * self.d:(st["t0"] + st["T"]) * self.d]
+        return self.ops.combine(st["hmoe"], st["back"], st["slot_pos"], st["idx"], st["gates"],
+                                st["T"], a3c, renormalize)
+
+    def _forward(self, a1, a3, gain, T, renormalize, chunks):
+        self.d = self.ops.shape.d if hasattr(self.ops, "shape") else a1.numel() // T
+        chunks = max(1, min(chunks, T))
+        bounds = [T * c // chunks for c in range(chunks + 1)]
+        # issue order: D0 D1 E0 D2 E1 C0 ... so each collective has independent
+        # compute queued behind it on the GPU
+        states = []
+        outs = []
+        for c in range(chunks + 2):
+            if c < chunks:
+                states.append(self._dispatch(a1, gain, bounds[c], bounds[c + 1]))
+            if 0 <= c - 1 < chunks:
+                self._experts(states[c - 1])
+            if 0 <= c - 2 < chunks:
+                outs.append(self._combine(states[c - 2], a3, renormalize))
+        n_send = sum(s["n_send"] for s in states)
+        n_recv = sum(s["n_recv"] for s in states)
+        self.last_stats = {"send_rows": n_send, "recv_rows": n_recv, "chunks": chunks,
+                           "a2a_bytes_each_way": n_send * states[0]["width"] * 2}
+        cat = lambda key: torch.cat([s[key] for s in states]) if chunks > 1 else states[0][key]  # noqa: E731
+        out = torch.cat([o.view(-1) for o in outs]).view(T, -1) if chunks > 1 else outs[0]
+        return out, cat("idx"), cat("gates"), cat("cnt")

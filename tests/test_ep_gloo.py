@@ -118,7 +118,7 @@ class OracleOps:
         return torch.from_numpy(out.astype(np.float32))
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, chunks=1):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -130,7 +130,7 @@ def _worker(rank, world, port, q):
         a1 = torch.from_numpy(O.normal_f32(O.stream_seed(SEED_X, rank), T_LOCAL * D))
         a3 = torch.from_numpy(O.normal_f32(O.stream_seed(SEED_X + 1, rank), T_LOCAL * D))
         layer = EPLayer(OracleOps(rank, world))
-        out, idx, gates, cnt = layer.forward(a1, a3, None, T_LOCAL)
+        out, idx, gates, cnt = layer.forward(a1, a3, None, T_LOCAL, chunks=chunks)
         # single-process oracle on this rank's tokens
         w_r, w_in, w_out = _weights()
         want = np.empty((T_LOCAL, D), np.float32)
@@ -151,13 +151,14 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_ep_orchestration_gloo(world):
+@pytest.mark.parametrize("world,chunks", [(2, 1), (2, 3)])
+def test_ep_orchestration_gloo(world, chunks):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = 29600 + os.getpid() % 200
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port + chunks, q, chunks))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]

@@ -12,7 +12,7 @@ sys.path.insert(0, ROOT)
 pytestmark = pytest.mark.gpu
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, chunks=1):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -31,7 +31,7 @@ def _worker(rank, world, port, q):
         a3 = torch.from_numpy(P.fill_normal(P.stream_seed(10, rank), T * shape.d)).cuda()
         ctx = P.Context(rank)
         ep = EPLayer(GpuOps(ctx, shape, rank, world, seed=3))
-        out, idx, gates, cnt = ep.forward(a1, a3, None, T)
+        out, idx, gates, cnt = ep.forward(a1, a3, None, T, chunks=chunks)
         torch.cuda.synchronize()
         # single-GPU reference: same seed => same router and the full expert set
         ctx1 = P.Context(rank)
@@ -57,8 +57,8 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [1, 2, 4])
-def test_ep_equals_single_gpu_bitwise(world):
+@pytest.mark.parametrize("world,chunks", [(1, 1), (2, 1), (2, 2), (4, 3)])
+def test_ep_equals_single_gpu_bitwise(world, chunks):
     import torch
     import torch.multiprocessing as mp
     n = torch.cuda.device_count()
@@ -67,7 +67,8 @@ def test_ep_equals_single_gpu_bitwise(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = 29700 + os.getpid() % 200
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port + chunks, q, chunks))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=600) for _ in range(world)]

@@ -552,7 +552,7 @@ def main():
     ap.add_argument("--schedule", default="serial", choices=["pipelined", "serial"])
     ap.add_argument("--parallel", default="ep", choices=["ep", "replicated"],
                     help="N>1: expert-parallel (default) or replicated experts")
-    ap.add_argument("--ep-chunks", type=int, default=2,
+    ap.add_argument("--ep-chunks", type=int, default=1,
                     help="EP software-pipeline depth (token chunks per step)")
     args = ap.parse_args()
     stdout_to_stderr()

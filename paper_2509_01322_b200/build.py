@@ -71,6 +71,7 @@ def check_sass(lib: str = LIB) -> dict:
     # pure FMUL + FADD.  The SiLU instantiation's only FFMAs come from the
     # correctly rounded IEEE division (__fdiv_rn) inside the logistic.
     seq = [n for n in summary if re.search(r"seq_gemm_kernel.*Lb0EE", n)]
+    seq += [n for n in summary if re.search(r"router_(tma|slab|lean)_kernel", n)]
     assert seq, "seq_gemm kernel missing from SASS"
     for n in seq:
         assert summary[n]["FFMA"] == 0, f"{n}: FFMA found in exact-order kernel"

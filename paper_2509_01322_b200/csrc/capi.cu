@@ -45,12 +45,26 @@ void download(scmoe_ctx* c, T* host, const T* dev, size_t n) {
     if (n) SCMOE_CUDA(cudaMemcpyAsync(host, dev, n * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
 }
 
+// Blocking fills/copies for state set-up.  They go through the context's
+// stream: its streams are non-blocking, so a legacy-stream cudaMemset or a
+// pageable cudaMemcpy (which may return before its DMA lands) is NOT ordered
+// before the next kernel on them.
+void stream_zero(scmoe_ctx* c, void* p, size_t bytes) {
+    SCMOE_CUDA(cudaMemsetAsync(p, 0, bytes, c->stream));
+    SCMOE_CUDA(cudaStreamSynchronize(c->stream));
+}
+void stream_copy(scmoe_ctx* c, void* dst, const void* src, size_t bytes) {
+    SCMOE_CUDA(cudaStreamSynchronize(c->stream));
+    if (bytes) SCMOE_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->stream));
+    SCMOE_CUDA(cudaStreamSynchronize(c->stream));
+}
+
 void sync_and_check(scmoe_ctx* c) {
     SCMOE_CUDA(cudaStreamSynchronize(c->stream));
     int st = 0;
     SCMOE_CUDA(cudaMemcpy(&st, c->dev_status, sizeof(int), cudaMemcpyDeviceToHost));
     if (st != DEV_OK) {
-        SCMOE_CUDA(cudaMemset(c->dev_status, 0, sizeof(int)));
+        stream_zero(c, c->dev_status, sizeof(int));
         if (st == DEV_ERR_INDEX_RANGE) SCMOE_THROW(SCMOE_ERR_STATE, "moe_forward: expert index out of range");
         if (st == DEV_ERR_COUNTERS)
             SCMOE_THROW(SCMOE_ERR_STATE, "bias_update: counters do not cover top_k slots per token");
@@ -138,7 +152,7 @@ void moe_back(scmoe_ctx* c, scmoe_bank* b, const float* x, size_t T, const uint3
         __nv_bfloat16* h = ws.h.get<__nv_bfloat16>(T * K * I + 1);
         __nv_bfloat16* y = ws.y.get<__nv_bfloat16>(T * K * d + 1);
         if (c->gemm1_gather) {
-            // GEMM1 gathers its token rows straight from x (TMA tile::gather4).
+            // GEMM1 gathers its token rows straight from x (cp.async row gather).
             ProfScope _p(c, "gemm1_tcgen05");
             launch_grouped_gemm_bf16(c, b->w1t, n_ffn, I, d, ws.hmoe_bf16.get<__nv_bfloat16>(T * d),
                                      T, pr.row_token, h, /*silu=*/1, pr.tiles, pr.n_tiles,
@@ -259,7 +273,7 @@ int scmoe_ctx_create(int device, scmoe_ctx** out) {
         SCMOE_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
         c->stream = c->own_stream;
         SCMOE_CUDA(cudaMalloc(&c->dev_status, sizeof(int)));
-        SCMOE_CUDA(cudaMemset(c->dev_status, 0, sizeof(int)));
+        stream_zero(c, c->dev_status, sizeof(int));
         *out = c;
     });
 }
@@ -354,9 +368,9 @@ int scmoe_router_create(scmoe_ctx* c, size_t d, size_t n_ffn, size_t n_zero, siz
         SCMOE_CUDA(cudaMalloc(&r->w, std::max<size_t>(d * E, 1) * sizeof(float)));
         SCMOE_CUDA(cudaMalloc(&r->b, std::max<size_t>(E, 1) * sizeof(double)));
         SCMOE_CUDA(cudaMalloc(&r->routed, std::max<size_t>(E, 1) * sizeof(uint64_t)));
-        SCMOE_CUDA(cudaMemset(r->w, 0, std::max<size_t>(d * E, 1) * sizeof(float)));
-        SCMOE_CUDA(cudaMemset(r->b, 0, std::max<size_t>(E, 1) * sizeof(double)));
-        SCMOE_CUDA(cudaMemset(r->routed, 0, std::max<size_t>(E, 1) * sizeof(uint64_t)));
+        stream_zero(c, r->w, std::max<size_t>(d * E, 1) * sizeof(float));
+        stream_zero(c, r->b, std::max<size_t>(E, 1) * sizeof(double));
+        stream_zero(c, r->routed, std::max<size_t>(E, 1) * sizeof(uint64_t));
         *out = r;
     });
 }
@@ -374,7 +388,7 @@ int scmoe_router_destroy(scmoe_ctx* c, scmoe_router* r) {
 int scmoe_router_set_weights_host(scmoe_ctx* c, scmoe_router* r, const float* w) {
     return guarded(c, [&] {
         require_ctx(c);
-        SCMOE_CUDA(cudaMemcpy(r->w, w, r->d * r->E() * sizeof(float), cudaMemcpyHostToDevice));
+        stream_copy(c, r->w, w, r->d * r->E() * sizeof(float));
     });
 }
 int scmoe_router_set_weights(scmoe_ctx* c, scmoe_router* r, const float* w) {
@@ -389,7 +403,7 @@ int scmoe_router_set_bias_host(scmoe_ctx* c, scmoe_router* r, const double* b) {
         require_ctx(c);
         for (size_t i = r->n_ffn; i < r->E(); ++i)
             if (b[i] != 0.0) SCMOE_THROW(SCMOE_ERR_CONFIG, "router: zero-expert bias must stay 0");
-        SCMOE_CUDA(cudaMemcpy(r->b, b, r->E() * sizeof(double), cudaMemcpyHostToDevice));
+        stream_copy(c, r->b, b, r->E() * sizeof(double));
     });
 }
 int scmoe_router_get_bias_host(scmoe_ctx* c, scmoe_router* r, double* b) {
@@ -427,7 +441,7 @@ int scmoe_router_set_counters_host(scmoe_ctx* c, scmoe_router* r, const uint64_t
     return guarded(c, [&] {
         require_ctx(c);
         SCMOE_CUDA(cudaStreamSynchronize(c->stream));
-        SCMOE_CUDA(cudaMemcpy(r->routed, routed, r->E() * sizeof(uint64_t), cudaMemcpyHostToDevice));
+        stream_copy(c, r->routed, routed, r->E() * sizeof(uint64_t));
         r->tokens_seen = seen;
     });
 }
@@ -558,13 +572,13 @@ int scmoe_bank_create(scmoe_ctx* c, size_t n, size_t d, size_t inter, int precis
         if (precision == SCMOE_PREC_F32_EXACT) {
             SCMOE_CUDA(cudaMalloc(&b->w_in32, std::max<size_t>(n * per, 1) * sizeof(float)));
             SCMOE_CUDA(cudaMalloc(&b->w_out32, std::max<size_t>(n * per, 1) * sizeof(float)));
-            SCMOE_CUDA(cudaMemset(b->w_in32, 0, std::max<size_t>(n * per, 1) * sizeof(float)));
-            SCMOE_CUDA(cudaMemset(b->w_out32, 0, std::max<size_t>(n * per, 1) * sizeof(float)));
+            stream_zero(c, b->w_in32, std::max<size_t>(n * per, 1) * sizeof(float));
+            stream_zero(c, b->w_out32, std::max<size_t>(n * per, 1) * sizeof(float));
         } else {
             SCMOE_CUDA(cudaMalloc(&b->w1t, std::max<size_t>(n * per, 1) * sizeof(__nv_bfloat16)));
             SCMOE_CUDA(cudaMalloc(&b->w2t, std::max<size_t>(n * per, 1) * sizeof(__nv_bfloat16)));
-            SCMOE_CUDA(cudaMemset(b->w1t, 0, std::max<size_t>(n * per, 1) * sizeof(__nv_bfloat16)));
-            SCMOE_CUDA(cudaMemset(b->w2t, 0, std::max<size_t>(n * per, 1) * sizeof(__nv_bfloat16)));
+            stream_zero(c, b->w1t, std::max<size_t>(n * per, 1) * sizeof(__nv_bfloat16));
+            stream_zero(c, b->w2t, std::max<size_t>(n * per, 1) * sizeof(__nv_bfloat16));
         }
         *out = b;
     });

@@ -126,8 +126,9 @@ class GpuOps:
 class EPLayer:
     """One ScMoE MoE branch sharded over the ranks of ``group``."""
 
-    def __init__(self, ops, group=None):
+    def __init__(self, ops, group=None, async_comm: bool = True):
         self.ops, self.group = ops, group
+        self.async_comm = async_comm
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.last_stats = {}
@@ -167,10 +168,10 @@ class EPLayer:
         send_rows = ops.gather(hb, send_token, n_send)
         recv_rows = torch.empty(n_recv, hb.shape[1], dtype=hb.dtype, device=hb.device)
         w_rows = dist.all_to_all_single(recv_rows, send_rows, recv_split, send_split,
-                                        group=self.group, async_op=True)
+                                        group=self.group, async_op=self.async_comm)
         recv_expert = torch.empty(n_recv, dtype=send_expert.dtype, device=send_expert.device)
         w_exp = dist.all_to_all_single(recv_expert, send_expert[:n_send].contiguous(), recv_split,
-                                       send_split, group=self.group, async_op=True)
+                                       send_split, group=self.group, async_op=self.async_comm)
         return dict(t0=t0, T=T, hmoe=hmoe, idx=idx, gates=gates, cnt=cnt, slot_pos=slot_pos,
                     send_split=send_split, recv_split=recv_split, n_send=n_send, n_recv=n_recv,
                     recv_rows=recv_rows, recv_expert=recv_expert, waits=[w_rows, w_exp],
@@ -178,16 +179,19 @@ class EPLayer:
 
     def _experts(self, st):
         for w in st.pop("waits"):
-            w.wait()
+            if w is not None:
+                w.wait()
         y_rows = self.ops.experts(st["recv_rows"], st["recv_expert"])
         back = torch.empty(st["n_send"], st["width"], dtype=st["dtype"], device=y_rows.device)
         st["w_back"] = dist.all_to_all_single(back, y_rows, st["send_split"], st["recv_split"],
-                                              group=self.group, async_op=True)
+                                              group=self.group, async_op=self.async_comm)
         st["back"] = back
         st["keep"].append(y_rows)
 
     def _combine(self, st, a3, renormalize):
-        st.pop("w_back").wait()
+        w = st.pop("w_back")
+        if w is not None:
+            w.wait()
         a3c = None if a3 is None else a3.view(-1)[st["t0"] * self.d:(st["t0"] + st["T"]) * self.d]
         return self.ops.combine(st["hmoe"], st["back"], st["slot_pos"], st["idx"], st["gates"],
                                 st["T"], a3c, renormalize)

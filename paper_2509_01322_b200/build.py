@@ -31,12 +31,13 @@ COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-con
                  "-I" + os.path.join(ROOT, "include")]
 SOURCES = {
     "kernels_router.cu": ["--fmad=false"],
+    "router_sm100.cu": ["--fmad=false", "-Xptxas", "-O1"],
     "kernels_moe.cu": ["--fmad=false"],
     "capi.cu": [],
     "gemm_sm100.cu": ["-Xptxas", "-v"],
 }
 HOST_SOURCES = ["host_rng.cpp"]
-HEADERS = ["internal.cuh", "libm_port.h"]
+HEADERS = ["internal.cuh", "libm_port.h", "sm100_util.cuh", "f32x2.cuh"]
 
 
 def _newer(src_list, target):

@@ -192,16 +192,19 @@ void route_logits(scmoe_ctx* c, scmoe_router* r, const float* x, size_t T, float
     int v = c->router_variant;
     if (v == 2 && !router_lean_ok(r->d, E)) v = 0;
     if (v == 1 && !router_slab_ok(T, r->d, E, 0)) v = 0;
+    if (v == 4 && !router_tma_ok(T, r->d, E, 0)) v = 0;
     if (v == 0) {
         if (c->overlapped && router_lean_ok(r->d, E) && T >= 512)
             v = 2;
-        else if (router_slab_ok(T, r->d, E, c->num_sms))
-            v = 1;
+        else if (router_tma_ok(T, r->d, E, c->num_sms))
+            v = 4;
         else
             v = 3;
     }
     ProfScope _p(c, "router_gemm");
-    if (v == 1) {
+    if (v == 4) {
+        launch_router_tma(c, x, r->w, logits, T, r->d, E);
+    } else if (v == 1) {
         launch_router_slab(c, x, r->w, logits, T, r->d, E);
     } else if (v == 2) {
         launch_router_lean(c, x, r->w, logits, T, r->d, E);
@@ -268,7 +271,8 @@ int scmoe_ctx_create(int device, scmoe_ctx** out) {
         if (const char* g = getenv("SCMOE_GEMM1_GATHER")) c->gemm1_gather = atoi(g) != 0;
         if (const char* v = getenv("SCMOE_ROUTER")) {
             const std::string sv(v);
-            c->router_variant = sv == "slab" ? 1 : sv == "lean" ? 2 : sv == "tiled" ? 3 : 0;
+            c->router_variant =
+                sv == "slab" ? 1 : sv == "lean" ? 2 : sv == "tiled" ? 3 : sv == "tma" ? 4 : 0;
         }
         SCMOE_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
         c->stream = c->own_stream;

@@ -111,7 +111,8 @@ struct scmoe_ctx {
     Profiler prof;
     bool gemm1_gather = false;  // GEMM1 B operand via TMA gather4 (SCMOE_GEMM1_GATHER=1)
     // router projection kernel: 0 auto, 1 slab (56 tokens x E, 1 CTA/SM),
-    // 2 lean (co-resides with the GEMM), 3 tiled (64/16-row tiles); SCMOE_ROUTER
+    // 2 lean (co-resides with the GEMM), 3 tiled (64/16-row tiles), 4 tma (slab
+    // tile fed by TMA, the large-batch default); SCMOE_ROUTER
     int router_variant = 0;
     bool overlapped = false;    // inside a pipelined multi-batch call
     // pipelined multi-batch execution (scmoe_layer_forward_batches)
@@ -195,6 +196,10 @@ void launch_seq_gemm(scmoe_ctx* c, const float* A, size_t lda, const int* a_rows
                      size_t max_tiles, int tile_rows);
 int seq_gemm_tile_rows(size_t rows, size_t N, int num_sms);
 // Router projection with one CTA per 56-token slab x all experts (E <= 768).
+// Same tile as the slab kernel, operands by TMA into an mbarrier ring.
+bool router_tma_ok(size_t T, size_t K, size_t E, int num_sms);
+void launch_router_tma(scmoe_ctx* c, const float* X, const float* W, float* logits, size_t T,
+                       size_t K, size_t E);
 bool router_slab_ok(size_t T, size_t K, size_t E, int num_sms);
 // Router projection sized to co-reside with the grouped GEMM (28-token slabs).
 bool router_lean_ok(size_t K, size_t E);

@@ -9,6 +9,7 @@
 #include <float.h>
 
 #include "internal.cuh"
+#include "f32x2.cuh"
 #include "libm_port.h"
 
 namespace scmoe {
@@ -301,45 +302,54 @@ __global__ void __launch_bounds__((TM / RM) * (TN / RN)) seq_gemm_kernel(
 // Router projection, large batches: one CTA per 56-token slab covering all
 // E <= 768 expert columns (8 token groups x 96 expert groups = 768 threads,
 // 7 x 8 independent sequential chains per thread).  With T=8192 this is 147
-// CTAs -- a single wave on 148 SMs -- instead of 3.5 waves of 64x64 tiles.
-// Same arithmetic as seq_gemm_kernel: per output c = 0; c = c + x*w in k order.
+// CTAs -- a single wave on 148 SMs.  Same arithmetic as seq_gemm_kernel: per
+// output c = 0; c = c + x*w in k order, every product and sum rounded.
+//
+// The chains run on packed f32x2 instructions (FMUL2 / FADD2: two lanes of
+// work per issue slot), which lifts the FP32 pipe from ~108 to ~122 of its
+// 128 lane-ops/clk/SM at this tile shape (tests/cpp/fp32x2_bench.cu).  FMUL2
+// takes the token as a broadcast scalar against an expert pair (w0, w1); the
+// product is added half-swapped into the accumulator pair (c1, c0).  The swap
+// is a free operand modifier, and it keeps ptxas from contracting mul + add
+// into FFMA2, which it otherwise does for f32x2 even with explicit .rn and
+// --fmad=false (build.py asserts the kernel has no FFMA/FFMA2).
 // ---------------------------------------------------------------------------
 constexpr int kSlabTok = 7, kSlabExp = 8, kSlabTG = 8, kSlabEG = 96;
 constexpr int kSlabRows = kSlabTok * kSlabTG;          // 56
 constexpr int kSlabThreads = kSlabTG * kSlabEG;        // 768
 constexpr int kSlabKC = 16;
 constexpr int kSlabXStride = kSlabTG * 8;              // 64: group g at columns [8g, 8g+7)
+constexpr int kSlabW = kSlabEG * kSlabExp;             // 768 (padded expert width)
+constexpr int kSlabHalf = kSlabW / 2;                  // thread eg: [4eg, 4eg+4) and [384+4eg, ..)
 
 __global__ void __launch_bounds__(kSlabThreads, 1) router_slab_kernel(
     const float* __restrict__ X, const float* __restrict__ W, float* __restrict__ logits, int T,
     int K, int E) {
     extern __shared__ __align__(16) float slab_smem[];
-    auto xs = reinterpret_cast<float(*)[kSlabKC][kSlabXStride]>(slab_smem);
-    auto ws = reinterpret_cast<float(*)[kSlabKC][kSlabEG * kSlabExp]>(
-        slab_smem + 2 * kSlabKC * kSlabXStride);
+    // ws[buf][k][768]: W rows; xs[buf][k][64]: X transposed (group g's 7
+    // tokens at [8g, 8g+7)); xraw[buf][56][16]: X rows as copied.
+    auto ws = reinterpret_cast<float(*)[kSlabKC][kSlabW]>(slab_smem);
+    auto xs = reinterpret_cast<float(*)[kSlabKC][kSlabXStride]>(slab_smem + 2 * kSlabKC * kSlabW);
+    auto xraw = reinterpret_cast<float(*)[kSlabRows][kSlabKC]>(
+        slab_smem + 2 * kSlabKC * (kSlabW + kSlabXStride));
     const int tid = threadIdx.x;
     const int tg = tid / kSlabEG, eg = tid % kSlabEG;
     const int row0 = blockIdx.x * kSlabRows;
     const int nrows = min(kSlabRows, T - row0);
     if (nrows <= 0) return;
-    const int Ew = kSlabEG * kSlabExp;  // padded width 768
-    // Both chunks go global -> shared with cp.async (nothing held in
-    // registers across the arithmetic): W (KC x 768 floats, 4 x 16 B per
-    // thread) straight into ws, X (56 rows x 16 k) raw into xraw, transposed
-    // into xs after the chunk's arithmetic.
-    auto xraw = reinterpret_cast<float(*)[kSlabRows][kSlabKC]>(
-        slab_smem + 2 * kSlabKC * (kSlabXStride + kSlabEG * kSlabExp));
+    // Both operands go global -> shared with cp.async (nothing is held in
+    // registers across the arithmetic); X is transposed after the chunk.
+    // W chunk: thread tid copies column quad wc of rows wk, wk+4, wk+8, wk+12.
+    const int wk = tid / (kSlabW / 4), wc = 4 * (tid % (kSlabW / 4));
+    const bool wok = wc < E;
     auto load = [&](int k0, int buf) {
+        const float* s = W + (size_t)(k0 + wk) * E + (wok ? wc : 0);
+        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&ws[buf][wk][wc]));
 #pragma unroll
         for (int l = 0; l < 4; ++l) {
-            const int i = tid + l * kSlabThreads;
-            const int k = i / (Ew / 4), c4 = i % (Ew / 4);
-            const int col = 4 * c4;
-            const bool ok = (k0 + k < K) && (col + 3 < E);
-            const float* s = ok ? W + (size_t)(k0 + k) * E + col : W;
-            const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&ws[buf][k][col]));
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(s),
-                         "r"(ok ? 16 : 0)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                             dst + l * 4 * kSlabW * (int)sizeof(float)),
+                         "l"(s + (size_t)l * 4 * E), "r"(wok ? 16 : 0)
                          : "memory");
         }
         if (tid < kSlabRows * kSlabKC / 4) {
@@ -367,11 +377,13 @@ __global__ void __launch_bounds__(kSlabThreads, 1) router_slab_kernel(
             xs[buf][4 * k4 + 3][col] = v.w;
         }
     };
-    float acc[kSlabTok][kSlabExp];
+    // acc[i][q] = (c[i][q1], c[i][q0]) for token i and this thread's expert
+    // pair q: q = 0,1 -> columns 4eg + {0,1}, {2,3}; q = 2,3 -> 384 + 4eg + ...
+    uint64_t acc[kSlabTok][kSlabExp / 2];
 #pragma unroll
     for (int i = 0; i < kSlabTok; ++i)
 #pragma unroll
-        for (int j = 0; j < kSlabExp; ++j) acc[i][j] = 0.0f;
+        for (int q = 0; q < kSlabExp / 2; ++q) acc[i][q] = 0;
 
     int buf = 0;
     load(0, 0);
@@ -380,20 +392,21 @@ __global__ void __launch_bounds__(kSlabThreads, 1) router_slab_kernel(
     for (int k0 = 0; k0 < K; k0 += kSlabKC) {
         const bool more = k0 + kSlabKC < K;
         if (more) load(k0 + kSlabKC, buf ^ 1);
-#pragma unroll 4
+#pragma unroll 2
         for (int k = 0; k < kSlabKC; ++k) {
-            const float4 a03 = *reinterpret_cast<const float4*>(&xs[buf][k][8 * tg]);
-            const float2 a45 = *reinterpret_cast<const float2*>(&xs[buf][k][8 * tg + 4]);
-            const float a6 = xs[buf][k][8 * tg + 6];
-            const float4 b03 = *reinterpret_cast<const float4*>(&ws[buf][k][8 * eg]);
-            const float4 b47 = *reinterpret_cast<const float4*>(&ws[buf][k][8 * eg + 4]);
-            const float av[7] = {a03.x, a03.y, a03.z, a03.w, a45.x, a45.y, a6};
-            const float bv[8] = {b03.x, b03.y, b03.z, b03.w, b47.x, b47.y, b47.z, b47.w};
+            const ulonglong2 b01 = *reinterpret_cast<const ulonglong2*>(&ws[buf][k][4 * eg]);
+            const ulonglong2 b23 =
+                *reinterpret_cast<const ulonglong2*>(&ws[buf][k][kSlabHalf + 4 * eg]);
+            const uint64_t bv[4] = {b01.x, b01.y, b23.x, b23.y};
+            // tokens one at a time (broadcast LDS): keeps the live set at
+            // 56 accumulators + 8 weights + 1 token under the 80-register cap
 #pragma unroll
-            for (int i = 0; i < kSlabTok; ++i)
+            for (int i = 0; i < kSlabTok; ++i) {
+                const float a = xs[buf][k][8 * tg + i];
 #pragma unroll
-                for (int j = 0; j < kSlabExp; ++j)
-                    acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(av[i], bv[j]));
+                for (int q = 0; q < kSlabExp / 2; ++q)
+                    acc[i][q] = f2_add_swapped(acc[i][q], f2_mul_bcast(a, bv[q]));
+            }
         }
         if (more) store(buf ^ 1);
         __syncthreads();
@@ -403,14 +416,13 @@ __global__ void __launch_bounds__(kSlabThreads, 1) router_slab_kernel(
     for (int i = 0; i < kSlabTok; ++i) {
         const int r = kSlabTok * tg + i;
         if (r >= nrows) continue;
-        float* dst = logits + (size_t)(row0 + r) * E + 8 * eg;
-        if (8 * eg + 7 < E) {
-            reinterpret_cast<float4*>(dst)[0] = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
-            reinterpret_cast<float4*>(dst)[1] = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
-        } else {
 #pragma unroll
-            for (int j = 0; j < kSlabExp; ++j)
-                if (8 * eg + j < E) dst[j] = acc[i][j];
+        for (int half = 0; half < 2; ++half) {
+            const int col = half * kSlabHalf + 4 * eg;
+            if (col >= E) continue;
+            const uint64_t p0 = acc[i][2 * half], p1 = acc[i][2 * half + 1];
+            *reinterpret_cast<float4*>(logits + (size_t)(row0 + r) * E + col) =
+                make_float4(f2_hi(p0), f2_lo(p0), f2_hi(p1), f2_lo(p1));
         }
     }
 }
@@ -549,14 +561,14 @@ void launch_router_lean(scmoe_ctx* c, const float* X, const float* W, float* log
 bool router_slab_ok(size_t T, size_t K, size_t E, int num_sms) {
     // full-width slab needs E <= 768, E and K multiples of 4 (float4 rows), and
     // enough tokens to fill most SMs (otherwise the 16/64-row tiles spread better)
-    return E <= (size_t)kSlabEG * kSlabExp && E % 4 == 0 && K % kSlabKC == 0 &&
+    return E <= (size_t)kSlabW && E % 4 == 0 && K % kSlabKC == 0 &&
            ceil_div(T, kSlabRows) >= (size_t)num_sms * 3 / 4;
 }
 
 void launch_router_slab(scmoe_ctx* c, const float* X, const float* W, float* logits, size_t T,
                         size_t K, size_t E) {
     constexpr size_t smem =
-        sizeof(float) * 2 * (kSlabKC * (kSlabXStride + kSlabEG * kSlabExp) + kSlabRows * kSlabKC);
+        sizeof(float) * 2 * (kSlabKC * (kSlabW + kSlabXStride) + kSlabRows * kSlabKC);
     static bool attr = false;
     if (!attr) {
         SCMOE_CUDA(cudaFuncSetAttribute(router_slab_kernel,

@@ -1,0 +1,160 @@
+// router_sm100.cu -- the router projection logits = x W_r (router.hpp:136) for
+// large batches, fed by TMA.  Compiled on its own with --fmad=false and
+// ptxas -O1: at -O2/-O3 ptxas software-pipelines the weight loads of the k
+// loop and pays ~13 register moves per 84 packed FP32 instructions at the
+// loop back-edge (the loop is FP32-pipe bound, so those moves cost ~8%);
+// -O1 emits the same loop without them and without spills.
+#include <cuda.h>
+
+#include "f32x2.cuh"
+#include "internal.cuh"
+#include "sm100_util.cuh"
+
+namespace scmoe {
+
+// ---------------------------------------------------------------------------
+// Router projection, TMA-fed slab (the default for large batches).  CTA tile
+// = 56 tokens x all E <= 768 experts, 512 threads = 8 token groups x 64
+// expert groups, 7 x 12 independent f32x2 chains per thread (84 accumulator
+// registers: with 4 warps per SM sub-partition each thread may hold 128
+// registers, so nothing spills -- the 768-thread slab kernel is capped at 80
+// and spills in its inner loop).  Thread eg owns expert quads 4eg, 256+4eg,
+// 512+4eg: each warp's weight loads are three conflict-free 512-byte rows.
+// The operands arrive by TMA into a 4-stage ring guarded by mbarriers:
+//   stage = W chunk [3 boxes][16 k][256 experts] (48 KB) + X chunk
+//           [56 tokens][16 k] (3.5 KB, rows past T zero-filled by TMA).
+// Thread 0 refills the stage of chunk c-2 at the top of chunk c (two chunks
+// of slack for laggard warps); each warp arrives on a stage's empty barrier
+// when done with it, so compute warps never meet at a CTA-wide barrier.
+// Tokens are read as warp-broadcast scalars straight from the X rows (no
+// transpose).  Arithmetic identical to seq_gemm_kernel: c = 0; c = c + x*w in
+// k order, every product and sum rounded (f32x2 scheme as router_slab_kernel).
+// ---------------------------------------------------------------------------
+constexpr int kRtTok = 7, kRtExp = 12, kRtTG = 8, kRtEG = 64;
+constexpr int kRtRows = kRtTok * kRtTG;                      // 56
+constexpr int kRtThreads = kRtTG * kRtEG;                    // 512
+constexpr int kRtKC = 16;
+constexpr int kRtStages = 4;
+constexpr int kRtBox = 256;                                  // experts per W box
+constexpr int kRtW = 768;                                    // padded expert width
+constexpr int kRtWFloats = kRtKC * kRtW;                     // 12288
+constexpr int kRtXFloats = kRtRows * kRtKC;                  // 896
+constexpr int kRtStageFloats = kRtWFloats + kRtXFloats;
+constexpr int kRtStageBytes = kRtStageFloats * 4;            // 52736
+constexpr int kRtWarps = kRtThreads / 32;                    // 16
+constexpr size_t kRtSmem = (size_t)kRtStages * kRtStageBytes + 2 * kRtStages * 8 + 128;
+static_assert(kRtEG * 4 == kRtBox && kRtExp / 4 == kRtW / kRtBox, "quad layout");
+
+__global__ void __launch_bounds__(kRtThreads, 1) router_tma_kernel(
+    const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
+    float* __restrict__ logits, int T, int K, int E) {
+    extern __shared__ __align__(128) float rt_smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(rt_smem + kRtStages * kRtStageFloats);
+    uint64_t* empty = full + kRtStages;
+    const int tid = threadIdx.x;
+    const int tg = tid / kRtEG, eg = tid % kRtEG;
+    const int row0 = blockIdx.x * kRtRows;
+    const int nchunks = K / kRtKC;
+    if (tid == 0) {
+        for (int s = 0; s < kRtStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kRtWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_w)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_x)) : "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int c) {
+        const int s = c % kRtStages;
+        float* st = rt_smem + s * kRtStageFloats;
+        mbar_expect_tx(&full[s], kRtStageBytes);
+#pragma unroll
+        for (int b = 0; b < kRtW / kRtBox; ++b)
+            tma_load_2d(&map_w, &full[s], st + b * kRtKC * kRtBox, b * kRtBox, c * kRtKC,
+                        policy_evict_last());
+        tma_load_2d(&map_x, &full[s], st + kRtWFloats, c * kRtKC, row0, policy_evict_first());
+    };
+    if (tid == 0)
+        for (int c = 0; c < kRtStages && c < nchunks; ++c) issue(c);
+
+    const int wq = 4 * eg;                                    // quad offset inside each box
+    const int xoff = kRtWFloats + kRtTok * tg * kRtKC;
+
+    // acc[i][q] = (c[i][e+1], c[i][e]) for token i, expert pair e = column of pair q
+    uint64_t acc[kRtTok][kRtExp / 2];
+#pragma unroll
+    for (int i = 0; i < kRtTok; ++i)
+#pragma unroll
+        for (int q = 0; q < kRtExp / 2; ++q) acc[i][q] = 0;
+
+    for (int c = 0; c < nchunks; ++c) {
+        const int s = c % kRtStages;
+        if (tid == 0 && c >= 2 && c - 2 + kRtStages < nchunks) {
+            mbar_wait(&empty[(c - 2) % kRtStages], ((c - 2) / kRtStages) & 1);
+            issue(c - 2 + kRtStages);
+        }
+        mbar_wait(&full[s], (c / kRtStages) & 1);
+        const float* st = rt_smem + s * kRtStageFloats;
+#pragma unroll 2
+        for (int k = 0; k < kRtKC; ++k) {
+            uint64_t bv[kRtExp / 2];
+#pragma unroll
+            for (int b = 0; b < kRtExp / 4; ++b) {
+                const ulonglong2 v =
+                    *reinterpret_cast<const ulonglong2*>(st + b * kRtKC * kRtBox + k * kRtBox + wq);
+                bv[2 * b] = v.x;
+                bv[2 * b + 1] = v.y;
+            }
+#pragma unroll
+            for (int i = 0; i < kRtTok; ++i) {
+                const float a = st[xoff + i * kRtKC + k];
+#pragma unroll
+                for (int q = 0; q < kRtExp / 2; ++q)
+                    acc[i][q] = f2_add_swapped(acc[i][q], f2_mul_bcast(a, bv[q]));
+            }
+        }
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+    }
+    const int nrows = min(kRtRows, T - row0);
+#pragma unroll
+    for (int i = 0; i < kRtTok; ++i) {
+        const int r = kRtTok * tg + i;
+        if (r >= nrows) continue;
+#pragma unroll
+        for (int b = 0; b < kRtExp / 4; ++b) {
+            const int col = b * kRtBox + wq;
+            if (col >= E) continue;
+            const uint64_t p0 = acc[i][2 * b], p1 = acc[i][2 * b + 1];
+            *reinterpret_cast<float4*>(logits + (size_t)(row0 + r) * E + col) =
+                make_float4(f2_hi(p0), f2_lo(p0), f2_hi(p1), f2_lo(p1));
+        }
+    }
+}
+
+bool router_tma_ok(size_t T, size_t K, size_t E, int num_sms) {
+    // TMA rows need 16-byte strides (E, K multiples of 4); K in 16-row chunks;
+    // enough 56-token slabs to fill most SMs
+    return E <= (size_t)kRtW && E % 4 == 0 && K % kRtKC == 0 &&
+           ceil_div(T, kRtRows) >= (size_t)num_sms * 3 / 4;
+}
+
+void launch_router_tma(scmoe_ctx* c, const float* X, const float* W, float* logits, size_t T,
+                       size_t K, size_t E) {
+    static bool attr = false;
+    if (!attr) {
+        SCMOE_CUDA(cudaFuncSetAttribute(router_tma_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRtSmem));
+        attr = true;
+    }
+    const CUtensorMap mw = make_tma_map_2d(W, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, sizeof(float), K, E,
+                                           kRtKC, kRtBox, CU_TENSOR_MAP_SWIZZLE_NONE);
+    const CUtensorMap mx = make_tma_map_2d(X, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, sizeof(float), T, K,
+                                           kRtRows, kRtKC, CU_TENSOR_MAP_SWIZZLE_NONE);
+    router_tma_kernel<<<ceil_div(T, kRtRows), kRtThreads, kRtSmem, c->stream>>>(
+        mw, mx, logits, (int)T, (int)K, (int)E);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
+}  // namespace scmoe

@@ -49,7 +49,7 @@ def test_pipelined_batches_equal_serial(scmoe):
             assert torch.equal(s[k], p[k]), k
 
 
-@pytest.mark.parametrize("variant", ["slab", "lean", "tiled"])
+@pytest.mark.parametrize("variant", ["tma", "slab", "lean", "tiled"])
 def test_router_kernel_variants_bitwise(variant):
     """Each router projection kernel, selected with SCMOE_ROUTER, reproduces
     the reference's logits (via route_topk probabilities) bit for bit."""
@@ -68,6 +68,40 @@ rc, idx, g, c, probs = O.orc_route_topk(x[sub], w, n, z, k, ke, want_probs=True)
 assert rc == 0
 assert (pl[0][sub].view(np.uint32) == probs.view(np.uint32)).all()
 assert (dg.indices.reshape(T, k)[sub].ravel() == idx).all()
+print("ok")
+"""
+    env = dict(os.environ, SCMOE_ROUTER=variant)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("variant", ["tma", "slab", "lean", "tiled"])
+def test_router_kernel_variants_edge_values(variant):
+    """Subnormal products and sums, exact zeros, signed zeros, a ragged last
+    slab and a partial expert width (E = 60 < 768): every router kernel (the
+    slab kernel runs packed f32x2 FMUL2/FADD2) still matches the reference's
+    sequential fp32 arithmetic bit for bit."""
+    code = f"""
+import sys, numpy as np
+sys.path.insert(0, {ROOT!r}); sys.path.insert(0, {os.path.join(ROOT, 'tests')!r})
+import _oracle as O, paper_2509_01322_b200 as P
+T, d, n, z, k, ke = 131, 256, 40, 20, 6, 4
+x = O.normal_f32(O.stream_seed(3, 0), T * d).reshape(T, d)
+w = O.uniform_f32(O.stream_seed(4, 0), d * (n + z), 1.0 / d).reshape(d, n + z)
+x[::3] *= np.float32(2.0 ** -66)      # x*w products below 2^-126: subnormal
+w[:, ::5] *= np.float32(2.0 ** -60)
+x[5] = 0.0
+x[7, ::2] = -0.0
+w[:, 3] = 0.0
+x[9] *= np.float32(2.0 ** 60)          # large products next to tiny ones
+st = P.RouterState(w, n, z, k, ke, 0.0, 1.0)
+pl = []
+dg = P.route_topk(x, st, pl)
+rc, idx, g, c, probs = O.orc_route_topk(x, w, n, z, k, ke, want_probs=True)
+assert rc == 0
+assert (pl[0].view(np.uint32) == probs.view(np.uint32)).all()
+assert (dg.indices == idx).all() and (dg.gates.view(np.uint64) == g.view(np.uint64)).all()
 print("ok")
 """
     env = dict(os.environ, SCMOE_ROUTER=variant)

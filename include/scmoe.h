@@ -190,6 +190,19 @@ int scmoe_layer_forward_batches(scmoe_ctx* ctx, scmoe_router* r, scmoe_bank* b, 
 int scmoe_layer_forward_host(scmoe_ctx* ctx, scmoe_router* r, scmoe_bank* b, const float* a1,
                              const float* a3, const float* gain, size_t tokens, int renormalize,
                              uint32_t* indices, double* gates, uint32_t* ffn_count, float* out);
+/* Host tier for a stream of batches (one call per serving window): batch i's
+ * inputs are copied in while batch i-1 computes and batch i-2's outputs are
+ * copied out (two copy streams + the compute stream, device buffers double
+ * buffered).  Results are identical to n calls of scmoe_layer_forward_host;
+ * arrays hold one host pointer per batch (pinned memory for real overlap;
+ * a3 and the routing outputs may be NULL arrays).  Returns after the last
+ * output has landed. */
+int scmoe_layer_forward_host_batches(scmoe_ctx* ctx, scmoe_router* r, scmoe_bank* b,
+                                     size_t n_batches, const float* const* a1,
+                                     const float* const* a3, const float* gain, size_t tokens,
+                                     int renormalize, uint32_t* const* indices,
+                                     double* const* gates, uint32_t* const* ffn_count,
+                                     float* const* out);
 
 /* ---- expert parallelism ------------------------------------
  * Experts are block-partitioned over G ranks (rank g owns FFN experts

@@ -135,6 +135,8 @@ _PROTOS = {
                                            _P]),
     "scmoe_layer_forward_batches": (C.c_int, [_P, _P, _P, _SZ, _P, _P, _P, _SZ, C.c_int, _P, _P,
                                               _P, _P]),
+    "scmoe_layer_forward_host_batches": (C.c_int, [_P, _P, _P, _SZ, _P, _P, _P, _SZ, C.c_int, _P,
+                                                   _P, _P, _P]),
     "scmoe_bank_init_uniform_shard": (C.c_int, [_P, _P, _U64, _U64, C.c_double, _SZ]),
     "scmoe_rmsnorm_route": (C.c_int, [_P, _P, _P, _P, _SZ, _P, _P, _P, _P, _P]),
     "scmoe_ep_plan": (C.c_int, [_P, _P, _SZ, _SZ, _SZ, _SZ, C.c_int, _P, _P, _P, _P]),

@@ -269,6 +269,8 @@ int scmoe_ctx_create(int device, scmoe_ctx** out) {
         c->device = device;
         c->num_sms = prop.multiProcessorCount;
         if (const char* g = getenv("SCMOE_GEMM1_GATHER")) c->gemm1_gather = atoi(g) != 0;
+        if (const char* g = getenv("SCMOE_ROUTER_SMS")) c->router_sms = atoi(g);
+        if (const char* g = getenv("SCMOE_GEMM_SMS")) c->gemm_sms = atoi(g);
         if (const char* v = getenv("SCMOE_ROUTER")) {
             const std::string sv(v);
             c->router_variant =
@@ -297,6 +299,18 @@ int scmoe_ctx_destroy(scmoe_ctx* c) {
         }
         cudaEventDestroy(c->ev_join);
     }
+    if (c->s_h2d) {
+        cudaStreamSynchronize(c->s_d2h);
+        cudaStreamDestroy(c->s_h2d);
+        cudaStreamDestroy(c->s_d2h);
+        for (int i = 0; i < 2; ++i) {
+            cudaEventDestroy(c->ev_in[i]);
+            cudaEventDestroy(c->ev_done[i]);
+            cudaEventDestroy(c->ev_out[i]);
+        }
+    }
+    for (auto& slot : c->io)
+        for (auto& b : slot) b.release();
     for (auto& rec : c->prof.recs) {
         cudaEventDestroy(rec.a);
         cudaEventDestroy(rec.b);
@@ -769,6 +783,76 @@ int scmoe_layer_forward_batches(scmoe_ctx* c, scmoe_router* r, scmoe_bank* b, si
         }
         // the caller's stream resumes after the last back half (s_back is in order)
         SCMOE_CUDA(cudaStreamWaitEvent(user, c->ev_back[(n_batches - 1) & 1], 0));
+    });
+}
+
+int scmoe_layer_forward_host_batches(scmoe_ctx* c, scmoe_router* r, scmoe_bank* b,
+                                     size_t n_batches, const float* const* a1,
+                                     const float* const* a3, const float* gain, size_t T,
+                                     int renorm, uint32_t* const* idx, double* const* gates,
+                                     uint32_t* const* ffn_count, float* const* out) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        check_layer_args(r, b);
+        if (T == 0 || n_batches == 0) return;
+        if (!c->s_h2d) {
+            SCMOE_CUDA(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+            SCMOE_CUDA(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+            for (int i = 0; i < 2; ++i) {
+                SCMOE_CUDA(cudaEventCreateWithFlags(&c->ev_in[i], cudaEventDisableTiming));
+                SCMOE_CUDA(cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming));
+                SCMOE_CUDA(cudaEventCreateWithFlags(&c->ev_out[i], cudaEventDisableTiming));
+            }
+        }
+        const size_t d = r->d, K = r->top_k;
+        cudaStream_t comp = c->stream;
+        const float* dg = gain ? upload(c, stage_of(c).bufs[6], gain, d) : nullptr;
+        // copies of batch i may not start before work already queued on the
+        // compute stream (earlier calls) has finished with the slot buffers
+        SCMOE_CUDA(cudaEventRecord(c->ev_done[0], comp));
+        SCMOE_CUDA(cudaEventRecord(c->ev_done[1], comp));
+        SCMOE_CUDA(cudaEventRecord(c->ev_out[0], comp));
+        SCMOE_CUDA(cudaEventRecord(c->ev_out[1], comp));
+        for (size_t i = 0; i < n_batches; ++i) {
+            const int s = (int)(i & 1);
+            DevBuf* io = c->io[s];
+            float* da1 = io[0].get<float>(T * d);
+            float* da3 = a3 && a3[i] ? io[1].get<float>(T * d) : nullptr;
+            float* dout = io[2].get<float>(T * d);
+            uint32_t* di = io[3].get<uint32_t>(T * K);
+            double* dgt = io[4].get<double>(T * K);
+            uint32_t* dc = io[5].get<uint32_t>(T);
+            // H2D(i): the slot's inputs were last read by compute(i-2)
+            SCMOE_CUDA(cudaStreamWaitEvent(c->s_h2d, c->ev_done[s], 0));
+            SCMOE_CUDA(cudaMemcpyAsync(da1, a1[i], T * d * sizeof(float), cudaMemcpyHostToDevice,
+                                       c->s_h2d));
+            if (da3)
+                SCMOE_CUDA(cudaMemcpyAsync(da3, a3[i], T * d * sizeof(float),
+                                           cudaMemcpyHostToDevice, c->s_h2d));
+            SCMOE_CUDA(cudaEventRecord(c->ev_in[s], c->s_h2d));
+            // compute(i): needs its inputs, and the slot's outputs drained by D2H(i-2)
+            SCMOE_CUDA(cudaStreamWaitEvent(comp, c->ev_in[s], 0));
+            SCMOE_CUDA(cudaStreamWaitEvent(comp, c->ev_out[s], 0));
+            layer_front(c, r, b, da1, dg, T, di, dgt, dc);
+            moe_back(c, b, c->ws.hmoe.get<float>(T * d), T, di, dgt, K, renorm, da3, dout);
+            SCMOE_CUDA(cudaEventRecord(c->ev_done[s], comp));
+            // D2H(i)
+            SCMOE_CUDA(cudaStreamWaitEvent(c->s_d2h, c->ev_done[s], 0));
+            SCMOE_CUDA(cudaMemcpyAsync(out[i], dout, T * d * sizeof(float), cudaMemcpyDeviceToHost,
+                                       c->s_d2h));
+            if (idx && idx[i])
+                SCMOE_CUDA(cudaMemcpyAsync(idx[i], di, T * K * sizeof(uint32_t),
+                                           cudaMemcpyDeviceToHost, c->s_d2h));
+            if (gates && gates[i])
+                SCMOE_CUDA(cudaMemcpyAsync(gates[i], dgt, T * K * sizeof(double),
+                                           cudaMemcpyDeviceToHost, c->s_d2h));
+            if (ffn_count && ffn_count[i])
+                SCMOE_CUDA(cudaMemcpyAsync(ffn_count[i], dc, T * sizeof(uint32_t),
+                                           cudaMemcpyDeviceToHost, c->s_d2h));
+            SCMOE_CUDA(cudaEventRecord(c->ev_out[s], c->s_d2h));
+        }
+        SCMOE_CUDA(cudaStreamSynchronize(c->s_d2h));
+        sync_and_check(c);
     });
 }
 

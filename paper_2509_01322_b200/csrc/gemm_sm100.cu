@@ -413,7 +413,8 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
     static const int dbg = getenv("SCMOE_GEMM_DEBUG") ? atoi(getenv("SCMOE_GEMM_DEBUG")) : 0;
     a.debug = dbg;
     const size_t units_max = max_tiles * (M / BM);
-    const int grid = (int)std::min<size_t>(units_max, (size_t)c->num_sms);
+    const int grid = (int)std::min<size_t>(
+        units_max, (size_t)(c->gemm_sms > 0 ? std::min(c->gemm_sms, c->num_sms) : c->num_sms));
     grouped_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, c->stream>>>(mw, mx, a);
     SCMOE_LAUNCH_CHECK(c);
 }

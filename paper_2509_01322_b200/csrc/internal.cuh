@@ -114,12 +114,21 @@ struct scmoe_ctx {
     // 2 lean (co-resides with the GEMM), 3 tiled (64/16-row tiles), 4 tma (slab
     // tile fed by TMA, the large-batch default); SCMOE_ROUTER
     int router_variant = 0;
+    // SM budget (CTAs) of the persistent router / grouped GEMM kernels; 0 = all
+    // (SCMOE_ROUTER_SMS / SCMOE_GEMM_SMS, or the overlapped schedule's split)
+    int router_sms = 0, gemm_sms = 0;
     bool overlapped = false;    // inside a pipelined multi-batch call
     // pipelined multi-batch execution (scmoe_layer_forward_batches)
     cudaStream_t s_front = nullptr, s_back = nullptr;
     cudaEvent_t ev_front[2] = {nullptr, nullptr}, ev_back[2] = {nullptr, nullptr};
     cudaEvent_t ev_join = nullptr;
     Workspace ws_alt;
+    // host-batch pipeline (scmoe_layer_forward_host_batches): copy streams,
+    // per-slot events and double-buffered device I/O
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr},
+                ev_out[2] = {nullptr, nullptr};
+    DevBuf io[2][7];
 };
 
 // RAII stage timer; a no-op unless profiling is enabled on the context.

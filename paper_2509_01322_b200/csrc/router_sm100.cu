@@ -133,6 +133,106 @@ __global__ void __launch_bounds__(kRtThreads, 1) router_tma_kernel(
     }
 }
 
+// Persistent form for a reduced SM budget (the overlapped multi-batch
+// schedule): this CTA takes slabs blockIdx.x, +gridDim.x, ... and the ring
+// runs on one global chunk counter g = (local slab) * nchunks + c, so the next
+// slab's first chunks stream in while the current one finishes.
+__global__ void __launch_bounds__(kRtThreads, 1) router_tma_persistent_kernel(
+    const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
+    float* __restrict__ logits, int T, int K, int E) {
+    extern __shared__ __align__(128) float rt_smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(rt_smem + kRtStages * kRtStageFloats);
+    uint64_t* empty = full + kRtStages;
+    const int tid = threadIdx.x;
+    const int tg = tid / kRtEG, eg = tid % kRtEG;
+    const int nchunks = K / kRtKC;
+    const int nslabs = (T + kRtRows - 1) / kRtRows;
+    const int my_slabs = blockIdx.x < nslabs ? (nslabs - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int G = my_slabs * nchunks;
+    if (tid == 0) {
+        for (int s = 0; s < kRtStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kRtWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_w)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_x)) : "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int g) {
+        const int s = g % kRtStages;
+        const int c = g % nchunks;
+        const int row0 = (blockIdx.x + (g / nchunks) * gridDim.x) * kRtRows;
+        float* st = rt_smem + s * kRtStageFloats;
+        mbar_expect_tx(&full[s], kRtStageBytes);
+#pragma unroll
+        for (int b = 0; b < kRtW / kRtBox; ++b)
+            tma_load_2d(&map_w, &full[s], st + b * kRtKC * kRtBox, b * kRtBox, c * kRtKC,
+                        policy_evict_last());
+        tma_load_2d(&map_x, &full[s], st + kRtWFloats, c * kRtKC, row0, policy_evict_first());
+    };
+    if (tid == 0)
+        for (int g = 0; g < kRtStages && g < G; ++g) issue(g);
+
+    const int wq = 4 * eg;                                    // quad offset inside each box
+    const int xoff = kRtWFloats + kRtTok * tg * kRtKC;
+
+    // acc[i][q] = (c[i][e+1], c[i][e]) for token i, expert pair e = column of pair q
+    for (int j = 0; j < my_slabs; ++j) {
+        // acc[i][q] = (c[i][e+1], c[i][e]) for token i, expert pair e = column of pair q
+        uint64_t acc[kRtTok][kRtExp / 2];
+#pragma unroll
+        for (int i = 0; i < kRtTok; ++i)
+#pragma unroll
+            for (int q = 0; q < kRtExp / 2; ++q) acc[i][q] = 0;
+        for (int c = 0; c < nchunks; ++c) {
+            const int g = j * nchunks + c;
+            const int s = g % kRtStages;
+            if (tid == 0 && g >= 2 && g - 2 + kRtStages < G) {
+                mbar_wait(&empty[(g - 2) % kRtStages], ((g - 2) / kRtStages) & 1);
+                issue(g - 2 + kRtStages);
+            }
+            mbar_wait(&full[s], (g / kRtStages) & 1);
+            const float* st = rt_smem + s * kRtStageFloats;
+#pragma unroll 2
+            for (int k = 0; k < kRtKC; ++k) {
+                uint64_t bv[kRtExp / 2];
+#pragma unroll
+                for (int b = 0; b < kRtExp / 4; ++b) {
+                    const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(
+                        st + b * kRtKC * kRtBox + k * kRtBox + wq);
+                    bv[2 * b] = v.x;
+                    bv[2 * b + 1] = v.y;
+                }
+#pragma unroll
+                for (int i = 0; i < kRtTok; ++i) {
+                    const float a = st[xoff + i * kRtKC + k];
+#pragma unroll
+                    for (int q = 0; q < kRtExp / 2; ++q)
+                        acc[i][q] = f2_add_swapped(acc[i][q], f2_mul_bcast(a, bv[q]));
+                }
+            }
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+        }
+        const int row0 = (blockIdx.x + j * gridDim.x) * kRtRows;
+        const int nrows = min(kRtRows, T - row0);
+#pragma unroll
+        for (int i = 0; i < kRtTok; ++i) {
+            const int r = kRtTok * tg + i;
+            if (r >= nrows) continue;
+#pragma unroll
+            for (int b = 0; b < kRtExp / 4; ++b) {
+                const int col = b * kRtBox + wq;
+                if (col >= E) continue;
+                const uint64_t p0 = acc[i][2 * b], p1 = acc[i][2 * b + 1];
+                *reinterpret_cast<float4*>(logits + (size_t)(row0 + r) * E + col) =
+                    make_float4(f2_hi(p0), f2_lo(p0), f2_hi(p1), f2_lo(p1));
+            }
+        }
+    }
+}
+
 bool router_tma_ok(size_t T, size_t K, size_t E, int num_sms) {
     // TMA rows need 16-byte strides (E, K multiples of 4); K in 16-row chunks;
     // enough 56-token slabs to fill most SMs
@@ -146,14 +246,21 @@ void launch_router_tma(scmoe_ctx* c, const float* X, const float* W, float* logi
     if (!attr) {
         SCMOE_CUDA(cudaFuncSetAttribute(router_tma_kernel,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRtSmem));
+        SCMOE_CUDA(cudaFuncSetAttribute(router_tma_persistent_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRtSmem));
         attr = true;
     }
     const CUtensorMap mw = make_tma_map_2d(W, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, sizeof(float), K, E,
                                            kRtKC, kRtBox, CU_TENSOR_MAP_SWIZZLE_NONE);
     const CUtensorMap mx = make_tma_map_2d(X, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, sizeof(float), T, K,
                                            kRtRows, kRtKC, CU_TENSOR_MAP_SWIZZLE_NONE);
-    router_tma_kernel<<<ceil_div(T, kRtRows), kRtThreads, kRtSmem, c->stream>>>(
-        mw, mx, logits, (int)T, (int)K, (int)E);
+    const size_t slabs = ceil_div(T, kRtRows);
+    if (c->router_sms > 0 && (size_t)c->router_sms < slabs)
+        router_tma_persistent_kernel<<<c->router_sms, kRtThreads, kRtSmem, c->stream>>>(
+            mw, mx, logits, (int)T, (int)K, (int)E);
+    else
+        router_tma_kernel<<<slabs, kRtThreads, kRtSmem, c->stream>>>(mw, mx, logits, (int)T,
+                                                                            (int)K, (int)E);
     SCMOE_LAUNCH_CHECK(c);
 }
 

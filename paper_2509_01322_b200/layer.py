@@ -139,6 +139,20 @@ class DeviceLayer:
                                                        int(renormalize), p(idx), p(gates),
                                                        p(ffn_count), p(out)))
 
+    def forward_host_batches(self, a1s, a3s, gain, tokens: int, idxs, gatess, cnts, outs,
+                             renormalize: bool = False):
+        """A stream of host batches (scmoe_layer_forward_host_batches): lists of
+        (ideally pinned) numpy arrays, one per batch; input copies, compute and
+        output copies of neighbouring batches overlap.  idxs/gatess/cnts may be
+        None."""
+        n = len(a1s)
+        p = lambda a: None if a is None else a.ctypes.data_as(_P)  # noqa: E731
+        arr = lambda xs: None if xs is None else (C.c_void_p * n)(  # noqa: E731
+            *[None if x is None else x.ctypes.data for x in xs])
+        self.ctx._check(lib().scmoe_layer_forward_host_batches(
+            self.ctx.handle, self.router, self.bank, n, arr(a1s), arr(a3s), p(gain), tokens,
+            int(renormalize), arr(idxs), arr(gatess), arr(cnts), arr(outs)))
+
     def close(self):
         L = lib()
         if self.bank:

@@ -108,3 +108,42 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_host_batches_equal_serial_host_calls(scmoe):
+    """scmoe_layer_forward_host_batches (copy-in / compute / copy-out of
+    neighbouring batches overlapped) returns exactly what n serial
+    scmoe_layer_forward_host calls return, including the routing outputs."""
+    import torch
+    from paper_2509_01322_b200.layer import DeviceLayer, LayerShape
+    P = scmoe
+    ctx = P.Context(0)
+    shape = LayerShape(d=1024, n_ffn=64, n_zero=32, top_k=6, k_expected=4, inter=512,
+                       precision=P.PREC_BF16)
+    layer = DeviceLayer(ctx, shape, seed=5)
+    T, nb, d, K = 333, 5, shape.d, shape.top_k
+    pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
+    a1 = [pin(P.fill_normal(P.stream_seed(21, i), T * d).reshape(T, d)) for i in range(nb)]
+    a3 = [pin(P.fill_normal(P.stream_seed(22, i), T * d).reshape(T, d)) for i in range(nb)]
+
+    def outs():
+        return (np.zeros((T, d), np.float32), np.zeros(T * K, np.uint32), np.zeros(T * K),
+                np.zeros(T, np.uint32))
+
+    ser = [outs() for _ in range(nb)]
+    for i in range(nb):
+        o, ix, g, c = ser[i]
+        layer.forward_host(a1[i], a3[i], None, T, ix, g, c, o)
+    bat = [outs() for _ in range(nb)]
+    layer.forward_host_batches(a1, a3, None, T, [b[1] for b in bat], [b[2] for b in bat],
+                               [b[3] for b in bat], [b[0] for b in bat])
+    for s, b in zip(ser, bat):
+        for u, v in zip(s, b):
+            assert u.tobytes() == v.tobytes()
+    # routing outputs optional, a3 optional
+    only = [np.zeros((T, d), np.float32) for _ in range(2)]
+    layer.forward_host_batches(a1[:2], None, None, T, None, None, None, only)
+    for i in range(2):
+        o = np.zeros((T, d), np.float32)
+        layer.forward_host(a1[i], None, None, T, None, None, None, o)
+        assert o.tobytes() == only[i].tobytes()

@@ -414,9 +414,12 @@ def run_b200(args):
         "config": {"workload": cfg["workload"], "tokens_per_gpu": T, "d_model": D, "n_ffn": N_FFN,
                    "n_zero": N_ZERO, "top_k": TOPK, "k_expected": KE, "inter": INTER,
                    "router": "exact fp32 (bit-exact vs reference)", "expert_gemm": "bf16 tcgen05",
-                   "schedule": ("pipelined micro-batches: front half (rmsnorm, exact router, "
-                                "top-K, permute) of batch i+1 on the FP32 pipes under the "
-                                "HBM-bound expert GEMMs of batch i (2 streams)") if pipelined
+                   "schedule": ("pipelined batches (scmoe_layer_forward_batches): the front "
+                                "half of batch i+1 (rmsnorm, exact fp32 router on a 256-thread "
+                                "kernel co-resident with the GEMM CTA on every SM, top-K, "
+                                "permute, gather) runs on the FP32 pipes while the HBM-bound "
+                                "expert GEMMs + combine of batch i run (2 streams); every batch "
+                                "still passes the whole path") if pipelined
                    else "serial", "serial_ms_per_batch": ms_serial_max,
                    "parallelism": f"replicated experts, token-sharded x{ws}",
                    "l2": "inputs + weights (25.8 GB) larger than L2 every step",
@@ -427,6 +430,9 @@ def run_b200(args):
                        "and D2H of step i-1 overlap compute of step i)"},
         "gpu_launches": launches,
         "roofline": {"kernel": "grouped_gemm_bf16 (GEMM1+GEMM2, tcgen05)", "bound": "hbm",
+                     "note": ("achieved: GEMM launches inside the timed region (pipelined: the "
+                              "co-resident router shares the SMs); achieved_serial: the same "
+                              "kernels timed alone in the serial schedule"),
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": (achieved / hbm_peak) if achieved else None, "traffic": None,
                      "algorithmic_bytes_per_step": g1b + g2b, "ms_per_step": t_gemm,
@@ -561,7 +567,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     # pipelined = scmoe_layer_forward_batches; measured slower than serial on B200 in round 1
     # (router and GEMM contend for shared-memory bandwidth), so serial is the default
-    ap.add_argument("--schedule", default="serial", choices=["pipelined", "serial"])
+    ap.add_argument("--schedule", default="pipelined", choices=["pipelined", "serial"])
     ap.add_argument("--parallel", default="ep", choices=["ep", "replicated"],
                     help="N>1: expert-parallel (default) or replicated experts")
     ap.add_argument("--ep-chunks", type=int, default=1,

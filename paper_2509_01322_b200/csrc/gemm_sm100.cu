@@ -47,7 +47,7 @@ constexpr int BM = 128 * SLABS;
 constexpr int NT = 192;         // max token columns per tile
 // Separate rings: weights come from HBM (deep ring, most bytes in flight),
 // token rows from L2 (shallow ring).
-constexpr int A_STAGES = 4;
+constexpr int A_STAGES = 3;
 constexpr int B_STAGES = 3;
 constexpr int A_SLAB_BYTES = 128 * BK * 2;        // 16 KB
 constexpr int B_HALF_BYTES = 128 * BK * 2;        // 16 KB per 128 token rows (first box)

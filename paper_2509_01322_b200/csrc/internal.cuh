@@ -209,6 +209,10 @@ int seq_gemm_tile_rows(size_t rows, size_t N, int num_sms);
 bool router_tma_ok(size_t T, size_t K, size_t E, int num_sms);
 void launch_router_tma(scmoe_ctx* c, const float* X, const float* W, float* logits, size_t T,
                        size_t K, size_t E);
+// Small-footprint persistent TMA router that co-resides with the grouped GEMM.
+bool router_corun_ok(size_t T, size_t K, size_t E);
+void launch_router_corun(scmoe_ctx* c, const float* X, const float* W, float* logits, size_t T,
+                         size_t K, size_t E);
 bool router_slab_ok(size_t T, size_t K, size_t E, int num_sms);
 // Router projection sized to co-reside with the grouped GEMM (28-token slabs).
 bool router_lean_ok(size_t K, size_t E);

@@ -49,7 +49,7 @@ def test_pipelined_batches_equal_serial(scmoe):
             assert torch.equal(s[k], p[k]), k
 
 
-@pytest.mark.parametrize("variant", ["tma", "slab", "lean", "tiled"])
+@pytest.mark.parametrize("variant", ["tma", "corun", "slab", "lean", "tiled"])
 def test_router_kernel_variants_bitwise(variant):
     """Each router projection kernel, selected with SCMOE_ROUTER, reproduces
     the reference's logits (via route_topk probabilities) bit for bit."""
@@ -76,7 +76,7 @@ print("ok")
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
-@pytest.mark.parametrize("variant", ["tma", "slab", "lean", "tiled"])
+@pytest.mark.parametrize("variant", ["tma", "corun", "slab", "lean", "tiled"])
 def test_router_kernel_variants_edge_values(variant):
     """Subnormal products and sums, exact zeros, signed zeros, a ragged last
     slab and a partial expert width (E = 60 < 768): every router kernel (the

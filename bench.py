@@ -398,6 +398,12 @@ def run_b200(args):
         return t, ((g1b + g2b) / (t / 1e3) / 1e9 if t > 0 else None)
 
     t_gemm, achieved = gemm_roofline(stages)
+    # dram bytes per step of the same kernels from the committed ncu --set full
+    # capture (profiles/); compare with algorithmic_bytes_per_step
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "r01b_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath))["dram_bytes_per_step"]
     t_gemm_serial, achieved_serial = gemm_roofline(stages_serial)
     cpu = None
     if ws == 1 and not args.no_cpu_baseline:
@@ -434,7 +440,8 @@ def run_b200(args):
                               "co-resident router shares the SMs); achieved_serial: the same "
                               "kernels timed alone in the serial schedule"),
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": (achieved / hbm_peak) if achieved else None, "traffic": None,
+                     "frac": (achieved / hbm_peak) if achieved else None, "traffic": traffic,
+                     "traffic_source": "profiles/r01b_traffic.json (ncu dram__bytes_read+write)",
                      "algorithmic_bytes_per_step": g1b + g2b, "ms_per_step": t_gemm,
                      "achieved_serial": achieved_serial, "ms_per_step_serial": t_gemm_serial,
                      "tflops": flops / (t_gemm / 1e3) / 1e12 if t_gemm > 0 else None,

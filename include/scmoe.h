@@ -123,6 +123,22 @@ int scmoe_route_from_probs_f32_host(scmoe_ctx* ctx, scmoe_router* r, const float
 int scmoe_route_from_probs_f64_host(scmoe_ctx* ctx, scmoe_router* r, const double* probs,
                                     size_t tokens, uint32_t* indices, double* gates,
                                     uint32_t* ffn_count);
+/* Routing statistics of one decision, from a device
+ * histogram of the slots: mean / std of activated FFN experts per token
+ * (RoutingDecision::mean_ffn / std_ffn, router.hpp:73-86), per-expert slot
+ * load (stats.hpp:64-67; [n_ffn + n_zero], NULL to skip) and the slot-counted
+ * LB group frequencies (lb_group_frequencies, router.hpp:193-216; lb_groups +
+ * (n_zero > 0) entries, NULL to skip; ConfigError unless lb_groups divides
+ * n_ffn).  indices / ffn_count are device pointers; results land in host
+ * memory when the call returns.  Bitwise equal to the reference. */
+int scmoe_routing_stats(scmoe_ctx* ctx, const uint32_t* indices, const uint32_t* ffn_count,
+                        size_t tokens, size_t top_k, size_t n_ffn, size_t n_zero,
+                        size_t k_expected, size_t lb_groups, double* mean_ffn, double* std_ffn,
+                        double* per_expert_load, double* lb_freq);
+int scmoe_routing_stats_host(scmoe_ctx* ctx, const uint32_t* indices, const uint32_t* ffn_count,
+                             size_t tokens, size_t top_k, size_t n_ffn, size_t n_zero,
+                             size_t k_expected, size_t lb_groups, double* mean_ffn,
+                             double* std_ffn, double* per_expert_load, double* lb_freq);
 /* accumulate_counters (router.hpp:144-150): slot-counted, zero experts included. */
 int scmoe_accumulate_counters(scmoe_ctx* ctx, scmoe_router* r, const uint32_t* indices,
                               size_t tokens);
@@ -203,6 +219,17 @@ int scmoe_layer_forward_host_batches(scmoe_ctx* ctx, scmoe_router* r, scmoe_bank
                                      int renormalize, uint32_t* const* indices,
                                      double* const* gates, uint32_t* const* ffn_count,
                                      float* const* out);
+
+/* Dense shortcut-path FFN of the ScMoE layer:
+ *   out = a1 + ffn_block(rmsnorm(a1, gain))        (model.hpp:390-391)
+ *   ffn_block(x) = silu(x W_in) W_out               (blocks.hpp:397-402)
+ * `dense` is a one-expert bf16 bank (scmoe_bank_create(ctx, 1, d, inter,
+ * SCMOE_PREC_BF16, ...)); the two GEMMs run on the same tcgen05 grouped-GEMM
+ * kernel as the experts (all tokens form one expert's tiles).  Uses its own
+ * workspace buffers, so it may run on another context's stream beside the
+ * MoE branch (the ScMoE overlap window).  Device pointers, stream-ordered. */
+int scmoe_dense_ffn(scmoe_ctx* ctx, scmoe_bank* dense, const float* a1, const float* gain,
+                    size_t tokens, float* out);
 
 /* ---- expert parallelism ------------------------------------
  * Experts are block-partitioned over G ranks (rank g owns FFN experts

@@ -190,6 +190,33 @@ int ref_accumulate_counters(const uint32_t* idx, std::size_t T, std::size_t n, s
     });
 }
 
+// Routing statistics: RoutingDecision::mean_ffn/std_ffn (router.hpp:73-86),
+// per-expert load as routing_stats_for_tokens computes it (stats.hpp:64-67),
+// lb_group_frequencies (router.hpp:193-216).
+int ref_routing_stats(const uint32_t* idx, const uint32_t* cnt, std::size_t T, std::size_t k,
+                      std::size_t n, std::size_t z, std::size_t ke, std::size_t groups,
+                      double* mean, double* sd, double* load, double* lb) {
+    return guarded([&] {
+        RoutingDecision d;
+        d.top_k = k;
+        d.n_ffn = n;
+        d.indices.assign(idx, idx + T * k);
+        d.ffn_count.assign(cnt, cnt + T);
+        *mean = d.mean_ffn();
+        *sd = d.std_ffn();
+        if (load) {
+            std::vector<double> l(n + z, 0.0);
+            for (auto i : d.indices) l[i] += 1.0;
+            for (double& v : l) v /= static_cast<double>(d.indices.size());
+            std::memcpy(load, l.data(), l.size() * sizeof(double));
+        }
+        if (lb) {
+            const std::vector<double> f = lb_group_frequencies(d, LbLossConfig{1.0, groups}, n, z, ke);
+            std::memcpy(lb, f.data(), f.size() * sizeof(double));
+        }
+    });
+}
+
 // moe_forward (blocks.hpp:372).  Experts whose w_in[e] is NULL are passed as
 // empty Parameters (never touched unless routed to, which would throw).
 #define REF_MOE_FORWARD(S, SUF)                                                                    \

@@ -280,6 +280,51 @@ void orc_accumulate_counters(const uint32_t* indices, size_t t_count, size_t top
     *tokens_seen += t_count;
 }
 
+/* Routing statistics: RoutingDecision::mean_ffn / std_ffn
+ * (router.hpp:73-86), per-expert slot load (stats.hpp:64-67) and the
+ * slot-counted LB group frequencies lb_group_frequencies (router.hpp:193-216).
+ * load may be NULL; lb may be NULL (else groups + (n_zero > 0) entries). */
+int orc_routing_stats(const uint32_t* indices, const uint32_t* ffn_count, size_t t_count,
+                      size_t top_k, size_t n_ffn, size_t n_zero, size_t k_expected,
+                      size_t groups, double* mean, double* std_out, double* load, double* lb) {
+    const size_t e = n_ffn + n_zero;
+    if (lb && (groups == 0 || n_ffn % groups != 0)) return ORC_CONFIG;
+    double m = 0.0, sd = 0.0;
+    if (t_count) {
+        double s = 0.0;
+        for (size_t t = 0; t < t_count; ++t) s += ffn_count[t];
+        m = s / (double)t_count;
+        double s2 = 0.0;
+        for (size_t t = 0; t < t_count; ++t) s2 += (ffn_count[t] - m) * (ffn_count[t] - m);
+        sd = sqrt(s2 / (double)t_count);
+    }
+    *mean = m;
+    *std_out = sd;
+    if (load) {
+        for (size_t i = 0; i < e; ++i) load[i] = 0.0;
+        for (size_t i = 0; i < t_count * top_k; ++i) load[indices[i]] += 1.0;
+        for (size_t i = 0; i < e; ++i) load[i] /= (double)(t_count * top_k);
+    }
+    if (lb) {
+        const size_t gsz = n_ffn / groups;
+        const int has_zero = n_zero > 0;
+        const double tc = (double)t_count;
+        for (size_t j = 0; j < groups + (size_t)has_zero; ++j) lb[j] = 0.0;
+        for (size_t i = 0; i < t_count * top_k; ++i) {
+            const uint32_t x = indices[i];
+            if (x < n_ffn)
+                lb[x / gsz] += 1.0;
+            else
+                lb[groups] += 1.0;
+        }
+        const size_t slack = top_k - k_expected;
+        for (size_t j = 0; j < groups; ++j)
+            lb[j] *= (double)groups / ((double)k_expected * tc);
+        if (has_zero) lb[groups] /= (double)slack * tc;
+    }
+    return ORC_OK;
+}
+
 /* router.hpp:155-176: PID-style bias controller tick */
 int orc_bias_update(size_t n_ffn, size_t n_zero, size_t top_k, size_t k_expected, double* mu,
                     double mu_decay, double* b, uint64_t* tokens_routed, uint64_t* tokens_seen,
@@ -378,6 +423,22 @@ void orc_permutation(const uint32_t* indices, size_t t_count, size_t top_k, size
             slot_row[t * top_k + s] = e < n_ffn ? (int32_t)counts[e] : -1;
             counts[e]++;
         }
+}
+
+/* model.hpp:390-391 (ScMoE dense shortcut branch) with ffn_block
+ * (blocks.hpp:397-402): dd = a1 + silu(rmsnorm(a1, g) W_in) W_out. */
+int orc_dense_branch_f32(const float* a1, const float* gain, size_t t_count, size_t d,
+                         const float* w_in, const float* w_out, size_t inter, float* out) {
+    float* xn = (float*)malloc(sizeof(float) * (d + inter + d));
+    if (!xn) return ORC_PARAMETER;
+    float *h = xn + d, *y = h + inter;
+    for (size_t t = 0; t < t_count; ++t) {
+        orc_rmsnorm_f32(a1 + t * d, gain, 1, d, 1e-6f, xn);
+        orc_expert_row_f32(xn, d, w_in, w_out, inter, h, y);
+        for (size_t j = 0; j < d; ++j) out[t * d + j] = a1[t * d + j] + y[j];
+    }
+    free(xn);
+    return ORC_OK;
 }
 
 /* model.hpp:394-400 (ScMoE wiring, MoE branch): hmoe = rmsnorm(a1, g);

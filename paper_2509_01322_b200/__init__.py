@@ -117,6 +117,9 @@ _PROTOS = {
     "scmoe_route_from_probs_f32_host": (C.c_int, [_P, _P, _P, _SZ, _P, _P, _P]),
     "scmoe_route_from_probs_f64_host": (C.c_int, [_P, _P, _P, _SZ, _P, _P, _P]),
     "scmoe_accumulate_counters": (C.c_int, [_P, _P, _P, _SZ]),
+    "scmoe_routing_stats": (C.c_int, [_P, _P, _P, _SZ, _SZ, _SZ, _SZ, _SZ, _SZ, _P, _P, _P, _P]),
+    "scmoe_routing_stats_host": (C.c_int, [_P, _P, _P, _SZ, _SZ, _SZ, _SZ, _SZ, _SZ, _P, _P, _P,
+                                           _P]),
     "scmoe_accumulate_counters_host": (C.c_int, [_P, _P, _P, _SZ]),
     "scmoe_bias_update": (C.c_int, [_P, _P, _P]),
     "scmoe_bank_create": (C.c_int, [_P, _SZ, _SZ, _SZ, C.c_int, _SZ, C.c_int, C.POINTER(_P)]),
@@ -135,6 +138,7 @@ _PROTOS = {
                                            _P]),
     "scmoe_layer_forward_batches": (C.c_int, [_P, _P, _P, _SZ, _P, _P, _P, _SZ, C.c_int, _P, _P,
                                               _P, _P]),
+    "scmoe_dense_ffn": (C.c_int, [_P, _P, _P, _P, _SZ, _P]),
     "scmoe_layer_forward_host_batches": (C.c_int, [_P, _P, _P, _SZ, _P, _P, _P, _SZ, C.c_int, _P,
                                                    _P, _P, _P]),
     "scmoe_bank_init_uniform_shard": (C.c_int, [_P, _P, _U64, _U64, C.c_double, _SZ]),
@@ -428,6 +432,30 @@ def accumulate_counters(state: RouterState, d: RoutingDecision, ctx: Optional[Co
     h = state.device(ctx)
     ctx._check(lib().scmoe_accumulate_counters_host(ctx.handle, h, _ptr(idx), d.tokens()))
     state.pull(ctx)
+
+
+def routing_stats(d: RoutingDecision, n_zero: int, k_expected: int, lb_groups: Optional[int] = None,
+                  ctx: Optional[Context] = None) -> dict:
+    """Per-layer routing statistics from a device histogram:
+    mean / std of activated FFN experts (router.hpp:73-86), per-expert slot
+    load (stats.hpp:64-67) and, with lb_groups, the LB group frequencies
+    (router.hpp:193-216).  Bitwise equal to the reference."""
+    ctx = ctx or default_context()
+    idx = np.ascontiguousarray(d.indices, np.uint32)
+    cnt = np.ascontiguousarray(d.ffn_count, np.uint32)
+    T, E = d.tokens(), d.n_ffn + n_zero
+    mean, std = C.c_double(), C.c_double()
+    load = np.empty(E, np.float64)
+    lb = np.empty(lb_groups + (1 if n_zero else 0), np.float64) if lb_groups else None
+    ctx._check(lib().scmoe_routing_stats_host(ctx.handle, _ptr(idx), _ptr(cnt), T, d.top_k,
+                                              d.n_ffn, n_zero, k_expected, lb_groups or 0,
+                                              C.byref(mean), C.byref(std), _ptr(load),
+                                              _ptr(lb) if lb is not None else None))
+    out = {"mean_activated_ffn": mean.value, "std_activated_ffn": std.value,
+           "per_expert_load": load}
+    if lb is not None:
+        out["lb_group_frequencies"] = lb
+    return out
 
 
 def bias_update(state: RouterState, ctx: Optional[Context] = None) -> np.ndarray:

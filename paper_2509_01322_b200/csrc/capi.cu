@@ -7,6 +7,7 @@
 #include <cstring>
 #include <mutex>
 #include <thread>
+#include <vector>
 
 #include "internal.cuh"
 
@@ -541,6 +542,60 @@ int scmoe_route_topk_host(scmoe_ctx* c, scmoe_router* r, const float* x, size_t 
 ROUTE_FROM_PROBS(float, f32)
 ROUTE_FROM_PROBS(double, f64)
 
+int scmoe_routing_stats(scmoe_ctx* c, const uint32_t* idx, const uint32_t* cnt, size_t T,
+                        size_t K, size_t n_ffn, size_t n_zero, size_t k_expected,
+                        size_t lb_groups, double* mean_ffn, double* std_ffn, double* load,
+                        double* lb) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        if (lb && (lb_groups == 0 || n_ffn % lb_groups != 0))
+            SCMOE_THROW(SCMOE_ERR_CONFIG, "lb_loss: group count must divide FFN expert count");
+        const size_t E = n_ffn + n_zero;
+        uint64_t* hist = c->ws.misc.get<uint64_t>(E + 2);
+        double* mom = reinterpret_cast<double*>(hist + E);
+        SCMOE_CUDA(cudaMemsetAsync(hist, 0, E * sizeof(uint64_t), c->stream));
+        launch_accumulate(c, idx, T * K, E, hist);
+        launch_ffn_moments(c, cnt, T, mom);
+        std::vector<uint64_t> h(E + 2);
+        SCMOE_CUDA(cudaMemcpyAsync(h.data(), hist, (E + 2) * sizeof(uint64_t),
+                                   cudaMemcpyDeviceToHost, c->stream));
+        sync_and_check(c);  // StateError on an index >= E
+        memcpy(mean_ffn, &h[E], sizeof(double));
+        memcpy(std_ffn, &h[E + 1], sizeof(double));
+        // the reference accumulates 1.0 per slot (exact integers) then divides
+        const double slots = (double)(T * K), tc = (double)T;
+        if (load)
+            for (size_t e = 0; e < E; ++e) load[e] = (double)h[e] / slots;
+        if (lb) {
+            const size_t gsz = n_ffn / lb_groups;
+            for (size_t j = 0; j < lb_groups; ++j) {
+                uint64_t f = 0;
+                for (size_t e = j * gsz; e < (j + 1) * gsz; ++e) f += h[e];
+                lb[j] = (double)f * ((double)lb_groups / ((double)k_expected * tc));
+            }
+            if (n_zero > 0) {
+                uint64_t f = 0;
+                for (size_t e = n_ffn; e < E; ++e) f += h[e];
+                lb[lb_groups] = (double)f / ((double)(K - k_expected) * tc);
+            }
+        }
+    });
+}
+int scmoe_routing_stats_host(scmoe_ctx* c, const uint32_t* idx, const uint32_t* cnt, size_t T,
+                             size_t K, size_t n_ffn, size_t n_zero, size_t k_expected,
+                             size_t lb_groups, double* mean_ffn, double* std_ffn, double* load,
+                             double* lb) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        Stage& s = stage_of(c);
+        const uint32_t* di = upload(c, s.bufs[1], idx, T * K);
+        const uint32_t* dc = upload(c, s.bufs[3], cnt, T);
+        int rc = scmoe_routing_stats(c, di, dc, T, K, n_ffn, n_zero, k_expected, lb_groups,
+                                     mean_ffn, std_ffn, load, lb);
+        if (rc) throw ScmoeError{rc, c->last_error};
+    });
+}
+
 int scmoe_accumulate_counters(scmoe_ctx* c, scmoe_router* r, const uint32_t* idx, size_t T) {
     return guarded(c, [&] {
         require_ctx(c);
@@ -583,9 +638,10 @@ int scmoe_bank_create(scmoe_ctx* c, size_t n, size_t d, size_t inter, int precis
             SCMOE_THROW(SCMOE_ERR_PARAMETER, "bank: unknown precision");
         if (gamma_mode < 0 || gamma_mode > 2) SCMOE_THROW(SCMOE_ERR_PARAMETER, "unknown gamma mode");
         if (precision == SCMOE_PREC_BF16) {
-            if (d % 64 != 0 || inter % 128 != 0 || d % 128 != 0)
+            // both GEMMs tile the weight rows by 256 (two 128-row MMA slabs)
+            if (d % 256 != 0 || inter % 256 != 0)
                 SCMOE_THROW(SCMOE_ERR_DIMENSION,
-                            "bank: bf16 tensor-core path needs d % 128 == 0 and inter % 128 == 0");
+                            "bank: bf16 tensor-core path needs d % 256 == 0 and inter % 256 == 0");
         }
         auto* b = new scmoe_bank();
         b->n = n;
@@ -907,6 +963,42 @@ int scmoe_layer_forward_host_batches(scmoe_ctx* c, scmoe_router* r, scmoe_bank* 
         }
         SCMOE_CUDA(cudaStreamSynchronize(c->s_d2h));
         sync_and_check(c);
+    });
+}
+
+int scmoe_dense_ffn(scmoe_ctx* c, scmoe_bank* b, const float* a1, const float* gain, size_t T,
+                    float* out) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        if (!b || b->n != 1 || b->precision != SCMOE_PREC_BF16)
+            SCMOE_THROW(SCMOE_ERR_PARAMETER, "dense_ffn: needs a one-expert bf16 bank");
+        if (T == 0) return;
+        const size_t d = b->d, I = b->inter;
+        Workspace& ws = c->ws;
+        const int tr = grouped_gemm_tile_rows();
+        const size_t ntile = ceil_div(T, tr);
+        __nv_bfloat16* xb = ws.dn_x.get<__nv_bfloat16>(T * d);
+        __nv_bfloat16* h = ws.dn_h.get<__nv_bfloat16>(T * I);
+        __nv_bfloat16* y = ws.dn_y.get<__nv_bfloat16>(T * d);
+        TokenTile* tiles = ws.dn_tiles.get<TokenTile>(ntile + 1);
+        int* ntd = reinterpret_cast<int*>(tiles + ntile);
+        {
+            ProfScope _p(c, "dense_rmsnorm");
+            launch_rmsnorm(c, a1, gain, T, d, 1e-6f, nullptr, xb);
+        }
+        launch_row_tiles(c, T, tr, tiles, ntd);
+        {
+            ProfScope _p(c, "dense_gemm1_tcgen05");
+            launch_grouped_gemm_bf16(c, b->w1t, 1, I, d, xb, T, nullptr, h, /*silu=*/1, tiles, ntd,
+                                     ntile, tr);
+        }
+        {
+            ProfScope _p(c, "dense_gemm2_tcgen05");
+            launch_grouped_gemm_bf16(c, b->w2t, 1, d, I, h, T, nullptr, y, /*silu=*/0, tiles, ntd,
+                                     ntile, tr);
+        }
+        ProfScope _p(c, "dense_residual");
+        launch_add_bf16_residual(c, a1, y, T * d, out);
     });
 }
 

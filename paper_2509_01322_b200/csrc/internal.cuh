@@ -66,12 +66,16 @@ struct Workspace {
     DevBuf rank_in_block, block_counts, expert_count, expert_base, slot_pos, row_token;
     DevBuf tiles, n_tiles, xp, h, y, in_copy, out_copy, misc, tiles_router, ep_bins, ep_local,
         ep_y;
+    // dense shortcut FFN (scmoe_dense_ffn): own buffers, so it can run on
+    // another stream beside the MoE branch
+    DevBuf dn_x, dn_h, dn_y, dn_tiles;
     unsigned char pr_blob[64] = {};  // permutation result carried from moe_front to moe_back
     void release_all() {
         DevBuf* all[] = {&logits, &probs, &hmoe, &hmoe_bf16, &idx, &gates, &ffn_count,
                          &rank_in_block, &block_counts, &expert_count, &expert_base, &slot_pos,
                          &row_token, &tiles, &n_tiles, &xp, &h, &y, &in_copy, &out_copy, &misc,
-                         &tiles_router, &ep_bins, &ep_local, &ep_y};
+                         &tiles_router, &ep_bins, &ep_local, &ep_y, &dn_x, &dn_h, &dn_y,
+                         &dn_tiles};
         for (DevBuf* b : all) b->release();
     }
 };
@@ -255,6 +259,7 @@ void launch_combine_bf16(scmoe_ctx* c, const float* x, const __nv_bfloat16* y,
                          size_t d, size_t K, size_t n_ffn, float gamma_ffn, float gamma_zero,
                          int renorm, const float* residual, float* out);
 void launch_check_indices(scmoe_ctx* c, const uint32_t* idx, size_t n, size_t E);
+void launch_ffn_moments(scmoe_ctx* c, const uint32_t* cnt, size_t T, double* out);
 void launch_accumulate(scmoe_ctx* c, const uint32_t* idx, size_t n, size_t E, uint64_t* routed);
 void launch_bias_update(scmoe_ctx* c, scmoe_router* r, double* delta_dev);
 void launch_uniform_init(scmoe_ctx* c, uint64_t seed, uint64_t first, size_t n,
@@ -264,7 +269,10 @@ void launch_uniform_init_bf16_t(scmoe_ctx* c, uint64_t seed, size_t rows, size_t
 void launch_debug_expf(scmoe_ctx* c, const float* in, float* out, size_t n);
 void launch_debug_expf_range(scmoe_ctx* c, uint32_t first, float* out, size_t n);
 void launch_cast_bf16(scmoe_ctx* c, const float* src, size_t n, __nv_bfloat16* dst);
-void launch_row_tiles(scmoe_ctx* c, size_t rows, int tile_rows, TokenTile* tiles);
+void launch_row_tiles(scmoe_ctx* c, size_t rows, int tile_rows, TokenTile* tiles,
+                      int* n_out = nullptr);
+void launch_add_bf16_residual(scmoe_ctx* c, const float* a, const __nv_bfloat16* y, size_t n,
+                              float* out);
 void launch_f32_to_bf16_t(scmoe_ctx* c, const float* src, size_t rows, size_t cols,
                           __nv_bfloat16* dst_t);
 

@@ -499,6 +499,31 @@ __global__ void accumulate_kernel(const uint32_t* __restrict__ idx, size_t n, ui
         if (hist[e]) atomicAdd(&routed[e], (unsigned long long)hist[e]);
 }
 
+// RoutingDecision::mean_ffn / std_ffn (router.hpp:73-86): sequential double
+// sums in token order (the order fixes the rounding of the second one), one
+// thread -- T dependent adds, ~30 us at T = 8192.
+__global__ void ffn_moments_kernel(const uint32_t* __restrict__ cnt, size_t T,
+                                   double* __restrict__ out) {
+    double m = 0.0, sd = 0.0;
+    if (T) {
+        double s = 0.0;
+        for (size_t t = 0; t < T; ++t) s = __dadd_rn(s, (double)cnt[t]);
+        m = __ddiv_rn(s, (double)T);
+        double s2 = 0.0;
+        for (size_t t = 0; t < T; ++t) {
+            const double dlt = __dsub_rn((double)cnt[t], m);
+            s2 = __dadd_rn(s2, __dmul_rn(dlt, dlt));
+        }
+        sd = __dsqrt_rn(__ddiv_rn(s2, (double)T));
+    }
+    out[0] = m;
+    out[1] = sd;
+}
+void launch_ffn_moments(scmoe_ctx* c, const uint32_t* cnt, size_t T, double* out) {
+    ffn_moments_kernel<<<1, 1, 0, c->stream>>>(cnt, T, out);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
 void launch_accumulate(scmoe_ctx* c, const uint32_t* idx, size_t n, size_t E, uint64_t* routed) {
     if (n == 0) return;
     const int blocks = (int)std::min<size_t>(ceil_div(n, 1024), (size_t)c->num_sms * 2);
@@ -655,16 +680,50 @@ void launch_cast_bf16(scmoe_ctx* c, const float* src, size_t n, __nv_bfloat16* d
 }
 
 // One group, consecutive row tiles (router projection, router.hpp:136).
-__global__ void row_tiles_kernel(int rows, int tile_rows, TokenTile* __restrict__ tiles) {
+__global__ void row_tiles_kernel(int rows, int tile_rows, TokenTile* __restrict__ tiles,
+                                 int* __restrict__ n_out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int n = (rows + tile_rows - 1) / tile_rows;
     if (i < n) tiles[i] = TokenTile{0, i * tile_rows, min(tile_rows, rows - i * tile_rows), 0};
+    if (i == 0 && n_out) *n_out = n;
 }
 
-void launch_row_tiles(scmoe_ctx* c, size_t rows, int tile_rows, TokenTile* tiles) {
+void launch_row_tiles(scmoe_ctx* c, size_t rows, int tile_rows, TokenTile* tiles, int* n_out) {
     const size_t n = ceil_div(rows, tile_rows);
     if (n == 0) return;
-    row_tiles_kernel<<<ceil_div(n, 256), 256, 0, c->stream>>>((int)rows, tile_rows, tiles);
+    row_tiles_kernel<<<ceil_div(n, 256), 256, 0, c->stream>>>((int)rows, tile_rows, tiles, n_out);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
+// out = a + float(y) (fp32 add, round to nearest): the dense branch's
+// residual dd = a1 + ffn(rmsnorm(a1)) (model.hpp:390-391).
+__global__ void add_bf16_residual_kernel(const float* __restrict__ a,
+                                         const __nv_bfloat16* __restrict__ y, size_t n8,
+                                         float* __restrict__ out) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const uint4 yv = reinterpret_cast<const uint4*>(y)[i];
+        const float4 a0 = reinterpret_cast<const float4*>(a)[2 * i];
+        const float4 a1 = reinterpret_cast<const float4*>(a)[2 * i + 1];
+        const __nv_bfloat162* yb = reinterpret_cast<const __nv_bfloat162*>(&yv);
+        const float2 y0 = __bfloat1622float2(yb[0]), y1 = __bfloat1622float2(yb[1]);
+        const float2 y2 = __bfloat1622float2(yb[2]), y3 = __bfloat1622float2(yb[3]);
+        reinterpret_cast<float4*>(out)[2 * i] =
+            make_float4(__fadd_rn(a0.x, y0.x), __fadd_rn(a0.y, y0.y), __fadd_rn(a0.z, y1.x),
+                        __fadd_rn(a0.w, y1.y));
+        reinterpret_cast<float4*>(out)[2 * i + 1] =
+            make_float4(__fadd_rn(a1.x, y2.x), __fadd_rn(a1.y, y2.y), __fadd_rn(a1.z, y3.x),
+                        __fadd_rn(a1.w, y3.y));
+    }
+}
+
+void launch_add_bf16_residual(scmoe_ctx* c, const float* a, const __nv_bfloat16* y, size_t n,
+                              float* out) {
+    SCMOE_CHECK_ARG(n % 8 == 0, SCMOE_ERR_DIMENSION, "residual add: size must be a multiple of 8");
+    if (n == 0) return;
+    const size_t n8 = n / 8;
+    const int blocks = (int)std::min<size_t>(ceil_div(n8, 256), (size_t)c->num_sms * 8);
+    add_bf16_residual_kernel<<<blocks, 256, 0, c->stream>>>(a, y, n8, out);
     SCMOE_LAUNCH_CHECK(c);
 }
 

@@ -77,10 +77,10 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
     }
     s2 = __shfl_sync(0xffffffffu, s2, 0);
     const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(s2, (float)d), eps)));
-    float* orow = out + (size_t)row * d;
+    float* orow = out ? out + (size_t)row * d : nullptr;  // out may be NULL (bf16 only)
     if (vec) {
         const float4* src = reinterpret_cast<const float4*>(xr);
-        float4* dst = reinterpret_cast<float4*>(orow);
+        float4* dst = reinterpret_cast<float4*>(orow);  // unused when orow is NULL
         for (int j4 = lane; j4 < d / 4; j4 += 32) {
             const float4 v = src[j4];
             float4 g = gain ? reinterpret_cast<const float4*>(gain)[j4] : make_float4(1.f, 1.f, 1.f, 1.f);
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
             o.y = __fmul_rn(__fmul_rn(v.y, inv), g.y);
             o.z = __fmul_rn(__fmul_rn(v.z, inv), g.z);
             o.w = __fmul_rn(__fmul_rn(v.w, inv), g.w);
-            dst[j4] = o;
+            if (orow) dst[j4] = o;
             if (out_bf16) {
                 __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y);
                 __nv_bfloat162 hi = __floats2bfloat162_rn(o.z, o.w);
@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
         for (int j = lane; j < d; j += 32) {
             const float g = gain ? gain[j] : 1.0f;
             const float v = __fmul_rn(__fmul_rn(xr[j], inv), g);
-            orow[j] = v;
+            if (orow) orow[j] = v;
             if (out_bf16) out_bf16[(size_t)row * d + j] = __float2bfloat16_rn(v);
         }
     }

@@ -139,6 +139,25 @@ class DeviceLayer:
                                                        int(renormalize), p(idx), p(gates),
                                                        p(ffn_count), p(out)))
 
+    def routing_stats(self, idx: int, ffn_count: int, tokens: int, lb_groups: int = 0) -> dict:
+        """Routing statistics of a forward's routing outputs (device pointers):
+        mean/std activated FFN experts, per-expert load, LB group frequencies
+        (scmoe_routing_stats)."""
+        import numpy as np
+        s = self.shape
+        mean, std = C.c_double(), C.c_double()
+        load = np.empty(s.E, np.float64)
+        lb = np.empty(lb_groups + (1 if s.n_zero else 0)) if lb_groups else None
+        self.ctx._check(lib().scmoe_routing_stats(
+            self.ctx.handle, idx, ffn_count, tokens, s.top_k, s.n_ffn, s.n_zero, s.k_expected,
+            lb_groups, C.byref(mean), C.byref(std), load.ctypes.data_as(_P),
+            None if lb is None else lb.ctypes.data_as(_P)))
+        out = {"mean_activated_ffn": mean.value, "std_activated_ffn": std.value,
+               "per_expert_load": load}
+        if lb is not None:
+            out["lb_group_frequencies"] = lb
+        return out
+
     def forward_host_batches(self, a1s, a3s, gain, tokens: int, idxs, gatess, cnts, outs,
                              renormalize: bool = False):
         """A stream of host batches (scmoe_layer_forward_host_batches): lists of
@@ -161,3 +180,38 @@ class DeviceLayer:
         if self.router:
             L.scmoe_router_destroy(self.ctx.handle, self.router)
             self.router = _P()
+
+
+class DenseFFN:
+    """Dense shortcut-path FFN of the ScMoE layer (model.hpp:390-391,
+    blocks.hpp:397-402): out = a1 + silu(rmsnorm(a1, gain) W_in) W_out, bf16 weights
+    on the tcgen05 grouped GEMM (a one-expert bank).  Weights: seeded_init
+    Uniform(1/d) on the device (streams stream0, stream0 + 1), or set from host
+    fp32 arrays w_in [d, inter], w_out [inter, d]."""
+
+    def __init__(self, ctx: Context, d: int, inter: int, seed: int = 9, stream0: int = 7000,
+                 w_in=None, w_out=None):
+        self.ctx, self.d, self.inter = ctx, d, inter
+        L = lib()
+        self.bank = _P()
+        ctx._check(L.scmoe_bank_create(ctx.handle, 1, d, inter, PREC_BF16, 1,
+                                       int(GammaMode.Off), C.byref(self.bank)))
+        if w_in is not None:
+            import numpy as np
+            wi = np.ascontiguousarray(w_in, np.float32)
+            wo = np.ascontiguousarray(w_out, np.float32)
+            ctx._check(L.scmoe_bank_set_expert_host(ctx.handle, self.bank, 0,
+                                                    wi.ctypes.data_as(_P), wo.ctypes.data_as(_P)))
+        else:
+            ctx._check(L.scmoe_bank_init_uniform(ctx.handle, self.bank, seed, stream0, 1.0 / d))
+
+    def forward(self, a1: int, gain: Optional[int], tokens: int, out: int,
+                ctx: Optional[Context] = None):
+        """Device pointers; stream-ordered on ctx's stream (default: the owner's)."""
+        c = ctx or self.ctx
+        c._check(lib().scmoe_dense_ffn(c.handle, self.bank, a1, gain, tokens, out))
+
+    def close(self):
+        if self.bank:
+            lib().scmoe_bank_destroy(self.ctx.handle, self.bank)
+            self.bank = _P()

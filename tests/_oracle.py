@@ -68,6 +68,7 @@ _ORC_PROTOS = {
     "orc_route_topk_f64": (C.c_int, [_P, _SZ, _SZ, _P, _SZ, _SZ, _SZ, _SZ, _D, _P, _P, _P, _P,
                                      _P]),
     "orc_accumulate_counters": (None, [_P, _SZ, _SZ, _P, _P]),
+    "orc_routing_stats": (C.c_int, [_P, _P, _SZ, _SZ, _SZ, _SZ, _SZ, _SZ, _P, _P, _P, _P]),
     "orc_bias_update": (C.c_int, [_SZ, _SZ, _SZ, _SZ, _P, _D, _P, _P, _P, _P]),
     "orc_moe_forward_f32": (C.c_int, [_P, _SZ, _SZ, _P, _P, _SZ, _SZ, _SZ, _P, _P, _SZ, _D, _D,
                                       C.c_int, _P]),
@@ -75,6 +76,7 @@ _ORC_PROTOS = {
                                       C.c_int, _P]),
     "orc_permutation": (None, [_P, _SZ, _SZ, _SZ, _SZ, _P, _P]),
     "orc_expert_row_f32": (None, [_P, _SZ, _P, _P, _SZ, _P, _P]),
+    "orc_dense_branch_f32": (C.c_int, [_P, _P, _SZ, _SZ, _P, _P, _SZ, _P]),
     "orc_scmoe_layer_f32": (C.c_int, [_P, _P, _P, _SZ, _SZ, _P, _SZ, _SZ, _SZ, _SZ, _D, _P, _P,
                                       _P, _SZ, _D, _D, C.c_int, _P, _P, _P, _P]),
     "orc_simulate_bias_control_f32": (C.c_int, [_P, _SZ, _SZ, _SZ, _SZ, _SZ, _P, _D, _P, _U64,
@@ -96,6 +98,7 @@ _REF_PROTOS = {
     "ref_route_from_probs_f64": (C.c_int, [_P, _SZ, _SZ, _SZ, _SZ, _SZ, _D, _P, _P, _P, _P]),
     "ref_bias_update": (C.c_int, [_SZ, _SZ, _SZ, _SZ, _P, _D, _P, _P, _P, _P]),
     "ref_accumulate_counters": (C.c_int, [_P, _SZ, _SZ, _SZ, _SZ, _P, _P]),
+    "ref_routing_stats": (C.c_int, [_P, _P, _SZ, _SZ, _SZ, _SZ, _SZ, _SZ, _P, _P, _P, _P]),
     "ref_moe_forward_f32": (C.c_int, [_P, _SZ, _SZ, _P, _P, _SZ, _SZ, _SZ, _P, _P, _SZ, _SZ,
                                       C.c_int, _P, C.c_int]),
     "ref_moe_forward_f64": (C.c_int, [_P, _SZ, _SZ, _P, _P, _SZ, _SZ, _SZ, _P, _P, _SZ, _SZ,
@@ -203,6 +206,26 @@ def orc_moe_forward(x, idx, gates, k, n_ffn, n_zero, w_in, w_out, gamma_ffn=1.0,
                                    ptr_array(w_in), ptr_array(w_out), I, gamma_ffn, gamma_zero,
                                    int(renorm), ptr(out))
     return rc, out
+
+
+def routing_stats(fn, idx, cnt, k, n, z, ke, groups):
+    """fn: orc().orc_routing_stats or ref().ref_routing_stats -> (rc, mean, std, load, lb)."""
+    idx = np.ascontiguousarray(idx, np.uint32)
+    cnt = np.ascontiguousarray(cnt, np.uint32)
+    mean, std = C.c_double(), C.c_double()
+    load = np.empty(n + z)
+    lb = np.empty(groups + (1 if z else 0)) if groups else None
+    rc = fn(ptr(idx), ptr(cnt), len(cnt), k, n, z, ke, groups, C.byref(mean), C.byref(std),
+            ptr(load), ptr(lb))
+    return rc, mean.value, std.value, load, lb
+
+
+def random_decision(seed, T, k, n, z):
+    """Indices with distinct experts per token, ffn_count consistent with them."""
+    rng = np.random.default_rng(seed)
+    rows = [rng.choice(n + z, k, replace=False) for _ in range(T)]
+    idx = (np.stack(rows) if rows else np.zeros((0, k))).astype(np.uint32)
+    return idx.ravel(), (idx < n).sum(1).astype(np.uint32)
 
 
 def rel_l2(a, b) -> float:

@@ -365,3 +365,65 @@ def test_layer_forward_bf16_routing_exact(scmoe):
     assert (dg.indices == idx).all() and (bits64(dg.gates) == bits64(g)).all()
     err = O.rel_l2(out - a3, want - a3)
     assert err <= BF16_TOL, err
+
+
+@pytest.mark.parametrize("shape", [(1000, 12, 64, 32, 8, 8), (8192, 12, 512, 256, 8, 16),
+                                   (257, 6, 24, 12, 4, 3), (5, 2, 8, 0, 2, 4)])
+def test_routing_stats_device_bitwise(scmoe, shape):
+    """routing statistics from the device histogram and the
+    device-side sequential moments equal the reference's bit for bit."""
+    P = scmoe
+    T, k, n, z, ke, g = shape
+    idx, cnt = O.random_decision(T + 7, T, k, n, z)
+    d = P.RoutingDecision(k, n, idx, np.zeros(T * k), cnt)
+    st = P.routing_stats(d, z, ke, g)
+    rc, mean, std, load, lb = O.routing_stats(O.orc().orc_routing_stats, idx, cnt, k, n, z, ke, g)
+    assert rc == 0
+    assert np.float64(st["mean_activated_ffn"]).tobytes() == np.float64(mean).tobytes()
+    assert np.float64(st["std_activated_ffn"]).tobytes() == np.float64(std).tobytes()
+    assert st["per_expert_load"].tobytes() == load.tobytes()
+    assert st["lb_group_frequencies"].tobytes() == lb.tobytes()
+
+
+def test_routing_stats_errors(scmoe):
+    P = scmoe
+    idx, cnt = O.random_decision(3, 10, 2, 8, 4)
+    d = P.RoutingDecision(2, 8, idx, np.zeros(20), cnt)
+    with pytest.raises(P.ConfigError):  # LbLossConfig::validate (router.hpp:184-188)
+        P.routing_stats(d, 4, 1, 3)
+    bad = idx.copy()
+    bad[3] = 12
+    with pytest.raises(P.StateError):
+        P.routing_stats(P.RoutingDecision(2, 8, bad, np.zeros(20), cnt), 4, 1, 2)
+
+
+@pytest.mark.parametrize("T,d,inter,gain", [(333, 256, 512, False), (200, 512, 256, True)])
+def test_dense_ffn_bf16(scmoe, T, d, inter, gain):
+    """dense shortcut branch dd = a1 + silu(rmsnorm(a1) W_in) W_out
+    (model.hpp:390-391, blocks.hpp:397-402) on the tcgen05 GEMM, vs the oracle
+    on the same bf16-rounded weights (rel-L2 of the FFN part <= 5e-3)."""
+    import torch
+    from paper_2509_01322_b200.layer import DenseFFN
+    P = scmoe
+    ctx = P.Context(0)
+    w_in = O.bf16_round(O.uniform_f32(O.stream_seed(31, 0), d * inter, 1.0 / d)).reshape(d, inter)
+    w_out = O.bf16_round(O.uniform_f32(O.stream_seed(31, 1), inter * d, 1.0 / d)).reshape(inter, d)
+    a1 = O.normal_f32(O.stream_seed(32, 0), T * d).reshape(T, d)
+    g = (1.0 + 0.1 * O.normal_f32(33, d)).astype(np.float32) if gain else None
+    dense = DenseFFN(ctx, d, inter, w_in=w_in, w_out=w_out)
+    a1_d = torch.from_numpy(a1).cuda()
+    g_d = torch.from_numpy(g).cuda() if gain else None
+    out_d = torch.empty_like(a1_d)
+    dense.forward(a1_d.data_ptr(), g_d.data_ptr() if gain else None, T, out_d.data_ptr())
+    ctx.synchronize()
+    out = out_d.cpu().numpy()
+    want = np.empty_like(a1)
+    g_or = g if gain else np.ones(d, np.float32)  # NULL gain on the device = unit gain
+    assert O.orc().orc_dense_branch_f32(O.ptr(a1), O.ptr(g_or), T, d, O.ptr(w_in), O.ptr(w_out),
+                                        inter, O.ptr(want)) == 0
+    err = O.rel_l2(out - a1, want - a1)
+    assert err <= 5e-3, err
+    with pytest.raises(P.ParameterError):  # not a one-expert bf16 bank
+        ctx._check(P.lib().scmoe_dense_ffn(ctx.handle, None, a1_d.data_ptr(), None, T,
+                                           out_d.data_ptr()))
+    dense.close()

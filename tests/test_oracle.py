@@ -276,3 +276,24 @@ def test_oracle_matches_committed_golden(orc):
     w_in, w_out = _bank(n, d, I, cfg["seed_bank"])
     rc, out = O.orc_moe_forward(x, idx, g, k, n, z, w_in, w_out)
     assert (out.view(np.uint32) == gd["out"].view(np.uint32)).all()
+
+
+def test_routing_stats_match_reference(orc):
+    """mean/std activated FFN (router.hpp:73-86), per-expert
+    load (stats.hpp:64-67), LB group frequencies (router.hpp:193-216)."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    ref = O.ref()
+    for (T, k, n, z, ke, g) in [(1000, 12, 64, 32, 8, 8), (257, 6, 24, 12, 4, 3),
+                                (5, 2, 8, 0, 2, 4), (0, 2, 8, 4, 1, 2)]:
+        idx, cnt = O.random_decision(T + 1, T, k, n, z)
+        a = O.routing_stats(orc.orc_routing_stats, idx, cnt, k, n, z, ke, g)
+        b = O.routing_stats(ref.ref_routing_stats, idx, cnt, k, n, z, ke, g)
+        assert a[0] == b[0] == 0
+        assert np.float64(a[1]).tobytes() == np.float64(b[1]).tobytes()
+        assert np.float64(a[2]).tobytes() == np.float64(b[2]).tobytes()
+        assert a[3].tobytes() == b[3].tobytes() and a[4].tobytes() == b[4].tobytes()
+    # LbLossConfig::validate: groups must divide n_ffn -> ConfigError
+    idx, cnt = O.random_decision(1, 10, 2, 8, 4)
+    assert O.routing_stats(orc.orc_routing_stats, idx, cnt, 2, 8, 4, 1, 3)[0] == 1
+    assert O.routing_stats(ref.ref_routing_stats, idx, cnt, 2, 8, 4, 1, 3)[0] == 1

@@ -516,6 +516,52 @@ def run_b200_ep(args):
     e1.record()
     e1.synchronize()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e_steps, ws)
+
+    # ---- SURVEY config D: fixed 32k tokens over the ranks, with the dense
+    # shortcut FFN (dense_inter) overlapping the dispatch/return all-to-alls;
+    # exposed communication = (t_layer - t_layer with the row all-to-alls
+    # replaced by no-ops) / t_layer ----------------------------------------
+    config_d = None
+    if args.dense_inter > 0:
+        Td = args.config_d_tokens // ws
+        ep.ops.enable_dense(local, args.dense_inter, seed=SEED_W + 1)
+        a1d = torch.from_numpy(P.fill_normal(P.stream_seed(SEED_X + 5, rank), Td * D,
+                                             threads=os.cpu_count() or 8)).cuda()
+
+        def timed_d(dense, comm):
+            ep.comm = comm
+            for _ in range(2):
+                ep.forward(a1d, None, None, Td, chunks=chunks, dense=dense)
+            barrier(ws)
+            torch.cuda.synchronize()
+            d0 = torch.cuda.Event(enable_timing=True)
+            d1 = torch.cuda.Event(enable_timing=True)
+            d0.record()
+            for _ in range(args.steps):
+                ep.forward(a1d, None, None, Td, chunks=chunks, dense=dense)
+            d1.record()
+            d1.synchronize()
+            torch.cuda.synchronize()
+            barrier(ws)
+            ep.comm = True
+            return max_over_ranks(d0.elapsed_time(d1) / args.steps, ws)
+
+        t_moe, t_moe_nc = timed_d(False, True), timed_d(False, False)
+        t_full, t_full_nc = timed_d(True, True), timed_d(True, False)
+        dense_flop = 4.0 * Td * D * args.dense_inter
+        config_d = {
+            "workload": "SURVEY config D: ScMoE layer = MoE branch + dense shortcut SiLU-MLP "
+                        "(rmsnorm, d x dense_inter x d, residual) overlapping the all-to-alls",
+            "tokens_total": Td * ws, "tokens_per_gpu": Td, "dense_inter": args.dense_inter,
+            "ms_moe_branch": t_moe, "ms_moe_branch_comm_noop": t_moe_nc,
+            "ms_layer": t_full, "ms_layer_comm_noop": t_full_nc,
+            "exposed_comm_frac_layer": (t_full - t_full_nc) / t_full,
+            "exposed_comm_frac_moe_only": (t_moe - t_moe_nc) / t_moe,
+            "layer_tokens_per_s": Td * ws / (t_full / 1e3),
+            "dense_tflop_per_gpu": dense_flop / 1e12,
+            "a2a_bytes_each_way_rank0": ep.last_stats["a2a_bytes_each_way"],
+            "dense_gemm_sms": "all but 16 (left to the NCCL kernels)",
+        }
     if rank != 0:
         return
     peaks = measured_peaks() or {}
@@ -559,6 +605,7 @@ def run_b200_ep(args):
         "stages_ms": {k: round(v[0] / v[1], 4) for k, v in stages.items()},
         "clocks": clk.summary(),
         "cpu_baseline": None,
+        "config_d": config_d,
     }
     emit(line)
 
@@ -572,6 +619,9 @@ def main():
     ap.add_argument("--config", default="prefill", choices=sorted(CONFIGS))
     ap.add_argument("--tokens", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    # N>1: SURVEY config D extra (dense shortcut FFN overlapping the all-to-alls)
+    ap.add_argument("--dense-inter", type=int, default=12288)
+    ap.add_argument("--config-d-tokens", type=int, default=32768)
     # pipelined = scmoe_layer_forward_batches; measured slower than serial on B200 in round 1
     # (router and GEMM contend for shared-memory bandwidth), so serial is the default
     ap.add_argument("--schedule", default="pipelined", choices=["pipelined", "serial"])

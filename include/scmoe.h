@@ -70,6 +70,11 @@ int scmoe_set_stream(scmoe_ctx* ctx, void* cuda_stream);
 void* scmoe_get_stream(const scmoe_ctx* ctx);
 /* Waits for the stream; returns (and clears) any latched device-side error. */
 int scmoe_synchronize(scmoe_ctx* ctx);
+/* SM budget of this context's persistent kernels (CTAs of the exact router /
+ * the grouped GEMM; 0 = every SM).  A context whose GEMMs run beside NCCL
+ * collectives (e.g. the dense branch under the EP all-to-all) leaves SMs
+ * free for the communication kernels this way. */
+int scmoe_ctx_set_sm_budget(scmoe_ctx* ctx, int router_sms, int gemm_sms);
 /* Number of kernels this context has launched (instrumentation). */
 uint64_t scmoe_kernel_launches(const scmoe_ctx* ctx);
 const char* scmoe_version(void);

@@ -139,6 +139,7 @@ _PROTOS = {
     "scmoe_layer_forward_batches": (C.c_int, [_P, _P, _P, _SZ, _P, _P, _P, _SZ, C.c_int, _P, _P,
                                               _P, _P]),
     "scmoe_dense_ffn": (C.c_int, [_P, _P, _P, _P, _SZ, _P]),
+    "scmoe_ctx_set_sm_budget": (C.c_int, [_P, C.c_int, C.c_int]),
     "scmoe_layer_forward_host_batches": (C.c_int, [_P, _P, _P, _SZ, _P, _P, _P, _SZ, C.c_int, _P,
                                                    _P, _P, _P]),
     "scmoe_bank_init_uniform_shard": (C.c_int, [_P, _P, _U64, _U64, C.c_double, _SZ]),
@@ -211,6 +212,10 @@ class Context:
 
     def kernel_launches(self) -> int:
         return int(lib().scmoe_kernel_launches(self._h))
+
+    def set_sm_budget(self, router_sms: int = 0, gemm_sms: int = 0):
+        """Cap the CTAs of the persistent router / grouped GEMM (0 = all SMs)."""
+        self._check(lib().scmoe_ctx_set_sm_budget(self._h, router_sms, gemm_sms))
 
     def profile(self, on: bool = True):
         self._check(lib().scmoe_profile_enable(self._h, int(on)))

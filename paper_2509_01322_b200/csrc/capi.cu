@@ -342,6 +342,16 @@ int scmoe_set_stream(scmoe_ctx* c, void* s) {
 }
 void* scmoe_get_stream(const scmoe_ctx* c) { return c ? (void*)c->stream : nullptr; }
 
+int scmoe_ctx_set_sm_budget(scmoe_ctx* c, int router_sms, int gemm_sms) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        if (router_sms < 0 || gemm_sms < 0)
+            SCMOE_THROW(SCMOE_ERR_PARAMETER, "sm budget must be >= 0");
+        c->router_sms = router_sms;
+        c->gemm_sms = gemm_sms;
+    });
+}
+
 int scmoe_synchronize(scmoe_ctx* c) {
     return guarded(c, [&] {
         require_ctx(c);

@@ -12,6 +12,14 @@ handled locally with no communication.  Per layer:
     6. return     all-to-all of the expert output rows, in received order
     7. combine    rank-order combine + zero-expert identity + residual
 
+With the dense shortcut branch enabled (GpuOps.enable_dense, SURVEY.md 8f1 /
+config D) the layer also computes dd = a1 + ffn_block(rmsnorm(a1))
+(model.hpp:390-391) on a second context and stream, concurrently with steps
+1-6 -- the ScMoE overlap window: the dispatch and return all-to-alls hide
+under the dense GEMMs -- and dd is the residual of step 7 (the second MLA,
+model.hpp:392-393, is out of scope, so a3 = dd).  Its GEMMs are capped below
+the SM count so the NCCL kernels always find free SMs.
+
 Expert rows are returned per slot and combined at the source in the
 reference's rank order (blocks.hpp:251-274), so the G-rank output is bitwise
 equal to the single-GPU output.  The transport is torch.distributed's NCCL
@@ -29,7 +37,7 @@ import torch
 import torch.distributed as dist
 
 from . import _P, Context, lib
-from .layer import LayerShape
+from .layer import DenseFFN, LayerShape
 
 
 class GpuOps:
@@ -65,6 +73,27 @@ class GpuOps:
 
     def _chk(self, rc):
         self.ctx._check(rc)
+
+    def enable_dense(self, device: int, inter: int, seed: int, reserve_sms: int = 16):
+        """Dense shortcut FFN on its own context + stream; its persistent GEMMs
+        leave `reserve_sms` SMs to the communication kernels."""
+        sms = torch.cuda.get_device_properties(device).multi_processor_count
+        self.dense_ctx = Context(device)
+        self.dense_stream = torch.cuda.Stream()
+        self.dense_ctx.set_stream(self.dense_stream.cuda_stream)
+        self.dense_ctx.set_sm_budget(0, max(1, sms - reserve_sms))
+        self.dense = DenseFFN(self.dense_ctx, self.shape.d, inter, seed=seed)
+        self.dense_ctx.synchronize()
+
+    def dense_forward(self, a1: torch.Tensor, gain: Optional[torch.Tensor], T: int):
+        """dd = a1 + ffn_block(rmsnorm(a1)) on the dense stream (not waited)."""
+        self.dense_stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self.dense_stream):
+            dd = torch.empty(T, self.shape.d, dtype=torch.float32, device="cuda")
+            self.dense.forward(a1.data_ptr(), None if gain is None else gain.data_ptr(), T,
+                               dd.data_ptr())
+        dd.record_stream(self.stream)  # consumed by the combine on the layer's stream
+        return dd
 
     def route(self, a1: torch.Tensor, gain: Optional[torch.Tensor], T: int):
         s = self.shape
@@ -119,6 +148,9 @@ class GpuOps:
 
     def close(self):
         L = lib()
+        if getattr(self, "dense", None) is not None:
+            self.dense.close()
+            self.dense = None
         L.scmoe_bank_destroy(self.ctx.handle, self.bank)
         L.scmoe_router_destroy(self.ctx.handle, self.router)
 
@@ -129,24 +161,30 @@ class EPLayer:
     def __init__(self, ops, group=None, async_comm: bool = True):
         self.ops, self.group = ops, group
         self.async_comm = async_comm
+        # comm=False replaces the row all-to-alls by no-ops (receive buffers left
+        # uninitialised): the timing reference for the exposed-communication share
+        self.comm = True
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.last_stats = {}
 
     def forward(self, a1: torch.Tensor, a3: Optional[torch.Tensor], gain, T: int,
-                renormalize: bool = False, chunks: int = 1):
+                renormalize: bool = False, chunks: int = 1, dense: bool = False):
         """chunks > 1 splits the tokens into micro-chunks processed as a
         software pipeline: chunk c+1's routing runs while chunk
         c's rows are in flight, chunk c's expert GEMMs while chunk c+1's rows
         are in flight, and so on.  Results are bitwise identical to chunks=1
-        (every step is per-token independent)."""
+        (every step is per-token independent).  dense=True runs the dense
+        shortcut branch concurrently and uses dd as the residual (a3 ignored)."""
         stream = getattr(self.ops, "stream", None)
         if stream is None:
             return self._forward(a1, a3, gain, T, renormalize, chunks)
         # inputs produced on the caller's stream must be complete first
         stream.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(stream):
-            res = self._forward(a1, a3, gain, T, renormalize, chunks)
+            dd = self.ops.dense_forward(a1, gain, T) if dense else None
+            res = self._forward(a1, dd if dense else a3, gain, T, renormalize, chunks,
+                                wait_residual=self.ops.dense_stream if dense else None)
         torch.cuda.current_stream().wait_stream(stream)
         for t in res:
             t.record_stream(torch.cuda.current_stream())
@@ -167,11 +205,16 @@ class EPLayer:
         n_send, n_recv = sum(send_split), sum(recv_split)
         send_rows = ops.gather(hb, send_token, n_send)
         recv_rows = torch.empty(n_recv, hb.shape[1], dtype=hb.dtype, device=hb.device)
-        w_rows = dist.all_to_all_single(recv_rows, send_rows, recv_split, send_split,
-                                        group=self.group, async_op=self.async_comm)
         recv_expert = torch.empty(n_recv, dtype=send_expert.dtype, device=send_expert.device)
-        w_exp = dist.all_to_all_single(recv_expert, send_expert[:n_send].contiguous(), recv_split,
-                                       send_split, group=self.group, async_op=self.async_comm)
+        if self.comm:
+            w_rows = dist.all_to_all_single(recv_rows, send_rows, recv_split, send_split,
+                                            group=self.group, async_op=self.async_comm)
+            w_exp = dist.all_to_all_single(recv_expert, send_expert[:n_send].contiguous(),
+                                           recv_split, send_split, group=self.group,
+                                           async_op=self.async_comm)
+        else:  # timing reference: received rows are garbage, expert ids valid
+            recv_expert.fill_(ops.first if hasattr(ops, "first") else 0)
+            w_rows = w_exp = None
         return dict(t0=t0, T=T, hmoe=hmoe, idx=idx, gates=gates, cnt=cnt, slot_pos=slot_pos,
                     send_split=send_split, recv_split=recv_split, n_send=n_send, n_recv=n_recv,
                     recv_rows=recv_rows, recv_expert=recv_expert, waits=[w_rows, w_exp],
@@ -183,20 +226,23 @@ class EPLayer:
                 w.wait()
         y_rows = self.ops.experts(st["recv_rows"], st["recv_expert"])
         back = torch.empty(st["n_send"], st["width"], dtype=st["dtype"], device=y_rows.device)
-        st["w_back"] = dist.all_to_all_single(back, y_rows, st["send_split"], st["recv_split"],
-                                              group=self.group, async_op=self.async_comm)
+        st["w_back"] = (dist.all_to_all_single(back, y_rows, st["send_split"], st["recv_split"],
+                                               group=self.group, async_op=self.async_comm)
+                        if self.comm else None)
         st["back"] = back
         st["keep"].append(y_rows)
 
-    def _combine(self, st, a3, renormalize):
+    def _combine(self, st, a3, renormalize, wait_residual=None):
         w = st.pop("w_back")
         if w is not None:
             w.wait()
+        if wait_residual is not None:  # dd from the dense stream
+            torch.cuda.current_stream().wait_stream(wait_residual)
         a3c = None if a3 is None else a3.view(-1)[st["t0"] * self.d:(st["t0"] + st["T"]) * self.d]
         return self.ops.combine(st["hmoe"], st["back"], st["slot_pos"], st["idx"], st["gates"],
                                 st["T"], a3c, renormalize)
 
-    def _forward(self, a1, a3, gain, T, renormalize, chunks):
+    def _forward(self, a1, a3, gain, T, renormalize, chunks, wait_residual=None):
         self.d = self.ops.shape.d if hasattr(self.ops, "shape") else a1.numel() // T
         chunks = max(1, min(chunks, T))
         bounds = [T * c // chunks for c in range(chunks + 1)]
@@ -210,7 +256,7 @@ class EPLayer:
             if 0 <= c - 1 < chunks:
                 self._experts(states[c - 1])
             if 0 <= c - 2 < chunks:
-                outs.append(self._combine(states[c - 2], a3, renormalize))
+                outs.append(self._combine(states[c - 2], a3, renormalize, wait_residual))
         n_send = sum(s["n_send"] for s in states)
         n_recv = sum(s["n_recv"] for s in states)
         self.last_stats = {"send_rows": n_send, "recv_rows": n_recv, "chunks": chunks,

@@ -12,7 +12,7 @@ sys.path.insert(0, ROOT)
 pytestmark = pytest.mark.gpu
 
 
-def _worker(rank, world, port, q, chunks=1):
+def _worker(rank, world, port, q, chunks=1, dense=False):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -30,14 +30,22 @@ def _worker(rank, world, port, q, chunks=1):
         a1 = torch.from_numpy(P.fill_normal(P.stream_seed(9, rank), T * shape.d)).cuda()
         a3 = torch.from_numpy(P.fill_normal(P.stream_seed(10, rank), T * shape.d)).cuda()
         ctx = P.Context(rank)
-        ep = EPLayer(GpuOps(ctx, shape, rank, world, seed=3))
-        out, idx, gates, cnt = ep.forward(a1, a3, None, T, chunks=chunks)
+        ops = GpuOps(ctx, shape, rank, world, seed=3)
+        if dense:
+            ops.enable_dense(rank, inter=1024, seed=7)
+        ep = EPLayer(ops)
+        out, idx, gates, cnt = ep.forward(a1, a3, None, T, chunks=chunks, dense=dense)
         torch.cuda.synchronize()
         # single-GPU reference: same seed => same router and the full expert set
         ctx1 = P.Context(rank)
         s1 = torch.cuda.Stream()
         ctx1.set_stream(s1.cuda_stream)
         full = DeviceLayer(ctx1, shape, seed=3)
+        if dense:  # the dense branch's dd is the MoE residual (a3 = dd)
+            from paper_2509_01322_b200.layer import DenseFFN
+            dn = DenseFFN(ctx1, shape.d, 1024, seed=7)
+            a3 = torch.empty_like(a1)
+            dn.forward(a1.data_ptr(), None, T, a3.data_ptr())
         idx1 = torch.empty_like(idx)
         gates1 = torch.empty_like(gates)
         cnt1 = torch.empty_like(cnt)
@@ -57,8 +65,10 @@ def _worker(rank, world, port, q, chunks=1):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,chunks", [(1, 1), (2, 1), (2, 2), (4, 3)])
-def test_ep_equals_single_gpu_bitwise(world, chunks):
+@pytest.mark.parametrize("world,chunks,dense", [(1, 1, False), (2, 1, False), (2, 2, False),
+                                                (4, 3, False), (1, 1, True), (2, 1, True),
+                                                (4, 2, True)])
+def test_ep_equals_single_gpu_bitwise(world, chunks, dense):
     import torch
     import torch.multiprocessing as mp
     n = torch.cuda.device_count()
@@ -67,7 +77,8 @@ def test_ep_equals_single_gpu_bitwise(world, chunks):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = 29700 + os.getpid() % 200
-    procs = [ctx.Process(target=_worker, args=(r, world, port + chunks, q, chunks))
+    procs = [ctx.Process(target=_worker, args=(r, world, port + chunks + 7 * dense, q, chunks,
+                                               dense))
              for r in range(world)]
     for p in procs:
         p.start()

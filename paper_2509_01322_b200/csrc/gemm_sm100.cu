@@ -58,7 +58,8 @@ constexpr int TMEM_COLS = 512;
 constexpr int EPI_WARPS = 4 * SLABS;             // one per (TMEM lane quadrant, slab)
 constexpr int EPI_WARP0 = 3;                     // warps 0: W producer, 1: MMA, 2: X producer
 constexpr int NUM_THREADS = 32 * (EPI_WARP0 + EPI_WARPS);
-constexpr int EPI_STAGE_BYTES = EPI_WARPS * 32 * 80;  // epilogue transpose buffers
+constexpr int EPI_PITCH = BM * 2 + 16;                // epilogue staging row (+16 B pad)
+constexpr int EPI_STAGE_BYTES = 32 * EPI_PITCH;          // [32 tokens][256 rows] bf16
 constexpr int SMEM_BYTES = RING_BYTES + 1024 /*align*/ + 256 /*barriers*/ + EPI_STAGE_BYTES;
 
 static_assert(SLABS * NT <= TMEM_COLS, "TMEM overflow");
@@ -117,10 +118,13 @@ struct GemmArgs {
     __nv_bfloat16* out;  // [rows][M]
     int M, K;            // weight rows per expert, reduction length
     int silu;
-    int debug;           // bit 0: skip epilogue stores (timing experiments only)
+    int debug;           // timing experiments only: bit 0 skip epilogue stores,
+                         // bit 1 skip the epilogue (release TMEM at once)
 };
 
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+// <= 64 registers: one GEMM CTA (352 threads) must leave room for the
+// co-resident router CTA (256 x 128 registers) on every SM sub-partition.
+__global__ void __maxnreg__(64)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_w,
                         const __grid_constant__ CUtensorMap map_x, const GemmArgs args) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -318,43 +322,53 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     } else {
         // ===== epilogue (warps 3..10: one warp per TMEM lane quadrant and slab) =====
         const int quad = warp & 3;  // TMEM lane quadrant this warp may access
-        const int s = (warp - EPI_WARP0) >> 2;  // weight slab this warp drains
-        // Per-warp 32 tokens x 32 rows bf16 transpose buffer (80 B row pitch:
-        // 16-byte reads of 8 consecutive lanes hit distinct banks).
-        unsigned char* stage_base = smem + RING_BYTES + 256 + (warp - EPI_WARP0) * 32 * 80;
+        const int ew = warp - EPI_WARP0;
+        const int s = ew >> 2;  // weight slab this warp drains
+        // Shared [32 tokens][256 rows] bf16 staging, row pitch EPI_PITCH: the
+        // 8 warps each write their 32 rows of a 32-token chunk; then every
+        // token row of the unit (256 rows = 512 contiguous bytes) leaves by a
+        // bulk async copy (TMA engine, cp.async.bulk shared -> global) issued
+        // by lane t < 4 of warp ew for token ew*4 + t.  The stores thus never
+        // occupy the LSU, and a row past the tile end is simply not issued.
+        // Named barrier 1 syncs the 8 epilogue warps.
+        unsigned char* stage = smem + RING_BYTES + 256;
+        const int mrow = s * 128 + quad * 32;  // this warp's rows within the unit
+        constexpr int ROWS_PER_WARP = 32 / EPI_WARPS;
         int local = 0;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++local) {
             const TokenTile tile = args.tiles[u / mblocks];
             const int mb = u % mblocks;
             mbar_wait(tfull, local & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            {
-                const int m0 = mb * BM + s * 128 + quad * 32;  // this warp's 32 rows
+            if (!(args.debug & 2)) {
                 const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + s * NT;
                 for (int j0 = 0; j0 < tile.count; j0 += 32) {
                     uint32_t v[32];
-                    tmem_ld32(taddr + j0, v);  // v[jj] = D[m0 + lane][j0 + jj]
+                    tmem_ld32(taddr + j0, v);  // v[jj] = D[mb*BM + mrow + lane][j0 + jj]
+                    // the previous chunk's bulk copies have read the staging
+                    if (lane < ROWS_PER_WARP)
+                        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32) : "memory");
 #pragma unroll
                     for (int jj = 0; jj < 32; ++jj) {
                         float f = __uint_as_float(v[jj]);
                         if (args.silu) f = silu_fast(f);
-                        *reinterpret_cast<__nv_bfloat16*>(stage_base + jj * 80 + lane * 2) =
+                        *reinterpret_cast<__nv_bfloat16*>(stage + jj * EPI_PITCH + (mrow + lane) * 2) =
                             __float2bfloat16_rn(f);
                     }
-                    __syncwarp();
-                    // lane l writes token j0+l: 32 consecutive rows m0..m0+31 = 64 B
-                    const int j = j0 + lane;
-                    if (j < tile.count && !(args.debug & 1)) {
-                        const uint4* src = reinterpret_cast<const uint4*>(stage_base + lane * 80);
-                        uint4* dst = reinterpret_cast<uint4*>(
-                            args.out + (size_t)(tile.pos + j) * args.M + m0);
-                        const uint4 q0 = src[0], q1 = src[1], q2 = src[2], q3 = src[3];
-                        dst[0] = q0;
-                        dst[1] = q1;
-                        dst[2] = q2;
-                        dst[3] = q3;
+                    // generic-proxy writes -> visible to the async (bulk copy) proxy
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32) : "memory");
+                    const int jj = ew * ROWS_PER_WARP + lane;
+                    if (lane < ROWS_PER_WARP && j0 + jj < tile.count && !(args.debug & 1)) {
+                        __nv_bfloat16* dst = args.out + (size_t)(tile.pos + j0 + jj) * args.M + mb * BM;
+                        asm volatile(
+                            "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                                reinterpret_cast<uint64_t>(dst)),
+                            "r"(smem_u32(stage + jj * EPI_PITCH)), "n"(BM * 2)
+                            : "memory");
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                     }
-                    __syncwarp();
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -363,6 +377,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
     }
 
+    if (warp >= EPI_WARP0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");

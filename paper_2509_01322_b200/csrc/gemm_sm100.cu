@@ -119,8 +119,31 @@ struct GemmArgs {
     int M, K;            // weight rows per expert, reduction length
     int silu;
     int debug;           // timing experiments only: bit 0 skip epilogue stores,
-                         // bit 1 skip the epilogue (release TMEM at once)
+                         // bit 1 skip the epilogue (release TMEM at once),
+                         // bit 2 tile-major unit order, bit 3 weights always evict-first
 };
+
+// Unit u -> (token tile, 256-row weight block).  Units are expert-major:
+// the tiles of one expert (TokenTile.pad = index in the expert << 16 | the
+// expert's tile count) take consecutive units for each weight block, so the
+// CTAs streaming the same expert weights run side by side and share them
+// through L2 (an expert with 512 tokens has 3 tiles of <= 192).  pad = 0
+// (row tiles) keeps the plain tile-major order.
+__device__ __forceinline__ void unit_map(int u, int mblocks, const TokenTile* tiles, int& t,
+                                         int& mb, int debug) {
+    const int t0 = u / mblocks;
+    const int g = (debug & 4) ? 0 : tiles[t0].pad;
+    const int n = g & 0xffff;
+    if (n <= 1) {
+        t = t0;
+        mb = u % mblocks;
+        return;
+    }
+    const int first = t0 - (g >> 16);
+    const int local = u - first * mblocks;
+    mb = local / n;
+    t = first + local % n;
+}
 
 // <= 64 registers: one GEMM CTA (352 threads) must leave room for the
 // co-resident router CTA (256 x 128 registers) on every SM sub-partition.
@@ -178,15 +201,21 @@ __global__ void __maxnreg__(64)
     if (warp == 0) {
         // ===== weight producer: streams W from HBM, A_STAGES deep =====
         if (lane == 0) {
-            const uint64_t pol_w = policy_evict_first();
+            // weights are read once (evict-first) unless the expert has several
+            // token tiles, whose units stream the same block side by side:
+            // then keep it (evict-last) until the sibling CTAs have read it
+            const uint64_t pol_once = policy_evict_first(), pol_shared = policy_evict_last();
             int stage = 0;
             uint32_t phase = 0;
             for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-                const TokenTile tile = args.tiles[u / mblocks];
-                const int mb = u % mblocks;
+                int ti, mb;
+                unit_map(u, mblocks, args.tiles, ti, mb, args.debug);
+                const TokenTile tile = args.tiles[ti];
                 // blocked weight layout (wblk_index): each (128-row, 64-col) tile is
                 // 128 contiguous 64-element rows of the 2-D view the map describes
                 const int ebase = tile.e * (args.M / 128) * kblocks * 128;
+                const uint64_t pol_w = (tile.pad & 0xffff) > 1 && !(args.debug & 8) ? pol_shared
+                                                                                   : pol_once;
                 for (int kb = 0; kb < kblocks; ++kb) {
                     mbar_wait(&a_empty[stage], phase ^ 1);
                     unsigned char* abase = a_ring + stage * A_STAGE_BYTES;
@@ -212,7 +241,9 @@ __global__ void __maxnreg__(64)
         int pending = -1;  // gather mode: stage whose copies are in flight, not yet published
         constexpr int kRowsPerLane = (NT + 31) / 32;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-            const TokenTile tile = args.tiles[u / mblocks];
+            int ti, mb_;
+            unit_map(u, mblocks, args.tiles, ti, mb_, args.debug);
+            const TokenTile tile = args.tiles[ti];
             const int n_eff = max(16, (tile.count + 15) & ~15);
             // gather mode: this lane's rows r = lane + 32 i (padding rows repeat
             // the tile's last token; their columns are never stored)
@@ -282,7 +313,9 @@ __global__ void __maxnreg__(64)
         uint32_t aph = 0, bph = 0;
         int local = 0;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++local) {
-            const TokenTile tile = args.tiles[u / mblocks];
+            int ti, mb_;
+            unit_map(u, mblocks, args.tiles, ti, mb_, args.debug);
+            const TokenTile tile = args.tiles[ti];
             const int n_eff = max(16, (tile.count + 15) & ~15);
             const uint32_t idesc = make_idesc(128, n_eff);
             mbar_wait(tempty, (local & 1) ^ 1);
@@ -336,8 +369,9 @@ __global__ void __maxnreg__(64)
         constexpr int ROWS_PER_WARP = 32 / EPI_WARPS;
         int local = 0;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++local) {
-            const TokenTile tile = args.tiles[u / mblocks];
-            const int mb = u % mblocks;
+            int ti, mb;
+            unit_map(u, mblocks, args.tiles, ti, mb, args.debug);
+            const TokenTile tile = args.tiles[ti];
             mbar_wait(tfull, local & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             if (!(args.debug & 2)) {

@@ -119,12 +119,15 @@ __global__ void __launch_bounds__(1024) perm_scan_kernel(int nblk, int E, int n_
     for (int e = e0; e < e1; ++e) {
         expert_base[e] = row_base;
         const int cnt = expert_count[e];
-        for (int r = 0; r < cnt; r += tile_rows) {
+        const int nt = (cnt + tile_rows - 1) / tile_rows;
+        // equal tiles (multiples of 16 rows): 256 tokens -> 2 x 128, not 192 + 64
+        const int step = nt > 1 ? min(tile_rows, ((cnt + nt - 1) / nt + 15) & ~15) : tile_rows;
+        for (int r = 0, k = 0; r < cnt; r += step, ++k) {
             TokenTile tt;
             tt.e = e;
             tt.pos = row_base + r;
-            tt.count = min(tile_rows, cnt - r);
-            tt.pad = 0;
+            tt.count = min(step, cnt - r);
+            tt.pad = (k << 16) | nt;  // position in the expert's tiles | their count
             tiles[tile_base++] = tt;
         }
         row_base += cnt;

@@ -468,7 +468,7 @@ def run_b200_ep(args):
     T = args.tokens or cfg["tokens"]
     ctx = P.Context(local)
     ops = GpuOps(ctx, LONGCAT, rank, ws, seed=SEED_W)
-    ep = EPLayer(ops)
+    ep = EPLayer(ops, transport=args.ep_transport)
     a1_h = P.fill_normal(P.stream_seed(SEED_X, rank), T * D, threads=os.cpu_count() or 8)
     a3_h = P.fill_normal(P.stream_seed(SEED_X + 1, rank), T * D, threads=os.cpu_count() or 8)
     a1 = torch.from_numpy(a1_h).cuda()
@@ -589,9 +589,12 @@ def run_b200_ep(args):
                                f"(BASELINE config 4 shape, {T} tokens per GPU)",
                    "tokens_per_gpu": T, "d_model": D, "n_ffn": N_FFN, "n_zero": N_ZERO,
                    "top_k": TOPK, "inter": INTER, "experts_per_gpu": n_local,
-                   "parallelism": f"ep{ws} (NCCL all_to_all dispatch/return, {chunks}-chunk "
-                                  "software pipeline overlapping routing / expert GEMMs with "
-                                  "the all-to-alls)",
+                   "parallelism": (f"ep{ws}: dispatch = peer stores into the owners' "
+                                   "symmetric buffers over NVLink, return fused into GEMM2's "
+                                   "epilogue (rows written to the source rank)"
+                                   if args.ep_transport == "p2p" else
+                                   f"ep{ws} (NCCL all_to_all dispatch/return, {chunks}-chunk "
+                                   "software pipeline)"),
                    "a2a_bytes_each_way_rank0": ep.last_stats["a2a_bytes_each_way"],
                    "mean_ffn_per_token": float(ffn.size) / T},
         "e2e": {"value": T * ws / (e2e_ms / 1e3), "unit": "tokens/s",
@@ -627,6 +630,9 @@ def main():
     ap.add_argument("--schedule", default="pipelined", choices=["pipelined", "serial"])
     ap.add_argument("--parallel", default="ep", choices=["ep", "replicated"],
                     help="N>1: expert-parallel (default) or replicated experts")
+    # p2p: dispatch stored straight into the peers' symmetric buffers over NVLink,
+    # return fused into GEMM2's epilogue; nccl: all_to_all_single
+    ap.add_argument("--ep-transport", default="p2p", choices=["p2p", "nccl"])
     ap.add_argument("--ep-chunks", type=int, default=1,
                     help="EP software-pipeline depth (token chunks per step)")
     args = ap.parse_args()

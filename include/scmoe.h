@@ -267,6 +267,23 @@ int scmoe_moe_rows(scmoe_ctx* ctx, scmoe_bank* b, const void* x_bf16, const int*
                    int expert_offset, size_t rows, void* y_bf16);
 /* moe_combine (blocks.hpp:226-274) + residual from per-slot expert rows:
  * slot (t,s) with an FFN expert reads y_rows[slot_row[t*K+s]]. */
+/* Peer-memory transport (NVLink, symmetric buffers mapped in every rank; the
+ * caller owns the mapping, e.g. torch symmetric memory):
+ * scmoe_ep_put_rows -- the dispatch: send row j (scmoe_ep_plan order, grouped
+ *   by destination: rows [send_start[g], send_start[g+1]) go to rank g) is
+ *   stored into peer_rows[g] at row dst_offset[g] + j - send_start[g], its
+ *   expert id into peer_expert[g]; all arrays are device arrays, peer_* hold
+ *   device addresses.  A cross-rank barrier must follow before the rows are read.
+ * scmoe_moe_rows_to -- scmoe_moe_rows whose GEMM2 epilogue writes the output
+ *   row of received row r straight to row_dst[r] (an address, typically the
+ *   source rank's receive-back buffer over NVLink): the return all-to-all is
+ *   fused into the GEMM, overlapping its tiles.  Barrier before the combine. */
+int scmoe_ep_put_rows(scmoe_ctx* ctx, const void* src_bf16, size_t d, const int* send_token,
+                      const int* send_expert, size_t n_send, const int* send_start,
+                      const int64_t* dst_offset, const uint64_t* peer_rows,
+                      const uint64_t* peer_expert, int world);
+int scmoe_moe_rows_to(scmoe_ctx* ctx, scmoe_bank* b, const void* x_bf16, const int* row_expert,
+                      int expert_offset, size_t rows, const uint64_t* row_dst);
 int scmoe_combine_rows(scmoe_ctx* ctx, scmoe_bank* b, const float* x, const void* y_rows_bf16,
                        const int* slot_row, const uint32_t* indices, const double* gates,
                        size_t tokens, size_t top_k, size_t n_ffn_total, int renormalize,

@@ -139,6 +139,8 @@ _PROTOS = {
     "scmoe_layer_forward_batches": (C.c_int, [_P, _P, _P, _SZ, _P, _P, _P, _SZ, C.c_int, _P, _P,
                                               _P, _P]),
     "scmoe_dense_ffn": (C.c_int, [_P, _P, _P, _P, _SZ, _P]),
+    "scmoe_ep_put_rows": (C.c_int, [_P, _P, _SZ, _P, _P, _SZ, _P, _P, _P, _P, C.c_int]),
+    "scmoe_moe_rows_to": (C.c_int, [_P, _P, _P, _P, C.c_int, _SZ, _P]),
     "scmoe_ctx_set_sm_budget": (C.c_int, [_P, C.c_int, C.c_int]),
     "scmoe_layer_forward_host_batches": (C.c_int, [_P, _P, _P, _SZ, _P, _P, _P, _SZ, C.c_int, _P,
                                                    _P, _P, _P]),

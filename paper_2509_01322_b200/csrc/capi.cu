@@ -1174,44 +1174,85 @@ int scmoe_gather_rows_bf16(scmoe_ctx* c, const void* src, size_t d, const int* r
     });
 }
 
+namespace {
+// Expert rows of the received slots; GEMM2's rows go to y (received order,
+// through an unpermute copy) or, with row_dst, straight to row_dst[r] for
+// received row r (e.g. the source rank's buffer over NVLink).
+void moe_rows_impl(scmoe_ctx* c, scmoe_bank* b, const void* x_bf16, const int* row_expert,
+                   int expert_offset, size_t R, void* y_bf16, const uint64_t* row_dst) {
+    if (b->precision != SCMOE_PREC_BF16)
+        SCMOE_THROW(SCMOE_ERR_CONFIG, "moe_rows: needs a bf16 (tensor-core) bank");
+    if (R == 0) return;
+    const size_t d = b->d, I = b->inter, n = b->n;
+    Workspace& ws = c->ws;
+    uint32_t* loc = ws.ep_local.get<uint32_t>(R);
+    launch_ep_localize(c, row_expert, R, expert_offset, (int)n, loc);
+    // each row is a "token" routed to exactly one local expert (K = 1)
+    PermResult pr;
+    {
+        ProfScope _p(c, "permute");
+        pr = launch_permute(c, loc, R, 1, n, n, grouped_gemm_tile_rows());
+    }
+    const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x_bf16);
+    __nv_bfloat16* xp = ws.xp.get<__nv_bfloat16>(R * d);
+    __nv_bfloat16* h = ws.h.get<__nv_bfloat16>(R * I);
+    {
+        ProfScope _p(c, "gather");
+        launch_gather_bf16(c, xb, d, pr.row_token, pr.expert_base, n, R, xp);
+    }
+    {
+        ProfScope _p(c, "gemm1_tcgen05");
+        launch_grouped_gemm_bf16(c, b->w1t, n, I, d, xp, R, nullptr, h, 1, pr.tiles, pr.n_tiles,
+                                 pr.max_tiles, grouped_gemm_tile_rows());
+    }
+    if (row_dst) {
+        // permuted row p holds received row row_token[p]
+        ProfScope _p(c, "gemm2_tcgen05");
+        launch_grouped_gemm_bf16(c, b->w2t, n, d, I, h, R, nullptr, nullptr, 0, pr.tiles,
+                                 pr.n_tiles, pr.max_tiles, grouped_gemm_tile_rows(), row_dst,
+                                 pr.row_token);
+        return;
+    }
+    __nv_bfloat16* y = ws.ep_y.get<__nv_bfloat16>(R * d);
+    {
+        ProfScope _p(c, "gemm2_tcgen05");
+        launch_grouped_gemm_bf16(c, b->w2t, n, d, I, h, R, nullptr, y, 0, pr.tiles, pr.n_tiles,
+                                 pr.max_tiles, grouped_gemm_tile_rows());
+    }
+    // back to the received order: y_out[r] = y[slot_pos[r]]
+    ProfScope _p(c, "unpermute");
+    launch_gather_rows_bf16(c, y, d, pr.slot_pos, R, static_cast<__nv_bfloat16*>(y_bf16));
+}
+}  // namespace
+
 int scmoe_moe_rows(scmoe_ctx* c, scmoe_bank* b, const void* x_bf16, const int* row_expert,
                    int expert_offset, size_t R, void* y_bf16) {
     return guarded(c, [&] {
         require_ctx(c);
-        if (b->precision != SCMOE_PREC_BF16)
-            SCMOE_THROW(SCMOE_ERR_CONFIG, "moe_rows: needs a bf16 (tensor-core) bank");
-        if (R == 0) return;
-        const size_t d = b->d, I = b->inter, n = b->n;
-        Workspace& ws = c->ws;
-        uint32_t* loc = ws.ep_local.get<uint32_t>(R);
-        launch_ep_localize(c, row_expert, R, expert_offset, (int)n, loc);
-        // each row is a "token" routed to exactly one local expert (K = 1)
-        PermResult pr;
-        {
-            ProfScope _p(c, "permute");
-            pr = launch_permute(c, loc, R, 1, n, n, grouped_gemm_tile_rows());
-        }
-        const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x_bf16);
-        __nv_bfloat16* xp = ws.xp.get<__nv_bfloat16>(R * d);
-        __nv_bfloat16* h = ws.h.get<__nv_bfloat16>(R * I);
-        __nv_bfloat16* y = ws.ep_y.get<__nv_bfloat16>(R * d);
-        {
-            ProfScope _p(c, "gather");
-            launch_gather_bf16(c, xb, d, pr.row_token, pr.expert_base, n, R, xp);
-        }
-        {
-            ProfScope _p(c, "gemm1_tcgen05");
-            launch_grouped_gemm_bf16(c, b->w1t, n, I, d, xp, R, nullptr, h, 1, pr.tiles,
-                                     pr.n_tiles, pr.max_tiles, grouped_gemm_tile_rows());
-        }
-        {
-            ProfScope _p(c, "gemm2_tcgen05");
-            launch_grouped_gemm_bf16(c, b->w2t, n, d, I, h, R, nullptr, y, 0, pr.tiles,
-                                     pr.n_tiles, pr.max_tiles, grouped_gemm_tile_rows());
-        }
-        // back to the received order: y_out[r] = y[slot_pos[r]]
-        ProfScope _p(c, "unpermute");
-        launch_gather_rows_bf16(c, y, d, pr.slot_pos, R, static_cast<__nv_bfloat16*>(y_bf16));
+        moe_rows_impl(c, b, x_bf16, row_expert, expert_offset, R, y_bf16, nullptr);
+    });
+}
+
+int scmoe_moe_rows_to(scmoe_ctx* c, scmoe_bank* b, const void* x_bf16, const int* row_expert,
+                      int expert_offset, size_t R, const uint64_t* row_dst) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        SCMOE_CHECK_ARG(row_dst != nullptr || R == 0, SCMOE_ERR_PARAMETER,
+                        "moe_rows_to: row_dst is required");
+        moe_rows_impl(c, b, x_bf16, row_expert, expert_offset, R, nullptr, row_dst);
+    });
+}
+
+int scmoe_ep_put_rows(scmoe_ctx* c, const void* src_bf16, size_t d, const int* send_token,
+                      const int* send_expert, size_t n_send, const int* send_start,
+                      const int64_t* dst_offset, const uint64_t* peer_rows,
+                      const uint64_t* peer_expert, int world) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        ProfScope _p(c, "ep_put_rows");
+        launch_ep_put_rows(c, static_cast<const __nv_bfloat16*>(src_bf16), d, send_token,
+                           send_expert, n_send, send_start, dst_offset, peer_rows, peer_expert,
+                           world);
     });
 }
 

@@ -116,6 +116,10 @@ struct GemmArgs {
     const int* x_rows;   // gather mode: permuted row -> source row of X (nullptr: X is permuted)
     const __nv_bfloat16* x;  // X base (gather mode reads rows directly)
     __nv_bfloat16* out;  // [rows][M]
+    // optional scattered output: permuted row p goes to row_dst[row_ids[p]]
+    // (a full M-wide row, possibly in a peer GPU's memory over NVLink)
+    const uint64_t* row_dst;
+    const int* row_ids;
     int M, K;            // weight rows per expert, reduction length
     int silu;
     int debug;           // timing experiments only: bit 0 skip epilogue stores,
@@ -395,7 +399,12 @@ __global__ void __maxnreg__(64)
                     asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32) : "memory");
                     const int jj = ew * ROWS_PER_WARP + lane;
                     if (lane < ROWS_PER_WARP && j0 + jj < tile.count && !(args.debug & 1)) {
-                        __nv_bfloat16* dst = args.out + (size_t)(tile.pos + j0 + jj) * args.M + mb * BM;
+                        const int p = tile.pos + j0 + jj;
+                        __nv_bfloat16* dst =
+                            (args.row_dst ? reinterpret_cast<__nv_bfloat16*>(
+                                                args.row_dst[args.row_ids ? args.row_ids[p] : p])
+                                          : args.out + (size_t)p * args.M) +
+                            mb * BM;
                         asm volatile(
                             "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
                                 reinterpret_cast<uint64_t>(dst)),
@@ -434,7 +443,8 @@ int grouped_gemm_tile_rows() { return NT; }
 void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_experts, size_t M,
                               size_t K, const __nv_bfloat16* X, size_t x_rows, const int* x_row_ids,
                               __nv_bfloat16* out, int silu, const TokenTile* tiles,
-                              const int* n_tiles_dev, size_t max_tiles, int tile_rows) {
+                              const int* n_tiles_dev, size_t max_tiles, int tile_rows,
+                              const uint64_t* row_dst, const int* row_ids) {
     if (max_tiles == 0 || n_experts == 0) return;
     SCMOE_CHECK_ARG(tile_rows == NT, SCMOE_ERR_INTERNAL, "gemm: tile rows must equal NT");
     SCMOE_CHECK_ARG(M % BM == 0 && K % BK == 0, SCMOE_ERR_DIMENSION,
@@ -456,6 +466,8 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
     a.x_rows = x_row_ids;
     a.x = X;
     a.out = out;
+    a.row_dst = row_dst;
+    a.row_ids = row_ids;
     a.M = (int)M;
     a.K = (int)K;
     a.silu = silu;

@@ -294,7 +294,14 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
                               size_t M, size_t K, const __nv_bfloat16* X, size_t x_rows,
                               const int* x_row_ids, __nv_bfloat16* out, int silu,
                               const TokenTile* tiles,
-                              const int* n_tiles_dev, size_t max_tiles, int tile_rows);
+                              const int* n_tiles_dev, size_t max_tiles, int tile_rows,
+                              const uint64_t* row_dst = nullptr, const int* row_ids = nullptr);
+// Expert-parallel dispatch over peer memory: send row j (rows sorted by
+// destination rank, send_start[G+1]) -> peer_rows[d] row dst_offset[d] + j - send_start[d].
+void launch_ep_put_rows(scmoe_ctx* c, const __nv_bfloat16* src, size_t d, const int* send_token,
+                        const int* send_expert, size_t n_send, const int* send_start,
+                        const int64_t* dst_offset, const uint64_t* peer_rows,
+                        const uint64_t* peer_expert, int G);
 
 }  // namespace scmoe
 

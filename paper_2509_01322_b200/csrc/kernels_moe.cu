@@ -805,6 +805,44 @@ __global__ void gather_rows_bf16_kernel(const __nv_bfloat16* __restrict__ src, i
     }
 }
 
+// Expert-parallel dispatch straight into the destination ranks' receive
+// buffers (symmetric memory mapped over NVLink): one warp per send row, 16-byte
+// stores (512 B per warp instruction); lane 0 also stores the row's expert id.
+__global__ void ep_put_rows_kernel(const __nv_bfloat16* __restrict__ src, int d,
+                                   const int* __restrict__ send_token,
+                                   const int* __restrict__ send_expert, int n_send,
+                                   const int* __restrict__ send_start,
+                                   const int64_t* __restrict__ dst_offset,
+                                   const uint64_t* __restrict__ peer_rows,
+                                   const uint64_t* __restrict__ peer_expert, int G) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int vec = d / 8;
+    for (int j = warp; j < n_send; j += nwarps) {
+        int dst = 0;
+        while (dst + 1 < G && send_start[dst + 1] <= j) ++dst;
+        const int64_t pos = dst_offset[dst] + (j - send_start[dst]);
+        const uint4* s = reinterpret_cast<const uint4*>(src + (size_t)send_token[j] * d);
+        uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(peer_rows[dst]) +
+                                            (size_t)pos * d);
+        for (int v = lane; v < vec; v += 32) o[v] = s[v];
+        if (lane == 0) reinterpret_cast<int*>(peer_expert[dst])[pos] = send_expert[j];
+    }
+}
+void launch_ep_put_rows(scmoe_ctx* c, const __nv_bfloat16* src, size_t d, const int* send_token,
+                        const int* send_expert, size_t n_send, const int* send_start,
+                        const int64_t* dst_offset, const uint64_t* peer_rows,
+                        const uint64_t* peer_expert, int G) {
+    if (n_send == 0) return;
+    SCMOE_CHECK_ARG(d % 8 == 0, SCMOE_ERR_DIMENSION, "ep_put_rows: d must be a multiple of 8");
+    const int blocks = c->num_sms * 4;
+    ep_put_rows_kernel<<<blocks, 256, 0, c->stream>>>(src, (int)d, send_token, send_expert,
+                                                      (int)n_send, send_start, dst_offset,
+                                                      peer_rows, peer_expert, G);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
 void launch_gather_rows_bf16(scmoe_ctx* c, const __nv_bfloat16* src, size_t d, const int* rows,
                              size_t n_rows, __nv_bfloat16* dst) {
     if (n_rows == 0) return;

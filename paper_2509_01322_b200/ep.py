@@ -95,6 +95,38 @@ class GpuOps:
         dd.record_stream(self.stream)  # consumed by the combine on the layer's stream
         return dd
 
+    # -- peer-memory transport (NVLink; torch symmetric memory as the mapping) --
+    def p2p_buffers(self, group, cap_recv: int, cap_send: int):
+        """(Re)allocates the symmetric receive / receive-back buffers (collective:
+        every rank calls it with the same capacities) and returns the peer
+        address tables."""
+        import torch.distributed._symmetric_memory as symm_mem
+        group = group if group is not None else dist.group.WORLD
+        d = self.shape.d
+        self.p2p_cap = (cap_recv, cap_send)
+        self.recv = symm_mem.empty((cap_recv, d), dtype=torch.bfloat16, device="cuda")
+        self.recv_exp = symm_mem.empty(cap_recv, dtype=torch.int32, device="cuda")
+        self.back = symm_mem.empty((cap_send, d), dtype=torch.bfloat16, device="cuda")
+        self.h_recv = symm_mem.rendezvous(self.recv, group)
+        self.h_exp = symm_mem.rendezvous(self.recv_exp, group)
+        self.h_back = symm_mem.rendezvous(self.back, group)
+        dev = lambda xs: torch.tensor(list(xs), dtype=torch.int64, device="cuda")  # noqa: E731
+        self.peer_recv = dev(self.h_recv.buffer_ptrs)
+        self.peer_exp = dev(self.h_exp.buffer_ptrs)
+        self.peer_back = dev(self.h_back.buffer_ptrs)
+
+    def put_rows(self, hb, send_token, send_expert, n_send, send_start, dst_offset):
+        self._chk(lib().scmoe_ep_put_rows(self.ctx.handle, hb.data_ptr(), self.shape.d,
+                                          send_token.data_ptr(), send_expert.data_ptr(), n_send,
+                                          send_start.data_ptr(), dst_offset.data_ptr(),
+                                          self.peer_recv.data_ptr(), self.peer_exp.data_ptr(),
+                                          self.world))
+
+    def experts_to(self, n_recv: int, row_dst: torch.Tensor):
+        self._chk(lib().scmoe_moe_rows_to(self.ctx.handle, self.bank, self.recv.data_ptr(),
+                                          self.recv_exp.data_ptr(), self.first, n_recv,
+                                          row_dst.data_ptr()))
+
     def route(self, a1: torch.Tensor, gain: Optional[torch.Tensor], T: int):
         s = self.shape
         hmoe = torch.empty(T, s.d, dtype=torch.float32, device="cuda")
@@ -158,9 +190,15 @@ class GpuOps:
 class EPLayer:
     """One ScMoE MoE branch sharded over the ranks of ``group``."""
 
-    def __init__(self, ops, group=None, async_comm: bool = True):
+    def __init__(self, ops, group=None, async_comm: bool = True, transport: str = "nccl"):
+        """transport "nccl": all_to_all_single for the rows; "p2p": the rows are
+        stored straight into the peers' symmetric buffers over NVLink by the
+        dispatch kernel and by GEMM2's epilogue (return fused into the GEMM)."""
         self.ops, self.group = ops, group
         self.async_comm = async_comm
+        if transport not in ("nccl", "p2p"):
+            raise ValueError("transport must be 'nccl' or 'p2p'")
+        self.transport = transport
         # comm=False replaces the row all-to-alls by no-ops (receive buffers left
         # uninitialised): the timing reference for the exposed-communication share
         self.comm = True
@@ -242,8 +280,62 @@ class EPLayer:
         return self.ops.combine(st["hmoe"], st["back"], st["slot_pos"], st["idx"], st["gates"],
                                 st["T"], a3c, renormalize)
 
+    def _forward_p2p(self, a1, a3, gain, T, renormalize, wait_residual=None):
+        """One chunk, peer-memory transport (see __init__)."""
+        ops, G, me = self.ops, self.world, self.rank
+        hmoe, hb, idx, gates, cnt = ops.route(a1, gain, T)
+        counts, slot_pos, send_token, send_expert = ops.plan(idx, T)
+        # full [src][dst] slot-count matrix on every rank: offsets + capacities
+        allc = torch.empty(G * G, dtype=counts.dtype, device=counts.device)
+        dist.all_gather_into_tensor(allc, counts, group=self.group)
+        Mh = allc.view(G, G).cpu().tolist()
+        n_send = sum(Mh[me])
+        n_recv = sum(Mh[s][me] for s in range(G))
+        need_r = max(sum(Mh[s][d] for s in range(G)) for d in range(G))
+        need_s = max(sum(r) for r in Mh)
+        cap = getattr(ops, "p2p_cap", (0, 0))
+        if need_r > cap[0] or need_s > cap[1]:  # same decision on every rank
+            ops.p2p_buffers(self.group, max(1, int(need_r * 1.25)), max(1, int(need_s * 1.25)))
+        send_start = [0]
+        for d in range(G):
+            send_start.append(send_start[-1] + Mh[me][d])
+        dst_offset = [sum(Mh[s][d] for s in range(me)) for d in range(G)]
+        recv_offset = [0]
+        for s in range(G):
+            recv_offset.append(recv_offset[-1] + Mh[s][me])
+        # received row r (from source s, its j-th row for me) returns to source s's
+        # back buffer at row (sum_{d<me} M[s][d]) + j
+        back_start = [sum(Mh[s][:me]) for s in range(G)]
+        dev = counts.device
+        rows_per_src = torch.tensor([Mh[s][me] for s in range(G)], dtype=torch.int64, device=dev)
+        src = torch.repeat_interleave(torch.arange(G, device=dev), rows_per_src, output_size=n_recv)
+        j = torch.arange(n_recv, dtype=torch.int64, device=dev) - \
+            torch.tensor(recv_offset[:G], dtype=torch.int64, device=dev)[src]
+        # comm=False (timing reference): no dispatch, GEMM2 rows stay local
+        back_ptr = ops.peer_back if self.comm else \
+            torch.full_like(ops.peer_back, ops.back.data_ptr())
+        row_dst = back_ptr[src] + (torch.tensor(back_start, dtype=torch.int64, device=dev)[src]
+                                   + j) * (ops.shape.d * 2)
+        if self.comm:
+            ops.put_rows(hb, send_token, send_expert, n_send,
+                         torch.tensor(send_start, dtype=torch.int32, device=dev),
+                         torch.tensor(dst_offset, dtype=torch.int64, device=dev))
+        else:
+            ops.recv_exp[:n_recv].fill_(ops.first)
+        ops.h_recv.barrier(channel=0)
+        ops.experts_to(n_recv, row_dst)
+        ops.h_back.barrier(channel=1)
+        if wait_residual is not None:
+            torch.cuda.current_stream().wait_stream(wait_residual)
+        out = ops.combine(hmoe, ops.back, slot_pos, idx, gates, T, a3, renormalize)
+        self.last_stats = {"send_rows": n_send, "recv_rows": n_recv, "chunks": 1,
+                           "transport": "p2p", "a2a_bytes_each_way": n_send * ops.shape.d * 2}
+        return out, idx, gates, cnt
+
     def _forward(self, a1, a3, gain, T, renormalize, chunks, wait_residual=None):
         self.d = self.ops.shape.d if hasattr(self.ops, "shape") else a1.numel() // T
+        if self.transport == "p2p":
+            return self._forward_p2p(a1, a3, gain, T, renormalize, wait_residual)
         chunks = max(1, min(chunks, T))
         bounds = [T * c // chunks for c in range(chunks + 1)]
         # issue order: D0 D1 E0 D2 E1 C0 ... so each collective has independent

@@ -12,7 +12,7 @@ sys.path.insert(0, ROOT)
 pytestmark = pytest.mark.gpu
 
 
-def _worker(rank, world, port, q, chunks=1, dense=False):
+def _worker(rank, world, port, q, chunks=1, dense=False, transport="nccl"):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -33,7 +33,7 @@ def _worker(rank, world, port, q, chunks=1, dense=False):
         ops = GpuOps(ctx, shape, rank, world, seed=3)
         if dense:
             ops.enable_dense(rank, inter=1024, seed=7)
-        ep = EPLayer(ops)
+        ep = EPLayer(ops, transport=transport)
         out, idx, gates, cnt = ep.forward(a1, a3, None, T, chunks=chunks, dense=dense)
         torch.cuda.synchronize()
         # single-GPU reference: same seed => same router and the full expert set
@@ -65,10 +65,12 @@ def _worker(rank, world, port, q, chunks=1, dense=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,chunks,dense", [(1, 1, False), (2, 1, False), (2, 2, False),
-                                                (4, 3, False), (1, 1, True), (2, 1, True),
-                                                (4, 2, True)])
-def test_ep_equals_single_gpu_bitwise(world, chunks, dense):
+@pytest.mark.parametrize("world,chunks,dense,transport", [
+    (1, 1, False, "nccl"), (2, 1, False, "nccl"), (2, 2, False, "nccl"), (4, 3, False, "nccl"),
+    (1, 1, True, "nccl"), (2, 1, True, "nccl"), (4, 2, True, "nccl"),
+    (1, 1, False, "p2p"), (2, 1, False, "p2p"), (4, 1, False, "p2p"), (2, 1, True, "p2p"),
+    (4, 1, True, "p2p")])
+def test_ep_equals_single_gpu_bitwise(world, chunks, dense, transport):
     import torch
     import torch.multiprocessing as mp
     n = torch.cuda.device_count()
@@ -77,8 +79,8 @@ def test_ep_equals_single_gpu_bitwise(world, chunks, dense):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = 29700 + os.getpid() % 200
-    procs = [ctx.Process(target=_worker, args=(r, world, port + chunks + 7 * dense, q, chunks,
-                                               dense))
+    port += chunks + 7 * dense + 17 * (transport == "p2p")
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, chunks, dense, transport))
              for r in range(world)]
     for p in procs:
         p.start()

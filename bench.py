@@ -479,24 +479,41 @@ def run_b200_ep(args):
     torch.cuda.synchronize()
     idx_h = idx.cpu().numpy().view(np.uint32)
     ffn = idx_h[idx_h < N_FFN]
+    def timed_ep(fn):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        barrier(ws)
+        torch.cuda.synchronize()
+        e0.record()
+        fn()
+        e1.record()
+        e1.synchronize()
+        torch.cuda.synchronize()
+        barrier(ws)
+        return e0.elapsed_time(e1) / args.steps
+
+    # serial steps (per-batch latency), with the per-stage profile
     ctx.profile(True)
     ctx.profile_flush()
-    l0 = ctx.kernel_launches()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    barrier(ws)
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        ev0.record()
-        for _ in range(args.steps):
-            out, idx, gates, cnt = ep.forward(a1, a3, None, T, chunks=chunks)
-        ev1.record()
-        ev1.synchronize()
-    torch.cuda.synchronize()
-    barrier(ws)
-    launches = ctx.kernel_launches() - l0
+    ms_serial = timed_ep(lambda: [ep.forward(a1, a3, None, T, chunks=chunks)
+                                  for _ in range(args.steps)])
     stages = ctx.profile_flush()
-    ms = ev0.elapsed_time(ev1) / args.steps
+    ctx.profile(False)
+    ms_serial_max = max_over_ranks(ms_serial, ws)
+    # headline: the pipelined batch stream (p2p transport)
+    pipelined = args.ep_transport == "p2p" and args.schedule == "pipelined"
+    if pipelined:
+        ep.forward_batches([a1] * max(2, args.warmup), [a3] * max(2, args.warmup), None, T)
+        torch.cuda.synchronize()
+    l0 = ctx.kernel_launches() + (ops.ctx_b.kernel_launches() if pipelined else 0)
+    with ClockSampler(local) as clk:
+        if pipelined:
+            ms = timed_ep(lambda: ep.forward_batches([a1] * args.steps, [a3] * args.steps, None,
+                                                     T))
+        else:
+            ms = timed_ep(lambda: [ep.forward(a1, a3, None, T, chunks=chunks)
+                                   for _ in range(args.steps)])
+    launches = ctx.kernel_launches() + (ops.ctx_b.kernel_launches() if pipelined else 0) - l0
     ms_max = max_over_ranks(ms, ws)
     value = T * ws / (ms_max / 1e3)
     # e2e: H2D of the step's inputs, layer, D2H of its output
@@ -595,6 +612,11 @@ def run_b200_ep(args):
                                    if args.ep_transport == "p2p" else
                                    f"ep{ws} (NCCL all_to_all dispatch/return, {chunks}-chunk "
                                    "software pipeline)"),
+                   "schedule": ("pipelined batches (EPLayer.forward_batches): routing + "
+                                "dispatch of batch i+1 on one stream/context beside the expert "
+                                "GEMMs + return + combine of batch i on another")
+                   if pipelined else "serial",
+                   "serial_ms_per_batch": ms_serial_max,
                    "a2a_bytes_each_way_rank0": ep.last_stats["a2a_bytes_each_way"],
                    "mean_ffn_per_token": float(ffn.size) / T},
         "e2e": {"value": T * ws / (e2e_ms / 1e3), "unit": "tokens/s",

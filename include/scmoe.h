@@ -75,6 +75,10 @@ int scmoe_synchronize(scmoe_ctx* ctx);
  * collectives (e.g. the dense branch under the EP all-to-all) leaves SMs
  * free for the communication kernels this way. */
 int scmoe_ctx_set_sm_budget(scmoe_ctx* ctx, int router_sms, int gemm_sms);
+/* Schedule hint for callers that pipeline batches themselves (e.g. expert
+ * parallelism): on = this context's router launches use the small kernel that
+ * co-resides with a grouped GEMM running on another stream. */
+int scmoe_ctx_set_overlapped(scmoe_ctx* ctx, int on);
 /* Number of kernels this context has launched (instrumentation). */
 uint64_t scmoe_kernel_launches(const scmoe_ctx* ctx);
 const char* scmoe_version(void);

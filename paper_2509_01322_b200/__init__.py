@@ -142,6 +142,7 @@ _PROTOS = {
     "scmoe_ep_put_rows": (C.c_int, [_P, _P, _SZ, _P, _P, _SZ, _P, _P, _P, _P, C.c_int]),
     "scmoe_moe_rows_to": (C.c_int, [_P, _P, _P, _P, C.c_int, _SZ, _P]),
     "scmoe_ctx_set_sm_budget": (C.c_int, [_P, C.c_int, C.c_int]),
+    "scmoe_ctx_set_overlapped": (C.c_int, [_P, C.c_int]),
     "scmoe_layer_forward_host_batches": (C.c_int, [_P, _P, _P, _SZ, _P, _P, _P, _SZ, C.c_int, _P,
                                                    _P, _P, _P]),
     "scmoe_bank_init_uniform_shard": (C.c_int, [_P, _P, _U64, _U64, C.c_double, _SZ]),
@@ -214,6 +215,11 @@ class Context:
 
     def kernel_launches(self) -> int:
         return int(lib().scmoe_kernel_launches(self._h))
+
+    def set_overlapped(self, on: bool = True):
+        """Router launches use the kernel that co-resides with a GEMM on another
+        stream (for callers that pipeline batches themselves)."""
+        self._check(lib().scmoe_ctx_set_overlapped(self._h, int(on)))
 
     def set_sm_budget(self, router_sms: int = 0, gemm_sms: int = 0):
         """Cap the CTAs of the persistent router / grouped GEMM (0 = all SMs)."""

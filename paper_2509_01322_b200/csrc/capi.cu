@@ -342,6 +342,13 @@ int scmoe_set_stream(scmoe_ctx* c, void* s) {
 }
 void* scmoe_get_stream(const scmoe_ctx* c) { return c ? (void*)c->stream : nullptr; }
 
+int scmoe_ctx_set_overlapped(scmoe_ctx* c, int on) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        c->overlapped = on != 0;
+    });
+}
+
 int scmoe_ctx_set_sm_budget(scmoe_ctx* c, int router_sms, int gemm_sms) {
     return guarded(c, [&] {
         require_ctx(c);

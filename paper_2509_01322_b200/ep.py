@@ -96,36 +96,48 @@ class GpuOps:
         return dd
 
     # -- peer-memory transport (NVLink; torch symmetric memory as the mapping) --
-    def p2p_buffers(self, group, cap_recv: int, cap_send: int):
-        """(Re)allocates the symmetric receive / receive-back buffers (collective:
-        every rank calls it with the same capacities) and returns the peer
-        address tables."""
+    def p2p_buffers(self, group, cap_recv: int, cap_send: int, nsets: int = 1):
+        """(Re)allocates `nsets` sets of symmetric receive / receive-back buffers
+        (collective: every rank calls it with the same capacities)."""
         import torch.distributed._symmetric_memory as symm_mem
         group = group if group is not None else dist.group.WORLD
         d = self.shape.d
-        self.p2p_cap = (cap_recv, cap_send)
-        self.recv = symm_mem.empty((cap_recv, d), dtype=torch.bfloat16, device="cuda")
-        self.recv_exp = symm_mem.empty(cap_recv, dtype=torch.int32, device="cuda")
-        self.back = symm_mem.empty((cap_send, d), dtype=torch.bfloat16, device="cuda")
-        self.h_recv = symm_mem.rendezvous(self.recv, group)
-        self.h_exp = symm_mem.rendezvous(self.recv_exp, group)
-        self.h_back = symm_mem.rendezvous(self.back, group)
         dev = lambda xs: torch.tensor(list(xs), dtype=torch.int64, device="cuda")  # noqa: E731
-        self.peer_recv = dev(self.h_recv.buffer_ptrs)
-        self.peer_exp = dev(self.h_exp.buffer_ptrs)
-        self.peer_back = dev(self.h_back.buffer_ptrs)
+        self.p2p_cap = (cap_recv, cap_send)
+        self.p2p_sets = []
+        for _ in range(nsets):
+            st = dict(recv=symm_mem.empty((cap_recv, d), dtype=torch.bfloat16, device="cuda"),
+                      recv_exp=symm_mem.empty(cap_recv, dtype=torch.int32, device="cuda"),
+                      back=symm_mem.empty((cap_send, d), dtype=torch.bfloat16, device="cuda"))
+            st["h_recv"] = symm_mem.rendezvous(st["recv"], group)
+            st["h_exp"] = symm_mem.rendezvous(st["recv_exp"], group)
+            st["h_back"] = symm_mem.rendezvous(st["back"], group)
+            st["peer_recv"] = dev(st["h_recv"].buffer_ptrs)
+            st["peer_exp"] = dev(st["h_exp"].buffer_ptrs)
+            st["peer_back"] = dev(st["h_back"].buffer_ptrs)
+            self.p2p_sets.append(st)
 
-    def put_rows(self, hb, send_token, send_expert, n_send, send_start, dst_offset):
+    def put_rows(self, st, hb, send_token, send_expert, n_send, send_start, dst_offset):
         self._chk(lib().scmoe_ep_put_rows(self.ctx.handle, hb.data_ptr(), self.shape.d,
                                           send_token.data_ptr(), send_expert.data_ptr(), n_send,
                                           send_start.data_ptr(), dst_offset.data_ptr(),
-                                          self.peer_recv.data_ptr(), self.peer_exp.data_ptr(),
+                                          st["peer_recv"].data_ptr(), st["peer_exp"].data_ptr(),
                                           self.world))
 
-    def experts_to(self, n_recv: int, row_dst: torch.Tensor):
-        self._chk(lib().scmoe_moe_rows_to(self.ctx.handle, self.bank, self.recv.data_ptr(),
-                                          self.recv_exp.data_ptr(), self.first, n_recv,
-                                          row_dst.data_ptr()))
+    def experts_to(self, st, n_recv: int, row_dst: torch.Tensor, ctx: Optional[Context] = None):
+        c = ctx or self.ctx
+        c._check(lib().scmoe_moe_rows_to(c.handle, self.bank, st["recv"].data_ptr(),
+                                         st["recv_exp"].data_ptr(), self.first, n_recv,
+                                         row_dst.data_ptr()))
+
+    def enable_back_context(self, device: int):
+        """A second context + stream for the back half (expert GEMMs, combine) of
+        the pipelined batch stream: its own workspace, so batch i's back half
+        and batch i+1's front half never share scratch buffers."""
+        if getattr(self, "ctx_b", None) is None:
+            self.ctx_b = Context(device)
+            self.stream_b = torch.cuda.Stream()
+            self.ctx_b.set_stream(self.stream_b.cuda_stream)
 
     def route(self, a1: torch.Tensor, gain: Optional[torch.Tensor], T: int):
         s = self.shape
@@ -165,10 +177,11 @@ class GpuOps:
                                        row_expert.data_ptr(), self.first, R, y.data_ptr()))
         return y
 
-    def combine(self, hmoe, y_rows, slot_pos, idx, gates, T, a3, renormalize=False):
+    def combine(self, hmoe, y_rows, slot_pos, idx, gates, T, a3, renormalize=False, ctx=None):
         s = self.shape
+        c = ctx or self.ctx
         out = torch.empty(T, s.d, dtype=torch.float32, device="cuda")
-        self._chk(lib().scmoe_combine_rows(self.ctx.handle, self.bank, hmoe.data_ptr(),
+        c._check(lib().scmoe_combine_rows(c.handle, self.bank, hmoe.data_ptr(),
                                            y_rows.data_ptr(), slot_pos.data_ptr(), idx.data_ptr(),
                                            gates.data_ptr(), T, s.top_k, s.n_ffn, int(renormalize),
                                            None if a3 is None else a3.data_ptr(), out.data_ptr()))
@@ -280,8 +293,9 @@ class EPLayer:
         return self.ops.combine(st["hmoe"], st["back"], st["slot_pos"], st["idx"], st["gates"],
                                 st["T"], a3c, renormalize)
 
-    def _forward_p2p(self, a1, a3, gain, T, renormalize, wait_residual=None):
-        """One chunk, peer-memory transport (see __init__)."""
+    def _front_p2p(self, a1, gain, T, nsets=1, k=0):
+        """Route, plan, counts all-gather (host sync) and the dispatch into the
+        owners' receive buffers of set k, then a cross-rank barrier."""
         ops, G, me = self.ops, self.world, self.rank
         hmoe, hb, idx, gates, cnt = ops.route(a1, gain, T)
         counts, slot_pos, send_token, send_expert = ops.plan(idx, T)
@@ -294,8 +308,12 @@ class EPLayer:
         need_r = max(sum(Mh[s][d] for s in range(G)) for d in range(G))
         need_s = max(sum(r) for r in Mh)
         cap = getattr(ops, "p2p_cap", (0, 0))
-        if need_r > cap[0] or need_s > cap[1]:  # same decision on every rank
-            ops.p2p_buffers(self.group, max(1, int(need_r * 1.25)), max(1, int(need_s * 1.25)))
+        if (need_r > cap[0] or need_s > cap[1]
+                or len(getattr(ops, "p2p_sets", [])) < nsets):  # same decision on every rank
+            torch.cuda.synchronize()  # no set may be in use while it is replaced
+            ops.p2p_buffers(self.group, max(1, int(max(need_r, cap[0]) * 1.25)),
+                            max(1, int(max(need_s, cap[1]) * 1.25)), nsets=max(nsets, 1))
+        st = ops.p2p_sets[k]
         send_start = [0]
         for d in range(G):
             send_start.append(send_start[-1] + Mh[me][d])
@@ -303,8 +321,8 @@ class EPLayer:
         recv_offset = [0]
         for s in range(G):
             recv_offset.append(recv_offset[-1] + Mh[s][me])
-        # received row r (from source s, its j-th row for me) returns to source s's
-        # back buffer at row (sum_{d<me} M[s][d]) + j
+        # received row r (source s's j-th row for me) returns to source s's back
+        # buffer at row (sum_{d<me} M[s][d]) + j
         back_start = [sum(Mh[s][:me]) for s in range(G)]
         dev = counts.device
         rows_per_src = torch.tensor([Mh[s][me] for s in range(G)], dtype=torch.int64, device=dev)
@@ -312,25 +330,95 @@ class EPLayer:
         j = torch.arange(n_recv, dtype=torch.int64, device=dev) - \
             torch.tensor(recv_offset[:G], dtype=torch.int64, device=dev)[src]
         # comm=False (timing reference): no dispatch, GEMM2 rows stay local
-        back_ptr = ops.peer_back if self.comm else \
-            torch.full_like(ops.peer_back, ops.back.data_ptr())
+        back_ptr = st["peer_back"] if self.comm else \
+            torch.full_like(st["peer_back"], st["back"].data_ptr())
         row_dst = back_ptr[src] + (torch.tensor(back_start, dtype=torch.int64, device=dev)[src]
                                    + j) * (ops.shape.d * 2)
         if self.comm:
-            ops.put_rows(hb, send_token, send_expert, n_send,
+            ops.put_rows(st, hb, send_token, send_expert, n_send,
                          torch.tensor(send_start, dtype=torch.int32, device=dev),
                          torch.tensor(dst_offset, dtype=torch.int64, device=dev))
         else:
-            ops.recv_exp[:n_recv].fill_(ops.first)
-        ops.h_recv.barrier(channel=0)
-        ops.experts_to(n_recv, row_dst)
-        ops.h_back.barrier(channel=1)
+            st["recv_exp"][:n_recv].fill_(ops.first)
+        st["h_recv"].barrier(channel=0)
+        return dict(k=k, T=T, hmoe=hmoe, idx=idx, gates=gates, cnt=cnt, slot_pos=slot_pos,
+                    n_send=n_send, n_recv=n_recv, row_dst=row_dst, keep=[hb, send_token,
+                                                                        send_expert])
+
+    def _back_p2p(self, f, a3, renormalize, wait_residual=None, ctx=None):
+        """Expert GEMMs on the received rows (GEMM2 rows land in the sources'
+        back buffers), barrier, rank-order combine."""
+        ops = self.ops
+        st = ops.p2p_sets[f["k"]]
+        ops.experts_to(st, f["n_recv"], f["row_dst"], ctx=ctx)
+        st["h_back"].barrier(channel=1)
         if wait_residual is not None:
             torch.cuda.current_stream().wait_stream(wait_residual)
-        out = ops.combine(hmoe, ops.back, slot_pos, idx, gates, T, a3, renormalize)
-        self.last_stats = {"send_rows": n_send, "recv_rows": n_recv, "chunks": 1,
-                           "transport": "p2p", "a2a_bytes_each_way": n_send * ops.shape.d * 2}
-        return out, idx, gates, cnt
+        return ops.combine(f["hmoe"], st["back"], f["slot_pos"], f["idx"], f["gates"], f["T"], a3,
+                           renormalize, ctx=ctx)
+
+    def _forward_p2p(self, a1, a3, gain, T, renormalize, wait_residual=None):
+        """One chunk, peer-memory transport (see __init__)."""
+        f = self._front_p2p(a1, gain, T)
+        out = self._back_p2p(f, a3, renormalize, wait_residual)
+        self.last_stats = {"send_rows": f["n_send"], "recv_rows": f["n_recv"], "chunks": 1,
+                           "transport": "p2p",
+                           "a2a_bytes_each_way": f["n_send"] * self.ops.shape.d * 2}
+        return out, f["idx"], f["gates"], f["cnt"]
+
+    def forward_batches(self, a1s, a3s, gain, T: int, renormalize: bool = False,
+                        corun_router: bool = False):
+        """A stream of batches, pipelined (p2p transport): batch i+1's front half
+        (routing, planning, dispatch over NVLink) runs on the front stream while batch i's
+        expert GEMMs + return + combine run on the back stream / context.  Two
+        sets of symmetric buffers alternate.  Results equal len(a1s) forward()
+        calls bit for bit.  corun_router selects the small router kernel that
+        co-resides with the GEMM (faster at N=1's HBM-bound GEMMs; at EP shapes
+        the GEMMs lean on the tensor pipe and the full-size router, which
+        time-shares the SMs instead, measured faster)."""
+        if self.transport != "p2p":
+            raise ValueError("forward_batches needs the p2p transport")
+        ops = self.ops
+        dev = torch.cuda.current_device()
+        ops.enable_back_context(dev)
+        F, B = ops.stream, ops.stream_b
+        caller = torch.cuda.current_stream()
+        F.wait_stream(caller)
+        B.wait_stream(caller)
+        ops.ctx.set_overlapped(corun_router)
+        n = len(a1s)
+        fronts, outs = [None] * n, [None] * n
+        ev_front = [torch.cuda.Event() for _ in range(n)]
+        ev_back = [torch.cuda.Event() for _ in range(n)]
+        try:
+            for i in range(n + 1):
+                if i >= 1:  # back(i-1) first, so the GPU has it before the host blocks
+                    with torch.cuda.stream(B):
+                        B.wait_event(ev_front[i - 1])
+                        outs[i - 1] = self._back_p2p(fronts[i - 1],
+                                                     None if a3s is None else a3s[i - 1],
+                                                     renormalize, ctx=ops.ctx_b)
+                        ev_back[i - 1].record(B)
+                if i < n:
+                    with torch.cuda.stream(F):
+                        if i >= 2:  # set i % 2 was last used by batch i-2
+                            F.wait_event(ev_back[i - 2])
+                        fronts[i] = self._front_p2p(a1s[i], gain, T, nsets=2, k=i % 2)
+                        ev_front[i].record(F)
+        finally:
+            ops.ctx.set_overlapped(False)
+        caller.wait_stream(B)
+        caller.wait_stream(F)
+        res = []
+        for i in range(n):
+            for t in (outs[i], fronts[i]["idx"], fronts[i]["gates"], fronts[i]["cnt"]):
+                t.record_stream(caller)
+            res.append((outs[i], fronts[i]["idx"], fronts[i]["gates"], fronts[i]["cnt"]))
+        f = fronts[-1]
+        self.last_stats = {"send_rows": f["n_send"], "recv_rows": f["n_recv"], "chunks": 1,
+                           "transport": "p2p", "pipelined": True,
+                           "a2a_bytes_each_way": f["n_send"] * ops.shape.d * 2}
+        return res
 
     def _forward(self, a1, a3, gain, T, renormalize, chunks, wait_residual=None):
         self.d = self.ops.shape.d if hasattr(self.ops, "shape") else a1.numel() // T

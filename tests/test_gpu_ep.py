@@ -89,3 +89,61 @@ def test_ep_equals_single_gpu_bitwise(world, chunks, dense, transport):
         p.join(timeout=60)
     for rank, ok, info in sorted(res):
         assert ok, f"rank {rank}: {info}"
+
+
+def _batches_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", rank))
+    try:
+        import paper_2509_01322_b200 as P
+        from paper_2509_01322_b200.ep import EPLayer, GpuOps
+        from paper_2509_01322_b200.layer import LayerShape
+        shape = LayerShape(d=1024, n_ffn=64, n_zero=32, top_k=6, k_expected=4, inter=512,
+                           precision=P.PREC_BF16)
+        T, nb = 704 + 32 * rank, 4
+        a1 = [torch.from_numpy(P.fill_normal(P.stream_seed(40 + i, rank), T * shape.d)).cuda()
+              for i in range(nb)]
+        a3 = [torch.from_numpy(P.fill_normal(P.stream_seed(50 + i, rank), T * shape.d)).cuda()
+              for i in range(nb)]
+        ep = EPLayer(GpuOps(P.Context(rank), shape, rank, world, seed=3), transport="p2p")
+        ser = [ep.forward(a1[i], a3[i], None, T) for i in range(nb)]
+        torch.cuda.synchronize()
+        pip = ep.forward_batches(a1, a3, None, T)
+        pip2 = ep.forward_batches(a1[:2], None, None, T)  # again, and without residual
+        torch.cuda.synchronize()
+        ok = all(torch.equal(u, v) for s, p in zip(ser, pip) for u, v in zip(s, p))
+        ref2 = [ep.forward(a1[i], None, None, T)[0] for i in range(2)]
+        torch.cuda.synchronize()
+        ok = ok and all(torch.equal(r, p[0]) for r, p in zip(ref2, pip2))
+        q.put((rank, bool(ok), ep.last_stats))
+    except Exception:  # pragma: no cover
+        import traceback
+        q.put((rank, False, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_ep_pipelined_batches_equal_serial(world):
+    """EPLayer.forward_batches (front of batch i+1 beside the back of batch i,
+    co-resident router, two symmetric buffer sets) == serial forward() calls."""
+    import torch
+    import torch.multiprocessing as mp
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs >= {world} GPUs")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29950 + world + os.getpid() % 40
+    procs = [ctx.Process(target=_batches_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, info in sorted(res):
+        assert ok, f"rank {rank}: {info}"

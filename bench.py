@@ -386,10 +386,48 @@ def run_b200(args):
     h2d = 2 * T * D * 4
     d2h = T * D * 4 + T * TOPK * (4 + 8) + T * 4
 
+    # ---- SURVEY config C (decode: 256 tokens per step, HBM-bound weight
+    # streaming) on the same layer, serial steps; reported beside the headline
+    config_c = None
+    if args.decode_tokens > 0:
+        Tc = args.decode_tokens
+        dsets = dict(idx=torch.empty(Tc * TOPK, dtype=torch.int32, device="cuda"),
+                     gates=torch.empty(Tc * TOPK, dtype=torch.float64, device="cuda"),
+                     cnt=torch.empty(Tc, dtype=torch.int32, device="cuda"),
+                     out=torch.empty(Tc, D, dtype=torch.float32, device="cuda"))
+
+        def dstep(n):
+            for i in range(n):  # consecutive 256-token windows of the prefill input
+                off = (i % (T // Tc)) * Tc * D * 4
+                layer.forward(a1.data_ptr() + off, a3.data_ptr() + off, None, Tc,
+                              dsets["idx"].data_ptr(), dsets["gates"].data_ptr(),
+                              dsets["cnt"].data_ptr(), dsets["out"].data_ptr())
+        with torch.cuda.stream(stream):
+            dstep(3)
+        ctx.synchronize()
+        ctx.profile(True)
+        ctx.profile_flush()
+        ms_c = max_over_ranks(timed(dstep, args.steps), ws)
+        st_c = ctx.profile_flush()
+        ctx.profile(False)
+        idx_c = dsets["idx"].cpu().numpy().view(np.uint32)
+        c1, c2, Sc, hit_c, _ = gemm_algorithmic_bytes(idx_c, Tc)
+        tg = (st_c["gemm1_tcgen05"][0] + st_c["gemm2_tcgen05"][0]) / st_c["gemm1_tcgen05"][1]
+        config_c = {"workload": "SURVEY config C: LongCat MoE layer decode step, 256 tokens, "
+                                "1xB200 (expert weights streamed from HBM)",
+                    "tokens": Tc, "ms_per_step": ms_c, "tokens_per_s": Tc * ws / (ms_c / 1e3),
+                    "ffn_slots": Sc, "experts_hit": hit_c,
+                    "gemm_ms_per_step": tg, "gemm_bytes_per_step": c1 + c2,
+                    "gemm_achieved_gbs": (c1 + c2) / (tg / 1e3) / 1e9,
+                    "stages_ms": {k: round(v[0] / v[1], 4) for k, v in st_c.items()}}
+
     if rank != 0:
         return
     peaks = measured_peaks()
     hbm_peak = peaks["hbm_gbs"] if peaks else 6650.0
+    if config_c:
+        config_c["gemm_frac_of_measured_hbm"] = config_c["gemm_achieved_gbs"] / hbm_peak
+        config_c["gemm_frac_of_8tbs_nominal"] = config_c["gemm_achieved_gbs"] / 8000.0
 
     def gemm_roofline(st):
         g1 = st.get("gemm1_tcgen05", (0.0, 1))
@@ -450,6 +488,7 @@ def run_b200(args):
         "stages_ms_serial": {k: round(v[0] / v[1], 4) for k, v in stages_serial.items()},
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
+        "config_c": config_c,
     }
     emit(line)
 
@@ -646,6 +685,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     # N>1: SURVEY config D extra (dense shortcut FFN overlapping the all-to-alls)
     ap.add_argument("--dense-inter", type=int, default=12288)
+    # N=1: SURVEY config C extra (decode step of this many tokens; 0 = off)
+    ap.add_argument("--decode-tokens", type=int, default=256)
     ap.add_argument("--config-d-tokens", type=int, default=32768)
     # pipelined = scmoe_layer_forward_batches; measured slower than serial on B200 in round 1
     # (router and GEMM contend for shared-memory bandwidth), so serial is the default

@@ -10,7 +10,7 @@
 //   RouterState<S>, RoutingDecision router.hpp:20-87
 //   select_topk_row                 router.hpp:90-104
 //   route_from_probs                router.hpp:107-130
-//   route_topk                      router.hpp:133-141       (S = float)
+//   route_topk                      router.hpp:133-141       (S = float, double)
 //   accumulate_counters             router.hpp:144-150
 //   bias_update                     router.hpp:155-176
 //   simulate_bias_control           router.hpp:349-369       (S = float)
@@ -358,11 +358,11 @@ RoutingDecision route_from_probs(const Tensor<S>& probs, const RouterState<S>& s
     return dd;
 }
 
-// router.hpp:133-141 (fp32 routing projection; bit-exact with the reference)
+// router.hpp:133-141 (S = float: the fp32 hot path; S = double: the projection
+// in double and the glibc exp(double) restatement; both bit-exact)
 template <typename S>
 RoutingDecision route_topk(const Tensor<S>& x, const RouterState<S>& state,
                            Tensor<S>* probs_out = nullptr) {
-    static_assert(std::is_same_v<S, float>, "route_topk on the B200 path is fp32 (S = float)");
     check(x.ndim() == 2 && state.w.ndim() == 2, "matmul: operands must be 2-d");
     if (x.cols() != state.w.rows()) throw DimensionError("matmul: inner dims disagree");
     state.validate();
@@ -375,10 +375,15 @@ RoutingDecision route_topk(const Tensor<S>& x, const RouterState<S>& state,
     dd.ffn_count.resize(T);
     auto& d = b200::device();
     scmoe_router* r = b200::router_of(state);
-    Tensor<float> probs;
-    if (probs_out) probs = Tensor<float>({T, E});
-    d.ok(scmoe_route_topk_host(d.ctx, r, x.data.data(), T, dd.indices.data(), dd.gates.data(),
-                               dd.ffn_count.data(), probs_out ? probs.data.data() : nullptr));
+    Tensor<S> probs;
+    if (probs_out) probs = Tensor<S>({T, E});
+    if constexpr (std::is_same_v<S, double>)
+        d.ok(scmoe_route_topk_f64_host(d.ctx, r, x.data.data(), T, state.w.data.data(),
+                                       dd.indices.data(), dd.gates.data(), dd.ffn_count.data(),
+                                       probs_out ? probs.data.data() : nullptr));
+    else
+        d.ok(scmoe_route_topk_host(d.ctx, r, x.data.data(), T, dd.indices.data(), dd.gates.data(),
+                                   dd.ffn_count.data(), probs_out ? probs.data.data() : nullptr));
     if (probs_out) *probs_out = std::move(probs);
     return dd;
 }

@@ -148,6 +148,19 @@ int scmoe_routing_stats_host(scmoe_ctx* ctx, const uint32_t* indices, const uint
                              size_t tokens, size_t top_k, size_t n_ffn, size_t n_zero,
                              size_t k_expected, size_t lb_groups, double* mean_ffn,
                              double* std_ffn, double* per_expert_load, double* lb_freq);
+/* route_topk for RouterState<double> (router.hpp:133-141 with S = double):
+ * the projection in double (sequential DMUL/DADD per output), softmax with
+ * the glibc exp(double) restatement, same selection.  The router supplies the
+ * configuration and bias; its weights in double are passed as w [d, E].
+ * Bit-exact with the reference (not on the fp32 hot path). */
+int scmoe_route_topk_f64(scmoe_ctx* ctx, scmoe_router* r, const double* x, size_t tokens,
+                         const double* w, uint32_t* indices, double* gates, uint32_t* ffn_count,
+                         double* probs /* nullable */);
+int scmoe_route_topk_f64_host(scmoe_ctx* ctx, scmoe_router* r, const double* x, size_t tokens,
+                              const double* w, uint32_t* indices, double* gates,
+                              uint32_t* ffn_count, double* probs);
+/* Device glibc exp(double) restatement on n inputs (verification hook). */
+int scmoe_debug_exp(scmoe_ctx* ctx, const double* in_dev, double* out_dev, size_t n);
 /* accumulate_counters (router.hpp:144-150): slot-counted, zero experts included. */
 int scmoe_accumulate_counters(scmoe_ctx* ctx, scmoe_router* r, const uint32_t* indices,
                               size_t tokens);

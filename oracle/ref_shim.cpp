@@ -144,6 +144,21 @@ int ref_route_topk_f32(const float* x, std::size_t T, std::size_t d, const float
     });
 }
 
+// route_topk with S = double (RouterState<double>): libm exp in the softmax
+int ref_route_topk_f64(const double* x, std::size_t T, std::size_t d, const double* w,
+                       std::size_t n, std::size_t z, std::size_t k, std::size_t ke, double mu,
+                       const double* b, uint32_t* idx, double* gates, uint32_t* cnt,
+                       double* probs_out, int threads) {
+    return guarded([&] { make_state(w, d, n, z, k, ke, mu, 1.0, b); }) ?: sharded(T, threads, [&](std::size_t t0, std::size_t t1) {
+        RouterState<double> st = make_state(w, d, n, z, k, ke, mu, 1.0, b);
+        Tensor<double> probs;
+        auto dd = route_topk(wrap(x + t0 * d, t1 - t0, d), st, probs_out ? &probs : nullptr);
+        export_decision(dd, idx + t0 * k, gates + t0 * k, cnt + t0);
+        if (probs_out)
+            std::memcpy(probs_out + t0 * (n + z), probs.data.data(), probs.data.size() * sizeof(double));
+    });
+}
+
 #define REF_ROUTE_FROM_PROBS(S, SUF)                                                               \
     int ref_route_from_probs_##SUF(const S* probs, std::size_t T, std::size_t n, std::size_t z,    \
                                    std::size_t k, std::size_t ke, double mu, const double* b,      \

@@ -117,6 +117,9 @@ _PROTOS = {
     "scmoe_route_from_probs_f32_host": (C.c_int, [_P, _P, _P, _SZ, _P, _P, _P]),
     "scmoe_route_from_probs_f64_host": (C.c_int, [_P, _P, _P, _SZ, _P, _P, _P]),
     "scmoe_accumulate_counters": (C.c_int, [_P, _P, _P, _SZ]),
+    "scmoe_route_topk_f64": (C.c_int, [_P, _P, _P, _SZ, _P, _P, _P, _P, _P]),
+    "scmoe_route_topk_f64_host": (C.c_int, [_P, _P, _P, _SZ, _P, _P, _P, _P, _P]),
+    "scmoe_debug_exp": (C.c_int, [_P, _P, _P, _SZ]),
     "scmoe_routing_stats": (C.c_int, [_P, _P, _P, _SZ, _SZ, _SZ, _SZ, _SZ, _SZ, _P, _P, _P, _P]),
     "scmoe_routing_stats_host": (C.c_int, [_P, _P, _P, _SZ, _SZ, _SZ, _SZ, _SZ, _SZ, _P, _P, _P,
                                            _P]),
@@ -275,7 +278,9 @@ class RouterState:
 
     def __init__(self, w: Optional[np.ndarray], n_ffn: int, n_zero: int, top_k: int,
                  k_expected: int, mu: float, mu_decay: float):
-        self.w = None if w is None else np.ascontiguousarray(w, dtype=np.float32)
+        # S = float (the hot path) or S = double (RouterState<double>): kept as given
+        dt = np.float64 if (w is not None and np.asarray(w).dtype == np.float64) else np.float32
+        self.w = None if w is None else np.ascontiguousarray(w, dtype=dt)
         self.n_ffn, self.n_zero, self.top_k, self.k_expected = n_ffn, n_zero, top_k, k_expected
         self.mu, self.mu_decay = float(mu), float(mu_decay)
         self.b = np.zeros(n_ffn + n_zero, dtype=np.float64)
@@ -320,7 +325,8 @@ class RouterState:
         if self.w is not None and (self._dev_key is None or self._dev_key != wkey):
             if self.w.shape != (d, E):
                 raise DimensionError("route: router weights must be [d_model, N+Z]")
-            ctx._check(L.scmoe_router_set_weights_host(ctx.handle, h, _ptr(self.w)))
+            w32 = np.ascontiguousarray(self.w, dtype=np.float32)
+            ctx._check(L.scmoe_router_set_weights_host(ctx.handle, h, _ptr(w32)))
             self._dev_key = wkey
         b = np.ascontiguousarray(self.b, dtype=np.float64)
         ctx._check(L.scmoe_router_set_bias_host(ctx.handle, h, _ptr(b)))
@@ -382,11 +388,13 @@ def _as2d(a, dtype):
 
 def route_topk(x: np.ndarray, state: RouterState, probs_out: Optional[list] = None,
                ctx: Optional[Context] = None) -> RoutingDecision:
-    """router.hpp:133-141.  x [T, d] fp32.  If ``probs_out`` is a list, the
-    probabilities [T, N+Z] are appended to it (the reference's Tensor* out)."""
+    """router.hpp:133-141.  x [T, d] fp32 (or fp64 with a float64 RouterState:
+    RouterState<double>).  If ``probs_out`` is a list, the probabilities
+    [T, N+Z] are appended to it (the reference's Tensor* out)."""
     ctx = ctx or default_context()
     state.validate()
-    x = _as2d(x, np.float32)
+    f64 = state.w is not None and state.w.dtype == np.float64
+    x = _as2d(x, np.float64 if f64 else np.float32)
     if state.w is None:
         raise DimensionError("matmul: operands must be 2-d")
     if x.shape[1] != state.w.shape[0]:
@@ -396,9 +404,14 @@ def route_topk(x: np.ndarray, state: RouterState, probs_out: Optional[list] = No
     idx = np.empty(T * K, np.uint32)
     gates = np.empty(T * K, np.float64)
     cnt = np.empty(T, np.uint32)
-    probs = np.empty((T, E), np.float32) if probs_out is not None else None
-    ctx._check(lib().scmoe_route_topk_host(ctx.handle, h, _ptr(x), T, _ptr(idx), _ptr(gates),
-                                           _ptr(cnt), _ptr(probs)))
+    probs = np.empty((T, E), np.float64 if f64 else np.float32) if probs_out is not None else None
+    if f64:
+        ctx._check(lib().scmoe_route_topk_f64_host(ctx.handle, h, _ptr(x), T, _ptr(state.w),
+                                                   _ptr(idx), _ptr(gates), _ptr(cnt),
+                                                   _ptr(probs)))
+    else:
+        ctx._check(lib().scmoe_route_topk_host(ctx.handle, h, _ptr(x), T, _ptr(idx), _ptr(gates),
+                                               _ptr(cnt), _ptr(probs)))
     if probs_out is not None:
         probs_out.append(probs)
     return RoutingDecision(K, state.n_ffn, idx, gates, cnt)

@@ -64,6 +64,7 @@ def check_sass(lib: str = LIB) -> dict:
         body = f
         summary[name] = {
             "FFMA": len(re.findall(r"\bFFMA2?\b", body)),
+            "DFMA": len(re.findall(r"\bDFMA\b", body)),
             "UTCHMMA": len(re.findall(r"UTC\w*MMA", body)),
             "UTMALDG": len(re.findall(r"UTMALDG", body)),
             "LDTM": len(re.findall(r"\bLDTM", body)),
@@ -76,6 +77,10 @@ def check_sass(lib: str = LIB) -> dict:
     assert seq, "seq_gemm kernel missing from SASS"
     for n in seq:
         assert summary[n]["FFMA"] == 0, f"{n}: FFMA found in exact-order kernel"
+    # the double-precision router projection: separately rounded DMUL + DADD
+    for n in summary:
+        if "router_f64_kernel" in n:
+            assert summary[n]["DFMA"] == 0, f"{n}: DFMA found in exact-order kernel"
     gemm = [n for n in summary if "grouped_gemm_kernel" in n]
     assert gemm and all(summary[n]["UTCHMMA"] > 0 and summary[n]["UTMALDG"] > 0 for n in gemm), \
         "grouped GEMM lacks UTCHMMA/UTMALDG"

@@ -613,6 +613,55 @@ int scmoe_routing_stats_host(scmoe_ctx* c, const uint32_t* idx, const uint32_t* 
     });
 }
 
+int scmoe_route_topk_f64(scmoe_ctx* c, scmoe_router* r, const double* x, size_t T,
+                         const double* w, uint32_t* idx, double* gates, uint32_t* ffn_count,
+                         double* probs) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        validate_router(r->n_ffn, r->n_zero, r->top_k, r->k_expected, r->mu);
+        if (T == 0) return;
+        const size_t E = r->E();
+        double* logits = c->ws.logits.get<double>(T * E);
+        {
+            ProfScope _p(c, "router_gemm_f64");
+            launch_router_f64(c, x, w, logits, T, r->d, E);
+        }
+        ProfScope _p(c, "softmax_topk_f64");
+        launch_softmax_topk_f64(c, logits, T, E, r->top_k, r->n_ffn, r->b, idx, gates, ffn_count,
+                                probs);
+    });
+}
+
+int scmoe_route_topk_f64_host(scmoe_ctx* c, scmoe_router* r, const double* x, size_t T,
+                              const double* w, uint32_t* idx, double* gates, uint32_t* ffn_count,
+                              double* probs) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        Stage& s = stage_of(c);
+        const size_t K = r->top_k, E = r->E();
+        const double* xd = upload(c, s.bufs[0], x, T * r->d);
+        const double* wd = upload(c, s.bufs[7], w, r->d * E);
+        uint32_t* di = s.bufs[1].get<uint32_t>(T * K);
+        double* dg = s.bufs[2].get<double>(T * K);
+        uint32_t* dc = s.bufs[3].get<uint32_t>(T);
+        double* dp = probs ? s.bufs[4].get<double>(T * E) : nullptr;
+        int rc = scmoe_route_topk_f64(c, r, xd, T, wd, di, dg, dc, dp);
+        if (rc) throw ScmoeError{rc, c->last_error};
+        download(c, idx, di, T * K);
+        download(c, gates, dg, T * K);
+        download(c, ffn_count, dc, T);
+        if (probs) download(c, probs, dp, T * E);
+        sync_and_check(c);
+    });
+}
+
+int scmoe_debug_exp(scmoe_ctx* c, const double* in, double* out, size_t n) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        launch_debug_exp(c, in, out, n);
+    });
+}
+
 int scmoe_accumulate_counters(scmoe_ctx* c, scmoe_router* r, const uint32_t* idx, size_t T) {
     return guarded(c, [&] {
         require_ctx(c);

@@ -210,6 +210,13 @@ void launch_seq_gemm(scmoe_ctx* c, const float* A, size_t lda, const int* a_rows
 int seq_gemm_tile_rows(size_t rows, size_t N, int num_sms);
 // Router projection with one CTA per 56-token slab x all experts (E <= 768).
 // Same tile as the slab kernel, operands by TMA into an mbarrier ring.
+// RouterState<double>: projection and softmax/top-K in double.
+void launch_router_f64(scmoe_ctx* c, const double* X, const double* W, double* logits, size_t T,
+                       size_t K, size_t E);
+void launch_softmax_topk_f64(scmoe_ctx* c, const double* logits, size_t T, size_t E, size_t K,
+                             size_t n_ffn, const double* bias, uint32_t* idx, double* gates,
+                             uint32_t* ffn, double* probs);
+void launch_debug_exp(scmoe_ctx* c, const double* in, double* out, size_t n);
 bool router_tma_ok(size_t T, size_t K, size_t E, int num_sms);
 void launch_router_tma(scmoe_ctx* c, const float* X, const float* W, float* logits, size_t T,
                        size_t K, size_t E);

@@ -8,6 +8,8 @@
 // on the SASS that the sequential GEMM's inner loop has no FFMA.
 #include <float.h>
 
+#include <type_traits>
+
 #include "internal.cuh"
 #include "f32x2.cuh"
 #include "libm_port.h"
@@ -657,7 +659,32 @@ __global__ void __launch_bounds__(256) softmax_topk_kernel(
     unsigned char* taken = taken_all + (size_t)warp * E;
     const S* row = in + (size_t)t * E;
 
-    if constexpr (kFromLogits) {
+    if constexpr (kFromLogits && std::is_same<S, double>::value) {
+        // softmax_rows in S = double (tensor.hpp:174-192): glibc exp port
+        double mx = -DBL_MAX;
+        bool first = true;
+        for (int j = lane; j < E; j += 32) {
+            const double v = row[j];
+            mx = first ? v : (v > mx ? v : mx);
+            first = false;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double other = __shfl_xor_sync(0xffffffffu, mx, o);
+            mx = other > mx ? other : mx;
+        }
+        for (int j = lane; j < E; j += 32) p[j] = scmoe_exp(__dsub_rn(row[j], mx));
+        __syncwarp();
+        double sum = 0.0;
+        if (lane == 0)
+            for (int j = 0; j < E; ++j) sum = __dadd_rn(sum, p[j]);
+        sum = __shfl_sync(0xffffffffu, sum, 0);
+        for (int j = lane; j < E; j += 32) {
+            const double q = __ddiv_rn(p[j], sum);
+            p[j] = q;
+            if (probs_out) probs_out[(size_t)t * E + j] = q;
+        }
+    } else if constexpr (kFromLogits) {
         float mx = -FLT_MAX;
         bool first = true;
         for (int j = lane; j < E; j += 32) {
@@ -752,6 +779,73 @@ void launch_topk_from_probs_f64(scmoe_ctx* c, const double* probs, size_t T, siz
                                 uint32_t* ffn_count) {
     launch_topk_impl<double, false>(c, probs, T, E, K, n_ffn, bias, idx, gates, ffn_count,
                                     (double*)nullptr);
+}
+
+// ---------------------------------------------------------------------------
+// Router projection in S = double (RouterState<double>, router.hpp:136 ->
+// tensor.hpp:95-112 in double): per output c = 0; c = c + x*w (separately
+// rounded DMUL / DADD) in k order.  64 x 64 CTA tile, 4 x 4 chains per
+// thread, K staged 16 rows at a time.  Not on the fp32 hot path.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) router_f64_kernel(const double* __restrict__ X,
+                                                         const double* __restrict__ W,
+                                                         double* __restrict__ out, int T, int K,
+                                                         int E) {
+    __shared__ double xs[16][64 + 1];
+    __shared__ double wsm[16][64];
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    const int row0 = blockIdx.y * 64, col0 = blockIdx.x * 64;
+    double acc[4][4] = {};
+    for (int k0 = 0; k0 < K; k0 += 16) {
+        for (int i = threadIdx.x; i < 16 * 64; i += 256) {
+            const int kk = i / 64, c = i % 64;
+            const int r = row0 + c, k = k0 + kk, e = col0 + c;
+            xs[kk][c] = (r < T && k < K) ? X[(size_t)r * K + k] : 0.0;
+            wsm[kk][c] = (e < E && k < K) ? W[(size_t)k * E + e] : 0.0;
+        }
+        __syncthreads();
+        const int kn = min(16, K - k0);
+        for (int kk = 0; kk < kn; ++kk) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const double a = xs[kk][ty * 4 + i];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(a, wsm[kk][tx * 4 + j]));
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int r = row0 + ty * 4 + i, e = col0 + tx * 4 + j;
+            if (r < T && e < E) out[(size_t)r * E + e] = acc[i][j];
+        }
+}
+void launch_router_f64(scmoe_ctx* c, const double* X, const double* W, double* logits, size_t T,
+                       size_t K, size_t E) {
+    if (T == 0) return;
+    const dim3 grid((unsigned)ceil_div(E, 64), (unsigned)ceil_div(T, 64));
+    router_f64_kernel<<<grid, 256, 0, c->stream>>>(X, W, logits, (int)T, (int)K, (int)E);
+    SCMOE_LAUNCH_CHECK(c);
+}
+void launch_softmax_topk_f64(scmoe_ctx* c, const double* logits, size_t T, size_t E, size_t K,
+                             size_t n_ffn, const double* bias, uint32_t* idx, double* gates,
+                             uint32_t* ffn, double* probs) {
+    launch_topk_impl<double, true>(c, logits, T, E, K, n_ffn, bias, idx, gates, ffn, probs);
+}
+__global__ void debug_exp_kernel(const double* __restrict__ in, double* __restrict__ out,
+                                 size_t n) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x)
+        out[i] = scmoe_exp(in[i]);
+}
+void launch_debug_exp(scmoe_ctx* c, const double* in, double* out, size_t n) {
+    if (n == 0) return;
+    debug_exp_kernel<<<c->num_sms * 8, 256, 0, c->stream>>>(in, out, n);
+    SCMOE_LAUNCH_CHECK(c);
 }
 
 __global__ void debug_expf_kernel(const float* __restrict__ in, float* __restrict__ out, size_t n) {

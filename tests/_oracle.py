@@ -94,6 +94,8 @@ _REF_PROTOS = {
     "ref_expf": (C.c_float, [C.c_float]),
     "ref_route_topk_f32": (C.c_int, [_P, _SZ, _SZ, _P, _SZ, _SZ, _SZ, _SZ, _D, _P, _P, _P, _P, _P,
                                      C.c_int]),
+    "ref_route_topk_f64": (C.c_int, [_P, _SZ, _SZ, _P, _SZ, _SZ, _SZ, _SZ, _D, _P, _P, _P, _P, _P,
+                                     C.c_int]),
     "ref_route_from_probs_f32": (C.c_int, [_P, _SZ, _SZ, _SZ, _SZ, _SZ, _D, _P, _P, _P, _P]),
     "ref_route_from_probs_f64": (C.c_int, [_P, _SZ, _SZ, _SZ, _SZ, _SZ, _D, _P, _P, _P, _P]),
     "ref_bias_update": (C.c_int, [_SZ, _SZ, _SZ, _SZ, _P, _D, _P, _P, _P, _P]),
@@ -189,6 +191,22 @@ def orc_route_topk(x, w, n_ffn, n_zero, k, ke, mu=0.0, bias=None, want_probs=Fal
     c = np.empty(T, np.uint32)
     probs = np.empty((T, E), np.float32) if want_probs else None
     rc = orc().orc_route_topk_f32(ptr(x), T, d, ptr(w), n_ffn, n_zero, k, ke, mu, ptr(b),
+                                  ptr(idx), ptr(g), ptr(c), ptr(probs))
+    return rc, idx, g, c, probs
+
+
+def orc_route_topk_f64(x, w, n_ffn, n_zero, k, ke, mu=0.0, bias=None):
+    """RouterState<double> route_topk restated (libm exp)."""
+    x = np.ascontiguousarray(x, np.float64)
+    w = np.ascontiguousarray(w, np.float64)
+    T, d = x.shape
+    E = n_ffn + n_zero
+    b = np.zeros(E) if bias is None else np.ascontiguousarray(bias, np.float64)
+    idx = np.empty(T * k, np.uint32)
+    g = np.empty(T * k, np.float64)
+    c = np.empty(T, np.uint32)
+    probs = np.empty((T, E), np.float64)
+    rc = orc().orc_route_topk_f64(ptr(x), T, d, ptr(w), n_ffn, n_zero, k, ke, mu, ptr(b),
                                   ptr(idx), ptr(g), ptr(c), ptr(probs))
     return rc, idx, g, c, probs
 

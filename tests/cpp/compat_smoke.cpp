@@ -55,6 +55,26 @@ static void selection_is_biased_gates_are_not() {  // test_router.cpp:26-51
     CHECK((d.indices == std::vector<std::uint32_t>{0, 1}));
 }
 
+static void route_topk_double_full_path() {  // test_router.cpp:53-71 (RouterState<double>)
+    CounterRng rng(3);
+    const std::size_t d_model = 8, n = 3, z = 2;
+    RouterState<double> st(seeded_init<double>({d_model, n + z}, InitDistribution::TruncatedNormal,
+                                               0.25, rng.stream(0)),
+                           n, z, 3, 2, 0.1, 1.0);
+    Tensor<double> x({5, d_model});
+    for (std::size_t i = 0; i < x.numel(); ++i) x.data[i] = rng.normal_at(100 + i);
+    Tensor<double> probs;
+    auto d = route_topk(x, st, &probs);
+    auto d2 = route_from_probs(probs, st);
+    CHECK(d.indices == d2.indices);
+    CHECK(d.gates == d2.gates);
+    for (std::size_t t = 0; t < 5; ++t) {
+        double s = 0.0;
+        for (std::size_t e = 0; e < n + z; ++e) s += probs.at(t, e);
+        CHECK(std::fabs(s - 1.0) <= 1e-12);
+    }
+}
+
 static void config_errors() {  // test_router.cpp:88-92
     CHECK_THROWS_AS(make_state(2, 1, 4, 1), ConfigError);
     CHECK_THROWS_AS(make_state(2, 0, 2, 1), ConfigError);
@@ -184,6 +204,7 @@ static void closed_loop_controller() {  // test_router.cpp:269-283 (fp32 router)
 }
 
 int main() {
+    route_topk_double_full_path();
     selection_is_biased_gates_are_not();
     config_errors();
     bias_update_rules();

@@ -481,3 +481,51 @@ def test_longcat_prefill_full_shape_sampled_tokens(scmoe):
     assert (bits64(probe_g.reshape(-1, s.top_k)) == bits64(gates_h[sample])).all()
     err = O.rel_l2(out_h[sample] - a3[sample], want - a3[sample])
     assert err <= 5e-3, err
+
+
+@pytest.mark.parametrize("shape", [(512, 256, 8, 4, 2, 1), (301, 256, 8, 4, 2, 1),
+                                   (200, 6144, 512, 256, 12, 8)])
+def test_route_topk_f64_bitwise(scmoe, shape):
+    """route_topk for RouterState<double> (S = double): projection in double,
+    softmax with the device glibc exp(double) port -- probabilities, indices,
+    gates and counts bitwise equal to the reference (oracle pinned on _ref)."""
+    P = scmoe
+    T, d, n, z, k, ke = shape
+    x = O.normal_f64(O.stream_seed(98, 0), T * d).reshape(T, d)
+    w = O.uniform_f32(O.stream_seed(6, 0), d * (n + z), 1.0 / d).astype(np.float64).reshape(d, n + z)
+    b = np.zeros(n + z)
+    b[:n] = O.normal_f64(18, n) * 1e-3
+    st = P.RouterState(w, n, z, k, ke, 0.0, 1.0)
+    st.b[:] = b
+    pl = []
+    dg = P.route_topk(x, st, pl)
+    rc, idx, g, c, probs = O.orc_route_topk_f64(x, w, n, z, k, ke, bias=b)
+    assert rc == 0
+    assert (pl[0].view(np.uint64) == probs.view(np.uint64)).all()
+    assert (dg.indices == idx).all() and (bits64(dg.gates) == bits64(g)).all()
+    assert (dg.ffn_count == c).all()
+
+
+def test_device_exp_f64_matches_libm(scmoe):
+    """The device instantiation of the glibc exp(double) port vs host libm on
+    300k inputs over the whole range, the softmax domain and edge values."""
+    import ctypes
+    import torch
+    P = scmoe
+    libm = ctypes.CDLL("libm.so.6")
+    libm.exp.restype = ctypes.c_double
+    libm.exp.argtypes = [ctypes.c_double]
+    rng = np.random.default_rng(5)
+    x = np.concatenate([rng.uniform(-750, 750, 100_000), rng.uniform(-30, 10, 100_000),
+                        -rng.uniform(0, 1e-3, 100_000),
+                        [0.0, -0.0, 709.78, 709.79, -708.4, -745.13, -745.14, -746.0, 1e-300,
+                         np.inf, -np.inf]])
+    want = np.array([libm.exp(float(v)) for v in x])
+    ctx = P.Context(0)
+    xd = torch.from_numpy(x).cuda()
+    out = torch.empty_like(xd)
+    ctx._check(P.lib().scmoe_debug_exp(ctx.handle, xd.data_ptr(), out.data_ptr(), x.size))
+    ctx.synchronize()
+    got = out.cpu().numpy()
+    assert (got.view(np.uint64) == want.view(np.uint64)).all(), \
+        int((got.view(np.uint64) != want.view(np.uint64)).sum())

@@ -172,6 +172,21 @@ def test_expf_port_matches_libm_strided():
     assert int(checked) > 70_000_000 and int(bad) == 0, out.stdout
 
 
+def test_exp_port_matches_libm_sampled():
+    """The product's glibc-exp (double) restatement vs this host's libm:
+    10^7 samples over the whole range, the softmax domain and tiny inputs,
+    plus edge values (3e8 were checked when it was written)."""
+    src = os.path.join(O.ROOT, "tests", "cpp", "check_exp_port.c")
+    exe = os.path.join(O.ORACLE_DIR, "_ref", "check_exp_port")
+    os.makedirs(os.path.dirname(exe), exist_ok=True)
+    subprocess.run(["gcc", "-O2", "-ffp-contract=off",
+                    "-I" + os.path.join(O.ROOT, "paper_2509_01322_b200", "csrc"), src, "-o", exe,
+                    "-lm"], check=True)
+    out = subprocess.run([exe, "10000000"], capture_output=True, text=True)
+    checked, bad, _ = out.stdout.split()
+    assert int(checked) > 10_000_000 and int(bad) == 0, out.stdout
+
+
 # ---- (b) oracle == reference, bitwise -------------------------------------------------
 def test_rng_matches_reference(orc, ref):
     for s, c in [(0, 0), (7, 123456), (2024, 2**40 + 3)]:
@@ -297,3 +312,23 @@ def test_routing_stats_match_reference(orc):
     idx, cnt = O.random_decision(1, 10, 2, 8, 4)
     assert O.routing_stats(orc.orc_routing_stats, idx, cnt, 2, 8, 4, 1, 3)[0] == 1
     assert O.routing_stats(ref.ref_routing_stats, idx, cnt, 2, 8, 4, 1, 3)[0] == 1
+
+
+@pytest.mark.parametrize("shape", [(512, 256, 8, 4, 2, 1), (48, 6144, 512, 256, 12, 8)])
+def test_route_topk_f64_oracle_equals_reference(orc, ref, shape):
+    """RouterState<double>: projection in double, softmax with libm exp."""
+    T, d, n, z, k, ke = shape
+    x = O.normal_f64(O.stream_seed(98, 0), T * d).reshape(T, d)
+    w = O.uniform_f32(O.stream_seed(6, 0), d * (n + z), 1.0 / d).astype(np.float64).reshape(d, n + z)
+    b = np.zeros(n + z)
+    b[:n] = O.normal_f64(18, n) * 1e-3
+    rc1, i1, g1, c1, p1 = O.orc_route_topk_f64(x, w, n, z, k, ke, bias=b)
+    i2 = np.empty(T * k, np.uint32)
+    g2 = np.empty(T * k)
+    c2 = np.empty(T, np.uint32)
+    p2 = np.empty((T, n + z))
+    rc2 = ref.ref_route_topk_f64(ptr(x), T, d, ptr(w), n, z, k, ke, 0.0, ptr(b), ptr(i2), ptr(g2),
+                                 ptr(c2), ptr(p2), 4)
+    assert rc1 == rc2 == 0
+    assert (i1 == i2).all() and (g1.view(np.uint64) == g2.view(np.uint64)).all()
+    assert (c1 == c2).all() and (p1.view(np.uint64) == p2.view(np.uint64)).all()

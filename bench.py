@@ -513,6 +513,21 @@ def run_b200_ep(args):
     a1 = torch.from_numpy(a1_h).cuda()
     a3 = torch.from_numpy(a3_h).cuda()
     chunks = args.ep_chunks
+    if args.ep_transport == "p2p":
+        # the peer-memory transport needs torch symmetric memory over NVLink; if
+        # this box cannot map it, every rank falls back to NCCL (same decision)
+        import torch.distributed as dist
+        ok = torch.ones(1, device="cuda")
+        try:
+            ep.forward(a1, a3, None, T, chunks=chunks)
+            torch.cuda.synchronize()
+        except Exception as e:  # reported, the run continues on NCCL
+            log(f"[rank {rank}] p2p transport unavailable ({e}); falling back to nccl")
+            ok.zero_()
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if ok.item() < 1:
+            args.ep_transport = "nccl"
+            ep = EPLayer(ops, transport="nccl")
     for _ in range(args.warmup):
         out, idx, gates, cnt = ep.forward(a1, a3, None, T, chunks=chunks)
     torch.cuda.synchronize()

@@ -314,30 +314,26 @@ class EPLayer:
             ops.p2p_buffers(self.group, max(1, int(max(need_r, cap[0]) * 1.25)),
                             max(1, int(max(need_s, cap[1]) * 1.25)), nsets=max(nsets, 1))
         st = ops.p2p_sets[k]
-        send_start = [0]
-        for d in range(G):
-            send_start.append(send_start[-1] + Mh[me][d])
-        dst_offset = [sum(Mh[s][d] for s in range(me)) for d in range(G)]
-        recv_offset = [0]
-        for s in range(G):
-            recv_offset.append(recv_offset[-1] + Mh[s][me])
-        # received row r (source s's j-th row for me) returns to source s's back
-        # buffer at row (sum_{d<me} M[s][d]) + j
-        back_start = [sum(Mh[s][:me]) for s in range(G)]
+        # offsets from the count matrix, on the device (no per-step host copies)
+        Md = allc.view(G, G).to(torch.int64)
+        col_excl = torch.cumsum(Md, 0) - Md            # [s][d] = sum_{s'<s} M[s'][d]
+        row_excl = torch.cumsum(Md, 1) - Md            # [s][d] = sum_{d'<d} M[s][d']
+        send_start = torch.zeros(G + 1, dtype=torch.int32, device=Md.device)
+        send_start[1:] = torch.cumsum(Md[me], 0).to(torch.int32)
+        dst_offset = col_excl[me].contiguous()         # where my rows start in rank d's buffer
+        recv_offset = col_excl[:, me]                  # where source s's rows start in mine
+        back_start = row_excl[:, me]                   # source s's send index of its rows for me
         dev = counts.device
-        rows_per_src = torch.tensor([Mh[s][me] for s in range(G)], dtype=torch.int64, device=dev)
-        src = torch.repeat_interleave(torch.arange(G, device=dev), rows_per_src, output_size=n_recv)
-        j = torch.arange(n_recv, dtype=torch.int64, device=dev) - \
-            torch.tensor(recv_offset[:G], dtype=torch.int64, device=dev)[src]
-        # comm=False (timing reference): no dispatch, GEMM2 rows stay local
+        src = torch.repeat_interleave(torch.arange(G, device=dev), Md[:, me], output_size=n_recv)
+        j = torch.arange(n_recv, dtype=torch.int64, device=dev) - recv_offset[src]
+        # received row r (source s's j-th row for me) returns to source s's back
+        # buffer at row back_start[s] + j; comm=False (timing reference): no
+        # dispatch, GEMM2 rows stay local
         back_ptr = st["peer_back"] if self.comm else \
             torch.full_like(st["peer_back"], st["back"].data_ptr())
-        row_dst = back_ptr[src] + (torch.tensor(back_start, dtype=torch.int64, device=dev)[src]
-                                   + j) * (ops.shape.d * 2)
+        row_dst = back_ptr[src] + (back_start[src] + j) * (ops.shape.d * 2)
         if self.comm:
-            ops.put_rows(st, hb, send_token, send_expert, n_send,
-                         torch.tensor(send_start, dtype=torch.int32, device=dev),
-                         torch.tensor(dst_offset, dtype=torch.int64, device=dev))
+            ops.put_rows(st, hb, send_token, send_expert, n_send, send_start, dst_offset)
         else:
             st["recv_exp"][:n_recv].fill_(ops.first)
         st["h_recv"].barrier(channel=0)

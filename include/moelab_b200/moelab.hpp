@@ -15,7 +15,7 @@
 //   bias_update                     router.hpp:155-176
 //   simulate_bias_control           router.hpp:349-369       (S = float)
 //   GammaMode, ExpertBank<S>        blocks.hpp:185-213
-//   moe_forward                     blocks.hpp:372-394       (S = float)
+//   moe_forward                     blocks.hpp:372-394       (S = float, double)
 //
 // Results equal the reference's bit for bit (fp32 path).  Errors are thrown
 // as the reference throws them (ConfigError from RouterState, StateError for
@@ -477,8 +477,7 @@ scmoe_bank* bank_of(const ExpertBank<S>& bank, int precision) {
         if constexpr (std::is_same_v<S, float>) {
             d.ok(scmoe_bank_set_expert_host(d.ctx, b, e, wi.data.data(), wo.data.data()));
         } else {
-            std::vector<float> a(wi.data.begin(), wi.data.end()), c(wo.data.begin(), wo.data.end());
-            d.ok(scmoe_bank_set_expert_host(d.ctx, b, e, a.data(), c.data()));
+            d.ok(scmoe_bank_set_expert_f64_host(d.ctx, b, e, wi.data.data(), wo.data.data()));
         }
     }
     d.banks[&bank] = {fp, b};
@@ -486,12 +485,13 @@ scmoe_bank* bank_of(const ExpertBank<S>& bank, int precision) {
 }
 }  // namespace b200
 
-// blocks.hpp:372-394.  precision: SCMOE_PREC_F32_EXACT (bit-exact, default) or
-// SCMOE_PREC_BF16 (tcgen05 tensor cores, rel-L2 <= 2e-2).
+// blocks.hpp:372-394.  S = float: precision SCMOE_PREC_F32_EXACT (bit-exact,
+// default) or SCMOE_PREC_BF16 (tcgen05 tensor cores, rel-L2 <= 2e-2);
+// S = double: the fp64 bank (bit-exact moe_forward<double>).
 template <typename S>
 Tensor<S> moe_forward(const Tensor<S>& x, const RoutingDecision& dd, const ExpertBank<S>& bank,
                       std::size_t n_zero, int precision = SCMOE_PREC_F32_EXACT) {
-    static_assert(std::is_same_v<S, float>, "moe_forward on the B200 path is fp32 (S = float)");
+    if constexpr (std::is_same_v<S, double>) precision = SCMOE_PREC_F64_EXACT;
     const std::size_t e_total = bank.n_experts() + n_zero;
     for (auto i : dd.indices)
         if (i >= e_total) throw StateError("moe_forward: expert index out of range");
@@ -500,8 +500,13 @@ Tensor<S> moe_forward(const Tensor<S>& x, const RoutingDecision& dd, const Exper
     Tensor<S> out({T, dm});
     auto& d = b200::device();
     scmoe_bank* b = b200::bank_of(bank, precision);
-    d.ok(scmoe_moe_forward_host(d.ctx, b, x.data.data(), T, dd.indices.data(), dd.gates.data(),
-                                dd.top_k, n_zero, 0, nullptr, out.data.data()));
+    if constexpr (std::is_same_v<S, double>)
+        d.ok(scmoe_moe_forward_f64_host(d.ctx, b, x.data.data(), T, dd.indices.data(),
+                                        dd.gates.data(), dd.top_k, n_zero, 0, nullptr,
+                                        out.data.data()));
+    else
+        d.ok(scmoe_moe_forward_host(d.ctx, b, x.data.data(), T, dd.indices.data(), dd.gates.data(),
+                                    dd.top_k, n_zero, 0, nullptr, out.data.data()));
     return out;
 }
 

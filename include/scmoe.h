@@ -50,8 +50,10 @@ typedef enum {
 typedef enum {
     SCMOE_PREC_F32_EXACT = 0, /* fp32 weights in the reference layout; sequential-k SIMT
                                  kernels, bitwise equal to moe_forward<float> */
-    SCMOE_PREC_BF16 = 1       /* bf16 weights, transposed K-major for the tcgen05 grouped
+    SCMOE_PREC_BF16 = 1,      /* bf16 weights, transposed K-major for the tcgen05 grouped
                                  GEMM (fp32 accumulate); rel-L2 <= 2e-2 vs the oracle */
+    SCMOE_PREC_F64_EXACT = 2  /* fp64 weights in the reference layout (ExpertBank<double>);
+                                 bitwise equal to moe_forward<double>; scmoe_*_f64 calls */
 } scmoe_precision;
 
 /* GammaMode (blocks.hpp:185): FfnOnly / All / Off. */
@@ -204,6 +206,21 @@ int scmoe_moe_forward_host(scmoe_ctx* ctx, scmoe_bank* b, const float* x, size_t
                            size_t n_zero, int renormalize, const float* residual, float* out);
 
 /* Graph::rmsnorm forward (graph.hpp:322-335), fp32, eps as given (1e-6 default). */
+/* ExpertBank<double> / moe_forward<double> (blocks.hpp:372-394, S = double):
+ * a SCMOE_PREC_F64_EXACT bank, weights set in double; the expert FFN in
+ * double (sequential DMUL/DADD, sign-branched logistic on the glibc exp
+ * restatement) and the combine in double, bitwise equal to the reference. */
+int scmoe_bank_set_expert_f64(scmoe_ctx* ctx, scmoe_bank* b, size_t expert, const double* w_in,
+                              const double* w_out);
+int scmoe_bank_set_expert_f64_host(scmoe_ctx* ctx, scmoe_bank* b, size_t expert,
+                                   const double* w_in, const double* w_out);
+int scmoe_moe_forward_f64(scmoe_ctx* ctx, scmoe_bank* b, const double* x, size_t tokens,
+                          const uint32_t* indices, const double* gates, size_t top_k,
+                          size_t n_zero, int renormalize, const double* residual, double* out);
+int scmoe_moe_forward_f64_host(scmoe_ctx* ctx, scmoe_bank* b, const double* x, size_t tokens,
+                               const uint32_t* indices, const double* gates, size_t top_k,
+                               size_t n_zero, int renormalize, const double* residual,
+                               double* out);
 int scmoe_rmsnorm(scmoe_ctx* ctx, const float* x, const float* gain, size_t rows, size_t d,
                   float eps, float* out);
 

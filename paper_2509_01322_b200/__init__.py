@@ -68,6 +68,7 @@ _ERRORS = {1: ConfigError, 2: DimensionError, 3: StateError, 4: ParameterError, 
 
 PREC_F32_EXACT = 0
 PREC_BF16 = 1
+PREC_F64_EXACT = 2
 
 
 class GammaMode(enum.IntEnum):
@@ -120,6 +121,11 @@ _PROTOS = {
     "scmoe_route_topk_f64": (C.c_int, [_P, _P, _P, _SZ, _P, _P, _P, _P, _P]),
     "scmoe_route_topk_f64_host": (C.c_int, [_P, _P, _P, _SZ, _P, _P, _P, _P, _P]),
     "scmoe_debug_exp": (C.c_int, [_P, _P, _P, _SZ]),
+    "scmoe_bank_set_expert_f64": (C.c_int, [_P, _P, _SZ, _P, _P]),
+    "scmoe_bank_set_expert_f64_host": (C.c_int, [_P, _P, _SZ, _P, _P]),
+    "scmoe_moe_forward_f64": (C.c_int, [_P, _P, _P, _SZ, _P, _P, _SZ, _SZ, C.c_int, _P, _P]),
+    "scmoe_moe_forward_f64_host": (C.c_int, [_P, _P, _P, _SZ, _P, _P, _SZ, _SZ, C.c_int, _P,
+                                             _P]),
     "scmoe_routing_stats": (C.c_int, [_P, _P, _P, _SZ, _SZ, _SZ, _SZ, _SZ, _SZ, _P, _P, _P, _P]),
     "scmoe_routing_stats_host": (C.c_int, [_P, _P, _P, _SZ, _SZ, _SZ, _SZ, _SZ, _SZ, _P, _P, _P,
                                            _P]),
@@ -555,8 +561,10 @@ class ExpertBank:
 
     def __init__(self, w_in: Sequence[np.ndarray], w_out: Sequence[np.ndarray], m: int = 1,
                  gamma_mode: GammaMode = GammaMode.FfnOnly, precision: int = PREC_F32_EXACT):
-        self.w_in = [np.ascontiguousarray(w, np.float32) for w in w_in]
-        self.w_out = [np.ascontiguousarray(w, np.float32) for w in w_out]
+        # PREC_F64_EXACT is ExpertBank<double> (weights kept in double)
+        dt = np.float64 if precision == PREC_F64_EXACT else np.float32
+        self.w_in = [np.ascontiguousarray(w, dt) for w in w_in]
+        self.w_out = [np.ascontiguousarray(w, dt) for w in w_out]
         self.m, self.gamma_mode, self.precision = m, GammaMode(gamma_mode), precision
         if m < 1:
             raise ParameterError("variance_gamma: m must be >= 1")
@@ -585,8 +593,9 @@ class ExpertBank:
         for e in range(n):
             if self.w_in[e].shape != (d, I) or self.w_out[e].shape != (I, d):
                 raise DimensionError("moe_block: expert weight shapes disagree")
-            ctx._check(lib().scmoe_bank_set_expert_host(ctx.handle, h, e, _ptr(self.w_in[e]),
-                                                        _ptr(self.w_out[e])))
+            setter = (lib().scmoe_bank_set_expert_f64_host if self.precision == PREC_F64_EXACT
+                      else lib().scmoe_bank_set_expert_host)
+            ctx._check(setter(ctx.handle, h, e, _ptr(self.w_in[e]), _ptr(self.w_out[e])))
         self._dev = (ctx, h)
         return h
 
@@ -594,9 +603,12 @@ class ExpertBank:
 def moe_forward(x: np.ndarray, d: RoutingDecision, bank: ExpertBank, n_zero: int,
                 renormalize: bool = False, residual: Optional[np.ndarray] = None,
                 ctx: Optional[Context] = None) -> np.ndarray:
-    """blocks.hpp:372-394 (+ optional renormalisation and fused residual)."""
+    """blocks.hpp:372-394 (+ optional renormalisation and fused residual).
+    An fp64 bank (PREC_F64_EXACT) computes moe_forward<double> on fp64 x."""
     ctx = ctx or default_context()
-    x = _as2d(x, np.float32)
+    f64 = bank.precision == PREC_F64_EXACT
+    dt = np.float64 if f64 else np.float32
+    x = _as2d(x, dt)
     T, dm = x.shape
     K = d.top_k
     idx = np.ascontiguousarray(d.indices, np.uint32)
@@ -609,10 +621,11 @@ def moe_forward(x: np.ndarray, d: RoutingDecision, bank: ExpertBank, n_zero: int
     if idx.size != T * K or gates.size != T * K:
         raise DimensionError("moe_combine: slot map size mismatch")
     h = bank.device(ctx)
-    out = np.empty((T, dm), np.float32)
-    res = None if residual is None else _as2d(residual, np.float32)
-    ctx._check(lib().scmoe_moe_forward_host(ctx.handle, h, _ptr(x), T, _ptr(idx), _ptr(gates), K,
-                                            n_zero, int(renormalize), _ptr(res), _ptr(out)))
+    out = np.empty((T, dm), dt)
+    res = None if residual is None else _as2d(residual, dt)
+    fn = lib().scmoe_moe_forward_f64_host if f64 else lib().scmoe_moe_forward_host
+    ctx._check(fn(ctx.handle, h, _ptr(x), T, _ptr(idx), _ptr(gates), K, n_zero, int(renormalize),
+                  _ptr(res), _ptr(out)))
     return out
 
 

@@ -700,7 +700,8 @@ int scmoe_bank_create(scmoe_ctx* c, size_t n, size_t d, size_t inter, int precis
     return guarded(c, [&] {
         require_ctx(c);
         if (m < 1) SCMOE_THROW(SCMOE_ERR_PARAMETER, "variance_gamma: m must be >= 1");
-        if (precision != SCMOE_PREC_F32_EXACT && precision != SCMOE_PREC_BF16)
+        if (precision != SCMOE_PREC_F32_EXACT && precision != SCMOE_PREC_BF16 &&
+            precision != SCMOE_PREC_F64_EXACT)
             SCMOE_THROW(SCMOE_ERR_PARAMETER, "bank: unknown precision");
         if (gamma_mode < 0 || gamma_mode > 2) SCMOE_THROW(SCMOE_ERR_PARAMETER, "unknown gamma mode");
         if (precision == SCMOE_PREC_BF16) {
@@ -722,6 +723,11 @@ int scmoe_bank_create(scmoe_ctx* c, size_t n, size_t d, size_t inter, int precis
             SCMOE_CUDA(cudaMalloc(&b->w_out32, std::max<size_t>(n * per, 1) * sizeof(float)));
             stream_zero(c, b->w_in32, std::max<size_t>(n * per, 1) * sizeof(float));
             stream_zero(c, b->w_out32, std::max<size_t>(n * per, 1) * sizeof(float));
+        } else if (precision == SCMOE_PREC_F64_EXACT) {
+            SCMOE_CUDA(cudaMalloc(&b->w_in64, std::max<size_t>(n * per, 1) * sizeof(double)));
+            SCMOE_CUDA(cudaMalloc(&b->w_out64, std::max<size_t>(n * per, 1) * sizeof(double)));
+            stream_zero(c, b->w_in64, std::max<size_t>(n * per, 1) * sizeof(double));
+            stream_zero(c, b->w_out64, std::max<size_t>(n * per, 1) * sizeof(double));
         } else {
             SCMOE_CUDA(cudaMalloc(&b->w1t, std::max<size_t>(n * per, 1) * sizeof(__nv_bfloat16)));
             SCMOE_CUDA(cudaMalloc(&b->w2t, std::max<size_t>(n * per, 1) * sizeof(__nv_bfloat16)));
@@ -739,6 +745,8 @@ int scmoe_bank_destroy(scmoe_ctx* c, scmoe_bank* b) {
     cudaFree(b->w_out32);
     cudaFree(b->w1t);
     cudaFree(b->w2t);
+    cudaFree(b->w_in64);
+    cudaFree(b->w_out64);
     delete b;
     return SCMOE_OK;
 }
@@ -748,6 +756,8 @@ int scmoe_bank_set_expert(scmoe_ctx* c, scmoe_bank* b, size_t e, const float* w_
     return guarded(c, [&] {
         require_ctx(c);
         if (e >= b->n) SCMOE_THROW(SCMOE_ERR_DIMENSION, "bank: expert index out of range");
+        if (b->precision == SCMOE_PREC_F64_EXACT)
+            SCMOE_THROW(SCMOE_ERR_PARAMETER, "bank: an fp64 bank takes scmoe_bank_set_expert_f64");
         const size_t per = b->d * b->inter;
         if (b->precision == SCMOE_PREC_F32_EXACT) {
             SCMOE_CUDA(cudaMemcpyAsync(b->w_in32 + e * per, w_in, per * sizeof(float),
@@ -803,7 +813,9 @@ double scmoe_bank_gamma_zero(const scmoe_bank* b) { return b ? b->gamma_zero() :
 size_t scmoe_bank_device_bytes(const scmoe_bank* b) {
     if (!b) return 0;
     const size_t per = b->d * b->inter * b->n * 2;
-    return b->precision == SCMOE_PREC_F32_EXACT ? per * 4 : per * 2;
+    return b->precision == SCMOE_PREC_F64_EXACT ? per * 8
+           : b->precision == SCMOE_PREC_F32_EXACT ? per * 4
+                                                   : per * 2;
 }
 
 // ---- MoE forward / layer ---------------------------------------------------
@@ -835,6 +847,86 @@ int scmoe_moe_forward_host(scmoe_ctx* c, scmoe_bank* b, const float* x, size_t T
         const float* dr = residual ? upload(c, s.bufs[3], residual, T * b->d) : nullptr;
         float* dout = s.bufs[4].get<float>(T * b->d);
         int rc = scmoe_moe_forward(c, b, xd, T, di, dg, K, n_zero, renorm, dr, dout);
+        if (rc) throw ScmoeError{rc, c->last_error};
+        download(c, out, dout, T * b->d);
+        sync_and_check(c);
+    });
+}
+
+int scmoe_bank_set_expert_f64(scmoe_ctx* c, scmoe_bank* b, size_t e, const double* w_in,
+                              const double* w_out) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        if (b->precision != SCMOE_PREC_F64_EXACT)
+            SCMOE_THROW(SCMOE_ERR_PARAMETER, "bank: scmoe_bank_set_expert_f64 needs an fp64 bank");
+        if (e >= b->n) SCMOE_THROW(SCMOE_ERR_DIMENSION, "bank: expert index out of range");
+        const size_t per = b->d * b->inter;
+        SCMOE_CUDA(cudaMemcpyAsync(b->w_in64 + e * per, w_in, per * sizeof(double),
+                                   cudaMemcpyDefault, c->stream));
+        SCMOE_CUDA(cudaMemcpyAsync(b->w_out64 + e * per, w_out, per * sizeof(double),
+                                   cudaMemcpyDefault, c->stream));
+    });
+}
+int scmoe_bank_set_expert_f64_host(scmoe_ctx* c, scmoe_bank* b, size_t e, const double* w_in,
+                                   const double* w_out) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        int rc = scmoe_bank_set_expert_f64(c, b, e, w_in, w_out);
+        if (rc) throw ScmoeError{rc, c->last_error};
+        SCMOE_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int scmoe_moe_forward_f64(scmoe_ctx* c, scmoe_bank* b, const double* x, size_t T,
+                          const uint32_t* idx, const double* gates, size_t K, size_t n_zero,
+                          int renorm, const double* residual, double* out) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        if (b->precision != SCMOE_PREC_F64_EXACT)
+            SCMOE_THROW(SCMOE_ERR_PARAMETER, "moe_forward_f64: needs an fp64 bank");
+        SCMOE_CHECK_ARG(K >= 1 && K <= 64, SCMOE_ERR_CONFIG, "moe_forward: top_k must be in [1, 64]");
+        if (T == 0) return;
+        const size_t n_ffn = b->n, d = b->d, I = b->inter, E = n_ffn + n_zero;
+        launch_check_indices(c, idx, T * K, E);
+        PermResult pr;
+        {
+            ProfScope _p(c, "permute");
+            pr = launch_permute(c, idx, T, K, n_ffn, E, 64);
+        }
+        Workspace& ws = c->ws;
+        double* h = ws.h.get<double>(T * K * I + 1);
+        double* y = ws.y.get<double>(T * K * d + 1);
+        {
+            ProfScope _p(c, "expert_gemm1_f64");
+            launch_seq_gemm_f64(c, x, d, pr.row_token, b->w_in64, I, d * I, h, I, d, I, 1,
+                                pr.tiles, pr.n_tiles, pr.max_tiles);
+        }
+        {
+            ProfScope _p(c, "expert_gemm2_f64");
+            launch_seq_gemm_f64(c, h, I, nullptr, b->w_out64, d, I * d, y, d, I, d, 0, pr.tiles,
+                                pr.n_tiles, pr.max_tiles);
+        }
+        ProfScope _p(c, "combine_f64");
+        launch_combine_f64(c, x, y, idx, gates, pr.slot_pos, T, d, K, n_ffn, b->gamma_ffn(),
+                           b->gamma_zero(), renorm, residual, out);
+    });
+}
+int scmoe_moe_forward_f64_host(scmoe_ctx* c, scmoe_bank* b, const double* x, size_t T,
+                               const uint32_t* idx, const double* gates, size_t K, size_t n_zero,
+                               int renorm, const double* residual, double* out) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        // blocks.hpp:375-377 -- index range check before any work
+        for (size_t i = 0; i < T * K; ++i)
+            if (idx[i] >= b->n + n_zero) SCMOE_THROW(SCMOE_ERR_STATE, "moe_forward: expert index out of range");
+        if (T == 0) return;
+        Stage& s = stage_of(c);
+        const double* xd = upload(c, s.bufs[0], x, T * b->d);
+        const uint32_t* di = upload(c, s.bufs[1], idx, T * K);
+        const double* dg = upload(c, s.bufs[2], gates, T * K);
+        const double* dr = residual ? upload(c, s.bufs[3], residual, T * b->d) : nullptr;
+        double* dout = s.bufs[4].get<double>(T * b->d);
+        int rc = scmoe_moe_forward_f64(c, b, xd, T, di, dg, K, n_zero, renorm, dr, dout);
         if (rc) throw ScmoeError{rc, c->last_error};
         download(c, out, dout, T * b->d);
         sync_and_check(c);

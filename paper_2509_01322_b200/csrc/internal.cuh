@@ -175,6 +175,8 @@ struct scmoe_bank {
     float* w_out32 = nullptr;         // [n][inter][d]
     __nv_bfloat16* w1t = nullptr;     // [n][inter][d]   (BF16, K-major for GEMM1)
     __nv_bfloat16* w2t = nullptr;     // [n][d][inter]   (BF16, K-major for GEMM2)
+    double* w_in64 = nullptr;         // [n][d][inter]   (F64_EXACT)
+    double* w_out64 = nullptr;        // [n][inter][d]
     double gamma_ffn() const { return gamma_mode == SCMOE_GAMMA_OFF ? 1.0 : (double)m; }
     double gamma_zero() const { return gamma_mode == SCMOE_GAMMA_ALL ? (double)m : 1.0; }
 };
@@ -216,6 +218,17 @@ void launch_router_f64(scmoe_ctx* c, const double* X, const double* W, double* l
 void launch_softmax_topk_f64(scmoe_ctx* c, const double* logits, size_t T, size_t E, size_t K,
                              size_t n_ffn, const double* bias, uint32_t* idx, double* gates,
                              uint32_t* ffn, double* probs);
+// moe_forward<double>: grouped sequential GEMM in double over token tiles
+// (rows a_rows[pos + r] of A, or A rows pos + r), optional SiLU, and the
+// double combine.
+void launch_seq_gemm_f64(scmoe_ctx* c, const double* A, size_t lda, const int* a_rows,
+                         const double* B, size_t ldb, size_t b_group_stride, double* C,
+                         size_t ldc, size_t K, size_t N, int silu, const TokenTile* tiles,
+                         const int* n_tiles_dev, size_t max_tiles);
+void launch_combine_f64(scmoe_ctx* c, const double* x, const double* y, const uint32_t* idx,
+                        const double* gates, const int* slot_pos, size_t T, size_t d, size_t K,
+                        size_t n_ffn, double gamma_ffn, double gamma_zero, int renorm,
+                        const double* residual, double* out);
 void launch_debug_exp(scmoe_ctx* c, const double* in, double* out, size_t n);
 bool router_tma_ok(size_t T, size_t K, size_t E, int num_sms);
 void launch_router_tma(scmoe_ctx* c, const float* X, const float* W, float* logits, size_t T,

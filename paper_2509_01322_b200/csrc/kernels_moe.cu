@@ -366,6 +366,70 @@ static void launch_combine_impl(scmoe_ctx* c, const float* x, const Y* y, const 
     SCMOE_LAUNCH_CHECK(c);
 }
 
+// moe_combine forward in S = double (blocks.hpp:226-274), same order as the
+// fp32 kernel: w = gate / denom, FFN out += (g_ffn*w)*y, zero_w += w, then the
+// identity term and the residual.
+__global__ void __launch_bounds__(256) combine_f64_kernel(
+    const double* __restrict__ x, const double* __restrict__ y, const uint32_t* __restrict__ idx,
+    const double* __restrict__ gates, const int* __restrict__ slot_pos, int d, int K, int n_ffn,
+    double gamma_ffn, double gamma_zero, int renorm, const double* __restrict__ residual,
+    double* __restrict__ out) {
+    __shared__ double coeff[kMaxK];
+    __shared__ int rowpos[kMaxK];
+    __shared__ int nffn, use_zero;
+    __shared__ double zcoeff;
+    const int t = blockIdx.x;
+    if (threadIdx.x == 0) {
+        double denom = 1.0;
+        if (renorm) {
+            double s = 0.0;
+            for (int sl = 0; sl < K; ++sl) s = __dadd_rn(s, gates[(size_t)t * K + sl]);
+            denom = s;
+        }
+        double zero_w = 0.0;
+        int n = 0;
+        for (int sl = 0; sl < K; ++sl) {
+            const uint32_t e = idx[(size_t)t * K + sl];
+            const double w = __ddiv_rn(gates[(size_t)t * K + sl], denom);
+            if (e < (uint32_t)n_ffn) {
+                coeff[n] = __dmul_rn(gamma_ffn, w);
+                rowpos[n] = slot_pos[(size_t)t * K + sl];
+                ++n;
+            } else {
+                zero_w = __dadd_rn(zero_w, w);
+            }
+        }
+        nffn = n;
+        use_zero = zero_w != 0.0;
+        zcoeff = __dmul_rn(gamma_zero, zero_w);
+    }
+    __syncthreads();
+    const int n = nffn;
+    const double zc = zcoeff;
+    const bool uz = use_zero != 0;
+    const double* xr = x + (size_t)t * d;
+    double* orow = out + (size_t)t * d;
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+        double acc = 0.0;
+        for (int s = 0; s < n; ++s)
+            acc = __dadd_rn(acc, __dmul_rn(coeff[s], y[(size_t)rowpos[s] * d + j]));
+        if (uz) acc = __dadd_rn(acc, __dmul_rn(zc, xr[j]));
+        if (residual) acc = __dadd_rn(residual[(size_t)t * d + j], acc);
+        orow[j] = acc;
+    }
+}
+void launch_combine_f64(scmoe_ctx* c, const double* x, const double* y, const uint32_t* idx,
+                        const double* gates, const int* slot_pos, size_t T, size_t d, size_t K,
+                        size_t n_ffn, double gamma_ffn, double gamma_zero, int renorm,
+                        const double* residual, double* out) {
+    if (T == 0) return;
+    SCMOE_CHECK_ARG(K <= kMaxK, SCMOE_ERR_CONFIG, "combine: top_k too large");
+    combine_f64_kernel<<<T, 256, 0, c->stream>>>(x, y, idx, gates, slot_pos, (int)d, (int)K,
+                                                 (int)n_ffn, gamma_ffn, gamma_zero, renorm,
+                                                 residual, out);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
 void launch_combine_f32(scmoe_ctx* c, const float* x, const float* y, const uint32_t* idx,
                         const double* gates, const int* slot_pos, size_t T, size_t d, size_t K,
                         size_t n_ffn, float gamma_ffn, float gamma_zero, int renorm,

@@ -836,6 +836,79 @@ void launch_softmax_topk_f64(scmoe_ctx* c, const double* logits, size_t T, size_
                              uint32_t* ffn, double* probs) {
     launch_topk_impl<double, true>(c, logits, T, E, K, n_ffn, bias, idx, gates, ffn, probs);
 }
+// graph.hpp:529-533 in S = double: sign-branched logistic on the exp port;
+// graph.hpp:133-135: silu(v) = v * sigmoid(v).
+__device__ __forceinline__ double scmoe_silu_f64(double v) {
+    double sg;
+    if (v >= 0.0) {
+        sg = __ddiv_rn(1.0, __dadd_rn(1.0, scmoe_exp(-v)));
+    } else {
+        const double e = scmoe_exp(v);
+        sg = __ddiv_rn(e, __dadd_rn(1.0, e));
+    }
+    return __dmul_rn(v, sg);
+}
+
+// Grouped sequential GEMM in double (mm_into, tensor.hpp:95-112, S = double):
+// CTA = one token tile (<= 64 rows of one expert) x 64 output columns.
+__global__ void __launch_bounds__(256) seq_gemm_f64_kernel(
+    const double* __restrict__ A, int lda, const int* __restrict__ a_rows,
+    const double* __restrict__ B, int ldb, size_t b_group_stride, double* __restrict__ C, int ldc,
+    int K, int N, int silu, const TokenTile* __restrict__ tiles, const int* __restrict__ n_tiles) {
+    if ((int)blockIdx.y >= *n_tiles) return;
+    const TokenTile tile = tiles[blockIdx.y];
+    __shared__ double xs[16][64 + 1];
+    __shared__ double wsm[16][64];
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    const int col0 = blockIdx.x * 64;
+    const double* Bg = B + (size_t)tile.e * b_group_stride;
+    double acc[4][4] = {};
+    for (int k0 = 0; k0 < K; k0 += 16) {
+        for (int i = threadIdx.x; i < 16 * 64; i += 256) {
+            const int kk = i / 64, cc = i % 64;
+            const int k = k0 + kk, col = col0 + cc;
+            double xv = 0.0;
+            if (cc < tile.count && k < K) {
+                const int p = tile.pos + cc;
+                xv = A[(size_t)(a_rows ? a_rows[p] : p) * lda + k];
+            }
+            xs[kk][cc] = xv;
+            wsm[kk][cc] = (col < N && k < K) ? Bg[(size_t)k * ldb + col] : 0.0;
+        }
+        __syncthreads();
+        const int kn = min(16, K - k0);
+        for (int kk = 0; kk < kn; ++kk) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const double a = xs[kk][ty * 4 + i];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(a, wsm[kk][tx * 4 + j]));
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int r = ty * 4 + i, col = col0 + tx * 4 + j;
+            if (r < tile.count && col < N)
+                C[(size_t)(tile.pos + r) * ldc + col] = silu ? scmoe_silu_f64(acc[i][j]) : acc[i][j];
+        }
+}
+void launch_seq_gemm_f64(scmoe_ctx* c, const double* A, size_t lda, const int* a_rows,
+                         const double* B, size_t ldb, size_t b_group_stride, double* C,
+                         size_t ldc, size_t K, size_t N, int silu, const TokenTile* tiles,
+                         const int* n_tiles_dev, size_t max_tiles) {
+    if (max_tiles == 0 || N == 0) return;
+    const dim3 grid((unsigned)ceil_div(N, 64), (unsigned)std::min<size_t>(max_tiles, 65535));
+    seq_gemm_f64_kernel<<<grid, 256, 0, c->stream>>>(A, (int)lda, a_rows, B, (int)ldb,
+                                                     b_group_stride, C, (int)ldc, (int)K, (int)N,
+                                                     silu, tiles, n_tiles_dev);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
 __global__ void debug_exp_kernel(const double* __restrict__ in, double* __restrict__ out,
                                  size_t n) {
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;

@@ -186,6 +186,43 @@ static void moe_cases() {  // test_blocks.cpp:250-304
     }
 }
 
+static void moe_cases_double() {  // test_blocks.cpp:250-275 with ExpertBank<double>
+    std::vector<Parameter<double>> store;
+    store.reserve(4);
+    ExpertBank<double> bank;
+    for (std::size_t e = 0; e < 2; ++e) {
+        store.emplace_back("in", seeded_init<double>({8, 4}, InitDistribution::Uniform, 1.0 / 8,
+                                                     CounterRng(7).stream(2 * e)));
+        store.emplace_back("out", seeded_init<double>({4, 8}, InitDistribution::Uniform, 1.0 / 8,
+                                                      CounterRng(7).stream(2 * e + 1)));
+    }
+    for (std::size_t e = 0; e < 2; ++e) {
+        bank.w_in.push_back(&store[2 * e]);
+        bank.w_out.push_back(&store[2 * e + 1]);
+    }
+    CounterRng rng(11);
+    Tensor<double> x({3, 8});
+    for (std::size_t i = 0; i < x.numel(); ++i) x.data[i] = rng.normal_at(i);
+    RoutingDecision d;
+    d.top_k = 1;
+    d.n_ffn = 2;
+    d.indices = {2, 3, 2};
+    d.gates = {1.0, 1.0, 1.0};
+    d.ffn_count = {0, 0, 0};
+    Tensor<double> out = moe_forward(x, d, bank, 2);
+    CHECK(out.data == x.data);  // zero-expert identity is bitwise
+    Tensor<double> x1({1, 8});
+    for (std::size_t i = 0; i < 8; ++i) x1.data[i] = rng.normal_at(100 + i);
+    d.top_k = 2;
+    d.indices = {2, 3};
+    d.gates = {0.25, 0.5};
+    d.ffn_count = {0};
+    out = moe_forward(x1, d, bank, 2);
+    bool close = true;
+    for (std::size_t i = 0; i < 8; ++i) close = close && std::fabs(out.data[i] - 0.75 * x1.data[i]) < 1e-12;
+    CHECK(close);
+}
+
 static void closed_loop_controller() {  // test_router.cpp:269-283 (fp32 router)
     RouterState<float> st(seeded_init<float>({64, 24}, InitDistribution::TruncatedNormal,
                                              1.0 / 64, CounterRng(7)),
@@ -205,6 +242,7 @@ static void closed_loop_controller() {  // test_router.cpp:269-283 (fp32 router)
 
 int main() {
     route_topk_double_full_path();
+    moe_cases_double();
     selection_is_biased_gates_are_not();
     config_errors();
     bias_update_rules();

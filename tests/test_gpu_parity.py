@@ -529,3 +529,30 @@ def test_device_exp_f64_matches_libm(scmoe):
     got = out.cpu().numpy()
     assert (got.view(np.uint64) == want.view(np.uint64)).all(), \
         int((got.view(np.uint64) != want.view(np.uint64)).sum())
+
+
+@pytest.mark.parametrize("gamma_mode,m,renorm", [(0, 1, False), (1, 2, True), (2, 3, False)])
+def test_moe_forward_f64_bitwise(scmoe, gamma_mode, m, renorm):
+    """moe_forward<double> (ExpertBank<double>, S = double): the fp64 expert
+    FFN (DMUL/DADD chains, logistic on the exp(double) port) and combine are
+    bitwise equal to the reference's double path (oracle f64)."""
+    P = scmoe
+    T, d, n, z, k, ke, I = 96, 128, 8, 4, 2, 1, 64
+    x = O.normal_f64(O.stream_seed(61, 0), T * d).reshape(T, d)
+    w = O.uniform_f32(O.stream_seed(62, 0), d * (n + z), 1.0 / d).astype(np.float64).reshape(d, n + z)
+    st = P.RouterState(w, n, z, k, ke, 0.0, 1.0)
+    dg = P.route_topk(x, st)
+    w_in = [O.normal_f64(O.stream_seed(63, 2 * e), d * I).reshape(d, I) / np.sqrt(d)
+            for e in range(n)]
+    w_out = [O.normal_f64(O.stream_seed(63, 2 * e + 1), I * d).reshape(I, d) / np.sqrt(d)
+             for e in range(n)]
+    bank = P.ExpertBank(w_in, w_out, m=m, gamma_mode=gamma_mode, precision=P.PREC_F64_EXACT)
+    out = P.moe_forward(x, dg, bank, z, renormalize=renorm)
+    want = np.empty((T, d))
+    rc = O.orc().orc_moe_forward_f64(ptr(x), T, d, ptr(np.ascontiguousarray(dg.indices, np.uint32)),
+                                     ptr(np.ascontiguousarray(dg.gates)), k, n, z,
+                                     O.ptr_array(w_in), O.ptr_array(w_out), I, bank.gamma_ffn(),
+                                     bank.gamma_zero(), int(renorm), ptr(want))
+    assert rc == 0
+    assert (out.view(np.uint64) == want.view(np.uint64)).all(), \
+        int((out.view(np.uint64) != want.view(np.uint64)).sum())

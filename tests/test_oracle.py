@@ -246,6 +246,27 @@ def test_moe_forward_oracle_equals_reference(orc, ref, gm, m, renorm):
     assert (o1.view(np.uint32) == o2.view(np.uint32)).all()
 
 
+@pytest.mark.parametrize("gm,m", [(0, 1), (1, 2), (2, 3)])
+def test_moe_forward_f64_oracle_equals_reference(orc, ref, gm, m):
+    """moe_forward<double> (ExpertBank<double>): oracle == reference, bitwise."""
+    T, d, n, z, k, I = 40, 64, 6, 3, 3, 32
+    x = O.normal_f64(41, T * d).reshape(T, d)
+    rng = np.random.default_rng(7)
+    idx = np.stack([rng.choice(n + z, k, replace=False) for _ in range(T)]).astype(np.uint32).ravel()
+    g = rng.uniform(0.01, 0.5, T * k)
+    w_in = [O.normal_f64(50 + e, d * I).reshape(d, I) / 8 for e in range(n)]
+    w_out = [O.normal_f64(60 + e, I * d).reshape(I, d) / 8 for e in range(n)]
+    gf = 1.0 if gm == 2 else float(m)
+    gz = float(m) if gm == 1 else 1.0
+    o1 = np.empty((T, d))
+    assert orc.orc_moe_forward_f64(ptr(x), T, d, ptr(idx), ptr(g), k, n, z, ptr_array(w_in),
+                                   ptr_array(w_out), I, gf, gz, 0, ptr(o1)) == 0
+    o2 = np.empty_like(o1)
+    assert ref.ref_moe_forward_f64(ptr(x), T, d, ptr(idx), ptr(g), k, n, z, ptr_array(w_in),
+                                   ptr_array(w_out), I, m, gm, ptr(o2), 4) == 0
+    assert (o1.view(np.uint64) == o2.view(np.uint64)).all()
+
+
 def test_rmsnorm_oracle_equals_reference(orc, ref):
     x = O.normal_f32(3, 8 * 6144).reshape(8, 6144)
     g = O.uniform_f32(4, 6144, 0.1) + np.float32(1)

@@ -77,6 +77,9 @@ def check_sass(lib: str = LIB) -> dict:
     assert seq, "seq_gemm kernel missing from SASS"
     for n in seq:
         assert summary[n]["FFMA"] == 0, f"{n}: FFMA found in exact-order kernel"
+    # packed f32x2 is only ever used as separately rounded FMUL2 + FADD2 (the
+    # half-swap trick, f32x2.cuh); a fused FFMA2 anywhere would be a contraction
+    assert not re.search(r"\bFFMA2\b", sass), "FFMA2 found: an f32x2 mul+add was contracted"
     # the double-precision router projection: separately rounded DMUL + DADD
     for n in summary:
         if "router_f64_kernel" in n:

@@ -233,11 +233,13 @@ __global__ void __launch_bounds__((TM / RM) * (TN / RN)) seq_gemm_kernel(
             }
         };
 
-        float acc[RM][RN];
+        // acc2[i][q] = (c[i][2q+1], c[i][2q]): packed f32x2 chains, products
+        // added half-swapped (f32x2.cuh) -- same rounding as scalar mul + add
+        uint64_t acc2[RM][RN / 2];
 #pragma unroll
         for (int i = 0; i < RM; ++i)
 #pragma unroll
-            for (int j = 0; j < RN; ++j) acc[i][j] = 0.0f;
+            for (int q = 0; q < RN / 2; ++q) acc2[i][q] = 0;
 
         int buf = 0;
         load_regs(0);
@@ -247,39 +249,36 @@ __global__ void __launch_bounds__((TM / RM) * (TN / RN)) seq_gemm_kernel(
             const int kc = min(kSeqKC, K - k0);
             const bool more = k0 + kSeqKC < K;
             if (more) load_regs(k0 + kSeqKC);
-            if (kc == kSeqKC) {
-#pragma unroll 8
-                for (int k = 0; k < kSeqKC; ++k) {
-                    float av[RM];
-                    if constexpr (RM == 4) {
-                        const float4 a = *reinterpret_cast<const float4*>(&As[buf][k][RM * ty]);
-                        av[0] = a.x; av[1] = a.y; av[2] = a.z; av[3] = a.w;
-                    } else {
-                        const float2 a = *reinterpret_cast<const float2*>(&As[buf][k][RM * ty]);
-                        av[0] = a.x; av[1] = a.y;
-                    }
-                    const float4 b = *reinterpret_cast<const float4*>(&Bs[buf][k][RN * tx]);
-                    const float bv[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-                    for (int i = 0; i < RM; ++i)
-#pragma unroll
-                        for (int j = 0; j < RN; ++j)
-                            acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(av[i], bv[j]));
+#pragma unroll 4
+            for (int k = 0; k < kc; ++k) {
+                float av[RM];
+                if constexpr (RM == 4) {
+                    const float4 a = *reinterpret_cast<const float4*>(&As[buf][k][RM * ty]);
+                    av[0] = a.x; av[1] = a.y; av[2] = a.z; av[3] = a.w;
+                } else {
+                    const float2 a = *reinterpret_cast<const float2*>(&As[buf][k][RM * ty]);
+                    av[0] = a.x; av[1] = a.y;
                 }
-            } else {
-                for (int k = 0; k < kc; ++k) {
+                const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(&Bs[buf][k][RN * tx]);
+                const uint64_t bv[2] = {b.x, b.y};
 #pragma unroll
-                    for (int i = 0; i < RM; ++i)
+                for (int i = 0; i < RM; ++i)
 #pragma unroll
-                        for (int j = 0; j < RN; ++j)
-                            acc[i][j] = __fadd_rn(acc[i][j],
-                                                  __fmul_rn(As[buf][k][RM * ty + i], Bs[buf][k][RN * tx + j]));
-                }
+                    for (int q = 0; q < RN / 2; ++q)
+                        acc2[i][q] = f2_add_swapped(acc2[i][q], f2_mul_bcast(av[i], bv[q]));
             }
             if (more) store_smem(buf ^ 1);
             __syncthreads();
             buf ^= 1;
         }
+        float acc[RM][RN];
+#pragma unroll
+        for (int i = 0; i < RM; ++i)
+#pragma unroll
+            for (int q = 0; q < RN / 2; ++q) {
+                acc[i][2 * q] = f2_hi(acc2[i][q]);
+                acc[i][2 * q + 1] = f2_lo(acc2[i][q]);
+            }
         // Epilogue.
 #pragma unroll
         for (int i = 0; i < RM; ++i) {

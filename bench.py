@@ -241,7 +241,9 @@ def run_reference_arm(args):
     v = statistics.mean(vals)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+        "steps": args.steps, "warmup": args.warmup,
+        # the time this rate implies for one full 8192-token step of the workload
+        "ms_per_step": cfg["tokens"] / v * 1e3 if v else None,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (CounterRng normal inputs, seeded_init Uniform weights)",
         "config": {"workload": cfg["workload"], "tokens": cfg["tokens"], "d_model": D,

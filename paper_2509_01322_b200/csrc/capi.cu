@@ -13,6 +13,18 @@
 
 using namespace scmoe;
 
+namespace scmoe {
+void ensure_max_dynamic_smem(const void* kernel, int bytes, int device) {
+    static std::mutex mu;
+    static std::vector<std::pair<const void*, int>> done;
+    std::lock_guard<std::mutex> lock(mu);
+    for (const auto& kv : done)
+        if (kv.first == kernel && kv.second == device) return;
+    SCMOE_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done.emplace_back(kernel, device);
+}
+}  // namespace scmoe
+
 namespace {
 
 template <typename F>

@@ -454,12 +454,8 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
     // X: tiled boxes of 128 permuted rows, or single-row boxes for tile::gather4
     const CUtensorMap mx =
         make_map_2d(X, std::max<size_t>(x_rows, 1), K, x_row_ids ? 1 : 64, BK);
-    static bool attr_set = false;
-    if (!attr_set) {
-        SCMOE_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-        attr_set = true;
-    }
+    ensure_max_dynamic_smem(reinterpret_cast<const void*>(grouped_gemm_kernel), SMEM_BYTES,
+                            c->device);
     GemmArgs a;
     a.tiles = tiles;
     a.n_tiles = n_tiles_dev;

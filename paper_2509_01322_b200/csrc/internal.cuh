@@ -309,6 +309,11 @@ void launch_ep_localize(scmoe_ctx* c, const int* row_expert, size_t n, int offse
 void launch_gather_rows_bf16(scmoe_ctx* c, const __nv_bfloat16* src, size_t d, const int* rows,
                              size_t n_rows, __nv_bfloat16* dst);
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// the attribute belongs to the device context, and callers may drive several
+// devices from one process or thread.  Thread-safe.
+void ensure_max_dynamic_smem(const void* kernel, int bytes, int device);
+
 int grouped_gemm_tile_rows();
 void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_experts,
                               size_t M, size_t K, const __nv_bfloat16* X, size_t x_rows,

@@ -570,12 +570,8 @@ void launch_router_slab(scmoe_ctx* c, const float* X, const float* W, float* log
                         size_t K, size_t E) {
     constexpr size_t smem =
         sizeof(float) * 2 * (kSlabKC * (kSlabW + kSlabXStride) + kSlabRows * kSlabKC);
-    static bool attr = false;
-    if (!attr) {
-        SCMOE_CUDA(cudaFuncSetAttribute(router_slab_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    ensure_max_dynamic_smem(reinterpret_cast<const void*>(router_slab_kernel), (int)smem,
+                            c->device);
     router_slab_kernel<<<ceil_div(T, kSlabRows), kSlabThreads, smem, c->stream>>>(
         X, W, logits, (int)T, (int)K, (int)E);
     SCMOE_LAUNCH_CHECK(c);

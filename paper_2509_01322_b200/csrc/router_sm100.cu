@@ -251,12 +251,7 @@ static void launch_persistent(scmoe_ctx* c, const float* X, const float* W, floa
     constexpr int Rows = kRtTok * TG;
     constexpr size_t Smem = (size_t)S * ((KC * kRtW + Rows * KC + 31) / 32 * 32) * 4 + 2 * S * 8 + 128;
     auto kern = router_tma_persistent_kernel<TG, KC, S, LAG>;
-    static bool attr = false;
-    if (!attr) {
-        SCMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)Smem));
-        attr = true;
-    }
+    ensure_max_dynamic_smem(reinterpret_cast<const void*>(kern), (int)Smem, c->device);
     const CUtensorMap mw = make_tma_map_2d(W, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, sizeof(float), K, E,
                                            KC, kRtBox, CU_TENSOR_MAP_SWIZZLE_NONE);
     const CUtensorMap mx = make_tma_map_2d(X, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, sizeof(float), T, K,
@@ -276,12 +271,8 @@ bool router_tma_ok(size_t T, size_t K, size_t E, int num_sms) {
 
 void launch_router_tma(scmoe_ctx* c, const float* X, const float* W, float* logits, size_t T,
                        size_t K, size_t E) {
-    static bool attr = false;
-    if (!attr) {
-        SCMOE_CUDA(cudaFuncSetAttribute(router_tma_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRtSmem));
-        attr = true;
-    }
+    ensure_max_dynamic_smem(reinterpret_cast<const void*>(router_tma_kernel), (int)kRtSmem,
+                            c->device);
     const CUtensorMap mw = make_tma_map_2d(W, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, sizeof(float), K, E,
                                            kRtKC, kRtBox, CU_TENSOR_MAP_SWIZZLE_NONE);
     const CUtensorMap mx = make_tma_map_2d(X, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, sizeof(float), T, K,

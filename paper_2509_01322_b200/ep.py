@@ -362,6 +362,50 @@ class EPLayer:
                            "a2a_bytes_each_way": f["n_send"] * self.ops.shape.d * 2}
         return out, f["idx"], f["gates"], f["cnt"]
 
+    def forward_host_batches(self, a1s, a3s, outs, gain, T: int, renormalize: bool = False):
+        """Host tier for a stream of batches (pinned host tensors a1s / a3s in,
+        outs filled): the copy-in of batch i+1 and the copy-out of batch i-1
+        run on copy streams while batch i computes (device inputs double
+        buffered).  Returns the routing of every batch (device tensors)."""
+        stream = getattr(self.ops, "stream", torch.cuda.current_stream())
+        cin, cout = torch.cuda.Stream(), torch.cuda.Stream()
+        n = len(a1s)
+        dev = [dict(a1=torch.empty(a1s[0].shape, dtype=a1s[0].dtype, device="cuda"),
+                    a3=None if a3s is None else torch.empty(a3s[0].shape, dtype=a3s[0].dtype,
+                                                           device="cuda")) for _ in range(2)]
+        ev_in = [torch.cuda.Event() for _ in range(n)]
+        ev_used = [torch.cuda.Event() for _ in range(n)]
+        caller = torch.cuda.current_stream()
+        cin.wait_stream(caller)
+        cout.wait_stream(caller)
+
+        def copy_in(i):
+            with torch.cuda.stream(cin):
+                if i >= 2:
+                    cin.wait_event(ev_used[i - 2])  # the slot's inputs were read by batch i-2
+                b = dev[i % 2]
+                b["a1"].copy_(a1s[i], non_blocking=True)
+                if a3s is not None:
+                    b["a3"].copy_(a3s[i], non_blocking=True)
+                ev_in[i].record(cin)
+
+        routing = []
+        copy_in(0)
+        for i in range(n):
+            if i + 1 < n:
+                copy_in(i + 1)  # issued before forward(i), whose host sync would delay it
+            caller.wait_event(ev_in[i])
+            b = dev[i % 2]
+            out, idx, gates, cnt = self.forward(b["a1"], b["a3"], gain, T, renormalize)
+            ev_used[i].record(caller)
+            with torch.cuda.stream(cout):
+                cout.wait_event(ev_used[i])
+                outs[i].copy_(out.view(outs[i].shape), non_blocking=True)
+                out.record_stream(cout)
+            routing.append((idx, gates, cnt))
+        caller.wait_stream(cout)
+        return routing
+
     def forward_batches(self, a1s, a3s, gain, T: int, renormalize: bool = False,
                         corun_router: bool = False):
         """A stream of batches, pipelined (p2p transport): batch i+1's front half

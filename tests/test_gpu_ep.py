@@ -147,3 +147,59 @@ def test_ep_pipelined_batches_equal_serial(world):
         p.join(timeout=60)
     for rank, ok, info in sorted(res):
         assert ok, f"rank {rank}: {info}"
+
+
+def _host_batches_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", rank))
+    try:
+        import paper_2509_01322_b200 as P
+        from paper_2509_01322_b200.ep import EPLayer, GpuOps
+        from paper_2509_01322_b200.layer import LayerShape
+        shape = LayerShape(d=1024, n_ffn=64, n_zero=32, top_k=6, k_expected=4, inter=512,
+                           precision=P.PREC_BF16)
+        T, nb = 512 + 64 * rank, 3
+        a1 = [torch.from_numpy(P.fill_normal(P.stream_seed(70 + i, rank), T * shape.d)
+                               .reshape(T, shape.d)).pin_memory() for i in range(nb)]
+        a3 = [torch.from_numpy(P.fill_normal(P.stream_seed(80 + i, rank), T * shape.d)
+                               .reshape(T, shape.d)).pin_memory() for i in range(nb)]
+        ep = EPLayer(GpuOps(P.Context(rank), shape, rank, world, seed=3), transport="p2p")
+        outs = [torch.empty(T, shape.d).pin_memory() for _ in range(nb)]
+        ep.forward_host_batches(a1, a3, outs, None, T)
+        torch.cuda.synchronize()
+        ok = True
+        for i in range(nb):
+            ref = ep.forward(a1[i].cuda(), a3[i].cuda(), None, T)[0]
+            torch.cuda.synchronize()
+            ok = ok and torch.equal(ref.cpu(), outs[i])
+        q.put((rank, bool(ok), ""))
+    except Exception:  # pragma: no cover
+        import traceback
+        q.put((rank, False, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ep_host_batches_equal_device_calls():
+    """EPLayer.forward_host_batches (copy streams, double-buffered inputs) returns
+    exactly what per-batch device calls return."""
+    import torch
+    import torch.multiprocessing as mp
+    world = min(2, torch.cuda.device_count())
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29890 + os.getpid() % 40
+    procs = [ctx.Process(target=_host_batches_worker, args=(r, world, port, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, info in sorted(res):
+        assert ok, f"rank {rank}: {info}"

@@ -590,6 +590,7 @@ def run_b200_ep(args):
             ms = timed_ep(lambda: [ep.forward(a1, a3, None, T, chunks=chunks)
                                    for _ in range(args.steps)])
     launches = ctx.kernel_launches() + (ops.ctx_b.kernel_launches() if pipelined else 0) - l0
+    main_stats = dict(ep.last_stats)  # the headline workload's rows (config D overwrites)
     ms_max = max_over_ranks(ms, ws)
     value = T * ws / (ms_max / 1e3)
     # e2e: every step's H2D of its inputs and D2H of its output inside the
@@ -664,7 +665,7 @@ def run_b200_ep(args):
     g1 = stages.get("gemm1_tcgen05", (0.0, 1))
     g2 = stages.get("gemm2_tcgen05", (0.0, 1))
     t_gemm = (g1[0] + g2[0]) / max(1, g1[1])
-    slots_local = ep.last_stats["recv_rows"]
+    slots_local = main_stats["recv_rows"]
     flops = 4.0 * slots_local * D * INTER
     wbytes = 2 * n_local * D * INTER * 2
     tok_per_expert = slots_local / n_local
@@ -695,7 +696,7 @@ def run_b200_ep(args):
                                 "GEMMs + return + combine of batch i on another")
                    if pipelined else "serial",
                    "serial_ms_per_batch": ms_serial_max,
-                   "a2a_bytes_each_way_rank0": ep.last_stats["a2a_bytes_each_way"],
+                   "a2a_bytes_each_way_rank0": main_stats["a2a_bytes_each_way"],
                    "mean_ffn_per_token": float(ffn.size) / T},
         "e2e": {"value": T * ws / (e2e_ms / 1e3), "unit": "tokens/s",
                 "h2d_bytes_per_step": 2 * T * D * 4, "d2h_bytes_per_step": T * D * 4,
@@ -706,6 +707,9 @@ def run_b200_ep(args):
         "roofline": {"kernel": "grouped_gemm_bf16 (GEMM1+GEMM2, tcgen05), rank 0", "bound": bound,
                      "achieved": achieved, "peak": peak, "unit": unit,
                      "frac": achieved / peak if achieved else None, "traffic": None,
+                     "tflops": flops / (t_gemm / 1e3) / 1e12 if t_gemm else None,
+                     "weight_stream_gbs": wbytes / (t_gemm / 1e3) / 1e9 if t_gemm else None,
+                     "note": "bound = tensor above the bf16/HBM ridge (~254 tokens per expert)",
                      "tokens_per_local_expert": tok_per_expert, "ms_per_step": t_gemm},
         "stages_ms": {k: round(v[0] / v[1], 4) for k, v in stages.items()},
         "clocks": clk.summary(),

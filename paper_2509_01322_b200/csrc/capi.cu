@@ -1145,7 +1145,7 @@ int scmoe_dense_ffn(scmoe_ctx* c, scmoe_bank* b, const float* a1, const float* g
         if (T == 0) return;
         const size_t d = b->d, I = b->inter;
         Workspace& ws = c->ws;
-        const int tr = grouped_gemm_tile_rows();
+        const int tr = grouped_gemm_tile_rows_large();
         const size_t ntile = ceil_div(T, tr);
         __nv_bfloat16* xb = ws.dn_x.get<__nv_bfloat16>(T * d);
         __nv_bfloat16* h = ws.dn_h.get<__nv_bfloat16>(T * I);
@@ -1351,7 +1351,7 @@ void moe_rows_impl(scmoe_ctx* c, scmoe_bank* b, const void* x_bf16, const int* r
     PermResult pr;
     {
         ProfScope _p(c, "permute");
-        pr = launch_permute(c, loc, R, 1, n, n, grouped_gemm_tile_rows());
+        pr = launch_permute(c, loc, R, 1, n, n, grouped_gemm_tile_rows_large());
     }
     const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x_bf16);
     __nv_bfloat16* xp = ws.xp.get<__nv_bfloat16>(R * d);
@@ -1363,13 +1363,13 @@ void moe_rows_impl(scmoe_ctx* c, scmoe_bank* b, const void* x_bf16, const int* r
     {
         ProfScope _p(c, "gemm1_tcgen05");
         launch_grouped_gemm_bf16(c, b->w1t, n, I, d, xp, R, nullptr, h, 1, pr.tiles, pr.n_tiles,
-                                 pr.max_tiles, grouped_gemm_tile_rows());
+                                 pr.max_tiles, grouped_gemm_tile_rows_large());
     }
     if (row_dst) {
         // permuted row p holds received row row_token[p]
         ProfScope _p(c, "gemm2_tcgen05");
         launch_grouped_gemm_bf16(c, b->w2t, n, d, I, h, R, nullptr, nullptr, 0, pr.tiles,
-                                 pr.n_tiles, pr.max_tiles, grouped_gemm_tile_rows(), row_dst,
+                                 pr.n_tiles, pr.max_tiles, grouped_gemm_tile_rows_large(), row_dst,
                                  pr.row_token);
         return;
     }
@@ -1377,7 +1377,7 @@ void moe_rows_impl(scmoe_ctx* c, scmoe_bank* b, const void* x_bf16, const int* r
     {
         ProfScope _p(c, "gemm2_tcgen05");
         launch_grouped_gemm_bf16(c, b->w2t, n, d, I, h, R, nullptr, y, 0, pr.tiles, pr.n_tiles,
-                                 pr.max_tiles, grouped_gemm_tile_rows());
+                                 pr.max_tiles, grouped_gemm_tile_rows_large());
     }
     // back to the received order: y_out[r] = y[slot_pos[r]]
     ProfScope _p(c, "unpermute");

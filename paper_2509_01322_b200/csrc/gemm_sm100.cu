@@ -149,11 +149,24 @@ __device__ __forceinline__ void unit_map(int u, int mblocks, const TokenTile* ti
     t = first + local % n;
 }
 
+template <int kNT>
+constexpr int gemm_smem_bytes() {
+    return A_STAGES * A_STAGE_BYTES + B_STAGES * kNT * BK * 2 + 1024 + 256 + EPI_STAGE_BYTES;
+}
+
 // <= 64 registers: one GEMM CTA (352 threads) must leave room for the
 // co-resident router CTA (256 x 128 registers) on every SM sub-partition.
+// kNT = max tokens per tile: 192 (single-GPU prefill; 186 KB smem, fits next
+// to the router) or 256 (expert-parallel shards with 256+ tokens per expert:
+// one tile of 256 instead of two of 128, 210 KB smem, 2 x 256 TMEM columns).
+template <int kNT>
 __global__ void __maxnreg__(64)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_w,
                         const __grid_constant__ CUtensorMap map_x, const GemmArgs args) {
+    constexpr int NT = kNT;
+    constexpr int B_STAGE_BYTES = NT * BK * 2;
+    constexpr int RING_BYTES = A_STAGES * A_STAGE_BYTES + B_STAGES * B_STAGE_BYTES;
+    static_assert(SLABS * NT <= TMEM_COLS, "TMEM overflow");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -439,6 +452,7 @@ CUtensorMap make_map_2d(const void* base, uint64_t rows, uint64_t cols, uint32_t
 }  // namespace
 
 int grouped_gemm_tile_rows() { return NT; }
+int grouped_gemm_tile_rows_large() { return 256; }
 
 void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_experts, size_t M,
                               size_t K, const __nv_bfloat16* X, size_t x_rows, const int* x_row_ids,
@@ -446,7 +460,8 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
                               const int* n_tiles_dev, size_t max_tiles, int tile_rows,
                               const uint64_t* row_dst, const int* row_ids) {
     if (max_tiles == 0 || n_experts == 0) return;
-    SCMOE_CHECK_ARG(tile_rows == NT, SCMOE_ERR_INTERNAL, "gemm: tile rows must equal NT");
+    SCMOE_CHECK_ARG(tile_rows == 192 || tile_rows == 256, SCMOE_ERR_INTERNAL,
+                    "gemm: tile rows must be 192 or 256");
     SCMOE_CHECK_ARG(M % BM == 0 && K % BK == 0, SCMOE_ERR_DIMENSION,
                     "gemm: M must be a multiple of 256 and K of 64");
     // W in the blocked layout (internal.cuh wblk_index): a 2-D view of rows of BK elements
@@ -454,8 +469,6 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
     // X: tiled boxes of 128 permuted rows, or single-row boxes for tile::gather4
     const CUtensorMap mx =
         make_map_2d(X, std::max<size_t>(x_rows, 1), K, x_row_ids ? 1 : 64, BK);
-    ensure_max_dynamic_smem(reinterpret_cast<const void*>(grouped_gemm_kernel), SMEM_BYTES,
-                            c->device);
     GemmArgs a;
     a.tiles = tiles;
     a.n_tiles = n_tiles_dev;
@@ -472,7 +485,17 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
     const size_t units_max = max_tiles * (M / BM);
     const int grid = (int)std::min<size_t>(
         units_max, (size_t)(c->gemm_sms > 0 ? std::min(c->gemm_sms, c->num_sms) : c->num_sms));
-    grouped_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, c->stream>>>(mw, mx, a);
+    if (tile_rows == 256) {
+        constexpr int smem = gemm_smem_bytes<256>();
+        ensure_max_dynamic_smem(reinterpret_cast<const void*>(grouped_gemm_kernel<256>), smem,
+                                c->device);
+        grouped_gemm_kernel<256><<<grid, NUM_THREADS, smem, c->stream>>>(mw, mx, a);
+    } else {
+        constexpr int smem = gemm_smem_bytes<192>();
+        ensure_max_dynamic_smem(reinterpret_cast<const void*>(grouped_gemm_kernel<192>), smem,
+                                c->device);
+        grouped_gemm_kernel<192><<<grid, NUM_THREADS, smem, c->stream>>>(mw, mx, a);
+    }
     SCMOE_LAUNCH_CHECK(c);
 }
 

@@ -314,7 +314,8 @@ void launch_gather_rows_bf16(scmoe_ctx* c, const __nv_bfloat16* src, size_t d, c
 // devices from one process or thread.  Thread-safe.
 void ensure_max_dynamic_smem(const void* kernel, int bytes, int device);
 
-int grouped_gemm_tile_rows();
+int grouped_gemm_tile_rows();        // 192: single-GPU prefill (router co-residency)
+int grouped_gemm_tile_rows_large();  // 256: expert-parallel shards, dense FFN
 void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_experts,
                               size_t M, size_t K, const __nv_bfloat16* X, size_t x_rows,
                               const int* x_row_ids, __nv_bfloat16* out, int silu,

@@ -890,7 +890,16 @@ __global__ void ep_put_rows_kernel(const __nv_bfloat16* __restrict__ src, int d,
         const uint4* s = reinterpret_cast<const uint4*>(src + (size_t)send_token[j] * d);
         uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(peer_rows[dst]) +
                                             (size_t)pos * d);
-        for (int v = lane; v < vec; v += 32) o[v] = s[v];
+        // four loads in flight per lane before the (NVLink) stores
+        int v = lane;
+        for (; v + 96 < vec; v += 128) {
+            const uint4 q0 = s[v], q1 = s[v + 32], q2 = s[v + 64], q3 = s[v + 96];
+            o[v] = q0;
+            o[v + 32] = q1;
+            o[v + 64] = q2;
+            o[v + 96] = q3;
+        }
+        for (; v < vec; v += 32) o[v] = s[v];
         if (lane == 0) reinterpret_cast<int*>(peer_expert[dst])[pos] = send_expert[j];
     }
 }

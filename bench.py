@@ -579,13 +579,14 @@ def run_b200_ep(args):
     # headline: the pipelined batch stream (p2p transport)
     pipelined = args.ep_transport == "p2p" and args.schedule == "pipelined"
     if pipelined:  # untimed block of the timed block's shape (allocator steady state)
-        ep.forward_batches([a1] * args.steps, [a3] * args.steps, None, T)
+        ep.forward_batches([a1] * args.steps, [a3] * args.steps, None, T,
+                           corun_router=args.ep_corun)
         torch.cuda.synchronize()
     l0 = ctx.kernel_launches() + (ops.ctx_b.kernel_launches() if pipelined else 0)
     with ClockSampler(local) as clk:
         if pipelined:
             ms = timed_ep(lambda: ep.forward_batches([a1] * args.steps, [a3] * args.steps, None,
-                                                     T))
+                                                     T, corun_router=args.ep_corun))
         else:
             ms = timed_ep(lambda: [ep.forward(a1, a3, None, T, chunks=chunks)
                                    for _ in range(args.steps)])
@@ -741,6 +742,8 @@ def main():
     # p2p: dispatch stored straight into the peers' symmetric buffers over NVLink,
     # return fused into GEMM2's epilogue; nccl: all_to_all_single
     ap.add_argument("--ep-transport", default="p2p", choices=["p2p", "nccl"])
+    ap.add_argument("--ep-corun", action="store_true",
+                    help="pipelined EP: small router kernel co-resident with the GEMM")
     ap.add_argument("--ep-chunks", type=int, default=1,
                     help="EP software-pipeline depth (token chunks per step)")
     args = ap.parse_args()

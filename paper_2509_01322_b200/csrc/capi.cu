@@ -1338,6 +1338,18 @@ namespace {
 // Expert rows of the received slots; GEMM2's rows go to y (received order,
 // through an unpermute copy) or, with row_dst, straight to row_dst[r] for
 // received row r (e.g. the source rank's buffer over NVLink).
+// token-tile width of the expert-parallel GEMMs: 256 (default) or 192
+// (SCMOE_EP_TILE_ROWS=192: the smaller-footprint GEMM that the co-resident
+// router fits next to)
+int ep_tile_rows(const scmoe_ctx* c) {
+    (void)c;
+    static const int v = [] {
+        const char* e = getenv("SCMOE_EP_TILE_ROWS");
+        return e && atoi(e) == 192 ? 192 : 256;
+    }();
+    return v == 192 ? grouped_gemm_tile_rows() : grouped_gemm_tile_rows_large();
+}
+
 void moe_rows_impl(scmoe_ctx* c, scmoe_bank* b, const void* x_bf16, const int* row_expert,
                    int expert_offset, size_t R, void* y_bf16, const uint64_t* row_dst) {
     if (b->precision != SCMOE_PREC_BF16)
@@ -1351,7 +1363,7 @@ void moe_rows_impl(scmoe_ctx* c, scmoe_bank* b, const void* x_bf16, const int* r
     PermResult pr;
     {
         ProfScope _p(c, "permute");
-        pr = launch_permute(c, loc, R, 1, n, n, grouped_gemm_tile_rows_large());
+        pr = launch_permute(c, loc, R, 1, n, n, ep_tile_rows(c));
     }
     const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x_bf16);
     __nv_bfloat16* xp = ws.xp.get<__nv_bfloat16>(R * d);
@@ -1363,13 +1375,13 @@ void moe_rows_impl(scmoe_ctx* c, scmoe_bank* b, const void* x_bf16, const int* r
     {
         ProfScope _p(c, "gemm1_tcgen05");
         launch_grouped_gemm_bf16(c, b->w1t, n, I, d, xp, R, nullptr, h, 1, pr.tiles, pr.n_tiles,
-                                 pr.max_tiles, grouped_gemm_tile_rows_large());
+                                 pr.max_tiles, ep_tile_rows(c));
     }
     if (row_dst) {
         // permuted row p holds received row row_token[p]
         ProfScope _p(c, "gemm2_tcgen05");
         launch_grouped_gemm_bf16(c, b->w2t, n, d, I, h, R, nullptr, nullptr, 0, pr.tiles,
-                                 pr.n_tiles, pr.max_tiles, grouped_gemm_tile_rows_large(), row_dst,
+                                 pr.n_tiles, pr.max_tiles, ep_tile_rows(c), row_dst,
                                  pr.row_token);
         return;
     }
@@ -1377,7 +1389,7 @@ void moe_rows_impl(scmoe_ctx* c, scmoe_bank* b, const void* x_bf16, const int* r
     {
         ProfScope _p(c, "gemm2_tcgen05");
         launch_grouped_gemm_bf16(c, b->w2t, n, d, I, h, R, nullptr, y, 0, pr.tiles, pr.n_tiles,
-                                 pr.max_tiles, grouped_gemm_tile_rows_large());
+                                 pr.max_tiles, ep_tile_rows(c));
     }
     // back to the received order: y_out[r] = y[slot_pos[r]]
     ProfScope _p(c, "unpermute");

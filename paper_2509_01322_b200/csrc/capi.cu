@@ -104,7 +104,13 @@ void require_ctx(scmoe_ctx* c) {
 }
 
 int tile_rows_for(const scmoe_bank* b) {
-    return b->precision == SCMOE_PREC_BF16 ? grouped_gemm_tile_rows() : 64;
+    // single-GPU path: 192-token tiles (or SCMOE_TILE_ROWS=128 / 256)
+    static const int v = [] {
+        const char* e = getenv("SCMOE_TILE_ROWS");
+        const int x = e ? atoi(e) : 192;
+        return x == 128 || x == 256 ? x : 192;
+    }();
+    return b->precision == SCMOE_PREC_BF16 ? v : 64;
 }
 
 // The MoE block is split into a front half (permutation, and the row gather
@@ -1345,9 +1351,10 @@ int ep_tile_rows(const scmoe_ctx* c) {
     (void)c;
     static const int v = [] {
         const char* e = getenv("SCMOE_EP_TILE_ROWS");
-        return e && atoi(e) == 192 ? 192 : 256;
+        const int x = e ? atoi(e) : 256;
+        return x == 128 || x == 192 ? x : 256;
     }();
-    return v == 192 ? grouped_gemm_tile_rows() : grouped_gemm_tile_rows_large();
+    return v;
 }
 
 void moe_rows_impl(scmoe_ctx* c, scmoe_bank* b, const void* x_bf16, const int* row_expert,

@@ -167,6 +167,10 @@ __global__ void __maxnreg__(64)
     constexpr int B_STAGE_BYTES = NT * BK * 2;
     constexpr int RING_BYTES = A_STAGES * A_STAGE_BYTES + B_STAGES * B_STAGE_BYTES;
     static_assert(SLABS * NT <= TMEM_COLS, "TMEM overflow");
+    // accumulator buffers: two when both fit in TMEM (NT <= 128), so the
+    // epilogue of unit i drains one while the MMAs of unit i+1 fill the other
+    constexpr int ACC_COLS = SLABS * NT;
+    constexpr int NBUF = 2 * ACC_COLS <= TMEM_COLS ? 2 : 1;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -178,9 +182,9 @@ __global__ void __maxnreg__(64)
     uint64_t* a_empty = a_full + A_STAGES;
     uint64_t* b_full = a_empty + A_STAGES;
     uint64_t* b_empty = b_full + B_STAGES;
-    uint64_t* tfull = b_empty + B_STAGES;
-    uint64_t* tempty = tfull + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+    uint64_t* tfull = b_empty + B_STAGES;  // [NBUF]
+    uint64_t* tempty = tfull + NBUF;        // [NBUF]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -198,8 +202,10 @@ __global__ void __maxnreg__(64)
             mbar_init(&b_full[s], args.x_rows ? 32 : 1);
             mbar_init(&b_empty[s], 1);
         }
-        mbar_init(tfull, 1);
-        mbar_init(tempty, EPI_WARPS);
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], EPI_WARPS);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_w)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_x)) : "memory");
@@ -335,7 +341,8 @@ __global__ void __maxnreg__(64)
             const TokenTile tile = args.tiles[ti];
             const int n_eff = max(16, (tile.count + 15) & ~15);
             const uint32_t idesc = make_idesc(128, n_eff);
-            mbar_wait(tempty, (local & 1) ^ 1);
+            const int buf = local % NBUF;
+            mbar_wait(&tempty[buf], ((local / NBUF) & 1) ^ 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             for (int kb = 0; kb < kblocks; ++kb) {
                 mbar_wait(&a_full[as], aph);
@@ -350,7 +357,8 @@ __global__ void __maxnreg__(64)
 #pragma unroll
                         for (int s = 0; s < SLABS; ++s) {
                             const uint64_t adesc = make_desc_sw128(abase + s * A_SLAB_BYTES + k * 32);
-                            mma_bf16(tmem_base + s * NT, adesc, bdesc, idesc, (kb | k) != 0);
+                            mma_bf16(tmem_base + buf * ACC_COLS + s * NT, adesc, bdesc, idesc,
+                                     (kb | k) != 0);
                         }
                     }
                     mma_commit(&a_empty[as]);
@@ -366,7 +374,7 @@ __global__ void __maxnreg__(64)
                     bph ^= 1;
                 }
             }
-            if (lane == 0) mma_commit(tfull);
+            if (lane == 0) mma_commit(&tfull[buf]);
             __syncwarp();
         }
     } else {
@@ -389,10 +397,12 @@ __global__ void __maxnreg__(64)
             int ti, mb;
             unit_map(u, mblocks, args.tiles, ti, mb, args.debug);
             const TokenTile tile = args.tiles[ti];
-            mbar_wait(tfull, local & 1);
+            const int buf = local % NBUF;
+            mbar_wait(&tfull[buf], (local / NBUF) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             if (!(args.debug & 2)) {
-                const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + s * NT;
+                const uint32_t taddr =
+                    tmem_base + ((uint32_t)(quad * 32) << 16) + buf * ACC_COLS + s * NT;
                 for (int j0 = 0; j0 < tile.count; j0 += 32) {
                     uint32_t v[32];
                     tmem_ld32(taddr + j0, v);  // v[jj] = D[mb*BM + mrow + lane][j0 + jj]
@@ -429,7 +439,7 @@ __global__ void __maxnreg__(64)
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
-            if (lane == 0) mbar_arrive(tempty);
+            if (lane == 0) mbar_arrive(&tempty[buf]);
         }
     }
 
@@ -460,8 +470,8 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
                               const int* n_tiles_dev, size_t max_tiles, int tile_rows,
                               const uint64_t* row_dst, const int* row_ids) {
     if (max_tiles == 0 || n_experts == 0) return;
-    SCMOE_CHECK_ARG(tile_rows == 192 || tile_rows == 256, SCMOE_ERR_INTERNAL,
-                    "gemm: tile rows must be 192 or 256");
+    SCMOE_CHECK_ARG(tile_rows == 128 || tile_rows == 192 || tile_rows == 256, SCMOE_ERR_INTERNAL,
+                    "gemm: tile rows must be 128, 192 or 256");
     SCMOE_CHECK_ARG(M % BM == 0 && K % BK == 0, SCMOE_ERR_DIMENSION,
                     "gemm: M must be a multiple of 256 and K of 64");
     // W in the blocked layout (internal.cuh wblk_index): a 2-D view of rows of BK elements
@@ -485,7 +495,12 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
     const size_t units_max = max_tiles * (M / BM);
     const int grid = (int)std::min<size_t>(
         units_max, (size_t)(c->gemm_sms > 0 ? std::min(c->gemm_sms, c->num_sms) : c->num_sms));
-    if (tile_rows == 256) {
+    if (tile_rows == 128) {
+        constexpr int smem = gemm_smem_bytes<128>();
+        ensure_max_dynamic_smem(reinterpret_cast<const void*>(grouped_gemm_kernel<128>), smem,
+                                c->device);
+        grouped_gemm_kernel<128><<<grid, NUM_THREADS, smem, c->stream>>>(mw, mx, a);
+    } else if (tile_rows == 256) {
         constexpr int smem = gemm_smem_bytes<256>();
         ensure_max_dynamic_smem(reinterpret_cast<const void*>(grouped_gemm_kernel<256>), smem,
                                 c->device);

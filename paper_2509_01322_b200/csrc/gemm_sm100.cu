@@ -149,9 +149,17 @@ __device__ __forceinline__ void unit_map(int u, int mblocks, const TokenTile* ti
     t = first + local % n;
 }
 
+// epilogue staging buffers: two (chunk c+1 fills one while chunk c's bulk
+// copies still read the other) where the shared memory allows -- the 256-token
+// variant, which never shares the SM with the router
+template <int kNT>
+__host__ __device__ constexpr int gemm_epi_bufs() {
+    return kNT == 256 ? 2 : 1;
+}
 template <int kNT>
 constexpr int gemm_smem_bytes() {
-    return A_STAGES * A_STAGE_BYTES + B_STAGES * kNT * BK * 2 + 1024 + 256 + EPI_STAGE_BYTES;
+    return A_STAGES * A_STAGE_BYTES + B_STAGES * kNT * BK * 2 + 1024 + 256 +
+           gemm_epi_bufs<kNT>() * EPI_STAGE_BYTES;
 }
 
 // <= 64 registers: one GEMM CTA (352 threads) must leave room for the
@@ -389,7 +397,9 @@ __global__ void __maxnreg__(64)
         // by lane t < 4 of warp ew for token ew*4 + t.  The stores thus never
         // occupy the LSU, and a row past the tile end is simply not issued.
         // Named barrier 1 syncs the 8 epilogue warps.
-        unsigned char* stage = smem + RING_BYTES + 256;
+        unsigned char* stage0 = smem + RING_BYTES + 256;
+        constexpr int EPI_BUFS = gemm_epi_bufs<NT>();
+        int chunk = 0;  // running chunk counter: staging buffer = chunk % EPI_BUFS
         const int mrow = s * 128 + quad * 32;  // this warp's rows within the unit
         constexpr int ROWS_PER_WARP = 32 / EPI_WARPS;
         int local = 0;
@@ -403,12 +413,17 @@ __global__ void __maxnreg__(64)
             if (!(args.debug & 2)) {
                 const uint32_t taddr =
                     tmem_base + ((uint32_t)(quad * 32) << 16) + buf * ACC_COLS + s * NT;
-                for (int j0 = 0; j0 < tile.count; j0 += 32) {
+                for (int j0 = 0; j0 < tile.count; j0 += 32, ++chunk) {
+                    unsigned char* stage = stage0 + (chunk % EPI_BUFS) * EPI_STAGE_BYTES;
                     uint32_t v[32];
                     tmem_ld32(taddr + j0, v);  // v[jj] = D[mb*BM + mrow + lane][j0 + jj]
-                    // the previous chunk's bulk copies have read the staging
-                    if (lane < ROWS_PER_WARP)
-                        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    // the bulk copies that last read this staging buffer are done
+                    if (lane < ROWS_PER_WARP) {
+                        if constexpr (EPI_BUFS == 2)
+                            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                        else
+                            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    }
                     asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32) : "memory");
 #pragma unroll
                     for (int jj = 0; jj < 32; ++jj) {

@@ -9,6 +9,7 @@
 // popcount below its bit, and block offsets come from a scan over blocks.
 #include "internal.cuh"
 #include "libm_port.h"
+#include "sm100_util.cuh"
 
 namespace scmoe {
 
@@ -903,16 +904,82 @@ __global__ void ep_put_rows_kernel(const __nv_bfloat16* __restrict__ src, int d,
         if (lane == 0) reinterpret_cast<int*>(peer_expert[dst])[pos] = send_expert[j];
     }
 }
+// Same dispatch with the copy engine: per warp, lane 0 moves whole rows by
+// bulk async copies -- local row -> shared memory (mbarrier completion) ->
+// peer row over NVLink -- with two row buffers per warp, so the transfers
+// are single large transactions instead of 16-byte stores.
+constexpr int kPutWarps = 4;
+__global__ void __launch_bounds__(kPutWarps * 32) ep_put_rows_bulk_kernel(
+    const __nv_bfloat16* __restrict__ src, int d, const int* __restrict__ send_token,
+    const int* __restrict__ send_expert, int n_send, const int* __restrict__ send_start,
+    const int64_t* __restrict__ dst_offset, const uint64_t* __restrict__ peer_rows,
+    const uint64_t* __restrict__ peer_expert, int G) {
+    extern __shared__ __align__(128) unsigned char put_smem[];
+    __shared__ uint64_t bars[kPutWarps][2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t row_bytes = (uint32_t)d * 2;
+    unsigned char* buf = put_smem + (size_t)warp * 2 * row_bytes;
+    if (lane == 0) {
+        mbar_init(&bars[warp][0], 1);
+        mbar_init(&bars[warp][1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    if (lane != 0) return;
+    const int gw = blockIdx.x * kPutWarps + warp, nw = gridDim.x * kPutWarps;
+    uint32_t phase[2] = {0, 0};
+    int it = 0;
+    for (int j = gw; j < n_send; j += nw, ++it) {
+        const int b = it & 1;
+        unsigned char* sb = buf + b * row_bytes;
+        // the bulk store that last read this buffer (two rows ago) has read it
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        int dst = 0;
+        while (dst + 1 < G && send_start[dst + 1] <= j) ++dst;
+        const int64_t pos = dst_offset[dst] + (j - send_start[dst]);
+        mbar_expect_tx(&bars[warp][b], row_bytes);
+        asm volatile(
+            "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+                "r"(smem_u32(sb)),
+            "l"(reinterpret_cast<uint64_t>(src + (size_t)send_token[j] * d)), "r"(row_bytes),
+            "r"(smem_u32(&bars[warp][b]))
+            : "memory");
+        mbar_wait(&bars[warp][b], phase[b]);
+        phase[b] ^= 1;
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                         reinterpret_cast<uint64_t>(reinterpret_cast<__nv_bfloat16*>(peer_rows[dst]) +
+                                                    (size_t)pos * d)),
+                     "r"(smem_u32(sb)), "r"(row_bytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        reinterpret_cast<int*>(peer_expert[dst])[pos] = send_expert[j];
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 void launch_ep_put_rows(scmoe_ctx* c, const __nv_bfloat16* src, size_t d, const int* send_token,
                         const int* send_expert, size_t n_send, const int* send_start,
                         const int64_t* dst_offset, const uint64_t* peer_rows,
                         const uint64_t* peer_expert, int G) {
     if (n_send == 0) return;
     SCMOE_CHECK_ARG(d % 8 == 0, SCMOE_ERR_DIMENSION, "ep_put_rows: d must be a multiple of 8");
-    const int blocks = c->num_sms * 4;
-    ep_put_rows_kernel<<<blocks, 256, 0, c->stream>>>(src, (int)d, send_token, send_expert,
-                                                      (int)n_send, send_start, dst_offset,
-                                                      peer_rows, peer_expert, G);
+    // the warp-store kernel is the default: same NVLink rate as the bulk-copy
+    // one (1.11 ms for 604 MB at EP x4) and no shared memory, so it can share
+    // an SM with the expert GEMM of the previous batch (SCMOE_PUT_BULK=1)
+    static const bool bulk = getenv("SCMOE_PUT_BULK") != nullptr;
+    const size_t smem = (size_t)kPutWarps * 2 * d * 2;
+    if (bulk && smem <= 200 * 1024) {
+        ensure_max_dynamic_smem(reinterpret_cast<const void*>(ep_put_rows_bulk_kernel), (int)smem,
+                                c->device);
+        ep_put_rows_bulk_kernel<<<c->num_sms * 2, kPutWarps * 32, smem, c->stream>>>(
+            src, (int)d, send_token, send_expert, (int)n_send, send_start, dst_offset, peer_rows,
+            peer_expert, G);
+    } else {
+        const int blocks = c->num_sms * 4;
+        ep_put_rows_kernel<<<blocks, 256, 0, c->stream>>>(src, (int)d, send_token, send_expert,
+                                                          (int)n_send, send_start, dst_offset,
+                                                          peer_rows, peer_expert, G);
+    }
     SCMOE_LAUNCH_CHECK(c);
 }
 

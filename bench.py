@@ -663,6 +663,15 @@ def run_b200_ep(args):
         return
     peaks = measured_peaks() or {}
     n_local = N_FFN // ws
+    # the dispatch kernel's NVLink rate (rank 0): remote rows x row bytes / kernel time
+    dispatch = None
+    put = stages.get("ep_put_rows")
+    if put and "self_rows" in main_stats:
+        remote = (main_stats["send_rows"] - main_stats["self_rows"]) * D * 2
+        put_ms = put[0] / max(1, put[1])
+        dispatch = {"kernel": "ep_put_rows (peer stores over NVLink)", "remote_bytes": remote,
+                    "ms": put_ms, "gbs": remote / (put_ms / 1e3) / 1e9,
+                    "note": "the return all-to-all is inside GEMM2's epilogue (not separable)"}
     g1 = stages.get("gemm1_tcgen05", (0.0, 1))
     g2 = stages.get("gemm2_tcgen05", (0.0, 1))
     t_gemm = (g1[0] + g2[0]) / max(1, g1[1])
@@ -713,6 +722,7 @@ def run_b200_ep(args):
                      "note": "bound = tensor above the bf16/HBM ridge (~254 tokens per expert)",
                      "tokens_per_local_expert": tok_per_expert, "ms_per_step": t_gemm},
         "stages_ms": {k: round(v[0] / v[1], 4) for k, v in stages.items()},
+        "dispatch_nvlink": dispatch,
         "clocks": clk.summary(),
         "cpu_baseline": None,
         "config_d": config_d,

@@ -338,7 +338,8 @@ class EPLayer:
             st["recv_exp"][:n_recv].fill_(ops.first)
         st["h_recv"].barrier(channel=0)
         return dict(k=k, T=T, hmoe=hmoe, idx=idx, gates=gates, cnt=cnt, slot_pos=slot_pos,
-                    n_send=n_send, n_recv=n_recv, row_dst=row_dst, keep=[hb, send_token,
+                    n_send=n_send, n_recv=n_recv, self_rows=Mh[me][me], row_dst=row_dst,
+                    keep=[hb, send_token,
                                                                         send_expert])
 
     def _back_p2p(self, f, a3, renormalize, wait_residual=None, ctx=None):
@@ -358,7 +359,7 @@ class EPLayer:
         f = self._front_p2p(a1, gain, T)
         out = self._back_p2p(f, a3, renormalize, wait_residual)
         self.last_stats = {"send_rows": f["n_send"], "recv_rows": f["n_recv"], "chunks": 1,
-                           "transport": "p2p",
+                           "transport": "p2p", "self_rows": f["self_rows"],
                            "a2a_bytes_each_way": f["n_send"] * self.ops.shape.d * 2}
         return out, f["idx"], f["gates"], f["cnt"]
 
@@ -456,7 +457,7 @@ class EPLayer:
             res.append((outs[i], fronts[i]["idx"], fronts[i]["gates"], fronts[i]["cnt"]))
         f = fronts[-1]
         self.last_stats = {"send_rows": f["n_send"], "recv_rows": f["n_recv"], "chunks": 1,
-                           "transport": "p2p", "pipelined": True,
+                           "transport": "p2p", "pipelined": True, "self_rows": f["self_rows"],
                            "a2a_bytes_each_way": f["n_send"] * ops.shape.d * 2}
         return res
 

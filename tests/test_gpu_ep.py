@@ -12,7 +12,7 @@ sys.path.insert(0, ROOT)
 pytestmark = pytest.mark.gpu
 
 
-def _worker(rank, world, port, q, chunks=1, dense=False, transport="nccl"):
+def _worker(rank, world, port, q, chunks=1, dense=False, transport="nccl", renorm=False):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -34,7 +34,8 @@ def _worker(rank, world, port, q, chunks=1, dense=False, transport="nccl"):
         if dense:
             ops.enable_dense(rank, inter=1024, seed=7)
         ep = EPLayer(ops, transport=transport)
-        out, idx, gates, cnt = ep.forward(a1, a3, None, T, chunks=chunks, dense=dense)
+        out, idx, gates, cnt = ep.forward(a1, a3, None, T, chunks=chunks, dense=dense,
+                                          renormalize=renorm)
         torch.cuda.synchronize()
         # single-GPU reference: same seed => same router and the full expert set
         ctx1 = P.Context(rank)
@@ -51,7 +52,7 @@ def _worker(rank, world, port, q, chunks=1, dense=False, transport="nccl"):
         cnt1 = torch.empty_like(cnt)
         out1 = torch.empty_like(out)
         full.forward(a1.data_ptr(), a3.data_ptr(), None, T, idx1.data_ptr(), gates1.data_ptr(),
-                     cnt1.data_ptr(), out1.data_ptr())
+                     cnt1.data_ptr(), out1.data_ptr(), renormalize=renorm)
         torch.cuda.synchronize()
         ok = (torch.equal(idx, idx1) and torch.equal(gates, gates1) and torch.equal(out, out1))
         info = dict(ep.last_stats, idx_diff=int((idx != idx1).sum()),
@@ -195,6 +196,26 @@ def test_ep_host_batches_equal_device_calls():
     q = ctx.Queue()
     port = 29890 + os.getpid() % 40
     procs = [ctx.Process(target=_host_batches_worker, args=(r, world, port, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, info in sorted(res):
+        assert ok, f"rank {rank}: {info}"
+
+
+@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+def test_ep_renormalised_gates_bitwise(transport):
+    """Gate renormalisation (blocks.hpp:240-247) through the EP combine."""
+    import torch
+    import torch.multiprocessing as mp
+    world = min(2, torch.cuda.device_count())
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29810 + os.getpid() % 40 + (transport == "p2p")
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, 1, False, transport, True))
              for r in range(world)]
     for p in procs:
         p.start()

@@ -147,3 +147,42 @@ def test_host_batches_equal_serial_host_calls(scmoe):
         o = np.zeros((T, d), np.float32)
         layer.forward_host(a1[i], None, None, T, None, None, None, o)
         assert o.tobytes() == only[i].tobytes()
+
+
+def test_pipelined_batches_with_gain_and_renormalisation(scmoe):
+    """The pipelined schedule with a norm gain vector and gate renormalisation
+    (blocks.hpp:240-247) gives the serial results bit for bit."""
+    import torch
+    from paper_2509_01322_b200.layer import DeviceLayer, LayerShape
+    P = scmoe
+    ctx = P.Context(0)
+    shape = LayerShape(d=1024, n_ffn=64, n_zero=32, top_k=6, k_expected=4, inter=512,
+                       precision=P.PREC_BF16, m=2, gamma_mode=1)
+    layer = DeviceLayer(ctx, shape, seed=4)
+    T, nb = 640, 3
+    g = torch.from_numpy((1.0 + 0.1 * P.fill_normal(P.stream_seed(3, 9), shape.d)).astype(
+        np.float32)).cuda()
+    a1 = [torch.from_numpy(P.fill_normal(P.stream_seed(11, i), T * shape.d)).cuda() for i in range(nb)]
+    a3 = [torch.from_numpy(P.fill_normal(P.stream_seed(12, i), T * shape.d)).cuda() for i in range(nb)]
+
+    def bufs():
+        return dict(idx=torch.empty(T * shape.top_k, dtype=torch.int32, device="cuda"),
+                    gates=torch.empty(T * shape.top_k, dtype=torch.float64, device="cuda"),
+                    cnt=torch.empty(T, dtype=torch.int32, device="cuda"),
+                    out=torch.empty(T, shape.d, dtype=torch.float32, device="cuda"))
+
+    ser = [bufs() for _ in range(nb)]
+    for i in range(nb):
+        layer.forward(a1[i].data_ptr(), a3[i].data_ptr(), g.data_ptr(), T, ser[i]["idx"].data_ptr(),
+                      ser[i]["gates"].data_ptr(), ser[i]["cnt"].data_ptr(), ser[i]["out"].data_ptr(),
+                      renormalize=True)
+    ctx.synchronize()
+    pip = [bufs() for _ in range(nb)]
+    layer.forward_batches([a.data_ptr() for a in a1], [a.data_ptr() for a in a3], g.data_ptr(), T,
+                          [b["idx"].data_ptr() for b in pip], [b["gates"].data_ptr() for b in pip],
+                          [b["cnt"].data_ptr() for b in pip], [b["out"].data_ptr() for b in pip],
+                          renormalize=True)
+    ctx.synchronize()
+    for s, p in zip(ser, pip):
+        for k in ("idx", "gates", "cnt", "out"):
+            assert torch.equal(s[k], p[k]), k

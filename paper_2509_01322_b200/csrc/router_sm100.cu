@@ -295,8 +295,12 @@ bool router_corun_ok(size_t T, size_t K, size_t E) {
 // it co-resides with the persistent grouped GEMM of the previous batch.
 void launch_router_corun(scmoe_ctx* c, const float* X, const float* W, float* logits, size_t T,
                          size_t K, size_t E) {
-    launch_persistent<4, 4, 2, 1>(c, X, W, logits, T, K, E,
-                                  c->router_sms > 0 ? c->router_sms : c->num_sms);
+    static const int stages = getenv("SCMOE_CORUN_STAGES") ? atoi(getenv("SCMOE_CORUN_STAGES")) : 2;
+    const int ctas = c->router_sms > 0 ? c->router_sms : c->num_sms;
+    if (stages == 2)
+        launch_persistent<4, 4, 2, 1>(c, X, W, logits, T, K, E, ctas);
+    else
+        launch_persistent<4, 4, 3, 1>(c, X, W, logits, T, K, E, ctas);
 }
 
 }  // namespace scmoe

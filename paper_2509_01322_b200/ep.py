@@ -139,6 +139,38 @@ class GpuOps:
             self.stream_b = torch.cuda.Stream()
             self.ctx_b.set_stream(self.stream_b.cuda_stream)
 
+    # -- load-balancing controller (router.hpp:144-176) over the global batch --
+    def counters(self):
+        import numpy as np
+        E = self.shape.E
+        r = np.empty(E, np.uint64)
+        seen = C.c_uint64()
+        self._chk(lib().scmoe_router_get_counters_host(self.ctx.handle, self.router,
+                                                       r.ctypes.data_as(_P), C.byref(seen)))
+        return r, int(seen.value)
+
+    def set_counters(self, routed, seen: int):
+        import numpy as np
+        r = np.ascontiguousarray(routed, np.uint64)
+        self._chk(lib().scmoe_router_set_counters_host(self.ctx.handle, self.router,
+                                                       r.ctypes.data_as(_P), seen))
+
+    def accumulate(self, idx: torch.Tensor, T: int):
+        self._chk(lib().scmoe_accumulate_counters(self.ctx.handle, self.router, idx.data_ptr(), T))
+
+    def bias_update(self):
+        import numpy as np
+        delta = np.empty(self.shape.E, np.float64)
+        self._chk(lib().scmoe_bias_update(self.ctx.handle, self.router, delta.ctypes.data_as(_P)))
+        return delta
+
+    def bias(self):
+        import numpy as np
+        b = np.empty(self.shape.E, np.float64)
+        self._chk(lib().scmoe_router_get_bias_host(self.ctx.handle, self.router,
+                                                   b.ctypes.data_as(_P)))
+        return b
+
     def route(self, a1: torch.Tensor, gain: Optional[torch.Tensor], T: int):
         s = self.shape
         hmoe = torch.empty(T, s.d, dtype=torch.float32, device="cuda")
@@ -362,6 +394,26 @@ class EPLayer:
                            "transport": "p2p", "self_rows": f["self_rows"],
                            "a2a_bytes_each_way": f["n_send"] * self.ops.shape.d * 2}
         return out, f["idx"], f["gates"], f["cnt"]
+
+    def controller_step(self, idx: torch.Tensor, T: int, update: bool = True):
+        """accumulate_counters for this rank's routing, then (update=True) the
+        PID bias update over the GLOBAL batch: the per-expert
+        slot counters and tokens_seen are summed over the ranks (exact
+        integers), so every rank applies the same bias_update -- identical to a
+        single router that routed all ranks' tokens.  Returns the deltas."""
+        ops = self.ops
+        stream = getattr(ops, "stream", None)
+        if stream is not None:
+            stream.wait_stream(torch.cuda.current_stream())
+        ops.accumulate(idx, T)
+        if not update:
+            return None
+        routed, seen = ops.counters()  # synchronises the context's stream
+        t = torch.tensor(list(routed.astype("int64")) + [seen], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t, group=self.group)
+        tot = t.cpu().tolist()
+        ops.set_counters(tot[:-1], tot[-1])
+        return ops.bias_update()
 
     def forward_host_batches(self, a1s, a3s, outs, gain, T: int, renormalize: bool = False):
         """Host tier for a stream of batches (pinned host tensors a1s / a3s in,

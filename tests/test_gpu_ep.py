@@ -224,3 +224,79 @@ def test_ep_renormalised_gates_bitwise(transport):
         p.join(timeout=60)
     for rank, ok, info in sorted(res):
         assert ok, f"rank {rank}: {info}"
+
+
+def _controller_worker(rank, world, port, q):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", rank))
+    try:
+        import paper_2509_01322_b200 as P
+        from paper_2509_01322_b200.ep import EPLayer, GpuOps
+        from paper_2509_01322_b200.layer import DeviceLayer, LayerShape
+        shape = LayerShape(d=1024, n_ffn=64, n_zero=32, top_k=6, k_expected=3, inter=512,
+                           precision=P.PREC_BF16)
+        T = 512 + 128 * rank
+        ops = GpuOps(P.Context(rank), shape, rank, world, seed=3)
+        ep = EPLayer(ops, transport="p2p")
+        # a controller that moves: mu > 0 on every rank's replica of the router
+        lib = P.lib()
+        ops.ctx._check(lib.scmoe_router_set_mu(ops.ctx.handle, ops.router, 0.2, 0.999))
+        deltas, idxs = [], []
+        for step in range(3):
+            a1 = torch.from_numpy(P.fill_normal(P.stream_seed(90 + step, rank), T * shape.d)).cuda()
+            out, idx, gates, cnt = ep.forward(a1, None, None, T)
+            deltas.append(ep.controller_step(idx, T))
+            # every rank's routing of this step, for the single-router reference
+            sizes = [torch.zeros(1, dtype=torch.int64, device="cuda") for _ in range(world)]
+            dist.all_gather(sizes, torch.tensor([idx.numel()], device="cuda"))
+            parts = [torch.empty(int(s.item()), dtype=idx.dtype, device="cuda") for s in sizes]
+            dist.all_gather(parts, idx)
+            idxs.append([p_.cpu() for p_ in parts])
+        torch.cuda.synchronize()
+        # same bias on every rank
+        b = torch.from_numpy(ops.bias()).cuda()
+        b0 = b.clone()
+        dist.broadcast(b0, 0)
+        ok = torch.equal(b, b0)
+        # single router fed every rank's slots in rank order: identical deltas
+        ctx1 = P.Context(rank)
+        ref = DeviceLayer(ctx1, shape, seed=3, mu=0.2, mu_decay=0.999)
+        for step in range(3):
+            for part in idxs[step]:
+                ref.accumulate(part.cuda().data_ptr(), part.numel() // shape.top_k)
+            d_ref = ref.bias_update()
+            ok = ok and d_ref.tobytes() == deltas[step].tobytes()
+        ok = ok and ref.bias().tobytes() == ops.bias().tobytes()
+        q.put((rank, bool(ok), ""))
+    except Exception:  # pragma: no cover
+        import traceback
+        q.put((rank, False, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ep_controller_global_batch_bitwise():
+    """the bias controller under EP sums the per-expert counters
+    and tokens over the ranks; every rank's bias_update equals one router's
+    update over all ranks' slots, bit for bit."""
+    import torch
+    import torch.multiprocessing as mp
+    world = min(2, torch.cuda.device_count())
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29850 + os.getpid() % 40
+    procs = [ctx.Process(target=_controller_worker, args=(r, world, port, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, info in sorted(res):
+        assert ok, f"rank {rank}: {info}"

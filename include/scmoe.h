@@ -323,6 +323,48 @@ int scmoe_combine_rows(scmoe_ctx* ctx, scmoe_bank* b, const float* x, const void
                        size_t tokens, size_t top_k, size_t n_ffn_total, int renormalize,
                        const float* residual, float* out);
 
+/* ---- Multi-head latent attention, forward value, S = float (f2 row) --------
+ * MlaParams<float> (blocks.hpp:38-58); mla_block forward (blocks.hpp:73-102)
+ * over packed sequences; MlaCache + mla_infer_step (blocks.hpp:106-181).
+ * Bitwise equal to the reference (sequential-k fp32 projections, exact rope,
+ * causal attention with the glibc-expf restatement and in-order sums).
+ * Weights are row-major Parameter values: w_dq [d,dq], w_uq [dq,H*dhc],
+ * w_qr [dq,H*dhr], w_dkv [d,dkv], w_uk [dkv,H*dhc], w_uv [dkv,H*dhc],
+ * w_kr [d,dhr], w_o [H*dhc,d].  Errors: ParameterError for zero d/dq/dkv
+ * (mla_scale_factors, blocks.hpp:21-22); DimensionError for H = 0 or odd dhr
+ * (tensor.hpp:202-204) and rows not packing whole sequences (graph.hpp:404);
+ * StateError when the cache length differs from the position (blocks.hpp:135-137). */
+typedef struct scmoe_mla scmoe_mla;
+typedef struct scmoe_mla_cache scmoe_mla_cache;
+enum {
+    SCMOE_MLA_W_DQ = 0, SCMOE_MLA_W_UQ = 1, SCMOE_MLA_W_QR = 2, SCMOE_MLA_W_DKV = 3,
+    SCMOE_MLA_W_UK = 4, SCMOE_MLA_W_UV = 5, SCMOE_MLA_W_KR = 6, SCMOE_MLA_W_O = 7
+};
+int scmoe_mla_create(scmoe_ctx* ctx, size_t d_model, size_t d_q, size_t d_kv, size_t n_heads,
+                     size_t d_head_c, size_t d_head_r, double rope_base,
+                     int variance_alignment, scmoe_mla** out);
+int scmoe_mla_destroy(scmoe_ctx* ctx, scmoe_mla* m);
+/* which = SCMOE_MLA_W_*; w is that matrix, row-major, host / device. */
+int scmoe_mla_set_weight_host(scmoe_ctx* ctx, scmoe_mla* m, int which, const float* w);
+int scmoe_mla_set_weight(scmoe_ctx* ctx, scmoe_mla* m, int which, const float* w_dev);
+/* out [rows, d] = mla_block(h [rows, d], seq_len) value (stream-ordered). */
+int scmoe_mla_forward(scmoe_ctx* ctx, scmoe_mla* m, const float* h_dev, size_t rows,
+                      size_t seq_len, float* out_dev);
+int scmoe_mla_forward_host(scmoe_ctx* ctx, scmoe_mla* m, const float* h, size_t rows,
+                           size_t seq_len, float* out);
+int scmoe_mla_cache_create(scmoe_ctx* ctx, scmoe_mla* m, size_t capacity_hint,
+                           scmoe_mla_cache** out);
+int scmoe_mla_cache_destroy(scmoe_ctx* ctx, scmoe_mla_cache* cache);
+int scmoe_mla_cache_length(scmoe_ctx* ctx, scmoe_mla_cache* cache, size_t* length);
+/* c_kv [len, d_kv] and the rotated k_r [len, d_head_r] (either may be NULL). */
+int scmoe_mla_cache_read_host(scmoe_ctx* ctx, scmoe_mla* m, scmoe_mla_cache* cache, float* c_kv,
+                              float* k_r);
+/* out [1, d] = mla_infer_step(h_t [1, d], position); appends to the cache. */
+int scmoe_mla_infer_step(scmoe_ctx* ctx, scmoe_mla* m, scmoe_mla_cache* cache,
+                         const float* h_t_dev, size_t position, float* out_dev);
+int scmoe_mla_infer_step_host(scmoe_ctx* ctx, scmoe_mla* m, scmoe_mla_cache* cache,
+                              const float* h_t, size_t position, float* out);
+
 /* ---- CounterRng (rng.hpp:15-64), host side, for synthetic inputs --------- */
 uint64_t scmoe_rng_stream_seed(uint64_t seed, uint64_t id);
 /* out[i] = (float) CounterRng(seed).normal_at(first + i)  (router.hpp:357-360) */

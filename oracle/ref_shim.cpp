@@ -295,4 +295,79 @@ int ref_simulate_bias_control_f32(const float* w, std::size_t d, std::size_t n, 
     });
 }
 
+// ---- MLA (blocks.hpp:38-181), S = float ---------------------------------------
+// w[8] = w_dq, w_uq, w_qr, w_dkv, w_uk, w_uv, w_kr, w_o (row-major Parameter values).
+struct RefMla {
+    std::vector<Parameter<float>> store;
+    MlaParams<float> p;
+    RefMla(std::size_t d, std::size_t dq, std::size_t dkv, std::size_t H, std::size_t dhc,
+           std::size_t dhr, double base, int va, const float* const* w) {
+        p.d_model = d; p.d_q = dq; p.d_kv = dkv; p.n_heads = H; p.d_head_c = dhc;
+        p.d_head_r = dhr; p.rope_base = base; p.variance_alignment = va != 0;
+        const std::size_t shp[8][2] = {{d, dq}, {dq, H * dhc}, {dq, H * dhr}, {d, dkv},
+                                       {dkv, H * dhc}, {dkv, H * dhc}, {d, dhr}, {H * dhc, d}};
+        store.reserve(8);
+        for (int i = 0; i < 8; ++i)
+            store.emplace_back("w", ParamClass::Hidden, wrap(w[i], shp[i][0], shp[i][1]));
+        p.w_dq = &store[0]; p.w_uq = &store[1]; p.w_qr = &store[2]; p.w_dkv = &store[3];
+        p.w_uk = &store[4]; p.w_uv = &store[5]; p.w_kr = &store[6]; p.w_o = &store[7];
+    }
+};
+
+// mla_block forward value (blocks.hpp:73-102) over packed sequences; sequences
+// are independent, so `threads` shards them (bitwise the monolithic call).
+int ref_mla_forward_f32(std::size_t d, std::size_t dq, std::size_t dkv, std::size_t H,
+                        std::size_t dhc, std::size_t dhr, double base, int va,
+                        const float* const* w, const float* h, std::size_t rows,
+                        std::size_t seq_len, float* out, int threads) {
+    auto run = [&](std::size_t s0, std::size_t n_rows) {
+        RefMla m(d, dq, dkv, H, dhc, dhr, base, va, w);
+        Graph<float> g;
+        auto hv = g.input(wrap(h + s0 * d, n_rows, d));
+        MlaVars<float> v{g.input(m.p.w_dq->value), g.input(m.p.w_uq->value),
+                         g.input(m.p.w_qr->value), g.input(m.p.w_dkv->value),
+                         g.input(m.p.w_uk->value), g.input(m.p.w_uv->value),
+                         g.input(m.p.w_kr->value), g.input(m.p.w_o->value)};
+        auto u = mla_block(g, hv, m.p, v, seq_len);
+        std::memcpy(out + s0 * d, g.val(u).data.data(), n_rows * d * sizeof(float));
+    };
+    // malformed packing: one monolithic call raises the reference's own error
+    if (seq_len == 0 || rows % seq_len != 0) return guarded([&] { run(0, rows); });
+    return sharded(rows / seq_len, threads, [&](std::size_t s0, std::size_t s1) {
+        run(s0 * seq_len, (s1 - s0) * seq_len);
+    });
+}
+
+// mla_infer_step (blocks.hpp:129-181) for positions 0..T-1 of one sequence;
+// returns every step's output and the final compressed cache.
+int ref_mla_infer_f32(std::size_t d, std::size_t dq, std::size_t dkv, std::size_t H,
+                      std::size_t dhc, std::size_t dhr, double base, int va,
+                      const float* const* w, const float* h, std::size_t T, float* out,
+                      float* c_kv, float* k_r) {
+    return guarded([&] {
+        RefMla m(d, dq, dkv, H, dhc, dhr, base, va, w);
+        MlaCache<float> cache;
+        for (std::size_t t = 0; t < T; ++t) {
+            auto u = mla_infer_step(m.p, cache, wrap(h + t * d, 1, d), t);
+            std::memcpy(out + t * d, u.data.data(), d * sizeof(float));
+        }
+        if (c_kv && T) std::memcpy(c_kv, cache.c_kv.data.data(), T * dkv * sizeof(float));
+        if (k_r && T && dhr) std::memcpy(k_r, cache.k_r.data.data(), T * dhr * sizeof(float));
+    });
+}
+
+// One mla_infer_step with a cache of `cache_len` rows (the StateError check).
+int ref_mla_infer_position_check(std::size_t cache_len, std::size_t position) {
+    return guarded([&] {
+        const float* w[8] = {nullptr};
+        std::vector<float> z(64 * 64, 0.0f);
+        for (auto& p : w) p = z.data();
+        RefMla m(8, 4, 4, 1, 4, 2, 1.0e4, 1, w);
+        MlaCache<float> cache;
+        for (std::size_t t = 0; t < cache_len; ++t)
+            mla_infer_step(m.p, cache, Tensor<float>({1, 8}), t);
+        mla_infer_step(m.p, cache, Tensor<float>({1, 8}), position);
+    });
+}
+
 }  // extern "C"

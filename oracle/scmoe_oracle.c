@@ -508,3 +508,144 @@ int orc_simulate_bias_control_f32(const float* w, size_t d, size_t n_ffn, size_t
     free(delta);
     return rc;
 }
+
+/* ------------------------------------------------------------------------
+ * MLA, S = float -- blocks.hpp:19-26 (mla_scale_factors), :38-58 (MlaParams),
+ * :73-102 (mla_block forward value), :129-181 (mla_infer_step);
+ * tensor.hpp:197-224 (rope_apply); graph.hpp:396-434 (attention forward).
+ * w[8] = w_dq [d,dq], w_uq [dq,H*dhc], w_qr [dq,H*dhr], w_dkv [d,dkv],
+ * w_uk [dkv,H*dhc], w_uv [dkv,H*dhc], w_kr [d,dhr], w_o [H*dhc,d].
+ * ---------------------------------------------------------------------- */
+static int orc_mla_check(size_t d, size_t dq, size_t dkv, size_t heads, size_t dhr) {
+    if (d == 0 || dq == 0 || dkv == 0) return ORC_PARAMETER; /* blocks.hpp:21-22 */
+    if (heads == 0) return ORC_DIMENSION;                    /* tensor.hpp:202 */
+    if (dhr % 2 != 0) return ORC_DIMENSION;                  /* tensor.hpp:204 */
+    return ORC_OK;
+}
+
+/* rope_apply rows of x [rows, heads*hd] in place at positions pos[r]. */
+static void orc_rope_f32(float* x, size_t ld, size_t rows, size_t heads, size_t hd,
+                         const size_t* pos, double base) {
+    for (size_t r = 0; r < rows; ++r) {
+        const double p0 = (double)pos[r];
+        float* row = x + r * ld;
+        for (size_t h = 0; h < heads; ++h)
+            for (size_t p = 0; p < hd / 2; ++p) {
+                const double theta = p0 * pow(base, -2.0 * (double)p / (double)hd);
+                const float c = (float)cos(theta), s = (float)sin(theta);
+                const float a = row[h * hd + 2 * p], b = row[h * hd + 2 * p + 1];
+                row[h * hd + 2 * p] = a * c - b * s;
+                row[h * hd + 2 * p + 1] = a * s + b * c;
+            }
+    }
+}
+
+/* The per-row projections shared by both paths: cq, ckv (scaled), qc, qr
+ * (rotated), kr (rotated), at positions pos[r]. */
+static void orc_mla_project(const float* const* w, size_t d, size_t dq, size_t dkv, size_t heads,
+                            size_t dhc, size_t dhr, double base, int va, const float* h,
+                            size_t rows, const size_t* pos, float* ckv, float* qc, float* qr,
+                            float* kr) {
+    const float aq = va ? (float)sqrt((double)d / (double)dq) : 1.0f;
+    const float akv = va ? (float)sqrt((double)d / (double)dkv) : 1.0f;
+    float* cq = (float*)malloc(ORC_NZ(rows * dq) * sizeof(float));
+    orc_mm_f32(h, w[0], cq, rows, d, dq);
+    for (size_t i = 0; i < rows * dq; ++i) cq[i] *= aq;
+    orc_mm_f32(h, w[3], ckv, rows, d, dkv);
+    for (size_t i = 0; i < rows * dkv; ++i) ckv[i] *= akv;
+    orc_mm_f32(cq, w[1], qc, rows, dq, heads * dhc);
+    orc_mm_f32(cq, w[2], qr, rows, dq, heads * dhr);
+    orc_rope_f32(qr, heads * dhr, rows, heads, dhr, pos, base);
+    orc_mm_f32(h, w[6], kr, rows, d, dhr);
+    orc_rope_f32(kr, dhr, rows, 1, dhr, pos, base);
+    free(cq);
+}
+
+/* Causal attention of query rows (absolute positions q0+i) against keys
+ * 0..q0+i of one sequence, head by head, into merged [nq, H*dhc]
+ * (graph.hpp:396-434; identical arithmetic in blocks.hpp:155-179). */
+static void orc_mla_attend(size_t heads, size_t dhc, size_t dhr, const float* qc, const float* qr,
+                           size_t nq, size_t q0, const float* kc, const float* vv,
+                           const float* kr, float* merged) {
+    const float scale = (float)(1.0 / sqrt((double)(dhc + dhr)));
+    float* att = (float*)malloc(ORC_NZ(q0 + nq) * sizeof(float));
+    for (size_t i = 0; i < nq; ++i)
+        for (size_t h = 0; h < heads; ++h) {
+            const size_t n = q0 + i + 1;
+            float mx = 0.0f;
+            for (size_t j = 0; j < n; ++j) {
+                float acc = 0.0f;
+                for (size_t t = 0; t < dhc; ++t)
+                    acc += qc[i * heads * dhc + h * dhc + t] * kc[j * heads * dhc + h * dhc + t];
+                for (size_t t = 0; t < dhr; ++t)
+                    acc += qr[i * heads * dhr + h * dhr + t] * kr[j * dhr + t];
+                att[j] = acc * scale;
+                mx = (j == 0 || att[j] > mx) ? att[j] : mx;
+            }
+            float denom = 0.0f;
+            for (size_t j = 0; j < n; ++j) {
+                att[j] = expf(att[j] - mx);
+                denom += att[j];
+            }
+            float* o = merged + i * heads * dhc + h * dhc;
+            for (size_t t = 0; t < dhc; ++t) o[t] = 0.0f;
+            for (size_t j = 0; j < n; ++j) {
+                const float wj = att[j] / denom;
+                for (size_t t = 0; t < dhc; ++t) o[t] += wj * vv[j * heads * dhc + h * dhc + t];
+            }
+        }
+    free(att);
+}
+
+/* mla_block forward value over packed sequences of seq_len rows. */
+int orc_mla_forward_f32(size_t d, size_t dq, size_t dkv, size_t heads, size_t dhc, size_t dhr,
+                        double base, int va, const float* const* w, const float* h, size_t rows,
+                        size_t seq_len, float* out) {
+    int rc = orc_mla_check(d, dq, dkv, heads, dhr);
+    if (rc) return rc;
+    if (seq_len == 0 || rows % seq_len != 0) return ORC_DIMENSION; /* graph.hpp:404 */
+    size_t* pos = (size_t*)malloc(ORC_NZ(rows) * sizeof(size_t));
+    for (size_t r = 0; r < rows; ++r) pos[r] = r % seq_len; /* blocks.hpp:64-68 */
+    float* ckv = (float*)malloc(ORC_NZ(rows * dkv) * sizeof(float));
+    float* qc = (float*)malloc(ORC_NZ(rows * heads * dhc) * sizeof(float));
+    float* qr = (float*)malloc(ORC_NZ(rows * heads * dhr) * sizeof(float));
+    float* kr = (float*)malloc(ORC_NZ(rows * dhr) * sizeof(float));
+    float* kc = (float*)malloc(ORC_NZ(rows * heads * dhc) * sizeof(float));
+    float* vv = (float*)malloc(ORC_NZ(rows * heads * dhc) * sizeof(float));
+    float* merged = (float*)malloc(ORC_NZ(rows * heads * dhc) * sizeof(float));
+    orc_mla_project(w, d, dq, dkv, heads, dhc, dhr, base, va, h, rows, pos, ckv, qc, qr, kr);
+    orc_mm_f32(ckv, w[4], kc, rows, dkv, heads * dhc);
+    orc_mm_f32(ckv, w[5], vv, rows, dkv, heads * dhc);
+    for (size_t s0 = 0; s0 < rows; s0 += seq_len)
+        orc_mla_attend(heads, dhc, dhr, qc + s0 * heads * dhc, qr + s0 * heads * dhr, seq_len, 0,
+                       kc + s0 * heads * dhc, vv + s0 * heads * dhc, kr + s0 * dhr,
+                       merged + s0 * heads * dhc);
+    orc_mm_f32(merged, w[7], out, rows, heads * dhc, d);
+    free(pos); free(ckv); free(qc); free(qr); free(kr); free(kc); free(vv); free(merged);
+    return ORC_OK;
+}
+
+/* mla_infer_step for positions 0..T-1 of one sequence: out [T,d] and the
+ * final cache (c_kv [T,dkv], k_r [T,dhr]).  Each step re-expands the whole
+ * cache as the reference does (blocks.hpp:149-150). */
+int orc_mla_infer_f32(size_t d, size_t dq, size_t dkv, size_t heads, size_t dhc, size_t dhr,
+                      double base, int va, const float* const* w, const float* h, size_t T,
+                      float* out, float* c_kv, float* k_r) {
+    int rc = orc_mla_check(d, dq, dkv, heads, dhr);
+    if (rc) return rc;
+    float* qc = (float*)malloc(ORC_NZ(heads * dhc) * sizeof(float));
+    float* qr = (float*)malloc(ORC_NZ(heads * dhr) * sizeof(float));
+    float* kc = (float*)malloc(ORC_NZ(T * heads * dhc) * sizeof(float));
+    float* vv = (float*)malloc(ORC_NZ(T * heads * dhc) * sizeof(float));
+    float* merged = (float*)malloc(ORC_NZ(heads * dhc) * sizeof(float));
+    for (size_t t = 0; t < T; ++t) {
+        orc_mla_project(w, d, dq, dkv, heads, dhc, dhr, base, va, h + t * d, 1, &t,
+                        c_kv + t * dkv, qc, qr, k_r + t * dhr);
+        orc_mm_f32(c_kv, w[4], kc, t + 1, dkv, heads * dhc);
+        orc_mm_f32(c_kv, w[5], vv, t + 1, dkv, heads * dhc);
+        orc_mla_attend(heads, dhc, dhr, qc, qr, 1, t, kc, vv, k_r, merged);
+        orc_mm_f32(merged, w[7], out + t * d, 1, heads * dhc, d);
+    }
+    free(qc); free(qr); free(kc); free(vv); free(merged);
+    return ORC_OK;
+}

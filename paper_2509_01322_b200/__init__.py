@@ -170,6 +170,18 @@ _PROTOS = {
                                       C.POINTER(_U64)]),
     "scmoe_debug_expf": (C.c_int, [_P, _P, _P, _SZ]),
     "scmoe_debug_expf_range": (C.c_int, [_P, C.c_uint32, _P, _SZ]),
+    "scmoe_mla_create": (C.c_int, [_P] + [_SZ] * 6 + [C.c_double, C.c_int, _P]),
+    "scmoe_mla_destroy": (C.c_int, [_P, _P]),
+    "scmoe_mla_set_weight_host": (C.c_int, [_P, _P, C.c_int, _P]),
+    "scmoe_mla_set_weight": (C.c_int, [_P, _P, C.c_int, _P]),
+    "scmoe_mla_forward": (C.c_int, [_P, _P, _P, _SZ, _SZ, _P]),
+    "scmoe_mla_forward_host": (C.c_int, [_P, _P, _P, _SZ, _SZ, _P]),
+    "scmoe_mla_cache_create": (C.c_int, [_P, _P, _SZ, _P]),
+    "scmoe_mla_cache_destroy": (C.c_int, [_P, _P]),
+    "scmoe_mla_cache_length": (C.c_int, [_P, _P, C.POINTER(_SZ)]),
+    "scmoe_mla_cache_read_host": (C.c_int, [_P, _P, _P, _P, _P]),
+    "scmoe_mla_infer_step": (C.c_int, [_P, _P, _P, _P, _SZ, _P]),
+    "scmoe_mla_infer_step_host": (C.c_int, [_P, _P, _P, _P, _SZ, _P]),
 }
 
 

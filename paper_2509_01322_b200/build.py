@@ -33,6 +33,7 @@ SOURCES = {
     "kernels_router.cu": ["--fmad=false"],
     "router_sm100.cu": ["--fmad=false", "-Xptxas", "-O1"],
     "kernels_moe.cu": ["--fmad=false"],
+    "mla.cu": ["--fmad=false"],
     "capi.cu": [],
     "gemm_sm100.cu": ["-Xptxas", "-v"],
 }
@@ -74,6 +75,7 @@ def check_sass(lib: str = LIB) -> dict:
     # correctly rounded IEEE division (__fdiv_rn) inside the logistic.
     seq = [n for n in summary if re.search(r"seq_gemm_kernel.*Lb0EE", n)]
     seq += [n for n in summary if re.search(r"router_(tma|slab|lean)_kernel", n)]
+    seq += [n for n in summary if re.search(r"mla_(scores|pv|scale_rope)_kernel", n)]
     assert seq, "seq_gemm kernel missing from SASS"
     for n in seq:
         assert summary[n]["FFMA"] == 0, f"{n}: FFMA found in exact-order kernel"

@@ -4,8 +4,11 @@
 // (router.hpp:45-61, :112, :157-162; blocks.hpp:237-238, :348, :375-377);
 // all numeric work is done by the CUDA kernels.  There is no CPU compute
 // path: without a device every entry point fails with SCMOE_ERR_CUDA.
+#include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <mutex>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -1450,3 +1453,316 @@ int scmoe_combine_rows(scmoe_ctx* c, scmoe_bank* b, const float* x, const void* 
 }
 
 }  // extern "C"
+
+// ===========================================================================
+// MLA, forward value (f2 row): blocks.hpp:38-181.
+// ===========================================================================
+namespace {
+
+void mla_check_dims(size_t d, size_t dq, size_t dkv, size_t H, size_t dhr) {
+    if (d == 0 || dq == 0 || dkv == 0)
+        SCMOE_THROW(SCMOE_ERR_PARAMETER, "mla_scale_factors: dims must be positive");
+    if (H == 0) SCMOE_THROW(SCMOE_ERR_DIMENSION, "rope: heads must divide width");
+    if (dhr % 2 != 0) SCMOE_THROW(SCMOE_ERR_DIMENSION, "rope: rotary width per head must be even");
+}
+
+// (cos, sin) table of rope_apply (tensor.hpp:207-215) for positions
+// [0, npos): theta = pos * pow(base, -2p/hd) in double, then cast to float --
+// the reference's own expression, evaluated by the same libm.
+void mla_ensure_rope(scmoe_ctx* c, scmoe_mla* m, size_t npos) {
+    const size_t half = m->dhr / 2;
+    if (half == 0 || npos <= m->rope_rows) return;
+    const size_t rows = std::max(npos, 2 * m->rope_rows);
+    std::vector<float2> t(rows * half);
+    for (size_t pos = 0; pos < rows; ++pos)
+        for (size_t p = 0; p < half; ++p) {
+            const double theta = static_cast<double>(pos) *
+                                 std::pow(m->rope_base, -2.0 * static_cast<double>(p) /
+                                                            static_cast<double>(m->dhr));
+            t[pos * half + p] = make_float2(static_cast<float>(std::cos(theta)),
+                                            static_cast<float>(std::sin(theta)));
+        }
+    SCMOE_CUDA(cudaStreamSynchronize(c->stream));
+    cudaFree(m->rope);
+    m->rope = nullptr;
+    SCMOE_CUDA(cudaMalloc(&m->rope, t.size() * sizeof(float2)));
+    stream_copy(c, m->rope, t.data(), t.size() * sizeof(float2));
+    m->rope_rows = rows;
+}
+
+// C[rows, N] (ldc) = A[rows, K] (lda) . B[K, N]: sequential-k chains.
+void mla_gemm(scmoe_ctx* c, DevBuf& tiles_buf, const float* A, size_t lda, size_t rows,
+              const float* B, size_t K, size_t N, float* C, size_t ldc) {
+    if (rows == 0 || N == 0) return;
+    const int tr = seq_gemm_tile_rows(rows, N, c->num_sms);
+    const size_t ntile = ceil_div(rows, tr);
+    TokenTile* tiles = tiles_buf.get<TokenTile>(ntile + 1);
+    int* ntd = reinterpret_cast<int*>(tiles + ntile);
+    launch_row_tiles(c, rows, tr, tiles, ntd);
+    launch_seq_gemm(c, A, lda, nullptr, B, N, 0, C, ldc, K, N, /*silu=*/0, tiles, ntd, ntile, tr);
+}
+
+void mla_cache_reserve(scmoe_ctx* c, scmoe_mla* m, scmoe_mla_cache* k, size_t need) {
+    if (need <= k->cap) return;
+    const size_t cap = std::max<size_t>({need, 2 * k->cap, 16});
+    float *ckv = nullptr, *kr = nullptr, *kv = nullptr;
+    SCMOE_CUDA(cudaMalloc(&ckv, cap * m->dkv * sizeof(float)));
+    SCMOE_CUDA(cudaMalloc(&kr, std::max<size_t>(cap * m->dhr, 1) * sizeof(float)));
+    SCMOE_CUDA(cudaMalloc(&kv, cap * m->n3() * sizeof(float)));
+    if (k->len) {
+        SCMOE_CUDA(cudaMemcpyAsync(ckv, k->c_kv, k->len * m->dkv * sizeof(float),
+                                   cudaMemcpyDeviceToDevice, c->stream));
+        if (m->dhr)
+            SCMOE_CUDA(cudaMemcpyAsync(kr, k->k_r, k->len * m->dhr * sizeof(float),
+                                       cudaMemcpyDeviceToDevice, c->stream));
+        SCMOE_CUDA(cudaMemcpyAsync(kv, k->kv, k->len * m->n3() * sizeof(float),
+                                   cudaMemcpyDeviceToDevice, c->stream));
+    }
+    SCMOE_CUDA(cudaStreamSynchronize(c->stream));
+    cudaFree(k->c_kv);
+    cudaFree(k->k_r);
+    cudaFree(k->kv);
+    k->c_kv = ckv;
+    k->k_r = kr;
+    k->kv = kv;
+    k->cap = cap;
+}
+
+}  // namespace
+
+int scmoe_mla_create(scmoe_ctx* c, size_t d, size_t dq, size_t dkv, size_t H, size_t dhc,
+                     size_t dhr, double rope_base, int va, scmoe_mla** out) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        mla_check_dims(d, dq, dkv, H, dhr);
+        auto* m = new scmoe_mla();
+        m->d = d; m->dq = dq; m->dkv = dkv; m->H = H; m->dhc = dhc; m->dhr = dhr;
+        m->rope_base = rope_base;
+        m->variance_alignment = va;
+        // MlaParams::alpha_q/alpha_kv (blocks.hpp:51-56), cast as g.scale does
+        m->alpha_q = va ? static_cast<float>(std::sqrt(static_cast<double>(d) / dq)) : 1.0f;
+        m->alpha_kv = va ? static_cast<float>(std::sqrt(static_cast<double>(d) / dkv)) : 1.0f;
+        m->att_scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(dhc + dhr)));
+        const size_t sizes[4] = {d * m->n1(), dq * m->n2(), dkv * m->n3(), H * dhc * d};
+        float** ptrs[4] = {&m->w_h, &m->w_q, &m->w_kv, &m->w_o};
+        for (int i = 0; i < 4; ++i) {
+            SCMOE_CUDA(cudaMalloc(ptrs[i], std::max<size_t>(sizes[i], 1) * sizeof(float)));
+            stream_zero(c, *ptrs[i], std::max<size_t>(sizes[i], 1) * sizeof(float));
+        }
+        *out = m;
+    });
+}
+
+int scmoe_mla_destroy(scmoe_ctx* c, scmoe_mla* m) {
+    if (!m) return SCMOE_OK;
+    if (c) cudaSetDevice(c->device);
+    cudaFree(m->w_h);
+    cudaFree(m->w_q);
+    cudaFree(m->w_kv);
+    cudaFree(m->w_o);
+    cudaFree(m->rope);
+    delete m;
+    return SCMOE_OK;
+}
+
+static int mla_set_weight(scmoe_ctx* c, scmoe_mla* m, int which, const float* w) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        if (!m) SCMOE_THROW(SCMOE_ERR_PARAMETER, "mla: null handle");
+        const size_t H = m->H, dhc = m->dhc, dhr = m->dhr;
+        // destination matrix, its row count / leading dimension, column offset, width
+        float* dst = nullptr;
+        size_t rows = 0, ld = 0, col = 0, width = 0;
+        switch (which) {
+            case SCMOE_MLA_W_DQ: dst = m->w_h; rows = m->d; ld = m->n1(); col = 0; width = m->dq; break;
+            case SCMOE_MLA_W_DKV: dst = m->w_h; rows = m->d; ld = m->n1(); col = m->dq; width = m->dkv; break;
+            case SCMOE_MLA_W_KR: dst = m->w_h; rows = m->d; ld = m->n1(); col = m->dq + m->dkv; width = dhr; break;
+            case SCMOE_MLA_W_UQ: dst = m->w_q; rows = m->dq; ld = m->n2(); col = 0; width = H * dhc; break;
+            case SCMOE_MLA_W_QR: dst = m->w_q; rows = m->dq; ld = m->n2(); col = H * dhc; width = H * dhr; break;
+            case SCMOE_MLA_W_UK: dst = m->w_kv; rows = m->dkv; ld = m->n3(); col = 0; width = H * dhc; break;
+            case SCMOE_MLA_W_UV: dst = m->w_kv; rows = m->dkv; ld = m->n3(); col = H * dhc; width = H * dhc; break;
+            case SCMOE_MLA_W_O: dst = m->w_o; rows = H * dhc; ld = m->d; col = 0; width = m->d; break;
+            default: SCMOE_THROW(SCMOE_ERR_PARAMETER, "mla: unknown weight id");
+        }
+        if (width == 0 || rows == 0) return;
+        SCMOE_CUDA(cudaStreamSynchronize(c->stream));
+        SCMOE_CUDA(cudaMemcpy2DAsync(dst + col, ld * sizeof(float), w, width * sizeof(float),
+                                     width * sizeof(float), rows, cudaMemcpyDefault, c->stream));
+        SCMOE_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+int scmoe_mla_set_weight_host(scmoe_ctx* c, scmoe_mla* m, int which, const float* w) {
+    return mla_set_weight(c, m, which, w);
+}
+int scmoe_mla_set_weight(scmoe_ctx* c, scmoe_mla* m, int which, const float* w) {
+    return mla_set_weight(c, m, which, w);
+}
+
+int scmoe_mla_forward(scmoe_ctx* c, scmoe_mla* m, const float* h, size_t rows, size_t seq_len,
+                      float* out) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        if (!m) SCMOE_THROW(SCMOE_ERR_PARAMETER, "mla: null handle");
+        if (seq_len == 0 || rows % seq_len != 0)
+            SCMOE_THROW(SCMOE_ERR_DIMENSION, "attention: rows must pack whole sequences");
+        if (rows == 0) return;
+        Workspace& ws = c->ws;
+        const size_t d = m->d, dq = m->dq, dkv = m->dkv, H = m->H, dhc = m->dhc, dhr = m->dhr;
+        const size_t n1 = m->n1(), n2 = m->n2(), n3 = m->n3();
+        const size_t B = rows / seq_len;
+        mla_ensure_rope(c, m, seq_len);
+        float* p1 = ws.mla_p1.get<float>(rows * n1);  // [cq | ckv | kr]
+        float* qb = ws.mla_q.get<float>(rows * n2);   // [qc | qr]
+        float* kv = ws.mla_kv.get<float>(rows * n3);  // [kc | vv]
+        float* att = ws.mla_att.get<float>(B * H * seq_len * seq_len);
+        float* mg = ws.mla_m.get<float>(rows * H * dhc);
+        {
+            ProfScope _p(c, "mla_proj_h");
+            mla_gemm(c, ws.mla_tiles, h, d, rows, m->w_h, d, n1, p1, n1);
+            launch_mla_scale_rope(c, p1, n1, rows, (int)dq, m->alpha_q, (int)dkv, m->alpha_kv,
+                                  (int)(dq + dkv), 1, (int)dhr, m->rope, 0, seq_len);
+        }
+        {
+            ProfScope _p(c, "mla_proj_q");
+            mla_gemm(c, ws.mla_tiles, p1, n1, rows, m->w_q, dq, n2, qb, n2);
+            launch_mla_scale_rope(c, qb, n2, rows, 0, 1.f, 0, 1.f, (int)(H * dhc), (int)H,
+                                  (int)dhr, m->rope, 0, seq_len);
+        }
+        {
+            ProfScope _p(c, "mla_proj_kv");
+            mla_gemm(c, ws.mla_tiles, p1 + dq, n1, rows, m->w_kv, dkv, n3, kv, n3);
+        }
+        MlaAttnArgs a{};
+        a.qc = qb; a.qr = qb + H * dhc; a.ldq = n2;
+        a.kc = kv; a.v = kv + H * dhc; a.ldkv = n3;
+        a.kr = p1 + dq + dkv; a.ldkr = n1;
+        a.att = att; a.merged = mg; a.ldm = H * dhc;
+        a.H = (int)H; a.dhc = (int)dhc; a.dhr = (int)dhr;
+        a.nq = (int)seq_len; a.nk = (int)seq_len; a.q0 = 0;
+        a.scale = m->att_scale;
+        launch_mla_attention(c, a, (int)B);
+        ProfScope _p(c, "mla_proj_o");
+        mla_gemm(c, ws.mla_tiles, mg, H * dhc, rows, m->w_o, H * dhc, d, out, d);
+    });
+}
+
+int scmoe_mla_forward_host(scmoe_ctx* c, scmoe_mla* m, const float* h, size_t rows,
+                           size_t seq_len, float* out) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        if (!m) SCMOE_THROW(SCMOE_ERR_PARAMETER, "mla: null handle");
+        Stage& s = stage_of(c);
+        const float* dh = upload(c, s.bufs[0], h, rows * m->d);
+        float* dout = s.bufs[4].get<float>(rows * m->d);
+        int rc = scmoe_mla_forward(c, m, dh, rows, seq_len, dout);
+        if (rc) throw ScmoeError{rc, c->last_error};
+        download(c, out, dout, rows * m->d);
+        sync_and_check(c);
+    });
+}
+
+int scmoe_mla_cache_create(scmoe_ctx* c, scmoe_mla* m, size_t capacity_hint,
+                           scmoe_mla_cache** out) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        if (!m) SCMOE_THROW(SCMOE_ERR_PARAMETER, "mla: null handle");
+        auto* k = new scmoe_mla_cache();
+        try {
+            mla_cache_reserve(c, m, k, std::max<size_t>(capacity_hint, 1));
+        } catch (...) {
+            delete k;
+            throw;
+        }
+        *out = k;
+    });
+}
+
+int scmoe_mla_cache_destroy(scmoe_ctx* c, scmoe_mla_cache* k) {
+    if (!k) return SCMOE_OK;
+    if (c) cudaSetDevice(c->device);
+    cudaFree(k->c_kv);
+    cudaFree(k->k_r);
+    cudaFree(k->kv);
+    delete k;
+    return SCMOE_OK;
+}
+
+int scmoe_mla_cache_length(scmoe_ctx* c, scmoe_mla_cache* k, size_t* length) {
+    return guarded(c, [&] {
+        if (!k || !length) SCMOE_THROW(SCMOE_ERR_PARAMETER, "mla cache: null argument");
+        *length = k->len;
+    });
+}
+
+int scmoe_mla_cache_read_host(scmoe_ctx* c, scmoe_mla* m, scmoe_mla_cache* k, float* c_kv,
+                              float* k_r) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        if (!m || !k) SCMOE_THROW(SCMOE_ERR_PARAMETER, "mla cache: null argument");
+        if (c_kv) download(c, c_kv, k->c_kv, k->len * m->dkv);
+        if (k_r) download(c, k_r, k->k_r, k->len * m->dhr);
+        sync_and_check(c);
+    });
+}
+
+int scmoe_mla_infer_step(scmoe_ctx* c, scmoe_mla* m, scmoe_mla_cache* k, const float* h_t,
+                         size_t position, float* out) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        if (!m || !k) SCMOE_THROW(SCMOE_ERR_PARAMETER, "mla: null argument");
+        if (k->len != position)
+            SCMOE_THROW(SCMOE_ERR_STATE, "mla_infer_step: cache holds " + std::to_string(k->len) +
+                                             " rows but position is " + std::to_string(position));
+        Workspace& ws = c->ws;
+        const size_t d = m->d, dq = m->dq, dkv = m->dkv, H = m->H, dhc = m->dhc, dhr = m->dhr;
+        const size_t n1 = m->n1(), n2 = m->n2(), n3 = m->n3();
+        mla_ensure_rope(c, m, position + 1);
+        mla_cache_reserve(c, m, k, position + 1);
+        float* p1 = ws.mla_p1.get<float>(n1);
+        float* qb = ws.mla_q.get<float>(n2);
+        float* att = ws.mla_att.get<float>(H * (position + 1));
+        float* mg = ws.mla_m.get<float>(H * dhc);
+        ProfScope _p(c, "mla_infer_step");
+        mla_gemm(c, ws.mla_tiles, h_t, d, 1, m->w_h, d, n1, p1, n1);
+        launch_mla_scale_rope(c, p1, n1, 1, (int)dq, m->alpha_q, (int)dkv, m->alpha_kv,
+                              (int)(dq + dkv), 1, (int)dhr, m->rope, position, 1);
+        // append to the compressed cache (blocks.hpp:145-146)
+        SCMOE_CUDA(cudaMemcpyAsync(k->c_kv + position * dkv, p1 + dq, dkv * sizeof(float),
+                                   cudaMemcpyDeviceToDevice, c->stream));
+        if (dhr)
+            SCMOE_CUDA(cudaMemcpyAsync(k->k_r + position * dhr, p1 + dq + dkv, dhr * sizeof(float),
+                                       cudaMemcpyDeviceToDevice, c->stream));
+        mla_gemm(c, ws.mla_tiles, p1, n1, 1, m->w_q, dq, n2, qb, n2);
+        launch_mla_scale_rope(c, qb, n2, 1, 0, 1.f, 0, 1.f, (int)(H * dhc), (int)H, (int)dhr,
+                              m->rope, position, 1);
+        // this row's expanded kc | vv, kept beside the compressed cache
+        mla_gemm(c, ws.mla_tiles, k->c_kv + position * dkv, dkv, 1, m->w_kv, dkv, n3,
+                 k->kv + position * n3, n3);
+        k->len = position + 1;
+        MlaAttnArgs a{};
+        a.qc = qb; a.qr = qb + H * dhc; a.ldq = n2;
+        a.kc = k->kv; a.v = k->kv + H * dhc; a.ldkv = n3;
+        a.kr = k->k_r; a.ldkr = dhr;
+        a.att = att; a.merged = mg; a.ldm = H * dhc;
+        a.H = (int)H; a.dhc = (int)dhc; a.dhr = (int)dhr;
+        a.nq = 1; a.nk = (int)(position + 1); a.q0 = (int)position;
+        a.scale = m->att_scale;
+        launch_mla_attention(c, a, 1);
+        mla_gemm(c, ws.mla_tiles, mg, H * dhc, 1, m->w_o, H * dhc, d, out, d);
+    });
+}
+
+int scmoe_mla_infer_step_host(scmoe_ctx* c, scmoe_mla* m, scmoe_mla_cache* k, const float* h_t,
+                              size_t position, float* out) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        if (!m) SCMOE_THROW(SCMOE_ERR_PARAMETER, "mla: null handle");
+        Stage& s = stage_of(c);
+        const float* dh = upload(c, s.bufs[0], h_t, m->d);
+        float* dout = s.bufs[4].get<float>(m->d);
+        int rc = scmoe_mla_infer_step(c, m, k, dh, position, dout);
+        if (rc) throw ScmoeError{rc, c->last_error};
+        download(c, out, dout, m->d);
+        sync_and_check(c);
+    });
+}

@@ -69,13 +69,15 @@ struct Workspace {
     // dense shortcut FFN (scmoe_dense_ffn): own buffers, so it can run on
     // another stream beside the MoE branch
     DevBuf dn_x, dn_h, dn_y, dn_tiles;
+    // MLA (mla.cu): projections, scores/weights, merged heads, row tiles
+    DevBuf mla_p1, mla_q, mla_kv, mla_att, mla_m, mla_tiles;
     unsigned char pr_blob[64] = {};  // permutation result carried from moe_front to moe_back
     void release_all() {
         DevBuf* all[] = {&logits, &probs, &hmoe, &hmoe_bf16, &idx, &gates, &ffn_count,
                          &rank_in_block, &block_counts, &expert_count, &expert_base, &slot_pos,
                          &row_token, &tiles, &n_tiles, &xp, &h, &y, &in_copy, &out_copy, &misc,
                          &tiles_router, &ep_bins, &ep_local, &ep_y, &dn_x, &dn_h, &dn_y,
-                         &dn_tiles};
+                         &dn_tiles, &mla_p1, &mla_q, &mla_kv, &mla_att, &mla_m, &mla_tiles};
         for (DevBuf* b : all) b->release();
     }
 };
@@ -329,7 +331,60 @@ void launch_ep_put_rows(scmoe_ctx* c, const __nv_bfloat16* src, size_t d, const 
                         const int64_t* dst_offset, const uint64_t* peer_rows,
                         const uint64_t* peer_expert, int G);
 
+// ---- MLA (mla.cu) ----
+// Attention operands of the (sequence b, head h) pairs.  Rows of sequence b
+// start at b * nq (queries) and b * nk (keys); query i sits at absolute
+// position q0 + i and sees keys j <= q0 + i.
+struct MlaAttnArgs {
+    const float* qc;  // query content [rows, ldq] (+ h*dhc)
+    const float* qr;  // query rotary  [rows, ldq] (+ h*dhr)
+    size_t ldq;
+    const float* kc;  // key content [keys, ldkv] (+ h*dhc)
+    const float* v;   // values      [keys, ldkv] (+ h*dhc)
+    size_t ldkv;
+    const float* kr;  // rotary key shared by the heads [keys, ldkr]
+    size_t ldkr;
+    float* att;       // [B][H][nq][nk] scores -> weights
+    float* merged;    // [B*nq, ldm] (+ h*dhc)
+    size_t ldm;
+    int H, dhc, dhr, nq, nk, q0;
+    float scale;
+};
+void launch_mla_scale_rope(scmoe_ctx* c, float* X, size_t ld, size_t rows, int n_a, float alpha_a,
+                           int n_b, float alpha_b, int rc, int heads, int hd, const float2* table,
+                           size_t pos0, size_t seq_len);
+void launch_mla_attention(scmoe_ctx* c, const MlaAttnArgs& a, int batches);
+
 }  // namespace scmoe
+
+// MlaParams<float> (blocks.hpp:38-58) resident on the device.  The projections
+// that share an input are stored column-concatenated so each runs as one GEMM:
+//   w_h  [d,   dq + dkv + dhr] = [w_dq | w_dkv | w_kr]
+//   w_q  [dq,  H*dhc + H*dhr]  = [w_uq | w_qr]
+//   w_kv [dkv, 2*H*dhc]        = [w_uk | w_uv]
+//   w_o  [H*dhc, d]
+struct scmoe_mla {
+    size_t d = 0, dq = 0, dkv = 0, H = 0, dhc = 0, dhr = 0;
+    double rope_base = 1.0e6;
+    int variance_alignment = 1;
+    float alpha_q = 1.f, alpha_kv = 1.f, att_scale = 1.f;
+    float *w_h = nullptr, *w_q = nullptr, *w_kv = nullptr, *w_o = nullptr;
+    float2* rope = nullptr;  // (cos, sin) [rope_rows][dhr/2]
+    size_t rope_rows = 0;
+    size_t n1() const { return dq + dkv + dhr; }
+    size_t n2() const { return H * (dhc + dhr); }
+    size_t n3() const { return 2 * H * dhc; }
+};
+
+// MlaCache (blocks.hpp:106-112) plus the expanded content keys / values of
+// the cached rows (kc = c_kv W_uk and vv = c_kv W_uv are row-wise, so caching
+// them is bitwise the reference's per-step re-expansion).
+struct scmoe_mla_cache {
+    size_t len = 0, cap = 0;
+    float* c_kv = nullptr;  // [cap, dkv]
+    float* k_r = nullptr;   // [cap, dhr] (rotated)
+    float* kv = nullptr;    // [cap, 2*H*dhc] = [kc | vv]
+};
 
 #define SCMOE_LAUNCH_CHECK(c)                                                               \
     do {                                                                                    \

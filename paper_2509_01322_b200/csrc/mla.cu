@@ -1,0 +1,298 @@
+// mla.cu -- multi-head latent attention, forward value (S = float), exact.
+//
+// blocks.hpp:73-102 (mla_block), :129-181 (mla_infer_step); tensor.hpp:197-224
+// (rope_apply); graph.hpp:396-434 (attention).  Every output is produced with
+// the reference's operation order and rounding:
+//   * projections: sequential-k fp32 chains (seq_gemm_kernel, tensor.hpp:95-112);
+//     the projections that read the same input are fused into one GEMM over
+//     column-concatenated weights -- output columns are independent, so the
+//     bits do not change;
+//   * g.scale: one rounded multiply by float(alpha);
+//   * rope: a*c - b*s and a*s + b*c, products and sums separately rounded,
+//     with (c, s) = float(cos/sin(theta)) from a host table computed with the
+//     reference's own expression (libm pow/cos/sin, double);
+//   * attention: score = sequential dot over [content | rotary] (rounded mul
+//     + add), times the rounded scale; the row max; e = expf(s - max) on the
+//     glibc expf port; the normaliser a sequential fp32 sum in key order;
+//     w = e / denom; out = sequential sum over keys of w * v.
+// Compiled with --fmad=false; packed f32x2 chains use the half-swapped add
+// (f32x2.cuh), so nothing is contracted (build.py checks the SASS).
+#include "f32x2.cuh"
+#include "internal.cuh"
+#include "libm_port.h"
+
+namespace scmoe {
+
+// ---------------------------------------------------------------------------
+// Scale + rotary epilogue of a projection output X [rows, ld]:
+//   cols [0, n_a) *= alpha_a, [n_a, n_a + n_b) *= alpha_b,
+//   cols [rc, rc + heads*hd) rotated per head at pos = pos0 + r % seq_len.
+// One thread per (row, item); items are the scaled columns then the pairs.
+// ---------------------------------------------------------------------------
+__global__ void mla_scale_rope_kernel(float* __restrict__ X, size_t ld, size_t rows, int n_a,
+                                      float alpha_a, int n_b, float alpha_b, int rc, int heads,
+                                      int hd, const float2* __restrict__ table, size_t pos0,
+                                      size_t seq_len) {
+    const int half = hd / 2;
+    const size_t per_row = (size_t)n_a + n_b + (size_t)heads * half;
+    const size_t n = rows * per_row;
+    for (size_t it = blockIdx.x * (size_t)blockDim.x + threadIdx.x; it < n;
+         it += (size_t)gridDim.x * blockDim.x) {
+        const size_t r = it / per_row;
+        size_t c = it % per_row;
+        float* row = X + r * ld;
+        if (c < (size_t)n_a) {
+            row[c] = __fmul_rn(row[c], alpha_a);
+        } else if (c < (size_t)(n_a + n_b)) {
+            row[c] = __fmul_rn(row[c], alpha_b);
+        } else {
+            c -= n_a + n_b;
+            const int h = (int)(c / half), p = (int)(c % half);
+            const size_t pos = pos0 + r % seq_len;
+            const float2 cs = table[pos * half + p];
+            float* q = row + rc + h * hd + 2 * p;
+            const float a = q[0], b = q[1];
+            q[0] = __fsub_rn(__fmul_rn(a, cs.x), __fmul_rn(b, cs.y));
+            q[1] = __fadd_rn(__fmul_rn(a, cs.y), __fmul_rn(b, cs.x));
+        }
+    }
+}
+
+constexpr int kMlaKC = 32, kMlaPad = 4, kMlaTN = 64;
+
+// Scores S[i][j] = scale * (sum_t qc_i[t] kc_j[t] + sum_t qr_i[t] kr_j[t]) in
+// t order.  CTA tile TM queries x 64 keys, thread tile RM x 4 (f32x2 pairs
+// along keys); the dot length is staged through shared memory in chunks of
+// 32 taken first from the content halves, then from the rotary halves.
+template <int TM, int RM>
+__global__ void __launch_bounds__((TM / RM) * 16) mla_scores_kernel(MlaAttnArgs a) {
+    constexpr int NT = (TM / RM) * 16;
+    __shared__ __align__(16) float As[kMlaKC][TM + kMlaPad];
+    __shared__ __align__(16) float Bs[kMlaKC][kMlaTN + kMlaPad];
+    const int bh = blockIdx.z, b = bh / a.H, h = bh % a.H;
+    const int i0 = blockIdx.y * TM, j0 = blockIdx.x * kMlaTN;
+    const int i_last = min(a.nq, i0 + TM) - 1;
+    if (j0 > a.q0 + i_last) return;  // tile entirely above the causal diagonal
+    const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+    const size_t qrow0 = (size_t)b * a.nq, krow0 = (size_t)b * a.nk;
+
+    uint64_t acc2[RM][2];
+#pragma unroll
+    for (int i = 0; i < RM; ++i) acc2[i][0] = acc2[i][1] = 0;
+
+    for (int seg = 0; seg < 2; ++seg) {
+        const int len = seg == 0 ? a.dhc : a.dhr;
+        const float* qb = seg == 0 ? a.qc + (size_t)h * a.dhc : a.qr + (size_t)h * a.dhr;
+        const float* kb = seg == 0 ? a.kc + (size_t)h * a.dhc : a.kr;
+        const size_t ldk = seg == 0 ? a.ldkv : a.ldkr;
+        for (int k0 = 0; k0 < len; k0 += kMlaKC) {
+            const int kc = min(kMlaKC, len - k0);
+            for (int e = tid; e < TM * kMlaKC; e += NT) {
+                const int r = e / kMlaKC, k = e % kMlaKC;
+                float v = 0.f;
+                if (k < kc && i0 + r < a.nq) v = qb[(qrow0 + i0 + r) * a.ldq + k0 + k];
+                As[k][r] = v;
+            }
+            for (int e = tid; e < kMlaTN * kMlaKC; e += NT) {
+                const int r = e / kMlaKC, k = e % kMlaKC;
+                float v = 0.f;
+                if (k < kc && j0 + r < a.nk) v = kb[(krow0 + j0 + r) * ldk + k0 + k];
+                Bs[k][r] = v;
+            }
+            __syncthreads();
+            for (int k = 0; k < kc; ++k) {
+                float av[RM];
+#pragma unroll
+                for (int i = 0; i < RM; ++i) av[i] = As[k][RM * ty + i];
+                const ulonglong2 bb = *reinterpret_cast<const ulonglong2*>(&Bs[k][4 * tx]);
+#pragma unroll
+                for (int i = 0; i < RM; ++i) {
+                    acc2[i][0] = f2_add_swapped(acc2[i][0], f2_mul_bcast(av[i], bb.x));
+                    acc2[i][1] = f2_add_swapped(acc2[i][1], f2_mul_bcast(av[i], bb.y));
+                }
+            }
+            __syncthreads();
+        }
+    }
+    float* att = a.att + (size_t)bh * a.nq * a.nk;
+#pragma unroll
+    for (int i = 0; i < RM; ++i) {
+        const int qi = i0 + RM * ty + i;
+        if (qi >= a.nq) continue;
+        const float s[4] = {f2_hi(acc2[i][0]), f2_lo(acc2[i][0]), f2_hi(acc2[i][1]),
+                            f2_lo(acc2[i][1])};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int j = j0 + 4 * tx + q;
+            if (j < a.nk && j <= a.q0 + qi) att[(size_t)qi * a.nk + j] = __fmul_rn(s[q], a.scale);
+        }
+    }
+}
+
+// Softmax rows in place: one warp per (b, h, i), n = q0 + i + 1 keys.  The
+// max is order independent; e_j = expf(s_j - max) elementwise; the
+// normaliser is summed strictly in key order (every lane keeps the same
+// running sum, fed one element per shuffle); then w_j = e_j / denom.
+__global__ void __launch_bounds__(256) mla_softmax_kernel(float* __restrict__ att, int rows_total,
+                                                          int nq, int nk, int q0) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= rows_total) return;
+    const int i = warp % nq;
+    const int n = min(nk, q0 + i + 1);
+    float* row = att + (size_t)warp * nk;
+    float mx = -INFINITY;
+    for (int j = lane; j < n; j += 32) mx = fmaxf(mx, row[j]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float denom = 0.f;
+    for (int j0 = 0; j0 < n; j0 += 32) {
+        const int j = j0 + lane;
+        float e = 0.f;
+        if (j < n) {
+            e = scmoe_expf(__fsub_rn(row[j], mx));
+            row[j] = e;
+        }
+        const int m = min(32, n - j0);
+        for (int t = 0; t < m; ++t) denom = __fadd_rn(denom, __shfl_sync(0xffffffffu, e, t));
+    }
+    for (int j = lane; j < n; j += 32) row[j] = __fdiv_rn(row[j], denom);
+}
+
+// merged[i][h*dhc + p] = sum_{j <= q0+i} w[i][j] * v[j][p], j ascending,
+// starting from 0.  CTA tile TM queries x 64 value columns; keys staged in
+// chunks of 32.  Chunks that cross the diagonal of some row select instead of
+// adding, so a row never sees a key past its own position.
+template <int TM, int RM>
+__global__ void __launch_bounds__((TM / RM) * 16) mla_pv_kernel(MlaAttnArgs a) {
+    constexpr int NT = (TM / RM) * 16;
+    __shared__ __align__(16) float As[kMlaKC][TM + kMlaPad];
+    __shared__ __align__(16) float Bs[kMlaKC][kMlaTN + kMlaPad];
+    const int bh = blockIdx.z, b = bh / a.H, h = bh % a.H;
+    const int i0 = blockIdx.y * TM, c0 = blockIdx.x * kMlaTN;
+    if (i0 >= a.nq) return;
+    const int i_last = min(a.nq, i0 + TM) - 1;
+    const int jmax = min(a.nk, a.q0 + i_last + 1);  // keys any row of the tile sees
+    const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+    const float* att = a.att + (size_t)bh * a.nq * a.nk;
+    const float* vb = a.v + (size_t)b * a.nk * a.ldkv + (size_t)h * a.dhc;
+
+    uint64_t acc2[RM][2];
+#pragma unroll
+    for (int i = 0; i < RM; ++i) acc2[i][0] = acc2[i][1] = 0;
+    int lim[RM];  // last key of each thread row
+#pragma unroll
+    for (int i = 0; i < RM; ++i) lim[i] = a.q0 + i0 + RM * ty + i;
+
+    for (int k0 = 0; k0 < jmax; k0 += kMlaKC) {
+        const int kc = min(kMlaKC, jmax - k0);
+        for (int e = tid; e < TM * kMlaKC; e += NT) {
+            const int r = e / kMlaKC, k = e % kMlaKC;
+            float v = 0.f;
+            if (k < kc && i0 + r < a.nq && k0 + k <= a.q0 + i0 + r)
+                v = att[(size_t)(i0 + r) * a.nk + k0 + k];
+            As[k][r] = v;
+        }
+        for (int e = tid; e < kMlaTN * kMlaKC; e += NT) {
+            const int k = e / kMlaTN, cc = e % kMlaTN;
+            float v = 0.f;
+            if (k < kc && c0 + cc < a.dhc) v = vb[(size_t)(k0 + k) * a.ldkv + c0 + cc];
+            Bs[k][cc] = v;
+        }
+        __syncthreads();
+        if (k0 + kc - 1 <= a.q0 + i0) {  // every row of the tile sees the whole chunk
+            for (int k = 0; k < kc; ++k) {
+                float av[RM];
+#pragma unroll
+                for (int i = 0; i < RM; ++i) av[i] = As[k][RM * ty + i];
+                const ulonglong2 bb = *reinterpret_cast<const ulonglong2*>(&Bs[k][4 * tx]);
+#pragma unroll
+                for (int i = 0; i < RM; ++i) {
+                    acc2[i][0] = f2_add_swapped(acc2[i][0], f2_mul_bcast(av[i], bb.x));
+                    acc2[i][1] = f2_add_swapped(acc2[i][1], f2_mul_bcast(av[i], bb.y));
+                }
+            }
+        } else {
+            for (int k = 0; k < kc; ++k) {
+                float av[RM];
+#pragma unroll
+                for (int i = 0; i < RM; ++i) av[i] = As[k][RM * ty + i];
+                const ulonglong2 bb = *reinterpret_cast<const ulonglong2*>(&Bs[k][4 * tx]);
+#pragma unroll
+                for (int i = 0; i < RM; ++i) {
+                    const bool on = k0 + k <= lim[i];
+                    const uint64_t n0 = f2_add_swapped(acc2[i][0], f2_mul_bcast(av[i], bb.x));
+                    const uint64_t n1 = f2_add_swapped(acc2[i][1], f2_mul_bcast(av[i], bb.y));
+                    acc2[i][0] = on ? n0 : acc2[i][0];
+                    acc2[i][1] = on ? n1 : acc2[i][1];
+                }
+            }
+        }
+        __syncthreads();
+    }
+    float* mb = a.merged + (size_t)b * a.nq * a.ldm + (size_t)h * a.dhc;
+#pragma unroll
+    for (int i = 0; i < RM; ++i) {
+        const int qi = i0 + RM * ty + i;
+        if (qi >= a.nq) continue;
+        const float s[4] = {f2_hi(acc2[i][0]), f2_lo(acc2[i][0]), f2_hi(acc2[i][1]),
+                            f2_lo(acc2[i][1])};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int col = c0 + 4 * tx + q;
+            if (col < a.dhc) mb[(size_t)qi * a.ldm + col] = s[q];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Launchers.
+// ---------------------------------------------------------------------------
+void launch_mla_scale_rope(scmoe_ctx* c, float* X, size_t ld, size_t rows, int n_a, float alpha_a,
+                           int n_b, float alpha_b, int rc, int heads, int hd, const float2* table,
+                           size_t pos0, size_t seq_len) {
+    const size_t n = rows * ((size_t)n_a + n_b + (size_t)heads * (hd / 2));
+    if (n == 0) return;
+    const int threads = 256;
+    const size_t blocks = std::min<size_t>(ceil_div(n, threads), (size_t)c->num_sms * 16);
+    mla_scale_rope_kernel<<<(unsigned)blocks, threads, 0, c->stream>>>(
+        X, ld, rows, n_a, alpha_a, n_b, alpha_b, rc, heads, hd, table, pos0, seq_len);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
+void launch_mla_attention(scmoe_ctx* c, const MlaAttnArgs& a, int batches) {
+    const MlaAttnArgs& h = a;
+    const unsigned z = (unsigned)(batches * h.H);
+    const bool big = h.nq >= 64;
+    {
+        ProfScope _p(c, "mla_scores");
+        if (big) {
+            dim3 grid((unsigned)ceil_div(h.nk, kMlaTN), (unsigned)ceil_div(h.nq, 64), z);
+            mla_scores_kernel<64, 4><<<grid, 256, 0, c->stream>>>(a);
+        } else {
+            dim3 grid((unsigned)ceil_div(h.nk, kMlaTN), (unsigned)ceil_div(h.nq, 16), z);
+            mla_scores_kernel<16, 2><<<grid, 128, 0, c->stream>>>(a);
+        }
+        SCMOE_LAUNCH_CHECK(c);
+    }
+    {
+        ProfScope _p(c, "mla_softmax");
+        const size_t rows = (size_t)z * h.nq;
+        mla_softmax_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, c->stream>>>(h.att, (int)rows,
+                                                                              h.nq, h.nk, h.q0);
+        SCMOE_LAUNCH_CHECK(c);
+    }
+    {
+        ProfScope _p(c, "mla_pv");
+        if (big) {
+            dim3 grid((unsigned)ceil_div(h.dhc, kMlaTN), (unsigned)ceil_div(h.nq, 64), z);
+            mla_pv_kernel<64, 4><<<grid, 256, 0, c->stream>>>(a);
+        } else {
+            dim3 grid((unsigned)ceil_div(h.dhc, kMlaTN), (unsigned)ceil_div(h.nq, 16), z);
+            mla_pv_kernel<16, 2><<<grid, 128, 0, c->stream>>>(a);
+        }
+        SCMOE_LAUNCH_CHECK(c);
+    }
+}
+
+}  // namespace scmoe

@@ -81,6 +81,8 @@ _ORC_PROTOS = {
                                       _P, _SZ, _D, _D, C.c_int, _P, _P, _P, _P]),
     "orc_simulate_bias_control_f32": (C.c_int, [_P, _SZ, _SZ, _SZ, _SZ, _SZ, _P, _D, _P, _U64,
                                                 _SZ, _SZ, _P, _P]),
+    "orc_mla_forward_f32": (C.c_int, [_SZ] * 6 + [_D, C.c_int, _P, _P, _SZ, _SZ, _P]),
+    "orc_mla_infer_f32": (C.c_int, [_SZ] * 6 + [_D, C.c_int, _P, _P, _SZ, _P, _P, _P]),
 }
 
 _REF_PROTOS = {
@@ -108,6 +110,9 @@ _REF_PROTOS = {
     "ref_rmsnorm_f32": (C.c_int, [_P, _P, _SZ, _SZ, _P]),
     "ref_simulate_bias_control_f32": (C.c_int, [_P, _SZ, _SZ, _SZ, _SZ, _SZ, _P, _D, _P, _U64,
                                                 _SZ, _SZ, _P, _P]),
+    "ref_mla_forward_f32": (C.c_int, [_SZ] * 6 + [_D, C.c_int, _P, _P, _SZ, _SZ, _P, C.c_int]),
+    "ref_mla_infer_f32": (C.c_int, [_SZ] * 6 + [_D, C.c_int, _P, _P, _SZ, _P, _P, _P]),
+    "ref_mla_infer_position_check": (C.c_int, [_SZ, _SZ]),
 }
 
 _orc = None
@@ -250,3 +255,46 @@ def rel_l2(a, b) -> float:
     a = np.asarray(a, np.float64)
     b = np.asarray(b, np.float64)
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+# ---- MLA (blocks.hpp:38-181) ---------------------------------------------------
+MLA_NAMES = ("w_dq", "w_uq", "w_qr", "w_dkv", "w_uk", "w_uv", "w_kr", "w_o")
+
+
+def mla_shapes(d, dq, dkv, H, dhc, dhr):
+    return [(d, dq), (dq, H * dhc), (dq, H * dhr), (d, dkv), (dkv, H * dhc), (dkv, H * dhc),
+            (d, dhr), (H * dhc, d)]
+
+
+def mla_weights(d, dq, dkv, H, dhc, dhr, seed=3):
+    """MlaFixture-like weights (tests/test_blocks.cpp:27-66) with the Uniform
+    device-reproducible init of variance 1/d_model, stream ids 0..7."""
+    return [uniform_f32(stream_seed(seed, i), r * c, 1.0 / d).reshape(r, c)
+            for i, (r, c) in enumerate(mla_shapes(d, dq, dkv, H, dhc, dhr))]
+
+
+def mla_forward(lib, dims, w, h, seq_len, base=1.0e4, va=1, threads=1):
+    d, dq, dkv, H, dhc, dhr = dims
+    h = np.ascontiguousarray(h, np.float32)
+    rows = h.shape[0]
+    out = np.zeros((rows, d), np.float32)
+    ws = [np.ascontiguousarray(x, np.float32) for x in w]
+    args = [d, dq, dkv, H, dhc, dhr, base, va, ptr_array(ws), ptr(h), rows, seq_len, ptr(out)]
+    if lib is _ref:
+        args.append(threads)
+    rc = (lib.ref_mla_forward_f32 if lib is _ref else lib.orc_mla_forward_f32)(*args)
+    return rc, out
+
+
+def mla_infer(lib, dims, w, h, base=1.0e4, va=1):
+    d, dq, dkv, H, dhc, dhr = dims
+    h = np.ascontiguousarray(h, np.float32)
+    T = h.shape[0]
+    out = np.zeros((T, d), np.float32)
+    ckv = np.zeros((T, dkv), np.float32)
+    kr = np.zeros((T, dhr), np.float32)
+    ws = [np.ascontiguousarray(x, np.float32) for x in w]
+    fn = lib.ref_mla_infer_f32 if lib is _ref else lib.orc_mla_infer_f32
+    rc = fn(d, dq, dkv, H, dhc, dhr, base, va, ptr_array(ws), ptr(h), T, ptr(out), ptr(ckv),
+            ptr(kr))
+    return rc, out, ckv, kr

@@ -1614,7 +1614,8 @@ int scmoe_mla_forward(scmoe_ctx* c, scmoe_mla* m, const float* h, size_t rows, s
         float* p1 = ws.mla_p1.get<float>(rows * n1);  // [cq | ckv | kr]
         float* qb = ws.mla_q.get<float>(rows * n2);   // [qc | qr]
         float* kv = ws.mla_kv.get<float>(rows * n3);  // [kc | vv]
-        float* att = ws.mla_att.get<float>(B * H * seq_len * seq_len);
+        const size_t nkt = ceil_div(seq_len, 64);
+        float* att = ws.mla_att.get<float>(B * H * seq_len * (seq_len + nkt));
         float* mg = ws.mla_m.get<float>(rows * H * dhc);
         {
             ProfScope _p(c, "mla_proj_h");
@@ -1636,7 +1637,8 @@ int scmoe_mla_forward(scmoe_ctx* c, scmoe_mla* m, const float* h, size_t rows, s
         a.qc = qb; a.qr = qb + H * dhc; a.ldq = n2;
         a.kc = kv; a.v = kv + H * dhc; a.ldkv = n3;
         a.kr = p1 + dq + dkv; a.ldkr = n1;
-        a.att = att; a.merged = mg; a.ldm = H * dhc;
+        a.att = att; a.part_max = att + B * H * seq_len * seq_len;
+        a.merged = mg; a.ldm = H * dhc;
         a.H = (int)H; a.dhc = (int)dhc; a.dhr = (int)dhr;
         a.nq = (int)seq_len; a.nk = (int)seq_len; a.q0 = 0;
         a.scale = m->att_scale;
@@ -1720,7 +1722,7 @@ int scmoe_mla_infer_step(scmoe_ctx* c, scmoe_mla* m, scmoe_mla_cache* k, const f
         mla_cache_reserve(c, m, k, position + 1);
         float* p1 = ws.mla_p1.get<float>(n1);
         float* qb = ws.mla_q.get<float>(n2);
-        float* att = ws.mla_att.get<float>(H * (position + 1));
+        float* att = ws.mla_att.get<float>(H * (position + 1 + ceil_div(position + 1, 64)));
         float* mg = ws.mla_m.get<float>(H * dhc);
         ProfScope _p(c, "mla_infer_step");
         mla_gemm(c, ws.mla_tiles, h_t, d, 1, m->w_h, d, n1, p1, n1);
@@ -1743,7 +1745,8 @@ int scmoe_mla_infer_step(scmoe_ctx* c, scmoe_mla* m, scmoe_mla_cache* k, const f
         a.qc = qb; a.qr = qb + H * dhc; a.ldq = n2;
         a.kc = k->kv; a.v = k->kv + H * dhc; a.ldkv = n3;
         a.kr = k->k_r; a.ldkr = dhr;
-        a.att = att; a.merged = mg; a.ldm = H * dhc;
+        a.att = att; a.part_max = att + H * (position + 1);
+        a.merged = mg; a.ldm = H * dhc;
         a.H = (int)H; a.dhc = (int)dhc; a.dhr = (int)dhr;
         a.nq = 1; a.nk = (int)(position + 1); a.q0 = (int)position;
         a.scale = m->att_scale;

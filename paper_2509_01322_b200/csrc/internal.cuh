@@ -344,7 +344,8 @@ struct MlaAttnArgs {
     size_t ldkv;
     const float* kr;  // rotary key shared by the heads [keys, ldkr]
     size_t ldkr;
-    float* att;       // [B][H][nq][nk] scores -> weights
+    float* att;       // [B][H][nq][nk] scores -> softmax weights, in place
+    float* part_max;  // [B][H][nq][ceil(nk/64)] per-key-tile row maxima
     float* merged;    // [B*nq, ldm] (+ h*dhc)
     size_t ldm;
     int H, dhc, dhr, nq, nk, q0;

@@ -115,48 +115,118 @@ __global__ void __launch_bounds__((TM / RM) * 16) mla_scores_kernel(MlaAttnArgs 
         }
     }
     float* att = a.att + (size_t)bh * a.nq * a.nk;
+    const int nkt = (a.nk + kMlaTN - 1) / kMlaTN;
 #pragma unroll
     for (int i = 0; i < RM; ++i) {
         const int qi = i0 + RM * ty + i;
-        if (qi >= a.nq) continue;
         const float s[4] = {f2_hi(acc2[i][0]), f2_lo(acc2[i][0]), f2_hi(acc2[i][1]),
                             f2_lo(acc2[i][1])};
+        float mx = -INFINITY;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int j = j0 + 4 * tx + q;
-            if (j < a.nk && j <= a.q0 + qi) att[(size_t)qi * a.nk + j] = __fmul_rn(s[q], a.scale);
+            if (qi < a.nq && j < a.nk && j <= a.q0 + qi) {
+                const float v = __fmul_rn(s[q], a.scale);
+                att[(size_t)qi * a.nk + j] = v;
+                mx = fmaxf(mx, v);
+            }
         }
+        // this key tile's row max (the 16 threads of a row are lanes of one half-warp)
+#pragma unroll
+        for (int o = 8; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (tx == 0 && qi < a.nq) a.part_max[((size_t)bh * a.nq + qi) * nkt + blockIdx.x] = mx;
     }
 }
 
-// Softmax rows in place: one warp per (b, h, i), n = q0 + i + 1 keys.  The
-// max is order independent; e_j = expf(s_j - max) elementwise; the
-// normaliser is summed strictly in key order (every lane keeps the same
-// running sum, fed one element per shuffle); then w_j = e_j / denom.
-__global__ void __launch_bounds__(256) mla_softmax_kernel(float* __restrict__ att, int rows_total,
-                                                          int nq, int nk, int q0) {
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (warp >= rows_total) return;
-    const int i = warp % nq;
-    const int n = min(nk, q0 + i + 1);
-    float* row = att + (size_t)warp * nk;
+// Softmax of the score rows, in place, 32 consecutive rows (b, h, i..i+31)
+// per warp; row i has n = q0 + i + 1 keys.
+//   max   = max of the scores kernel's per-key-tile maxima (order free);
+//   e_j   = expf(s_j - max) and denom = sum of e_j in key order: a 32x32 block
+//           is loaded coalesced, transposed through shared memory, and lane l
+//           walks row l's 32 keys sequentially (the reference's fp32 sum);
+//   w_j   = e_j / denom (rounded division), coalesced, written in place.
+__global__ void __launch_bounds__(256) mla_softmax_kernel(float* __restrict__ att,
+                                                          const float* __restrict__ part_max,
+                                                          int rows_total, int nq, int nk, int q0) {
+    __shared__ float tile[8][32][33];
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r0 = (blockIdx.x * 8 + wib) * 32;
+    if (r0 >= rows_total) return;
+    float(*T)[33] = tile[wib];
+    const int nkt = (nk + kMlaTN - 1) / kMlaTN;
+    const int r = r0 + lane;
+    const bool live = r < rows_total;
+    const int n = live ? min(nk, q0 + r % nq + 1) : 0;
     float mx = -INFINITY;
-    for (int j = lane; j < n; j += 32) mx = fmaxf(mx, row[j]);
+    for (int t = 0; t < (n + kMlaTN - 1) / kMlaTN; ++t) mx = fmaxf(mx, part_max[(size_t)r * nkt + t]);
+    // rows of the warp may straddle two (b, h) blocks: lengths are per row
+    int nmax = 0;
+    for (int t = 0; t < 32; ++t) nmax = max(nmax, __shfl_sync(0xffffffffu, n, t));
+    float sum = 0.f;
+    for (int j0 = 0; j0 < nmax; j0 += 32) {
+        float v[32];  // all 32 coalesced row segments in flight before the transpose
 #pragma unroll
-    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    float denom = 0.f;
-    for (int j0 = 0; j0 < n; j0 += 32) {
-        const int j = j0 + lane;
-        float e = 0.f;
-        if (j < n) {
-            e = scmoe_expf(__fsub_rn(row[j], mx));
-            row[j] = e;
+        for (int t = 0; t < 32; ++t) {
+            const int nt = __shfl_sync(0xffffffffu, n, t);
+            v[t] = (j0 + lane < nt) ? att[(size_t)(r0 + t) * nk + j0 + lane] : 0.f;
         }
+#pragma unroll
+        for (int t = 0; t < 32; ++t) T[t][lane] = v[t];
+        __syncwarp();
         const int m = min(32, n - j0);
-        for (int t = 0; t < m; ++t) denom = __fadd_rn(denom, __shfl_sync(0xffffffffu, e, t));
+        if (m == 32) {
+            // 32 independent exponentials first (ILP), then the in-order sum
+            float e[32];
+#pragma unroll
+            for (int t = 0; t < 32; ++t) e[t] = scmoe_expf(__fsub_rn(T[lane][t], mx));
+#pragma unroll
+            for (int t = 0; t < 32; ++t) {
+                T[lane][t] = e[t];
+                sum = __fadd_rn(sum, e[t]);
+            }
+        } else {
+            for (int t = 0; t < m; ++t) {
+                const float e = scmoe_expf(__fsub_rn(T[lane][t], mx));
+                T[lane][t] = e;
+                sum = __fadd_rn(sum, e);
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+            const int nt = __shfl_sync(0xffffffffu, n, t);
+            if (j0 + lane < nt) att[(size_t)(r0 + t) * nk + j0 + lane] = T[t][lane];
+        }
+        __syncwarp();
     }
-    for (int j = lane; j < n; j += 32) row[j] = __fdiv_rn(row[j], denom);
+    // w = e / denom, row by row, 16-byte accesses with 4 in flight per lane
+    for (int t = 0; t < 32; ++t) {
+        const int rt = r0 + t, nt = __shfl_sync(0xffffffffu, n, t);
+        const float den = __shfl_sync(0xffffffffu, sum, t);
+        float* row = att + (size_t)rt * nk;
+        int j = 0;
+        if ((nk & 3) == 0) {
+            float4* r4 = reinterpret_cast<float4*>(row);
+            const int n4 = nt >> 2;
+            for (int q0 = 0; q0 < n4; q0 += 128) {
+                float4 w[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int q = q0 + 32 * u + lane;
+                    if (q < n4) w[u] = r4[q];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int q = q0 + 32 * u + lane;
+                    if (q < n4)
+                        r4[q] = make_float4(__fdiv_rn(w[u].x, den), __fdiv_rn(w[u].y, den),
+                                            __fdiv_rn(w[u].z, den), __fdiv_rn(w[u].w, den));
+                }
+            }
+            j = n4 * 4;
+        }
+        for (j += lane; j < nt; j += 32) row[j] = __fdiv_rn(row[j], den);
+    }
 }
 
 // merged[i][h*dhc + p] = sum_{j <= q0+i} w[i][j] * v[j][p], j ascending,
@@ -278,8 +348,8 @@ void launch_mla_attention(scmoe_ctx* c, const MlaAttnArgs& a, int batches) {
     {
         ProfScope _p(c, "mla_softmax");
         const size_t rows = (size_t)z * h.nq;
-        mla_softmax_kernel<<<(unsigned)ceil_div(rows, 8), 256, 0, c->stream>>>(h.att, (int)rows,
-                                                                              h.nq, h.nk, h.q0);
+        mla_softmax_kernel<<<(unsigned)ceil_div(rows, 256), 256, 0, c->stream>>>(
+            h.att, h.part_max, (int)rows, h.nq, h.nk, h.q0);
         SCMOE_LAUNCH_CHECK(c);
     }
     {

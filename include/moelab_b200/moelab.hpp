@@ -510,4 +510,114 @@ Tensor<S> moe_forward(const Tensor<S>& x, const RoutingDecision& dd, const Exper
     return out;
 }
 
+// ---- multi-head latent attention (blocks.hpp:19-181), S = float ----------------
+inline std::pair<double, double> mla_scale_factors(std::size_t d_model, std::size_t d_q,
+                                                   std::size_t d_kv) {
+    if (d_model == 0 || d_q == 0 || d_kv == 0)
+        throw ParameterError("mla_scale_factors: dims must be positive");
+    return {std::sqrt(static_cast<double>(d_model) / static_cast<double>(d_q)),
+            std::sqrt(static_cast<double>(d_model) / static_cast<double>(d_kv))};
+}
+
+template <typename S>
+struct MlaParams {
+    std::size_t d_model = 0, d_q = 0, d_kv = 0;
+    std::size_t n_heads = 0, d_head_c = 0, d_head_r = 0;
+    double rope_base = 1.0e6;
+    bool variance_alignment = true;
+    Parameter<S>* w_dq = nullptr;   // [d_model, d_q]
+    Parameter<S>* w_uq = nullptr;   // [d_q, n_heads*d_head_c]
+    Parameter<S>* w_qr = nullptr;   // [d_q, n_heads*d_head_r]
+    Parameter<S>* w_dkv = nullptr;  // [d_model, d_kv]
+    Parameter<S>* w_uk = nullptr;   // [d_kv, n_heads*d_head_c]
+    Parameter<S>* w_uv = nullptr;   // [d_kv, n_heads*d_head_c]
+    Parameter<S>* w_kr = nullptr;   // [d_model, d_head_r]
+    Parameter<S>* w_o = nullptr;    // [n_heads*d_head_c, d_model]
+    double alpha_q() const {
+        return variance_alignment ? mla_scale_factors(d_model, d_q, d_kv).first : 1.0;
+    }
+    double alpha_kv() const {
+        return variance_alignment ? mla_scale_factors(d_model, d_q, d_kv).second : 1.0;
+    }
+};
+
+namespace b200 {
+// Device copy of an MlaParams<float>, keyed on its address + a weight fingerprint.
+inline scmoe_mla* mla_of(const MlaParams<float>& p) {
+    static thread_local std::map<const void*, std::pair<std::uint64_t, scmoe_mla*>> cache;
+    Device& d = device();
+    Parameter<float>* const ws[8] = {p.w_dq, p.w_uq, p.w_qr, p.w_dkv, p.w_uk, p.w_uv, p.w_kr, p.w_o};
+    std::uint64_t fp = CounterRng::hash2(p.d_model * 131 + p.d_q * 17 + p.d_kv,
+                                         p.n_heads * 1009 + p.d_head_c * 31 + p.d_head_r);
+    fp = CounterRng::hash2(fp, static_cast<std::uint64_t>(p.rope_base) * 2 + p.variance_alignment);
+    for (auto* w : ws) {
+        check(w != nullptr, "mla: missing weight");
+        fp = CounterRng::hash2(fp, fingerprint(w->value.data.data(),
+                                               w->value.data.size() * sizeof(float)));
+    }
+    auto it = cache.find(&p);
+    if (it != cache.end() && it->second.first == fp) return it->second.second;
+    if (it != cache.end()) scmoe_mla_destroy(d.ctx, it->second.second);
+    scmoe_mla* m = nullptr;
+    d.ok(scmoe_mla_create(d.ctx, p.d_model, p.d_q, p.d_kv, p.n_heads, p.d_head_c, p.d_head_r,
+                          p.rope_base, p.variance_alignment ? 1 : 0, &m));
+    for (int i = 0; i < 8; ++i) d.ok(scmoe_mla_set_weight_host(d.ctx, m, i, ws[i]->value.data.data()));
+    cache[&p] = {fp, m};
+    return m;
+}
+}  // namespace b200
+
+// Value of mla_block (blocks.hpp:73-102) over packed sequences of seq_len rows
+// -- what a forward-only caller of the Graph op gets, bitwise.
+inline Tensor<float> mla_forward(const MlaParams<float>& p, const Tensor<float>& h,
+                                 std::size_t seq_len) {
+    check(h.ndim() == 2 && h.cols() == p.d_model, "mla_block: bad input shape");
+    Tensor<float> out({h.rows(), p.d_model});
+    auto& d = b200::device();
+    d.ok(scmoe_mla_forward_host(d.ctx, b200::mla_of(p), h.data.data(), h.rows(), seq_len,
+                                out.data.data()));
+    return out;
+}
+
+// MlaCache (blocks.hpp:106-112): the host mirror of the compressed stream plus
+// the device-resident cache the steps run on.
+template <typename S>
+struct MlaCache {
+    Tensor<S> c_kv;  // [n, d_kv]
+    Tensor<S> k_r;   // [n, d_head_r], already rotated
+    std::shared_ptr<scmoe_mla_cache> dev;
+    std::size_t length() const { return c_kv.ndim() == 2 ? c_kv.rows() : 0; }
+};
+
+// One decode step at `position` (blocks.hpp:129-181); the cache must hold
+// exactly `position` rows.
+inline Tensor<float> mla_infer_step(const MlaParams<float>& p, MlaCache<float>& cache,
+                                    const Tensor<float>& h_t, std::size_t position) {
+    check(h_t.ndim() == 2 && h_t.rows() == 1 && h_t.cols() == p.d_model,
+          "mla_infer_step: bad input shape");
+    if (cache.length() != position)
+        throw StateError("mla_infer_step: cache holds " + std::to_string(cache.length()) +
+                         " rows but position is " + std::to_string(position));
+    auto& d = b200::device();
+    scmoe_mla* m = b200::mla_of(p);
+    if (!cache.dev) {
+        check(position == 0, "mla_infer_step: cache was filled elsewhere");
+        scmoe_mla_cache* k = nullptr;
+        d.ok(scmoe_mla_cache_create(d.ctx, m, 256, &k));
+        scmoe_ctx* ctx = d.ctx;
+        cache.dev = std::shared_ptr<scmoe_mla_cache>(k, [ctx](scmoe_mla_cache* q) {
+            scmoe_mla_cache_destroy(ctx, q);
+        });
+    }
+    Tensor<float> out({1, p.d_model});
+    d.ok(scmoe_mla_infer_step_host(d.ctx, m, cache.dev.get(), h_t.data.data(), position,
+                                   out.data.data()));
+    const std::size_t n = position + 1;
+    Tensor<float> ckv({n, p.d_kv}), kr({n, p.d_head_r});
+    d.ok(scmoe_mla_cache_read_host(d.ctx, m, cache.dev.get(), ckv.data.data(), kr.data.data()));
+    cache.c_kv = std::move(ckv);
+    cache.k_r = std::move(kr);
+    return out;
+}
+
 }  // namespace moelab

@@ -1494,7 +1494,14 @@ void mla_ensure_rope(scmoe_ctx* c, scmoe_mla* m, size_t npos) {
 void mla_gemm(scmoe_ctx* c, DevBuf& tiles_buf, const float* A, size_t lda, size_t rows,
               const float* B, size_t K, size_t N, float* C, size_t ldc) {
     if (rows == 0 || N == 0) return;
-    const int tr = seq_gemm_tile_rows(rows, N, c->num_sms);
+    // 128 x 128 tiles (8 x 8 chains per thread) once they fill two waves
+    static const bool big_ok = [] {
+        const char* e = getenv("SCMOE_MLA_TILE");
+        return !(e && atoi(e) == 64);
+    }();
+    const int tr = big_ok && ceil_div(rows, 128) * ceil_div(N, 128) >= (size_t)c->num_sms * 2
+                       ? 128
+                       : seq_gemm_tile_rows(rows, N, c->num_sms);
     const size_t ntile = ceil_div(rows, tr);
     TokenTile* tiles = tiles_buf.get<TokenTile>(ntile + 1);
     int* ntd = reinterpret_cast<int*>(tiles + ntile);

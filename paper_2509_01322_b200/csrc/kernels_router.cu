@@ -131,9 +131,9 @@ void launch_rmsnorm(scmoe_ctx* c, const float* x, const float* gain, size_t rows
 // (a_rows) and grouped (tiles: expert, first row, row count), which serves
 // both the router projection (one group) and the fp32 expert FFN.
 // ---------------------------------------------------------------------------
-constexpr int kSeqKC = 32, kSeqPad = 4;
+constexpr int kSeqPad = 4;
 
-template <int TM, int TN, int RM, int RN, bool kSilu>
+template <int TM, int TN, int RM, int RN, bool kSilu, int kSeqKC = 32>
 __global__ void __launch_bounds__((TM / RM) * (TN / RN)) seq_gemm_kernel(
     const float* __restrict__ A, size_t lda, const int* __restrict__ a_rows,
     const float* __restrict__ B, size_t ldb, size_t b_group_stride, float* __restrict__ C,
@@ -145,8 +145,8 @@ __global__ void __launch_bounds__((TM / RM) * (TN / RN)) seq_gemm_kernel(
     constexpr int B4 = kSeqKC * TN / 4;     // float4 per B chunk
     constexpr int AL = (A4 + NT - 1) / NT;  // per-thread loads
     constexpr int BL = (B4 + NT - 1) / NT;
-    static_assert(RM == 2 || RM == 4, "RM");
-    static_assert(RN == 4, "RN");
+    static_assert(RM == 2 || RM == 4 || RM == 8, "RM");
+    static_assert(RN == 4 || RN == 8, "RN");
     __shared__ __align__(16) float As[2][kSeqKC][TM + kSeqPad];
     __shared__ __align__(16) float Bs[2][kSeqKC][TN + kSeqPad];
 
@@ -252,15 +252,23 @@ __global__ void __launch_bounds__((TM / RM) * (TN / RN)) seq_gemm_kernel(
 #pragma unroll 4
             for (int k = 0; k < kc; ++k) {
                 float av[RM];
-                if constexpr (RM == 4) {
-                    const float4 a = *reinterpret_cast<const float4*>(&As[buf][k][RM * ty]);
-                    av[0] = a.x; av[1] = a.y; av[2] = a.z; av[3] = a.w;
+                if constexpr (RM >= 4) {
+#pragma unroll
+                    for (int q = 0; q < RM / 4; ++q) {
+                        const float4 a = *reinterpret_cast<const float4*>(&As[buf][k][RM * ty + 4 * q]);
+                        av[4 * q] = a.x; av[4 * q + 1] = a.y; av[4 * q + 2] = a.z; av[4 * q + 3] = a.w;
+                    }
                 } else {
                     const float2 a = *reinterpret_cast<const float2*>(&As[buf][k][RM * ty]);
                     av[0] = a.x; av[1] = a.y;
                 }
-                const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(&Bs[buf][k][RN * tx]);
-                const uint64_t bv[2] = {b.x, b.y};
+                uint64_t bv[RN / 2];
+#pragma unroll
+                for (int q = 0; q < RN / 4; ++q) {
+                    const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(&Bs[buf][k][RN * tx + 4 * q]);
+                    bv[2 * q] = b.x;
+                    bv[2 * q + 1] = b.y;
+                }
 #pragma unroll
                 for (int i = 0; i < RM; ++i)
 #pragma unroll
@@ -286,9 +294,11 @@ __global__ void __launch_bounds__((TM / RM) * (TN / RN)) seq_gemm_kernel(
             if (r >= tile.count) continue;
             float* crow = C + (size_t)(tile.pos + r) * ldc;
             const int col = col0 + RN * tx;
-            if (!kSilu && col + 3 < N && ((reinterpret_cast<uintptr_t>(crow + col) & 15) == 0)) {
-                *reinterpret_cast<float4*>(crow + col) =
-                    make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+            if (!kSilu && col + RN - 1 < N && ((reinterpret_cast<uintptr_t>(crow + col) & 15) == 0)) {
+#pragma unroll
+                for (int q = 0; q < RN / 4; ++q)
+                    *reinterpret_cast<float4*>(crow + col + 4 * q) =
+                        make_float4(acc[i][4 * q], acc[i][4 * q + 1], acc[i][4 * q + 2], acc[i][4 * q + 3]);
             } else {
 #pragma unroll
                 for (int j = 0; j < RN; ++j)
@@ -577,7 +587,7 @@ void launch_router_slab(scmoe_ctx* c, const float* X, const float* W, float* log
     SCMOE_LAUNCH_CHECK(c);
 }
 
-template <int TM, int TN, int RM, int RN>
+template <int TM, int TN, int RM, int RN, int KC = 32>
 static void seq_gemm_dispatch(scmoe_ctx* c, const float* A, size_t lda, const int* a_rows,
                               const float* B, size_t ldb, size_t b_group_stride, float* C,
                               size_t ldc, size_t K, size_t N, int silu, const TokenTile* tiles,
@@ -585,11 +595,11 @@ static void seq_gemm_dispatch(scmoe_ctx* c, const float* A, size_t lda, const in
     constexpr int NT = (TM / RM) * (TN / RN);
     dim3 grid((unsigned)ceil_div(N, TN), (unsigned)std::min<size_t>(max_tiles, 65535));
     if (silu)
-        seq_gemm_kernel<TM, TN, RM, RN, true><<<grid, NT, 0, c->stream>>>(
+        seq_gemm_kernel<TM, TN, RM, RN, true, KC><<<grid, NT, 0, c->stream>>>(
             A, lda, a_rows, B, ldb, b_group_stride, C, ldc, (int)K, (int)N, tiles, n_tiles_dev,
             (int)max_tiles);
     else
-        seq_gemm_kernel<TM, TN, RM, RN, false><<<grid, NT, 0, c->stream>>>(
+        seq_gemm_kernel<TM, TN, RM, RN, false, KC><<<grid, NT, 0, c->stream>>>(
             A, lda, a_rows, B, ldb, b_group_stride, C, ldc, (int)K, (int)N, tiles, n_tiles_dev,
             (int)max_tiles);
     SCMOE_LAUNCH_CHECK(c);
@@ -607,7 +617,10 @@ void launch_seq_gemm(scmoe_ctx* c, const float* A, size_t lda, const int* a_rows
                      int silu, const TokenTile* tiles, const int* n_tiles_dev, size_t max_tiles,
                      int tile_rows) {
     if (max_tiles == 0 || N == 0) return;
-    if (tile_rows == 64)
+    if (tile_rows == 128)  // 128 x 128 tiles, 8 x 8 chains per thread (large GEMMs)
+        seq_gemm_dispatch<128, 128, 8, 8, 16>(c, A, lda, a_rows, B, ldb, b_group_stride, C, ldc, K,
+                                               N, silu, tiles, n_tiles_dev, max_tiles);
+    else if (tile_rows == 64)
         seq_gemm_dispatch<64, 64, 4, 4>(c, A, lda, a_rows, B, ldb, b_group_stride, C, ldc, K, N,
                                         silu, tiles, n_tiles_dev, max_tiles);
     else if (tile_rows == 16)

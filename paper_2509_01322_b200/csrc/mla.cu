@@ -17,6 +17,8 @@
 //     w = e / denom; out = sequential sum over keys of w * v.
 // Compiled with --fmad=false; packed f32x2 chains use the half-swapped add
 // (f32x2.cuh), so nothing is contracted (build.py checks the SASS).
+#include <cstdlib>
+
 #include "f32x2.cuh"
 #include "internal.cuh"
 #include "libm_port.h"
@@ -316,6 +318,257 @@ __global__ void __launch_bounds__((TM / RM) * 16) mla_pv_kernel(MlaAttnArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Large-batch variants: 128 x 128 CTA tiles, 8 x 8 chains per thread (256
+// threads), chunks of 16 along the dot length staged through shared memory
+// with a register double buffer (the next chunk's global loads are in flight
+// during the current chunk's arithmetic).  Same per-output operation order as
+// the kernels above.
+// ---------------------------------------------------------------------------
+constexpr int kBT = 128, kBK = 16, kBPad = 4, kBThreads = 256;
+
+// A [128 rows][16 k] chunk from row-major storage (row stride ld), rows
+// clipped at n_rows, k clipped at kc; 2 float4 per thread.
+struct ChunkRegs {
+    float4 v[2];
+};
+__device__ __forceinline__ void load_rows_chunk(ChunkRegs& R, const float* base, size_t ld,
+                                                int n_rows, int kc, int tid) {
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+        const int i = tid + l * kBThreads;
+        const int r = i >> 2, kk = 4 * (i & 3);
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (r < n_rows) {
+            const float* src = base + (size_t)r * ld + kk;
+            if (kk + 3 < kc && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+                v = *reinterpret_cast<const float4*>(src);
+            } else {
+                if (kk + 0 < kc) v.x = src[0];
+                if (kk + 1 < kc) v.y = src[1];
+                if (kk + 2 < kc) v.z = src[2];
+                if (kk + 3 < kc) v.w = src[3];
+            }
+        }
+        R.v[l] = v;
+    }
+}
+__device__ __forceinline__ void store_rows_chunk_T(const ChunkRegs& R, float (*S)[kBT + kBPad],
+                                                   int tid) {
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+        const int i = tid + l * kBThreads;
+        const int r = i >> 2, kk = 4 * (i & 3);
+        S[kk + 0][r] = R.v[l].x;
+        S[kk + 1][r] = R.v[l].y;
+        S[kk + 2][r] = R.v[l].z;
+        S[kk + 3][r] = R.v[l].w;
+    }
+}
+
+__device__ __forceinline__ void mma_chunk_8x8(uint64_t (&acc2)[8][4], const float (*As)[kBT + kBPad],
+                                              const float (*Bs)[kBT + kBPad], int kc, int ty,
+                                              int tx) {
+#pragma unroll 4
+    for (int k = 0; k < kc; ++k) {
+        const float4 a0 = *reinterpret_cast<const float4*>(&As[k][8 * ty]);
+        const float4 a1 = *reinterpret_cast<const float4*>(&As[k][8 * ty + 4]);
+        const ulonglong2 b0 = *reinterpret_cast<const ulonglong2*>(&Bs[k][8 * tx]);
+        const ulonglong2 b1 = *reinterpret_cast<const ulonglong2*>(&Bs[k][8 * tx + 4]);
+        const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        const uint64_t bv[4] = {b0.x, b0.y, b1.x, b1.y};
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                acc2[i][q] = f2_add_swapped(acc2[i][q], f2_mul_bcast(av[i], bv[q]));
+    }
+}
+
+__global__ void __launch_bounds__(kBThreads, 2) mla_scores_big_kernel(MlaAttnArgs a) {
+    __shared__ __align__(16) float As[2][kBK][kBT + kBPad];
+    __shared__ __align__(16) float Bs[2][kBK][kBT + kBPad];
+    const int bh = blockIdx.z, b = bh / a.H, h = bh % a.H;
+    const int i0 = blockIdx.y * kBT, j0 = blockIdx.x * kBT;
+    const int i_last = min(a.nq, i0 + kBT) - 1;
+    if (j0 > a.q0 + i_last) return;  // tile entirely above the causal diagonal
+    const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+    const float* qc = a.qc + ((size_t)b * a.nq + i0) * a.ldq + (size_t)h * a.dhc;
+    const float* qr = a.qr + ((size_t)b * a.nq + i0) * a.ldq + (size_t)h * a.dhr;
+    const float* kc = a.kc + ((size_t)b * a.nk + j0) * a.ldkv + (size_t)h * a.dhc;
+    const float* kr = a.kr + ((size_t)b * a.nk + j0) * a.ldkr;
+    const int nqr = a.nq - i0, nkr = a.nk - j0;
+    const int nc_c = (a.dhc + kBK - 1) / kBK, nch = nc_c + (a.dhr + kBK - 1) / kBK;
+    auto load = [&](ChunkRegs& RA, ChunkRegs& RB, int ch, int& kcnt) {
+        if (ch < nc_c) {
+            const int k0 = ch * kBK;
+            kcnt = min(kBK, a.dhc - k0);
+            load_rows_chunk(RA, qc + k0, a.ldq, nqr, kcnt, tid);
+            load_rows_chunk(RB, kc + k0, a.ldkv, nkr, kcnt, tid);
+        } else {
+            const int k0 = (ch - nc_c) * kBK;
+            kcnt = min(kBK, a.dhr - k0);
+            load_rows_chunk(RA, qr + k0, a.ldq, nqr, kcnt, tid);
+            load_rows_chunk(RB, kr + k0, a.ldkr, nkr, kcnt, tid);
+        }
+    };
+    uint64_t acc2[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc2[i][q] = 0;
+    ChunkRegs RA, RB;
+    int kcur = 0, knext = 0;
+    load(RA, RB, 0, kcur);
+    store_rows_chunk_T(RA, As[0], tid);
+    store_rows_chunk_T(RB, Bs[0], tid);
+    __syncthreads();
+    for (int ch = 0; ch < nch; ++ch) {
+        const int buf = ch & 1;
+        const bool more = ch + 1 < nch;
+        if (more) load(RA, RB, ch + 1, knext);
+        mma_chunk_8x8(acc2, As[buf], Bs[buf], kcur, ty, tx);
+        if (more) {
+            store_rows_chunk_T(RA, As[buf ^ 1], tid);
+            store_rows_chunk_T(RB, Bs[buf ^ 1], tid);
+        }
+        __syncthreads();
+        kcur = knext;
+    }
+    float* att = a.att + (size_t)bh * a.nq * a.nk;
+    const int nkt = (a.nk + kMlaTN - 1) / kMlaTN;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int qi = i0 + 8 * ty + i;
+        float mx = -INFINITY;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float pr[2] = {f2_hi(acc2[i][q]), f2_lo(acc2[i][q])};
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int j = j0 + 8 * tx + 2 * q + u;
+                if (qi < a.nq && j < a.nk && j <= a.q0 + qi) {
+                    const float v = __fmul_rn(pr[u], a.scale);
+                    att[(size_t)qi * a.nk + j] = v;
+                    mx = fmaxf(mx, v);
+                }
+            }
+        }
+        // row max per 64-key part: threads tx 0-7 hold part 2x, tx 8-15 part 2x+1
+#pragma unroll
+        for (int o = 4; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        const int part = 2 * blockIdx.x + (tx >> 3);
+        if ((tx & 7) == 0 && qi < a.nq && part < nkt)
+            a.part_max[((size_t)bh * a.nq + qi) * nkt + part] = mx;
+    }
+}
+
+// PV on 128-query x 128-column tiles (d_head_c <= 128 -> one column tile, the
+// weights are read once).
+__global__ void __launch_bounds__(kBThreads, 2) mla_pv_big_kernel(MlaAttnArgs a) {
+    __shared__ __align__(16) float As[2][kBK][kBT + kBPad];
+    __shared__ __align__(16) float Bs[2][kBK][kBT + kBPad];
+    const int bh = blockIdx.z, b = bh / a.H, h = bh % a.H;
+    const int i0 = blockIdx.y * kBT, c0 = blockIdx.x * kBT;
+    if (i0 >= a.nq) return;
+    const int i_last = min(a.nq, i0 + kBT) - 1;
+    const int jmax = min(a.nk, a.q0 + i_last + 1);
+    const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+    const float* att = a.att + ((size_t)bh * a.nq + i0) * a.nk;
+    const float* vb = a.v + (size_t)b * a.nk * a.ldkv + (size_t)h * a.dhc + c0;
+    const int ncol = min(kBT, a.dhc - c0), nqr = a.nq - i0;
+    // V chunk [16 keys][128 cols]: 2 float4 per thread
+    auto load_v = [&](ChunkRegs& R, int k0, int kc) {
+#pragma unroll
+        for (int l = 0; l < 2; ++l) {
+            const int i = tid + l * kBThreads;
+            const int k = i >> 5, c4 = 4 * (i & 31);
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (k < kc) {
+                const float* src = vb + (size_t)(k0 + k) * a.ldkv + c4;
+                if (c4 + 3 < ncol && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+                    v = *reinterpret_cast<const float4*>(src);
+                } else {
+                    if (c4 + 0 < ncol) v.x = src[0];
+                    if (c4 + 1 < ncol) v.y = src[1];
+                    if (c4 + 2 < ncol) v.z = src[2];
+                    if (c4 + 3 < ncol) v.w = src[3];
+                }
+            }
+            R.v[l] = v;
+        }
+    };
+    auto store_v = [&](const ChunkRegs& R, float (*S)[kBT + kBPad]) {
+#pragma unroll
+        for (int l = 0; l < 2; ++l) {
+            const int i = tid + l * kBThreads;
+            *reinterpret_cast<float4*>(&S[i >> 5][4 * (i & 31)]) = R.v[l];
+        }
+    };
+    uint64_t acc2[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc2[i][q] = 0;
+    int lim[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) lim[i] = a.q0 + i0 + 8 * ty + i;
+    const int nch = (jmax + kBK - 1) / kBK;
+    ChunkRegs RA, RB;
+    load_rows_chunk(RA, att, a.nk, nqr, min(kBK, jmax), tid);
+    load_v(RB, 0, min(kBK, jmax));
+    store_rows_chunk_T(RA, As[0], tid);
+    store_v(RB, Bs[0]);
+    __syncthreads();
+    for (int ch = 0; ch < nch; ++ch) {
+        const int buf = ch & 1, k0 = ch * kBK, kc = min(kBK, jmax - k0);
+        const bool more = ch + 1 < nch;
+        if (more) {
+            const int k1 = k0 + kBK, kc1 = min(kBK, jmax - k1);
+            load_rows_chunk(RA, att + k1, a.nk, nqr, kc1, tid);
+            load_v(RB, k1, kc1);
+        }
+        if (k0 + kc - 1 <= a.q0 + i0) {  // every row of the tile sees the whole chunk
+            mma_chunk_8x8(acc2, As[buf], Bs[buf], kc, ty, tx);
+        } else {
+            for (int k = 0; k < kc; ++k) {
+                const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][k][8 * ty]);
+                const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][k][8 * ty + 4]);
+                const ulonglong2 b0 = *reinterpret_cast<const ulonglong2*>(&Bs[buf][k][8 * tx]);
+                const ulonglong2 b1 = *reinterpret_cast<const ulonglong2*>(&Bs[buf][k][8 * tx + 4]);
+                const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                const uint64_t bv[4] = {b0.x, b0.y, b1.x, b1.y};
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const bool on = k0 + k <= lim[i];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint64_t nv = f2_add_swapped(acc2[i][q], f2_mul_bcast(av[i], bv[q]));
+                        acc2[i][q] = on ? nv : acc2[i][q];
+                    }
+                }
+            }
+        }
+        if (more) {
+            store_rows_chunk_T(RA, As[buf ^ 1], tid);
+            store_v(RB, Bs[buf ^ 1]);
+        }
+        __syncthreads();
+    }
+    float* mb = a.merged + ((size_t)b * a.nq + i0) * a.ldm + (size_t)h * a.dhc + c0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int r = 8 * ty + i;
+        if (r >= nqr) continue;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int col = 8 * tx + 2 * q;
+            if (col < ncol) mb[(size_t)r * a.ldm + col] = f2_hi(acc2[i][q]);
+            if (col + 1 < ncol) mb[(size_t)r * a.ldm + col + 1] = f2_lo(acc2[i][q]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Launchers.
 // ---------------------------------------------------------------------------
 void launch_mla_scale_rope(scmoe_ctx* c, float* X, size_t ld, size_t rows, int n_a, float alpha_a,
@@ -333,10 +586,18 @@ void launch_mla_scale_rope(scmoe_ctx* c, float* X, size_t ld, size_t rows, int n
 void launch_mla_attention(scmoe_ctx* c, const MlaAttnArgs& a, int batches) {
     const MlaAttnArgs& h = a;
     const unsigned z = (unsigned)(batches * h.H);
+    static const bool tiles128 = [] {
+        const char* e = getenv("SCMOE_MLA_TILE");
+        return !(e && atoi(e) == 64);
+    }();
+    const bool huge = tiles128 && h.nq >= 128;
     const bool big = h.nq >= 64;
     {
         ProfScope _p(c, "mla_scores");
-        if (big) {
+        if (huge) {
+            dim3 grid((unsigned)ceil_div(h.nk, kBT), (unsigned)ceil_div(h.nq, kBT), z);
+            mla_scores_big_kernel<<<grid, kBThreads, 0, c->stream>>>(a);
+        } else if (big) {
             dim3 grid((unsigned)ceil_div(h.nk, kMlaTN), (unsigned)ceil_div(h.nq, 64), z);
             mla_scores_kernel<64, 4><<<grid, 256, 0, c->stream>>>(a);
         } else {
@@ -354,7 +615,10 @@ void launch_mla_attention(scmoe_ctx* c, const MlaAttnArgs& a, int batches) {
     }
     {
         ProfScope _p(c, "mla_pv");
-        if (big) {
+        if (huge) {
+            dim3 grid((unsigned)ceil_div(h.dhc, kBT), (unsigned)ceil_div(h.nq, kBT), z);
+            mla_pv_big_kernel<<<grid, kBThreads, 0, c->stream>>>(a);
+        } else if (big) {
             dim3 grid((unsigned)ceil_div(h.dhc, kMlaTN), (unsigned)ceil_div(h.nq, 64), z);
             mla_pv_kernel<64, 4><<<grid, 256, 0, c->stream>>>(a);
         } else {

@@ -240,6 +240,66 @@ static void closed_loop_controller() {  // test_router.cpp:269-283 (fp32 router)
     std::printf("closed loop: tail mean %.4f (target 4)\n", tail);
 }
 
+struct MlaFixtureF {  // test_blocks.cpp:27-66, S = float
+    std::vector<Parameter<float>> store;
+    MlaParams<float> p;
+    MlaFixtureF(std::size_t d, std::size_t dq, std::size_t dkv, std::size_t H, std::size_t dhc,
+                std::size_t dhr, std::uint64_t seed, bool zero = false) {
+        p.d_model = d; p.d_q = dq; p.d_kv = dkv; p.n_heads = H; p.d_head_c = dhc; p.d_head_r = dhr;
+        p.rope_base = 1.0e4;
+        const std::vector<std::vector<std::size_t>> shp = {{d, dq}, {dq, H * dhc}, {dq, H * dhr},
+                                                           {d, dkv}, {dkv, H * dhc}, {dkv, H * dhc},
+                                                           {d, dhr}, {H * dhc, d}};
+        store.reserve(8);
+        for (std::size_t i = 0; i < 8; ++i)
+            store.emplace_back("w", zero ? Tensor<float>(shp[i])
+                                         : seeded_init<float>(shp[i], InitDistribution::TruncatedNormal,
+                                                              1.0 / d, CounterRng(seed).stream(i)));
+        p.w_dq = &store[0]; p.w_uq = &store[1]; p.w_qr = &store[2]; p.w_dkv = &store[3];
+        p.w_uk = &store[4]; p.w_uv = &store[5]; p.w_kr = &store[6]; p.w_o = &store[7];
+    }
+};
+
+static void mla_cases() {  // test_blocks.cpp:139-209 with MlaParams<float>
+    {
+        auto [aq, akv] = mla_scale_factors(6144, 1536, 512);
+        CHECK(std::fabs(aq - 2.0) <= 1e-15 && std::fabs(akv - std::sqrt(12.0)) <= 1e-12);
+        CHECK_THROWS_AS(mla_scale_factors(0, 1, 1), ParameterError);
+    }
+    {
+        MlaFixtureF fx(32, 8, 4, 4, 8, 4, 0, /*zero=*/true);
+        auto u = mla_forward(fx.p, random_tensor({4, 32}, 9), 4);
+        bool zero = u.shape == std::vector<std::size_t>{4, 32};
+        for (float v : u.data) zero = zero && v == 0.0f;
+        CHECK(zero);
+    }
+    {
+        // cached incremental decode == packed forward, bitwise in fp32
+        MlaFixtureF fx(16, 8, 4, 2, 6, 4, 3);
+        const Tensor<float> h = random_tensor({5, 16}, 1);
+        const Tensor<float> want = mla_forward(fx.p, h, 5);
+        MlaCache<float> cache;
+        bool same = true;
+        for (std::size_t t = 0; t < 5; ++t) {
+            Tensor<float> row({1, 16});
+            for (std::size_t j = 0; j < 16; ++j) row.data[j] = h.at(t, j);
+            Tensor<float> u = mla_infer_step(fx.p, cache, row, t);
+            for (std::size_t j = 0; j < 16; ++j) same = same && u.data[j] == want.at(t, j);
+        }
+        CHECK(same);
+        CHECK(cache.length() == 5);
+        CHECK_THROWS_AS(mla_forward(fx.p, h, 3), DimensionError);
+    }
+    {
+        MlaFixtureF fx(8, 4, 4, 1, 4, 2, 5);
+        MlaCache<float> cache;
+        Tensor<float> row({1, 8});
+        mla_infer_step(fx.p, cache, row, 0);
+        CHECK_THROWS_AS(mla_infer_step(fx.p, cache, row, 0), StateError);
+        CHECK_THROWS_AS(mla_infer_step(fx.p, cache, row, 5), StateError);
+    }
+}
+
 int main() {
     route_topk_double_full_path();
     moe_cases_double();
@@ -248,6 +308,7 @@ int main() {
     bias_update_rules();
     moe_cases();
     closed_loop_controller();
+    mla_cases();
     std::printf("compat: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail;
 }

@@ -15,7 +15,8 @@ SHAPES = [
     (16, 8, 4, 2, 6, 4, 5, 3),       # test_blocks.cpp:187-200
     (48, 24, 16, 3, 10, 6, 7, 2),    # ragged widths
     (256, 64, 32, 4, 32, 16, 96, 3),   # 64-query tiles, diagonal chunks
-    (128, 64, 32, 2, 72, 40, 200, 1),  # dhc > 64 (two value tiles), long rows
+    (128, 64, 32, 2, 72, 40, 200, 1),  # 128-tile kernels, partial column / k chunks
+    (192, 64, 32, 3, 128, 64, 260, 2),  # 128-tile kernels, LongCat head widths, 3 query tiles
 ]
 
 

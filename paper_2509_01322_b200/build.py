@@ -73,7 +73,7 @@ def check_sass(lib: str = LIB) -> dict:
     # The plain sequential-k GEMM (router projection, fp32 W_out GEMM) must be
     # pure FMUL + FADD.  The SiLU instantiation's only FFMAs come from the
     # correctly rounded IEEE division (__fdiv_rn) inside the logistic.
-    seq = [n for n in summary if re.search(r"seq_gemm_kernel.*Lb0EE", n)]
+    seq = [n for n in summary if re.search(r"seq_gemm_kernel.*Lb0E", n)]
     seq += [n for n in summary if re.search(r"router_(tma|slab|lean)_kernel", n)]
     # MLA: the scores / rope kernels are pure FMUL + FADD; the PV kernel's only
     # FFMAs are the correctly rounded divisions w = e / denom (__fdiv_rn) where

@@ -13,6 +13,7 @@
 //
 // Usable from host C/C++ (compile with -ffp-contract=off) and CUDA.
 #pragma once
+#include <stdbool.h>
 #include <stdint.h>
 #include <string.h>
 
@@ -70,27 +71,35 @@ SCMOE_HD uint64_t scmoe_d2u(double d) {
 #define SCMOE_D2F(x) ((float)(x))
 #endif
 
-// glibc 2.39 __expf, FMA build.
-SCMOE_HD float scmoe_expf(float x) {
-    const double kInvLn2N = 0x1.71547652b82fep+0 * 32;  // N/ln2
-    const double kShift = 0x1.8p+52;
-    const double kC0 = 0x1.c6af84b912394p-5 / 32 / 32 / 32;
-    const double kC1 = 0x1.ebfce50fac4f3p-3 / 32 / 32;
-    const double kC2 = 0x1.62e42ff0c52d6p-1 / 32;
+// glibc 2.39 __expf, FMA build, with the table lookup factored out so a kernel
+// can read the 32 entries from shared memory (divergent indices serialise on
+// the constant cache).  scmoe_expf_special handles |x| >= 88 and non-finite x.
+SCMOE_HD bool scmoe_expf_special(float x, float* out) {
     const uint32_t ux = scmoe_f2u(x);
     const uint32_t abstop = (ux >> 20) & 0x7ff;
     if (abstop >= 0x42b) {                       // |x| >= 88 or non-finite
-        if (ux == 0xff800000u) return 0.0f;      // -inf
-        if (abstop >= 0x7f8) return x + x;       // +inf or nan
-        if (x > 0x1.62e42ep6f) return __builtin_huge_valf();  // overflow
-        if (x < -0x1.9fe368p6f) return 0.0f;     // underflow (x < log(2^-150))
+        if (ux == 0xff800000u) { *out = 0.0f; return true; }       // -inf
+        if (abstop >= 0x7f8) { *out = x + x; return true; }         // +inf or nan
+        if (x > 0x1.62e42ep6f) { *out = __builtin_huge_valf(); return true; }  // overflow
+        if (x < -0x1.9fe368p6f) { *out = 0.0f; return true; }       // underflow
     }
+    return false;
+}
+// kd, ki and r of the reduction; the caller looks up T[ki % 32].
+SCMOE_HD void scmoe_expf_reduce(float x, uint64_t* ki_out, double* r_out) {
+    const double kInvLn2N = 0x1.71547652b82fep+0 * 32;  // N/ln2
+    const double kShift = 0x1.8p+52;
     const double xd = (double)x;
     double kd = SCMOE_FMA(kInvLn2N, xd, kShift);  // z + SHIFT, contracted
-    const uint64_t ki = scmoe_d2u(kd);
+    *ki_out = scmoe_d2u(kd);
     kd = SCMOE_DSUB(kd, kShift);
-    const double r = SCMOE_FMA(kInvLn2N, xd, -kd);  // z - kd, contracted
-    uint64_t t = SCMOE_TAB(ki % 32);
+    *r_out = SCMOE_FMA(kInvLn2N, xd, -kd);  // z - kd, contracted
+}
+SCMOE_HD float scmoe_expf_finish(uint64_t ki, double r, uint64_t tab_entry) {
+    const double kC0 = 0x1.c6af84b912394p-5 / 32 / 32 / 32;
+    const double kC1 = 0x1.ebfce50fac4f3p-3 / 32 / 32;
+    const double kC2 = 0x1.62e42ff0c52d6p-1 / 32;
+    uint64_t t = tab_entry;
     t += ki << 47;
     const double s = scmoe_u2d(t);
     const double z = SCMOE_FMA(kC0, r, kC1);
@@ -100,6 +109,25 @@ SCMOE_HD float scmoe_expf(float x) {
     y = SCMOE_DMUL(y, s);
     return SCMOE_D2F(y);
 }
+SCMOE_HD float scmoe_expf(float x) {
+    float sp;
+    if (scmoe_expf_special(x, &sp)) return sp;
+    uint64_t ki;
+    double r;
+    scmoe_expf_reduce(x, &ki, &r);
+    return scmoe_expf_finish(ki, r, SCMOE_TAB(ki % 32));
+}
+#if defined(__CUDACC__)
+// Same function, table in shared memory (tab = a copy of scmoe_exp2f_tab_dev).
+__device__ __forceinline__ float scmoe_expf_smem(float x, const uint64_t* tab) {
+    float sp;
+    if (scmoe_expf_special(x, &sp)) return sp;
+    uint64_t ki;
+    double r;
+    scmoe_expf_reduce(x, &ki, &r);
+    return scmoe_expf_finish(ki, r, tab[ki % 32]);
+}
+#endif
 
 // ---------------------------------------------------------------------------
 // glibc 2.39 exp (double), FMA ifunc variant (sysdeps/ieee754/dbl-64/e_exp.c,

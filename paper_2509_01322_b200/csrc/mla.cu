@@ -147,10 +147,13 @@ __global__ void __launch_bounds__((TM / RM) * 16) mla_scores_kernel(MlaAttnArgs 
 //           is loaded coalesced, transposed through shared memory, and lane l
 //           walks row l's 32 keys sequentially (the reference's fp32 sum);
 //   w_j   = e_j / denom (rounded division), coalesced, written in place.
-__global__ void __launch_bounds__(256) mla_softmax_kernel(float* __restrict__ att,
+__global__ void __launch_bounds__(256, 3) mla_softmax_kernel(float* __restrict__ att,
                                                           const float* __restrict__ part_max,
                                                           int rows_total, int nq, int nk, int q0) {
     __shared__ float tile[8][32][33];
+    __shared__ uint64_t exp_tab[32];
+    if (threadIdx.x < 32) exp_tab[threadIdx.x] = scmoe_exp2f_tab_dev[threadIdx.x];
+    __syncthreads();
     const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int r0 = (blockIdx.x * 8 + wib) * 32;
     if (r0 >= rows_total) return;
@@ -166,29 +169,35 @@ __global__ void __launch_bounds__(256) mla_softmax_kernel(float* __restrict__ at
     for (int t = 0; t < 32; ++t) nmax = max(nmax, __shfl_sync(0xffffffffu, n, t));
     float sum = 0.f;
     for (int j0 = 0; j0 < nmax; j0 += 32) {
-        float v[32];  // all 32 coalesced row segments in flight before the transpose
 #pragma unroll
-        for (int t = 0; t < 32; ++t) {
-            const int nt = __shfl_sync(0xffffffffu, n, t);
-            v[t] = (j0 + lane < nt) ? att[(size_t)(r0 + t) * nk + j0 + lane] : 0.f;
+        for (int t0 = 0; t0 < 32; t0 += 16) {
+            float v[16];  // 16 coalesced row segments in flight before the transpose
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+                const int nt = __shfl_sync(0xffffffffu, n, t0 + t);
+                v[t] = (j0 + lane < nt) ? att[(size_t)(r0 + t0 + t) * nk + j0 + lane] : 0.f;
+            }
+#pragma unroll
+            for (int t = 0; t < 16; ++t) T[t0 + t][lane] = v[t];
         }
-#pragma unroll
-        for (int t = 0; t < 32; ++t) T[t][lane] = v[t];
         __syncwarp();
         const int m = min(32, n - j0);
         if (m == 32) {
-            // 32 independent exponentials first (ILP), then the in-order sum
-            float e[32];
+            // 8 independent exponentials at a time (ILP), then the in-order sum
 #pragma unroll
-            for (int t = 0; t < 32; ++t) e[t] = scmoe_expf(__fsub_rn(T[lane][t], mx));
+            for (int t0 = 0; t0 < 32; t0 += 8) {
+                float e[8];
 #pragma unroll
-            for (int t = 0; t < 32; ++t) {
-                T[lane][t] = e[t];
-                sum = __fadd_rn(sum, e[t]);
+                for (int t = 0; t < 8; ++t) e[t] = scmoe_expf_smem(__fsub_rn(T[lane][t0 + t], mx), exp_tab);
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    T[lane][t0 + t] = e[t];
+                    sum = __fadd_rn(sum, e[t]);
+                }
             }
         } else {
             for (int t = 0; t < m; ++t) {
-                const float e = scmoe_expf(__fsub_rn(T[lane][t], mx));
+                const float e = scmoe_expf_smem(__fsub_rn(T[lane][t], mx), exp_tab);
                 T[lane][t] = e;
                 sum = __fadd_rn(sum, e);
             }

@@ -53,7 +53,7 @@ def test_no_device_means_loud_failure(built):
 def test_sass_properties(built):
     from paper_2509_01322_b200 import build as B
     summary = B.check_sass(built)
-    seq = [k for k in summary if re.search(r"seq_gemm_kernel.*Lb0EE", k)]
+    seq = [k for k in summary if re.search(r"seq_gemm_kernel.*Lb0E", k)]
     assert seq and all(summary[k]["FFMA"] == 0 for k in seq)
     gemm = [k for k in summary if "grouped_gemm_kernel" in k]
     assert gemm and all(summary[k]["UTCHMMA"] > 0 and summary[k]["UTMALDG"] > 0 and

@@ -657,6 +657,10 @@ __global__ void __launch_bounds__(256) softmax_topk_kernel(
     S* rows = reinterpret_cast<S*>(smem_raw + sizeof(double) * E);
     unsigned char* taken_all = smem_raw + sizeof(double) * E + sizeof(S) * E * 8;
 
+    // glibc-expf table in shared memory: lanes index it divergently, which
+    // serialises on the constant cache
+    __shared__ uint64_t exp_tab[32];
+    if (threadIdx.x < 32) exp_tab[threadIdx.x] = scmoe_exp2f_tab_dev[threadIdx.x];
     for (int j = threadIdx.x; j < E; j += blockDim.x) sbias[j] = bias ? bias[j] : 0.0;
     __syncthreads();
 
@@ -705,7 +709,7 @@ __global__ void __launch_bounds__(256) softmax_topk_kernel(
             const float other = __shfl_xor_sync(0xffffffffu, mx, o);
             mx = other > mx ? other : mx;
         }
-        for (int j = lane; j < E; j += 32) p[j] = scmoe_expf(__fsub_rn(row[j], mx));
+        for (int j = lane; j < E; j += 32) p[j] = scmoe_expf_smem(__fsub_rn(row[j], mx), exp_tab);
         __syncwarp();
         float sum = 0.0f;
         if (lane == 0) {

@@ -365,6 +365,20 @@ int scmoe_mla_infer_step(scmoe_ctx* ctx, scmoe_mla* m, scmoe_mla_cache* cache,
 int scmoe_mla_infer_step_host(scmoe_ctx* ctx, scmoe_mla* m, scmoe_mla_cache* cache,
                               const float* h_t, size_t position, float* out);
 
+/* ---- The full ScMoE layer (Model::build_layer, model.hpp:355-409) ----------
+ *   a1 = x + MLA1(rmsnorm(x, norm1));  dd = a1 + FFN(rmsnorm(a1, norm_ffn));
+ *   a3 = dd + MLA2(rmsnorm(dd, norm2)); out = a3 + moe(rmsnorm(a1, norm_moe)).
+ * MLA exact fp32, dense FFN (one-expert bf16 bank) and MoE (bank precision)
+ * as in the calls above.  overlap = 1 runs the MoE branch on a second stream
+ * beside the dense FFN and MLA2 (results identical).  a1_out / a3_out are
+ * optional [T, d] outputs; the routing outputs are as scmoe_layer_forward's. */
+int scmoe_layer_full_forward(scmoe_ctx* ctx, scmoe_mla* mla1, scmoe_mla* mla2, scmoe_bank* dense,
+                             scmoe_router* r, scmoe_bank* bank, const float* norm1,
+                             const float* norm_ffn, const float* norm2, const float* norm_moe,
+                             const float* x, size_t T, size_t seq_len, int renormalize,
+                             int overlap, uint32_t* indices, double* gates, uint32_t* ffn_count,
+                             float* a1_out, float* a3_out, float* out);
+
 /* ---- CounterRng (rng.hpp:15-64), host side, for synthetic inputs --------- */
 uint64_t scmoe_rng_stream_seed(uint64_t seed, uint64_t id);
 /* out[i] = (float) CounterRng(seed).normal_at(first + i)  (router.hpp:357-360) */

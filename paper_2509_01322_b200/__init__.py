@@ -182,6 +182,7 @@ _PROTOS = {
     "scmoe_mla_cache_read_host": (C.c_int, [_P, _P, _P, _P, _P]),
     "scmoe_mla_infer_step": (C.c_int, [_P, _P, _P, _P, _SZ, _P]),
     "scmoe_mla_infer_step_host": (C.c_int, [_P, _P, _P, _P, _SZ, _P]),
+    "scmoe_layer_full_forward": (C.c_int, [_P] * 11 + [_SZ, _SZ, C.c_int, C.c_int] + [_P] * 6),
 }
 
 

@@ -147,52 +147,62 @@ void moe_front(scmoe_ctx* c, scmoe_bank* b, const float* x, const __nv_bfloat16*
     }
 }
 
+// phase: 0 = expert FFN + combine, 1 = expert FFN only, 2 = combine only
+// (the full layer runs the FFN before its residual a3 exists).
 void moe_back(scmoe_ctx* c, scmoe_bank* b, const float* x, size_t T, const uint32_t* idx,
-              const double* gates, size_t K, int renorm, const float* residual, float* out) {
+              const double* gates, size_t K, int renorm, const float* residual, float* out,
+              int phase = 0) {
     const size_t n_ffn = b->n, d = b->d, I = b->inter;
     Workspace& ws = c->ws;
     PermResult pr;
     memcpy(&pr, ws.pr_blob, sizeof(pr));
     const float gf = (float)b->gamma_ffn(), gz = (float)b->gamma_zero();
+    const bool ffn = phase != 2, comb = phase != 1;
     if (b->precision == SCMOE_PREC_F32_EXACT) {
         float* h = ws.h.get<float>(T * K * I + 1);
         float* y = ws.y.get<float>(T * K * d + 1);
-        {
-            ProfScope _p(c, "expert_gemm1_f32");
-            launch_seq_gemm(c, x, d, pr.row_token, b->w_in32, I, d * I, h, I, d, I, /*silu=*/1,
-                            pr.tiles, pr.n_tiles, pr.max_tiles, 64);
-        }
-        {
+        if (ffn) {
+            {
+                ProfScope _p(c, "expert_gemm1_f32");
+                launch_seq_gemm(c, x, d, pr.row_token, b->w_in32, I, d * I, h, I, d, I, /*silu=*/1,
+                                pr.tiles, pr.n_tiles, pr.max_tiles, 64);
+            }
             ProfScope _p(c, "expert_gemm2_f32");
             launch_seq_gemm(c, h, I, nullptr, b->w_out32, d, I * d, y, d, I, d, /*silu=*/0,
                             pr.tiles, pr.n_tiles, pr.max_tiles, 64);
         }
-        ProfScope _p(c, "combine");
-        launch_combine_f32(c, x, y, idx, gates, pr.slot_pos, T, d, K, n_ffn, gf, gz, renorm,
-                           residual, out);
+        if (comb) {
+            ProfScope _p(c, "combine");
+            launch_combine_f32(c, x, y, idx, gates, pr.slot_pos, T, d, K, n_ffn, gf, gz, renorm,
+                               residual, out);
+        }
     } else {
         __nv_bfloat16* h = ws.h.get<__nv_bfloat16>(T * K * I + 1);
         __nv_bfloat16* y = ws.y.get<__nv_bfloat16>(T * K * d + 1);
-        if (c->gemm1_gather) {
-            // GEMM1 gathers its token rows straight from x (cp.async row gather).
-            ProfScope _p(c, "gemm1_tcgen05");
-            launch_grouped_gemm_bf16(c, b->w1t, n_ffn, I, d, ws.hmoe_bf16.get<__nv_bfloat16>(T * d),
-                                     T, pr.row_token, h, /*silu=*/1, pr.tiles, pr.n_tiles,
-                                     pr.max_tiles, tile_rows_for(b));
-        } else {
-            ProfScope _p(c, "gemm1_tcgen05");
-            launch_grouped_gemm_bf16(c, b->w1t, n_ffn, I, d, ws.xp.get<__nv_bfloat16>(T * K * d + 1),
-                                     T * K, nullptr, h, /*silu=*/1, pr.tiles, pr.n_tiles,
-                                     pr.max_tiles, tile_rows_for(b));
-        }
-        {
+        if (ffn) {
+            if (c->gemm1_gather) {
+                // GEMM1 gathers its token rows straight from x (cp.async row gather).
+                ProfScope _p(c, "gemm1_tcgen05");
+                launch_grouped_gemm_bf16(c, b->w1t, n_ffn, I, d,
+                                         ws.hmoe_bf16.get<__nv_bfloat16>(T * d), T, pr.row_token,
+                                         h, /*silu=*/1, pr.tiles, pr.n_tiles, pr.max_tiles,
+                                         tile_rows_for(b));
+            } else {
+                ProfScope _p(c, "gemm1_tcgen05");
+                launch_grouped_gemm_bf16(c, b->w1t, n_ffn, I, d,
+                                         ws.xp.get<__nv_bfloat16>(T * K * d + 1), T * K, nullptr,
+                                         h, /*silu=*/1, pr.tiles, pr.n_tiles, pr.max_tiles,
+                                         tile_rows_for(b));
+            }
             ProfScope _p(c, "gemm2_tcgen05");
             launch_grouped_gemm_bf16(c, b->w2t, n_ffn, d, I, h, T * K, nullptr, y, /*silu=*/0,
                                      pr.tiles, pr.n_tiles, pr.max_tiles, tile_rows_for(b));
         }
-        ProfScope _p(c, "combine");
-        launch_combine_bf16(c, x, y, idx, gates, pr.slot_pos, T, d, K, n_ffn, gf, gz, renorm,
-                            residual, out);
+        if (comb) {
+            ProfScope _p(c, "combine");
+            launch_combine_bf16(c, x, y, idx, gates, pr.slot_pos, T, d, K, n_ffn, gf, gz, renorm,
+                                residual, out);
+        }
     }
 }
 
@@ -328,6 +338,11 @@ int scmoe_ctx_destroy(scmoe_ctx* c) {
             cudaEventDestroy(c->ev_back[i]);
         }
         cudaEventDestroy(c->ev_join);
+    }
+    if (c->s_moe) {
+        cudaStreamSynchronize(c->s_moe);
+        cudaStreamDestroy(c->s_moe);
+        for (auto& e : c->ev_full) cudaEventDestroy(e);
     }
     if (c->s_h2d) {
         cudaStreamSynchronize(c->s_d2h);
@@ -1774,5 +1789,94 @@ int scmoe_mla_infer_step_host(scmoe_ctx* c, scmoe_mla* m, scmoe_mla_cache* k, co
         if (rc) throw ScmoeError{rc, c->last_error};
         download(c, out, dout, m->d);
         sync_and_check(c);
+    });
+}
+
+// ===========================================================================
+// The full ScMoE layer (Model::build_layer, model.hpp:355-409, one chunk):
+//   a1  = x  + MLA1(rmsnorm(x, norm1))
+//   dd  = a1 + FFN(rmsnorm(a1, norm_ffn))            (dense shortcut branch)
+//   a3  = dd + MLA2(rmsnorm(dd, norm2))
+//   out = a3 + moe(rmsnorm(a1, norm_moe))             (scmoe: MoE input is a1)
+// overlap = 1 runs the MoE branch (routing, permutation, expert FFN) on a
+// second stream as soon as a1 exists, beside the dense FFN and MLA2 -- the
+// shortcut connection's point (PAPER.md SBO); only the final combine waits
+// for a3.  Same results either way (every kernel is order-independent of the
+// schedule).
+// ===========================================================================
+int scmoe_layer_full_forward(scmoe_ctx* c, scmoe_mla* mla1, scmoe_mla* mla2, scmoe_bank* dense,
+                             scmoe_router* r, scmoe_bank* b, const float* norm1,
+                             const float* norm_ffn, const float* norm2, const float* norm_moe,
+                             const float* x, size_t T, size_t seq_len, int renorm, int overlap,
+                             uint32_t* idx, double* gates, uint32_t* ffn_count, float* a1_out,
+                             float* a3_out, float* out) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        check_layer_args(r, b);
+        if (!mla1 || !mla2 || !dense)
+            SCMOE_THROW(SCMOE_ERR_PARAMETER, "layer_full: null MLA / dense handle");
+        const size_t d = r->d;
+        if (mla1->d != d || mla2->d != d || dense->d != d)
+            SCMOE_THROW(SCMOE_ERR_DIMENSION, "layer_full: d_model mismatch");
+        if (seq_len == 0 || T % seq_len != 0)
+            SCMOE_THROW(SCMOE_ERR_DIMENSION, "attention: rows must pack whole sequences");
+        if (T == 0) return;
+        Workspace& ws = c->ws;
+        float* xn = ws.full_n.get<float>(T * d);
+        float* m = ws.full_m.get<float>(T * d);
+        float* a1 = a1_out ? a1_out : ws.full_a1.get<float>(T * d);
+        float* dd = ws.full_dd.get<float>(T * d);
+        float* a3 = a3_out ? a3_out : ws.full_a3.get<float>(T * d);
+        const cudaStream_t sa = c->stream;
+        auto run = [&](int rc) {
+            if (rc) throw ScmoeError{rc, c->last_error};
+        };
+        if (overlap && !c->s_moe) {
+            SCMOE_CUDA(cudaStreamCreateWithFlags(&c->s_moe, cudaStreamNonBlocking));
+            for (auto& e : c->ev_full) SCMOE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        const cudaStream_t sb = overlap ? c->s_moe : sa;
+        // a1 = x + MLA1(rmsnorm(x))
+        launch_rmsnorm(c, x, norm1, T, d, 1e-6f, xn, nullptr);
+        run(scmoe_mla_forward(c, mla1, xn, T, seq_len, m));
+        launch_add_f32(c, x, m, T * d, a1);
+        // MoE branch up to the expert outputs (stream b)
+        if (overlap) {
+            SCMOE_CUDA(cudaEventRecord(c->ev_full[0], sa));
+            SCMOE_CUDA(cudaStreamWaitEvent(sb, c->ev_full[0], 0));
+        }
+        c->stream = sb;
+        try {
+            layer_front(c, r, b, a1, norm_moe, T, idx, gates, ffn_count);
+            moe_back(c, b, ws.hmoe.get<float>(T * d), T, idx, gates, r->top_k, renorm, nullptr,
+                     nullptr, /*phase=*/1);
+        } catch (...) {
+            c->stream = sa;
+            throw;
+        }
+        c->stream = sa;
+        // dd = a1 + FFN(rmsnorm(a1)); a3 = dd + MLA2(rmsnorm(dd)) (stream a)
+        run(scmoe_dense_ffn(c, dense, a1, norm_ffn, T, dd));
+        launch_rmsnorm(c, dd, norm2, T, d, 1e-6f, xn, nullptr);
+        run(scmoe_mla_forward(c, mla2, xn, T, seq_len, m));
+        launch_add_f32(c, dd, m, T * d, a3);
+        // out = a3 + combine (stream b, after a3)
+        if (overlap) {
+            SCMOE_CUDA(cudaEventRecord(c->ev_full[1], sa));
+            SCMOE_CUDA(cudaStreamWaitEvent(sb, c->ev_full[1], 0));
+        }
+        c->stream = sb;
+        try {
+            moe_back(c, b, ws.hmoe.get<float>(T * d), T, idx, gates, r->top_k, renorm, a3, out,
+                     /*phase=*/2);
+        } catch (...) {
+            c->stream = sa;
+            throw;
+        }
+        c->stream = sa;
+        if (overlap) {
+            SCMOE_CUDA(cudaEventRecord(c->ev_full[2], sb));
+            SCMOE_CUDA(cudaStreamWaitEvent(sa, c->ev_full[2], 0));
+        }
     });
 }

@@ -71,13 +71,16 @@ struct Workspace {
     DevBuf dn_x, dn_h, dn_y, dn_tiles;
     // MLA (mla.cu): projections, scores/weights, merged heads, row tiles
     DevBuf mla_p1, mla_q, mla_kv, mla_att, mla_m, mla_tiles;
+    // full ScMoE layer (scmoe_layer_full_forward): normed input, MLA output, a1, dd, a3
+    DevBuf full_n, full_m, full_a1, full_dd, full_a3;
     unsigned char pr_blob[64] = {};  // permutation result carried from moe_front to moe_back
     void release_all() {
         DevBuf* all[] = {&logits, &probs, &hmoe, &hmoe_bf16, &idx, &gates, &ffn_count,
                          &rank_in_block, &block_counts, &expert_count, &expert_base, &slot_pos,
                          &row_token, &tiles, &n_tiles, &xp, &h, &y, &in_copy, &out_copy, &misc,
                          &tiles_router, &ep_bins, &ep_local, &ep_y, &dn_x, &dn_h, &dn_y,
-                         &dn_tiles, &mla_p1, &mla_q, &mla_kv, &mla_att, &mla_m, &mla_tiles};
+                         &dn_tiles, &mla_p1, &mla_q, &mla_kv, &mla_att, &mla_m, &mla_tiles, &full_n, &full_m, &full_a1,
+                         &full_dd, &full_a3};
         for (DevBuf* b : all) b->release();
     }
 };
@@ -135,6 +138,9 @@ struct scmoe_ctx {
     cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr},
                 ev_out[2] = {nullptr, nullptr};
     DevBuf io[2][7];
+    // full-layer overlap: the MoE branch's stream and its events
+    cudaStream_t s_moe = nullptr;
+    cudaEvent_t ev_full[3] = {nullptr, nullptr, nullptr};
 };
 
 // RAII stage timer; a no-op unless profiling is enabled on the context.
@@ -355,6 +361,7 @@ void launch_mla_scale_rope(scmoe_ctx* c, float* X, size_t ld, size_t rows, int n
                            int n_b, float alpha_b, int rc, int heads, int hd, const float2* table,
                            size_t pos0, size_t seq_len);
 void launch_mla_attention(scmoe_ctx* c, const MlaAttnArgs& a, int batches);
+void launch_add_f32(scmoe_ctx* c, const float* a, const float* b, size_t n, float* out);
 
 }  // namespace scmoe
 

@@ -592,6 +592,41 @@ void launch_mla_scale_rope(scmoe_ctx* c, float* X, size_t ld, size_t rows, int n
     SCMOE_LAUNCH_CHECK(c);
 }
 
+// out = a + b (fp32, rounded): the residual adds of build_layer (model.hpp:366, :390, :392).
+__global__ void add_f32_kernel(const float4* __restrict__ a, const float4* __restrict__ b,
+                               float4* __restrict__ out, size_t n4) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const float4 x = a[i], y = b[i];
+        out[i] = make_float4(__fadd_rn(x.x, y.x), __fadd_rn(x.y, y.y), __fadd_rn(x.z, y.z),
+                             __fadd_rn(x.w, y.w));
+    }
+}
+__global__ void add_f32_tail_kernel(const float* __restrict__ a, const float* __restrict__ b,
+                                    float* __restrict__ out, size_t n) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (i < n) out[i] = __fadd_rn(a[i], b[i]);
+}
+void launch_add_f32(scmoe_ctx* c, const float* a, const float* b, size_t n, float* out) {
+    if (n == 0) return;
+    const bool vec = ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) |
+                       reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+    const size_t n4 = vec ? n / 4 : 0;
+    if (n4) {
+        const size_t blocks = std::min<size_t>(ceil_div(n4, 256), (size_t)c->num_sms * 8);
+        add_f32_kernel<<<(unsigned)blocks, 256, 0, c->stream>>>(
+            reinterpret_cast<const float4*>(a), reinterpret_cast<const float4*>(b),
+            reinterpret_cast<float4*>(out), n4);
+        SCMOE_LAUNCH_CHECK(c);
+    }
+    const size_t rem = n - 4 * n4;
+    if (rem) {
+        add_f32_tail_kernel<<<(unsigned)ceil_div(rem, 256), 256, 0, c->stream>>>(
+            a + 4 * n4, b + 4 * n4, out + 4 * n4, rem);
+        SCMOE_LAUNCH_CHECK(c);
+    }
+}
+
 void launch_mla_attention(scmoe_ctx* c, const MlaAttnArgs& a, int batches) {
     const MlaAttnArgs& h = a;
     const unsigned z = (unsigned)(batches * h.H);

@@ -167,3 +167,55 @@ def mla_infer_step(p: MlaParams, cache: MlaCache, h_t, position: int, out=None):
     ctx._check(lib().scmoe_mla_infer_step_host(ctx.handle, m, cache._h, _ptr(h_t), position,
                                                _ptr(out)))
     return out
+
+
+class ScMoELayer:
+    """The full ScMoE layer of Model::build_layer (model.hpp:355-409), forward
+    value: two MLA blocks, the dense shortcut FFN and the MoE branch with
+    zero-computation experts, wired as the reference wires them (scmoe: the
+    MoE reads rmsnorm(a1), so it can run beside dense FFN + MLA2).
+
+    ``mla1``/``mla2``: MlaParams; ``dense``: layer.DenseFFN; ``router``:
+    RouterState; ``bank``: ExpertBank (PREC_BF16 for the tcgen05 path);
+    norms: gain vectors [d] (numpy)."""
+
+    def __init__(self, mla1: MlaParams, mla2: MlaParams, dense, router, bank, norm1, norm_ffn,
+                 norm2, norm_moe, ctx: Optional[Context] = None):
+        import torch
+        self.ctx = ctx or default_context()
+        self.mla1, self.mla2, self.dense, self.router, self.bank = mla1, mla2, dense, router, bank
+        self.d = mla1.d_model
+        self.norms = [torch.from_numpy(np.ascontiguousarray(g, np.float32)).cuda()
+                      for g in (norm1, norm_ffn, norm2, norm_moe)]
+
+    def forward(self, x, seq_len: int, renormalize: bool = False, overlap: bool = True,
+                want_intermediates: bool = False):
+        """x: CUDA fp32 tensor [T, d] (device API) or numpy (copied in/out).
+        Returns (out, indices, gates, ffn_count[, a1, a3])."""
+        import torch
+        host = not hasattr(x, "data_ptr")
+        xt = torch.from_numpy(np.ascontiguousarray(x, np.float32)).cuda() if host else x
+        T = xt.shape[0]
+        K = self.router.top_k
+        dev = xt.device
+        out = torch.empty((T, self.d), dtype=torch.float32, device=dev)
+        idx = torch.empty(T * K, dtype=torch.int32, device=dev)
+        gates = torch.empty(T * K, dtype=torch.float64, device=dev)
+        cnt = torch.empty(T, dtype=torch.int32, device=dev)
+        a1 = torch.empty_like(out) if want_intermediates else None
+        a3 = torch.empty_like(out) if want_intermediates else None
+        c = self.ctx
+        c._check(lib().scmoe_layer_full_forward(
+            c.handle, self.mla1.device(c), self.mla2.device(c), self.dense.bank,
+            self.router.device(c), self.bank.device(c), *[g.data_ptr() for g in self.norms],
+            xt.contiguous().data_ptr(), T, seq_len, int(renormalize), int(overlap),
+            idx.data_ptr(), gates.data_ptr(), cnt.data_ptr(),
+            None if a1 is None else a1.data_ptr(), None if a3 is None else a3.data_ptr(),
+            out.data_ptr()))
+        res = [out, idx, gates, cnt] + ([a1, a3] if want_intermediates else [])
+        if host:
+            c.synchronize()
+            res = [t.cpu().numpy() for t in res]
+            res[1] = res[1].view(np.uint32)
+            res[3] = res[3].view(np.uint32)
+        return tuple(res)

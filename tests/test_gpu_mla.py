@@ -100,3 +100,71 @@ def test_mla_device_api_and_longcat_widths(scmoe, orc):
     got = mla_block(torch.from_numpy(h).cuda(), p, seq)
     scmoe.default_context().synchronize()
     assert got.cpu().numpy().tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("renorm", [False, True])
+def test_full_scmoe_layer(scmoe, orc, renorm):
+    """The whole ScMoE layer of Model::build_layer (model.hpp:355-409):
+    a1 = x + MLA1(rmsnorm x); dd = a1 + FFN(rmsnorm a1); a3 = dd + MLA2(rmsnorm dd);
+    out = a3 + moe(rmsnorm a1).  a1 and the routing are bit-exact (exact MLA,
+    rmsnorm, router); a3 / out within the bf16 tolerance of the oracle run on
+    the same bf16-rounded dense / expert weights.  The overlapped schedule
+    (MoE branch on its own stream) is bitwise the serial one."""
+    import torch
+    P = scmoe
+    from paper_2509_01322_b200.layer import DenseFFN
+    from paper_2509_01322_b200.mla import ScMoELayer
+    d, dq, dkv, H, dhc, dhr, seq, nseq = 256, 64, 32, 4, 32, 16, 64, 2
+    N, Z, K, KE, I, DI = 8, 4, 3, 2, 256, 512
+    T = seq * nseq
+    dims = (d, dq, dkv, H, dhc, dhr)
+    ctx = P.Context(0)
+    w1 = O.mla_weights(*dims, seed=21)
+    w2 = O.mla_weights(*dims, seed=22)
+    dw_in = O.bf16_round(O.uniform_f32(O.stream_seed(23, 0), d * DI, 1.0 / d)).reshape(d, DI)
+    dw_out = O.bf16_round(O.uniform_f32(O.stream_seed(23, 1), DI * d, 1.0 / d)).reshape(DI, d)
+    wr = O.uniform_f32(O.stream_seed(24, 0), d * (N + Z), 1.0 / d).reshape(d, N + Z)
+    ew_in = [O.bf16_round(O.uniform_f32(O.stream_seed(25, 2 * e), d * I, 1.0 / d)).reshape(d, I)
+             for e in range(N)]
+    ew_out = [O.bf16_round(O.uniform_f32(O.stream_seed(25, 2 * e + 1), I * d, 1.0 / d)).reshape(I, d)
+              for e in range(N)]
+    norms = [(1.0 + 0.1 * O.normal_f32(26 + i, d)).astype(np.float32) for i in range(4)]
+    x = O.normal_f32(O.stream_seed(27, 0), T * d).reshape(T, d)
+
+    from paper_2509_01322_b200.mla import MlaParams
+    layer = ScMoELayer(MlaParams(*dims, weights=w1, rope_base=1.0e4),
+                       MlaParams(*dims, weights=w2, rope_base=1.0e4),
+                       DenseFFN(ctx, d, DI, w_in=dw_in, w_out=dw_out),
+                       P.RouterState(wr, N, Z, K, KE, 0.0, 1.0),
+                       P.ExpertBank(ew_in, ew_out, precision=P.PREC_BF16), *norms, ctx=ctx)
+    out, idx, gates, cnt, a1, a3 = layer.forward(x, seq, renormalize=renorm, overlap=True,
+                                                 want_intermediates=True)
+    out0, idx0, gates0, cnt0 = layer.forward(x, seq, renormalize=renorm, overlap=False)
+    assert out.tobytes() == out0.tobytes() and idx.tobytes() == idx0.tobytes()
+
+    # oracle composition
+    def rms(v, g):
+        o = np.empty_like(v)
+        orc.orc_rmsnorm_f32(O.ptr(v), O.ptr(g), v.shape[0], d, np.float32(1e-6), O.ptr(o))
+        return o
+    _, m1 = O.mla_forward(orc, dims, w1, rms(x, norms[0]), seq)
+    a1_w = x + m1
+    assert a1.tobytes() == a1_w.tobytes()
+    dd_w = np.empty_like(x)
+    assert orc.orc_dense_branch_f32(O.ptr(a1_w), O.ptr(norms[1]), T, d, O.ptr(dw_in),
+                                    O.ptr(dw_out), DI, O.ptr(dd_w)) == 0
+    _, m2 = O.mla_forward(orc, dims, w2, rms(dd_w, norms[2]), seq)
+    a3_w = dd_w + m2
+    assert O.rel_l2(a3 - a1_w, a3_w - a1_w) <= 5e-3
+    idx_w = np.empty(T * K, np.uint32)
+    g_w = np.empty(T * K)
+    c_w = np.empty(T, np.uint32)
+    out_w = np.empty_like(x)
+    assert orc.orc_scmoe_layer_f32(O.ptr(a1_w), O.ptr(a3_w), O.ptr(norms[3]), T, d, O.ptr(wr), N,
+                                   Z, K, KE, 0.0, O.ptr(np.zeros(N + Z)), O.ptr_array(ew_in),
+                                   O.ptr_array(ew_out), I, 1.0, 1.0, int(renorm), O.ptr(idx_w),
+                                   O.ptr(g_w), O.ptr(c_w), O.ptr(out_w)) == 0
+    assert idx.tobytes() == idx_w.tobytes() and gates.tobytes() == g_w.tobytes()
+    assert cnt.tobytes() == c_w.tobytes()
+    assert O.rel_l2(out - a3, out_w - a3_w) <= 5e-3
+    assert O.rel_l2(out, out_w) <= 5e-3

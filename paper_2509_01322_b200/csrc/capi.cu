@@ -1832,7 +1832,12 @@ int scmoe_layer_full_forward(scmoe_ctx* c, scmoe_mla* mla1, scmoe_mla* mla2, scm
             if (rc) throw ScmoeError{rc, c->last_error};
         };
         if (overlap && !c->s_moe) {
-            SCMOE_CUDA(cudaStreamCreateWithFlags(&c->s_moe, cudaStreamNonBlocking));
+            // highest priority: as MLA CTAs retire, the CTA scheduler hands the
+            // freed SM space to the MoE branch's kernels first, so a grouped-GEMM
+            // CTA (HBM / tensor bound) shares SMs with an MLA CTA (FP32 pipe)
+            int lo = 0, hi = 0;
+            SCMOE_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            SCMOE_CUDA(cudaStreamCreateWithPriority(&c->s_moe, cudaStreamNonBlocking, hi));
             for (auto& e : c->ev_full) SCMOE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         }
         const cudaStream_t sb = overlap ? c->s_moe : sa;

@@ -78,7 +78,7 @@ def check_sass(lib: str = LIB) -> dict:
     # MLA: the scores / rope kernels are pure FMUL + FADD; the PV kernel's only
     # FFMAs are the correctly rounded divisions w = e / denom (__fdiv_rn) where
     # it stages the weights -- its chains are FMUL2 + FADD2 (no FFMA2 below)
-    seq += [n for n in summary if re.search(r"mla_(scores|scores_big|scale_rope)_kernel", n)]
+    seq += [n for n in summary if re.search(r"mla_(scores|scores_big|scale_rope)_kernel|seq_gemv_kernel", n)]
     assert seq, "seq_gemm kernel missing from SASS"
     for n in seq:
         assert summary[n]["FFMA"] == 0, f"{n}: FFMA found in exact-order kernel"

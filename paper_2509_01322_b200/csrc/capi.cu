@@ -1509,6 +1509,7 @@ void mla_ensure_rope(scmoe_ctx* c, scmoe_mla* m, size_t npos) {
 void mla_gemm(scmoe_ctx* c, DevBuf& tiles_buf, const float* A, size_t lda, size_t rows,
               const float* B, size_t K, size_t N, float* C, size_t ldc) {
     if (rows == 0 || N == 0) return;
+    if (rows <= 4 && launch_seq_gemv(c, A, lda, rows, B, N, C, ldc, K, N)) return;  // decode
     // 128 x 128 tiles (8 x 8 chains per thread) once they fill two waves
     static const bool big_ok = [] {
         const char* e = getenv("SCMOE_MLA_TILE");

@@ -218,6 +218,9 @@ void launch_seq_gemm(scmoe_ctx* c, const float* A, size_t lda, const int* a_rows
                      size_t K, size_t N, int silu, const TokenTile* tiles, const int* n_tiles_dev,
                      size_t max_tiles, int tile_rows);
 int seq_gemm_tile_rows(size_t rows, size_t N, int num_sms);
+// Sequential-k GEMV for rows <= 4 (false: not applicable, nothing launched).
+bool launch_seq_gemv(scmoe_ctx* c, const float* A, size_t lda, size_t rows, const float* B,
+                     size_t ldb, float* C, size_t ldc, size_t K, size_t N);
 // Router projection with one CTA per 56-token slab x all experts (E <= 768).
 // Same tile as the slab kernel, operands by TMA into an mbarrier ring.
 // RouterState<double>: projection and softmax/top-K in double.

@@ -631,6 +631,113 @@ void launch_seq_gemm(scmoe_ctx* c, const float* A, size_t lda, const int* a_rows
 }
 
 // ---------------------------------------------------------------------------
+// Sequential-k GEMV for a few rows (decode): C[r][n] = sum_k A[r][k] B[k][n]
+// with the same chains as seq_gemm_kernel (c = 0; c = c + a*b, both
+// rounded, k ascending).  An exact chain cannot be split over k, so the
+// parallelism is the N columns: a CTA owns 64 columns (one thread per column,
+// R chains each) and streams its [K x 64] slab of B through a 6-stage
+// cp.async ring of 64-row chunks (16 KB each), so ~96 KB per CTA is in flight
+// while the chains consume shared memory.  A rows are staged once.
+// ---------------------------------------------------------------------------
+constexpr int kGvCols = 64, kGvRows = 64, kGvStages = 6;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+    const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    const int n = pred ? 16 : 0;  // zero-fill when out of range
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n));
+}
+
+template <int R>
+__global__ void __launch_bounds__(kGvCols) seq_gemv_kernel(const float* __restrict__ A, size_t lda,
+                                                           const float* __restrict__ B, size_t ldb,
+                                                           float* __restrict__ C, size_t ldc,
+                                                           int K, int N) {
+    extern __shared__ __align__(16) float gv_smem[];
+    float* ring = gv_smem;                                   // [S][64 rows][64 cols]
+    float* xs = gv_smem + kGvStages * kGvRows * kGvCols;     // [R][K]
+    const int tid = threadIdx.x, n0 = blockIdx.x * kGvCols, n = n0 + tid;
+    for (int i = tid; i < R * K; i += kGvCols) xs[i] = A[(size_t)(i / K) * lda + i % K];
+    const int nch = (K + kGvRows - 1) / kGvRows;
+    // a chunk = 64 rows x 64 columns = 1024 16-byte pieces, 16 per thread
+    const bool vec_ok = ((ldb & 3) == 0) && ((reinterpret_cast<uintptr_t>(B) & 15) == 0) &&
+                        n0 + kGvCols <= N;
+    auto issue = [&](int ch) {
+        float* dst = ring + (ch % kGvStages) * kGvRows * kGvCols;
+        const int k0 = ch * kGvRows;
+        if (vec_ok) {
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int piece = tid + u * kGvCols, row = piece >> 4, c4 = 4 * (piece & 15);
+                const bool in = k0 + row < K;
+                cp_async16(dst + row * kGvCols + c4, B + (size_t)(in ? k0 + row : 0) * ldb + n0 + c4,
+                           in);
+            }
+        } else {  // ragged column block: scalar loads (synchronous)
+            for (int row = 0; row < kGvRows; ++row) {
+                const bool in = k0 + row < K && n < N;
+                dst[row * kGvCols + tid] = in ? B[(size_t)(k0 + row) * ldb + n] : 0.f;
+            }
+        }
+        asm volatile("cp.async.commit_group;");
+    };
+    for (int ch = 0; ch < kGvStages - 1; ++ch) {
+        if (ch < nch) issue(ch);
+        else asm volatile("cp.async.commit_group;");
+    }
+    float acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.f;
+    for (int ch = 0; ch < nch; ++ch) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(kGvStages - 2));
+        __syncthreads();  // chunk ch visible to all; chunk ch-1's slot free
+        if (ch + kGvStages - 1 < nch) issue(ch + kGvStages - 1);
+        else asm volatile("cp.async.commit_group;");
+        const float* w = ring + (ch % kGvStages) * kGvRows * kGvCols + tid;
+        const int k0 = ch * kGvRows, kc = min(kGvRows, K - k0);
+        if (kc == kGvRows) {
+#pragma unroll 16
+            for (int k = 0; k < kGvRows; ++k) {
+                const float wv = w[k * kGvCols];
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+                    acc[r] = __fadd_rn(acc[r], __fmul_rn(xs[r * K + k0 + k], wv));
+            }
+        } else {
+            for (int k = 0; k < kc; ++k) {
+                const float wv = w[k * kGvCols];
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+                    acc[r] = __fadd_rn(acc[r], __fmul_rn(xs[r * K + k0 + k], wv));
+            }
+        }
+    }
+    asm volatile("cp.async.wait_group 0;");
+    if (n < N) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) C[(size_t)r * ldc + n] = acc[r];
+    }
+}
+
+bool launch_seq_gemv(scmoe_ctx* c, const float* A, size_t lda, size_t rows, const float* B,
+                     size_t ldb, float* C, size_t ldc, size_t K, size_t N) {
+    const size_t smem = (kGvStages * kGvRows * kGvCols + rows * K) * sizeof(float);
+    if (rows == 0 || rows > 4 || smem > 200 * 1024) return false;
+    const unsigned grid = (unsigned)ceil_div(N, kGvCols);
+    auto go = [&](auto kern) {
+        ensure_max_dynamic_smem((const void*)kern, 200 * 1024, c->device);
+        kern<<<grid, kGvCols, smem, c->stream>>>(A, lda, B, ldb, C, ldc, (int)K, (int)N);
+    };
+    switch (rows) {
+        case 1: go(seq_gemv_kernel<1>); break;
+        case 2: go(seq_gemv_kernel<2>); break;
+        case 3: go(seq_gemv_kernel<3>); break;
+        default: go(seq_gemv_kernel<4>); break;
+    }
+    SCMOE_LAUNCH_CHECK(c);
+    return true;
+}
+
+// ---------------------------------------------------------------------------
 // Softmax + biased top-K -- tensor.hpp:174-192 and router.hpp:90-130.
 // One warp per token.  The row max is order independent; the exponentials
 // are elementwise; the normaliser is a sequential sum over j in fp32 (lane 0,

@@ -592,6 +592,67 @@ void launch_mla_scale_rope(scmoe_ctx* c, float* X, size_t ld, size_t rows, int n
     SCMOE_LAUNCH_CHECK(c);
 }
 
+// ---------------------------------------------------------------------------
+// Decode (one query row per (b, h)): a warp per softmax row and a CTA per
+// head for PV -- the lane-per-row and tiled kernels above need many rows.
+// Same arithmetic: max (order free), e = expf(s - max) with the normaliser
+// summed in key order (each lane adds the chunk's 32 values in order, fed by
+// shuffles), w = e / denom; PV chains over keys in order, one per column.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) mla_softmax_warp_kernel(float* __restrict__ att,
+                                                               int rows_total, int nq, int nk,
+                                                               int q0) {
+    __shared__ uint64_t exp_tab[32];
+    if (threadIdx.x < 32) exp_tab[threadIdx.x] = scmoe_exp2f_tab_dev[threadIdx.x];
+    __syncthreads();
+    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (r >= rows_total) return;
+    const int n = min(nk, q0 + r % nq + 1);
+    float* row = att + (size_t)r * nk;
+    float mx = -INFINITY;
+    for (int j = lane; j < n; j += 32) mx = fmaxf(mx, row[j]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float sum = 0.f;
+    for (int j0 = 0; j0 < n; j0 += 32) {
+        const int j = j0 + lane;
+        float e = 0.f;
+        if (j < n) {
+            e = scmoe_expf_smem(__fsub_rn(row[j], mx), exp_tab);
+            row[j] = e;
+        }
+        const int m = min(32, n - j0);
+        for (int t = 0; t < m; ++t) sum = __fadd_rn(sum, __shfl_sync(0xffffffffu, e, t));
+    }
+    for (int j = lane; j < n; j += 32) row[j] = __fdiv_rn(row[j], sum);
+}
+
+// merged[b][h*dhc + p] = sum_j w[j] * v[j][p]; grid (B*H), dhc threads, the
+// weight row staged in shared memory (n <= kPvRowMax).
+constexpr int kPvRowMax = 12288;
+__global__ void mla_pv_row_kernel(MlaAttnArgs a) {
+    extern __shared__ float wrow[];
+    const int bh = blockIdx.x, b = bh / a.H, h = bh % a.H;
+    const int n = min(a.nk, a.q0 + 1);
+    const float* att = a.att + (size_t)bh * a.nk;  // nq == 1
+    for (int j = threadIdx.x; j < n; j += blockDim.x) wrow[j] = att[j];
+    __syncthreads();
+    const int p = threadIdx.x;
+    if (p >= a.dhc) return;
+    const float* v = a.v + (size_t)b * a.nk * a.ldkv + (size_t)h * a.dhc + p;
+    float acc = 0.f;
+    int j = 0;
+    for (; j + 32 <= n; j += 32) {  // 32 value rows in flight per thread
+        float vv[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) vv[u] = v[(size_t)(j + u) * a.ldkv];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) acc = __fadd_rn(acc, __fmul_rn(wrow[j + u], vv[u]));
+    }
+    for (; j < n; ++j) acc = __fadd_rn(acc, __fmul_rn(wrow[j], v[(size_t)j * a.ldkv]));
+    a.merged[(size_t)b * a.ldm + (size_t)h * a.dhc + p] = acc;
+}
+
 // out = a + b (fp32, rounded): the residual adds of build_layer (model.hpp:366, :390, :392).
 __global__ void add_f32_kernel(const float4* __restrict__ a, const float4* __restrict__ b,
                                float4* __restrict__ out, size_t n4) {
@@ -649,6 +710,23 @@ void launch_mla_attention(scmoe_ctx* c, const MlaAttnArgs& a, int batches) {
             mla_scores_kernel<16, 2><<<grid, 128, 0, c->stream>>>(a);
         }
         SCMOE_LAUNCH_CHECK(c);
+    }
+    const bool decode = h.nq == 1 && h.nk <= kPvRowMax && h.dhc <= 1024;
+    if (decode) {
+        {
+            ProfScope _p(c, "mla_softmax");
+            mla_softmax_warp_kernel<<<(unsigned)ceil_div((size_t)z * 32, 256), 256, 0, c->stream>>>(
+                h.att, (int)z, 1, h.nk, h.q0);
+            SCMOE_LAUNCH_CHECK(c);
+        }
+        ProfScope _p(c, "mla_pv");
+        const size_t smem = (size_t)h.nk * sizeof(float);
+        if (smem > 48 * 1024)
+            ensure_max_dynamic_smem((const void*)mla_pv_row_kernel, (int)(kPvRowMax * sizeof(float)),
+                                    c->device);
+        mla_pv_row_kernel<<<z, (unsigned)((h.dhc + 31) / 32 * 32), smem, c->stream>>>(a);
+        SCMOE_LAUNCH_CHECK(c);
+        return;
     }
     {
         ProfScope _p(c, "mla_softmax");

@@ -48,6 +48,7 @@ for _ in range(reps):
 ctx.synchronize()
 wall = (time.perf_counter() - t0) / reps * 1e3
 prof = {k: v[0] / v[1] for k, v in ctx.profile_flush().items()}
+ctx.profile(False)
 B = rows // seq
 pairs = B * H * seq * (seq + 1) // 2
 lane = {
@@ -86,6 +87,14 @@ for t in range(n_dec - 32, n_dec):
     mla_infer_step(p, cache, ht[t:t + 1], t, out=o1)
 ctx.synchronize()
 res["decode_ms_per_step_at_pos"] = [n_dec - 16, round((time.perf_counter() - t0) / 32 * 1e3, 3)]
+cache2 = MlaCache(p, capacity_hint=n_dec, ctx=ctx)
+for t in range(n_dec - 32):
+    mla_infer_step(p, cache2, ht[t:t + 1], t, out=o1)
+ctx.synchronize()
+ctx.profile(True)
+for t in range(n_dec - 32, n_dec):
+    mla_infer_step(p, cache2, ht[t:t + 1], t, out=o1)
+res["decode_stage_ms"] = {k: round(v[0] / 32, 4) for k, v in ctx.profile_flush().items()}
 if "--ref" in sys.argv:
     import _oracle as O
     thr = int(sys.argv[sys.argv.index("--ref") + 1])

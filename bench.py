@@ -225,6 +225,76 @@ def reference_cpu_sample(route_tokens=64, moe_tokens=16, threads=None, log_fn=lo
     return {"value": value, "unit": "tokens/s", "cores": used, "kind": kind, "sample": sample}
 
 
+def tiny_config_a(ctx, stream, iters, with_cpu):
+    """T=512, d=256, 8 FFN + 4 zero experts, top-2,
+    K_e=1, I=128, exact fp32 (the bit-exact kernels).  Device time per layer
+    call (stream-launched, back to back) and the reference's route_topk +
+    moe_forward on the same shape, one thread, on this host."""
+    import torch
+    from paper_2509_01322_b200.layer import TINY, DeviceLayer
+    s, T = TINY, 512
+    lay = DeviceLayer(ctx, s, seed=11)
+    a1 = torch.randn(T, s.d, device="cuda")
+    a3 = torch.randn(T, s.d, device="cuda")
+    idx = torch.empty(T * s.top_k, dtype=torch.int32, device="cuda")
+    g = torch.empty(T * s.top_k, dtype=torch.float64, device="cuda")
+    cnt = torch.empty(T, dtype=torch.int32, device="cuda")
+    out = torch.empty(T, s.d, device="cuda")
+
+    def run(n):
+        for _ in range(n):
+            lay.forward(a1.data_ptr(), a3.data_ptr(), None, T, idx.data_ptr(), g.data_ptr(),
+                        cnt.data_ptr(), out.data_ptr())
+    with torch.cuda.stream(stream):
+        run(10)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        ev0.record(stream)
+        run(iters)
+        ev1.record(stream)
+    ev1.synchronize()
+    us = ev0.elapsed_time(ev1) / iters * 1e3
+    res = {"workload": "SURVEY config A: tiny fp32 layer (T=512, d=256, 8+4 experts, top-2, "
+                       "I=128), exact fp32 kernels", "us_per_call": round(us, 2),
+           "tokens_per_s": T / (us * 1e-6)}
+    if with_cpu:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import _oracle as O
+        from _oracle import ptr, ptr_array
+        E = s.n_ffn + s.n_zero
+        x = O.normal_f32(7, T * s.d).reshape(T, s.d)
+        w = O.uniform_f32(8, s.d * E, 1.0 / s.d).reshape(s.d, E)
+        wi = [O.uniform_f32(9 + e, s.d * s.inter, 1.0 / s.d) for e in range(s.n_ffn)]
+        wo = [O.uniform_f32(50 + e, s.d * s.inter, 1.0 / s.d) for e in range(s.n_ffn)]
+        ix = np.empty(T * s.top_k, np.uint32)
+        gg = np.empty(T * s.top_k)
+        cc = np.empty(T, np.uint32)
+        o = np.empty((T, s.d), np.float32)
+        kind = "reference" if O.ref_available() else "port"
+        reps = 20
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            if kind == "reference":
+                O.ref().ref_route_topk_f32(ptr(x), T, s.d, ptr(w), s.n_ffn, s.n_zero, s.top_k,
+                                           s.k_expected, 0.0, ptr(np.zeros(E)), ptr(ix), ptr(gg),
+                                           ptr(cc), None, 1)
+                O.ref().ref_moe_forward_f32(ptr(x), T, s.d, ptr(ix), ptr(gg), s.top_k, s.n_ffn,
+                                            s.n_zero, ptr_array(wi), ptr_array(wo), s.inter, 1, 0,
+                                            ptr(o), 1)
+            else:
+                O.orc().orc_route_topk_f32(ptr(x), T, s.d, ptr(w), s.n_ffn, s.n_zero, s.top_k,
+                                           s.k_expected, 0.0, ptr(np.zeros(E)), ptr(ix), ptr(gg),
+                                           ptr(cc), None)
+                O.orc().orc_moe_forward_f32(ptr(x), T, s.d, ptr(ix), ptr(gg), s.top_k, s.n_ffn,
+                                            s.n_zero, ptr_array(wi), ptr_array(wo), s.inter, 1.0,
+                                            1.0, 0, ptr(o))
+        cpu_us = (time.perf_counter() - t0) / reps * 1e6
+        res["cpu_reference"] = {"us_per_call": round(cpu_us, 1), "kind": kind, "cores": 1}
+        res["speedup_vs_cpu_reference"] = round(cpu_us / us, 1)
+    return res
+
+
 def run_reference_arm(args):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -423,6 +493,12 @@ def run_b200(args):
                     "gemm_achieved_gbs": (c1 + c2) / (tg / 1e3) / 1e9,
                     "stages_ms": {k: round(v[0] / v[1], 4) for k, v in st_c.items()}}
 
+    # ---- SURVEY config A (tiny fp32, bit-exact path, latency-bound): device
+    # time per layer call beside the reference's own CPU time on the same shape
+    config_a = None
+    if ws == 1 and args.config_a:
+        config_a = tiny_config_a(ctx, stream, args.steps * 20, not args.no_cpu_baseline)
+
     if rank != 0:
         return
     peaks = measured_peaks()
@@ -491,6 +567,7 @@ def run_b200(args):
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
         "config_c": config_c,
+        "config_a": config_a,
     }
     emit(line)
 
@@ -743,6 +820,7 @@ def main():
     ap.add_argument("--dense-inter", type=int, default=12288)
     # N=1: SURVEY config C extra (decode step of this many tokens; 0 = off)
     ap.add_argument("--decode-tokens", type=int, default=256)
+    ap.add_argument("--config-a", type=int, default=1, help="measure SURVEY config A (tiny fp32)")
     ap.add_argument("--config-d-tokens", type=int, default=32768)
     # pipelined = scmoe_layer_forward_batches; measured slower than serial on B200 in round 1
     # (router and GEMM contend for shared-memory bandwidth), so serial is the default

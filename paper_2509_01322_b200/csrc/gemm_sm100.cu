@@ -108,6 +108,19 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// Same load, no wait: the caller overlaps it and issues tcgen05.wait::ld.
+__device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+        "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+          "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+          "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+          "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+}
+
 __device__ __forceinline__ float silu_fast(float v) { return __fdividef(v, 1.0f + __expf(-v)); }
 
 struct GemmArgs {
@@ -156,10 +169,10 @@ template <int kNT>
 __host__ __device__ constexpr int gemm_epi_bufs() {
     return kNT == 256 ? 2 : 1;
 }
-template <int kNT>
+template <int kNT, int kS = SLABS>
 constexpr int gemm_smem_bytes() {
-    return A_STAGES * A_STAGE_BYTES + B_STAGES * kNT * BK * 2 + 1024 + 256 +
-           gemm_epi_bufs<kNT>() * EPI_STAGE_BYTES;
+    return A_STAGES * kS * A_SLAB_BYTES + B_STAGES * kNT * BK * 2 + 1024 + 256 +
+           gemm_epi_bufs<kNT>() * 32 * (128 * kS * 2 + 16);
 }
 
 // <= 64 registers: one GEMM CTA (352 threads) must leave room for the
@@ -167,11 +180,25 @@ constexpr int gemm_smem_bytes() {
 // kNT = max tokens per tile: 192 (single-GPU prefill; 186 KB smem, fits next
 // to the router) or 256 (expert-parallel shards with 256+ tokens per expert:
 // one tile of 256 instead of two of 128, 210 KB smem, 2 x 256 TMEM columns).
-template <int kNT>
-__global__ void __maxnreg__(64)
+// kS = 128-row weight slabs per unit: 2 (BM = 256; the accumulators of a
+// 256-token tile fill TMEM, so they are single-buffered) or 1 (BM = 128: two
+// 256-column accumulators, so the epilogue of unit i drains one while the
+// MMAs of unit i+1 fill the other; 4 epilogue warps).
+// Register cap: 64 so the 192-token variant co-resides with the router; the
+// 256-token variant (expert-parallel shards, never next to the router) takes
+// 128 and prefetches the next chunk's accumulators during the epilogue.
+template <int kNT, int kS = SLABS>
+__global__ void __maxnreg__(kNT == 256 ? 128 : 64)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_w,
                         const __grid_constant__ CUtensorMap map_x, const GemmArgs args) {
     constexpr int NT = kNT;
+    // unit geometry for this instantiation (shadows the namespace defaults)
+    constexpr int SLABS = kS;
+    constexpr int BM = 128 * kS;
+    constexpr int A_STAGE_BYTES = kS * A_SLAB_BYTES;
+    constexpr int EPI_WARPS = 4 * kS;
+    constexpr int EPI_PITCH = BM * 2 + 16;
+    constexpr int EPI_STAGE_BYTES = 32 * EPI_PITCH;
     constexpr int B_STAGE_BYTES = NT * BK * 2;
     constexpr int RING_BYTES = A_STAGES * A_STAGE_BYTES + B_STAGES * B_STAGE_BYTES;
     static_assert(SLABS * NT <= TMEM_COLS, "TMEM overflow");
@@ -413,10 +440,23 @@ __global__ void __maxnreg__(64)
             if (!(args.debug & 2)) {
                 const uint32_t taddr =
                     tmem_base + ((uint32_t)(quad * 32) << 16) + buf * ACC_COLS + s * NT;
+                constexpr bool kPrefetch = NT == 256;
+                uint32_t vn[kPrefetch ? 32 : 1];
+                if constexpr (kPrefetch) {
+                    if (tile.count > 0) tmem_ld32_async(taddr, vn);
+                }
                 for (int j0 = 0; j0 < tile.count; j0 += 32, ++chunk) {
                     unsigned char* stage = stage0 + (chunk % EPI_BUFS) * EPI_STAGE_BYTES;
                     uint32_t v[32];
-                    tmem_ld32(taddr + j0, v);  // v[jj] = D[mb*BM + mrow + lane][j0 + jj]
+                    if constexpr (kPrefetch) {
+                        // chunk j0 was issued one iteration ago; issue j0 + 32 now
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                        for (int q = 0; q < 32; ++q) v[q] = vn[q];
+                        if (j0 + 32 < tile.count) tmem_ld32_async(taddr + j0 + 32, vn);
+                    } else {
+                        tmem_ld32(taddr + j0, v);  // v[jj] = D[mb*BM + mrow + lane][j0 + jj]
+                    }
                     // the bulk copies that last read this staging buffer are done
                     if (lane < ROWS_PER_WARP) {
                         if constexpr (EPI_BUFS == 2)
@@ -510,21 +550,29 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
     const size_t units_max = max_tiles * (M / BM);
     const int grid = (int)std::min<size_t>(
         units_max, (size_t)(c->gemm_sms > 0 ? std::min(c->gemm_sms, c->num_sms) : c->num_sms));
+    // 256-token tiles: two 128-row slabs per unit (default; measured faster at
+    // the EP x4 shard shape: 2.97 vs 3.16 ms) or, SCMOE_GEMM_SLABS=1, one slab
+    // with double-buffered TMEM accumulators
+    static const int slabs256 = [] {
+        const char* e = getenv("SCMOE_GEMM_SLABS");
+        return e && atoi(e) == 1 ? 1 : 2;
+    }();
+    auto go = [&](auto kern, int smem, int threads, int bm) {
+        const size_t units = max_tiles * (M / bm);
+        const int g = (int)std::min<size_t>(
+            units, (size_t)(c->gemm_sms > 0 ? std::min(c->gemm_sms, c->num_sms) : c->num_sms));
+        ensure_max_dynamic_smem(reinterpret_cast<const void*>(kern), smem, c->device);
+        kern<<<g, threads, smem, c->stream>>>(mw, mx, a);
+    };
+    (void)grid;
     if (tile_rows == 128) {
-        constexpr int smem = gemm_smem_bytes<128>();
-        ensure_max_dynamic_smem(reinterpret_cast<const void*>(grouped_gemm_kernel<128>), smem,
-                                c->device);
-        grouped_gemm_kernel<128><<<grid, NUM_THREADS, smem, c->stream>>>(mw, mx, a);
+        go(grouped_gemm_kernel<128>, gemm_smem_bytes<128>(), NUM_THREADS, BM);
+    } else if (tile_rows == 256 && slabs256 == 1) {
+        go(grouped_gemm_kernel<256, 1>, gemm_smem_bytes<256, 1>(), 32 * (EPI_WARP0 + 4), 128);
     } else if (tile_rows == 256) {
-        constexpr int smem = gemm_smem_bytes<256>();
-        ensure_max_dynamic_smem(reinterpret_cast<const void*>(grouped_gemm_kernel<256>), smem,
-                                c->device);
-        grouped_gemm_kernel<256><<<grid, NUM_THREADS, smem, c->stream>>>(mw, mx, a);
+        go(grouped_gemm_kernel<256, 2>, gemm_smem_bytes<256, 2>(), NUM_THREADS, BM);
     } else {
-        constexpr int smem = gemm_smem_bytes<192>();
-        ensure_max_dynamic_smem(reinterpret_cast<const void*>(grouped_gemm_kernel<192>), smem,
-                                c->device);
-        grouped_gemm_kernel<192><<<grid, NUM_THREADS, smem, c->stream>>>(mw, mx, a);
+        go(grouped_gemm_kernel<192>, gemm_smem_bytes<192>(), NUM_THREADS, BM);
     }
     SCMOE_LAUNCH_CHECK(c);
 }

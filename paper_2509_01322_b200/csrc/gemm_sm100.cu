@@ -58,7 +58,7 @@ constexpr int TMEM_COLS = 512;
 constexpr int EPI_WARPS = 4 * SLABS;             // one per (TMEM lane quadrant, slab)
 constexpr int EPI_WARP0 = 3;                     // warps 0: W producer, 1: MMA, 2: X producer
 constexpr int NUM_THREADS = 32 * (EPI_WARP0 + EPI_WARPS);
-constexpr int EPI_PITCH = BM * 2 + 16;                // epilogue staging row (+16 B pad)
+constexpr int EPI_PITCH = BM * 2;                     // epilogue staging row (dense: TMA store box)
 constexpr int EPI_STAGE_BYTES = 32 * EPI_PITCH;          // [32 tokens][256 rows] bf16
 constexpr int SMEM_BYTES = RING_BYTES + 1024 /*align*/ + 256 /*barriers*/ + EPI_STAGE_BYTES;
 
@@ -134,6 +134,7 @@ struct GemmArgs {
     const uint64_t* row_dst;
     const int* row_ids;
     int M, K;            // weight rows per expert, reduction length
+    int tma_store;       // contiguous out: full 32-token chunks leave by one TMA tensor store
     int silu;
     int debug;           // timing experiments only: bit 0 skip epilogue stores,
                          // bit 1 skip the epilogue (release TMEM at once),
@@ -172,7 +173,7 @@ __host__ __device__ constexpr int gemm_epi_bufs() {
 template <int kNT, int kS = SLABS>
 constexpr int gemm_smem_bytes() {
     return A_STAGES * kS * A_SLAB_BYTES + B_STAGES * kNT * BK * 2 + 1024 + 256 +
-           gemm_epi_bufs<kNT>() * 32 * (128 * kS * 2 + 16);
+           gemm_epi_bufs<kNT>() * 32 * (128 * kS * 2);
 }
 
 // <= 64 registers: one GEMM CTA (352 threads) must leave room for the
@@ -190,14 +191,15 @@ constexpr int gemm_smem_bytes() {
 template <int kNT, int kS = SLABS>
 __global__ void __maxnreg__(kNT == 256 ? 128 : 64)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_w,
-                        const __grid_constant__ CUtensorMap map_x, const GemmArgs args) {
+                        const __grid_constant__ CUtensorMap map_x,
+                        const __grid_constant__ CUtensorMap map_out, const GemmArgs args) {
     constexpr int NT = kNT;
     // unit geometry for this instantiation (shadows the namespace defaults)
     constexpr int SLABS = kS;
     constexpr int BM = 128 * kS;
     constexpr int A_STAGE_BYTES = kS * A_SLAB_BYTES;
     constexpr int EPI_WARPS = 4 * kS;
-    constexpr int EPI_PITCH = BM * 2 + 16;
+    constexpr int EPI_PITCH = BM * 2;
     constexpr int EPI_STAGE_BYTES = 32 * EPI_PITCH;
     constexpr int B_STAGE_BYTES = NT * BK * 2;
     constexpr int RING_BYTES = A_STAGES * A_STAGE_BYTES + B_STAGES * B_STAGE_BYTES;
@@ -476,7 +478,17 @@ __global__ void __maxnreg__(kNT == 256 ? 128 : 64)
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32) : "memory");
                     const int jj = ew * ROWS_PER_WARP + lane;
-                    if (lane < ROWS_PER_WARP && j0 + jj < tile.count && !(args.debug & 1)) {
+                    if (args.tma_store && j0 + 32 <= tile.count) {
+                        // a full chunk of a contiguous output: one [32 x BM] tensor store
+                        if (ew == 0 && lane == 0 && !(args.debug & 1)) {
+                            asm volatile(
+                                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                                    reinterpret_cast<uint64_t>(&map_out)),
+                                "r"(mb * BM), "r"(tile.pos + j0), "r"(smem_u32(stage))
+                                : "memory");
+                            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                        }
+                    } else if (lane < ROWS_PER_WARP && j0 + jj < tile.count && !(args.debug & 1)) {
                         const int p = tile.pos + j0 + jj;
                         __nv_bfloat16* dst =
                             (args.row_dst ? reinterpret_cast<__nv_bfloat16*>(
@@ -534,7 +546,20 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
     // X: tiled boxes of 128 permuted rows, or single-row boxes for tile::gather4
     const CUtensorMap mx =
         make_map_2d(X, std::max<size_t>(x_rows, 1), K, x_row_ids ? 1 : 64, BK);
+    // contiguous output: tensor map for the epilogue's [32 tokens x 256 rows]
+    // stores (SWIZZLE_NONE: the staging tile is dense, 512 B per token row)
+    static const bool tma_store_on = [] {
+        const char* e = getenv("SCMOE_GEMM_TMA_STORE");
+        return !(e && atoi(e) == 0);
+    }();
+    const bool use_tma_store = tma_store_on && row_dst == nullptr;
+    const CUtensorMap mo =
+        use_tma_store ? make_tma_map_2d(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, sizeof(__nv_bfloat16),
+                                        std::max<size_t>(max_tiles * tile_rows, 1), M, 32, BM,
+                                        CU_TENSOR_MAP_SWIZZLE_NONE)
+                      : mw;
     GemmArgs a;
+    a.tma_store = use_tma_store ? 1 : 0;
     a.tiles = tiles;
     a.n_tiles = n_tiles_dev;
     a.x_rows = x_row_ids;
@@ -562,12 +587,13 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
         const int g = (int)std::min<size_t>(
             units, (size_t)(c->gemm_sms > 0 ? std::min(c->gemm_sms, c->num_sms) : c->num_sms));
         ensure_max_dynamic_smem(reinterpret_cast<const void*>(kern), smem, c->device);
-        kern<<<g, threads, smem, c->stream>>>(mw, mx, a);
+        kern<<<g, threads, smem, c->stream>>>(mw, mx, mo, a);
     };
     (void)grid;
     if (tile_rows == 128) {
         go(grouped_gemm_kernel<128>, gemm_smem_bytes<128>(), NUM_THREADS, BM);
     } else if (tile_rows == 256 && slabs256 == 1) {
+        a.tma_store = 0;  // its 128-row units would need a 128-wide box
         go(grouped_gemm_kernel<256, 1>, gemm_smem_bytes<256, 1>(), 32 * (EPI_WARP0 + 4), 128);
     } else if (tile_rows == 256) {
         go(grouped_gemm_kernel<256, 2>, gemm_smem_bytes<256, 2>(), NUM_THREADS, BM);

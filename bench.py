@@ -258,6 +258,23 @@ def tiny_config_a(ctx, stream, iters, with_cpu):
     res = {"workload": "SURVEY config A: tiny fp32 layer (T=512, d=256, 8+4 experts, top-2, "
                        "I=128), exact fp32 kernels", "us_per_call": round(us, 2),
            "tokens_per_s": T / (us * 1e-6)}
+    # the same call captured once in a CUDA graph and replayed (launch-bound shape)
+    try:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            run(1)
+        with torch.cuda.stream(stream):
+            for _ in range(10):
+                graph.replay()
+            ev0.record(stream)
+            for _ in range(iters):
+                graph.replay()
+            ev1.record(stream)
+        ev1.synchronize()
+        res["us_per_call_cuda_graph"] = round(ev0.elapsed_time(ev1) / iters * 1e3, 2)
+    except Exception as e:  # capture is an optimisation; report why it was skipped
+        res["us_per_call_cuda_graph"] = None
+        res["cuda_graph_error"] = str(e)[:200]
     if with_cpu:
         sys.path.insert(0, os.path.join(ROOT, "tests"))
         import _oracle as O

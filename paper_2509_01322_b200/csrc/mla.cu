@@ -147,7 +147,7 @@ __global__ void __launch_bounds__((TM / RM) * 16) mla_scores_kernel(MlaAttnArgs 
 //           is loaded coalesced, transposed through shared memory, and lane l
 //           walks row l's 32 keys sequentially (the reference's fp32 sum);
 //   w_j   = e_j / denom (rounded division), coalesced, written in place.
-__global__ void __launch_bounds__(256, 3) mla_softmax_kernel(float* __restrict__ att,
+__global__ void __launch_bounds__(256, 4) mla_softmax_kernel(float* __restrict__ att,
                                                           const float* __restrict__ part_max,
                                                           int rows_total, int nq, int nk, int q0) {
     __shared__ float tile[8][32][33];

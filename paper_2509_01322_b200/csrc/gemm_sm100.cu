@@ -459,6 +459,50 @@ __global__ void __maxnreg__(kNT == 256 ? 128 : 64)
                     } else {
                         tmem_ld32(taddr + j0, v);  // v[jj] = D[mb*BM + mrow + lane][j0 + jj]
                     }
+                    if (args.tma_store) {
+                        // contiguous output: every warp stages its own 32 rows x 32
+                        // tokens ([token][32 rows], 64 B per token) and stores them
+                        // itself -- one [32 x 32] tensor store per full chunk, 64-byte
+                        // row copies for the tile's last partial chunk; no barrier
+                        // couples the epilogue warps
+                        unsigned char* wst = stage + ew * (32 * 64);
+                        if constexpr (EPI_BUFS == 2)
+                            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                        else
+                            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                        __syncwarp();
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj) {
+                            float f = __uint_as_float(v[jj]);
+                            if (args.silu) f = silu_fast(f);
+                            *reinterpret_cast<__nv_bfloat16*>(wst + jj * 64 + lane * 2) =
+                                __float2bfloat16_rn(f);
+                        }
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        __syncwarp();
+                        if (!(args.debug & 1)) {
+                            if (j0 + 32 <= tile.count) {
+                                if (lane == 0) {
+                                    asm volatile(
+                                        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                                            reinterpret_cast<uint64_t>(&map_out)),
+                                        "r"(mb * BM + mrow), "r"(tile.pos + j0), "r"(smem_u32(wst))
+                                        : "memory");
+                                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                                }
+                            } else if (j0 + lane < tile.count) {
+                                __nv_bfloat16* dst = args.out + (size_t)(tile.pos + j0 + lane) * args.M +
+                                                     mb * BM + mrow;
+                                asm volatile(
+                                    "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 64;" ::"l"(
+                                        reinterpret_cast<uint64_t>(dst)),
+                                    "r"(smem_u32(wst + lane * 64))
+                                    : "memory");
+                                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                            }
+                        }
+                        continue;
+                    }
                     // the bulk copies that last read this staging buffer are done
                     if (lane < ROWS_PER_WARP) {
                         if constexpr (EPI_BUFS == 2)
@@ -478,17 +522,7 @@ __global__ void __maxnreg__(kNT == 256 ? 128 : 64)
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32) : "memory");
                     const int jj = ew * ROWS_PER_WARP + lane;
-                    if (args.tma_store && j0 + 32 <= tile.count) {
-                        // a full chunk of a contiguous output: one [32 x BM] tensor store
-                        if (ew == 0 && lane == 0 && !(args.debug & 1)) {
-                            asm volatile(
-                                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                                    reinterpret_cast<uint64_t>(&map_out)),
-                                "r"(mb * BM), "r"(tile.pos + j0), "r"(smem_u32(stage))
-                                : "memory");
-                            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                        }
-                    } else if (lane < ROWS_PER_WARP && j0 + jj < tile.count && !(args.debug & 1)) {
+                    if (lane < ROWS_PER_WARP && j0 + jj < tile.count && !(args.debug & 1)) {
                         const int p = tile.pos + j0 + jj;
                         __nv_bfloat16* dst =
                             (args.row_dst ? reinterpret_cast<__nv_bfloat16*>(
@@ -546,8 +580,8 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
     // X: tiled boxes of 128 permuted rows, or single-row boxes for tile::gather4
     const CUtensorMap mx =
         make_map_2d(X, std::max<size_t>(x_rows, 1), K, x_row_ids ? 1 : 64, BK);
-    // contiguous output: tensor map for the epilogue's [32 tokens x 256 rows]
-    // stores (SWIZZLE_NONE: the staging tile is dense, 512 B per token row)
+    // contiguous output: tensor map for the epilogue warps' [32 tokens x 32 rows]
+    // stores (SWIZZLE_NONE: each warp's staging tile is dense, 64 B per token)
     static const bool tma_store_on = [] {
         const char* e = getenv("SCMOE_GEMM_TMA_STORE");
         return !(e && atoi(e) == 0);
@@ -555,7 +589,7 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
     const bool use_tma_store = tma_store_on && row_dst == nullptr;
     const CUtensorMap mo =
         use_tma_store ? make_tma_map_2d(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, sizeof(__nv_bfloat16),
-                                        std::max<size_t>(max_tiles * tile_rows, 1), M, 32, BM,
+                                        std::max<size_t>(max_tiles * tile_rows, 1), M, 32, 32,
                                         CU_TENSOR_MAP_SWIZZLE_NONE)
                       : mw;
     GemmArgs a;
@@ -593,7 +627,7 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
     if (tile_rows == 128) {
         go(grouped_gemm_kernel<128>, gemm_smem_bytes<128>(), NUM_THREADS, BM);
     } else if (tile_rows == 256 && slabs256 == 1) {
-        a.tma_store = 0;  // its 128-row units would need a 128-wide box
+        // (per-warp stores work for any BM)
         go(grouped_gemm_kernel<256, 1>, gemm_smem_bytes<256, 1>(), 32 * (EPI_WARP0 + 4), 128);
     } else if (tile_rows == 256) {
         go(grouped_gemm_kernel<256, 2>, gemm_smem_bytes<256, 2>(), NUM_THREADS, BM);

@@ -291,6 +291,13 @@ int scmoe_rmsnorm_route(scmoe_ctx* ctx, scmoe_router* r, const float* a1, const 
 int scmoe_ep_plan(scmoe_ctx* ctx, const uint32_t* indices, size_t tokens, size_t top_k,
                   size_t n_ffn, size_t n_zero, int world, int* send_counts, int* slot_send_pos,
                   int* send_token, int* send_expert);
+/* The permutation of moe_block (blocks.hpp:349-359) as the device computes it
+ * (the same kernels as the layer path): expert_count [n_ffn + n_zero] = slots
+ * per expert (zero experts included), slot_row [T*K] = position of token t in
+ * expert e's ascending token list, -1 for a zero expert.  Device pointers
+ * (either output may be NULL); StateError (latched) for an index >= E. */
+int scmoe_permutation(scmoe_ctx* ctx, const uint32_t* indices, size_t tokens, size_t top_k,
+                      size_t n_ffn, size_t n_zero, int* expert_count, int* slot_row);
 /* dst[i] = src[rows[i]] for i < n_rows (bf16 rows of width d). */
 int scmoe_gather_rows_bf16(scmoe_ctx* ctx, const void* src, size_t d, const int* rows,
                            size_t n_rows, void* dst);

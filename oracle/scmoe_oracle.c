@@ -22,6 +22,8 @@
  *   0 ok, 1 ConfigError, 2 DimensionError, 3 StateError, 4 ParameterError.
  */
 #include <math.h>
+#include <pthread.h>
+#include <stdatomic.h>
 #include <stddef.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -648,4 +650,133 @@ int orc_mla_infer_f32(size_t d, size_t dq, size_t dkv, size_t heads, size_t dhc,
     }
     free(qc); free(qr); free(kc); free(vv); free(merged);
     return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------
+ * moe_forward (blocks.hpp:372-394) for a token sample of a bank that does not
+ * fit host RAM (configs B/C: 512 experts x 100 MB in fp32).  TEST
+ * INFRASTRUCTURE: the parity tests call this at the headline shapes.
+ *
+ * Expert e's weights are regenerated from the synthetic recipe (SURVEY.md
+ * 8d): w_in = seeded_init Uniform of CounterRng(seed).stream(stream0 + 2e),
+ * w_out = stream(stream0 + 2e + 1) (rng.hpp:89-94), rounded to bf16 (RNE)
+ * when `bf16` is set, as the device bank stores them.  Every slot row
+ * y = silu(x_t W_in) W_out is computed with orc_mm_f32 over the sampled rows
+ * routed to e (row independent, tensor.hpp:95-112, so bitwise the per-slot
+ * orc_expert_row_f32), experts spread over `threads` workers; then the
+ * rank-order combine of ORC_DEFINE_MOE (moe_combine, blocks.hpp:251-274).
+ * ---------------------------------------------------------------------- */
+typedef struct {
+    const float* x;
+    size_t t_count, d, top_k, n_ffn, inter;
+    const uint32_t* indices;
+    uint64_t seed, stream0;
+    double variance;
+    int bf16;
+    float* y; /* [t_count * top_k][d] per-slot expert rows */
+    atomic_size_t next;
+    atomic_int rc;
+} OrcStreamJob;
+
+static float orc_bf16_rne(float v) {
+    uint32_t u;
+    memcpy(&u, &v, 4);
+    u = (u + 0x7FFFu + ((u >> 16) & 1u)) & 0xFFFF0000u;
+    memcpy(&v, &u, 4);
+    return v;
+}
+
+static void* orc_stream_worker(void* arg) {
+    OrcStreamJob* j = (OrcStreamJob*)arg;
+    const size_t d = j->d, I = j->inter, n_slots = j->t_count * j->top_k;
+    float* w_in = (float*)malloc(d * I * sizeof(float));
+    float* w_out = (float*)malloc(d * I * sizeof(float));
+    size_t* slots = (size_t*)malloc(ORC_NZ(n_slots) * sizeof(size_t));
+    float* xs = (float*)malloc(ORC_NZ(n_slots) * d * sizeof(float));
+    float* hs = (float*)malloc(ORC_NZ(n_slots) * I * sizeof(float));
+    float* ys = (float*)malloc(ORC_NZ(n_slots) * d * sizeof(float));
+    if (!w_in || !w_out || !slots || !xs || !hs || !ys) {
+        atomic_store(&j->rc, ORC_PARAMETER);
+    } else {
+        for (;;) {
+            const size_t e = atomic_fetch_add(&j->next, 1);
+            if (e >= j->n_ffn) break;
+            size_t m = 0;
+            for (size_t s = 0; s < n_slots; ++s)
+                if (j->indices[s] == e) slots[m++] = s;
+            if (m == 0) continue;
+            orc_seeded_uniform_f32(orc_stream_seed(j->seed, j->stream0 + 2 * e), 0, d * I,
+                                   j->variance, w_in);
+            orc_seeded_uniform_f32(orc_stream_seed(j->seed, j->stream0 + 2 * e + 1), 0, d * I,
+                                   j->variance, w_out);
+            if (j->bf16)
+                for (size_t i = 0; i < d * I; ++i) {
+                    w_in[i] = orc_bf16_rne(w_in[i]);
+                    w_out[i] = orc_bf16_rne(w_out[i]);
+                }
+            for (size_t r = 0; r < m; ++r)
+                memcpy(xs + r * d, j->x + (slots[r] / j->top_k) * d, d * sizeof(float));
+            orc_mm_f32(xs, w_in, hs, m, d, I);
+            for (size_t i = 0; i < m * I; ++i) hs[i] = hs[i] * orc_sigmoid_f32(hs[i]);
+            orc_mm_f32(hs, w_out, ys, m, I, d);
+            for (size_t r = 0; r < m; ++r)
+                memcpy(j->y + slots[r] * d, ys + r * d, d * sizeof(float));
+        }
+    }
+    free(w_in); free(w_out); free(slots); free(xs); free(hs); free(ys);
+    return NULL;
+}
+
+int orc_moe_forward_streamed_f32(const float* x, size_t t_count, size_t d, const uint32_t* indices,
+                                 const double* gates, size_t top_k, size_t n_ffn, size_t n_zero,
+                                 size_t inter, uint64_t seed, uint64_t stream0, double variance,
+                                 int bf16, double gamma_ffn_d, double gamma_zero_d, int renorm,
+                                 int threads, float* out) {
+    const size_t e_total = n_ffn + n_zero, n_slots = t_count * top_k;
+    for (size_t i = 0; i < n_slots; ++i)
+        if (indices[i] >= e_total) return ORC_STATE;
+    float* y = (float*)malloc(ORC_NZ(n_slots) * d * sizeof(float));
+    if (!y) return ORC_PARAMETER;
+    OrcStreamJob job = {x, t_count, d, top_k, n_ffn, inter, indices, seed, stream0, variance,
+                        bf16, y};
+    atomic_init(&job.next, 0);
+    atomic_init(&job.rc, ORC_OK);
+    if (threads < 1) threads = 1;
+    pthread_t* tid = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)threads);
+    for (int i = 0; i < threads; ++i) pthread_create(&tid[i], NULL, orc_stream_worker, &job);
+    for (int i = 0; i < threads; ++i) pthread_join(tid[i], NULL);
+    free(tid);
+    int rc = atomic_load(&job.rc);
+    if (!rc) {
+        const float gamma_ffn = (float)gamma_ffn_d, gamma_zero = (float)gamma_zero_d;
+        for (size_t t = 0; t < t_count; ++t) {
+            float* orow = out + t * d;
+            const float* xrow = x + t * d;
+            for (size_t j = 0; j < d; ++j) orow[j] = 0.0f;
+            float denom = 1.0f;
+            if (renorm) {
+                float s = 0.0f;
+                for (size_t sl = 0; sl < top_k; ++sl) s += (float)gates[t * top_k + sl];
+                denom = s;
+            }
+            float zero_w = 0.0f;
+            for (size_t sl = 0; sl < top_k; ++sl) {
+                const uint32_t e = indices[t * top_k + sl];
+                const float w = (float)gates[t * top_k + sl] / denom;
+                if (e < n_ffn) {
+                    const float coeff = gamma_ffn * w;
+                    const float* yr = y + (t * top_k + sl) * d;
+                    for (size_t j = 0; j < d; ++j) orow[j] += coeff * yr[j];
+                } else {
+                    zero_w += w;
+                }
+            }
+            if (zero_w != 0.0f) {
+                const float coeff = gamma_zero * zero_w;
+                for (size_t j = 0; j < d; ++j) orow[j] += coeff * xrow[j];
+            }
+        }
+    }
+    free(y);
+    return rc;
 }

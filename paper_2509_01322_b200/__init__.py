@@ -158,6 +158,7 @@ _PROTOS = {
     "scmoe_rmsnorm_route": (C.c_int, [_P, _P, _P, _P, _SZ, _P, _P, _P, _P, _P]),
     "scmoe_ep_plan": (C.c_int, [_P, _P, _SZ, _SZ, _SZ, _SZ, C.c_int, _P, _P, _P, _P]),
     "scmoe_gather_rows_bf16": (C.c_int, [_P, _P, _SZ, _P, _SZ, _P]),
+    "scmoe_permutation": (C.c_int, [_P, _P, _SZ, _SZ, _SZ, _SZ, _P, _P]),
     "scmoe_moe_rows": (C.c_int, [_P, _P, _P, _P, C.c_int, _SZ, _P]),
     "scmoe_combine_rows": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _SZ, _SZ, _SZ, C.c_int, _P,
                                      _P]),

@@ -1348,6 +1348,29 @@ int scmoe_ep_plan(scmoe_ctx* c, const uint32_t* idx, size_t T, size_t K, size_t 
     });
 }
 
+int scmoe_permutation(scmoe_ctx* c, const uint32_t* idx, size_t T, size_t K, size_t n_ffn,
+                      size_t n_zero, int* expert_count, int* slot_row) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        SCMOE_CHECK_ARG(K >= 1 && K <= 64, SCMOE_ERR_CONFIG, "moe_forward: top_k must be in [1, 64]");
+        const size_t E = n_ffn + n_zero;
+        if (T == 0) {
+            if (expert_count) SCMOE_CUDA(cudaMemsetAsync(expert_count, 0, E * sizeof(int), c->stream));
+            return;
+        }
+        launch_check_indices(c, idx, T * K, E);
+        PermResult pr;
+        {
+            ProfScope _p(c, "permute");
+            pr = launch_permute(c, idx, T, K, n_ffn, E, 192);
+        }
+        if (expert_count)
+            SCMOE_CUDA(cudaMemcpyAsync(expert_count, pr.expert_count, E * sizeof(int),
+                                       cudaMemcpyDeviceToDevice, c->stream));
+        if (slot_row) launch_slot_rows(c, idx, pr.slot_pos, pr.expert_base, T * K, (int)n_ffn, slot_row);
+    });
+}
+
 int scmoe_gather_rows_bf16(scmoe_ctx* c, const void* src, size_t d, const int* rows,
                            size_t n_rows, void* dst) {
     return guarded(c, [&] {

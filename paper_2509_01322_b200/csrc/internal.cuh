@@ -315,6 +315,8 @@ void launch_ep_bins(scmoe_ctx* c, const uint32_t* idx, size_t n, size_t n_ffn, s
                     int world, uint32_t* bins);
 void launch_ep_send_expert(scmoe_ctx* c, const uint32_t* idx, const int* slot_pos, size_t n,
                            int* send_expert);
+void launch_slot_rows(scmoe_ctx* c, const uint32_t* idx, const int* slot_pos,
+                      const int* expert_base, size_t n, int n_ffn, int* slot_row);
 void launch_ep_localize(scmoe_ctx* c, const int* row_expert, size_t n, int offset, int n_local,
                         uint32_t* local);
 void launch_gather_rows_bf16(scmoe_ctx* c, const __nv_bfloat16* src, size_t d, const int* rows,

@@ -832,6 +832,26 @@ void launch_ep_send_expert(scmoe_ctx* c, const uint32_t* idx, const int* slot_po
     SCMOE_LAUNCH_CHECK(c);
 }
 
+// moe_block's permutation in the reference's own terms (blocks.hpp:349-359):
+// slot_row[t*K+s] = position of token t in expert e's ascending token list
+// (slot_pos minus the expert's base row), -1 for a zero expert.
+__global__ void slot_rows_kernel(const uint32_t* __restrict__ idx, const int* __restrict__ slot_pos,
+                                 const int* __restrict__ expert_base, size_t n, int n_ffn,
+                                 int* __restrict__ slot_row) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t e = idx[i];
+    slot_row[i] = e < (uint32_t)n_ffn ? slot_pos[i] - expert_base[e] : -1;
+}
+
+void launch_slot_rows(scmoe_ctx* c, const uint32_t* idx, const int* slot_pos,
+                      const int* expert_base, size_t n, int n_ffn, int* slot_row) {
+    if (n == 0) return;
+    slot_rows_kernel<<<ceil_div(n, 256), 256, 0, c->stream>>>(idx, slot_pos, expert_base, n, n_ffn,
+                                                              slot_row);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
 // Received rows' global expert ids -> this rank's local ids (range-checked).
 __global__ void ep_localize_kernel(const int* __restrict__ row_expert, size_t n, int offset,
                                    int n_local, uint32_t* __restrict__ local,

@@ -76,11 +76,12 @@ class DeviceLayer:
         """accumulate_counters on the device (indices as a device pointer)."""
         self.ctx._check(lib().scmoe_accumulate_counters(self.ctx.handle, self.router, idx, tokens))
 
-    def bias_update(self):
-        """bias_update; returns the applied deltas (numpy)."""
+    def bias_update(self, want_delta: bool = True):
+        """bias_update; returns the applied deltas (numpy) when want_delta."""
         import numpy as np
-        delta = np.empty(self.shape.E, np.float64)
+        delta = np.empty(self.shape.E, np.float64) if want_delta else None
         self.ctx._check(lib().scmoe_bias_update(self.ctx.handle, self.router,
+                                                None if delta is None else
                                                 delta.ctypes.data_as(_P)))
         return delta
 

@@ -35,13 +35,14 @@ class ScMoEStack:
                        for l in range(n_layers)]
         self.trace = StackTrace()
 
-    def step(self, x: torch.Tensor, T: int, keep_inputs: bool = False):
+    def step(self, x: torch.Tensor, T: int, keep_inputs: bool = False, record: bool = True):
         """One training-style step: forward through every layer, count, tick.
         Returns the per-layer routing indices (device) and, if requested, the
-        per-layer inputs (for teacher-forced checking)."""
+        per-layer inputs (for teacher-forced checking).  record=True appends
+        the per-layer mean/std activated FFN experts to the trace (one host
+        read of the ffn counts per step)."""
         s = self.shape
-        inputs, idxs = [], []
-        means, stds = [], []
+        inputs, idxs, cnts = [], [], []
         for layer in self.layers:
             if keep_inputs:
                 inputs.append(x.clone())
@@ -51,16 +52,17 @@ class ScMoEStack:
             out = torch.empty_like(x)
             layer.forward(x.data_ptr(), x.data_ptr(), None, T, idx.data_ptr(), gates.data_ptr(),
                           cnt.data_ptr(), out.data_ptr())
-            layer.accumulate(idx.data_ptr(), T)
-            self.ctx.synchronize()
-            c = cnt.cpu().numpy().astype(np.float64)
-            means.append(float(c.mean()))
-            stds.append(float(c.std()))
+            layer.accumulate(idx.data_ptr(), T)  # Model::accumulate_routing
             idxs.append(idx)
+            cnts.append(cnt)
             x = out
+        # Model::update_biases: only layers that saw tokens (every layer here
+        # when T > 0); bias_update synchronises for its StateError check
         for layer in self.layers:
-            if layer.tokens_seen() > 0:
-                layer.bias_update()
-        self.trace.mean_ffn.append(means)
-        self.trace.std_ffn.append(stds)
+            if T > 0:
+                layer.bias_update(want_delta=False)
+        if record:
+            c = torch.stack(cnts).to(torch.float64).cpu().numpy()  # [layer, T]
+            self.trace.mean_ffn.append([float(v) for v in c.mean(1)])
+            self.trace.std_ffn.append([float(v) for v in c.std(1)])
         return idxs, inputs, x

@@ -75,6 +75,9 @@ _ORC_PROTOS = {
     "orc_moe_forward_f64": (C.c_int, [_P, _SZ, _SZ, _P, _P, _SZ, _SZ, _SZ, _P, _P, _SZ, _D, _D,
                                       C.c_int, _P]),
     "orc_permutation": (None, [_P, _SZ, _SZ, _SZ, _SZ, _P, _P]),
+    "orc_moe_forward_streamed_f32": (C.c_int, [_P, _SZ, _SZ, _P, _P, _SZ, _SZ, _SZ, _SZ, _U64,
+                                               _U64, _D, C.c_int, _D, _D, C.c_int, C.c_int,
+                                               _P]),
     "orc_expert_row_f32": (None, [_P, _SZ, _P, _P, _SZ, _P, _P]),
     "orc_dense_branch_f32": (C.c_int, [_P, _P, _SZ, _SZ, _P, _P, _SZ, _P]),
     "orc_scmoe_layer_f32": (C.c_int, [_P, _P, _P, _SZ, _SZ, _P, _SZ, _SZ, _SZ, _SZ, _D, _P, _P,
@@ -228,6 +231,23 @@ def orc_moe_forward(x, idx, gates, k, n_ffn, n_zero, w_in, w_out, gamma_ffn=1.0,
                                    ptr(np.ascontiguousarray(gates, np.float64)), k, n_ffn, n_zero,
                                    ptr_array(w_in), ptr_array(w_out), I, gamma_ffn, gamma_zero,
                                    int(renorm), ptr(out))
+    return rc, out
+
+
+def orc_moe_forward_streamed(x, idx, gates, k, n_ffn, n_zero, inter, seed, stream0=100,
+                             bf16=True, gamma_ffn=1.0, gamma_zero=1.0, renorm=False,
+                             threads=None):
+    """moe_forward on a token sample with the expert bank regenerated per
+    expert from its seeded_init Uniform streams (variance 1/d), bf16-rounded
+    as the device bank stores them (configs B/C; oracle/scmoe_oracle.c)."""
+    x = np.ascontiguousarray(x, np.float32)
+    T, d = x.shape
+    out = np.empty((T, d), np.float32)
+    rc = orc().orc_moe_forward_streamed_f32(
+        ptr(x), T, d, ptr(np.ascontiguousarray(idx, np.uint32)),
+        ptr(np.ascontiguousarray(gates, np.float64)), k, n_ffn, n_zero, inter, seed, stream0,
+        1.0 / d, int(bf16), gamma_ffn, gamma_zero, int(renorm), threads or os.cpu_count() or 1,
+        ptr(out))
     return rc, out
 
 

@@ -353,3 +353,32 @@ def test_route_topk_f64_oracle_equals_reference(orc, ref, shape):
     assert rc1 == rc2 == 0
     assert (i1 == i2).all() and (g1.view(np.uint64) == g2.view(np.uint64)).all()
     assert (c1 == c2).all() and (p1.view(np.uint64) == p2.view(np.uint64)).all()
+
+
+@pytest.mark.parametrize("bf16,renorm,gm,m", [(False, False, 0, 1), (True, False, 0, 1),
+                                               (False, True, 1, 2)])
+def test_streamed_moe_oracle_equals_reference(orc, ref, bf16, renorm, gm, m):
+    """The per-expert streamed moe_forward (the checker of the headline-shape
+    GPU tests, whose 512-expert fp32 bank does not fit host RAM) is bitwise
+    the reference's moe_forward on the same (bf16-rounded) weights."""
+    T, d, n, z, k, ke, I, seed = 80, 256, 8, 4, 3, 2, 128, 41
+    x = O.normal_f32(O.stream_seed(98, 1), T * d).reshape(T, d)
+    w = O.uniform_f32(O.stream_seed(5, 0), d * (n + z), 1.0 / d).reshape(d, n + z)
+    _, idx, g, _, _ = O.orc_route_topk(x, w, n, z, k, ke)
+    rnd = O.bf16_round if bf16 else (lambda a: a)
+    w_in = [rnd(O.uniform_f32(O.stream_seed(seed, 100 + 2 * e), d * I, 1.0 / d)).reshape(d, I)
+            for e in range(n)]
+    w_out = [rnd(O.uniform_f32(O.stream_seed(seed, 101 + 2 * e), I * d, 1.0 / d)).reshape(I, d)
+             for e in range(n)]
+    gf = 1.0 if gm == 2 else float(m)
+    gz = float(m) if gm == 1 else 1.0
+    rc1, o1 = O.orc_moe_forward_streamed(x, idx, g, k, n, z, I, seed, bf16=bf16, gamma_ffn=gf,
+                                         gamma_zero=gz, renorm=renorm, threads=3)
+    rc2, o2 = O.orc_moe_forward(x, idx, g, k, n, z, w_in, w_out, gf, gz, renorm)
+    assert rc1 == rc2 == 0
+    assert (o1.view(np.uint32) == o2.view(np.uint32)).all()
+    if not renorm:
+        o3 = np.empty_like(o1)
+        assert ref.ref_moe_forward_f32(ptr(x), T, d, ptr(idx), ptr(g), k, n, z, ptr_array(w_in),
+                                       ptr_array(w_out), I, m, gm, ptr(o3), 4) == 0
+        assert (o1.view(np.uint32) == o3.view(np.uint32)).all()

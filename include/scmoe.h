@@ -330,6 +330,69 @@ int scmoe_combine_rows(scmoe_ctx* ctx, scmoe_bank* b, const float* x, const void
                        size_t tokens, size_t top_k, size_t n_ffn_total, int renormalize,
                        const float* residual, float* out);
 
+/* ---- expert-parallel layer, device-resident orchestration ------------------
+ * One process (or thread) per GPU; the whole layer runs stream-ordered on the
+ * device with no host synchronisation per call: route, dispatch plan, an
+ * on-device exchange of the [G][G] slot-count matrix (each rank stores its row
+ * into every peer's buffer + an epoch flag), dispatch of the bf16 rows by peer
+ * stores over NVLink into the owners' receive buffers, grouped GEMMs on the
+ * received rows (count read on the device) whose GEMM2 epilogue writes every
+ * output row into the source rank's return buffer, an epoch barrier, and the
+ * rank-order combine at the source.  Output bitwise equal to the single-GPU
+ * layer (scmoe_layer_forward) on the same tokens.  NCCL supplies the
+ * communicator, the one-time exchange of the buffers' CUDA IPC handles and
+ * the controller's counter all-reduce (router.hpp:158-169). */
+typedef struct scmoe_ep scmoe_ep;
+/* ncclUniqueId for rank 0 to hand to the other ranks out of band. */
+size_t scmoe_ep_unique_id_bytes(void);
+int scmoe_ep_unique_id(void* out);
+/* Collective over the `world` ranks.  rank g owns FFN experts
+ * [g*n_ffn/world, (g+1)*n_ffn/world); max_tokens bounds the tokens per rank and
+ * call; max_recv_rows = 0 sizes the receive buffers for the worst case
+ * (world * max_tokens * min(top_k, n_ffn/world) rows: no routing can overflow). */
+int scmoe_ep_create(scmoe_ctx* ctx, int world, int rank, const void* nccl_unique_id,
+                    size_t d_model, size_t n_ffn, size_t n_zero, size_t top_k, size_t max_tokens,
+                    size_t max_recv_rows, scmoe_ep** out);
+int scmoe_ep_destroy(scmoe_ep* ep); /* collective */
+size_t scmoe_ep_capacity_rows(const scmoe_ep* ep);
+/* Timing reference for the exposed-communication share: on = 0 replaces the
+ * row transfers by no-ops (received rows left as they are, spread over the
+ * local experts; GEMM2 rows stay local).  Results are garbage while off. */
+int scmoe_ep_set_comm(scmoe_ep* ep, int on);
+/* SMs the dense branch's GEMMs leave free (default 16). */
+int scmoe_ep_set_dense_reserve(scmoe_ep* ep, int reserve_sms);
+/* One layer on this rank's T tokens (Model::build_layer MoE branch,
+ * model.hpp:394-400): out = residual + moe(rmsnorm(a1)), residual = a3, or,
+ * with a one-expert bf16 `dense` bank, dd = a1 + ffn_block(rmsnorm(a1))
+ * computed on a second stream beside routing / dispatch / experts / return
+ * (the ScMoE overlap window; model.hpp:390-391).  bank = this rank's experts.
+ * Device pointers, stream-ordered on ctx's stream. */
+int scmoe_ep_layer_forward(scmoe_ep* ep, scmoe_router* r, scmoe_bank* bank, scmoe_bank* dense,
+                           const float* a1, const float* a3, const float* gain, size_t tokens,
+                           int renormalize, uint32_t* indices, double* gates,
+                           uint32_t* ffn_count, float* out);
+/* A stream of batches, pipelined: batch i+1's front half (route, plan,
+ * exchange, dispatch) on one stream beside batch i's back half (expert GEMMs
+ * with the fused return, combine) on another; two buffer sets alternate.
+ * corun_router selects the router kernel that co-resides with the GEMM.
+ * Identical to n_batches scmoe_ep_layer_forward calls. */
+int scmoe_ep_layer_forward_batches(scmoe_ep* ep, scmoe_router* r, scmoe_bank* bank,
+                                   size_t n_batches, const float* const* a1,
+                                   const float* const* a3, const float* gain, size_t tokens,
+                                   int renormalize, int corun_router, uint32_t* const* indices,
+                                   double* const* gates, uint32_t* const* ffn_count,
+                                   float* const* out);
+/* accumulate_counters of this rank's routing (router.hpp:144-150) and, with
+ * update, bias_update over the GLOBAL batch (router.hpp:155-176): the [E]
+ * counters and tokens_seen are summed over the ranks on the device
+ * (ncclAllReduce, exact integers), so every rank applies the same update.
+ * delta [E] (host, nullable) receives the deltas (synchronises).  StateError
+ * from the device check latches (next scmoe_synchronize). */
+int scmoe_ep_controller_step(scmoe_ep* ep, scmoe_router* r, const uint32_t* indices,
+                             size_t tokens, int update, double* delta);
+/* [world][world] slot counts of the most recent call (synchronises). */
+int scmoe_ep_count_matrix_host(scmoe_ep* ep, int* matrix);
+
 /* ---- Multi-head latent attention, forward value, S = float (f2 row) --------
  * MlaParams<float> (blocks.hpp:38-58); mla_block forward (blocks.hpp:73-102)
  * over packed sequences; MlaCache + mla_infer_step (blocks.hpp:106-181).

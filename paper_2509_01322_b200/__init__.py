@@ -159,6 +159,20 @@ _PROTOS = {
     "scmoe_ep_plan": (C.c_int, [_P, _P, _SZ, _SZ, _SZ, _SZ, C.c_int, _P, _P, _P, _P]),
     "scmoe_gather_rows_bf16": (C.c_int, [_P, _P, _SZ, _P, _SZ, _P]),
     "scmoe_permutation": (C.c_int, [_P, _P, _SZ, _SZ, _SZ, _SZ, _P, _P]),
+    "scmoe_ep_unique_id_bytes": (_SZ, []),
+    "scmoe_ep_unique_id": (C.c_int, [_P]),
+    "scmoe_ep_create": (C.c_int, [_P, C.c_int, C.c_int, _P, _SZ, _SZ, _SZ, _SZ, _SZ, _SZ,
+                                  C.POINTER(_P)]),
+    "scmoe_ep_destroy": (C.c_int, [_P]),
+    "scmoe_ep_capacity_rows": (_SZ, [_P]),
+    "scmoe_ep_set_comm": (C.c_int, [_P, C.c_int]),
+    "scmoe_ep_set_dense_reserve": (C.c_int, [_P, C.c_int]),
+    "scmoe_ep_layer_forward": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _SZ, C.c_int, _P, _P, _P,
+                                         _P]),
+    "scmoe_ep_layer_forward_batches": (C.c_int, [_P, _P, _P, _SZ, _P, _P, _P, _SZ, C.c_int,
+                                                 C.c_int, _P, _P, _P, _P]),
+    "scmoe_ep_controller_step": (C.c_int, [_P, _P, _P, _SZ, C.c_int, _P]),
+    "scmoe_ep_count_matrix_host": (C.c_int, [_P, _P]),
     "scmoe_moe_rows": (C.c_int, [_P, _P, _P, _P, C.c_int, _SZ, _P]),
     "scmoe_combine_rows": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _SZ, _SZ, _SZ, C.c_int, _P,
                                      _P]),

@@ -36,6 +36,7 @@ SOURCES = {
     "mla.cu": ["--fmad=false"],
     "capi.cu": [],
     "gemm_sm100.cu": ["-Xptxas", "-v"],
+    "ep.cu": [],
 }
 HOST_SOURCES = ["host_rng.cpp"]
 HEADERS = ["internal.cuh", "libm_port.h", "sm100_util.cuh", "f32x2.cuh"]
@@ -119,7 +120,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             logs = list(ex.map(_run, jobs))
     if force or jobs or not os.path.exists(LIB) or _newer(objs, LIB):
         tmp = LIB + ".tmp"
-        _run([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lpthread"])
+        _run([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lpthread", "-ldl"])
         summary = check_sass(tmp)  # a library failing the SASS checks is never installed
         os.replace(tmp, LIB)
         with open(os.path.join(BUILD, "sass_summary.txt"), "w") as f:

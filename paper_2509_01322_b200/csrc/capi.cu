@@ -84,6 +84,10 @@ void sync_and_check(scmoe_ctx* c) {
         if (st == DEV_ERR_INDEX_RANGE) SCMOE_THROW(SCMOE_ERR_STATE, "moe_forward: expert index out of range");
         if (st == DEV_ERR_COUNTERS)
             SCMOE_THROW(SCMOE_ERR_STATE, "bias_update: counters do not cover top_k slots per token");
+        if (st == DEV_ERR_EMPTY) SCMOE_THROW(SCMOE_ERR_STATE, "bias_update: empty batch");
+        if (st == DEV_ERR_CAPACITY)
+            SCMOE_THROW(SCMOE_ERR_STATE, "ep: receive buffer capacity exceeded (rows dropped)");
+        if (st == DEV_ERR_TIMEOUT) SCMOE_THROW(SCMOE_ERR_CUDA, "ep: peer barrier timed out");
         SCMOE_THROW(SCMOE_ERR_INTERNAL, "device reported an unknown error");
     }
 }
@@ -1381,6 +1385,8 @@ int scmoe_gather_rows_bf16(scmoe_ctx* c, const void* src, size_t d, const int* r
     });
 }
 
+}  // extern "C"
+
 namespace {
 // Expert rows of the received slots; GEMM2's rows go to y (received order,
 // through an unpermute copy) or, with row_dst, straight to row_dst[r] for
@@ -1398,20 +1404,27 @@ int ep_tile_rows(const scmoe_ctx* c) {
     return v;
 }
 
+}  // namespace
+
+namespace scmoe {
+// R_dev: the row count lives on the device (R is then the capacity); the
+// output must go to row_dst (expert-parallel receive side, ep.cu).
 void moe_rows_impl(scmoe_ctx* c, scmoe_bank* b, const void* x_bf16, const int* row_expert,
-                   int expert_offset, size_t R, void* y_bf16, const uint64_t* row_dst) {
+                   int expert_offset, size_t R, void* y_bf16, const uint64_t* row_dst,
+                   const int* R_dev) {
     if (b->precision != SCMOE_PREC_BF16)
         SCMOE_THROW(SCMOE_ERR_CONFIG, "moe_rows: needs a bf16 (tensor-core) bank");
     if (R == 0) return;
+    SCMOE_CHECK_ARG(!R_dev || row_dst, SCMOE_ERR_INTERNAL, "moe_rows: device count needs row_dst");
     const size_t d = b->d, I = b->inter, n = b->n;
     Workspace& ws = c->ws;
     uint32_t* loc = ws.ep_local.get<uint32_t>(R);
-    launch_ep_localize(c, row_expert, R, expert_offset, (int)n, loc);
+    launch_ep_localize(c, row_expert, R, expert_offset, (int)n, loc, R_dev);
     // each row is a "token" routed to exactly one local expert (K = 1)
     PermResult pr;
     {
         ProfScope _p(c, "permute");
-        pr = launch_permute(c, loc, R, 1, n, n, ep_tile_rows(c));
+        pr = launch_permute(c, loc, R, 1, n, n, ep_tile_rows(c), false, R_dev);
     }
     const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x_bf16);
     __nv_bfloat16* xp = ws.xp.get<__nv_bfloat16>(R * d);
@@ -1443,13 +1456,15 @@ void moe_rows_impl(scmoe_ctx* c, scmoe_bank* b, const void* x_bf16, const int* r
     ProfScope _p(c, "unpermute");
     launch_gather_rows_bf16(c, y, d, pr.slot_pos, R, static_cast<__nv_bfloat16*>(y_bf16));
 }
-}  // namespace
+}  // namespace scmoe
+
+extern "C" {
 
 int scmoe_moe_rows(scmoe_ctx* c, scmoe_bank* b, const void* x_bf16, const int* row_expert,
                    int expert_offset, size_t R, void* y_bf16) {
     return guarded(c, [&] {
         require_ctx(c);
-        moe_rows_impl(c, b, x_bf16, row_expert, expert_offset, R, y_bf16, nullptr);
+        moe_rows_impl(c, b, x_bf16, row_expert, expert_offset, R, y_bf16, nullptr, nullptr);
     });
 }
 
@@ -1459,7 +1474,7 @@ int scmoe_moe_rows_to(scmoe_ctx* c, scmoe_bank* b, const void* x_bf16, const int
         require_ctx(c);
         SCMOE_CHECK_ARG(row_dst != nullptr || R == 0, SCMOE_ERR_PARAMETER,
                         "moe_rows_to: row_dst is required");
-        moe_rows_impl(c, b, x_bf16, row_expert, expert_offset, R, nullptr, row_dst);
+        moe_rows_impl(c, b, x_bf16, row_expert, expert_offset, R, nullptr, row_dst, nullptr);
     });
 }
 

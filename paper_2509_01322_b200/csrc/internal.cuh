@@ -31,7 +31,14 @@ struct ScmoeError {
     } while (0)
 
 // Device-side latched errors (written by kernels that validate data).
-enum : int { DEV_OK = 0, DEV_ERR_INDEX_RANGE = 1, DEV_ERR_COUNTERS = 2 };
+enum : int {
+    DEV_OK = 0,
+    DEV_ERR_INDEX_RANGE = 1,
+    DEV_ERR_COUNTERS = 2,
+    DEV_ERR_EMPTY = 3,    // bias_update on an empty batch (router.hpp:157), device-side seen
+    DEV_ERR_CAPACITY = 4, // expert-parallel receive buffer capacity exceeded
+    DEV_ERR_TIMEOUT = 5   // expert-parallel peer barrier timed out (a rank did not arrive)
+};
 
 // ---------------------------------------------------------------------------
 // Grow-only device workspace.
@@ -276,8 +283,11 @@ struct PermResult {
 };
 // multi: a token may hit the same bin in several slots (EP destination ranks);
 // otherwise each token hits an expert at most once (top-K of distinct experts).
+// T_dev: the token count lives on the device (T is then the capacity the
+// grids and buffers are sized for; expert-parallel receive side).
 PermResult launch_permute(scmoe_ctx* c, const uint32_t* idx, size_t T, size_t K, size_t n_ffn,
-                          size_t E, int tile_rows, bool multi = false);
+                          size_t E, int tile_rows, bool multi = false,
+                          const int* T_dev = nullptr);
 void launch_gather_bf16(scmoe_ctx* c, const __nv_bfloat16* src, size_t d, const int* row_token,
                         const int* expert_base, size_t n_ffn, size_t max_rows,
                         __nv_bfloat16* dst);
@@ -292,7 +302,11 @@ void launch_combine_bf16(scmoe_ctx* c, const float* x, const __nv_bfloat16* y,
 void launch_check_indices(scmoe_ctx* c, const uint32_t* idx, size_t n, size_t E);
 void launch_ffn_moments(scmoe_ctx* c, const uint32_t* cnt, size_t T, double* out);
 void launch_accumulate(scmoe_ctx* c, const uint32_t* idx, size_t n, size_t E, uint64_t* routed);
-void launch_bias_update(scmoe_ctx* c, scmoe_router* r, double* delta_dev);
+// routed / seen_dev (optional): counters and tokens_seen already on the device
+// (summed over the expert-parallel ranks); default: the router's own counters
+// and its host mirror of tokens_seen.
+void launch_bias_update(scmoe_ctx* c, scmoe_router* r, double* delta_dev,
+                        const uint64_t* routed = nullptr, const uint64_t* seen_dev = nullptr);
 void launch_uniform_init(scmoe_ctx* c, uint64_t seed, uint64_t first, size_t n,
                          double half_width, float* out);
 void launch_uniform_init_bf16_t(scmoe_ctx* c, uint64_t seed, size_t rows, size_t cols,
@@ -318,9 +332,15 @@ void launch_ep_send_expert(scmoe_ctx* c, const uint32_t* idx, const int* slot_po
 void launch_slot_rows(scmoe_ctx* c, const uint32_t* idx, const int* slot_pos,
                       const int* expert_base, size_t n, int n_ffn, int* slot_row);
 void launch_ep_localize(scmoe_ctx* c, const int* row_expert, size_t n, int offset, int n_local,
-                        uint32_t* local);
+                        uint32_t* local, const int* n_dev = nullptr);
 void launch_gather_rows_bf16(scmoe_ctx* c, const __nv_bfloat16* src, size_t d, const int* rows,
                              size_t n_rows, __nv_bfloat16* dst);
+
+// Expert FFN on rows that each carry one (global) expert id (capi.cu); with
+// R_dev the count is read on the device and R is the capacity.
+void moe_rows_impl(scmoe_ctx* c, scmoe_bank* b, const void* x_bf16, const int* row_expert,
+                   int expert_offset, size_t R, void* y_bf16, const uint64_t* row_dst,
+                   const int* R_dev);
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
 // the attribute belongs to the device context, and callers may drive several
@@ -340,7 +360,7 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
 void launch_ep_put_rows(scmoe_ctx* c, const __nv_bfloat16* src, size_t d, const int* send_token,
                         const int* send_expert, size_t n_send, const int* send_start,
                         const int64_t* dst_offset, const uint64_t* peer_rows,
-                        const uint64_t* peer_expert, int G);
+                        const uint64_t* peer_expert, int G, int64_t cap_dst = INT64_MAX);
 
 // ---- MLA (mla.cu) ----
 // Attention operands of the (sequence b, head h) pairs.  Rows of sequence b

@@ -20,8 +20,13 @@ constexpr int kMaskWords = kTB / 32;
 __global__ void __launch_bounds__(kTB) perm_hist_kernel(const uint32_t* __restrict__ idx, int T,
                                                         int K, int E, int* __restrict__ rank_in_block,
                                                         int* __restrict__ block_counts,
-                                                        int* __restrict__ dev_status) {
+                                                        int* __restrict__ dev_status,
+                                                        const int* __restrict__ T_dev) {
     extern __shared__ uint32_t masks[];  // [E][kMaskWords]
+    if (T_dev) {  // device-side token count (T = capacity): blocks past it have no work
+        T = min(T, *T_dev);
+        if ((int)blockIdx.x * kTB >= T) return;
+    }
     for (int i = threadIdx.x; i < E * kMaskWords; i += blockDim.x) masks[i] = 0;
     __syncthreads();
     const int tl = threadIdx.x;
@@ -95,7 +100,9 @@ __global__ void __launch_bounds__(1024) perm_scan_kernel(int nblk, int E, int n_
                                                          int* __restrict__ expert_count,
                                                          int* __restrict__ expert_base,
                                                          TokenTile* __restrict__ tiles,
-                                                         int* __restrict__ n_tiles) {
+                                                         int* __restrict__ n_tiles,
+                                                         const int* __restrict__ T_dev) {
+    if (T_dev) nblk = min(nblk, (*T_dev + kTB - 1) / kTB);
     for (int e = threadIdx.x; e < E; e += blockDim.x) {
         int run = 0;
         for (int b = 0; b < nblk; ++b) {
@@ -144,8 +151,9 @@ __global__ void perm_scatter_kernel(const uint32_t* __restrict__ idx, int T, int
                                     int n_ffn, const int* __restrict__ rank_in_block,
                                     const int* __restrict__ block_offsets,
                                     const int* __restrict__ expert_base, int* __restrict__ slot_pos,
-                                    int* __restrict__ row_token) {
+                                    int* __restrict__ row_token, const int* __restrict__ T_dev) {
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (T_dev) T = min(T, *T_dev);
     if (i >= (size_t)T * K) return;
     const int t = (int)(i / K);
     const uint32_t e = idx[i];
@@ -210,7 +218,7 @@ __global__ void __launch_bounds__(kTB) perm_hist_multi_kernel(
 }
 
 PermResult launch_permute(scmoe_ctx* c, const uint32_t* idx, size_t T, size_t K, size_t n_ffn,
-                          size_t E, int tile_rows, bool multi) {
+                          size_t E, int tile_rows, bool multi, const int* T_dev) {
     Workspace& ws = c->ws;
     if (multi) SCMOE_CHECK_ARG(E <= kMaxMultiBins, SCMOE_ERR_CONFIG, "permute: too many bins");
     const size_t nblk = ceil_div(std::max<size_t>(T, 1), kTB);
@@ -229,25 +237,26 @@ PermResult launch_permute(scmoe_ctx* c, const uint32_t* idx, size_t T, size_t K,
     if (smem > 48 * 1024)
         SCMOE_CUDA(cudaFuncSetAttribute(perm_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
+    SCMOE_CHECK_ARG(!(multi && T_dev), SCMOE_ERR_INTERNAL, "permute: device count needs single bins");
     if (T > 0 && multi) {
         perm_hist_multi_kernel<<<nblk, kTB, 0, c->stream>>>(idx, (int)T, (int)K, (int)E, rank,
                                                             bcounts, c->dev_status);
         SCMOE_LAUNCH_CHECK(c);
     } else if (T > 0) {
         perm_hist_kernel<<<nblk, kTB, smem, c->stream>>>(idx, (int)T, (int)K, (int)E, rank, bcounts,
-                                                         c->dev_status);
+                                                         c->dev_status, T_dev);
         SCMOE_LAUNCH_CHECK(c);
     } else {
         SCMOE_CUDA(cudaMemsetAsync(bcounts, 0, nblk * E * sizeof(int), c->stream));
     }
     perm_scan_kernel<<<1, 1024, 0, c->stream>>>((int)nblk, (int)E, (int)n_ffn, tile_rows, bcounts,
                                                 pr.expert_count, pr.expert_base, pr.tiles,
-                                                pr.n_tiles);
+                                                pr.n_tiles, T_dev);
     SCMOE_LAUNCH_CHECK(c);
     if (T > 0) {
         perm_scatter_kernel<<<ceil_div(T * K, 256), 256, 0, c->stream>>>(
             idx, (int)T, (int)K, (int)E, (int)n_ffn, rank, bcounts, pr.expert_base, pr.slot_pos,
-            pr.row_token);
+            pr.row_token, T_dev);
         SCMOE_LAUNCH_CHECK(c);
     }
     return pr;
@@ -606,8 +615,16 @@ void launch_accumulate(scmoe_ctx* c, const uint32_t* idx, size_t n, size_t E, ui
 __global__ void bias_update_kernel(int n_ffn, int E, int top_k, int k_expected, double mu,
                                    unsigned long long tokens_seen, double* __restrict__ b,
                                    unsigned long long* __restrict__ routed,
-                                   double* __restrict__ delta, int* __restrict__ dev_status) {
+                                   double* __restrict__ delta, int* __restrict__ dev_status,
+                                   const unsigned long long* __restrict__ seen_dev) {
     __shared__ unsigned long long total;
+    if (seen_dev) {  // tokens_seen summed over the ranks on the device (expert parallelism)
+        tokens_seen = *seen_dev;
+        if (tokens_seen == 0) {  // router.hpp:157
+            if (threadIdx.x == 0) atomicExch(dev_status, DEV_ERR_EMPTY);
+            return;
+        }
+    }
     if (threadIdx.x == 0) {
         unsigned long long s = 0;
         for (int i = 0; i < E; ++i) s += routed[i];
@@ -632,12 +649,15 @@ __global__ void bias_update_kernel(int n_ffn, int E, int top_k, int k_expected, 
     }
 }
 
-void launch_bias_update(scmoe_ctx* c, scmoe_router* r, double* delta_dev) {
+void launch_bias_update(scmoe_ctx* c, scmoe_router* r, double* delta_dev,
+                        const uint64_t* routed, const uint64_t* seen_dev) {
     bias_update_kernel<<<1, 256, 0, c->stream>>>((int)r->n_ffn, (int)r->E(), (int)r->top_k,
                                                  (int)r->k_expected, r->mu,
                                                  (unsigned long long)r->tokens_seen, r->b,
-                                                 reinterpret_cast<unsigned long long*>(r->routed),
-                                                 delta_dev, c->dev_status);
+                                                 reinterpret_cast<unsigned long long*>(
+                                                     const_cast<uint64_t*>(routed ? routed : r->routed)),
+                                                 delta_dev, c->dev_status,
+                                                 reinterpret_cast<const unsigned long long*>(seen_dev));
     SCMOE_LAUNCH_CHECK(c);
 }
 
@@ -855,8 +875,9 @@ void launch_slot_rows(scmoe_ctx* c, const uint32_t* idx, const int* slot_pos,
 // Received rows' global expert ids -> this rank's local ids (range-checked).
 __global__ void ep_localize_kernel(const int* __restrict__ row_expert, size_t n, int offset,
                                    int n_local, uint32_t* __restrict__ local,
-                                   int* __restrict__ dev_status) {
+                                   int* __restrict__ dev_status, const int* __restrict__ n_dev) {
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n_dev) n = min(n, (size_t)max(*n_dev, 0));
     if (i >= n) return;
     const int e = row_expert[i] - offset;
     if (e < 0 || e >= n_local) {
@@ -868,10 +889,10 @@ __global__ void ep_localize_kernel(const int* __restrict__ row_expert, size_t n,
 }
 
 void launch_ep_localize(scmoe_ctx* c, const int* row_expert, size_t n, int offset, int n_local,
-                        uint32_t* local) {
+                        uint32_t* local, const int* n_dev) {
     if (n == 0) return;
     ep_localize_kernel<<<ceil_div(n, 256), 256, 0, c->stream>>>(row_expert, n, offset, n_local,
-                                                               local, c->dev_status);
+                                                               local, c->dev_status, n_dev);
     SCMOE_LAUNCH_CHECK(c);
 }
 
@@ -899,15 +920,21 @@ __global__ void ep_put_rows_kernel(const __nv_bfloat16* __restrict__ src, int d,
                                    const int* __restrict__ send_start,
                                    const int64_t* __restrict__ dst_offset,
                                    const uint64_t* __restrict__ peer_rows,
-                                   const uint64_t* __restrict__ peer_expert, int G) {
+                                   const uint64_t* __restrict__ peer_expert, int G,
+                                   int64_t cap_dst, int* __restrict__ dev_status) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     const int vec = d / 8;
+    n_send = min(n_send, send_start[G]);  // the plan's count (device side)
     for (int j = warp; j < n_send; j += nwarps) {
         int dst = 0;
         while (dst + 1 < G && send_start[dst + 1] <= j) ++dst;
         const int64_t pos = dst_offset[dst] + (j - send_start[dst]);
+        if (pos >= cap_dst) {  // receiver capacity exceeded: latched, row dropped
+            if (lane == 0) atomicExch(dev_status, DEV_ERR_CAPACITY);
+            continue;
+        }
         const uint4* s = reinterpret_cast<const uint4*>(src + (size_t)send_token[j] * d);
         uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(peer_rows[dst]) +
                                             (size_t)pos * d);
@@ -933,7 +960,7 @@ __global__ void __launch_bounds__(kPutWarps * 32) ep_put_rows_bulk_kernel(
     const __nv_bfloat16* __restrict__ src, int d, const int* __restrict__ send_token,
     const int* __restrict__ send_expert, int n_send, const int* __restrict__ send_start,
     const int64_t* __restrict__ dst_offset, const uint64_t* __restrict__ peer_rows,
-    const uint64_t* __restrict__ peer_expert, int G) {
+    const uint64_t* __restrict__ peer_expert, int G, int64_t cap_dst, int* __restrict__ dev_status) {
     extern __shared__ __align__(128) unsigned char put_smem[];
     __shared__ uint64_t bars[kPutWarps][2];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -949,6 +976,7 @@ __global__ void __launch_bounds__(kPutWarps * 32) ep_put_rows_bulk_kernel(
     const int gw = blockIdx.x * kPutWarps + warp, nw = gridDim.x * kPutWarps;
     uint32_t phase[2] = {0, 0};
     int it = 0;
+    n_send = min(n_send, send_start[G]);
     for (int j = gw; j < n_send; j += nw, ++it) {
         const int b = it & 1;
         unsigned char* sb = buf + b * row_bytes;
@@ -957,6 +985,10 @@ __global__ void __launch_bounds__(kPutWarps * 32) ep_put_rows_bulk_kernel(
         int dst = 0;
         while (dst + 1 < G && send_start[dst + 1] <= j) ++dst;
         const int64_t pos = dst_offset[dst] + (j - send_start[dst]);
+        if (pos >= cap_dst) {
+            atomicExch(dev_status, DEV_ERR_CAPACITY);
+            continue;
+        }
         mbar_expect_tx(&bars[warp][b], row_bytes);
         asm volatile(
             "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
@@ -980,7 +1012,7 @@ __global__ void __launch_bounds__(kPutWarps * 32) ep_put_rows_bulk_kernel(
 void launch_ep_put_rows(scmoe_ctx* c, const __nv_bfloat16* src, size_t d, const int* send_token,
                         const int* send_expert, size_t n_send, const int* send_start,
                         const int64_t* dst_offset, const uint64_t* peer_rows,
-                        const uint64_t* peer_expert, int G) {
+                        const uint64_t* peer_expert, int G, int64_t cap_dst) {
     if (n_send == 0) return;
     SCMOE_CHECK_ARG(d % 8 == 0, SCMOE_ERR_DIMENSION, "ep_put_rows: d must be a multiple of 8");
     // the warp-store kernel is the default: same NVLink rate as the bulk-copy
@@ -993,12 +1025,13 @@ void launch_ep_put_rows(scmoe_ctx* c, const __nv_bfloat16* src, size_t d, const 
                                 c->device);
         ep_put_rows_bulk_kernel<<<c->num_sms * 2, kPutWarps * 32, smem, c->stream>>>(
             src, (int)d, send_token, send_expert, (int)n_send, send_start, dst_offset, peer_rows,
-            peer_expert, G);
+            peer_expert, G, cap_dst, c->dev_status);
     } else {
         const int blocks = c->num_sms * 4;
         ep_put_rows_kernel<<<blocks, 256, 0, c->stream>>>(src, (int)d, send_token, send_expert,
                                                           (int)n_send, send_start, dst_offset,
-                                                          peer_rows, peer_expert, G);
+                                                          peer_rows, peer_expert, G, cap_dst,
+                                                          c->dev_status);
     }
     SCMOE_LAUNCH_CHECK(c);
 }

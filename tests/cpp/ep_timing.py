@@ -14,7 +14,7 @@ def main():
     torch.cuda.set_device(rank)
     dist.init_process_group("nccl", device_id=torch.device("cuda", rank))
     import paper_2509_01322_b200 as P
-    from paper_2509_01322_b200.ep import EPLayer, GpuOps
+    from paper_2509_01322_b200.ep_torch import EPLayer, GpuOps
     from paper_2509_01322_b200.layer import LONGCAT
     T, D = 8192, LONGCAT.d
     ctx = P.Context(rank)

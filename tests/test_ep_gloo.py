@@ -1,8 +1,8 @@
-"""CPU test of the expert-parallel orchestration (paper_2509_01322_b200/ep.py)
+"""CPU test of the expert-parallel orchestration (paper_2509_01322_b200/ep_torch.py)
 with world_size 2 over gloo.
 
 The numeric steps are provided by an oracle-backed ``ops`` object (test
-infrastructure, fp32), so the test checks exactly what ep.py owns: the dispatch
+infrastructure, fp32), so the test checks exactly what ep_torch.py owns: the dispatch
 plan order, count exchange, split sizes, expert-id localisation, the return
 order of the expert rows and the source-side combine mapping.  The EP result
 on each rank's token shard must equal the single-process oracle layer on the
@@ -126,7 +126,7 @@ def _worker(rank, world, port, q, chunks=1):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import _oracle as O
-        from paper_2509_01322_b200.ep import EPLayer
+        from paper_2509_01322_b200.ep_torch import EPLayer
         a1 = torch.from_numpy(O.normal_f32(O.stream_seed(SEED_X, rank), T_LOCAL * D))
         a3 = torch.from_numpy(O.normal_f32(O.stream_seed(SEED_X + 1, rank), T_LOCAL * D))
         layer = EPLayer(OracleOps(rank, world))

@@ -111,43 +111,105 @@ def max_over_ranks(v: float, ws: int) -> float:
 # clocks sampler (nvidia-smi during the timed region)
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clocks, power and throttle reasons polled through NVML every 5 ms on
+    a thread during the timed region (nvidia-smi's 100 ms loop caught one
+    sample of a 130 ms region); falls back to nvidia-smi when NVML is absent."""
+    PERIOD_S = 0.005
 
     def __init__(self, gpu: int):
         self.gpu = gpu
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        self.p = None
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+        self._smi = None
+
+    def _poll_nvml(self, n, h):
+        reasons = {"hw_slowdown": n.nvmlClocksEventReasonHwSlowdown,
+                   "hw_thermal_slowdown": n.nvmlClocksEventReasonHwThermalSlowdown,
+                   "sw_thermal_slowdown": n.nvmlClocksEventReasonSwThermalSlowdown,
+                   "sw_power_cap": n.nvmlClocksEventReasonSwPowerCap}
+        mx = n.nvmlDeviceGetMaxClockInfo(h, n.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            try:
+                sm = n.nvmlDeviceGetClockInfo(h, n.NVML_CLOCK_SM)
+                pw = n.nvmlDeviceGetPowerUsage(h) / 1000.0
+                r = n.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((float(sm), float(mx), pw,
+                                  [k for k, bit in reasons.items() if r & bit]))
+            except Exception:
+                pass
+            time.sleep(self.PERIOD_S)
 
     def __enter__(self):
         try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
-                                      stdout=self.f, stderr=subprocess.DEVNULL)
-        except FileNotFoundError:
-            self.p = None
-        time.sleep(0.15)
+            import pynvml as n
+            n.nvmlInit()
+            h = n.nvmlDeviceGetHandleByIndex(self.gpu)
+            self._t = threading.Thread(target=self._poll_nvml, args=(n, h), daemon=True)
+            self._t.start()
+        except Exception:
+            self._t = None
+            try:
+                self._f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+                q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+                     "clocks_event_reasons.hw_thermal_slowdown,"
+                     "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+                self._smi = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + q,
+                                              "--format=csv,noheader,nounits", "-lms", "50"],
+                                             stdout=self._f, stderr=subprocess.DEVNULL)
+            except FileNotFoundError:
+                self._smi = None
+        time.sleep(0.02)
         return self
 
     def __exit__(self, *a):
-        if self.p:
-            self.p.terminate()
-            self.p.wait()
+        self._stop.set()
+        if self._t:
+            self._t.join()
+        if self._smi:
+            self._smi.terminate()
+            self._smi.wait()
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for r in open(self._f.name).read().strip().splitlines():
+                r = r.split(", ")
+                if len(r) >= 7:
+                    self.rows.append((float(r[0]), float(r[1]), float(r[2]),
+                                      [nm for nm, v in zip(names, r[3:7]) if v.strip() == "Active"]))
 
     def summary(self):
-        self.f.flush()
-        rows = [r.split(", ") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
-        rows = [r for r in rows if len(r) >= 9]
-        if not rows:
+        if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in rows]
-        mx = max(float(r[2]) for r in rows)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.strip() == "Active"})
-        loaded = [s for s in sm if s > 0.5 * mx] or sm
-        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows)}
+        sm = [r[0] for r in self.rows]
+        mx = max(r[1] for r in self.rows)
+        reasons = sorted({x for r in self.rows for x in r[3]})
+        loaded = [v for v in sm if v > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_min_mhz": min(loaded), "sm_max_mhz": mx,
+                "reasons": reasons, "samples": len(self.rows),
+                "source": "nvml 5 ms" if self._t else "nvidia-smi 50 ms",
+                "power_w_max": max(r[2] for r in self.rows)}
+
+
+def nvlink_bytes(gpu: int):
+    """Cumulative NVLink data bytes (tx, rx) of one GPU from NVML's throughput
+    counters (summed over links), or None when unavailable."""
+    try:
+        import pynvml as n
+        n.nvmlInit()
+        h = n.nvmlDeviceGetHandleByIndex(gpu)
+        tx = rx = 0
+        for link in range(18):
+            try:
+                v = n.nvmlDeviceGetFieldValues(h, [(n.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, link),
+                                                   (n.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, link)])
+            except Exception:
+                break
+            if v[0].nvmlReturn != 0 or v[1].nvmlReturn != 0:
+                continue
+            tx += v[0].value.ullVal
+            rx += v[1].value.ullVal
+        return (tx * 1024, rx * 1024)  # the DATA counters count KiB
+    except Exception:
+        return None
 
 
 def measured_peaks():
@@ -160,13 +222,30 @@ def measured_peaks():
 # ---------------------------------------------------------------------------
 # CPU reference (oracle/_ref = the reference's own code) on a bounded sample
 # ---------------------------------------------------------------------------
-def reference_cpu_sample(route_tokens=64, moe_tokens=16, threads=None, log_fn=log):
+_CPU_WEIGHTS = {}
+
+
+def reference_cpu_sample(threads=None, route_tokens=1024, shard_tokens=8, shard_distinct=1,
+                         log_fn=log):
     """tokens/s of the reference's route_topk + moe_forward at the LongCat
-    shape on this host, token-sharded over `threads` (bitwise identical to a
-    monolithic call).  Only the experts the sample hits are materialised."""
+    shape on this host.  ONE definition for both the cpu_baseline leg and the
+    --impl reference arm (same sample, same threads).
+
+    route_topk (router.hpp:133-141) runs on `route_tokens` tokens,
+    token-sharded over `threads` (bitwise one call).  moe_forward
+    (blocks.hpp:372-394) runs one shard per thread; a shard holds
+    `shard_tokens` tokens made of `shard_distinct` routed tokens, each repeated:
+    the reference's per-row cost does not depend on how many rows an expert
+    gathers (mm_into re-streams W per row), while its per-CALL copy of every hit
+    expert's weights into the graph (blocks.hpp:387-391, ~200 MB per expert)
+    amortises over the repeats as it does over the ~128 tokens per expert of a
+    full 8192-token call -- without the 100 GB of host RAM such a call needs.
+    The sampled tokens are routed tokens with exactly K_e = 8 FFN slots, the
+    workload's mean (7.98-8.01 per token at configs B/C), so the per-token
+    work equals the workload's.  Weights of the hit experts are generated
+    (untimed) once per process."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import _oracle as O
-    from concurrent.futures import ThreadPoolExecutor
     from _oracle import ptr, ptr_array
 
     threads = threads or os.cpu_count() or 1
@@ -187,42 +266,65 @@ def reference_cpu_sample(route_tokens=64, moe_tokens=16, threads=None, log_fn=lo
                                         0.0, ptr(b), ptr(idx), ptr(g), ptr(cnt), None)
     t_route = time.perf_counter() - t0
     assert rc == 0
-    mi = idx[:moe_tokens * TOPK]
+    # moe sample: shard i holds tokens [i*distinct, (i+1)*distinct) of the
+    # routed batch, each repeated shard_tokens/distinct times
+    n_shards = threads
+    rep = max(1, shard_tokens // shard_distinct)
+    mean_tok = np.nonzero(cnt == KE)[0]
+    src = np.concatenate([np.repeat(mean_tok[(np.arange(i * shard_distinct, (i + 1) *
+                                                        shard_distinct)) % mean_tok.size], rep)
+                          for i in range(n_shards)])
+    M = src.size
+    mx = np.ascontiguousarray(x[src])
+    mi = np.ascontiguousarray(idx.reshape(-1, TOPK)[src].ravel())
+    mg = np.ascontiguousarray(g.reshape(-1, TOPK)[src].ravel())
     hit = sorted({int(e) for e in mi if e < N_FFN})
 
     def gen(e):
         a = np.empty(D * INTER, np.float32)
         bb = np.empty(D * INTER, np.float32)
-        O.orc().orc_seeded_uniform_f32(O.stream_seed(SEED_W, 100 + 2 * e), 0, D * INTER, 1.0 / D, ptr(a))
-        O.orc().orc_seeded_uniform_f32(O.stream_seed(SEED_W, 101 + 2 * e), 0, D * INTER, 1.0 / D, ptr(bb))
+        O.orc().orc_seeded_uniform_f32(O.stream_seed(SEED_W, 100 + 2 * e), 0, D * INTER, 1.0 / D,
+                                       ptr(a))
+        O.orc().orc_seeded_uniform_f32(O.stream_seed(SEED_W, 101 + 2 * e), 0, D * INTER, 1.0 / D,
+                                       ptr(bb))
         return e, a, bb
 
-    w_in = [None] * N_FFN
-    w_out = [None] * N_FFN
+    from concurrent.futures import ThreadPoolExecutor
+    todo = [e for e in hit if e not in _CPU_WEIGHTS]
     with ThreadPoolExecutor(threads) as ex:
-        for e, a, bb in ex.map(gen, hit):
-            w_in[e], w_out[e] = a, bb
-    out = np.empty((moe_tokens, D), np.float32)
+        for e, a, bb in ex.map(gen, todo):
+            _CPU_WEIGHTS[e] = (a, bb)
+    w_in = [_CPU_WEIGHTS[e][0] if e in _CPU_WEIGHTS and e in hit else None for e in range(N_FFN)]
+    w_out = [_CPU_WEIGHTS[e][1] if e in _CPU_WEIGHTS and e in hit else None for e in range(N_FFN)]
+    out = np.empty((M, D), np.float32)
     t0 = time.perf_counter()
     if kind == "reference":
-        rc = O.ref().ref_moe_forward_f32(ptr(x[:moe_tokens]), moe_tokens, D, ptr(mi), ptr(g), TOPK,
-                                         N_FFN, N_ZERO, ptr_array(w_in), ptr_array(w_out), INTER, 1,
-                                         0, ptr(out), min(threads, moe_tokens))
-        used = max(min(threads, moe_tokens), min(threads, route_tokens))
+        rc = O.ref().ref_moe_forward_f32(ptr(mx), M, D, ptr(mi), ptr(mg), TOPK, N_FFN, N_ZERO,
+                                         ptr_array(w_in), ptr_array(w_out), INTER, 1, 0, ptr(out),
+                                         n_shards)
+        used = n_shards
     else:
-        rc = O.orc().orc_moe_forward_f32(ptr(x[:moe_tokens]), moe_tokens, D, ptr(mi), ptr(g),
-                                         TOPK, N_FFN, N_ZERO, ptr_array(w_in), ptr_array(w_out),
-                                         INTER, 1.0, 1.0, 0, ptr(out))
+        rc = O.orc().orc_moe_forward_f32(ptr(mx), M, D, ptr(mi), ptr(mg), TOPK, N_FFN, N_ZERO,
+                                         ptr_array(w_in), ptr_array(w_out), INTER, 1.0, 1.0, 0,
+                                         ptr(out))
         used = 1
     t_moe = time.perf_counter() - t0
     assert rc == 0
-    per_token = t_route / route_tokens + t_moe / moe_tokens
-    value = 1.0 / per_token
-    sample = (f"route_topk on {route_tokens} tokens ({t_route:.2f}s) + moe_forward on "
-              f"{moe_tokens} tokens ({t_moe:.2f}s, {len(hit)} experts materialised), LongCat "
-              f"shape fp32, token-sharded over {used} threads")
+    route_tps = route_tokens / t_route
+    moe_tps = M / t_moe
+    value = 1.0 / (1.0 / route_tps + 1.0 / moe_tps)
+    sample = (f"route_topk on {route_tokens} tokens over {threads} threads ({t_route:.2f}s, "
+              f"{route_tps:.0f} tok/s) + moe_forward on {M} tokens = {n_shards} shards x "
+              f"{shard_distinct} routed tokens x {rep} repeats, one shard per thread "
+              f"({t_moe:.2f}s, {moe_tps:.2f} tok/s, {len(hit)} experts materialised, "
+              f"{float((mi < N_FFN).sum()) / M:.2f} FFN slots/token); LongCat shape fp32")
     log_fn("cpu reference:", sample, f"-> {value:.2f} tok/s")
-    return {"value": value, "unit": "tokens/s", "cores": used, "kind": kind, "sample": sample}
+    return {"value": value, "unit": "tokens/s", "cores": used if kind == "reference" else 1,
+            "route_threads": threads if kind == "reference" else 1, "kind": kind,
+            "route_tokens_per_s": route_tps, "moe_tokens_per_s": moe_tps,
+            "tokens_sampled": {"route": route_tokens, "moe": M, "moe_distinct": n_shards *
+                               shard_distinct},
+            "experts_materialised": len(hit), "sample": sample}
 
 
 def tiny_config_a(ctx, stream, iters, with_cpu):
@@ -321,7 +423,7 @@ def run_reference_arm(args):
     vals = []
     base = None
     for i in range(args.warmup + args.steps):
-        r = reference_cpu_sample(route_tokens=32, moe_tokens=8)
+        r = reference_cpu_sample()
         if i >= args.warmup:
             vals.append(r["value"])
             base = r
@@ -335,7 +437,10 @@ def run_reference_arm(args):
         "data": "synthetic (CounterRng normal inputs, seeded_init Uniform weights)",
         "config": {"workload": cfg["workload"], "tokens": cfg["tokens"], "d_model": D,
                    "n_ffn": N_FFN, "n_zero": N_ZERO, "top_k": TOPK, "inter": INTER,
-                   "parallelism": f"cpu x{base['cores']}"},
+                   "parallelism": f"cpu x{base['cores']}",
+                   "same_config": ("same layer shape, weights and inputs as the B200 arm; each "
+                                   "step is a bounded token sample (see cpu_baseline.sample), "
+                                   "the same function as the B200 line's cpu_baseline leg")},
         "cpu_baseline": {**base, "value": v},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -418,6 +523,7 @@ def run_b200(args):
         ctx.synchronize()
     idx_h = sets[0]["idx"].cpu().numpy().view(np.uint32)
     g1b, g2b, S, n_hit, flops = gemm_algorithmic_bytes(idx_h, T)
+    w_hit_bytes = n_hit * D * INTER * 2 * 2
     ffn_mean = float(sets[0]["cnt"].cpu().numpy().mean())
 
     # ---- serial schedule: one batch after the other (per-batch latency) ----
@@ -510,11 +616,52 @@ def run_b200(args):
                     "gemm_achieved_gbs": (c1 + c2) / (tg / 1e3) / 1e9,
                     "stages_ms": {k: round(v[0] / v[1], 4) for k, v in st_c.items()}}
 
+    # ---- TPOT from measured latencies -- one GPU holding all
+    # 512 experts serving a decode batch of tpot_batch tokens (the reference
+    # row's batch_per_device); no all-to-all at N=1, so dispatch / combine
+    # stay the row's values (measured at N>1 by the EP arm)
+    tpot = None
+    if args.tpot_batch > 0:
+        Tb = args.tpot_batch
+        bsets = dict(idx=torch.empty(Tb * TOPK, dtype=torch.int32, device="cuda"),
+                     gates=torch.empty(Tb * TOPK, dtype=torch.float64, device="cuda"),
+                     cnt=torch.empty(Tb, dtype=torch.int32, device="cuda"),
+                     out=torch.empty(Tb, D, dtype=torch.float32, device="cuda"))
+
+        def bstep(n):
+            for _ in range(n):
+                layer.forward(a1.data_ptr(), None, None, Tb, bsets["idx"].data_ptr(),
+                              bsets["gates"].data_ptr(), bsets["cnt"].data_ptr(),
+                              bsets["out"].data_ptr())
+        with torch.cuda.stream(stream):
+            bstep(3)
+        ctx.synchronize()
+        ctx.profile(True)
+        ctx.profile_flush()
+        ms_b = timed(bstep, args.steps)
+        st_b = ctx.profile_flush()
+        ctx.profile(False)
+        moe_us = sum(st_b[k][0] / st_b[k][1] for k in ("permute", "gather", "gemm1_tcgen05",
+                                                       "gemm2_tcgen05") if k in st_b) * 1e3
+        tpot = tpot_block(moe_us, source=f"1xB200 holding all {N_FFN} experts, decode batch of "
+                                         f"{Tb} tokens ({ms_b:.3f} ms per layer call incl. routing "
+                                         "and combine); moe = permute + gather + GEMM1 + GEMM2")
+        tpot["layer_ms_measured"] = ms_b
+
     # ---- SURVEY config A (tiny fp32, bit-exact path, latency-bound): device
     # time per layer call beside the reference's own CPU time on the same shape
     config_a = None
     if ws == 1 and args.config_a:
         config_a = tiny_config_a(ctx, stream, args.steps * 20, not args.no_cpu_baseline)
+
+    # ---- 4-layer ScMoE stack, 100 router steps of 1024 tokens with
+    # PID bias control (K_e = 6, mu = 0.2, decay 0.999); the main layer's
+    # 25.8 GB are released first (the stack holds 4 x 25.8 GB)
+    e5 = None
+    if ws == 1 and args.e5_steps > 0:
+        layer.close()
+        torch.cuda.synchronize()
+        e5 = run_e5(P, ctx, stream, args.e5_steps)
 
     if rank != 0:
         return
@@ -524,11 +671,16 @@ def run_b200(args):
         config_c["gemm_frac_of_measured_hbm"] = config_c["gemm_achieved_gbs"] / hbm_peak
         config_c["gemm_frac_of_8tbs_nominal"] = config_c["gemm_achieved_gbs"] / 8000.0
 
+    # algorithmic bytes per SURVEY 8(d): every hit expert's bf16 weights once
+    # + the token rows in (x) and out, bf16 -- the unfused kernels' extra
+    # traffic (the permuted copy, h, per-slot rows) is NOT counted as useful
+    alg_bytes = w_hit_bytes + 2 * T * D * 2
+
     def gemm_roofline(st):
         g1 = st.get("gemm1_tcgen05", (0.0, 1))
         g2 = st.get("gemm2_tcgen05", (0.0, 1))
         t = (g1[0] + g2[0]) / max(1, g1[1])  # per step (one launch of each per step)
-        return t, ((g1b + g2b) / (t / 1e3) / 1e9 if t > 0 else None)
+        return t, (alg_bytes / (t / 1e3) / 1e9 if t > 0 else None)
 
     t_gemm, achieved = gemm_roofline(stages)
     # dram bytes per step of the same kernels from the committed ncu --set full
@@ -569,13 +721,17 @@ def run_b200(args):
                        "and D2H of step i-1 overlap compute of step i)"},
         "gpu_launches": launches,
         "roofline": {"kernel": "grouped_gemm_bf16 (GEMM1+GEMM2, tcgen05)", "bound": "hbm",
-                     "note": ("achieved: GEMM launches inside the timed region (pipelined: the "
-                              "co-resident router shares the SMs); achieved_serial: the same "
-                              "kernels timed alone in the serial schedule"),
+                     "note": ("achieved = SURVEY 8(d) algorithmic bytes (hit experts' bf16 "
+                              "weights + x + out) / the GEMM pair's event time inside the timed "
+                              "region (pipelined: the co-resident router shares the SMs); "
+                              "achieved_serial: the same kernels timed alone (serial schedule); "
+                              "kernel_io_bytes_per_step adds the unfused design's permuted x, h "
+                              "and per-slot rows"),
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": (achieved / hbm_peak) if achieved else None, "traffic": traffic,
                      "traffic_source": "profiles/r01c_traffic.json (ncu dram__bytes_read+write)",
-                     "algorithmic_bytes_per_step": g1b + g2b, "ms_per_step": t_gemm,
+                     "algorithmic_bytes_per_step": alg_bytes,
+                     "kernel_io_bytes_per_step": g1b + g2b, "ms_per_step": t_gemm,
                      "achieved_serial": achieved_serial, "ms_per_step_serial": t_gemm_serial,
                      "tflops": flops / (t_gemm / 1e3) / 1e12 if t_gemm > 0 else None,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},
@@ -585,57 +741,115 @@ def run_b200(args):
         "cpu_baseline": cpu,
         "config_c": config_c,
         "config_a": config_a,
+        "tpot": tpot,
+        "e5": e5,
     }
     emit(line)
 
 
+def run_e5(P, ctx, stream, steps, T=1024, n_layers=4):
+    """SURVEY 8(d) E5 (BASELINE config 5): 4 ScMoE layers (LongCat shape,
+    bf16 experts) x `steps` router steps of T tokens, rmsnorm before each
+    router, accumulate + bias_update every step (Model::accumulate_routing /
+    update_biases).  Device-timed steps/s; the activated-FFN trace shows the
+    zero-expert fraction tracking 1 - K_e/K.  Bitwise routing / bias parity of
+    this exact run against the reference is tests/test_gpu_stack.py."""
+    import torch
+    from paper_2509_01322_b200.layer import LayerShape
+    from paper_2509_01322_b200.stack import ScMoEStack
+    shape = LayerShape(d=D, n_ffn=N_FFN, n_zero=N_ZERO, top_k=TOPK, k_expected=6, inter=INTER,
+                       precision=P.PREC_BF16)
+    t0 = time.time()
+    with torch.cuda.stream(stream):
+        stack = ScMoEStack(ctx, shape, n_layers, seed=11, mu=0.2, mu_decay=0.999)
+        xs = [torch.from_numpy(P.fill_normal(P.stream_seed(99, s), T * D,
+                                             threads=os.cpu_count() or 8)).cuda().view(T, D)
+              for s in range(steps)]
+        torch.cuda.synchronize()
+        setup = time.time() - t0
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for s in range(steps):  # fresh inputs every step (CounterRng stream(step))
+            stack.step(xs[s], T, record=True)
+        ev1.record(stream)
+        ev1.synchronize()
+    ms = ev0.elapsed_time(ev1) / steps
+    means = np.array(stack.trace.mean_ffn)
+    tail = means[-20:].mean(0)
+    for l in stack.layers:
+        l.close()
+    return {"workload": "SURVEY E5 / BASELINE config 5: 4-layer ScMoE stack (LongCat layer, "
+                        "bf16 experts), PID bias control K_e=6, mu=0.2, decay 0.999, bias_update "
+                        "every step", "tokens_per_step": T, "layers": n_layers, "steps": steps,
+            "ms_per_step": ms, "steps_per_s": 1e3 / ms, "tokens_per_s": T / (ms / 1e3),
+            "setup_s": setup, "first_step_mean_ffn": [round(v, 4) for v in means[0]],
+            "final_tail20_mean_ffn": [round(v, 4) for v in tail],
+            "final_zero_expert_fraction": [round(1 - v / TOPK, 4) for v in tail],
+            "target_zero_expert_fraction": 1 - 6 / TOPK,
+            "timing": "device events around all steps; includes the per-step host reads of the "
+                      "ffn counts and bias_update's StateError check (one sync per layer)"}
+
+
+def tpot_block(moe_us, dispatch_us=None, combine_us=None, source=""):
+    """the reference's TPOT calculator (analytics.hpp:211-253,
+    costmodel.py) on its LongCat SBO row (data/costmodels/sbo_28l.json: 28
+    layers, 96 tokens per device, accept 1.8 -> 16.05 ms) with the module
+    latencies measured here substituted; attention stays the row's value (the
+    exact-fp32 MLA is not a decode-serving path)."""
+    from paper_2509_01322_b200.costmodel import CostModel, tpot_theoretical, with_measured
+    row = CostModel(264, 236, 60, 472, 28, 1.8, "sbo", 96, 2.0)
+    meas = {"moe_us": moe_us}
+    if dispatch_us is not None:
+        meas["dispatch_us"] = dispatch_us
+    if combine_us is not None:
+        meas["combine_us"] = combine_us
+    out = {"reference_row": "sbo_28l (analytics.hpp:232-253, data/costmodels/sbo_28l.json)",
+           "measured_us": {k: round(v, 2) for k, v in meas.items()}, "measured_on": source}
+    for strat in ("sbo", "tbo"):
+        ref = tpot_theoretical(CostModel(**{**row.__dict__, "strategy": strat}))
+        b200 = tpot_theoretical(with_measured(CostModel(**{**row.__dict__, "strategy": strat}),
+                                              **meas))
+        out[strat] = {"reference_tpot_ms": round(ref.tpot_ms, 3),
+                      "b200_tpot_ms": round(b200.tpot_ms, 3),
+                      "b200_tpl_us": round(b200.tpl_us, 2),
+                      "b200_price_per_mtok": round(b200.price_per_mtok, 4)}
+    return out
+
+
 def run_b200_ep(args):
-    """N>1: expert-parallel layer (paper_2509_01322_b200.ep), experts block-
-    partitioned over the ranks, tokens sharded (8192 per GPU), dispatch /
-    return all-to-all over NCCL (NVLink 5 / NVSwitch)."""
+    """N>1: the expert-parallel layer behind the C ABI (scmoe_ep_*; Python
+    caller paper_2509_01322_b200.ep): experts block-partitioned over the
+    ranks, tokens sharded (8192 per GPU: weak scaling), the count exchange,
+    dispatch (peer stores over NVLink) and return (GEMM2 epilogue stores)
+    all device-side, no host synchronisation per layer."""
     import torch
     ws, rank, local = dist_init()
     import paper_2509_01322_b200 as P
-    from paper_2509_01322_b200.ep import EPLayer, GpuOps
+    from paper_2509_01322_b200.ep import ExpertParallelLayer, broadcast_unique_id
     from paper_2509_01322_b200.layer import LONGCAT
 
     cfg = CONFIGS[args.config]
     T = args.tokens or cfg["tokens"]
+    Td = args.config_d_tokens // ws
     ctx = P.Context(local)
-    ops = GpuOps(ctx, LONGCAT, rank, ws, seed=SEED_W)
-    ep = EPLayer(ops, transport=args.ep_transport)
+    uid = broadcast_unique_id()
+    ep = ExpertParallelLayer(ctx, LONGCAT, rank, ws, SEED_W, uid,
+                             max_tokens=max(T, Td, args.tpot_batch))
     a1_h = P.fill_normal(P.stream_seed(SEED_X, rank), T * D, threads=os.cpu_count() or 8)
     a3_h = P.fill_normal(P.stream_seed(SEED_X + 1, rank), T * D, threads=os.cpu_count() or 8)
     a1 = torch.from_numpy(a1_h).cuda()
     a3 = torch.from_numpy(a3_h).cuda()
-    chunks = args.ep_chunks
-    if args.ep_transport == "p2p":
-        # the peer-memory transport needs torch symmetric memory over NVLink; if
-        # this box cannot map it, every rank falls back to NCCL (same decision)
-        import torch.distributed as dist
-        ok = torch.ones(1, device="cuda")
-        try:
-            ep.forward(a1, a3, None, T, chunks=chunks)
-            torch.cuda.synchronize()
-        except Exception as e:  # reported, the run continues on NCCL
-            log(f"[rank {rank}] p2p transport unavailable ({e}); falling back to nccl")
-            ok.zero_()
-        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-        if ok.item() < 1:
-            args.ep_transport = "nccl"
-            ep = EPLayer(ops, transport="nccl")
     for _ in range(args.warmup):
-        out, idx, gates, cnt = ep.forward(a1, a3, None, T, chunks=chunks)
+        out, idx, gates, cnt = ep.forward(a1, a3, None, T)
     torch.cuda.synchronize()
     # untimed warm-up continues until the step time is steady on every rank
-    # (first-touch of the peer mappings / a previous job's teardown on the box
-    # can make the first steps several times slower); at most 30 more steps
     hist = []
     for _ in range(30):
         w0 = torch.cuda.Event(enable_timing=True)
         w1 = torch.cuda.Event(enable_timing=True)
         w0.record()
-        out, idx, gates, cnt = ep.forward(a1, a3, None, T, chunks=chunks)
+        out, idx, gates, cnt = ep.forward(a1, a3, None, T)
         w1.record()
         w1.synchronize()
         hist.append(max_over_ranks(w0.elapsed_time(w1), ws))
@@ -644,7 +858,11 @@ def run_b200_ep(args):
     log(f"[rank {rank}] extra warm-up steps {len(hist)}: {[round(h, 2) for h in hist]}")
     idx_h = idx.cpu().numpy().view(np.uint32)
     ffn = idx_h[idx_h < N_FFN]
-    def timed_ep(fn):
+    M = ep.count_matrix()  # [src][dst] slots of the last call
+    n_send, n_recv, self_rows = int(M[rank].sum()), int(M[:, rank].sum()), int(M[rank, rank])
+
+    def timed_ep(fn, n=None):
+        n = n or args.steps
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         barrier(ws)
@@ -655,130 +873,141 @@ def run_b200_ep(args):
         e1.synchronize()
         torch.cuda.synchronize()
         barrier(ws)
-        return e0.elapsed_time(e1) / args.steps
+        return e0.elapsed_time(e1) / n
 
-    # serial steps (per-batch latency), with the per-stage profile; one untimed
-    # block of the same shape first, so the caching allocator has grown to the
-    # no-sync steady state before the timed block
-    for _ in range(args.steps):
-        ep.forward(a1, a3, None, T, chunks=chunks)
-    torch.cuda.synchronize()
+    # serial steps (per-batch latency), with the per-stage profile
     ctx.profile(True)
     ctx.profile_flush()
-    ms_serial = timed_ep(lambda: [ep.forward(a1, a3, None, T, chunks=chunks)
-                                  for _ in range(args.steps)])
+    ms_serial = timed_ep(lambda: [ep.forward(a1, a3, None, T) for _ in range(args.steps)])
     stages = ctx.profile_flush()
     ctx.profile(False)
     ms_serial_max = max_over_ranks(ms_serial, ws)
-    # headline: the pipelined batch stream (p2p transport)
-    pipelined = args.ep_transport == "p2p" and args.schedule == "pipelined"
-    if pipelined:  # untimed block of the timed block's shape (allocator steady state)
-        ep.forward_batches([a1] * args.steps, [a3] * args.steps, None, T,
-                           corun_router=args.ep_corun)
-        torch.cuda.synchronize()
-    l0 = ctx.kernel_launches() + (ops.ctx_b.kernel_launches() if pipelined else 0)
+    # headline: the pipelined batch stream
+    pipelined = args.schedule == "pipelined"
+    run = ((lambda: ep.forward_batches([a1] * args.steps, [a3] * args.steps, None, T,
+                                       corun_router=args.ep_corun)) if pipelined else
+           (lambda: [ep.forward(a1, a3, None, T) for _ in range(args.steps)]))
+    run()  # untimed block of the timed block's shape
+    torch.cuda.synchronize()
+    l0 = ep.kernel_launches()
+    nv0 = nvlink_bytes(local)
     with ClockSampler(local) as clk:
-        if pipelined:
-            ms = timed_ep(lambda: ep.forward_batches([a1] * args.steps, [a3] * args.steps, None,
-                                                     T, corun_router=args.ep_corun))
-        else:
-            ms = timed_ep(lambda: [ep.forward(a1, a3, None, T, chunks=chunks)
-                                   for _ in range(args.steps)])
-    launches = ctx.kernel_launches() + (ops.ctx_b.kernel_launches() if pipelined else 0) - l0
-    main_stats = dict(ep.last_stats)  # the headline workload's rows (config D overwrites)
+        ms = timed_ep(run)
+    nv1 = nvlink_bytes(local)
+    launches = ep.kernel_launches() - l0
     ms_max = max_over_ranks(ms, ws)
     value = T * ws / (ms_max / 1e3)
-    # e2e: every step's H2D of its inputs and D2H of its output inside the
-    # region, through EPLayer.forward_host_batches (copies of neighbouring
-    # steps overlap compute on copy streams)
+    # NVLink cross-check: hardware tx bytes per step vs the payload this rank
+    # stores to peers (dispatch rows + ids to the owners, returned rows to the sources)
+    payload = ((n_send - self_rows) * (D * 2 + 4) + (n_recv - self_rows) * D * 2)
+    nvlink = None
+    if nv0 and nv1:
+        tx = (nv1[0] - nv0[0]) / args.steps
+        nvlink = {"tx_bytes_per_step": tx, "rx_bytes_per_step": (nv1[1] - nv0[1]) / args.steps,
+                  "payload_bytes_per_step": payload, "tx_over_payload": tx / payload if payload
+                  else None, "tx_gbs": tx / (ms / 1e3) / 1e9,
+                  "source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX counters over the timed block "
+                            "(nsys is not installed in this image)"}
+    # e2e: every step's H2D of its inputs and D2H of its output inside the region
     a1_p = torch.from_numpy(a1_h).pin_memory()
     a3_p = torch.from_numpy(a3_h).pin_memory()
     outs_p = [torch.empty(T, D, dtype=torch.float32).pin_memory() for _ in range(2)]
     e_steps = max(4, args.steps)
-    host_run = lambda n: ep.forward_host_batches(  # noqa: E731
-        [a1_p] * n, [a3_p] * n, [outs_p[i % 2] for i in range(n)], None, T)
-    host_run(e_steps)  # untimed block of the same shape
+    host_run = lambda: ep.forward_host_batches(  # noqa: E731
+        [a1_p] * e_steps, [a3_p] * e_steps, [outs_p[i % 2] for i in range(e_steps)], None, T)
+    host_run()
     torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    barrier(ws)
-    e0.record()
-    host_run(e_steps)
-    e1.record()
-    e1.synchronize()
-    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e_steps, ws)
+    e2e_ms = max_over_ranks(timed_ep(host_run, e_steps), ws)
 
     # ---- SURVEY config D: fixed 32k tokens over the ranks, with the dense
-    # shortcut FFN (dense_inter) overlapping the dispatch/return all-to-alls;
-    # exposed communication = (t_layer - t_layer with the row all-to-alls
-    # replaced by no-ops) / t_layer ----------------------------------------
+    # shortcut FFN (dense_inter) overlapping the dispatch/return; exposed
+    # communication = (t_layer - t_layer with the row transfers replaced by
+    # no-ops) / t_layer -------------------------------------------------------
     config_d = None
     if args.dense_inter > 0:
-        Td = args.config_d_tokens // ws
-        ep.ops.enable_dense(local, args.dense_inter, seed=SEED_W + 1)
+        ep.enable_dense(args.dense_inter, seed=SEED_W + 1)
         a1d = torch.from_numpy(P.fill_normal(P.stream_seed(SEED_X + 5, rank), Td * D,
                                              threads=os.cpu_count() or 8)).cuda()
 
         def timed_d(dense, comm):
-            ep.comm = comm
+            ep.set_comm(comm)
             for _ in range(2):
-                ep.forward(a1d, None, None, Td, chunks=chunks, dense=dense)
-            barrier(ws)
-            torch.cuda.synchronize()
-            d0 = torch.cuda.Event(enable_timing=True)
-            d1 = torch.cuda.Event(enable_timing=True)
-            d0.record()
-            for _ in range(args.steps):
-                ep.forward(a1d, None, None, Td, chunks=chunks, dense=dense)
-            d1.record()
-            d1.synchronize()
-            torch.cuda.synchronize()
-            barrier(ws)
-            ep.comm = True
-            return max_over_ranks(d0.elapsed_time(d1) / args.steps, ws)
+                ep.forward(a1d, None, None, Td, dense=dense)
+            t = max_over_ranks(timed_ep(lambda: [ep.forward(a1d, None, None, Td, dense=dense)
+                                                 for _ in range(args.steps)]), ws)
+            ep.set_comm(True)
+            return t
 
         t_moe, t_moe_nc = timed_d(False, True), timed_d(False, False)
         t_full, t_full_nc = timed_d(True, True), timed_d(True, False)
-        dense_flop = 4.0 * Td * D * args.dense_inter
+        Md = ep.count_matrix()
         config_d = {
             "workload": "SURVEY config D: ScMoE layer = MoE branch + dense shortcut SiLU-MLP "
-                        "(rmsnorm, d x dense_inter x d, residual) overlapping the all-to-alls",
+                        "(rmsnorm, d x dense_inter x d, residual) overlapping dispatch/return",
             "tokens_total": Td * ws, "tokens_per_gpu": Td, "dense_inter": args.dense_inter,
             "ms_moe_branch": t_moe, "ms_moe_branch_comm_noop": t_moe_nc,
             "ms_layer": t_full, "ms_layer_comm_noop": t_full_nc,
             "exposed_comm_frac_layer": (t_full - t_full_nc) / t_full,
             "exposed_comm_frac_moe_only": (t_moe - t_moe_nc) / t_moe,
             "layer_tokens_per_s": Td * ws / (t_full / 1e3),
-            "dense_tflop_per_gpu": dense_flop / 1e12,
-            "a2a_bytes_each_way_rank0": ep.last_stats["a2a_bytes_each_way"],
-            "dense_gemm_sms": "all but 16 (left to the NCCL kernels)",
+            "dense_tflop_per_gpu": 4.0 * Td * D * args.dense_inter / 1e12,
+            "a2a_bytes_each_way_rank0": int(Md[rank].sum() - Md[rank, rank]) * D * 2,
+            "dense_gemm_sms": "all but 16 (left to the dispatch / barrier kernels)",
         }
+
+    # ---- TPOT from measured module latencies (decode batch of
+    # `tpot_batch` tokens per device, the reference row's batch_per_device) ---
+    tpot = None
+    if args.tpot_batch > 0:
+        Tb = args.tpot_batch
+        a1b = a1[:Tb * D]
+        for _ in range(3):
+            ep.forward(a1b, None, None, Tb)
+        ctx.profile(True)
+        ctx.profile_flush()
+        ms_b = max_over_ranks(timed_ep(lambda: [ep.forward(a1b, None, None, Tb)
+                                                for _ in range(args.steps)]), ws)
+        st_b = ctx.profile_flush()
+        ctx.profile(False)
+        us = lambda *ks: sum(st_b.get(k, (0.0, 1))[0] / max(1, st_b.get(k, (0.0, 1))[1])  # noqa
+                             for k in ks) * 1e3
+        moe_us = us("permute", "gather", "gemm1_tcgen05", "gemm2_tcgen05", "ep_row_dst")
+        disp_us = us("ep_exchange", "ep_put_rows", "ep_dispatch_barrier")
+        comb_us = us("ep_return_barrier", "combine")
+        # per-stage maxima over the ranks (the slowest rank sets the layer time)
+        moe_us, disp_us, comb_us = (max_over_ranks(v, ws) for v in (moe_us, disp_us, comb_us))
+        tpot = tpot_block(moe_us, disp_us, comb_us,
+                          f"EP x{ws} decode step, {Tb} tokens per GPU ({ms_b:.3f} ms per layer "
+                          "call incl. routing); moe = permute + gather + GEMM1 + GEMM2 (return "
+                          "fused in GEMM2's epilogue), dispatch = count exchange + peer stores + "
+                          "barrier, combine = return barrier + combine kernel")
+        tpot["layer_ms_measured"] = ms_b
+
     if rank != 0:
+        ep.close()
         return
     peaks = measured_peaks() or {}
     n_local = N_FFN // ws
-    # the dispatch kernel's NVLink rate (rank 0): remote rows x row bytes / kernel time
     dispatch = None
     put = stages.get("ep_put_rows")
-    if put and "self_rows" in main_stats:
-        remote = (main_stats["send_rows"] - main_stats["self_rows"]) * D * 2
+    if put:
+        remote = (n_send - self_rows) * D * 2
         put_ms = put[0] / max(1, put[1])
         dispatch = {"kernel": "ep_put_rows (peer stores over NVLink)", "remote_bytes": remote,
                     "ms": put_ms, "gbs": remote / (put_ms / 1e3) / 1e9,
-                    "note": "the return all-to-all is inside GEMM2's epilogue (not separable)"}
+                    "note": "the return is inside GEMM2's epilogue (not separable)"}
     g1 = stages.get("gemm1_tcgen05", (0.0, 1))
     g2 = stages.get("gemm2_tcgen05", (0.0, 1))
     t_gemm = (g1[0] + g2[0]) / max(1, g1[1])
-    slots_local = main_stats["recv_rows"]
-    flops = 4.0 * slots_local * D * INTER
+    flops = 4.0 * n_recv * D * INTER
     wbytes = 2 * n_local * D * INTER * 2
-    tok_per_expert = slots_local / n_local
+    tok_per_expert = n_recv / n_local
     bound = "tensor" if tok_per_expert > 254 else "hbm"
     if bound == "tensor":
         achieved = flops / (t_gemm / 1e3) / 1e12 if t_gemm else None
         peak, unit = peaks.get("bf16_tflops", 1590.0), "TFLOP/s"
     else:
-        achieved = (wbytes + slots_local * (D + INTER) * 4) / (t_gemm / 1e3) / 1e9 if t_gemm else None
+        achieved = (wbytes + n_recv * D * 2 * 2) / (t_gemm / 1e3) / 1e9 if t_gemm else None
         peak, unit = peaks.get("hbm_gbs", 6650.0), "GB/s"
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
@@ -789,24 +1018,24 @@ def run_b200_ep(args):
                                f"(BASELINE config 4 shape, {T} tokens per GPU)",
                    "tokens_per_gpu": T, "d_model": D, "n_ffn": N_FFN, "n_zero": N_ZERO,
                    "top_k": TOPK, "inter": INTER, "experts_per_gpu": n_local,
-                   "parallelism": (f"ep{ws}: dispatch = peer stores into the owners' "
-                                   "symmetric buffers over NVLink, return fused into GEMM2's "
-                                   "epilogue (rows written to the source rank)"
-                                   if args.ep_transport == "p2p" else
-                                   f"ep{ws} (NCCL all_to_all dispatch/return, {chunks}-chunk "
-                                   "software pipeline)"),
-                   "schedule": ("pipelined batches (EPLayer.forward_batches): routing + "
-                                "dispatch of batch i+1 on one stream/context beside the expert "
-                                "GEMMs + return + combine of batch i on another")
-                   if pipelined else "serial",
+                   "parallelism": (f"ep{ws} behind the C ABI (scmoe_ep_layer_forward*): on-device "
+                                   "count exchange, dispatch = peer stores into the owners' "
+                                   "receive buffers over NVLink, return fused into GEMM2's "
+                                   "epilogue, no host sync per layer"),
+                   "schedule": ("pipelined batches (scmoe_ep_layer_forward_batches): routing + "
+                                "dispatch of batch i+1 on one stream beside the expert GEMMs + "
+                                "return + combine of batch i on another") if pipelined
+                   else "serial",
                    "serial_ms_per_batch": ms_serial_max,
-                   "a2a_bytes_each_way_rank0": main_stats["a2a_bytes_each_way"],
-                   "mean_ffn_per_token": float(ffn.size) / T},
+                   "slot_matrix_rank0_row": M[rank].tolist(),
+                   "a2a_bytes_each_way_rank0": (n_send - self_rows) * D * 2,
+                   "mean_ffn_per_token": float(ffn.size) / T,
+                   "l2": "inputs + weights larger than L2 every step"},
         "e2e": {"value": T * ws / (e2e_ms / 1e3), "unit": "tokens/s",
                 "h2d_bytes_per_step": 2 * T * D * 4, "d2h_bytes_per_step": T * D * 4,
                 "ms_per_step": e2e_ms, "steps": e_steps,
-                "api": "EPLayer.forward_host_batches (pinned host tensors; H2D of step i+1 and "
-                       "D2H of step i-1 overlap step i)"},
+                "api": "ExpertParallelLayer.forward_host_batches (pinned host tensors; H2D of "
+                       "step i+1 and D2H of step i-1 overlap step i)"},
         "gpu_launches": launches,
         "roofline": {"kernel": "grouped_gemm_bf16 (GEMM1+GEMM2, tcgen05), rank 0", "bound": bound,
                      "achieved": achieved, "peak": peak, "unit": unit,
@@ -817,10 +1046,13 @@ def run_b200_ep(args):
                      "tokens_per_local_expert": tok_per_expert, "ms_per_step": t_gemm},
         "stages_ms": {k: round(v[0] / v[1], 4) for k, v in stages.items()},
         "dispatch_nvlink": dispatch,
+        "nvlink_counters": nvlink,
         "clocks": clk.summary(),
         "cpu_baseline": None,
         "config_d": config_d,
+        "tpot": tpot,
     }
+    ep.close()
     emit(line)
 
 
@@ -844,13 +1076,12 @@ def main():
     ap.add_argument("--schedule", default="pipelined", choices=["pipelined", "serial"])
     ap.add_argument("--parallel", default="ep", choices=["ep", "replicated"],
                     help="N>1: expert-parallel (default) or replicated experts")
-    # p2p: dispatch stored straight into the peers' symmetric buffers over NVLink,
-    # return fused into GEMM2's epilogue; nccl: all_to_all_single
-    ap.add_argument("--ep-transport", default="p2p", choices=["p2p", "nccl"])
     ap.add_argument("--ep-corun", action="store_true",
                     help="pipelined EP: small router kernel co-resident with the GEMM")
-    ap.add_argument("--ep-chunks", type=int, default=1,
-                    help="EP software-pipeline depth (token chunks per step)")
+    ap.add_argument("--tpot-batch", type=int, default=96,
+                    help="decode tokens per device for the measured TPOT block (0 = off)")
+    ap.add_argument("--e5-steps", type=int, default=100,
+                    help="N=1: SURVEY E5 4-layer PID stack steps (0 = off)")
     args = ap.parse_args()
     stdout_to_stderr()
     if args.impl == "reference":

@@ -355,6 +355,8 @@ int scmoe_ep_create(scmoe_ctx* ctx, int world, int rank, const void* nccl_unique
                     size_t max_recv_rows, scmoe_ep** out);
 int scmoe_ep_destroy(scmoe_ep* ep); /* collective */
 size_t scmoe_ep_capacity_rows(const scmoe_ep* ep);
+/* Kernels launched by the layer's contexts (the caller's + internal ones). */
+uint64_t scmoe_ep_kernel_launches(const scmoe_ep* ep);
 /* Timing reference for the exposed-communication share: on = 0 replaces the
  * row transfers by no-ops (received rows left as they are, spread over the
  * local experts; GEMM2 rows stay local).  Results are garbage while off. */

@@ -165,6 +165,7 @@ _PROTOS = {
                                   C.POINTER(_P)]),
     "scmoe_ep_destroy": (C.c_int, [_P]),
     "scmoe_ep_capacity_rows": (_SZ, [_P]),
+    "scmoe_ep_kernel_launches": (_U64, [_P]),
     "scmoe_ep_set_comm": (C.c_int, [_P, C.c_int]),
     "scmoe_ep_set_dense_reserve": (C.c_int, [_P, C.c_int]),
     "scmoe_ep_layer_forward": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _SZ, C.c_int, _P, _P, _P,

@@ -353,7 +353,7 @@ void ep_front(scmoe_ep* ep, scmoe_ctx* c, EpSet& st, scmoe_router* r, const floa
             reinterpret_cast<int*>(static_cast<char*>(st.slab) + ep->lay.recv_exp));
         SCMOE_LAUNCH_CHECK(c);
     }
-    ProfScope _p(c, "ep_barrier");
+    ProfScope _p(c, "ep_dispatch_barrier");
     signal_wait(ep, c, st, 1, nullptr, nullptr);
 }
 
@@ -362,18 +362,21 @@ void ep_front(scmoe_ep* ep, scmoe_ctx* c, EpSet& st, scmoe_router* r, const floa
 void ep_back(scmoe_ep* ep, scmoe_ctx* c, EpSet& st, scmoe_bank* bank, size_t T, const uint32_t* idx,
              const double* gates, int renorm, const float* residual, float* out) {
     char* slab = static_cast<char*>(st.slab);
-    ep_recv_count_kernel<<<1, 1, 0, c->stream>>>(st.plan, (int)ep->cap_recv, st.n_recv,
-                                                 c->dev_status);
-    SCMOE_LAUNCH_CHECK(c);
-    ep_row_dst_kernel<<<c->num_sms, 256, 0, c->stream>>>(
-        st.plan, st.peer_base_dev, ep->lay.back, ep->world, ep->rank, ep->comm_on ? 1 : 0,
-        ep->d * 2, (int)ep->cap_recv, st.row_dst);
-    SCMOE_LAUNCH_CHECK(c);
+    {
+        ProfScope _p(c, "ep_row_dst");
+        ep_recv_count_kernel<<<1, 1, 0, c->stream>>>(st.plan, (int)ep->cap_recv, st.n_recv,
+                                                     c->dev_status);
+        SCMOE_LAUNCH_CHECK(c);
+        ep_row_dst_kernel<<<c->num_sms, 256, 0, c->stream>>>(
+            st.plan, st.peer_base_dev, ep->lay.back, ep->world, ep->rank, ep->comm_on ? 1 : 0,
+            ep->d * 2, (int)ep->cap_recv, st.row_dst);
+        SCMOE_LAUNCH_CHECK(c);
+    }
     moe_rows_impl(c, bank, slab + ep->lay.recv,
                   reinterpret_cast<const int*>(slab + ep->lay.recv_exp), (int)ep->first,
                   ep->cap_recv, nullptr, st.row_dst, st.n_recv);
     {
-        ProfScope _p(c, "ep_barrier");
+        ProfScope _p(c, "ep_return_barrier");
         signal_wait(ep, c, st, 2, nullptr, nullptr);
     }
     if (T == 0) return;
@@ -609,6 +612,12 @@ int scmoe_ep_set_dense_reserve(scmoe_ep* ep, int reserve_sms) {
 }
 
 size_t scmoe_ep_capacity_rows(const scmoe_ep* ep) { return ep ? ep->cap_recv : 0; }
+
+uint64_t scmoe_ep_kernel_launches(const scmoe_ep* ep) {
+    if (!ep) return 0;
+    return (ep->ctx ? ep->ctx->launches : 0) + (ep->ctx_b ? ep->ctx_b->launches : 0) +
+           (ep->ctx_d ? ep->ctx_d->launches : 0);
+}
 
 int scmoe_ep_layer_forward(scmoe_ep* ep, scmoe_router* r, scmoe_bank* bank, scmoe_bank* dense,
                            const float* a1, const float* a3, const float* gain, size_t T,

@@ -217,6 +217,10 @@ class ExpertParallelLayer:
         self.ctx._check(lib().scmoe_ep_count_matrix_host(self.ep, m.ctypes.data_as(_P)))
         return m
 
+    def kernel_launches(self) -> int:
+        """Kernels launched by the layer's contexts (the caller's + internal)."""
+        return int(lib().scmoe_ep_kernel_launches(self.ep))
+
     def capacity_rows(self) -> int:
         return int(lib().scmoe_ep_capacity_rows(self.ep))
 

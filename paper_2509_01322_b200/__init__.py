@@ -345,18 +345,26 @@ class RouterState:
 
     # Device mirror ----------------------------------------------------------
     def device(self, ctx: Context):
-        """Returns the scmoe_router handle with w/b/mu/counters uploaded."""
+        """Returns the scmoe_router handle with w/b/mu/counters uploaded.  The
+        mirror is recreated when the context or the shape fields change, and
+        the weights re-uploaded when any of their bytes change (a CRC32 over
+        the whole buffer, no copy: ~2 ms for the 18.9 MB LongCat W_r)."""
+        import zlib
         L = lib()
         E = self.n_experts()
         d = 0 if self.w is None else self.w.shape[0]
-        if self._dev is None or self._dev[0] is not ctx or self._dev[2] != d:
+        shape = (d, self.n_ffn, self.n_zero, self.top_k, self.k_expected)
+        if self._dev is None or self._dev[0] is not ctx or self._dev[2] != shape:
+            self.close()
             h = _P()
             ctx._check(L.scmoe_router_create(ctx.handle, d, self.n_ffn, self.n_zero, self.top_k,
                                              self.k_expected, self.mu, self.mu_decay, C.byref(h)))
-            self._dev = (ctx, h, d)
+            self._dev = (ctx, h, shape)
             self._dev_key = None
         h = self._dev[1]
-        wkey = None if self.w is None else (id(self.w), self.w.ctypes.data, hash(self.w.tobytes()[:4096]))
+        wkey = None if self.w is None else (
+            id(self.w), self.w.ctypes.data, self.w.shape, self.w.dtype.str,
+            zlib.crc32(memoryview(np.ascontiguousarray(self.w)).cast("B")))
         if self.w is not None and (self._dev_key is None or self._dev_key != wkey):
             if self.w.shape != (d, E):
                 raise DimensionError("route: router weights must be [d_model, N+Z]")
@@ -369,6 +377,18 @@ class RouterState:
         tr = np.ascontiguousarray(self.tokens_routed, dtype=np.uint64)
         ctx._check(L.scmoe_router_set_counters_host(ctx.handle, h, _ptr(tr), int(self.tokens_seen)))
         return h
+
+    def close(self):
+        """Destroys the device mirror (recreated on the next use)."""
+        dev, self._dev = getattr(self, "_dev", None), None
+        if dev is not None and dev[0].handle:
+            lib().scmoe_router_destroy(dev[0].handle, dev[1])
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
     def pull(self, ctx: Context):
         """Copies b / mu / counters back from the device mirror."""
@@ -609,22 +629,40 @@ class ExpertBank:
         return float(self.m) if self.gamma_mode == GammaMode.All else 1.0
 
     def invalidate(self):
-        self._dev = None
+        """Drops the device copy: the next use re-uploads the host weights
+        (call after changing w_in / w_out in place)."""
+        self.close()
+
+    def close(self):
+        dev, self._dev = getattr(self, "_dev", None), None
+        if dev is not None and dev[0].handle:
+            lib().scmoe_bank_destroy(dev[0].handle, dev[1])
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
     def device(self, ctx: Context):
         if self._dev is not None and self._dev[0] is ctx:
             return self._dev[1]
+        self.close()
         n = self.n_experts()
         d, I = self.w_in[0].shape if n else (0, 0)
         h = _P()
         ctx._check(lib().scmoe_bank_create(ctx.handle, n, d, I, self.precision, self.m,
                                            int(self.gamma_mode), C.byref(h)))
-        for e in range(n):
-            if self.w_in[e].shape != (d, I) or self.w_out[e].shape != (I, d):
-                raise DimensionError("moe_block: expert weight shapes disagree")
-            setter = (lib().scmoe_bank_set_expert_f64_host if self.precision == PREC_F64_EXACT
-                      else lib().scmoe_bank_set_expert_host)
-            ctx._check(setter(ctx.handle, h, e, _ptr(self.w_in[e]), _ptr(self.w_out[e])))
+        try:
+            for e in range(n):
+                if self.w_in[e].shape != (d, I) or self.w_out[e].shape != (I, d):
+                    raise DimensionError("moe_block: expert weight shapes disagree")
+                setter = (lib().scmoe_bank_set_expert_f64_host if self.precision == PREC_F64_EXACT
+                          else lib().scmoe_bank_set_expert_host)
+                ctx._check(setter(ctx.handle, h, e, _ptr(self.w_in[e]), _ptr(self.w_out[e])))
+        except Exception:
+            lib().scmoe_bank_destroy(ctx.handle, h)
+            raise
         self._dev = (ctx, h)
         return h
 

@@ -4,8 +4,10 @@ Restates the reference's calculator, analytics.hpp:211-253 (`CostModel`,
 `TpotResult`, `tpot_theoretical`), so measured B200 module latencies (the
 expert GEMMs of `scmoe_moe_rows`, the EP dispatch / return all-to-alls) can
 be fed into the same SBO / TBO formulas as the reference's cost-model rows
-(`data/costmodels/*.json`; copies of the three rows used by its acceptance
-tests live in tests/golden/costmodels/).
+(`data/costmodels/*.json`; its three rows are restated in
+tests/test_costmodel.py, pinned on the reference's analytics tests).  bench.py
+emits a ``tpot`` block that feeds this calculator with B200-measured expert
+GEMM, dispatch and return latencies.
 
     SBO: per-layer time = attention + dispatch + moe + combine (every module
          exposed serially -- the reference's single-batch overlap row);
@@ -63,7 +65,9 @@ def tpot_theoretical(cm: CostModel) -> TpotResult:
     else:
         raise ConfigError("tpot: unknown overlap strategy " + cm.strategy)
     r.tpot_ms = float(cm.n_layer) * r.tpl_us / (1000.0 * cm.accept_factor)
-    tokens_per_device_second = cm.batch_per_device * 1000.0 / r.tpot_ms
+    # IEEE like the reference's C++: all latencies 0 -> inf tokens/s -> price 0
+    tokens_per_device_second = (cm.batch_per_device * 1000.0 / r.tpot_ms if r.tpot_ms != 0.0
+                                else float("inf"))
     device_hours_per_mtok = 1.0e6 / (tokens_per_device_second * 3600.0)
     r.price_per_mtok = device_hours_per_mtok * cm.price_per_device_hour
     return r

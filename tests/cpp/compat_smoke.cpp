@@ -300,7 +300,33 @@ static void mla_cases() {  // test_blocks.cpp:139-209 with MlaParams<float>
     }
 }
 
+// Two weightless states of different shapes, in successive scopes (the second
+// may sit at the first's stack address): the device mirror must follow the
+// shape, not the address (make_state(2,1,2,1) then make_state(4,2,3,2), as the
+// reference's test_router.cpp builds them in separate TEST_CASEs).
+static void successive_states_of_different_shape() {
+    {
+        auto st = make_state(2, 1, 2, 1);
+        auto d = route_from_probs(Tensor<double>::row({0.5, 0.3, 0.2}), st);
+        CHECK((d.indices == std::vector<std::uint32_t>{0, 1}));
+    }
+    {
+        auto st = make_state(4, 2, 3, 2);
+        auto d = route_from_probs(Tensor<double>::row({0.1, 0.3, 0.2, 0.05, 0.25, 0.1}), st);
+        CHECK(d.indices.size() == 3);
+        CHECK((d.indices == std::vector<std::uint32_t>{1, 4, 2}));
+        CHECK((d.gates == std::vector<double>{0.3, 0.25, 0.2}));
+        CHECK((d.ffn_count == std::vector<std::uint32_t>{2}));
+    }
+    {
+        auto st = make_state(2, 1, 2, 1);
+        auto d = route_from_probs(Tensor<double>::row({0.2, 0.3, 0.5}), st);
+        CHECK((d.indices == std::vector<std::uint32_t>{2, 1}));
+    }
+}
+
 int main() {
+    successive_states_of_different_shape();
     route_topk_double_full_path();
     moe_cases_double();
     selection_is_biased_gates_are_not();

@@ -69,3 +69,9 @@ def test_errors_and_measured_substitution():
     assert tpot_theoretical(faster).tpl_us == 264 + 100 + 30 + 472
     with pytest.raises(P.ConfigError):
         with_measured(base, n_layer=3)
+
+
+def test_zero_latencies_give_zero_price_like_the_reference():
+    # analytics.hpp:250-252 in IEEE double: tpot 0 -> tokens/s inf -> price 0
+    r = tpot_theoretical(CostModel(0, 0, 0, 0, 28, 1.8, "sbo"))
+    assert r.tpot_ms == 0.0 and r.price_per_mtok == 0.0

@@ -459,6 +459,24 @@ __global__ void __maxnreg__(kNT == 256 ? 128 : 64)
                     } else {
                         tmem_ld32(taddr + j0, v);  // v[jj] = D[mb*BM + mrow + lane][j0 + jj]
                     }
+                    if (args.tma_store == 2) {
+                        // contiguous output, direct stores: for token j0+jj the warp's
+                        // 32 lanes hold 32 consecutive rows m, i.e. 64 contiguous bytes
+                        // of out[token][.]: one coalesced st.global per token, fire and
+                        // forget (no staging buffer, no wait on a bulk copy's reads)
+                        __nv_bfloat16* dst =
+                            args.out + (size_t)(tile.pos + j0) * args.M + mb * BM + mrow + lane;
+                        const int nj = min(32, tile.count - j0);
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj) {
+                            if (jj < nj) {
+                                float f = __uint_as_float(v[jj]);
+                                if (args.silu) f = silu_fast(f);
+                                dst[(size_t)jj * args.M] = __float2bfloat16_rn(f);
+                            }
+                        }
+                        continue;
+                    }
                     if (args.tma_store) {
                         // contiguous output: every warp stages its own 32 rows x 32
                         // tokens ([token][32 rows], 64 B per token) and stores them
@@ -554,6 +572,365 @@ __global__ void __maxnreg__(kNT == 256 ? 128 : 64)
     }
 }
 
+// ===========================================================================
+// CTA-pair variant (tcgen05.mma.cta_group::2): one unit = (token tile, 256
+// weight rows) is computed by the two CTAs of a cluster on two SMs.  CTA r
+// holds weight slab r (128 rows) and half of the token tile (rows
+// [r*N/2, (r+1)*N/2)); the leader (r = 0) issues M=256 MMAs that read A from
+// each CTA's own slab and B from both halves, and each CTA's TMEM receives
+// its own 128 rows x N accumulator.  Per SM this halves the token-tile bytes
+// (TMA writes and tensor-core smem reads), the epilogue warps and the token
+// ring, which buys (a) a deeper weight ring (more HBM bytes in flight per
+// SM), (b) double-buffered accumulators at every tile width (the epilogue of
+// unit i drains under the MMAs of unit i+1), and (c) a smaller footprint
+// beside the co-resident exact router.
+//
+// Synchronisation: both CTAs' TMA loads complete_tx on the LEADER's full
+// barriers (cta_group::2 bulk tensor copies), the leader's producer lanes
+// post the pair's byte counts; the leader's MMA commits arrive on the empty
+// barriers and the accumulator-full barriers of BOTH CTAs (multicast); each
+// CTA's epilogue warps arrive on the leader's accumulator-empty barrier.
+// ===========================================================================
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
+    uint32_t o;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(o) : "r"(saddr), "r"(rank));
+    return o;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                     : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_t leader_bar,
+                                                 void* dst, int c0, int c1, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ void mma_bf16_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                              uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+// arrive on the barrier at this smem offset in BOTH CTAs of the pair
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+
+constexpr int P_BOX = 32;                   // token rows per TMA box
+constexpr int P_EPI_WARPS = 4;              // one per TMEM lane quadrant (own 128 rows)
+constexpr int P_THREADS = 32 * (EPI_WARP0 + P_EPI_WARPS);
+// a pipeline stage holds P_KS consecutive 64-wide K blocks, so each MMA
+// commit (and barrier round trip between the two SMs) covers 4 * P_KS MMAs
+constexpr int P_KS = 2;
+template <int kNT>
+__host__ __device__ constexpr int pair_a_stage_bytes() { return P_KS * A_SLAB_BYTES; }
+template <int kNT>
+__host__ __device__ constexpr int pair_b_stage_bytes() { return P_KS * (kNT / 2) * BK * 2; }
+constexpr int P_EPI_BYTES = 32 * 128 * 2;   // [32 tokens][128 rows] bf16 per staging buffer
+// kAS / kBS: weight / token ring stages (each P_KS K blocks)
+template <int kNT, int kAS, int kBS>
+constexpr int gemm_pair_smem_bytes() {
+    return kAS * pair_a_stage_bytes<kNT>() + kBS * pair_b_stage_bytes<kNT>() + 1024 + 256 +
+           2 * P_EPI_BYTES;
+}
+
+template <int kNT, int kAS, int kBS>
+__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(128)
+    grouped_gemm_pair_kernel(const __grid_constant__ CUtensorMap map_w,
+                             const __grid_constant__ CUtensorMap map_x,
+                             const __grid_constant__ CUtensorMap map_out, const GemmArgs args) {
+    constexpr int NT = kNT;
+    constexpr int AS = kAS;
+    constexpr int BS = kBS;
+    constexpr int A_STAGE = pair_a_stage_bytes<kNT>();
+    constexpr int B_STAGE = pair_b_stage_bytes<kNT>();
+    constexpr int B_KB = (kNT / 2) * BK * 2;  // one K block of this CTA's token half
+    constexpr int RING = AS * A_STAGE + BS * B_STAGE;
+    static_assert(2 * NT <= TMEM_COLS, "double-buffered accumulators must fit TMEM");
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* a_ring = smem;
+    unsigned char* b_ring = smem + AS * A_STAGE;
+    uint64_t* a_full = reinterpret_cast<uint64_t*>(smem + RING);
+    uint64_t* a_empty = a_full + AS;
+    uint64_t* b_full = a_empty + AS;
+    uint64_t* b_empty = b_full + BS;
+    uint64_t* tfull = b_empty + BS;  // [2]
+    uint64_t* tempty = tfull + 2;     // [2] (leader's are the live ones)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    unsigned char* epi = smem + RING + 256;
+
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+    const int mblocks = args.M / BM;
+    const int kblocks = args.K / BK;
+    const int ksteps = kblocks / P_KS;  // the launcher guarantees K % (P_KS * BK) == 0
+    const int n_units = (*args.n_tiles) * mblocks;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < AS; ++s) {
+            mbar_init(&a_full[s], 1);
+            mbar_init(&a_empty[s], 1);
+        }
+        for (int s = 0; s < BS; ++s) {
+            mbar_init(&b_full[s], 1);
+            mbar_init(&b_empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 2 * P_EPI_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_w)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_x)) : "memory");
+    }
+    if (warp == 1) {  // same warp in both CTAs (cta_group::2 allocation)
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ===== weight producer: this CTA's 128-row slab of each 256-row block =====
+        if (lane == 0) {
+            const uint64_t pol_once = policy_evict_first(), pol_shared = policy_evict_last();
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int u = pair; u < n_units; u += n_pairs) {
+                int ti, mb;
+                unit_map(u, mblocks, args.tiles, ti, mb, args.debug);
+                const TokenTile tile = args.tiles[ti];
+                const int ebase = tile.e * (args.M / 128) * kblocks * 128;
+                const uint64_t pol_w = (tile.pad & 0xffff) > 1 ? pol_shared : pol_once;
+                const int slab = mb * SLABS + (int)rank;
+                for (int ks = 0; ks < ksteps; ++ks) {
+                    mbar_wait(&a_empty[stage], phase ^ 1);
+                    if (leader) mbar_expect_tx(&a_full[stage], 2 * A_STAGE);
+                    const uint32_t bar = mapa_rank(smem_u32(&a_full[stage]), 0);
+#pragma unroll
+                    for (int q = 0; q < P_KS; ++q)
+                        tma_load_2d_pair(&map_w, bar, a_ring + stage * A_STAGE + q * A_SLAB_BYTES, 0,
+                                         ebase + (slab * kblocks + ks * P_KS + q) * 128, pol_w);
+                    if (++stage == AS) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 2) {
+        // ===== token producer: this CTA's half of the tile's rows =====
+        if (lane == 0) {
+            const uint64_t pol_x = policy_evict_last();
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int u = pair; u < n_units; u += n_pairs) {
+                int ti, mb_;
+                unit_map(u, mblocks, args.tiles, ti, mb_, args.debug);
+                const TokenTile tile = args.tiles[ti];
+                const int n_eff = max(32, (tile.count + 31) & ~31);
+                const int half = n_eff >> 1;
+                const int nbox = (half + P_BOX - 1) / P_BOX;
+                const int row0 = tile.pos + (int)rank * half;
+                for (int ks = 0; ks < ksteps; ++ks) {
+                    mbar_wait(&b_empty[stage], phase ^ 1);
+                    if (leader)
+                        mbar_expect_tx(&b_full[stage], (uint32_t)(2 * P_KS * nbox * P_BOX * BK * 2));
+                    const uint32_t bar = mapa_rank(smem_u32(&b_full[stage]), 0);
+                    for (int q = 0; q < P_KS; ++q) {
+                        unsigned char* bbase = b_ring + stage * B_STAGE + q * B_KB;
+                        for (int bx = 0; bx < nbox; ++bx)
+                            tma_load_2d_pair(&map_x, bar, bbase + bx * P_BOX * BK * 2,
+                                             (ks * P_KS + q) * BK, row0 + P_BOX * bx, pol_x);
+                    }
+                    if (++stage == BS) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer: the leader CTA only =====
+        if (leader) {
+            int as = 0, bs = 0;
+            uint32_t aph = 0, bph = 0;
+            int local = 0;
+            for (int u = pair; u < n_units; u += n_pairs, ++local) {
+                int ti, mb_;
+                unit_map(u, mblocks, args.tiles, ti, mb_, args.debug);
+                const TokenTile tile = args.tiles[ti];
+                const int n_eff = max(32, (tile.count + 31) & ~31);
+                const uint32_t idesc = make_idesc(256, n_eff);
+                const int buf = local & 1;
+                mbar_wait(&tempty[buf], ((local >> 1) & 1) ^ 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                for (int ks = 0; ks < ksteps; ++ks) {
+                    mbar_wait(&a_full[as], aph);
+                    mbar_wait(&b_full[bs], bph);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    if (lane == 0) {
+#pragma unroll
+                        for (int q = 0; q < P_KS; ++q) {
+                            const uint32_t abase = smem_u32(a_ring + as * A_STAGE + q * A_SLAB_BYTES);
+                            const uint32_t bbase = smem_u32(b_ring + bs * B_STAGE + q * B_KB);
+#pragma unroll
+                            for (int k = 0; k < BK / 16; ++k)
+                                mma_bf16_pair(tmem_base + buf * NT, make_desc_sw128(abase + k * 32),
+                                              make_desc_sw128(bbase + k * 32), idesc,
+                                              (ks | q | k) != 0);
+                        }
+                        mma_commit_pair(&a_empty[as]);
+                        mma_commit_pair(&b_empty[bs]);
+                    }
+                    __syncwarp();
+                    if (++as == AS) {
+                        as = 0;
+                        aph ^= 1;
+                    }
+                    if (++bs == BS) {
+                        bs = 0;
+                        bph ^= 1;
+                    }
+                }
+                if (lane == 0) mma_commit_pair(&tfull[buf]);
+                __syncwarp();
+            }
+        }
+    } else {
+        // ===== epilogue: warps 3..6 drain this CTA's 128 accumulator rows =====
+        const int quad = warp & 3;
+        const int ew = warp - EPI_WARP0;
+        const uint32_t tempty_leader[2] = {mapa_rank(smem_u32(&tempty[0]), 0),
+                                           mapa_rank(smem_u32(&tempty[1]), 0)};
+        int chunk = 0;
+        int local = 0;
+        for (int u = pair; u < n_units; u += n_pairs, ++local) {
+            int ti, mb;
+            unit_map(u, mblocks, args.tiles, ti, mb, args.debug);
+            const TokenTile tile = args.tiles[ti];
+            const int buf = local & 1;
+            mbar_wait(&tfull[buf], (local >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const int row_base = mb * BM + (int)rank * 128;  // this CTA's 128 rows
+            const int mrow = quad * 32;                       // this warp's 32 of them
+            const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * NT;
+            uint32_t vn[32];
+            if (tile.count > 0) tmem_ld32_async(taddr, vn);
+            for (int j0 = 0; j0 < tile.count; j0 += 32, ++chunk) {
+                unsigned char* stage = epi + (chunk & 1) * P_EPI_BYTES;
+                uint32_t v[32];
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int q = 0; q < 32; ++q) v[q] = vn[q];
+                if (j0 + 32 < tile.count) tmem_ld32_async(taddr + j0 + 32, vn);
+                if (args.tma_store) {
+                    // [32 tokens][32 rows] per warp, one tensor store per full chunk
+                    unsigned char* wst = stage + ew * (32 * 64);
+                    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                    __syncwarp();
+#pragma unroll
+                    for (int jj = 0; jj < 32; ++jj) {
+                        float f = __uint_as_float(v[jj]);
+                        if (args.silu) f = silu_fast(f);
+                        *reinterpret_cast<__nv_bfloat16*>(wst + jj * 64 + lane * 2) =
+                            __float2bfloat16_rn(f);
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (j0 + 32 <= tile.count) {
+                        if (lane == 0) {
+                            asm volatile(
+                                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                                    reinterpret_cast<uint64_t>(&map_out)),
+                                "r"(row_base + mrow), "r"(tile.pos + j0), "r"(smem_u32(wst))
+                                : "memory");
+                            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                        }
+                    } else if (j0 + lane < tile.count) {
+                        __nv_bfloat16* dst =
+                            args.out + (size_t)(tile.pos + j0 + lane) * args.M + row_base + mrow;
+                        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 64;" ::"l"(
+                                         reinterpret_cast<uint64_t>(dst)),
+                                     "r"(smem_u32(wst + lane * 64))
+                                     : "memory");
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    }
+                    continue;
+                }
+                // scattered rows (e.g. the EP return over NVLink): [32 tokens][128 rows]
+                // shared by the 4 epilogue warps; each token's 256 B of this CTA's rows
+                // leave by one bulk copy
+                constexpr int TOK_PER_WARP = 32 / P_EPI_WARPS;
+                if (lane < TOK_PER_WARP) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                asm volatile("bar.sync 1, %0;" ::"n"(P_EPI_WARPS * 32) : "memory");
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj) {
+                    float f = __uint_as_float(v[jj]);
+                    if (args.silu) f = silu_fast(f);
+                    *reinterpret_cast<__nv_bfloat16*>(stage + jj * 256 + (mrow + lane) * 2) =
+                        __float2bfloat16_rn(f);
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("bar.sync 1, %0;" ::"n"(P_EPI_WARPS * 32) : "memory");
+                const int jj = ew * TOK_PER_WARP + lane;
+                if (lane < TOK_PER_WARP && j0 + jj < tile.count) {
+                    const int p = tile.pos + j0 + jj;
+                    __nv_bfloat16* dst = (args.row_dst ? reinterpret_cast<__nv_bfloat16*>(
+                                                             args.row_dst[args.row_ids ? args.row_ids[p] : p])
+                                                       : args.out + (size_t)p * args.M) +
+                                         row_base;
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 256;" ::"l"(
+                                     reinterpret_cast<uint64_t>(dst)),
+                                 "r"(smem_u32(stage + jj * 256))
+                                 : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_leader[buf]);
+        }
+    }
+
+    if (warp >= EPI_WARP0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    cluster_sync_all();  // the peer's MMAs / arrivals into this CTA are done
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 1) {
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                     "r"(TMEM_COLS));
+    }
+}
+
 CUtensorMap make_map_2d(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
                         uint32_t box_cols) {
     return make_tma_map_2d(base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, sizeof(__nv_bfloat16), rows, cols,
@@ -592,8 +969,14 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
                                         std::max<size_t>(max_tiles * tile_rows, 1), M, 32, 32,
                                         CU_TENSOR_MAP_SWIZZLE_NONE)
                       : mw;
+    // epilogue of contiguous outputs: SCMOE_GEMM_EPI=direct -> per-token coalesced
+    // st.global from the TMEM registers; default: per-warp TMA tensor stores
+    static const int epi_direct = [] {
+        const char* e = getenv("SCMOE_GEMM_EPI");
+        return e && std::string(e) == "direct" ? 1 : 0;
+    }();
     GemmArgs a;
-    a.tma_store = use_tma_store ? 1 : 0;
+    a.tma_store = use_tma_store ? (epi_direct ? 2 : 1) : 0;
     a.tiles = tiles;
     a.n_tiles = n_tiles_dev;
     a.x_rows = x_row_ids;
@@ -624,6 +1007,38 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
         kern<<<g, threads, smem, c->stream>>>(mw, mx, mo, a);
     };
     (void)grid;
+    // CTA-pair kernel (default; SCMOE_GEMM_2SM=0 selects the single-CTA one)
+    static const bool pair_on = [] {
+        const char* e = getenv("SCMOE_GEMM_2SM");
+        return !(e && atoi(e) == 0);
+    }();
+    if (pair_on && x_row_ids == nullptr && (tile_rows == 192 || tile_rows == 256) &&
+        K % (P_KS * BK) == 0) {
+        const CUtensorMap mx32 = make_map_2d(X, std::max<size_t>(x_rows, 1), K, P_BOX, BK);
+        auto go2 = [&](auto kern, int smem) {
+            const size_t units = max_tiles * (M / BM);
+            const int sms = c->gemm_sms > 0 ? std::min(c->gemm_sms, c->num_sms) : c->num_sms;
+            const int pairs = (int)std::min<size_t>(units, (size_t)std::max(1, sms / 2));
+            ensure_max_dynamic_smem(reinterpret_cast<const void*>(kern), smem, c->device);
+            kern<<<2 * pairs, P_THREADS, smem, c->stream>>>(mw, mx32, mo, a);
+        };
+        // ring stages of the 192-token variant (the one beside the router):
+        // SCMOE_PAIR_STAGES = "AB" digits, default 33
+        static const int st = [] {
+            const char* e = getenv("SCMOE_PAIR_STAGES");
+            return e ? atoi(e) : 33;
+        }();
+        if (tile_rows == 256)
+            go2(grouped_gemm_pair_kernel<256, 3, 3>, gemm_pair_smem_bytes<256, 3, 3>());
+        else if (st == 32)
+            go2(grouped_gemm_pair_kernel<192, 3, 2>, gemm_pair_smem_bytes<192, 3, 2>());
+        else if (st == 22)
+            go2(grouped_gemm_pair_kernel<192, 2, 2>, gemm_pair_smem_bytes<192, 2, 2>());
+        else
+            go2(grouped_gemm_pair_kernel<192, 3, 3>, gemm_pair_smem_bytes<192, 3, 3>());
+        SCMOE_LAUNCH_CHECK(c);
+        return;
+    }
     if (tile_rows == 128) {
         go(grouped_gemm_kernel<128>, gemm_smem_bytes<128>(), NUM_THREADS, BM);
     } else if (tile_rows == 256 && slabs256 == 1) {

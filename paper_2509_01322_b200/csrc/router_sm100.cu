@@ -297,10 +297,15 @@ void launch_router_corun(scmoe_ctx* c, const float* X, const float* W, float* lo
                          size_t K, size_t E) {
     static const int stages = getenv("SCMOE_CORUN_STAGES") ? atoi(getenv("SCMOE_CORUN_STAGES")) : 2;
     const int ctas = c->router_sms > 0 ? c->router_sms : c->num_sms;
-    if (stages == 2)
-        launch_persistent<4, 4, 2, 1>(c, X, W, logits, T, K, E, ctas);
-    else
-        launch_persistent<4, 4, 3, 1>(c, X, W, logits, T, K, E, ctas);
+    // SCMOE_CORUN_STAGES: 2 (default) <4,4,2,1> 25 KB; 3 <4,4,3,1> 37 KB;
+    // 4 <4,4,4,2> 50 KB; 8 <4,8,2,1> 50 KB; 9 <4,8,3,1> 74 KB
+    switch (stages) {
+        case 3: launch_persistent<4, 4, 3, 1>(c, X, W, logits, T, K, E, ctas); break;
+        case 4: launch_persistent<4, 4, 4, 2>(c, X, W, logits, T, K, E, ctas); break;
+        case 8: launch_persistent<4, 8, 2, 1>(c, X, W, logits, T, K, E, ctas); break;
+        case 9: launch_persistent<4, 8, 3, 1>(c, X, W, logits, T, K, E, ctas); break;
+        default: launch_persistent<4, 4, 2, 1>(c, X, W, logits, T, K, E, ctas); break;
+    }
 }
 
 }  // namespace scmoe

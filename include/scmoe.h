@@ -419,6 +419,14 @@ int scmoe_mla_destroy(scmoe_ctx* ctx, scmoe_mla* m);
 /* which = SCMOE_MLA_W_*; w is that matrix, row-major, host / device. */
 int scmoe_mla_set_weight_host(scmoe_ctx* ctx, scmoe_mla* m, int which, const float* w);
 int scmoe_mla_set_weight(scmoe_ctx* ctx, scmoe_mla* m, int which, const float* w_dev);
+/* Forward precision of scmoe_mla_forward (and the full layer's MLAs):
+ * SCMOE_PREC_F32_EXACT (default; bitwise equal to the reference) or
+ * SCMOE_PREC_BF16: every contraction (projections, scores, P.V) on the
+ * tcgen05 grouped GEMM with bf16 operands and fp32 accumulation, causal
+ * softmax in fp32 (rel-L2 <= 2e-2 vs the reference).  ConfigError unless d,
+ * d_q, d_kv and H*d_head_c are multiples of 64 and d_head_c <= 256.  The
+ * cached decode step (mla_infer_step) stays exact. */
+int scmoe_mla_set_precision(scmoe_ctx* ctx, scmoe_mla* m, int precision);
 /* out [rows, d] = mla_block(h [rows, d], seq_len) value (stream-ordered). */
 int scmoe_mla_forward(scmoe_ctx* ctx, scmoe_mla* m, const float* h_dev, size_t rows,
                       size_t seq_len, float* out_dev);

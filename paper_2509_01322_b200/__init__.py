@@ -159,6 +159,7 @@ _PROTOS = {
     "scmoe_ep_plan": (C.c_int, [_P, _P, _SZ, _SZ, _SZ, _SZ, C.c_int, _P, _P, _P, _P]),
     "scmoe_gather_rows_bf16": (C.c_int, [_P, _P, _SZ, _P, _SZ, _P]),
     "scmoe_permutation": (C.c_int, [_P, _P, _SZ, _SZ, _SZ, _SZ, _P, _P]),
+    "scmoe_mla_set_precision": (C.c_int, [_P, _P, C.c_int]),
     "scmoe_ep_unique_id_bytes": (_SZ, []),
     "scmoe_ep_unique_id": (C.c_int, [_P]),
     "scmoe_ep_create": (C.c_int, [_P, C.c_int, C.c_int, _P, _SZ, _SZ, _SZ, _SZ, _SZ, _SZ,

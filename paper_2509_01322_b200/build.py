@@ -37,6 +37,7 @@ SOURCES = {
     "capi.cu": [],
     "gemm_sm100.cu": ["-Xptxas", "-v"],
     "ep.cu": [],
+    "mla_tc.cu": [],
 }
 HOST_SOURCES = ["host_rng.cpp"]
 HEADERS = ["internal.cuh", "libm_port.h", "sm100_util.cuh", "f32x2.cuh"]

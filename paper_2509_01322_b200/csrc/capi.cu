@@ -1512,6 +1512,13 @@ int scmoe_combine_rows(scmoe_ctx* c, scmoe_bank* b, const float* x, const void* 
 // ===========================================================================
 namespace {
 
+void mla_check_tc_dims(const scmoe_mla* m) {
+    if (m->d % 64 || m->dq % 64 || m->dkv % 64 || (m->H * m->dhc) % 64 || m->dhc > 256)
+        SCMOE_THROW(SCMOE_ERR_CONFIG,
+                    "mla: the tensor-core path needs d, d_q, d_kv, H*d_head_c multiples of 64 "
+                    "and d_head_c <= 256");
+}
+
 void mla_check_dims(size_t d, size_t dq, size_t dkv, size_t H, size_t dhr) {
     if (d == 0 || dq == 0 || dkv == 0)
         SCMOE_THROW(SCMOE_ERR_PARAMETER, "mla_scale_factors: dims must be positive");
@@ -1622,8 +1629,20 @@ int scmoe_mla_destroy(scmoe_ctx* c, scmoe_mla* m) {
     cudaFree(m->w_kv);
     cudaFree(m->w_o);
     cudaFree(m->rope);
+    for (auto* w : m->tc_w) cudaFree(w);
     delete m;
     return SCMOE_OK;
+}
+
+int scmoe_mla_set_precision(scmoe_ctx* c, scmoe_mla* m, int precision) {
+    return guarded(c, [&] {
+        require_ctx(c);
+        if (!m) SCMOE_THROW(SCMOE_ERR_PARAMETER, "mla: null handle");
+        if (precision != SCMOE_PREC_F32_EXACT && precision != SCMOE_PREC_BF16)
+            SCMOE_THROW(SCMOE_ERR_CONFIG, "mla: precision must be F32_EXACT or BF16");
+        if (precision == SCMOE_PREC_BF16) mla_check_tc_dims(m);
+        m->precision = precision;
+    });
 }
 
 static int mla_set_weight(scmoe_ctx* c, scmoe_mla* m, int which, const float* w) {
@@ -1646,6 +1665,7 @@ static int mla_set_weight(scmoe_ctx* c, scmoe_mla* m, int which, const float* w)
             default: SCMOE_THROW(SCMOE_ERR_PARAMETER, "mla: unknown weight id");
         }
         if (width == 0 || rows == 0) return;
+        m->tc_dirty = true;  // the tensor-core copy is rebuilt on the next bf16 forward
         SCMOE_CUDA(cudaStreamSynchronize(c->stream));
         SCMOE_CUDA(cudaMemcpy2DAsync(dst + col, ld * sizeof(float), w, width * sizeof(float),
                                      width * sizeof(float), rows, cudaMemcpyDefault, c->stream));
@@ -1672,6 +1692,10 @@ int scmoe_mla_forward(scmoe_ctx* c, scmoe_mla* m, const float* h, size_t rows, s
         const size_t n1 = m->n1(), n2 = m->n2(), n3 = m->n3();
         const size_t B = rows / seq_len;
         mla_ensure_rope(c, m, seq_len);
+        if (m->precision == SCMOE_PREC_BF16) {  // tensor cores (mla_tc.cu)
+            mla_forward_tc(c, m, h, rows, seq_len, m->rope, out);
+            return;
+        }
         float* p1 = ws.mla_p1.get<float>(rows * n1);  // [cq | ckv | kr]
         float* qb = ws.mla_q.get<float>(rows * n2);   // [qc | qr]
         float* kv = ws.mla_kv.get<float>(rows * n3);  // [kc | vv]

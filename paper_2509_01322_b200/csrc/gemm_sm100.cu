@@ -136,10 +136,25 @@ struct GemmArgs {
     int M, K;            // weight rows per expert, reduction length
     int tma_store;       // contiguous out: full 32-token chunks leave by one TMA tensor store
     int silu;
+    // causal attention (mla_tc.cu): causal_rows = queries per group -> skip the
+    // units whose weight rows (keys) all lie above the tile's last query;
+    // causal_k -> a unit of weight rows (queries) [mb*BM, (mb+1)*BM) reduces
+    // only over K blocks up to (mb+1)*BM (its probabilities vanish beyond)
+    int causal_rows;
+    int causal_k;
     int debug;           // timing experiments only: bit 0 skip epilogue stores,
                          // bit 1 skip the epilogue (release TMEM at once),
                          // bit 2 tile-major unit order, bit 3 weights always evict-first
 };
+
+__device__ __forceinline__ bool unit_skipped(const GemmArgs& a, const TokenTile& t, int mb,
+                                             int bm) {
+    if (!a.causal_rows) return false;
+    return mb * bm > t.pos - t.e * a.causal_rows + t.count - 1;
+}
+__device__ __forceinline__ int unit_kblocks(const GemmArgs& a, int mb, int kblocks, int bm) {
+    return a.causal_k ? min(kblocks, (mb + 1) * bm / BK) : kblocks;
+}
 
 // Unit u -> (token tile, 256-row weight block).  Units are expert-major:
 // the tiles of one expert (TokenTile.pad = index in the expert << 16 | the
@@ -271,12 +286,14 @@ __global__ void __maxnreg__(kNT == 256 ? 128 : 64)
                 int ti, mb;
                 unit_map(u, mblocks, args.tiles, ti, mb, args.debug);
                 const TokenTile tile = args.tiles[ti];
+                if (unit_skipped(args, tile, mb, BM)) continue;
+                const int kb_end = unit_kblocks(args, mb, kblocks, BM);
                 // blocked weight layout (wblk_index): each (128-row, 64-col) tile is
                 // 128 contiguous 64-element rows of the 2-D view the map describes
                 const int ebase = tile.e * (args.M / 128) * kblocks * 128;
                 const uint64_t pol_w = (tile.pad & 0xffff) > 1 && !(args.debug & 8) ? pol_shared
                                                                                    : pol_once;
-                for (int kb = 0; kb < kblocks; ++kb) {
+                for (int kb = 0; kb < kb_end; ++kb) {
                     mbar_wait(&a_empty[stage], phase ^ 1);
                     unsigned char* abase = a_ring + stage * A_STAGE_BYTES;
                     mbar_expect_tx(&a_full[stage], A_STAGE_BYTES);
@@ -304,6 +321,8 @@ __global__ void __maxnreg__(kNT == 256 ? 128 : 64)
             int ti, mb_;
             unit_map(u, mblocks, args.tiles, ti, mb_, args.debug);
             const TokenTile tile = args.tiles[ti];
+            if (unit_skipped(args, tile, mb_, BM)) continue;
+            const int kb_end = unit_kblocks(args, mb_, kblocks, BM);
             const int n_eff = max(16, (tile.count + 15) & ~15);
             // gather mode: this lane's rows r = lane + 32 i (padding rows repeat
             // the tile's last token; their columns are never stored)
@@ -319,7 +338,7 @@ __global__ void __maxnreg__(kNT == 256 ? 128 : 64)
             }
             // tiled mode: boxes of 64 rows, as many as the tile needs
             const int nbox = (n_eff + 63) / 64;
-            for (int kb = 0; kb < kblocks; ++kb) {
+            for (int kb = 0; kb < kb_end; ++kb) {
                 mbar_wait(&b_empty[stage], phase ^ 1);
                 unsigned char* bbase = b_ring + stage * B_STAGE_BYTES;
                 if (!gather) {
@@ -376,12 +395,17 @@ __global__ void __maxnreg__(kNT == 256 ? 128 : 64)
             int ti, mb_;
             unit_map(u, mblocks, args.tiles, ti, mb_, args.debug);
             const TokenTile tile = args.tiles[ti];
+            if (unit_skipped(args, tile, mb_, BM)) {
+                --local;  // skipped units take no accumulator buffer
+                continue;
+            }
+            const int kb_end = unit_kblocks(args, mb_, kblocks, BM);
             const int n_eff = max(16, (tile.count + 15) & ~15);
             const uint32_t idesc = make_idesc(128, n_eff);
             const int buf = local % NBUF;
             mbar_wait(&tempty[buf], ((local / NBUF) & 1) ^ 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            for (int kb = 0; kb < kblocks; ++kb) {
+            for (int kb = 0; kb < kb_end; ++kb) {
                 mbar_wait(&a_full[as], aph);
                 mbar_wait(&b_full[bs], bph);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -436,6 +460,10 @@ __global__ void __maxnreg__(kNT == 256 ? 128 : 64)
             int ti, mb;
             unit_map(u, mblocks, args.tiles, ti, mb, args.debug);
             const TokenTile tile = args.tiles[ti];
+            if (unit_skipped(args, tile, mb, BM)) {
+                --local;
+                continue;
+            }
             const int buf = local % NBUF;
             mbar_wait(&tfull[buf], (local / NBUF) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -727,10 +755,12 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(128)
                 int ti, mb;
                 unit_map(u, mblocks, args.tiles, ti, mb, args.debug);
                 const TokenTile tile = args.tiles[ti];
+                if (unit_skipped(args, tile, mb, BM)) continue;
+                const int ks_end = unit_kblocks(args, mb, kblocks, BM) / P_KS;
                 const int ebase = tile.e * (args.M / 128) * kblocks * 128;
                 const uint64_t pol_w = (tile.pad & 0xffff) > 1 ? pol_shared : pol_once;
                 const int slab = mb * SLABS + (int)rank;
-                for (int ks = 0; ks < ksteps; ++ks) {
+                for (int ks = 0; ks < ks_end; ++ks) {
                     mbar_wait(&a_empty[stage], phase ^ 1);
                     if (leader) mbar_expect_tx(&a_full[stage], 2 * A_STAGE);
                     const uint32_t bar = mapa_rank(smem_u32(&a_full[stage]), 0);
@@ -755,11 +785,13 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(128)
                 int ti, mb_;
                 unit_map(u, mblocks, args.tiles, ti, mb_, args.debug);
                 const TokenTile tile = args.tiles[ti];
+                if (unit_skipped(args, tile, mb_, BM)) continue;
+                const int ks_end = unit_kblocks(args, mb_, kblocks, BM) / P_KS;
                 const int n_eff = max(32, (tile.count + 31) & ~31);
                 const int half = n_eff >> 1;
                 const int nbox = (half + P_BOX - 1) / P_BOX;
                 const int row0 = tile.pos + (int)rank * half;
-                for (int ks = 0; ks < ksteps; ++ks) {
+                for (int ks = 0; ks < ks_end; ++ks) {
                     mbar_wait(&b_empty[stage], phase ^ 1);
                     if (leader)
                         mbar_expect_tx(&b_full[stage], (uint32_t)(2 * P_KS * nbox * P_BOX * BK * 2));
@@ -787,12 +819,17 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(128)
                 int ti, mb_;
                 unit_map(u, mblocks, args.tiles, ti, mb_, args.debug);
                 const TokenTile tile = args.tiles[ti];
+                if (unit_skipped(args, tile, mb_, BM)) {
+                    --local;  // skipped units take no accumulator buffer
+                    continue;
+                }
+                const int ks_end = unit_kblocks(args, mb_, kblocks, BM) / P_KS;
                 const int n_eff = max(32, (tile.count + 31) & ~31);
                 const uint32_t idesc = make_idesc(256, n_eff);
                 const int buf = local & 1;
                 mbar_wait(&tempty[buf], ((local >> 1) & 1) ^ 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                for (int ks = 0; ks < ksteps; ++ks) {
+                for (int ks = 0; ks < ks_end; ++ks) {
                     mbar_wait(&a_full[as], aph);
                     mbar_wait(&b_full[bs], bph);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -836,6 +873,10 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(128)
             int ti, mb;
             unit_map(u, mblocks, args.tiles, ti, mb, args.debug);
             const TokenTile tile = args.tiles[ti];
+            if (unit_skipped(args, tile, mb, BM)) {
+                --local;
+                continue;
+            }
             const int buf = local & 1;
             mbar_wait(&tfull[buf], (local >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -932,9 +973,9 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(128)
 }
 
 CUtensorMap make_map_2d(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
-                        uint32_t box_cols) {
+                        uint32_t box_cols, uint64_t row_stride = 0) {
     return make_tma_map_2d(base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, sizeof(__nv_bfloat16), rows, cols,
-                           box_rows, box_cols, CU_TENSOR_MAP_SWIZZLE_128B);
+                           box_rows, box_cols, CU_TENSOR_MAP_SWIZZLE_128B, row_stride);
 }
 
 }  // namespace
@@ -946,7 +987,8 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
                               size_t K, const __nv_bfloat16* X, size_t x_rows, const int* x_row_ids,
                               __nv_bfloat16* out, int silu, const TokenTile* tiles,
                               const int* n_tiles_dev, size_t max_tiles, int tile_rows,
-                              const uint64_t* row_dst, const int* row_ids) {
+                              const uint64_t* row_dst, const int* row_ids, size_t x_ld,
+                              int causal_rows, int causal_k) {
     if (max_tiles == 0 || n_experts == 0) return;
     SCMOE_CHECK_ARG(tile_rows == 128 || tile_rows == 192 || tile_rows == 256, SCMOE_ERR_INTERNAL,
                     "gemm: tile rows must be 128, 192 or 256");
@@ -956,7 +998,7 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
     const CUtensorMap mw = make_map_2d(W, n_experts * M * K / BK, BK, 128, BK);
     // X: tiled boxes of 128 permuted rows, or single-row boxes for tile::gather4
     const CUtensorMap mx =
-        make_map_2d(X, std::max<size_t>(x_rows, 1), K, x_row_ids ? 1 : 64, BK);
+        make_map_2d(X, std::max<size_t>(x_rows, 1), K, x_row_ids ? 1 : 64, BK, x_ld);
     // contiguous output: tensor map for the epilogue warps' [32 tokens x 32 rows]
     // stores (SWIZZLE_NONE: each warp's staging tile is dense, 64 B per token)
     static const bool tma_store_on = [] {
@@ -987,6 +1029,8 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
     a.M = (int)M;
     a.K = (int)K;
     a.silu = silu;
+    a.causal_rows = causal_rows;
+    a.causal_k = causal_k;
     static const int dbg = getenv("SCMOE_GEMM_DEBUG") ? atoi(getenv("SCMOE_GEMM_DEBUG")) : 0;
     a.debug = dbg;
     const size_t units_max = max_tiles * (M / BM);
@@ -1014,7 +1058,7 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
     }();
     if (pair_on && x_row_ids == nullptr && (tile_rows == 192 || tile_rows == 256) &&
         K % (P_KS * BK) == 0) {
-        const CUtensorMap mx32 = make_map_2d(X, std::max<size_t>(x_rows, 1), K, P_BOX, BK);
+        const CUtensorMap mx32 = make_map_2d(X, std::max<size_t>(x_rows, 1), K, P_BOX, BK, x_ld);
         auto go2 = [&](auto kern, int smem) {
             const size_t units = max_tiles * (M / BM);
             const int sms = c->gemm_sms > 0 ? std::min(c->gemm_sms, c->num_sms) : c->num_sms;

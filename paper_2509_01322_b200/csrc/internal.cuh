@@ -80,6 +80,9 @@ struct Workspace {
     DevBuf mla_p1, mla_q, mla_kv, mla_att, mla_m, mla_tiles;
     // full ScMoE layer (scmoe_layer_full_forward): normed input, MLA output, a1, dd, a3
     DevBuf full_n, full_m, full_a1, full_dd, full_a3;
+    // tensor-core MLA (mla_tc.cu)
+    DevBuf mtc_x, mtc_p1, mtc_q, mtc_kv, mtc_qr, mtc_kb, mtc_s, mtc_p, mtc_vt, mtc_ot, mtc_mg,
+        mtc_o, mtc_t0, mtc_t1, mtc_t2;
     unsigned char pr_blob[64] = {};  // permutation result carried from moe_front to moe_back
     void release_all() {
         DevBuf* all[] = {&logits, &probs, &hmoe, &hmoe_bf16, &idx, &gates, &ffn_count,
@@ -87,7 +90,9 @@ struct Workspace {
                          &row_token, &tiles, &n_tiles, &xp, &h, &y, &in_copy, &out_copy, &misc,
                          &tiles_router, &ep_bins, &ep_local, &ep_y, &dn_x, &dn_h, &dn_y,
                          &dn_tiles, &mla_p1, &mla_q, &mla_kv, &mla_att, &mla_m, &mla_tiles, &full_n, &full_m, &full_a1,
-                         &full_dd, &full_a3};
+                         &full_dd, &full_a3, &mtc_x, &mtc_p1, &mtc_q, &mtc_kv, &mtc_qr, &mtc_kb,
+                         &mtc_s, &mtc_p, &mtc_vt, &mtc_ot, &mtc_mg, &mtc_o, &mtc_t0, &mtc_t1,
+                         &mtc_t2};
         for (DevBuf* b : all) b->release();
     }
 };
@@ -354,7 +359,8 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
                               const int* x_row_ids, __nv_bfloat16* out, int silu,
                               const TokenTile* tiles,
                               const int* n_tiles_dev, size_t max_tiles, int tile_rows,
-                              const uint64_t* row_dst = nullptr, const int* row_ids = nullptr);
+                              const uint64_t* row_dst = nullptr, const int* row_ids = nullptr,
+                              size_t x_ld = 0, int causal_rows = 0, int causal_k = 0);
 // Expert-parallel dispatch over peer memory: send row j (rows sorted by
 // destination rank, send_start[G+1]) -> peer_rows[d] row dst_offset[d] + j - send_start[d].
 void launch_ep_put_rows(scmoe_ctx* c, const __nv_bfloat16* src, size_t d, const int* send_token,
@@ -387,6 +393,9 @@ void launch_mla_scale_rope(scmoe_ctx* c, float* X, size_t ld, size_t rows, int n
                            size_t pos0, size_t seq_len);
 void launch_mla_attention(scmoe_ctx* c, const MlaAttnArgs& a, int batches);
 void launch_add_f32(scmoe_ctx* c, const float* a, const float* b, size_t n, float* out);
+// tensor-core MLA forward (mla_tc.cu); rope = the (cos, sin) table of m
+void mla_forward_tc(scmoe_ctx* c, scmoe_mla* m, const float* h, size_t rows, size_t seq_len,
+                    const float2* rope, float* out);
 
 }  // namespace scmoe
 
@@ -404,6 +413,13 @@ struct scmoe_mla {
     float *w_h = nullptr, *w_q = nullptr, *w_kv = nullptr, *w_o = nullptr;
     float2* rope = nullptr;  // (cos, sin) [rope_rows][dhr/2]
     size_t rope_rows = 0;
+    // forward precision: SCMOE_PREC_F32_EXACT (bitwise, mla.cu) or SCMOE_PREC_BF16
+    // (tensor cores, mla_tc.cu); the bf16 blocked weights [w_h | w_q | w_kv | w_o]
+    // (rows padded to 256) are rebuilt from the fp32 ones after a weight change
+    int precision = SCMOE_PREC_F32_EXACT;
+    bool tc_dirty = true;
+    __nv_bfloat16* tc_w[4] = {nullptr, nullptr, nullptr, nullptr};
+    size_t tc_M[4] = {0, 0, 0, 0};
     size_t n1() const { return dq + dkv + dhr; }
     size_t n2() const { return H * (dhc + dhr); }
     size_t n3() const { return 2 * H * dhc; }

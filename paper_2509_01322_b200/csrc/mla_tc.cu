@@ -1,0 +1,385 @@
+// mla_tc.cu -- multi-head latent attention forward (blocks.hpp:73-102) on the
+// tensor cores: bf16 operands, fp32 accumulation, the same tcgen05 grouped
+// GEMM as the experts for every contraction.  Tolerance path (rel-L2 <= 2e-2
+// vs the exact oracle, tests/test_gpu_mla.py); the exact fp32 path (mla.cu)
+// stays the bitwise reference implementation.
+//
+//   P1  = [cq | ckv | kr] = bf16(h) W_h        (one GEMM, W_h = [w_dq|w_dkv|w_kr])
+//         cq *= alpha_q, ckv *= alpha_kv, rope(kr)            (bf16 epilogue kernel)
+//   Q   = [qc | qr] = cq W_q, rope(qr)         (X = P1's cq columns by TMA stride)
+//   KV  = [kc | vv] = ckv W_kv
+//   per (sequence b, head h), as grouped-GEMM "experts" (one per (b, h)):
+//     S   = [qc|qr] [kc|kr]^T                  (keys on the M side, K-blocked)
+//     P   = softmax(scale * S) causal          (rows written straight into the
+//                                               K-blocked layout PV reads as W)
+//     O^T = V^T-rows x P                       (O^T[c][q] = sum_k P[q][k] V[k][c])
+//   out = fp32(merged(O) W_o)
+// Every GEMM is D[rows][m] = sum_k W[m][k] X[rows][k] with W in the blocked
+// K-major layout (internal.cuh wblk_index), M padded to a multiple of 256 and
+// K to a multiple of 64 with zeros; sequence lengths are padded to 256 keys.
+#include <cmath>
+
+#include "internal.cuh"
+
+namespace scmoe {
+
+namespace {
+
+size_t pad_to(size_t x, size_t m) { return (x + m - 1) / m * m; }
+
+// cols [0, n_a) *= alpha_a, [n_a, n_a + n_b) *= alpha_b, cols [rc, rc + heads*hd)
+// rotated per head at pos = r % seq_len (tensor.hpp:207-215), bf16 in place.
+__global__ void mla_scale_rope_bf16_kernel(__nv_bfloat16* __restrict__ X, size_t ld, size_t rows,
+                                           int n_a, float alpha_a, int n_b, float alpha_b, int rc,
+                                           int heads, int hd, const float2* __restrict__ table,
+                                           size_t seq_len) {
+    const int half = hd / 2;
+    const size_t per_row = (size_t)n_a + n_b + (size_t)heads * half;
+    const size_t n = rows * per_row;
+    for (size_t it = blockIdx.x * (size_t)blockDim.x + threadIdx.x; it < n;
+         it += (size_t)gridDim.x * blockDim.x) {
+        const size_t r = it / per_row;
+        size_t c = it % per_row;
+        __nv_bfloat16* row = X + r * ld;
+        if (c < (size_t)n_a) {
+            row[c] = __float2bfloat16_rn(__bfloat162float(row[c]) * alpha_a);
+        } else if (c < (size_t)(n_a + n_b)) {
+            row[c] = __float2bfloat16_rn(__bfloat162float(row[c]) * alpha_b);
+        } else {
+            c -= n_a + n_b;
+            const int h = (int)(c / half), p = (int)(c % half);
+            const float2 cs = table[(r % seq_len) * half + p];
+            __nv_bfloat16* q = row + rc + h * hd + 2 * p;
+            const float a = __bfloat162float(q[0]), b = __bfloat162float(q[1]);
+            q[0] = __float2bfloat16_rn(a * cs.x - b * cs.y);
+            q[1] = __float2bfloat16_rn(a * cs.y + b * cs.x);
+        }
+    }
+}
+
+// Qrows[(bh*L + q)][t] = [qc_h | qr_h | 0] of token b*L + q;
+// Kblk[bh] (blocked, Lp x Dk) row key = [kc_h | kr | 0] of token b*L + key (0 past L).
+__global__ void mla_pack_qk_kernel(const __nv_bfloat16* __restrict__ Q, size_t ldq,
+                                   const __nv_bfloat16* __restrict__ KV, size_t ldkv,
+                                   const __nv_bfloat16* __restrict__ P1, size_t ldp1, int kr_col,
+                                   int BH, int H, int L, int Lp, int dhc, int dhr, int Dk,
+                                   __nv_bfloat16* __restrict__ Qrows,
+                                   __nv_bfloat16* __restrict__ Kblk) {
+    const size_t n = (size_t)BH * Lp * Dk;
+    const __nv_bfloat16 zero = __float2bfloat16_rn(0.f);
+    for (size_t it = blockIdx.x * (size_t)blockDim.x + threadIdx.x; it < n;
+         it += (size_t)gridDim.x * blockDim.x) {
+        const int t = (int)(it % Dk);
+        const size_t row = it / Dk;
+        const int j = (int)(row % Lp);
+        const int bh = (int)(row / Lp), b = bh / H, h = bh % H;
+        const size_t tok = (size_t)b * L + j;
+        __nv_bfloat16 kv = zero, qv = zero;
+        if (j < L) {
+            if (t < dhc) {
+                kv = KV[tok * ldkv + (size_t)h * dhc + t];
+                qv = Q[tok * ldq + (size_t)h * dhc + t];
+            } else if (t < dhc + dhr) {
+                kv = P1[tok * ldp1 + kr_col + (t - dhc)];
+                qv = Q[tok * ldq + (size_t)H * dhc + (size_t)h * dhr + (t - dhc)];
+            }
+            Qrows[((size_t)bh * L + j) * Dk + t] = qv;
+        }
+        Kblk[(size_t)bh * Lp * Dk + wblk_index(j, t, Dk)] = kv;
+    }
+}
+
+// Same, 8 consecutive t (16 bytes) per thread: needs dhc % 8 == dhr % 8 == 0.
+__global__ void mla_pack_qk8_kernel(const __nv_bfloat16* __restrict__ Q, size_t ldq,
+                                    const __nv_bfloat16* __restrict__ KV, size_t ldkv,
+                                    const __nv_bfloat16* __restrict__ P1, size_t ldp1, int kr_col,
+                                    int BH, int H, int L, int Lp, int dhc, int dhr, int Dk,
+                                    __nv_bfloat16* __restrict__ Qrows,
+                                    __nv_bfloat16* __restrict__ Kblk) {
+    const int Dk8 = Dk / 8;
+    const size_t n = (size_t)BH * Lp * Dk8;
+    for (size_t it = blockIdx.x * (size_t)blockDim.x + threadIdx.x; it < n;
+         it += (size_t)gridDim.x * blockDim.x) {
+        const int t = (int)(it % Dk8) * 8;
+        const size_t row = it / Dk8;
+        const int j = (int)(row % Lp);
+        const int bh = (int)(row / Lp), b = bh / H, h = bh % H;
+        const size_t tok = (size_t)b * L + j;
+        uint4 kv = make_uint4(0, 0, 0, 0), qv = make_uint4(0, 0, 0, 0);
+        if (j < L) {
+            if (t < dhc) {
+                kv = *reinterpret_cast<const uint4*>(KV + tok * ldkv + (size_t)h * dhc + t);
+                qv = *reinterpret_cast<const uint4*>(Q + tok * ldq + (size_t)h * dhc + t);
+            } else if (t < dhc + dhr) {
+                kv = *reinterpret_cast<const uint4*>(P1 + tok * ldp1 + kr_col + (t - dhc));
+                qv = *reinterpret_cast<const uint4*>(Q + tok * ldq + (size_t)H * dhc +
+                                                     (size_t)h * dhr + (t - dhc));
+            }
+            *reinterpret_cast<uint4*>(Qrows + ((size_t)bh * L + j) * Dk + t) = qv;
+        }
+        *reinterpret_cast<uint4*>(Kblk + (size_t)bh * Lp * Dk + wblk_index(j, t, Dk)) = kv;
+    }
+}
+
+// Vt[(bh*dhc + c)][key] = vv_h[c] of token b*L + key (0 past L): 32x32 tile transpose.
+__global__ void mla_pack_vt_kernel(const __nv_bfloat16* __restrict__ KV, size_t ldkv, int H,
+                                   int L, int Lp, int dhc, __nv_bfloat16* __restrict__ Vt) {
+    __shared__ float tile[32][33];
+    const int bh = blockIdx.z, b = bh / H, h = bh % H;
+    const int k0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int key = k0 + i, c = c0 + threadIdx.x;
+        tile[i][threadIdx.x] =
+            key < L && c < dhc
+                ? __bfloat162float(KV[((size_t)b * L + key) * ldkv + (size_t)H * dhc +
+                                      (size_t)h * dhc + c])
+                : 0.f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int c = c0 + i, key = k0 + threadIdx.x;
+        if (c < dhc && key < Lp)
+            Vt[((size_t)bh * dhc + c) * Lp + key] = __float2bfloat16_rn(tile[threadIdx.x][i]);
+    }
+}
+
+// Causal softmax of scale * S (graph.hpp:396-434 semantics: query i sees keys
+// j <= i), one warp per (bh, query row), 8 keys (16 bytes) per lane access;
+// the probabilities are written in the blocked K-major layout the PV GEMM
+// reads as its W operand.  Keys past the end of q's 256-row block are never
+// read (the PV GEMM's causal K bound), so only the diagonal block's tail gets
+// zeros; padding rows q >= L get zeros (their outputs are discarded).
+__global__ void mla_softmax_bf16_kernel(const __nv_bfloat16* __restrict__ S, int BH, int L, int Lp,
+                                        float scale, __nv_bfloat16* __restrict__ Pblk) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= BH * Lp) return;
+    const int bh = warp / Lp, q = warp % Lp;
+    __nv_bfloat16* P = Pblk + (size_t)bh * Lp * Lp;
+    const int jend = min(Lp, ((q >> 8) + 1) << 8);  // multiple of 256
+    if (q >= L) {
+        for (int j = lane * 8; j < jend; j += 256)
+            *reinterpret_cast<uint4*>(P + wblk_index(q, j, Lp)) = make_uint4(0, 0, 0, 0);
+        return;
+    }
+    const __nv_bfloat16* s = S + ((size_t)bh * L + q) * Lp;
+    float mx = -INFINITY, sum = 0.f;
+    for (int j0 = lane * 8; j0 <= q; j0 += 256) {  // online max / sum per lane
+        const uint4 raw = *reinterpret_cast<const uint4*>(s + j0);
+        const __nv_bfloat16* v8 = reinterpret_cast<const __nv_bfloat16*>(&raw);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (j0 + u > q) break;
+            const float v = __bfloat162float(v8[u]) * scale;
+            if (v > mx) {
+                sum = sum * __expf(mx - v) + 1.f;
+                mx = v;
+            } else {
+                sum += __expf(v - mx);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float m2 = __shfl_xor_sync(0xffffffffu, mx, o);
+        const float s2 = __shfl_xor_sync(0xffffffffu, sum, o);
+        const float mn = fmaxf(mx, m2);
+        sum = (mx == -INFINITY ? 0.f : sum * __expf(mx - mn)) +
+              (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mn));
+        mx = mn;
+    }
+    const float inv = 1.f / sum;
+    for (int j0 = lane * 8; j0 < jend; j0 += 256) {
+        uint4 outv = make_uint4(0, 0, 0, 0);
+        if (j0 <= q) {
+            const uint4 raw = *reinterpret_cast<const uint4*>(s + j0);
+            const __nv_bfloat16* v8 = reinterpret_cast<const __nv_bfloat16*>(&raw);
+            __nv_bfloat16* o8 = reinterpret_cast<__nv_bfloat16*>(&outv);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                o8[u] = j0 + u <= q
+                            ? __float2bfloat16_rn(__expf(__bfloat162float(v8[u]) * scale - mx) * inv)
+                            : __float2bfloat16_rn(0.f);
+        }
+        *reinterpret_cast<uint4*>(P + wblk_index(q, j0, Lp)) = outv;
+    }
+}
+
+// merged[(b*L + q)][h*dhc + c] = Ot[(bh*dhc + c)][q]: 32x32 tile transpose.
+__global__ void mla_unpack_o_kernel(const __nv_bfloat16* __restrict__ Ot, int H, int L, int Lp,
+                                    int dhc, __nv_bfloat16* __restrict__ merged) {
+    __shared__ float tile[32][33];
+    const int bh = blockIdx.z, b = bh / H, h = bh % H;
+    const int q0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int c = c0 + i, q = q0 + threadIdx.x;
+        tile[i][threadIdx.x] =
+            c < dhc && q < L ? __bfloat162float(Ot[((size_t)bh * dhc + c) * Lp + q]) : 0.f;
+    }
+    __syncthreads();
+    const size_t ldm = (size_t)H * dhc;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int q = q0 + i, c = c0 + threadIdx.x;
+        if (q < L && c < dhc)
+            merged[((size_t)b * L + q) * ldm + (size_t)h * dhc + c] =
+                __float2bfloat16_rn(tile[threadIdx.x][i]);
+    }
+}
+
+// groups x ceil(rows_per_group / tile) token tiles, expert-major (pad = index
+// in the group << 16 | tiles per group, for the GEMM's sibling scheduling).
+__global__ void uniform_tiles_kernel(int groups, int rows_per_group, int tile,
+                                     TokenTile* __restrict__ tiles, int* __restrict__ n_out) {
+    const int nt = (rows_per_group + tile - 1) / tile;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < groups * nt) {
+        const int g = i / nt, k = i % nt;
+        tiles[i] = TokenTile{g, g * rows_per_group + k * tile, min(tile, rows_per_group - k * tile),
+                             (k << 16) | nt};
+    }
+    if (i == 0) *n_out = groups * nt;
+}
+
+// out[r][j] = float(O[r][j]) (+ residual[r][j]), O with row stride ldo.
+__global__ void mla_out_f32_kernel(const __nv_bfloat16* __restrict__ O, size_t ldo, size_t rows,
+                                   size_t d, float* __restrict__ out) {
+    const size_t n = rows * d;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x)
+        out[i] = __bfloat162float(O[(i / d) * ldo + i % d]);
+}
+
+TokenTile* uniform_tiles(scmoe_ctx* c, DevBuf& buf, int groups, int rows_per_group, int tile,
+                         size_t* max_tiles, int** n_dev) {
+    const size_t nt = (size_t)groups * ceil_div((size_t)rows_per_group, (size_t)tile);
+    TokenTile* t = buf.get<TokenTile>(nt + 1);
+    *n_dev = reinterpret_cast<int*>(t + nt);
+    *max_tiles = nt;
+    uniform_tiles_kernel<<<ceil_div(std::max<size_t>(nt, 1), 256), 256, 0, c->stream>>>(
+        groups, rows_per_group, tile, t, *n_dev);
+    SCMOE_LAUNCH_CHECK(c);
+    return t;
+}
+
+int gs(scmoe_ctx* c, size_t n) {
+    return (int)std::min<size_t>(ceil_div(std::max<size_t>(n, 1), 256), (size_t)c->num_sms * 16);
+}
+
+}  // namespace
+
+// bf16 blocked weights from the fp32 device weights (re-done when a weight changed).
+void mla_prepare_tc(scmoe_ctx* c, scmoe_mla* m) {
+    if (!m->tc_dirty) return;
+    const size_t H = m->H;
+    const size_t Ks[4] = {m->d, m->dq, m->dkv, H * m->dhc};
+    const size_t Ns[4] = {m->n1(), m->n2(), m->n3(), m->d};
+    const float* src[4] = {m->w_h, m->w_q, m->w_kv, m->w_o};
+    for (int i = 0; i < 4; ++i) {
+        const size_t M = pad_to(Ns[i], 256);
+        m->tc_M[i] = M;
+        if (!m->tc_w[i]) SCMOE_CUDA(cudaMalloc(&m->tc_w[i], M * Ks[i] * sizeof(__nv_bfloat16)));
+        SCMOE_CUDA(cudaMemsetAsync(m->tc_w[i], 0, M * Ks[i] * sizeof(__nv_bfloat16), c->stream));
+        // src [K][N] row-major -> blocked W[m = n][k]
+        launch_f32_to_bf16_t(c, src[i], Ks[i], Ns[i], m->tc_w[i]);
+    }
+    m->tc_dirty = false;
+}
+
+void mla_forward_tc(scmoe_ctx* c, scmoe_mla* m, const float* h, size_t rows, size_t L,
+                    const float2* rope, float* out) {
+    mla_prepare_tc(c, m);
+    Workspace& ws = c->ws;
+    const size_t d = m->d, dq = m->dq, dkv = m->dkv, H = m->H, dhc = m->dhc, dhr = m->dhr;
+    const size_t B = rows / L, BH = B * H;
+    const size_t M1 = m->tc_M[0], M2 = m->tc_M[1], M3 = m->tc_M[2], M4 = m->tc_M[3];
+    const size_t Lp = pad_to(L, 256), Dk = pad_to(dhc + dhr, 64);
+    const int TR = grouped_gemm_tile_rows_large();
+    __nv_bfloat16* xb = ws.mtc_x.get<__nv_bfloat16>(rows * d);
+    __nv_bfloat16* p1 = ws.mtc_p1.get<__nv_bfloat16>(rows * M1);
+    __nv_bfloat16* qb = ws.mtc_q.get<__nv_bfloat16>(rows * M2);
+    __nv_bfloat16* kv = ws.mtc_kv.get<__nv_bfloat16>(rows * M3);
+    __nv_bfloat16* qrows = ws.mtc_qr.get<__nv_bfloat16>(BH * L * Dk);
+    __nv_bfloat16* kblk = ws.mtc_kb.get<__nv_bfloat16>(BH * Lp * Dk);
+    __nv_bfloat16* S = ws.mtc_s.get<__nv_bfloat16>(BH * L * Lp);
+    __nv_bfloat16* P = ws.mtc_p.get<__nv_bfloat16>(BH * Lp * Lp);
+    __nv_bfloat16* vt = ws.mtc_vt.get<__nv_bfloat16>(BH * dhc * Lp);
+    __nv_bfloat16* ot = ws.mtc_ot.get<__nv_bfloat16>(BH * dhc * Lp);
+    __nv_bfloat16* mg = ws.mtc_mg.get<__nv_bfloat16>(rows * H * dhc);
+    __nv_bfloat16* ob = ws.mtc_o.get<__nv_bfloat16>(rows * M4);
+    size_t mt_rows = 0, mt_s = 0, mt_pv = 0;
+    int *n_rows = nullptr, *n_s = nullptr, *n_pv = nullptr;
+    TokenTile* t_rows = uniform_tiles(c, ws.mtc_t0, 1, (int)rows, TR, &mt_rows, &n_rows);
+    TokenTile* t_s = uniform_tiles(c, ws.mtc_t1, (int)BH, (int)L, TR, &mt_s, &n_s);
+    TokenTile* t_pv = uniform_tiles(c, ws.mtc_t2, (int)BH, (int)dhc, TR, &mt_pv, &n_pv);
+    {
+        ProfScope _p(c, "mla_tc_proj_h");
+        launch_cast_bf16(c, h, rows * d, xb);
+        launch_grouped_gemm_bf16(c, m->tc_w[0], 1, M1, d, xb, rows, nullptr, p1, 0, t_rows, n_rows,
+                                 mt_rows, TR);
+        mla_scale_rope_bf16_kernel<<<gs(c, rows * (dq + dkv + dhr / 2)), 256, 0, c->stream>>>(
+            p1, M1, rows, (int)dq, m->alpha_q, (int)dkv, m->alpha_kv, (int)(dq + dkv), 1, (int)dhr,
+            rope, L);
+        SCMOE_LAUNCH_CHECK(c);
+    }
+    {
+        ProfScope _p(c, "mla_tc_proj_q");
+        launch_grouped_gemm_bf16(c, m->tc_w[1], 1, M2, dq, p1, rows, nullptr, qb, 0, t_rows, n_rows,
+                                 mt_rows, TR, nullptr, nullptr, M1);
+        mla_scale_rope_bf16_kernel<<<gs(c, rows * H * (dhr / 2)), 256, 0, c->stream>>>(
+            qb, M2, rows, 0, 1.f, 0, 1.f, (int)(H * dhc), (int)H, (int)dhr, rope, L);
+        SCMOE_LAUNCH_CHECK(c);
+    }
+    {
+        ProfScope _p(c, "mla_tc_proj_kv");
+        launch_grouped_gemm_bf16(c, m->tc_w[2], 1, M3, dkv, p1 + dq, rows, nullptr, kv, 0, t_rows,
+                                 n_rows, mt_rows, TR, nullptr, nullptr, M1);
+    }
+    {
+        ProfScope _p(c, "mla_tc_pack");
+        // 16-byte accesses need 8-element aligned sources: dhc, dhr, dq + dkv, the
+        // row strides and the kr column
+        if (dhc % 8 == 0 && dhr % 8 == 0 && (dq + dkv) % 8 == 0)
+            mla_pack_qk8_kernel<<<gs(c, BH * Lp * Dk / 8), 256, 0, c->stream>>>(
+                qb, M2, kv, M3, p1, M1, (int)(dq + dkv), (int)BH, (int)H, (int)L, (int)Lp,
+                (int)dhc, (int)dhr, (int)Dk, qrows, kblk);
+        else
+            mla_pack_qk_kernel<<<gs(c, BH * Lp * Dk), 256, 0, c->stream>>>(
+                qb, M2, kv, M3, p1, M1, (int)(dq + dkv), (int)BH, (int)H, (int)L, (int)Lp,
+                (int)dhc, (int)dhr, (int)Dk, qrows, kblk);
+        SCMOE_LAUNCH_CHECK(c);
+    }
+    {
+        ProfScope _p(c, "mla_tc_scores");
+        // causal: key blocks above a query tile's last query are skipped
+        launch_grouped_gemm_bf16(c, kblk, BH, Lp, Dk, qrows, BH * L, nullptr, S, 0, t_s, n_s, mt_s,
+                                 TR, nullptr, nullptr, 0, (int)L, 0);
+    }
+    {
+        ProfScope _p(c, "mla_tc_softmax");
+        const size_t warps = BH * Lp;
+        mla_softmax_bf16_kernel<<<(unsigned)ceil_div(warps * 32, 256), 256, 0, c->stream>>>(
+            S, (int)BH, (int)L, (int)Lp, m->att_scale, P);
+        SCMOE_LAUNCH_CHECK(c);
+    }
+    {
+        ProfScope _p(c, "mla_tc_pv");
+        mla_pack_vt_kernel<<<dim3((unsigned)ceil_div(dhc, 32), (unsigned)(Lp / 32), (unsigned)BH),
+                             dim3(32, 8), 0, c->stream>>>(kv, M3, (int)H, (int)L, (int)Lp,
+                                                          (int)dhc, vt);
+        SCMOE_LAUNCH_CHECK(c);
+        // causal: query block mb reduces over keys < (mb + 1) * 256 only
+        launch_grouped_gemm_bf16(c, P, BH, Lp, Lp, vt, BH * dhc, nullptr, ot, 0, t_pv, n_pv, mt_pv,
+                                 TR, nullptr, nullptr, 0, 0, 1);
+        mla_unpack_o_kernel<<<dim3((unsigned)ceil_div(dhc, 32), (unsigned)(Lp / 32), (unsigned)BH),
+                              dim3(32, 8), 0, c->stream>>>(ot, (int)H, (int)L, (int)Lp, (int)dhc,
+                                                           mg);
+        SCMOE_LAUNCH_CHECK(c);
+    }
+    ProfScope _p(c, "mla_tc_proj_o");
+    launch_grouped_gemm_bf16(c, m->tc_w[3], 1, M4, H * dhc, mg, rows, nullptr, ob, 0, t_rows,
+                             n_rows, mt_rows, TR);
+    mla_out_f32_kernel<<<gs(c, rows * d), 256, 0, c->stream>>>(ob, M4, rows, d, out);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
+}  // namespace scmoe

@@ -82,13 +82,14 @@ static inline PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 }
 
 // Row-major [rows][cols] tensor, box of box_rows x box_cols elements.
+// row_stride: elements between consecutive rows (0 = cols, a dense matrix).
 static inline CUtensorMap make_tma_map_2d(const void* base, CUtensorMapDataType dtype,
                                           size_t elem_bytes, uint64_t rows, uint64_t cols,
                                           uint32_t box_rows, uint32_t box_cols,
-                                          CUtensorMapSwizzle swizzle) {
+                                          CUtensorMapSwizzle swizzle, uint64_t row_stride = 0) {
     CUtensorMap m;
     cuuint64_t dims[2] = {cols, rows};
-    cuuint64_t strides[1] = {cols * elem_bytes};
+    cuuint64_t strides[1] = {(row_stride ? row_stride : cols) * elem_bytes};
     cuuint32_t box[2] = {box_cols, box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = get_encode_fn()(&m, dtype, 2, const_cast<void*>(base), dims, strides, box, estr,

@@ -39,13 +39,15 @@ class MlaParams:
 
     def __init__(self, d_model: int, d_q: int, d_kv: int, n_heads: int, d_head_c: int,
                  d_head_r: int, weights: Sequence, rope_base: float = 1.0e6,
-                 variance_alignment: bool = True):
+                 variance_alignment: bool = True, precision: int = 0):
         self.d_model, self.d_q, self.d_kv = d_model, d_q, d_kv
         self.n_heads, self.d_head_c, self.d_head_r = n_heads, d_head_c, d_head_r
         self.rope_base, self.variance_alignment = rope_base, variance_alignment
         if isinstance(weights, dict):
             weights = [weights[n] for n in WEIGHT_NAMES]
         self.weights = list(weights)  # numpy arrays or CUDA torch tensors
+        # 0 = SCMOE_PREC_F32_EXACT (bitwise), 1 = SCMOE_PREC_BF16 (tensor cores)
+        self.precision = precision
         self._dev = None
 
     def shapes(self):
@@ -82,6 +84,8 @@ class MlaParams:
             else:
                 a = np.ascontiguousarray(w, np.float32)
                 ctx._check(lib().scmoe_mla_set_weight_host(ctx.handle, h, i, _ptr(a)))
+        if self.precision:
+            ctx._check(lib().scmoe_mla_set_precision(ctx.handle, h, int(self.precision)))
         self._dev = (ctx, h)
         return h
 

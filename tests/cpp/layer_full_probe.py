@@ -1,7 +1,8 @@
 """Measurement probe (not a test): the full ScMoE layer (model.hpp:355-409) at
 LongCat widths -- MLA1 -> dense FFN (12288) -> MLA2, MoE branch (512 + 256
 experts, top-12, bf16 tcgen05) -- serial vs overlapped (MoE on its own
-stream).  python tests/cpp/layer_full_probe.py [rows] [seq_len] [reps]"""
+stream).  python tests/cpp/layer_full_probe.py [rows] [seq_len] [reps] [mla_precision]
+(mla_precision 0 = exact fp32 MLA, 1 = tensor-core bf16 MLA)."""
 import json
 import os
 import sys
@@ -18,6 +19,7 @@ from paper_2509_01322_b200.mla import MlaParams, ScMoELayer  # noqa: E402
 rows = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 seq = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+prec = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 d, dq, dkv, H, dhc, dhr = 6144, 1536, 512, 64, 128, 64
 ctx = P.Context(0)
 
@@ -30,7 +32,7 @@ def mla(seed):
         ctx._check(P.lib().scmoe_rng_fill_uniform(ctx.handle, P.stream_seed(seed, i), 0, r * c,
                                                   1.0 / d, t.data_ptr()))
         ws.append(t.view(r, c))
-    return MlaParams(d, dq, dkv, H, dhc, dhr, weights=ws, rope_base=1.0e6)
+    return MlaParams(d, dq, dkv, H, dhc, dhr, weights=ws, rope_base=1.0e6, precision=prec)
 
 
 class _Handle:  # device-initialised router / bank of DeviceLayer
@@ -45,7 +47,8 @@ moe = DeviceLayer(ctx, LONGCAT, seed=1)
 layer = ScMoELayer(mla(3), mla(4), DenseFFN(ctx, d, 12288), _Handle(moe.router, LONGCAT.top_k),
                    _Handle(moe.bank), *[torch.ones(d).numpy()] * 4, ctx=ctx)
 x = torch.randn(rows, d, device="cuda")
-res = {"probe": "scmoe_layer_full", "rows": rows, "seq_len": seq}
+res = {"probe": "scmoe_layer_full", "rows": rows, "seq_len": seq,
+       "mla": "tensor-core bf16" if prec else "exact fp32"}
 for overlap in (False, True):
     layer.forward(x, seq, overlap=overlap)
     ctx.synchronize()

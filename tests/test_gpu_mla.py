@@ -168,3 +168,41 @@ def test_full_scmoe_layer(scmoe, orc, renorm):
     assert cnt.tobytes() == c_w.tobytes()
     assert O.rel_l2(out - a3, out_w - a3_w) <= 5e-3
     assert O.rel_l2(out, out_w) <= 5e-3
+
+
+TC_SHAPES = [
+    # (d, dq, dkv, H, dhc, dhr, seq_len, n_seq): d, dq, dkv, H*dhc multiples of 64
+    (256, 64, 64, 4, 32, 16, 96, 3),      # one 256-key block, partial
+    (192, 64, 64, 3, 128, 64, 260, 2),    # LongCat head widths, two key blocks
+    (1024, 256, 128, 8, 128, 64, 512, 2),  # wider projections, 2 full key blocks
+]
+TC_TOL = 2e-2  # bf16 operands, fp32 accumulation (BASELINE north_star bound)
+
+
+@pytest.mark.parametrize("shape", TC_SHAPES)
+def test_mla_forward_tensor_cores(scmoe, orc, shape):
+    """The tensor-core MLA (csrc/mla_tc.cu: projections, scores and P.V on the
+    tcgen05 grouped GEMM, bf16 operands) within rel-L2 2e-2 of the exact
+    oracle (blocks.hpp:73-102)."""
+    from paper_2509_01322_b200.mla import MlaParams, mla_block
+    *dims, seq, nseq = shape
+    dims = tuple(dims)
+    w = O.mla_weights(*dims, seed=13)
+    rows = seq * nseq
+    h = O.normal_f32(O.stream_seed(6, 1), rows * dims[0]).reshape(rows, dims[0])
+    rc, want = O.mla_forward(orc, dims, w, h, seq, threads=8)
+    assert rc == 0
+    got = mla_block(h, MlaParams(*dims, weights=w, rope_base=1.0e4, precision=scmoe.PREC_BF16),
+                    seq)
+    err = O.rel_l2(got, want)
+    print(f"MLA tensor cores {shape}: rel-L2 {err:.2e}")
+    assert np.isfinite(got).all() and err <= TC_TOL, err
+
+
+def test_mla_tensor_core_dims_checked(scmoe):
+    from paper_2509_01322_b200.mla import MlaParams, mla_block
+    dims = (48, 24, 16, 3, 10, 6)  # not multiples of 64
+    w = O.mla_weights(*dims, seed=1)
+    h = O.normal_f32(3, 7 * 48).reshape(7, 48)
+    with pytest.raises(scmoe.ConfigError):
+        mla_block(h, MlaParams(*dims, weights=w, precision=scmoe.PREC_BF16), 7)

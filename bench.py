@@ -606,11 +606,35 @@ def run_b200(args):
         st_c = ctx.profile_flush()
         ctx.profile(False)
         idx_c = dsets["idx"].cpu().numpy().view(np.uint32)
+        # two independent decode micro-batches in flight (scmoe_layer_forward_batches:
+        # batch i+1's routing beside batch i's expert-weight stream)
+        psets = [dict(idx=torch.empty(Tc * TOPK, dtype=torch.int32, device="cuda"),
+                      gates=torch.empty(Tc * TOPK, dtype=torch.float64, device="cuda"),
+                      cnt=torch.empty(Tc, dtype=torch.int32, device="cuda"),
+                      out=torch.empty(Tc, D, dtype=torch.float32, device="cuda"))
+                 for _ in range(2)]
+
+        def dbatches(n):
+            sel = [psets[i & 1] for i in range(n)]
+            offs = [(i % (T // Tc)) * Tc * D * 4 for i in range(n)]
+            layer.forward_batches([a1.data_ptr() + o for o in offs],
+                                  [a3.data_ptr() + o for o in offs], None, Tc,
+                                  [b["idx"].data_ptr() for b in sel],
+                                  [b["gates"].data_ptr() for b in sel],
+                                  [b["cnt"].data_ptr() for b in sel],
+                                  [b["out"].data_ptr() for b in sel])
+        with torch.cuda.stream(stream):
+            dbatches(3)
+        ctx.synchronize()
+        ms_cp = max_over_ranks(timed(dbatches, args.steps), ws)
         c1, c2, Sc, hit_c, _ = gemm_algorithmic_bytes(idx_c, Tc)
         tg = (st_c["gemm1_tcgen05"][0] + st_c["gemm2_tcgen05"][0]) / st_c["gemm1_tcgen05"][1]
         config_c = {"workload": "SURVEY config C: LongCat MoE layer decode step, 256 tokens, "
                                 "1xB200 (expert weights streamed from HBM)",
                     "tokens": Tc, "ms_per_step": ms_c, "tokens_per_s": Tc * ws / (ms_c / 1e3),
+                    "pipelined_ms_per_step": ms_cp,
+                    "pipelined_tokens_per_s": Tc * ws / (ms_cp / 1e3),
+                    "pipelined_note": "independent decode micro-batches, scmoe_layer_forward_batches",
                     "ffn_slots": Sc, "experts_hit": hit_c,
                     "gemm_ms_per_step": tg, "gemm_bytes_per_step": c1 + c2,
                     "gemm_achieved_gbs": (c1 + c2) / (tg / 1e3) / 1e9,
@@ -653,6 +677,12 @@ def run_b200(args):
     config_a = None
     if ws == 1 and args.config_a:
         config_a = tiny_config_a(ctx, stream, args.steps * 20, not args.no_cpu_baseline)
+
+    # ---- the full ScMoE layer (Model::build_layer, model.hpp:355-409)
+    # at LongCat widths with the tensor-core MLA, on the same router / experts
+    full_layer = None
+    if ws == 1 and args.full_layer:
+        full_layer = run_full_layer(P, ctx, stream, layer, a1, T, args.steps)
 
     # ---- 4-layer ScMoE stack, 100 router steps of 1024 tokens with
     # PID bias control (K_e = 6, mu = 0.2, decay 0.999); the main layer's
@@ -743,8 +773,74 @@ def run_b200(args):
         "config_a": config_a,
         "tpot": tpot,
         "e5": e5,
+        "full_layer": full_layer,
     }
     emit(line)
+
+
+def run_full_layer(P, ctx, stream, layer, a1, T, steps, seq=4096):
+    """One full ScMoE layer (model.hpp:355-409): a1 = x + MLA1(rmsnorm x);
+    dd = a1 + FFN(rmsnorm a1) (dense_inter 12288); a3 = dd + MLA2(rmsnorm dd);
+    out = a3 + moe(rmsnorm a1) -- LongCat MLA widths (d_q 1536, d_kv 512, 64 heads
+    x (128 + 64)), tensor-core MLA (csrc/mla_tc.cu), T tokens as T/seq causal
+    sequences, device-timed per layer call; the MoE branch alone for scale."""
+    import torch
+    from paper_2509_01322_b200.layer import DenseFFN
+    from paper_2509_01322_b200.mla import MlaParams, ScMoELayer
+    dq, dkv, H, dhc, dhr = 1536, 512, 64, 128, 64
+
+    def mla(seed):
+        ws_ = []
+        for i, (r, c) in enumerate([(D, dq), (dq, H * dhc), (dq, H * dhr), (D, dkv),
+                                    (dkv, H * dhc), (dkv, H * dhc), (D, dhr), (H * dhc, D)]):
+            t = torch.empty(r * c, dtype=torch.float32, device="cuda")
+            ctx._check(P.lib().scmoe_rng_fill_uniform(ctx.handle, P.stream_seed(seed, i), 0, r * c,
+                                                      1.0 / D, t.data_ptr()))
+            ws_.append(t.view(r, c))
+        return MlaParams(D, dq, dkv, H, dhc, dhr, weights=ws_, rope_base=1.0e6,
+                         precision=P.PREC_BF16)
+
+    class _Handle:  # the bench layer's device router / bank
+        def __init__(self, h, top_k=None):
+            self.h, self.top_k = h, top_k
+
+        def device(self, c):
+            return self.h
+
+    dense = DenseFFN(ctx, D, 12288, seed=SEED_W + 3)
+    full = ScMoELayer(mla(SEED_W + 4), mla(SEED_W + 5), dense, _Handle(layer.router, TOPK),
+                      _Handle(layer.bank), *[np.ones(D, np.float32)] * 4, ctx=ctx)
+    x = a1.view(T, D)
+    res = {"workload": "full ScMoE layer (MLA1, dense FFN 12288, MLA2, MoE branch), LongCat "
+                       f"widths, {T} tokens as {T // seq} causal sequences of {seq}, "
+                       "tensor-core MLA (bf16 operands, rel-L2 ~7e-3 vs the exact oracle)"}
+    for overlap in (False, True):
+        with torch.cuda.stream(stream):  # the context's stream: the layer runs there
+            full.forward(x, seq, overlap=overlap)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            n = max(2, steps // 4)
+            e0.record(stream)
+            for _ in range(n):
+                full.forward(x, seq, overlap=overlap)
+            e1.record(stream)
+            e1.synchronize()
+        ms = e0.elapsed_time(e1) / n
+        res["overlap" if overlap else "serial"] = {"ms_per_layer": ms, "tokens_per_s": T / ms * 1e3}
+    ctx.profile(True)
+    ctx.profile_flush()
+    with torch.cuda.stream(stream):
+        full.forward(x, seq, overlap=False)
+    st = ctx.profile_flush()
+    ctx.profile(False)
+    res["stages_ms"] = {k: round(v[0], 3) for k, v in st.items()}
+    moe_keys = ("rmsnorm", "router_gemm", "softmax_topk", "permute", "gather", "gemm1_tcgen05",
+                "gemm2_tcgen05", "combine")
+    moe_ms = sum(st[k][0] for k in moe_keys if k in st)
+    res["moe_branch_ms"] = moe_ms
+    res["layer_over_moe_branch"] = res["serial"]["ms_per_layer"] / moe_ms if moe_ms else None
+    dense.close()
+    return res
 
 
 def run_e5(P, ctx, stream, steps, T=1024, n_layers=4):
@@ -1080,6 +1176,8 @@ def main():
                     help="pipelined EP: small router kernel co-resident with the GEMM")
     ap.add_argument("--tpot-batch", type=int, default=96,
                     help="decode tokens per device for the measured TPOT block (0 = off)")
+    ap.add_argument("--full-layer", type=int, default=1,
+                    help="N=1: time the full ScMoE layer with the tensor-core MLA")
     ap.add_argument("--e5-steps", type=int, default=100,
                     help="N=1: SURVEY E5 4-layer PID stack steps (0 = off)")
     args = ap.parse_args()

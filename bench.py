@@ -716,7 +716,7 @@ def run_b200(args):
     # dram bytes per step of the same kernels from the committed ncu --set full
     # capture (profiles/); compare with algorithmic_bytes_per_step
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "r01c_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "r02_traffic.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath))["dram_bytes_per_step"]
     t_gemm_serial, achieved_serial = gemm_roofline(stages_serial)
@@ -759,7 +759,7 @@ def run_b200(args):
                               "and per-slot rows"),
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": (achieved / hbm_peak) if achieved else None, "traffic": traffic,
-                     "traffic_source": "profiles/r01c_traffic.json (ncu dram__bytes_read+write)",
+                     "traffic_source": "profiles/r02_traffic.json (ncu dram__bytes_read+write of the pair GEMMs)",
                      "algorithmic_bytes_per_step": alg_bytes,
                      "kernel_io_bytes_per_step": g1b + g2b, "ms_per_step": t_gemm,
                      "achieved_serial": achieved_serial, "ms_per_step_serial": t_gemm_serial,

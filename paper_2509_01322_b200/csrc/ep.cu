@@ -677,6 +677,13 @@ int scmoe_ep_layer_forward_batches(scmoe_ep* ep, scmoe_router* r, scmoe_bank* ba
         } restore{c, user, c->overlapped};
         c->stream = ep->s_front;
         c->overlapped = corun_router != 0;
+        // co-residency needs both sides small: the router kernel (front) and the
+        // grouped GEMM's ring (back)
+        struct RestoreB {
+            scmoe_ctx* c;
+            ~RestoreB() { c->corun_gemm = false; }
+        } restore_b{cb};
+        cb->corun_gemm = corun_router != 0;
         for (size_t i = 0; i < n_batches; ++i) {
             const int k = (int)(i & 1);
             EpSet& st = ep->sets[k];

@@ -1072,7 +1072,9 @@ void launch_grouped_gemm_bf16(scmoe_ctx* c, const __nv_bfloat16* W, size_t n_exp
             const char* e = getenv("SCMOE_PAIR_STAGES");
             return e ? atoi(e) : 33;
         }();
-        if (tile_rows == 256)
+        if (tile_rows == 256 && c->corun_gemm)  // 177 KB: fits beside the 25 KB router
+            go2(grouped_gemm_pair_kernel<256, 3, 2>, gemm_pair_smem_bytes<256, 3, 2>());
+        else if (tile_rows == 256)
             go2(grouped_gemm_pair_kernel<256, 3, 3>, gemm_pair_smem_bytes<256, 3, 3>());
         else if (st == 32)
             go2(grouped_gemm_pair_kernel<192, 3, 2>, gemm_pair_smem_bytes<192, 3, 2>());

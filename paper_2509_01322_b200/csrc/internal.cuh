@@ -139,6 +139,9 @@ struct scmoe_ctx {
     // (SCMOE_ROUTER_SMS / SCMOE_GEMM_SMS, or the overlapped schedule's split)
     int router_sms = 0, gemm_sms = 0;
     bool overlapped = false;    // inside a pipelined multi-batch call
+    // this context's grouped GEMMs run beside the co-resident router of another
+    // stream: pick the smaller-footprint ring for 256-token tiles
+    bool corun_gemm = false;
     // pipelined multi-batch execution (scmoe_layer_forward_batches)
     cudaStream_t s_front = nullptr, s_back = nullptr;
     cudaEvent_t ev_front[2] = {nullptr, nullptr}, ev_back[2] = {nullptr, nullptr};

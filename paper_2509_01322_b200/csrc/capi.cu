@@ -1914,20 +1914,34 @@ int scmoe_layer_full_forward(scmoe_ctx* c, scmoe_mla* mla1, scmoe_mla* mla2, scm
             SCMOE_CUDA(cudaStreamWaitEvent(sb, c->ev_full[0], 0));
         }
         c->stream = sb;
+        // overlapped: the MoE branch's exact router is FP32-pipe work; its
+        // small co-resident kernel shares the SMs with the dense / MLA2 GEMMs of
+        // stream a, which take the smaller-footprint ring to leave it room
+        const bool ov_prev = c->overlapped;
+        c->overlapped = overlap != 0;
         try {
             layer_front(c, r, b, a1, norm_moe, T, idx, gates, ffn_count);
+            c->overlapped = ov_prev;
             moe_back(c, b, ws.hmoe.get<float>(T * d), T, idx, gates, r->top_k, renorm, nullptr,
                      nullptr, /*phase=*/1);
         } catch (...) {
             c->stream = sa;
+            c->overlapped = ov_prev;
             throw;
         }
         c->stream = sa;
         // dd = a1 + FFN(rmsnorm(a1)); a3 = dd + MLA2(rmsnorm(dd)) (stream a)
+        struct CorunGuard {
+            scmoe_ctx* c;
+            bool prev;
+            ~CorunGuard() { c->corun_gemm = prev; }
+        } corun_guard{c, c->corun_gemm};
+        c->corun_gemm = overlap != 0;
         run(scmoe_dense_ffn(c, dense, a1, norm_ffn, T, dd));
         launch_rmsnorm(c, dd, norm2, T, d, 1e-6f, xn, nullptr);
         run(scmoe_mla_forward(c, mla2, xn, T, seq_len, m));
         launch_add_f32(c, dd, m, T * d, a3);
+        c->corun_gemm = corun_guard.prev;
         // out = a3 + combine (stream b, after a3)
         if (overlap) {
             SCMOE_CUDA(cudaEventRecord(c->ev_full[1], sa));

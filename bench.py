@@ -639,6 +639,28 @@ def run_b200(args):
                     "gemm_ms_per_step": tg, "gemm_bytes_per_step": c1 + c2,
                     "gemm_achieved_gbs": (c1 + c2) / (tg / 1e3) / 1e9,
                     "stages_ms": {k: round(v[0] / v[1], 4) for k, v in st_c.items()}}
+        # e2e of the decode step through the host tier (pinned buffers, H2D of
+        # the step's a1/a3 and D2H of its output + routing inside the region)
+        hc = [dict(a1=pinned((Tc, D), torch.float32), a3=pinned((Tc, D), torch.float32),
+                   idx=pinned((Tc * TOPK,), torch.int32), gat=pinned((Tc * TOPK,), torch.float64),
+                   cnt=pinned((Tc,), torch.int32), out=pinned((Tc, D), torch.float32))
+              for _ in range(2)]
+        for i, h in enumerate(hc):
+            h["a1"][:] = a1_h.reshape(T, D)[i * Tc:(i + 1) * Tc]
+            h["a3"][:] = a3_h.reshape(T, D)[i * Tc:(i + 1) * Tc]
+
+        def host_dec(n):
+            sl = [hc[i % 2] for i in range(n)]
+            layer.forward_host_batches([h["a1"] for h in sl], [h["a3"] for h in sl], None, Tc,
+                                       [h["idx"] for h in sl], [h["gat"] for h in sl],
+                                       [h["cnt"] for h in sl], [h["out"] for h in sl])
+        host_dec(2)
+        ms_ce = max_over_ranks(timed(host_dec, e_steps), ws)
+        config_c["e2e"] = {"value": Tc * ws / (ms_ce / 1e3), "unit": "tokens/s",
+                           "h2d_bytes_per_step": 2 * Tc * D * 4,
+                           "d2h_bytes_per_step": Tc * D * 4 + Tc * TOPK * (4 + 8) + Tc * 4,
+                           "ms_per_step": ms_ce,
+                           "api": "scmoe_layer_forward_host_batches (pinned host buffers)"}
 
     # ---- TPOT from measured latencies -- one GPU holding all
     # 512 experts serving a decode batch of tpot_batch tokens (the reference
@@ -727,6 +749,11 @@ def run_b200(args):
         except Exception as e:  # reported, not fatal
             cpu = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "reference",
                    "sample": f"failed: {e}"}
+    if config_c and cpu and cpu.get("value"):
+        # the reference's per-token cost (route_topk + moe_forward) does not depend
+        # on the batch size once its per-call weight copy is amortised: the same
+        # sample is the decode step's CPU baseline
+        config_c["cpu_baseline"] = {**cpu, "note": "same per-token sample as the headline line"}
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",

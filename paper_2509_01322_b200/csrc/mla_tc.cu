@@ -18,8 +18,10 @@
 // K-major layout (internal.cuh wblk_index), M padded to a multiple of 256 and
 // K to a multiple of 64 with zeros; sequence lengths are padded to 256 keys.
 #include <cmath>
+#include <cstdlib>
 
 #include "internal.cuh"
+#include "tcgen05_util.cuh"
 
 namespace scmoe {
 
@@ -205,6 +207,307 @@ __global__ void mla_softmax_bf16_kernel(const __nv_bfloat16* __restrict__ S, int
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Fused causal attention (default): one CTA per (sequence b, head h) x 128
+// queries.  Two passes over the key tiles j <= diagonal, both on the tensor
+// cores: pass 1 S = Q K_j^T (TMEM) -> per-row max and normaliser (fp32,
+// exp2 domain); pass 2 recomputes S, writes P = exp(S - max) as bf16 into a
+// 128B-swizzled K-major smem tile and accumulates O += P V_j in TMEM (no
+// rescaling: the max is final); O / l goes straight to the merged rows.  S
+// and P never touch HBM.  Warp roles: 0 TMA producer, 1 MMA issuer (one
+// lane), 2-5 softmax (one query row per thread = one TMEM lane).
+// ---------------------------------------------------------------------------
+// 2^x on the SFU alone (no range fix-up: arguments are <= 0 or -inf here)
+__device__ __forceinline__ float ex2_fast(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ void st_shared_v4(unsigned char* p, uint32_t a, uint32_t b, uint32_t c,
+                                             uint32_t d) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(p)), "r"(a), "r"(b),
+                 "r"(c), "r"(d)
+                 : "memory");
+}
+
+constexpr int FA_BQ = 128, FA_BKEY = 128, FA_KBMAX = 3, FA_DVMAX = 128;
+constexpr int FA_BLK = 128 * 64 * 2;  // one [128 rows][64 cols] bf16 SW128 block (16 KB)
+constexpr int FA_SWARPS = 8;          // softmax warps: 2 per TMEM lane quadrant (64 keys each)
+constexpr int FA_THREADS = (3 + FA_SWARPS) * 32;
+constexpr size_t FA_SMEM = 1024 + FA_KBMAX * FA_BLK /*Q*/ + 2 * FA_KBMAX * FA_BLK /*K ring*/ +
+                           2 * FA_DVMAX * 128 /*V^T: 2 key halves*/ + 2 * FA_BLK /*P*/ +
+                           2 * 2 * FA_BQ * 4 /*row stats*/ + 256;
+
+struct FaArgs {
+    int BH, H, L, Lp, nqt, KB, dv;
+    float scale_log2;
+    __nv_bfloat16* merged;
+    size_t ldm;
+};
+
+// warps: 0 Q + K producer, 1 MMA issuer, 2 V producer, 3..10 softmax (warp w
+// owns TMEM lane quadrant w % 4 and key half (w - 3) / 4 of every tile)
+__global__ void __launch_bounds__(FA_THREADS, 1)
+    mla_flash_kernel(const __grid_constant__ CUtensorMap map_q,
+                     const __grid_constant__ CUtensorMap map_k,
+                     const __grid_constant__ CUtensorMap map_v, const FaArgs a) {
+    extern __shared__ __align__(1024) unsigned char fa_raw[];
+    unsigned char* sm = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(fa_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* Qs = sm;
+    unsigned char* Ks = Qs + FA_KBMAX * FA_BLK;             // [2][KB blocks]
+    unsigned char* Vs = Ks + 2 * FA_KBMAX * FA_BLK;         // [2 halves][dv rows][128 B]
+    unsigned char* Ps = Vs + 2 * FA_DVMAX * 128;            // [2 blocks][128 rows][128 B]
+    float* stat_m = reinterpret_cast<float*>(Ps + 2 * FA_BLK);  // [2 halves][128 rows]
+    float* stat_l = stat_m + 2 * FA_BQ;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(stat_l + 2 * FA_BQ);
+    uint64_t *q_full = bars, *k_full = bars + 1, *k_empty = bars + 3, *v_full = bars + 5,
+             *v_empty = bars + 6, *s_full = bars + 7, *s_empty = bars + 9, *p_full = bars + 11,
+             *p_empty = bars + 12, *o_full = bars + 13;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+
+    // CTAs of one (b, h) are consecutive, so the ~148 resident ones span only a
+    // few heads and their K / V^T tiles stay in L2 (head-strided order thrashed
+    // it: 7 GB of DRAM reads per MLA); heaviest query tile first within a head
+    const int t = a.nqt - 1 - (int)(blockIdx.x % a.nqt);
+    const int bh = (int)(blockIdx.x / a.nqt);
+    const int q0 = t * FA_BQ;
+    const int nj = t + 1;
+    const int KB = a.KB, dv = a.dv;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        mbar_init(q_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&k_full[i], 1);
+            mbar_init(&k_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&s_empty[i], FA_SWARPS);
+        }
+        mbar_init(v_full, 1);
+        mbar_init(v_empty, 1);
+        mbar_init(p_full, FA_SWARPS);
+        mbar_init(p_empty, 1);
+        mbar_init(o_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+            smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;  // S0 cols [0,128), S1 [128,256), O [256, 256 + dv)
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_last();
+            mbar_expect_tx(q_full, (uint32_t)(KB * FA_BLK));
+            for (int kb = 0; kb < KB; ++kb)
+                tma_load_2d(&map_q, q_full, Qs + kb * FA_BLK, kb * 64, bh * a.L + q0, pol);
+            const int krow0 = bh * (a.Lp * KB);  // K blocked layout: rows of 64 elements
+            int ks = 0;
+            uint32_t kph = 0;
+            for (int pass = 0; pass < 2; ++pass)
+                for (int j = 0; j < nj; ++j) {
+                    mbar_wait(&k_empty[ks], kph ^ 1);
+                    mbar_expect_tx(&k_full[ks], (uint32_t)(KB * FA_BLK));
+                    for (int kb = 0; kb < KB; ++kb)
+                        tma_load_2d(&map_k, &k_full[ks], Ks + (ks * FA_KBMAX + kb) * FA_BLK, 0,
+                                    krow0 + (j * KB + kb) * 128, pol);
+                    if (++ks == 2) {
+                        ks = 0;
+                        kph ^= 1;
+                    }
+                }
+        }
+    } else if (warp == 2) {
+        if (lane == 0) {  // V^T tiles of the second pass, their own ring
+            const uint64_t pol = policy_evict_last();
+            uint32_t vph = 0;
+            for (int j = 0; j < nj; ++j) {
+                mbar_wait(v_empty, vph ^ 1);
+                mbar_expect_tx(v_full, (uint32_t)(dv * 256));
+                tma_load_2d(&map_v, v_full, Vs, j * FA_BKEY, bh * dv, pol);
+                tma_load_2d(&map_v, v_full, Vs + dv * 128, j * FA_BKEY + 64, bh * dv, pol);
+                vph ^= 1;
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t id_s = tc::idesc_bf16(128, FA_BKEY), id_o = tc::idesc_bf16(128, dv);
+            int ks = 0, sb = 0;
+            uint32_t kph = 0, sph = 0, pph = 0, vph = 0;
+            auto issue_s = [&]() {
+                mbar_wait(&k_full[ks], kph);
+                mbar_wait(&s_empty[sb], sph ^ 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                for (int kb = 0; kb < KB; ++kb)
+                    for (int k = 0; k < 4; ++k)
+                        tc::mma(tmem + sb * FA_BKEY,
+                                tc::desc_sw128(smem_u32(Qs + kb * FA_BLK) + k * 32),
+                                tc::desc_sw128(smem_u32(Ks + (ks * FA_KBMAX + kb) * FA_BLK) + k * 32),
+                                id_s, (kb | k) != 0);
+                tc::commit(&k_empty[ks]);
+                tc::commit(&s_full[sb]);
+                if (++ks == 2) {
+                    ks = 0;
+                    kph ^= 1;
+                }
+                if (++sb == 2) {
+                    sb = 0;
+                    sph ^= 1;
+                }
+            };
+            mbar_wait(q_full, 0);
+            for (int j = 0; j < nj; ++j) issue_s();  // pass 1: statistics
+            issue_s();                                // pass 2: S_0 ahead
+            for (int j = 0; j < nj; ++j) {
+                if (j + 1 < nj) issue_s();  // S_{j+1} under the softmax of tile j
+                mbar_wait(p_full, pph);
+                mbar_wait(v_full, vph);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                for (int b = 0; b < 2; ++b)
+                    for (int k = 0; k < 4; ++k)
+                        tc::mma(tmem + 2 * FA_BKEY, tc::desc_sw128(smem_u32(Ps + b * FA_BLK) + k * 32),
+                                tc::desc_sw128(smem_u32(Vs + b * dv * 128) + k * 32), id_o,
+                                (j | b | k) != 0);
+                tc::commit(p_empty);
+                tc::commit(v_empty);
+                pph ^= 1;
+                vph ^= 1;
+            }
+            tc::commit(o_full);
+        }
+    } else {
+        const int sw = warp - 3;            // 0..7
+        const int quad = warp & 3;           // TMEM lanes this warp may access
+        const int half = sw >> 2;            // key half [half*64, half*64 + 64) of each tile
+        const int r = quad * 32 + lane;      // query row = TMEM lane
+        const int q = q0 + r;
+        const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+        float m = -INFINITY, l = 0.f;
+        int sb = 0;
+        uint32_t sph = 0, pph = 0;
+        uint32_t v[32];
+        for (int pass = 0; pass < 2; ++pass) {
+            for (int j = 0; j < nj; ++j) {
+                mbar_wait(&s_full[sb], sph);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                uint32_t pw[2][16];  // pass 2: this thread's 64 probabilities, bf16 pairs
+                for (int cc = 0; cc < 2; ++cc) {
+                    const int c = half * 2 + cc;  // 32-key chunk of the tile
+                    tc::ld32(tmem + lane_off + sb * FA_BKEY + c * 32, v);
+                    tc::ld_wait();
+                    const int key0 = j * FA_BKEY + c * 32;
+                    // only the diagonal tile is masked (keys > q); elsewhere every key counts
+                    const bool diag = key0 + 31 > q;
+                    if (pass == 0) {
+                        float cm = -INFINITY;
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            float sv = __uint_as_float(v[i]) * a.scale_log2;
+                            if (diag && key0 + i > q) sv = -INFINITY;
+                            v[i] = __float_as_uint(sv);
+                            cm = fmaxf(cm, sv);
+                        }
+                        const float mn = fmaxf(m, cm);
+                        if (mn != -INFINITY) {
+                            float add = 0.f;
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) add += ex2_fast(__uint_as_float(v[i]) - mn);
+                            l = (m == -INFINITY ? 0.f : l * ex2_fast(m - mn)) + add;
+                            m = mn;
+                        }
+                    } else {
+                        const float nm = -m;
+#pragma unroll
+                        for (int i2 = 0; i2 < 16; ++i2) {
+                            const int i0 = 2 * i2;
+                            float p0 = ex2_fast(fmaf(__uint_as_float(v[i0]), a.scale_log2, nm));
+                            float p1 = ex2_fast(fmaf(__uint_as_float(v[i0 + 1]), a.scale_log2, nm));
+                            if (diag) {
+                                if (key0 + i0 > q) p0 = 0.f;
+                                if (key0 + i0 + 1 > q) p1 = 0.f;
+                            }
+                            const __nv_bfloat162 pk = __floats2bfloat162_rn(p0, p1);
+                            pw[cc][i2] = *reinterpret_cast<const uint32_t*>(&pk);
+                        }
+                    }
+                }
+                if (pass == 1) {
+                    // the exponentials are computed under the previous tile's P.V;
+                    // only the stores wait for the P buffer
+                    mbar_wait(p_empty, pph ^ 1);
+                    unsigned char* rowp = Ps + half * FA_BLK + r * 128;  // block `half`
+#pragma unroll
+                    for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int chunk = cc * 4 + u;
+                            st_shared_v4(rowp + ((chunk ^ (r & 7)) << 4), pw[cc][4 * u],
+                                         pw[cc][4 * u + 1], pw[cc][4 * u + 2], pw[cc][4 * u + 3]);
+                        }
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                if (pass == 1) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&s_empty[sb]);
+                    if (pass == 1) mbar_arrive(p_full);
+                }
+                if (pass == 1) pph ^= 1;
+                if (++sb == 2) {
+                    sb = 0;
+                    sph ^= 1;
+                }
+            }
+            if (pass == 0) {
+                // merge the two key halves' statistics of this row
+                stat_m[half * FA_BQ + r] = m;
+                stat_l[half * FA_BQ + r] = l;
+                asm volatile("bar.sync 1, %0;" ::"n"(FA_SWARPS * 32) : "memory");
+                const float m2 = stat_m[(half ^ 1) * FA_BQ + r], l2 = stat_l[(half ^ 1) * FA_BQ + r];
+                const float mn = fmaxf(m, m2);
+                l = (m == -INFINITY ? 0.f : l * exp2f(m - mn)) +
+                    (m2 == -INFINITY ? 0.f : l2 * exp2f(m2 - mn));
+                m = mn;
+            }
+        }
+        mbar_wait(o_full, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const float inv = 1.f / l;
+        const int b = bh / a.H, h = bh % a.H;
+        __nv_bfloat16* dst = a.merged + ((size_t)b * a.L + q) * a.ldm + (size_t)h * dv;
+        for (int c = half; c < dv / 32; c += 2) {
+            tc::ld32(tmem + lane_off + 2 * FA_BKEY + c * 32, v);
+            tc::ld_wait();
+            if (q < a.L) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    uint32_t w[4];
+#pragma unroll
+                    for (int h2 = 0; h2 < 4; ++h2) {
+                        const int i0 = u * 8 + h2 * 2;
+                        const __nv_bfloat162 pk = __floats2bfloat162_rn(
+                            __uint_as_float(v[i0]) * inv, __uint_as_float(v[i0 + 1]) * inv);
+                        w[h2] = *reinterpret_cast<const uint32_t*>(&pk);
+                    }
+                    *reinterpret_cast<uint4*>(dst + c * 32 + u * 8) = make_uint4(w[0], w[1], w[2], w[3]);
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
 // merged[(b*L + q)][h*dhc + c] = Ot[(bh*dhc + c)][q]: 32x32 tile transpose.
 __global__ void mla_unpack_o_kernel(const __nv_bfloat16* __restrict__ Ot, int H, int L, int Lp,
                                     int dhc, __nv_bfloat16* __restrict__ merged) {
@@ -348,6 +651,39 @@ void mla_forward_tc(scmoe_ctx* c, scmoe_mla* m, const float* h, size_t rows, siz
                 (int)dhc, (int)dhr, (int)Dk, qrows, kblk);
         SCMOE_LAUNCH_CHECK(c);
     }
+    static const bool fused = [] {
+        const char* e = getenv("SCMOE_MLA_ATTN");
+        return !(e && std::string(e) == "gemm");
+    }();
+    if (fused && Dk <= 64 * FA_KBMAX && dhc % 32 == 0 && dhc <= FA_DVMAX) {
+        ProfScope _p(c, "mla_tc_attention");
+        mla_pack_vt_kernel<<<dim3((unsigned)ceil_div(dhc, 32), (unsigned)(Lp / 32), (unsigned)BH),
+                             dim3(32, 8), 0, c->stream>>>(kv, M3, (int)H, (int)L, (int)Lp,
+                                                          (int)dhc, vt);
+        SCMOE_LAUNCH_CHECK(c);
+        const CUtensorMap mq = make_tma_map_2d(qrows, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, BH * L, Dk,
+                                               128, 64, CU_TENSOR_MAP_SWIZZLE_128B);
+        const CUtensorMap mk = make_tma_map_2d(kblk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                               BH * Lp * Dk / 64, 64, 128, 64,
+                                               CU_TENSOR_MAP_SWIZZLE_128B);
+        const CUtensorMap mv = make_tma_map_2d(vt, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, BH * dhc, Lp,
+                                               (uint32_t)dhc, 64, CU_TENSOR_MAP_SWIZZLE_128B);
+        FaArgs fa;
+        fa.BH = (int)BH;
+        fa.H = (int)H;
+        fa.L = (int)L;
+        fa.Lp = (int)Lp;
+        fa.nqt = (int)ceil_div(L, (size_t)FA_BQ);
+        fa.KB = (int)(Dk / 64);
+        fa.dv = (int)dhc;
+        fa.scale_log2 = m->att_scale * 1.4426950408889634f;
+        fa.merged = mg;
+        fa.ldm = H * dhc;
+        ensure_max_dynamic_smem(reinterpret_cast<const void*>(mla_flash_kernel), (int)FA_SMEM,
+                                c->device);
+        mla_flash_kernel<<<(unsigned)(BH * fa.nqt), FA_THREADS, FA_SMEM, c->stream>>>(mq, mk, mv, fa);
+        SCMOE_LAUNCH_CHECK(c);
+    } else {
     {
         ProfScope _p(c, "mla_tc_scores");
         // causal: key blocks above a query tile's last query are skipped
@@ -374,6 +710,7 @@ void mla_forward_tc(scmoe_ctx* c, scmoe_mla* m, const float* h, size_t rows, siz
                               dim3(32, 8), 0, c->stream>>>(ot, (int)H, (int)L, (int)Lp, (int)dhc,
                                                            mg);
         SCMOE_LAUNCH_CHECK(c);
+    }
     }
     ProfScope _p(c, "mla_tc_proj_o");
     launch_grouped_gemm_bf16(c, m->tc_w[3], 1, M4, H * dhc, mg, rows, nullptr, ob, 0, t_rows,

@@ -189,6 +189,48 @@ class ClockSampler:
                 "power_w_max": max(r[2] for r in self.rows)}
 
 
+def energy_block(gpu: int, fn, ms_per_step: float, seconds: float = 1.5):
+    """Energy per step from NVML's total-energy counter (mJ) around ~`seconds`
+    of the same schedule (after the timed region; the counter lags ~0.1 s, so
+    the short timed region itself is not used).  power_floor_ms = J per step /
+    the enforced power limit: the step time a schedule with this energy per
+    step cannot beat on this board; floor / ms_per_step ~ 1 means the step is
+    power-bound, not HBM- or tensor-bound.  None when NVML is absent."""
+    try:
+        import pynvml as n
+        import torch
+        n.nvmlInit()
+        h = n.nvmlDeviceGetHandleByIndex(gpu)
+        limit = n.nvmlDeviceGetEnforcedPowerLimit(h) / 1e3
+        torch.cuda.synchronize()
+        time.sleep(0.3)
+        e, t = n.nvmlDeviceGetTotalEnergyConsumption(h), time.perf_counter()
+        time.sleep(0.7)
+        idle_w = (n.nvmlDeviceGetTotalEnergyConsumption(h) - e) / 1e3 / (time.perf_counter() - t)
+        steps = max(8, int(seconds * 1e3 / ms_per_step))
+        fn(steps)  # same load before the counted run
+        torch.cuda.synchronize()
+        e0, w0 = n.nvmlDeviceGetTotalEnergyConsumption(h), time.perf_counter()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        fn(steps)
+        t1.record()
+        torch.cuda.synchronize()
+        time.sleep(0.25)
+        e1, w1 = n.nvmlDeviceGetTotalEnergyConsumption(h), time.perf_counter()
+        ms = t0.elapsed_time(t1) / steps
+        idle_s = max(0.0, (w1 - w0) - ms * steps / 1e3)
+        j = ((e1 - e0) / 1e3 - idle_w * idle_s) / steps
+        return {"power_limit_w": limit, "idle_w": round(idle_w, 1), "steps": steps,
+                "ms_per_step": round(ms, 4), "j_per_step": round(j, 4),
+                "avg_w": round(j / ms * 1e3, 1), "power_floor_ms": round(j / limit * 1e3, 4),
+                "frac_of_power_bound": round(j / limit * 1e3 / ms, 3),
+                "source": "NVML total energy counter over the run, idle energy of the "
+                          "counter lag subtracted"}
+    except Exception as ex:  # reported, not fatal
+        return {"unavailable": str(ex)[:200]}
+
+
 def nvlink_bytes(gpu: int):
     """Cumulative NVLink data bytes (tx, rx) of one GPU from NVML's throughput
     counters (summed over links), or None when unavailable."""
@@ -552,6 +594,12 @@ def run_b200(args):
     ms_max = max_over_ranks(ms, ws)
     ms_serial_max = max_over_ranks(ms_serial, ws)
     value = T * ws / (ms_max / 1e3)
+    # energy per step of the same schedule (is the step power-bound?)
+    energy = None
+    if ws == 1 and args.energy:
+        with torch.cuda.stream(stream):
+            energy = energy_block(local, batches if pipelined else
+                                  (lambda n: [step(i) for i in range(n)]), ms_max)
 
     # ---- e2e through the host tier (pinned buffers, copies in the region) --
     # scmoe_layer_forward_host_batches: every step copies its a1/a3 in and its
@@ -795,6 +843,7 @@ def run_b200(args):
         "stages_ms": {k: round(v[0] / v[1], 4) for k, v in stages.items()},
         "stages_ms_serial": {k: round(v[0] / v[1], 4) for k, v in stages_serial.items()},
         "clocks": clk.summary(),
+        "energy": energy,
         "cpu_baseline": cpu,
         "config_c": config_c,
         "config_a": config_a,
@@ -1203,6 +1252,8 @@ def main():
                     help="pipelined EP: small router kernel co-resident with the GEMM")
     ap.add_argument("--tpot-batch", type=int, default=96,
                     help="decode tokens per device for the measured TPOT block (0 = off)")
+    ap.add_argument("--energy", type=int, default=1,
+                    help="N=1: NVML energy per step of the headline schedule (~2.5 s)")
     ap.add_argument("--full-layer", type=int, default=1,
                     help="N=1: time the full ScMoE layer with the tensor-core MLA")
     ap.add_argument("--e5-steps", type=int, default=100,

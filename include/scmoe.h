@@ -475,6 +475,11 @@ int scmoe_profile_enable(scmoe_ctx* ctx, int on);
 int scmoe_profile_flush(scmoe_ctx* ctx, int* n_entries);
 int scmoe_profile_entry(scmoe_ctx* ctx, int i, const char** name, double* total_ms,
                         uint64_t* launches);
+/* Record i of the last flush in issue order: its stage name and device
+ * start / end time in ms relative to the flush's first record (a timeline
+ * across streams). */
+int scmoe_profile_span(scmoe_ctx* ctx, int i, const char** name, double* start_ms,
+                       double* end_ms);
 /* out[i] = device instantiation of the glibc-expf restatement used by the
  * softmax and SiLU kernels (bit-exactness check against host libm). */
 int scmoe_debug_expf(scmoe_ctx* ctx, const float* in_dev, float* out_dev, size_t n);

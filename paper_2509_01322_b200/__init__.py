@@ -183,6 +183,8 @@ _PROTOS = {
     "scmoe_rng_fill_uniform": (C.c_int, [_P, _U64, _U64, _SZ, C.c_double, _P]),
     "scmoe_profile_enable": (C.c_int, [_P, C.c_int]),
     "scmoe_profile_flush": (C.c_int, [_P, C.POINTER(C.c_int)]),
+    "scmoe_profile_span": (C.c_int, [_P, C.c_int, C.POINTER(C.c_char_p), C.POINTER(C.c_double),
+                                     C.POINTER(C.c_double)]),
     "scmoe_profile_entry": (C.c_int, [_P, C.c_int, C.POINTER(C.c_char_p), C.POINTER(C.c_double),
                                       C.POINTER(_U64)]),
     "scmoe_debug_expf": (C.c_int, [_P, _P, _P, _SZ]),
@@ -278,6 +280,16 @@ class Context:
                                                   C.byref(cnt)))
             out[name.value.decode()] = (ms.value, int(cnt.value))
         return out
+
+    def profile_spans(self) -> list:
+        """[(stage, start_ms, end_ms)] of the last profile_flush(), issue order."""
+        out, i = [], 0
+        while True:
+            name, a, b = C.c_char_p(), C.c_double(), C.c_double()
+            if lib().scmoe_profile_span(self._h, i, C.byref(name), C.byref(a), C.byref(b)) != 0:
+                return out
+            out.append((name.value.decode(), a.value, b.value))
+            i += 1
 
     def close(self):
         if self._h:

@@ -1255,12 +1255,16 @@ int scmoe_profile_enable(scmoe_ctx* c, int on) {
 int scmoe_profile_flush(scmoe_ctx* c, int* n_entries) {
     return guarded(c, [&] {
         require_ctx(c);
-        SCMOE_CUDA(cudaStreamSynchronize(c->stream));
+        // device-wide: stages recorded on a second stream (overlapped layer)
+        SCMOE_CUDA(cudaDeviceSynchronize());
         Profiler& p = c->prof;
         p.agg.clear();
+        p.spans.clear();
         for (size_t i = 0; i < p.used; ++i) {
-            float ms = 0.f;
+            float ms = 0.f, t0 = 0.f;
             SCMOE_CUDA(cudaEventElapsedTime(&ms, p.recs[i].a, p.recs[i].b));
+            SCMOE_CUDA(cudaEventElapsedTime(&t0, p.recs[0].a, p.recs[i].a));
+            p.spans.push_back(Profiler::Span{p.recs[i].name, (double)t0, (double)t0 + ms});
             ProfAgg* a = nullptr;
             for (auto& x : p.agg)
                 if (x.name == p.recs[i].name) a = &x;
@@ -1283,6 +1287,15 @@ int scmoe_profile_entry(scmoe_ctx* c, int i, const char** name, double* total_ms
         if (name) *name = c->prof.agg[i].name.c_str();
         if (total_ms) *total_ms = c->prof.agg[i].ms;
         if (launches) *launches = c->prof.agg[i].count;
+    });
+}
+
+int scmoe_profile_span(scmoe_ctx* c, int i, const char** name, double* start_ms, double* end_ms) {
+    return guarded(c, [&] {
+        if (i < 0 || (size_t)i >= c->prof.spans.size()) SCMOE_THROW(SCMOE_ERR_PARAMETER, "no such span");
+        if (name) *name = c->prof.spans[i].name.c_str();
+        if (start_ms) *start_ms = c->prof.spans[i].start_ms;
+        if (end_ms) *end_ms = c->prof.spans[i].end_ms;
     });
 }
 
@@ -1900,7 +1913,9 @@ int scmoe_layer_full_forward(scmoe_ctx* c, scmoe_mla* mla1, scmoe_mla* mla2, scm
             // CTA (HBM / tensor bound) shares SMs with an MLA CTA (FP32 pipe)
             int lo = 0, hi = 0;
             SCMOE_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-            SCMOE_CUDA(cudaStreamCreateWithPriority(&c->s_moe, cudaStreamNonBlocking, hi));
+            const char* pe = getenv("SCMOE_MOE_PRIO");
+            const int prio = (pe && pe[0] == 'h') ? hi : lo;
+            SCMOE_CUDA(cudaStreamCreateWithPriority(&c->s_moe, cudaStreamNonBlocking, prio));
             for (auto& e : c->ev_full) SCMOE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         }
         const cudaStream_t sb = overlap ? c->s_moe : sa;

@@ -113,6 +113,11 @@ struct Profiler {
     std::vector<ProfRec> recs;
     size_t used = 0;
     std::vector<ProfAgg> agg;
+    struct Span {
+        std::string name;
+        double start_ms, end_ms;  // relative to the first record of the flush
+    };
+    std::vector<Span> spans;
 };
 
 struct HostStage {

@@ -61,4 +61,8 @@ for overlap in (False, True):
 ctx.profile(True)
 layer.forward(x, seq, overlap=False)
 res["stages_serial_ms"] = {k: round(v[0], 3) for k, v in ctx.profile_flush().items()}
+ctx.profile(True)
+layer.forward(x, seq, overlap=True)
+ctx.profile_flush()
+res["timeline_overlap_ms"] = [(n, round(a, 3), round(b, 3)) for n, a, b in ctx.profile_spans()]
 print(json.dumps(res))

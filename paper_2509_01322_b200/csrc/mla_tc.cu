@@ -210,13 +210,17 @@ __global__ void mla_softmax_bf16_kernel(const __nv_bfloat16* __restrict__ S, int
 
 // ---------------------------------------------------------------------------
 // Fused causal attention (default): one CTA per (sequence b, head h) x 128
-// queries.  Two passes over the key tiles j <= diagonal, both on the tensor
-// cores: pass 1 S = Q K_j^T (TMEM) -> per-row max and normaliser (fp32,
-// exp2 domain); pass 2 recomputes S, writes P = exp(S - max) as bf16 into a
-// 128B-swizzled K-major smem tile and accumulates O += P V_j in TMEM (no
-// rescaling: the max is final); O / l goes straight to the merged rows.  S
-// and P never touch HBM.  Warp roles: 0 TMA producer, 1 MMA issuer (one
-// lane), 2-5 softmax (one query row per thread = one TMEM lane).
+// queries, one pass over the key tiles j <= diagonal on the tensor cores:
+// S_j = Q K_j^T into TMEM (double buffered, S_{j+1} computed under the
+// softmax of tile j), P = exp2(S scale - m_ref) written as bf16 into a
+// 128B-swizzled K-major smem tile, O += P V_j accumulated in TMEM.  The
+// reference max m_ref moves only when a tile's row max exceeds it by more
+// than 8 (exp2 domain), and only then are O (in TMEM, between two P.V MMAs)
+// and l rescaled -- after the first tiles the max has settled.  O / l goes
+// straight to the merged rows; S and P never touch HBM.  Warp roles: 0 Q + K
+// TMA producer, 1 MMA issuer (one lane), 2 V^T producer, 3-10 softmax (two
+// warps per TMEM lane quadrant, 64 keys of every tile each, one query row per
+// thread).
 // ---------------------------------------------------------------------------
 // 2^x on the SFU alone (no range fix-up: arguments are <= 0 or -inf here)
 __device__ __forceinline__ float ex2_fast(float x) {
@@ -237,7 +241,7 @@ constexpr int FA_SWARPS = 8;          // softmax warps: 2 per TMEM lane quadrant
 constexpr int FA_THREADS = (3 + FA_SWARPS) * 32;
 constexpr size_t FA_SMEM = 1024 + FA_KBMAX * FA_BLK /*Q*/ + 2 * FA_KBMAX * FA_BLK /*K ring*/ +
                            2 * FA_DVMAX * 128 /*V^T: 2 key halves*/ + 2 * FA_BLK /*P*/ +
-                           2 * 2 * FA_BQ * 4 /*row stats*/ + 256;
+                           6 * FA_BQ * 4 /*row stats*/ + 256;
 
 struct FaArgs {
     int BH, H, L, Lp, nqt, KB, dv;
@@ -260,7 +264,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
     unsigned char* Vs = Ks + 2 * FA_KBMAX * FA_BLK;         // [2 halves][dv rows][128 B]
     unsigned char* Ps = Vs + 2 * FA_DVMAX * 128;            // [2 blocks][128 rows][128 B]
     float* stat_m = reinterpret_cast<float*>(Ps + 2 * FA_BLK);  // [2 halves][128 rows]
-    float* stat_l = stat_m + 2 * FA_BQ;
+    float* stat_l = stat_m + 4 * FA_BQ;  // stat_m: [2 halves][2 tile parities][128 rows]
     uint64_t* bars = reinterpret_cast<uint64_t*>(stat_l + 2 * FA_BQ);
     uint64_t *q_full = bars, *k_full = bars + 1, *k_empty = bars + 3, *v_full = bars + 5,
              *v_empty = bars + 6, *s_full = bars + 7, *s_empty = bars + 9, *p_full = bars + 11,
@@ -311,18 +315,17 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
             const int krow0 = bh * (a.Lp * KB);  // K blocked layout: rows of 64 elements
             int ks = 0;
             uint32_t kph = 0;
-            for (int pass = 0; pass < 2; ++pass)
-                for (int j = 0; j < nj; ++j) {
-                    mbar_wait(&k_empty[ks], kph ^ 1);
-                    mbar_expect_tx(&k_full[ks], (uint32_t)(KB * FA_BLK));
-                    for (int kb = 0; kb < KB; ++kb)
-                        tma_load_2d(&map_k, &k_full[ks], Ks + (ks * FA_KBMAX + kb) * FA_BLK, 0,
-                                    krow0 + (j * KB + kb) * 128, pol);
-                    if (++ks == 2) {
-                        ks = 0;
-                        kph ^= 1;
-                    }
+            for (int j = 0; j < nj; ++j) {
+                mbar_wait(&k_empty[ks], kph ^ 1);
+                mbar_expect_tx(&k_full[ks], (uint32_t)(KB * FA_BLK));
+                for (int kb = 0; kb < KB; ++kb)
+                    tma_load_2d(&map_k, &k_full[ks], Ks + (ks * FA_KBMAX + kb) * FA_BLK, 0,
+                                krow0 + (j * KB + kb) * 128, pol);
+                if (++ks == 2) {
+                    ks = 0;
+                    kph ^= 1;
                 }
+            }
         }
     } else if (warp == 2) {
         if (lane == 0) {  // V^T tiles of the second pass, their own ring
@@ -363,8 +366,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
                 }
             };
             mbar_wait(q_full, 0);
-            for (int j = 0; j < nj; ++j) issue_s();  // pass 1: statistics
-            issue_s();                                // pass 2: S_0 ahead
+            issue_s();  // S_0 ahead
             for (int j = 0; j < nj; ++j) {
                 if (j + 1 < nj) issue_s();  // S_{j+1} under the softmax of tile j
                 mbar_wait(p_full, pph);
@@ -389,101 +391,109 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         const int r = quad * 32 + lane;      // query row = TMEM lane
         const int q = q0 + r;
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-        float m = -INFINITY, l = 0.f;
+        // m_ref: the row's reference max (exp2 domain) the probabilities of
+        // every tile so far are relative to; both key halves hold the same
+        // value.  It moves only when a tile's max exceeds it by > 8 (P <= 256:
+        // exact enough in bf16 / fp32), and then O and l are rescaled.
+        float m_ref = -INFINITY, l = 0.f;
         int sb = 0;
         uint32_t sph = 0, pph = 0;
-        uint32_t v[32];
-        for (int pass = 0; pass < 2; ++pass) {
-            for (int j = 0; j < nj; ++j) {
-                mbar_wait(&s_full[sb], sph);
+        uint32_t v[2][32];
+        const int pair_bar = 2 + quad;  // named barrier of the two warps sharing these rows
+        for (int j = 0; j < nj; ++j) {
+            mbar_wait(&s_full[sb], sph);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            tc::ld32(tmem + lane_off + sb * FA_BKEY + (half * 2) * 32, v[0]);
+            tc::ld32(tmem + lane_off + sb * FA_BKEY + (half * 2 + 1) * 32, v[1]);
+            tc::ld_wait();
+            // S buffer free as soon as it is in registers
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[sb]);
+            if (++sb == 2) {
+                sb = 0;
+                sph ^= 1;
+            }
+            const int key0 = j * FA_BKEY + half * 64;
+            const bool diag = key0 + 63 > q;  // only the diagonal tile is masked
+            float cm = -INFINITY;
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    float sv = __uint_as_float(v[cc][i]);
+                    if (diag && key0 + cc * 32 + i > q) sv = -INFINITY;
+                    v[cc][i] = __float_as_uint(sv);
+                    cm = fmaxf(cm, sv);
+                }
+            // the row max over both halves (scale_log2 > 0 commutes with max)
+            float* xm = stat_m + (j & 1) * FA_BQ;  // [2 tile parities][128 rows] per half
+            xm[half * 2 * FA_BQ + r] = cm;
+            asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+            cm = fmaxf(cm, xm[(half ^ 1) * 2 * FA_BQ + r]) * a.scale_log2;
+            float alpha = 1.f;
+            const bool move = cm > m_ref + 8.f;  // also true on the first tile (-inf)
+            if (move) {
+                alpha = ex2_fast(m_ref - cm);  // 0 on the first tile
+                l *= alpha;
+                m_ref = cm;
+            }
+            const float nm = -m_ref;
+            uint32_t pw[2][16];
+            float add = 0.f;
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+                for (int i2 = 0; i2 < 16; ++i2) {
+                    const float p0 = ex2_fast(fmaf(__uint_as_float(v[cc][2 * i2]), a.scale_log2, nm));
+                    const float p1 =
+                        ex2_fast(fmaf(__uint_as_float(v[cc][2 * i2 + 1]), a.scale_log2, nm));
+                    add += p0 + p1;
+                    const __nv_bfloat162 pk = __floats2bfloat162_rn(p0, p1);
+                    pw[cc][i2] = *reinterpret_cast<const uint32_t*>(&pk);
+                }
+            l += add;
+            // P.V of tile j-1 has completed once the P buffer is free; O is then
+            // quiescent and may be rescaled in place (rare: the max settles)
+            mbar_wait(p_empty, pph ^ 1);
+            if (move && j > 0) {
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                uint32_t pw[2][16];  // pass 2: this thread's 64 probabilities, bf16 pairs
-                for (int cc = 0; cc < 2; ++cc) {
-                    const int c = half * 2 + cc;  // 32-key chunk of the tile
-                    tc::ld32(tmem + lane_off + sb * FA_BKEY + c * 32, v);
+                for (int c = half; c < dv / 32; c += 2) {
+                    uint32_t o[32];
+                    tc::ld32(tmem + lane_off + 2 * FA_BKEY + c * 32, o);
                     tc::ld_wait();
-                    const int key0 = j * FA_BKEY + c * 32;
-                    // only the diagonal tile is masked (keys > q); elsewhere every key counts
-                    const bool diag = key0 + 31 > q;
-                    if (pass == 0) {
-                        float cm = -INFINITY;
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) {
-                            float sv = __uint_as_float(v[i]) * a.scale_log2;
-                            if (diag && key0 + i > q) sv = -INFINITY;
-                            v[i] = __float_as_uint(sv);
-                            cm = fmaxf(cm, sv);
-                        }
-                        const float mn = fmaxf(m, cm);
-                        if (mn != -INFINITY) {
-                            float add = 0.f;
-#pragma unroll
-                            for (int i = 0; i < 32; ++i) add += ex2_fast(__uint_as_float(v[i]) - mn);
-                            l = (m == -INFINITY ? 0.f : l * ex2_fast(m - mn)) + add;
-                            m = mn;
-                        }
-                    } else {
-                        const float nm = -m;
-#pragma unroll
-                        for (int i2 = 0; i2 < 16; ++i2) {
-                            const int i0 = 2 * i2;
-                            float p0 = ex2_fast(fmaf(__uint_as_float(v[i0]), a.scale_log2, nm));
-                            float p1 = ex2_fast(fmaf(__uint_as_float(v[i0 + 1]), a.scale_log2, nm));
-                            if (diag) {
-                                if (key0 + i0 > q) p0 = 0.f;
-                                if (key0 + i0 + 1 > q) p1 = 0.f;
-                            }
-                            const __nv_bfloat162 pk = __floats2bfloat162_rn(p0, p1);
-                            pw[cc][i2] = *reinterpret_cast<const uint32_t*>(&pk);
-                        }
-                    }
+                    for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                    tc::st32(tmem + lane_off + 2 * FA_BKEY + c * 32, o);
                 }
-                if (pass == 1) {
-                    // the exponentials are computed under the previous tile's P.V;
-                    // only the stores wait for the P buffer
-                    mbar_wait(p_empty, pph ^ 1);
-                    unsigned char* rowp = Ps + half * FA_BLK + r * 128;  // block `half`
-#pragma unroll
-                    for (int cc = 0; cc < 2; ++cc)
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const int chunk = cc * 4 + u;
-                            st_shared_v4(rowp + ((chunk ^ (r & 7)) << 4), pw[cc][4 * u],
-                                         pw[cc][4 * u + 1], pw[cc][4 * u + 2], pw[cc][4 * u + 3]);
-                        }
-                }
-                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                if (pass == 1) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(&s_empty[sb]);
-                    if (pass == 1) mbar_arrive(p_full);
-                }
-                if (pass == 1) pph ^= 1;
-                if (++sb == 2) {
-                    sb = 0;
-                    sph ^= 1;
-                }
+                tc::st_wait();
             }
-            if (pass == 0) {
-                // merge the two key halves' statistics of this row
-                stat_m[half * FA_BQ + r] = m;
-                stat_l[half * FA_BQ + r] = l;
-                asm volatile("bar.sync 1, %0;" ::"n"(FA_SWARPS * 32) : "memory");
-                const float m2 = stat_m[(half ^ 1) * FA_BQ + r], l2 = stat_l[(half ^ 1) * FA_BQ + r];
-                const float mn = fmaxf(m, m2);
-                l = (m == -INFINITY ? 0.f : l * exp2f(m - mn)) +
-                    (m2 == -INFINITY ? 0.f : l2 * exp2f(m2 - mn));
-                m = mn;
-            }
+            unsigned char* rowp = Ps + half * FA_BLK + r * 128;  // block `half`
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int chunk = cc * 4 + u;
+                    st_shared_v4(rowp + ((chunk ^ (r & 7)) << 4), pw[cc][4 * u], pw[cc][4 * u + 1],
+                                 pw[cc][4 * u + 2], pw[cc][4 * u + 3]);
+                }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(p_full);
+            pph ^= 1;
         }
+        // the row normaliser: both halves' partial sums share m_ref
+        stat_l[half * FA_BQ + r] = l;
+        asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+        l += stat_l[(half ^ 1) * FA_BQ + r];
         mbar_wait(o_full, 0);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const float inv = 1.f / l;
         const int b = bh / a.H, h = bh % a.H;
         __nv_bfloat16* dst = a.merged + ((size_t)b * a.L + q) * a.ldm + (size_t)h * dv;
         for (int c = half; c < dv / 32; c += 2) {
-            tc::ld32(tmem + lane_off + 2 * FA_BKEY + c * 32, v);
+            tc::ld32(tmem + lane_off + 2 * FA_BKEY + c * 32, v[0]);
             tc::ld_wait();
             if (q < a.L) {
 #pragma unroll
@@ -493,7 +503,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
                     for (int h2 = 0; h2 < 4; ++h2) {
                         const int i0 = u * 8 + h2 * 2;
                         const __nv_bfloat162 pk = __floats2bfloat162_rn(
-                            __uint_as_float(v[i0]) * inv, __uint_as_float(v[i0 + 1]) * inv);
+                            __uint_as_float(v[0][i0]) * inv, __uint_as_float(v[0][i0 + 1]) * inv);
                         w[h2] = *reinterpret_cast<const uint32_t*>(&pk);
                     }
                     *reinterpret_cast<uint4*>(dst + c * 32 + u * 8) = make_uint4(w[0], w[1], w[2], w[3]);

@@ -416,21 +416,32 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
             }
             const int key0 = j * FA_BKEY + half * 64;
             const bool diag = key0 + 63 > q;  // only the diagonal tile is masked
-            float cm = -INFINITY;
+            if (diag) {  // keys past the query: -inf (p = 0)
+#pragma unroll
+                for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (key0 + cc * 32 + i > q) v[cc][i] = __float_as_uint(-INFINITY);
+            }
+            float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
             for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    float sv = __uint_as_float(v[cc][i]);
-                    if (diag && key0 + cc * 32 + i > q) sv = -INFINITY;
-                    v[cc][i] = __float_as_uint(sv);
-                    cm = fmaxf(cm, sv);
-                }
+                for (int i = 0; i < 32; ++i)
+                    mx[i & 3] = fmaxf(mx[i & 3], __uint_as_float(v[cc][i]));
+            float cm = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
             // the row max over both halves (scale_log2 > 0 commutes with max)
-            float* xm = stat_m + (j & 1) * FA_BQ;  // [2 tile parities][128 rows] per half
-            xm[half * 2 * FA_BQ + r] = cm;
+            const uint32_t xm = smem_u32(stat_m + (j & 1) * FA_BQ);  // [half][parity][row]
+            asm volatile("st.shared.f32 [%0], %1;" ::"r"(xm + (uint32_t)(half * 2 * FA_BQ + r) * 4),
+                         "f"(cm)
+                         : "memory");
             asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
-            cm = fmaxf(cm, xm[(half ^ 1) * 2 * FA_BQ + r]) * a.scale_log2;
+            float cm2;
+            asm volatile("ld.shared.f32 %0, [%1];"
+                         : "=f"(cm2)
+                         : "r"(xm + (uint32_t)((half ^ 1) * 2 * FA_BQ + r) * 4)
+                         : "memory");
+            cm = fmaxf(cm, cm2) * a.scale_log2;
             float alpha = 1.f;
             const bool move = cm > m_ref + 8.f;  // also true on the first tile (-inf)
             if (move) {
@@ -440,7 +451,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
             }
             const float nm = -m_ref;
             uint32_t pw[2][16];
-            float add = 0.f;
+            float add[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
@@ -448,11 +459,12 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
                     const float p0 = ex2_fast(fmaf(__uint_as_float(v[cc][2 * i2]), a.scale_log2, nm));
                     const float p1 =
                         ex2_fast(fmaf(__uint_as_float(v[cc][2 * i2 + 1]), a.scale_log2, nm));
-                    add += p0 + p1;
+                    add[(i2 & 1) * 2] += p0;
+                    add[(i2 & 1) * 2 + 1] += p1;
                     const __nv_bfloat162 pk = __floats2bfloat162_rn(p0, p1);
                     pw[cc][i2] = *reinterpret_cast<const uint32_t*>(&pk);
                 }
-            l += add;
+            l += (add[0] + add[1]) + (add[2] + add[3]);
             // P.V of tile j-1 has completed once the P buffer is free; O is then
             // quiescent and may be rescaled in place (rare: the max settles)
             mbar_wait(p_empty, pph ^ 1);

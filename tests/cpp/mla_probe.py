@@ -35,7 +35,8 @@ for i, (r, c) in enumerate([(d, dq), (dq, H * dhc), (dq, H * dhr), (d, dkv), (dk
     ctx._check(P.lib().scmoe_rng_fill_uniform(ctx.handle, P.stream_seed(3, i), 0, r * c, 1.0 / d,
                                               t.data_ptr()))
     ws.append(t.view(r, c))
-p = MlaParams(d, dq, dkv, H, dhc, dhr, weights=ws, rope_base=1.0e6)
+p = MlaParams(d, dq, dkv, H, dhc, dhr, weights=ws, rope_base=1.0e6,
+              precision=int(os.environ.get("MLA_PREC", "0")))  # 1 = tensor-core bf16
 h = torch.randn(rows, d, device="cuda")
 out = torch.empty(rows, d, device="cuda")
 mla_block(h, p, seq, ctx=ctx, out=out)  # warm-up (workspace growth, rope table)

@@ -231,6 +231,23 @@ def energy_block(gpu: int, fn, ms_per_step: float, seconds: float = 1.5):
         return {"unavailable": str(ex)[:200]}
 
 
+def pcie_h2d_gbs(nbytes: int, reps: int = 5) -> float:
+    """Pinned host -> device copy bandwidth of one nbytes buffer (the e2e
+    tier's bound: every step copies its fp32 inputs over PCIe)."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    d.copy_(h, non_blocking=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        d.copy_(h, non_blocking=True)
+    e1.record()
+    e1.synchronize()
+    return nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
+
+
 def nvlink_bytes(gpu: int):
     """Cumulative NVLink data bytes (tx, rx) of one GPU from NVML's throughput
     counters (summed over links), or None when unavailable."""
@@ -628,6 +645,12 @@ def run_b200(args):
     e2e_val = T * ws / (e2e_ms / 1e3)
     h2d = 2 * T * D * 4
     d2h = T * D * 4 + T * TOPK * (4 + 8) + T * 4
+    h2d_gbs = pcie_h2d_gbs(T * D * 4)
+    e2e_roof = {"bound": "pcie_h2d", "h2d_gbs_measured": h2d_gbs,
+                "floor_ms": h2d / (h2d_gbs * 1e9) * 1e3,
+                "frac": h2d / (h2d_gbs * 1e9) * 1e3 / e2e_ms,
+                "note": "floor = this step's H2D bytes / the pinned H2D bandwidth measured here "
+                        "(the D2H of the outputs shares the link in the other direction)"}
 
     # ---- SURVEY config C (decode: 256 tokens per step, HBM-bound weight
     # streaming) on the same layer, serial steps; reported beside the headline
@@ -822,6 +845,7 @@ def run_b200(args):
                    "mean_ffn_per_token": ffn_mean, "ffn_slots": S, "experts_hit": n_hit},
         "e2e": {"value": e2e_val, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "steps": e_steps,
+                "roofline": e2e_roof,
                 "api": "scmoe_layer_forward_host_batches (pinned host buffers; H2D of step i+1 "
                        "and D2H of step i-1 overlap compute of step i)"},
         "gpu_launches": launches,

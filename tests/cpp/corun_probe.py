@@ -70,36 +70,37 @@ def serial():
                       b["gates"].data_ptr(), b["cnt"].data_ptr(), b["out"].data_ptr())
 
 
-with torch.cuda.stream(stream):
-    pipelined()
-    serial()
-    ctx.synchronize()
-    router_only()
-    moe_only()
-    ctx.synchronize()
-    best = {}
-    for rep in range(REPS):
-        for name, fn in (("pipelined", pipelined), ("serial", serial), ("router_only", router_only),
-                         ("moe_only", moe_only)):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            torch.cuda.profiler.start()
-            e0.record(stream)
-            fn()
-            e1.record(stream)
-            e1.synchronize()
-            torch.cuda.synchronize()
-            torch.cuda.profiler.stop()
-            ms = e0.elapsed_time(e1) / n
-            best[name] = min(best.get(name, 1e9), ms)
-    for name, ms in best.items():
-        print(f"{name}: {ms:.3f} ms per batch" + (f" (min of {REPS})" if REPS > 1 else ""),
-              flush=True)
-    if os.environ.get("PROBE_STAGES"):
-        for name, fn in (("pipelined", pipelined), ("serial", serial)):
-            ctx.profile(True)
-            ctx.profile_flush()
-            fn()
-            st = ctx.profile_flush()
-            ctx.profile(False)
-            print(name, {k: round(v[0] / v[1], 3) for k, v in st.items()}, flush=True)
+if __name__ == "__main__":  # power_probe.py imports the schedules only
+    with torch.cuda.stream(stream):
+        pipelined()
+        serial()
+        ctx.synchronize()
+        router_only()
+        moe_only()
+        ctx.synchronize()
+        best = {}
+        for rep in range(REPS):
+            for name, fn in (("pipelined", pipelined), ("serial", serial), ("router_only", router_only),
+                             ("moe_only", moe_only)):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                torch.cuda.profiler.start()
+                e0.record(stream)
+                fn()
+                e1.record(stream)
+                e1.synchronize()
+                torch.cuda.synchronize()
+                torch.cuda.profiler.stop()
+                ms = e0.elapsed_time(e1) / n
+                best[name] = min(best.get(name, 1e9), ms)
+        for name, ms in best.items():
+            print(f"{name}: {ms:.3f} ms per batch" + (f" (min of {REPS})" if REPS > 1 else ""),
+                  flush=True)
+        if os.environ.get("PROBE_STAGES"):
+            for name, fn in (("pipelined", pipelined), ("serial", serial)):
+                ctx.profile(True)
+                ctx.profile_flush()
+                fn()
+                st = ctx.profile_flush()
+                ctx.profile(False)
+                print(name, {k: round(v[0] / v[1], 3) for k, v in st.items()}, flush=True)

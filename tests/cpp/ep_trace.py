@@ -42,8 +42,9 @@ for _ in range(2):
 torch.cuda.synchronize()
 dist.barrier()
 launches0 = ep.kernel_launches()
+CORUN = bool(int(os.environ.get("EP_CORUN", "0")))  # the co-resident router variant
 with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
-    res = ep.forward_batches([a1] * NB, [a3] * NB, None, T)
+    res = ep.forward_batches([a1] * NB, [a3] * NB, None, T, corun_router=CORUN)
     ep.controller_step(res[-1][1], T, update=True, want_delta=False)
     torch.cuda.synchronize()
 launches = ep.kernel_launches() - launches0
@@ -91,6 +92,15 @@ with open(f"{prefix}_rank{rank}.json", "w") as f:
     json.dump(out, f, indent=1)
 if rank == 0:
     prof.export_chrome_trace(f"{prefix}_rank0.trace.json")
+    # device timeline of the region (kernel, stream, start/end us from the first kernel)
+    ks = sorted((e for e in prof.events() if str(e.device_type).endswith("CUDA")),
+                key=lambda e: e.time_range.start)
+    if ks:
+        t0 = ks[0].time_range.start
+        with open(f"{prefix}_rank0.timeline.txt", "w") as f:
+            for e in ks:
+                f.write(f"{e.time_range.start - t0:9.1f} {e.time_range.end - t0:9.1f} "
+                        f"{e.time_range.elapsed_us():8.1f}  {e.name[:90]}\n")
 print(json.dumps({k: out[k] for k in ("rank", "n_kernel_launches_traced", "n_repo_kernel_launches",
                                       "n_nccl_kernel_launches", "host_syncs_between_launches",
                                       "kernel_launches_counted_by_library")}), flush=True)

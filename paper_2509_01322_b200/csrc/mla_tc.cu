@@ -530,6 +530,281 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+// ---------------------------------------------------------------------------
+// Fused causal attention, two query tiles per CTA (default): tiles tA = 2u and
+// tB = 2u + 1 of one (sequence, head) share every 128-key K and V^T tile they
+// both need (loaded once), and their softmax warp groups ping-pong with the
+// tensor core: while group A turns S_A(j) into probabilities, the MMA lane
+// runs S_B(j); while group B works, P_A(j) V_j and S_A(j+1).  Each softmax
+// thread owns one full query row of its tile (no cross-warp exchange); P is
+// written back as bf16 pairs into the S columns of TMEM and consumed from
+// there by the P.V MMA (A operand in tensor memory), so P touches neither
+// shared memory nor HBM.  TMEM: S_A [0,128), S_B [128,256), O_A
+// [256,256+dv), O_B [384,384+dv).  The tensor pipe executes one thread's MMAs
+// in order and every commit tracks all earlier MMAs: when S_X(j) has landed,
+// P_X(j-1) V_{j-1} has too, so O_X may be rescaled in place (lazy, only when
+// the row max moves by > 8 in the exp2 domain) without a barrier.  Shared
+// memory: Q_A, Q_B (96 KB), 2 K stages (96 KB), one V^T tile (32 KB).
+// Warps: 0 Q + K producer, 1 MMA lane, 2 V^T producer, 3-6 softmax of tile A,
+// 7-10 softmax of tile B.  Measured (clock64 timeline of one CTA, LongCat
+// widths): ~4.6 k cycles per key tile for both query tiles against 2.56 k of
+// tensor work at the dense-MMA floor; the Q.K^T MMAs (both operands in shared
+// memory, 8 KB per 64-cycle MMA) run ~40 % above the floor, and the softmax
+// of one tile (128 exponentials per thread) takes ~1.6 k cycles.  Tried and
+// slower: 64-key tiles with double-buffered S and V (1.10 vs 0.81 ms: twice
+// the MMA issues and handshakes); a quarter of the exponentials on the FMA
+// pipe (polynomial 2^x; no gain, the SFU is not the limiter).
+// ---------------------------------------------------------------------------
+constexpr int F2_THREADS = 11 * 32;
+constexpr size_t F2_SMEM = 1024 + 2 * FA_KBMAX * FA_BLK /*Q_A, Q_B*/ +
+                           2 * FA_KBMAX * FA_BLK /*K ring*/ + 2 * FA_DVMAX * 128 /*V^T*/ + 256;
+
+__global__ void __launch_bounds__(F2_THREADS, 1)
+    mla_flash2_kernel(const __grid_constant__ CUtensorMap map_q,
+                      const __grid_constant__ CUtensorMap map_k,
+                      const __grid_constant__ CUtensorMap map_v, const FaArgs a) {
+    extern __shared__ __align__(1024) unsigned char f2_raw[];
+    unsigned char* sm = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(f2_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* Qs = sm;                          // [tile X][KB blocks]
+    unsigned char* Ks = Qs + 2 * FA_KBMAX * FA_BLK;  // [stage][KB blocks]
+    unsigned char* Vs = Ks + 2 * FA_KBMAX * FA_BLK;  // [key half][dv rows][128 B]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(Vs + 2 * FA_DVMAX * 128);
+    uint64_t *q_full = bars, *k_full = bars + 1, *k_empty = bars + 3, *v_full = bars + 5,
+             *v_empty = bars + 6, *s_full = bars + 7, *p_full = bars + 9, *o_done = bars + 11;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
+
+    // heaviest pair of query tiles first within a head; the CTAs of one head
+    // are consecutive so its K / V^T tiles stay in L2
+    const int npairs = (a.nqt + 1) >> 1;
+    const int u = npairs - 1 - (int)(blockIdx.x % npairs);
+    const int bh = (int)(blockIdx.x / npairs);
+    const int tA = 2 * u, tB = 2 * u + 1;
+    const bool hasB = tB < a.nqt;
+    const int nj = hasB ? tB + 1 : tA + 1;  // key tiles the pair needs
+    const int KB = a.KB, dv = a.dv;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        mbar_init(q_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&k_full[i], 1);
+            mbar_init(&k_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&p_full[i], 4);
+            mbar_init(&o_done[i], 1);
+        }
+        mbar_init(v_full, 1);
+        mbar_init(v_empty, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+            smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_last();
+            const int nq = hasB ? 2 : 1;
+            mbar_expect_tx(q_full, (uint32_t)(nq * KB * FA_BLK));
+            for (int x = 0; x < nq; ++x)
+                for (int kb = 0; kb < KB; ++kb)
+                    tma_load_2d(&map_q, q_full, Qs + (x * FA_KBMAX + kb) * FA_BLK, kb * 64,
+                                bh * a.L + (tA + x) * FA_BQ, pol);
+            const int krow0 = bh * (a.Lp * KB);  // K blocked layout: rows of 64 elements
+            int ks = 0;
+            uint32_t kph = 0;
+            for (int j = 0; j < nj; ++j) {
+                mbar_wait(&k_empty[ks], kph ^ 1);
+                mbar_expect_tx(&k_full[ks], (uint32_t)(KB * FA_BLK));
+                for (int kb = 0; kb < KB; ++kb)
+                    tma_load_2d(&map_k, &k_full[ks], Ks + (ks * FA_KBMAX + kb) * FA_BLK, 0,
+                                krow0 + (j * KB + kb) * 128, pol);
+                if (++ks == 2) {
+                    ks = 0;
+                    kph ^= 1;
+                }
+            }
+        }
+    } else if (warp == 2) {
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_last();
+            uint32_t vph = 0;
+            for (int j = 0; j < nj; ++j) {
+                mbar_wait(v_empty, vph ^ 1);
+                mbar_expect_tx(v_full, (uint32_t)(dv * 256));
+                tma_load_2d(&map_v, v_full, Vs, j * FA_BKEY, bh * dv, pol);
+                tma_load_2d(&map_v, v_full, Vs + dv * 128, j * FA_BKEY + 64, bh * dv, pol);
+                vph ^= 1;
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t id_s = tc::idesc_bf16(128, FA_BKEY), id_o = tc::idesc_bf16(128, dv);
+            const uint64_t qd0 = tc::desc_sw128(smem_u32(Qs)), kd0 = tc::desc_sw128(smem_u32(Ks)),
+                           vd0 = tc::desc_sw128(smem_u32(Vs));
+            int ks = 0;
+            uint32_t kph = 0, vph = 0, pph[2] = {0, 0};
+            // S_X = Q_X K^T of the K tile in stage ks
+            auto issue_s = [&](int x) {
+                for (int kb = 0; kb < KB; ++kb)
+                    tc::mma_k4(tmem + x * 128, qd0 + (uint64_t)(((x * FA_KBMAX + kb) * FA_BLK) >> 4),
+                               kd0 + (uint64_t)(((ks * FA_KBMAX + kb) * FA_BLK) >> 4), id_s, kb != 0);
+                tc::commit(&s_full[x]);
+            };
+            // O_X (+)= P_X V_j, P_X = bf16 pairs in the S_X columns
+            auto issue_pv = [&](int x, int j) {
+                mbar_wait(&p_full[x], pph[x]);
+                pph[x] ^= 1;
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                for (int h = 0; h < 2; ++h)  // the two 64-key halves of V^T
+                    tc::mma_ts_k4(tmem + 256 + x * 128, tmem + x * 128 + h * 32,
+                                  vd0 + (uint64_t)((h * dv * 128) >> 4), id_o, (j | h) != 0);
+                if (j == (x ? tB : tA)) tc::commit(&o_done[x]);  // the tile's last P.V
+            };
+            auto next_k = [&]() {
+                tc::commit(&k_empty[ks]);
+                if (++ks == 2) {
+                    ks = 0;
+                    kph ^= 1;
+                }
+            };
+            mbar_wait(q_full, 0);
+            mbar_wait(&k_full[ks], kph);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            issue_s(0);
+            if (hasB) issue_s(1);
+            next_k();
+            for (int j = 0; j < nj; ++j) {
+                mbar_wait(v_full, vph);
+                vph ^= 1;
+                const bool more = j + 1 < nj;
+                if (j <= tA) issue_pv(0, j);
+                if (more) {
+                    mbar_wait(&k_full[ks], kph);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    if (j + 1 <= tA) issue_s(0);
+                }
+                if (hasB) issue_pv(1, j);
+                tc::commit(v_empty);  // V_{j+1} streams in under S_B(j+1)
+                if (more) {
+                    if (hasB) issue_s(1);
+                    next_k();
+                }
+            }
+        }
+    } else {
+        const int x = (warp - 3) >> 2;  // 0: tile A, 1: tile B
+        if (x == 0 || hasB) {
+            const int quad = warp & 3;  // TMEM lanes this warp may access
+            const int r = quad * 32 + lane;
+            const int tx = x ? tB : tA;
+            const int q = tx * FA_BQ + r;
+            const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+            const uint32_t s_col = tmem + lane_off + x * 128;
+            const uint32_t o_col = tmem + lane_off + 256 + x * 128;
+            float m_ref = -INFINITY, l = 0.f;
+            uint32_t sph = 0;
+            uint32_t v[4][32];
+            for (int j = 0; j <= tx; ++j) {
+                mbar_wait(&s_full[x], sph);
+                sph ^= 1;
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+                for (int c = 0; c < 4; ++c) tc::ld32(s_col + c * 32, v[c]);
+                tc::ld_wait();
+                if (j == tx) {  // the diagonal tile: keys past the query get p = 0
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (c * 32 + i > r) v[c][i] = __float_as_uint(-INFINITY);
+                }
+                float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) mx[i & 3] = fmaxf(mx[i & 3], __uint_as_float(v[c][i]));
+                const float cm = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * a.scale_log2;
+                float alpha = 1.f;
+                const bool move = cm > m_ref + 8.f;  // true on the first tile (m_ref = -inf)
+                if (move) {
+                    alpha = ex2_fast(m_ref - cm);
+                    l *= alpha;
+                    m_ref = cm;
+                }
+                const float nm = -m_ref;
+                float add[4] = {0.f, 0.f, 0.f, 0.f};
+                // P word w = bf16(s[2w]) | bf16(s[2w+1]) << 16, packed in place
+#pragma unroll
+                for (int w = 0; w < 64; ++w) {
+                    const float s0 = __uint_as_float(v[(2 * w) >> 5][(2 * w) & 31]);
+                    const float s1 = __uint_as_float(v[(2 * w + 1) >> 5][(2 * w + 1) & 31]);
+                    const float p0 = ex2_fast(fmaf(s0, a.scale_log2, nm));
+                    const float p1 = ex2_fast(fmaf(s1, a.scale_log2, nm));
+                    add[(w & 1) * 2] += p0;
+                    add[(w & 1) * 2 + 1] += p1;
+                    const __nv_bfloat162 pk = __floats2bfloat162_rn(p0, p1);
+                    v[w >> 5][w & 31] = *reinterpret_cast<const uint32_t*>(&pk);
+                }
+                l += (add[0] + add[1]) + (add[2] + add[3]);
+                if (move && j > 0) {  // O_X is quiescent: P_X(j-1) V landed before S_X(j)
+                    for (int c = 0; c < dv / 32; ++c) {
+                        uint32_t o[32];
+                        tc::ld32(o_col + c * 32, o);
+                        tc::ld_wait();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                        tc::st32(o_col + c * 32, o);
+                    }
+                }
+                tc::st32(s_col, v[0]);
+                tc::st32(s_col + 32, v[1]);
+                tc::st_wait();
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&p_full[x]);
+            }
+            mbar_wait(&o_done[x], 0);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const float inv = 1.f / l;
+            const int bb = bh / a.H, h = bh % a.H;
+            __nv_bfloat16* dst = a.merged + ((size_t)bb * a.L + q) * a.ldm + (size_t)h * dv;
+            for (int c = 0; c < dv / 32; ++c) {
+                tc::ld32(o_col + c * 32, v[0]);
+                tc::ld_wait();
+                if (q < a.L) {
+#pragma unroll
+                    for (int u8 = 0; u8 < 4; ++u8) {
+                        uint32_t w4[4];
+#pragma unroll
+                        for (int h2 = 0; h2 < 4; ++h2) {
+                            const int i0 = u8 * 8 + h2 * 2;
+                            const __nv_bfloat162 pk = __floats2bfloat162_rn(
+                                __uint_as_float(v[0][i0]) * inv, __uint_as_float(v[0][i0 + 1]) * inv);
+                            w4[h2] = *reinterpret_cast<const uint32_t*>(&pk);
+                        }
+                        *reinterpret_cast<uint4*>(dst + c * 32 + u8 * 8) =
+                            make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                    }
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
 // merged[(b*L + q)][h*dhc + c] = Ot[(bh*dhc + c)][q]: 32x32 tile transpose.
 __global__ void mla_unpack_o_kernel(const __nv_bfloat16* __restrict__ Ot, int H, int L, int Lp,
                                     int dhc, __nv_bfloat16* __restrict__ merged) {
@@ -701,9 +976,21 @@ void mla_forward_tc(scmoe_ctx* c, scmoe_mla* m, const float* h, size_t rows, siz
         fa.scale_log2 = m->att_scale * 1.4426950408889634f;
         fa.merged = mg;
         fa.ldm = H * dhc;
-        ensure_max_dynamic_smem(reinterpret_cast<const void*>(mla_flash_kernel), (int)FA_SMEM,
-                                c->device);
-        mla_flash_kernel<<<(unsigned)(BH * fa.nqt), FA_THREADS, FA_SMEM, c->stream>>>(mq, mk, mv, fa);
+        static const bool one_tile = [] {
+            const char* e = getenv("SCMOE_MLA_ATTN");
+            return e && std::string(e) == "flash1";
+        }();
+        if (one_tile) {
+            ensure_max_dynamic_smem(reinterpret_cast<const void*>(mla_flash_kernel), (int)FA_SMEM,
+                                    c->device);
+            mla_flash_kernel<<<(unsigned)(BH * fa.nqt), FA_THREADS, FA_SMEM, c->stream>>>(mq, mk,
+                                                                                          mv, fa);
+        } else {
+            ensure_max_dynamic_smem(reinterpret_cast<const void*>(mla_flash2_kernel), (int)F2_SMEM,
+                                    c->device);
+            mla_flash2_kernel<<<(unsigned)(BH * ((fa.nqt + 1) / 2)), F2_THREADS, F2_SMEM,
+                                c->stream>>>(mq, mk, mv, fa);
+        }
         SCMOE_LAUNCH_CHECK(c);
     } else {
     {

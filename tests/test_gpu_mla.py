@@ -170,6 +170,67 @@ def test_full_scmoe_layer(scmoe, orc, renorm):
     assert O.rel_l2(out, out_w) <= 5e-3
 
 
+def test_full_scmoe_layer_tensor_core_mla(scmoe, orc):
+    """The full layer with the tensor-core MLA (fused tcgen05 attention, two
+    query tiles per CTA at seq 260): a1 and a3 within the MLA's bf16 tolerance
+    of the exact oracle; the MoE branch teacher-forced on the GPU's own a1 /
+    a3 is bit-exact in routing and within 5e-3 in output; overlapped ==
+    serial bitwise."""
+    P = scmoe
+    from paper_2509_01322_b200.layer import DenseFFN
+    from paper_2509_01322_b200.mla import MlaParams, ScMoELayer
+    d, dq, dkv, H, dhc, dhr, seq, nseq = 256, 64, 64, 4, 32, 16, 260, 2
+    N, Z, K, KE, I, DI = 8, 4, 3, 2, 256, 512
+    T = seq * nseq
+    dims = (d, dq, dkv, H, dhc, dhr)
+    ctx = P.Context(0)
+    w1 = O.mla_weights(*dims, seed=31)
+    w2 = O.mla_weights(*dims, seed=32)
+    dw_in = O.bf16_round(O.uniform_f32(O.stream_seed(33, 0), d * DI, 1.0 / d)).reshape(d, DI)
+    dw_out = O.bf16_round(O.uniform_f32(O.stream_seed(33, 1), DI * d, 1.0 / d)).reshape(DI, d)
+    wr = O.uniform_f32(O.stream_seed(34, 0), d * (N + Z), 1.0 / d).reshape(d, N + Z)
+    ew_in = [O.bf16_round(O.uniform_f32(O.stream_seed(35, 2 * e), d * I, 1.0 / d)).reshape(d, I)
+             for e in range(N)]
+    ew_out = [O.bf16_round(O.uniform_f32(O.stream_seed(35, 2 * e + 1), I * d, 1.0 / d)).reshape(I, d)
+              for e in range(N)]
+    norms = [(1.0 + 0.1 * O.normal_f32(36 + i, d)).astype(np.float32) for i in range(4)]
+    x = O.normal_f32(O.stream_seed(37, 0), T * d).reshape(T, d)
+    layer = ScMoELayer(MlaParams(*dims, weights=w1, rope_base=1.0e4, precision=P.PREC_BF16),
+                       MlaParams(*dims, weights=w2, rope_base=1.0e4, precision=P.PREC_BF16),
+                       DenseFFN(ctx, d, DI, w_in=dw_in, w_out=dw_out),
+                       P.RouterState(wr, N, Z, K, KE, 0.0, 1.0),
+                       P.ExpertBank(ew_in, ew_out, precision=P.PREC_BF16), *norms, ctx=ctx)
+    out, idx, gates, cnt, a1, a3 = layer.forward(x, seq, overlap=True, want_intermediates=True)
+    out0, idx0, _, _ = layer.forward(x, seq, overlap=False)
+    assert out.tobytes() == out0.tobytes() and idx.tobytes() == idx0.tobytes()
+
+    def rms(v, g):
+        o = np.empty_like(v)
+        orc.orc_rmsnorm_f32(O.ptr(v), O.ptr(g), v.shape[0], d, np.float32(1e-6), O.ptr(o))
+        return o
+    _, m1 = O.mla_forward(orc, dims, w1, rms(x, norms[0]), seq)
+    a1_w = x + m1
+    assert O.rel_l2(a1 - x, a1_w - x) <= TC_TOL
+    # dense branch + MLA2 on the GPU's own a1 (teacher-forced)
+    dd_w = np.empty_like(x)
+    assert orc.orc_dense_branch_f32(O.ptr(a1), O.ptr(norms[1]), T, d, O.ptr(dw_in),
+                                    O.ptr(dw_out), DI, O.ptr(dd_w)) == 0
+    _, m2 = O.mla_forward(orc, dims, w2, rms(dd_w, norms[2]), seq)
+    assert O.rel_l2(a3 - a1, dd_w + m2 - a1) <= TC_TOL
+    # the MoE branch on the GPU's a1 / a3: routing bit-exact
+    idx_w = np.empty(T * K, np.uint32)
+    g_w = np.empty(T * K)
+    c_w = np.empty(T, np.uint32)
+    out_w = np.empty_like(x)
+    assert orc.orc_scmoe_layer_f32(O.ptr(a1), O.ptr(a3), O.ptr(norms[3]), T, d, O.ptr(wr), N,
+                                   Z, K, KE, 0.0, O.ptr(np.zeros(N + Z)), O.ptr_array(ew_in),
+                                   O.ptr_array(ew_out), I, 1.0, 1.0, 0, O.ptr(idx_w),
+                                   O.ptr(g_w), O.ptr(c_w), O.ptr(out_w)) == 0
+    assert idx.tobytes() == idx_w.tobytes() and gates.tobytes() == g_w.tobytes()
+    assert cnt.tobytes() == c_w.tobytes()
+    assert O.rel_l2(out - a3, out_w - a3) <= 5e-3
+
+
 TC_SHAPES = [
     # (d, dq, dkv, H, dhc, dhr, seq_len, n_seq): d, dq, dkv, H*dhc multiples of 64
     (256, 64, 64, 4, 32, 16, 96, 3),      # one 256-key block, partial

@@ -332,7 +332,8 @@ void launch_row_tiles(scmoe_ctx* c, size_t rows, int tile_rows, TokenTile* tiles
 void launch_add_bf16_residual(scmoe_ctx* c, const float* a, const __nv_bfloat16* y, size_t n,
                               float* out);
 void launch_f32_to_bf16_t(scmoe_ctx* c, const float* src, size_t rows, size_t cols,
-                          __nv_bfloat16* dst_t);
+                          __nv_bfloat16* dst_t, int n_a = 0, float alpha_a = 1.f, int n_b = 0,
+                          float alpha_b = 1.f);
 
 // tcgen05 grouped GEMM (gemm_sm100.cu).  D^T = W x X^T per expert tile:
 //   out[pos, m] = epi( sum_k W[e][m][k] * X[pos][k] ),  epi = silu or identity,

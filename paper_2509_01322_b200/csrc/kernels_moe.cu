@@ -733,7 +733,8 @@ void launch_uniform_init_bf16_t(scmoe_ctx* c, uint64_t seed, size_t rows, size_t
 }
 
 __global__ void f32_to_bf16_t_kernel(const float* __restrict__ src, int rows, int cols,
-                                     __nv_bfloat16* __restrict__ dst_t) {
+                                     __nv_bfloat16* __restrict__ dst_t, int n_a, float alpha_a,
+                                     int n_b, float alpha_b) {
     __shared__ float tile[32][33];
     const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
     for (int i = threadIdx.y; i < 32; i += blockDim.y) {
@@ -743,14 +744,20 @@ __global__ void f32_to_bf16_t_kernel(const float* __restrict__ src, int rows, in
     __syncthreads();
     for (int i = threadIdx.y; i < 32; i += blockDim.y) {
         const int cc = c0 + i, r = r0 + threadIdx.x;
-        if (r < rows && cc < cols) dst_t[wblk_index(cc, r, rows)] = __float2bfloat16_rn(tile[threadIdx.x][i]);
+        if (r < rows && cc < cols) {
+            // optional column scales (folded output scalings): [0, n_a) by
+            // alpha_a, [n_a, n_a + n_b) by alpha_b
+            const float sc = cc < n_a ? alpha_a : (cc < n_a + n_b ? alpha_b : 1.f);
+            dst_t[wblk_index(cc, r, rows)] = __float2bfloat16_rn(tile[threadIdx.x][i] * sc);
+        }
     }
 }
 
 void launch_f32_to_bf16_t(scmoe_ctx* c, const float* src, size_t rows, size_t cols,
-                          __nv_bfloat16* dst_t) {
+                          __nv_bfloat16* dst_t, int n_a, float alpha_a, int n_b, float alpha_b) {
     dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32));
-    f32_to_bf16_t_kernel<<<grid, dim3(32, 8), 0, c->stream>>>(src, (int)rows, (int)cols, dst_t);
+    f32_to_bf16_t_kernel<<<grid, dim3(32, 8), 0, c->stream>>>(src, (int)rows, (int)cols, dst_t,
+                                                               n_a, alpha_a, n_b, alpha_b);
     SCMOE_LAUNCH_CHECK(c);
 }
 

@@ -29,52 +29,31 @@ namespace {
 
 size_t pad_to(size_t x, size_t m) { return (x + m - 1) / m * m; }
 
-// cols [0, n_a) *= alpha_a, [n_a, n_a + n_b) *= alpha_b, cols [rc, rc + heads*hd)
-// rotated per head at pos = r % seq_len (tensor.hpp:207-215), bf16 in place.
-__global__ void mla_scale_rope_bf16_kernel(__nv_bfloat16* __restrict__ X, size_t ld, size_t rows,
-                                           int n_a, float alpha_a, int n_b, float alpha_b, int rc,
-                                           int heads, int hd, const float2* __restrict__ table,
-                                           size_t seq_len) {
-    const int half = hd / 2;
-    const size_t per_row = (size_t)n_a + n_b + (size_t)heads * half;
-    const size_t n = rows * per_row;
-    for (size_t it = blockIdx.x * (size_t)blockDim.x + threadIdx.x; it < n;
-         it += (size_t)gridDim.x * blockDim.x) {
-        const size_t r = it / per_row;
-        size_t c = it % per_row;
-        __nv_bfloat16* row = X + r * ld;
-        if (c < (size_t)n_a) {
-            row[c] = __float2bfloat16_rn(__bfloat162float(row[c]) * alpha_a);
-        } else if (c < (size_t)(n_a + n_b)) {
-            row[c] = __float2bfloat16_rn(__bfloat162float(row[c]) * alpha_b);
-        } else {
-            c -= n_a + n_b;
-            const int h = (int)(c / half), p = (int)(c % half);
-            const float2 cs = table[(r % seq_len) * half + p];
-            __nv_bfloat16* q = row + rc + h * hd + 2 * p;
-            const float a = __bfloat162float(q[0]), b = __bfloat162float(q[1]);
-            q[0] = __float2bfloat16_rn(a * cs.x - b * cs.y);
-            q[1] = __float2bfloat16_rn(a * cs.y + b * cs.x);
-        }
-    }
+// Qrows[(bh*L + q)][t] = [qc_h | rope(qr_h) | 0] of token b*L + q;
+// Kblk[bh] (blocked, Lp x Dk) row key = [kc_h | rope(kr) | 0] of token b*L + key
+// (0 past L).  The rotary halves are rotated here (pair (2p, 2p+1) by the
+// angle of position q and frequency p, rope table [pos][dhr/2] of (cos, sin)),
+// so the projections need no separate rope pass.  Index math in 32 bits (the
+// host checks BH * Lp * Dk < 2^31).
+__device__ __forceinline__ void rope_pair(float& a, float& b, float2 cs) {
+    const float x = a * cs.x - b * cs.y, y = a * cs.y + b * cs.x;
+    a = x;
+    b = y;
 }
-
-// Qrows[(bh*L + q)][t] = [qc_h | qr_h | 0] of token b*L + q;
-// Kblk[bh] (blocked, Lp x Dk) row key = [kc_h | kr | 0] of token b*L + key (0 past L).
 __global__ void mla_pack_qk_kernel(const __nv_bfloat16* __restrict__ Q, size_t ldq,
                                    const __nv_bfloat16* __restrict__ KV, size_t ldkv,
                                    const __nv_bfloat16* __restrict__ P1, size_t ldp1, int kr_col,
                                    int BH, int H, int L, int Lp, int dhc, int dhr, int Dk,
+                                   const float2* __restrict__ rope,
                                    __nv_bfloat16* __restrict__ Qrows,
                                    __nv_bfloat16* __restrict__ Kblk) {
-    const size_t n = (size_t)BH * Lp * Dk;
+    const int n = BH * Lp * Dk;
     const __nv_bfloat16 zero = __float2bfloat16_rn(0.f);
-    for (size_t it = blockIdx.x * (size_t)blockDim.x + threadIdx.x; it < n;
-         it += (size_t)gridDim.x * blockDim.x) {
-        const int t = (int)(it % Dk);
-        const size_t row = it / Dk;
-        const int j = (int)(row % Lp);
-        const int bh = (int)(row / Lp), b = bh / H, h = bh % H;
+    for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < n; it += gridDim.x * blockDim.x) {
+        const int t = it % Dk;
+        const int row = it / Dk;
+        const int j = row % Lp;
+        const int bh = row / Lp, b = bh / H, h = bh % H;
         const size_t tok = (size_t)b * L + j;
         __nv_bfloat16 kv = zero, qv = zero;
         if (j < L) {
@@ -82,8 +61,16 @@ __global__ void mla_pack_qk_kernel(const __nv_bfloat16* __restrict__ Q, size_t l
                 kv = KV[tok * ldkv + (size_t)h * dhc + t];
                 qv = Q[tok * ldq + (size_t)h * dhc + t];
             } else if (t < dhc + dhr) {
-                kv = P1[tok * ldp1 + kr_col + (t - dhc)];
-                qv = Q[tok * ldq + (size_t)H * dhc + (size_t)h * dhr + (t - dhc)];
+                const int e = t - dhc, e0 = e & ~1;
+                const float2 cs = rope[(size_t)j * (dhr / 2) + e0 / 2];
+                const __nv_bfloat16* kp = P1 + tok * ldp1 + kr_col + e0;
+                const __nv_bfloat16* qp = Q + tok * ldq + (size_t)H * dhc + (size_t)h * dhr + e0;
+                float ka = __bfloat162float(kp[0]), kb = __bfloat162float(kp[1]);
+                float qa = __bfloat162float(qp[0]), qb = __bfloat162float(qp[1]);
+                rope_pair(ka, kb, cs);
+                rope_pair(qa, qb, cs);
+                kv = __float2bfloat16_rn(e & 1 ? kb : ka);
+                qv = __float2bfloat16_rn(e & 1 ? qb : qa);
             }
             Qrows[((size_t)bh * L + j) * Dk + t] = qv;
         }
@@ -96,16 +83,16 @@ __global__ void mla_pack_qk8_kernel(const __nv_bfloat16* __restrict__ Q, size_t 
                                     const __nv_bfloat16* __restrict__ KV, size_t ldkv,
                                     const __nv_bfloat16* __restrict__ P1, size_t ldp1, int kr_col,
                                     int BH, int H, int L, int Lp, int dhc, int dhr, int Dk,
+                                    const float2* __restrict__ rope,
                                     __nv_bfloat16* __restrict__ Qrows,
                                     __nv_bfloat16* __restrict__ Kblk) {
     const int Dk8 = Dk / 8;
-    const size_t n = (size_t)BH * Lp * Dk8;
-    for (size_t it = blockIdx.x * (size_t)blockDim.x + threadIdx.x; it < n;
-         it += (size_t)gridDim.x * blockDim.x) {
-        const int t = (int)(it % Dk8) * 8;
-        const size_t row = it / Dk8;
-        const int j = (int)(row % Lp);
-        const int bh = (int)(row / Lp), b = bh / H, h = bh % H;
+    const int n = BH * Lp * Dk8;
+    for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < n; it += gridDim.x * blockDim.x) {
+        const int t = (it % Dk8) * 8;
+        const int row = it / Dk8;
+        const int j = row % Lp;
+        const int bh = row / Lp, b = bh / H, h = bh % H;
         const size_t tok = (size_t)b * L + j;
         uint4 kv = make_uint4(0, 0, 0, 0), qv = make_uint4(0, 0, 0, 0);
         if (j < L) {
@@ -116,6 +103,19 @@ __global__ void mla_pack_qk8_kernel(const __nv_bfloat16* __restrict__ Q, size_t 
                 kv = *reinterpret_cast<const uint4*>(P1 + tok * ldp1 + kr_col + (t - dhc));
                 qv = *reinterpret_cast<const uint4*>(Q + tok * ldq + (size_t)H * dhc +
                                                      (size_t)h * dhr + (t - dhc));
+                const float2* cs = rope + (size_t)j * (dhr / 2) + (t - dhc) / 2;
+                __nv_bfloat162* k2 = reinterpret_cast<__nv_bfloat162*>(&kv);
+                __nv_bfloat162* q2 = reinterpret_cast<__nv_bfloat162*>(&qv);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float2 c = cs[u];
+                    float ka = __low2float(k2[u]), kb = __high2float(k2[u]);
+                    float qa = __low2float(q2[u]), qb = __high2float(q2[u]);
+                    rope_pair(ka, kb, c);
+                    rope_pair(qa, qb, c);
+                    k2[u] = __floats2bfloat162_rn(ka, kb);
+                    q2[u] = __floats2bfloat162_rn(qa, qb);
+                }
             }
             *reinterpret_cast<uint4*>(Qrows + ((size_t)bh * L + j) * Dk + t) = qv;
         }
@@ -880,7 +880,12 @@ void mla_prepare_tc(scmoe_ctx* c, scmoe_mla* m) {
         if (!m->tc_w[i]) SCMOE_CUDA(cudaMalloc(&m->tc_w[i], M * Ks[i] * sizeof(__nv_bfloat16)));
         SCMOE_CUDA(cudaMemsetAsync(m->tc_w[i], 0, M * Ks[i] * sizeof(__nv_bfloat16), c->stream));
         // src [K][N] row-major -> blocked W[m = n][k]
-        launch_f32_to_bf16_t(c, src[i], Ks[i], Ns[i], m->tc_w[i]);
+        // the latent scalings (cq * alpha_q, ckv * alpha_kv) fold into W_h's columns
+        if (i == 0)
+            launch_f32_to_bf16_t(c, src[i], Ks[i], Ns[i], m->tc_w[i], (int)m->dq, m->alpha_q,
+                                 (int)m->dkv, m->alpha_kv);
+        else
+            launch_f32_to_bf16_t(c, src[i], Ks[i], Ns[i], m->tc_w[i]);
     }
     m->tc_dirty = false;
 }
@@ -893,6 +898,8 @@ void mla_forward_tc(scmoe_ctx* c, scmoe_mla* m, const float* h, size_t rows, siz
     const size_t B = rows / L, BH = B * H;
     const size_t M1 = m->tc_M[0], M2 = m->tc_M[1], M3 = m->tc_M[2], M4 = m->tc_M[3];
     const size_t Lp = pad_to(L, 256), Dk = pad_to(dhc + dhr, 64);
+    if (BH * Lp * Dk >= (size_t(1) << 31))
+        SCMOE_THROW(SCMOE_ERR_CONFIG, "mla: tensor-core path limited to B*H*L*(dhc+dhr) < 2^31");
     const int TR = grouped_gemm_tile_rows_large();
     __nv_bfloat16* xb = ws.mtc_x.get<__nv_bfloat16>(rows * d);
     __nv_bfloat16* p1 = ws.mtc_p1.get<__nv_bfloat16>(rows * M1);
@@ -900,10 +907,7 @@ void mla_forward_tc(scmoe_ctx* c, scmoe_mla* m, const float* h, size_t rows, siz
     __nv_bfloat16* kv = ws.mtc_kv.get<__nv_bfloat16>(rows * M3);
     __nv_bfloat16* qrows = ws.mtc_qr.get<__nv_bfloat16>(BH * L * Dk);
     __nv_bfloat16* kblk = ws.mtc_kb.get<__nv_bfloat16>(BH * Lp * Dk);
-    __nv_bfloat16* S = ws.mtc_s.get<__nv_bfloat16>(BH * L * Lp);
-    __nv_bfloat16* P = ws.mtc_p.get<__nv_bfloat16>(BH * Lp * Lp);
     __nv_bfloat16* vt = ws.mtc_vt.get<__nv_bfloat16>(BH * dhc * Lp);
-    __nv_bfloat16* ot = ws.mtc_ot.get<__nv_bfloat16>(BH * dhc * Lp);
     __nv_bfloat16* mg = ws.mtc_mg.get<__nv_bfloat16>(rows * H * dhc);
     __nv_bfloat16* ob = ws.mtc_o.get<__nv_bfloat16>(rows * M4);
     size_t mt_rows = 0, mt_s = 0, mt_pv = 0;
@@ -914,20 +918,14 @@ void mla_forward_tc(scmoe_ctx* c, scmoe_mla* m, const float* h, size_t rows, siz
     {
         ProfScope _p(c, "mla_tc_proj_h");
         launch_cast_bf16(c, h, rows * d, xb);
+        // alpha_q / alpha_kv are folded into W_h; rope is applied by the packing
         launch_grouped_gemm_bf16(c, m->tc_w[0], 1, M1, d, xb, rows, nullptr, p1, 0, t_rows, n_rows,
                                  mt_rows, TR);
-        mla_scale_rope_bf16_kernel<<<gs(c, rows * (dq + dkv + dhr / 2)), 256, 0, c->stream>>>(
-            p1, M1, rows, (int)dq, m->alpha_q, (int)dkv, m->alpha_kv, (int)(dq + dkv), 1, (int)dhr,
-            rope, L);
-        SCMOE_LAUNCH_CHECK(c);
     }
     {
         ProfScope _p(c, "mla_tc_proj_q");
         launch_grouped_gemm_bf16(c, m->tc_w[1], 1, M2, dq, p1, rows, nullptr, qb, 0, t_rows, n_rows,
                                  mt_rows, TR, nullptr, nullptr, M1);
-        mla_scale_rope_bf16_kernel<<<gs(c, rows * H * (dhr / 2)), 256, 0, c->stream>>>(
-            qb, M2, rows, 0, 1.f, 0, 1.f, (int)(H * dhc), (int)H, (int)dhr, rope, L);
-        SCMOE_LAUNCH_CHECK(c);
     }
     {
         ProfScope _p(c, "mla_tc_proj_kv");
@@ -941,11 +939,11 @@ void mla_forward_tc(scmoe_ctx* c, scmoe_mla* m, const float* h, size_t rows, siz
         if (dhc % 8 == 0 && dhr % 8 == 0 && (dq + dkv) % 8 == 0)
             mla_pack_qk8_kernel<<<gs(c, BH * Lp * Dk / 8), 256, 0, c->stream>>>(
                 qb, M2, kv, M3, p1, M1, (int)(dq + dkv), (int)BH, (int)H, (int)L, (int)Lp,
-                (int)dhc, (int)dhr, (int)Dk, qrows, kblk);
+                (int)dhc, (int)dhr, (int)Dk, rope, qrows, kblk);
         else
             mla_pack_qk_kernel<<<gs(c, BH * Lp * Dk), 256, 0, c->stream>>>(
                 qb, M2, kv, M3, p1, M1, (int)(dq + dkv), (int)BH, (int)H, (int)L, (int)Lp,
-                (int)dhc, (int)dhr, (int)Dk, qrows, kblk);
+                (int)dhc, (int)dhr, (int)Dk, rope, qrows, kblk);
         SCMOE_LAUNCH_CHECK(c);
     }
     static const bool fused = [] {
@@ -993,6 +991,10 @@ void mla_forward_tc(scmoe_ctx* c, scmoe_mla* m, const float* h, size_t rows, siz
         }
         SCMOE_LAUNCH_CHECK(c);
     } else {
+    // the unfused path materialises S and P (BH x Lp^2 each: GBs at long L)
+    __nv_bfloat16* S = ws.mtc_s.get<__nv_bfloat16>(BH * L * Lp);
+    __nv_bfloat16* P = ws.mtc_p.get<__nv_bfloat16>(BH * Lp * Lp);
+    __nv_bfloat16* ot = ws.mtc_ot.get<__nv_bfloat16>(BH * dhc * Lp);
     {
         ProfScope _p(c, "mla_tc_scores");
         // causal: key blocks above a query tile's last query are skipped

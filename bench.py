@@ -231,21 +231,27 @@ def energy_block(gpu: int, fn, ms_per_step: float, seconds: float = 1.5):
         return {"unavailable": str(ex)[:200]}
 
 
-def pcie_h2d_gbs(nbytes: int, reps: int = 5) -> float:
+def pcie_h2d_gbs(nbytes: int, reps: int = 4, trials: int = 3) -> float:
     """Pinned host -> device copy bandwidth of one nbytes buffer (the e2e
-    tier's bound: every step copies its fp32 inputs over PCIe)."""
+    tier's bound: every step copies its fp32 inputs over PCIe); best of
+    `trials` runs of `reps` back-to-back copies (the link is shared and noisy
+    on these boxes: 42-56 GB/s run to run)."""
     import torch
     h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    h.fill_(1)
     d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
     d.copy_(h, non_blocking=True)
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
-        d.copy_(h, non_blocking=True)
-    e1.record()
-    e1.synchronize()
-    return nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
+    best = 0.0
+    for _ in range(trials):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            d.copy_(h, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        best = max(best, nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    return best
 
 
 def nvlink_bytes(gpu: int):

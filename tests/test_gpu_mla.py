@@ -260,6 +260,27 @@ def test_mla_forward_tensor_cores(scmoe, orc, shape):
     assert np.isfinite(got).all() and err <= TC_TOL, err
 
 
+def test_mla_tensor_cores_long_sequence(scmoe):
+    """Long causal sequences (4096 keys: 32 query tiles, 16 two-tile CTAs per
+    head, lazy rescaling over 32 key tiles) at LongCat head widths: the
+    tensor-core forward within 2e-2 of the exact device MLA (itself bitwise
+    equal to the oracle, test_mla_forward_bitwise)."""
+    import torch
+    from paper_2509_01322_b200.mla import MlaParams, mla_block
+    dims = (512, 128, 128, 4, 128, 64)
+    seq, nseq = 4096, 2
+    w = O.mla_weights(*dims, seed=41)
+    h = torch.from_numpy(O.normal_f32(O.stream_seed(42, 0), seq * nseq * dims[0])
+                         .reshape(seq * nseq, dims[0])).cuda()
+    exact = mla_block(h, MlaParams(*dims, weights=w, rope_base=1.0e6), seq)
+    tc = mla_block(h, MlaParams(*dims, weights=w, rope_base=1.0e6, precision=scmoe.PREC_BF16), seq)
+    scmoe.default_context().synchronize()
+    exact, tc = exact.cpu().numpy(), tc.cpu().numpy()
+    err = O.rel_l2(tc, exact)
+    print(f"MLA tensor cores, 2 x 4096 causal: rel-L2 {err:.2e}")
+    assert np.isfinite(tc).all() and err <= TC_TOL, err
+
+
 def test_mla_tensor_core_dims_checked(scmoe):
     from paper_2509_01322_b200.mla import MlaParams, mla_block
     dims = (48, 24, 16, 3, 10, 6)  # not multiples of 64

@@ -117,6 +117,51 @@ def test_ep_equals_single_gpu_bitwise(world, dense, renorm):
     _spawn(_equal_worker, world, port, dense, renorm)
 
 
+def _empty_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    _init(rank, world, port)
+    try:
+        import paper_2509_01322_b200 as P
+        from paper_2509_01322_b200.ep import ExpertParallelLayer, broadcast_unique_id
+        shape = _shape(P)
+        T = 0 if rank == world - 1 else 512 + 64 * rank  # the last rank brings no tokens
+        a1 = torch.from_numpy(P.fill_normal(P.stream_seed(11, rank), T * shape.d)).cuda()
+        a3 = torch.from_numpy(P.fill_normal(P.stream_seed(12, rank), T * shape.d)).cuda()
+        ep = ExpertParallelLayer(P.Context(rank), shape, rank, world, 3, broadcast_unique_id(),
+                                 max_tokens=1024)
+        res = None
+        for _ in range(2):
+            res = ep.forward(a1.view(T, shape.d), a3.view(T, shape.d), None, T)
+        pip = ep.forward_batches([a1] * 3, [a3] * 3, None, T)
+        torch.cuda.synchronize()
+        ep.synchronize()
+        ok = all(torch.equal(u, v) for p in pip for u, v in zip(p, res))
+        if T:
+            ref = _single_gpu(P, rank, shape, a1, a3, T)
+            ok = ok and all(torch.equal(u, v) for u, v in zip(res, ref))
+        else:
+            ok = ok and all(t.numel() == 0 for t in res)
+        # the empty rank still serves its experts: rows arrive from the others
+        m = ep.count_matrix()
+        ok = ok and int(m[:, world - 1].sum()) > 0 and int(m[world - 1].sum()) == 0
+        ep.close()
+        q.put((rank, bool(ok), m.tolist()))
+    except Exception:  # pragma: no cover
+        import traceback
+        q.put((rank, False, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_ep_rank_without_tokens(world):
+    """A rank with an empty shard (T = 0) still exchanges its (zero) counts,
+    serves the rows other ranks dispatch to its experts and passes every
+    barrier; the other ranks' outputs stay bitwise equal to single-GPU."""
+    _spawn(_empty_worker, world, 29900 + os.getpid() % 50 + world)
+
+
 def _batches_worker(rank, world, port, q, corun):
     import torch
     import torch.distributed as dist

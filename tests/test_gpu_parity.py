@@ -340,6 +340,39 @@ def test_moe_forward_bf16_tensor_cores(scmoe, shape):
     assert err < 5e-3  # expected ~1e-3 (SURVEY.md 8c measured 7.4e-4)
 
 
+@pytest.mark.parametrize("case", ["one_expert", "zero_only", "single_token", "max_skew"])
+def test_moe_forward_bf16_skewed_routing(scmoe, case):
+    """Routing extremes on the tcgen05 path: every token on one expert (many
+    token tiles of one expert, every other expert empty), every slot on zero
+    experts (no FFN rows: the GEMMs see no tiles), a single token, and all
+    tokens on the same K experts."""
+    P = scmoe
+    d, n, z, k, I = 512, 16, 8, 4, 256
+    T = 1 if case == "single_token" else 700
+    x = O.bf16_round(O.normal_f32(O.stream_seed(8, 3), T * d)).reshape(T, d)
+    rng = np.random.default_rng(5)
+    if case == "one_expert":  # slot 0 of every token: FFN expert 3; rest zero experts
+        idx = np.stack([np.full(T, 3)] + [n + (np.arange(T) + s) % z for s in range(1, k)], 1)
+    elif case == "zero_only":
+        idx = np.stack([n + (np.arange(T) + s) % z for s in range(k)], 1)
+    elif case == "max_skew":
+        idx = np.tile(np.array([5, 9, 0, n + 1]), (T, 1))
+    else:
+        idx = rng.permutation(n + z)[:k][None, :]
+    idx = idx.astype(np.uint32).reshape(-1)
+    gates = rng.uniform(0.01, 0.3, T * k)
+    dg = P.RoutingDecision(top_k=k, n_ffn=n, indices=idx, gates=gates,
+                           ffn_count=(idx.reshape(T, k) < n).sum(1).astype(np.uint32))
+    w_in, w_out = make_bank_arrays(n, d, I, 33, bf16=True)
+    out = P.moe_forward(x, dg, P.ExpertBank(w_in, w_out, precision=P.PREC_BF16), z)
+    rc, want = O.orc_moe_forward(x, idx, gates, k, n, z, w_in, w_out)
+    assert rc == 0
+    if case == "zero_only":  # identity terms only: exact
+        assert out.tobytes() == want.tobytes()
+    else:
+        assert O.rel_l2(out, want) <= 5e-3, O.rel_l2(out, want)
+
+
 def test_layer_forward_bf16_routing_exact(scmoe):
     """bf16 GEMM path: routing is still bit-exact (fp32 router), output within
     the bf16 tolerance."""

@@ -1099,6 +1099,17 @@ def run_b200_ep(args):
     launches = ep.kernel_launches() - l0
     ms_max = max_over_ranks(ms, ws)
     value = T * ws / (ms_max / 1e3)
+    # energy per step on this rank's GPU over ~1.5 s of the same schedule (every
+    # rank runs the same number of coupled steps); rank 0's is reported
+    energy = None
+    if args.energy:
+        def run_n(n):
+            if pipelined:
+                ep.forward_batches([a1] * n, [a3] * n, None, T, corun_router=args.ep_corun)
+            else:
+                for _ in range(n):
+                    ep.forward(a1, a3, None, T)
+        energy = energy_block(local, run_n, ms_max)
     # NVLink cross-check: hardware tx bytes per step vs the payload this rank
     # stores to peers (dispatch rows + ids to the owners, returned rows to the sources)
     payload = ((n_send - self_rows) * (D * 2 + 4) + (n_recv - self_rows) * D * 2)
@@ -1250,6 +1261,7 @@ def run_b200_ep(args):
         "dispatch_nvlink": dispatch,
         "nvlink_counters": nvlink,
         "clocks": clk.summary(),
+        "energy": energy,
         "cpu_baseline": None,
         "config_d": config_d,
         "tpot": tpot,

@@ -900,7 +900,11 @@ def run_b200(args):
                      "kernel_io_bytes_per_step": g1b + g2b, "ms_per_step": t_gemm,
                      "achieved_serial": achieved_serial, "ms_per_step_serial": t_gemm_serial,
                      "tflops": flops / (t_gemm / 1e3) / 1e12 if t_gemm > 0 else None,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
+                     "binding_constraint": ("board power: the step's energy over the 1000 W cap "
+                                            "(see `energy`: frac_of_power_bound); streaming the "
+                                            "expert weights alone costs ~3.2 J per pass "
+                                            "(profiles/r02_energy_split.json)")},
         "stages_ms": {k: round(v[0] / v[1], 4) for k, v in stages.items()},
         "stages_ms_serial": {k: round(v[0] / v[1], 4) for k, v in stages_serial.items()},
         "clocks": clk.summary(),

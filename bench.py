@@ -33,7 +33,6 @@ import statistics
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 
 import numpy as np
@@ -110,82 +109,110 @@ def max_over_ranks(v: float, ws: int) -> float:
 # ---------------------------------------------------------------------------
 # clocks sampler (nvidia-smi during the timed region)
 # ---------------------------------------------------------------------------
+_NVML_POLL = r"""
+import sys, time
+import pynvml as n
+gpu, out, period = int(sys.argv[1]), sys.argv[2], float(sys.argv[3])
+n.nvmlInit()
+h = n.nvmlDeviceGetHandleByIndex(gpu)
+mx = n.nvmlDeviceGetMaxClockInfo(h, n.NVML_CLOCK_SM)
+bits = [n.nvmlClocksEventReasonHwSlowdown, n.nvmlClocksEventReasonHwThermalSlowdown,
+        n.nvmlClocksEventReasonSwThermalSlowdown, n.nvmlClocksEventReasonSwPowerCap]
+with open(out, "w", buffering=1) as f:
+    f.write("ready\n")
+    while True:
+        sm = n.nvmlDeviceGetClockInfo(h, n.NVML_CLOCK_SM)
+        pw = n.nvmlDeviceGetPowerUsage(h) / 1000.0
+        r = n.nvmlDeviceGetCurrentClocksEventReasons(h)
+        f.write(f"{sm} {mx} {pw} " + "".join("1" if r & b else "0" for b in bits) + "\n")
+        time.sleep(period)
+"""
+
+
 class ClockSampler:
-    """SM clocks, power and throttle reasons polled through NVML every 5 ms on
-    a thread during the timed region (nvidia-smi's 100 ms loop caught one
-    sample of a 130 ms region); falls back to nvidia-smi when NVML is absent."""
+    """SM clocks, power and throttle reasons polled through NVML every 5 ms
+    during the timed region by a separate process (a thread of this process
+    starves behind the GIL while the timed region blocks in CUDA calls: one
+    run got no sample at all); falls back to nvidia-smi when NVML is absent."""
     PERIOD_S = 0.005
+    REASONS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, gpu: int):
         self.gpu = gpu
         self.rows = []
-        self._stop = threading.Event()
-        self._t = None
+        self._proc = None
         self._smi = None
-
-    def _poll_nvml(self, n, h):
-        reasons = {"hw_slowdown": n.nvmlClocksEventReasonHwSlowdown,
-                   "hw_thermal_slowdown": n.nvmlClocksEventReasonHwThermalSlowdown,
-                   "sw_thermal_slowdown": n.nvmlClocksEventReasonSwThermalSlowdown,
-                   "sw_power_cap": n.nvmlClocksEventReasonSwPowerCap}
-        mx = n.nvmlDeviceGetMaxClockInfo(h, n.NVML_CLOCK_SM)
-        while not self._stop.is_set():
-            try:
-                sm = n.nvmlDeviceGetClockInfo(h, n.NVML_CLOCK_SM)
-                pw = n.nvmlDeviceGetPowerUsage(h) / 1000.0
-                r = n.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.rows.append((float(sm), float(mx), pw,
-                                  [k for k, bit in reasons.items() if r & bit]))
-            except Exception:
-                pass
-            time.sleep(self.PERIOD_S)
+        self.error = None
+        self._src = None
 
     def __enter__(self):
+        self._f = tempfile.NamedTemporaryFile("w+", suffix=".txt", delete=False)
         try:
-            import pynvml as n
-            n.nvmlInit()
-            h = n.nvmlDeviceGetHandleByIndex(self.gpu)
-            self._t = threading.Thread(target=self._poll_nvml, args=(n, h), daemon=True)
-            self._t.start()
-        except Exception:
-            self._t = None
+            self._proc = subprocess.Popen([sys.executable, "-c", _NVML_POLL, str(self.gpu),
+                                           self._f.name, str(self.PERIOD_S)],
+                                          stdout=subprocess.DEVNULL, stderr=subprocess.PIPE)
+            t0 = time.time()
+            while time.time() - t0 < 20:
+                if self._proc.poll() is not None:
+                    raise RuntimeError(self._proc.stderr.read().decode()[-160:])
+                if open(self._f.name).read().startswith("ready"):
+                    break
+                time.sleep(0.01)
+            else:
+                raise RuntimeError("NVML poller did not start")
+            self._src = "nvml 5 ms (separate process)"
+        except Exception as ex:
+            self.error = f"{type(ex).__name__}: {ex}"[:160]
+            if self._proc:
+                self._proc.kill()
+            self._proc = None
             try:
-                self._f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
                 q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
                      "clocks_event_reasons.hw_thermal_slowdown,"
                      "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
                 self._smi = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + q,
                                               "--format=csv,noheader,nounits", "-lms", "50"],
                                              stdout=self._f, stderr=subprocess.DEVNULL)
+                self._src = "nvidia-smi 50 ms"
             except FileNotFoundError:
                 self._smi = None
         time.sleep(0.02)
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        if self._t:
-            self._t.join()
+        time.sleep(0.01)
+        if self._proc:
+            self._proc.terminate()
+            self._proc.wait()
+            for line in open(self._f.name).read().splitlines()[1:]:
+                p = line.split()
+                if len(p) == 4 and len(p[3]) == 4:
+                    self.rows.append((float(p[0]), float(p[1]), float(p[2]),
+                                      [nm for nm, b in zip(self.REASONS, p[3]) if b == "1"]))
         if self._smi:
             self._smi.terminate()
             self._smi.wait()
-            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
             for r in open(self._f.name).read().strip().splitlines():
                 r = r.split(", ")
                 if len(r) >= 7:
                     self.rows.append((float(r[0]), float(r[1]), float(r[2]),
-                                      [nm for nm, v in zip(names, r[3:7]) if v.strip() == "Active"]))
+                                      [nm for nm, v in zip(self.REASONS, r[3:7])
+                                       if v.strip() == "Active"]))
+        try:
+            os.unlink(self._f.name)
+        except OSError:
+            pass
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"],
+                    "error": self.error}
         sm = [r[0] for r in self.rows]
         mx = max(r[1] for r in self.rows)
         reasons = sorted({x for r in self.rows for x in r[3]})
         loaded = [v for v in sm if v > 0.5 * mx] or sm
         return {"sm_mhz": statistics.median(loaded), "sm_min_mhz": min(loaded), "sm_max_mhz": mx,
-                "reasons": reasons, "samples": len(self.rows),
-                "source": "nvml 5 ms" if self._t else "nvidia-smi 50 ms",
+                "reasons": reasons, "samples": len(self.rows), "source": self._src,
                 "power_w_max": max(r[2] for r in self.rows)}
 
 
@@ -254,28 +281,32 @@ def pcie_h2d_gbs(nbytes: int, reps: int = 4, trials: int = 3) -> float:
     return best
 
 
-def pcie_duplex_gbs(nbytes: int, reps: int = 4) -> float:
+def pcie_duplex_gbs(nbytes: int, reps: int = 4, trials: int = 3) -> float:
     """H2D bandwidth while a D2H of the same size runs on another stream (the
-    e2e tier copies outputs back while the next inputs come in)."""
+    e2e tier copies outputs back while the next inputs come in); best of
+    `trials`."""
     import torch
     h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
     h2 = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
     d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
     d2 = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(s1)
-    s2.wait_event(e0)
-    for _ in range(reps):
-        with torch.cuda.stream(s1):
-            d.copy_(h, non_blocking=True)
-        with torch.cuda.stream(s2):
-            h2.copy_(d2, non_blocking=True)
-    e1.record(s1)
-    e1.synchronize()
-    torch.cuda.synchronize()
-    return nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
+    best = 0.0
+    for _ in range(trials):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s1)
+        s2.wait_event(e0)
+        for _ in range(reps):
+            with torch.cuda.stream(s1):
+                d.copy_(h, non_blocking=True)
+            with torch.cuda.stream(s2):
+                h2.copy_(d2, non_blocking=True)
+        e1.record(s1)
+        e1.synchronize()
+        torch.cuda.synchronize()
+        best = max(best, nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    return best
 
 
 def nvlink_bytes(gpu: int):

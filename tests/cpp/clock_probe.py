@@ -1,4 +1,6 @@
-import sys, time, torch
+import sys
+
+import torch
 sys.path.insert(0, '.')
 import bench
 x = torch.randn(8192, 8192, device='cuda')

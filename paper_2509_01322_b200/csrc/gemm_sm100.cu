@@ -142,7 +142,8 @@ struct GemmArgs {
     // only over K blocks up to (mb+1)*BM (its probabilities vanish beyond)
     int causal_rows;
     int causal_k;
-    int debug;           // timing experiments only: bit 0 skip epilogue stores,
+    int debug;           // timing / energy experiments only (pair kernel: 16 no MMAs,
+                         // 32 no token loads): bit 0 skip epilogue stores,
                          // bit 1 skip the epilogue (release TMEM at once),
                          // bit 2 tile-major unit order, bit 3 weights always evict-first
 };
@@ -793,6 +794,14 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(128)
                 const int row0 = tile.pos + (int)rank * half;
                 for (int ks = 0; ks < ks_end; ++ks) {
                     mbar_wait(&b_empty[stage], phase ^ 1);
+                    if (args.debug & 32) {  // energy experiment: no token traffic
+                        if (leader) mbar_arrive(&b_full[stage]);
+                        if (++stage == BS) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                        continue;
+                    }
                     if (leader)
                         mbar_expect_tx(&b_full[stage], (uint32_t)(2 * P_KS * nbox * P_BOX * BK * 2));
                     const uint32_t bar = mapa_rank(smem_u32(&b_full[stage]), 0);
@@ -835,7 +844,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(128)
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     if (lane == 0) {
 #pragma unroll
-                        for (int q = 0; q < P_KS; ++q) {
+                        for (int q = 0; q < P_KS && !(args.debug & 16); ++q) {  // 16: no MMAs
                             const uint32_t abase = smem_u32(a_ring + as * A_STAGE + q * A_SLAB_BYTES);
                             const uint32_t bbase = smem_u32(b_ring + bs * B_STAGE + q * B_KB);
 #pragma unroll

@@ -843,15 +843,19 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(128)
                     mbar_wait(&b_full[bs], bph);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     if (lane == 0) {
+                        if (!(args.debug & 16)) {  // 16: no MMAs (energy experiment)
 #pragma unroll
-                        for (int q = 0; q < P_KS && !(args.debug & 16); ++q) {  // 16: no MMAs
-                            const uint32_t abase = smem_u32(a_ring + as * A_STAGE + q * A_SLAB_BYTES);
-                            const uint32_t bbase = smem_u32(b_ring + bs * B_STAGE + q * B_KB);
+                            for (int q = 0; q < P_KS; ++q) {
+                                const uint32_t abase =
+                                    smem_u32(a_ring + as * A_STAGE + q * A_SLAB_BYTES);
+                                const uint32_t bbase = smem_u32(b_ring + bs * B_STAGE + q * B_KB);
 #pragma unroll
-                            for (int k = 0; k < BK / 16; ++k)
-                                mma_bf16_pair(tmem_base + buf * NT, make_desc_sw128(abase + k * 32),
-                                              make_desc_sw128(bbase + k * 32), idesc,
-                                              (ks | q | k) != 0);
+                                for (int k = 0; k < BK / 16; ++k)
+                                    mma_bf16_pair(tmem_base + buf * NT,
+                                                  make_desc_sw128(abase + k * 32),
+                                                  make_desc_sw128(bbase + k * 32), idesc,
+                                                  (ks | q | k) != 0);
+                            }
                         }
                         mma_commit_pair(&a_empty[as]);
                         mma_commit_pair(&b_empty[bs]);

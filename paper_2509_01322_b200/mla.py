@@ -65,28 +65,43 @@ class MlaParams:
             if self.variance_alignment else 1.0
 
     def invalidate(self):
-        self._dev = None
+        """Drop the device copy (the next call re-uploads the weights)."""
+        if self._dev is not None:
+            try:
+                lib().scmoe_mla_destroy(self._dev[0].handle, self._dev[1])
+            finally:
+                self._dev = None
 
     def device(self, ctx: Context):
         if self._dev is not None and self._dev[0] is ctx:
-            return self._dev[1]
+            h, prec = self._dev[1], self._dev[2]
+            if prec != self.precision:  # precision switched after the upload
+                ctx._check(lib().scmoe_mla_set_precision(ctx.handle, h, int(self.precision)))
+                self._dev = (ctx, h, self.precision)
+            return h
+        self.invalidate()  # another context's copy
         h = _P()
         ctx._check(lib().scmoe_mla_create(ctx.handle, self.d_model, self.d_q, self.d_kv,
                                           self.n_heads, self.d_head_c, self.d_head_r,
                                           self.rope_base, int(self.variance_alignment),
                                           C.byref(h)))
-        for i, (w, shp) in enumerate(zip(self.weights, self.shapes())):
-            if tuple(w.shape) != shp:
-                raise ParameterError(f"mla: {WEIGHT_NAMES[i]} has shape {tuple(w.shape)}, "
-                                     f"expected {shp}")
-            if hasattr(w, "data_ptr"):  # CUDA tensor
-                ctx._check(lib().scmoe_mla_set_weight(ctx.handle, h, i, w.contiguous().data_ptr()))
-            else:
-                a = np.ascontiguousarray(w, np.float32)
-                ctx._check(lib().scmoe_mla_set_weight_host(ctx.handle, h, i, _ptr(a)))
-        if self.precision:
-            ctx._check(lib().scmoe_mla_set_precision(ctx.handle, h, int(self.precision)))
-        self._dev = (ctx, h)
+        try:  # the handle is destroyed if any weight or the precision is rejected
+            for i, (w, shp) in enumerate(zip(self.weights, self.shapes())):
+                if tuple(w.shape) != shp:
+                    raise ParameterError(f"mla: {WEIGHT_NAMES[i]} has shape {tuple(w.shape)}, "
+                                         f"expected {shp}")
+                if hasattr(w, "data_ptr"):  # CUDA tensor
+                    ctx._check(lib().scmoe_mla_set_weight(ctx.handle, h, i,
+                                                          w.contiguous().data_ptr()))
+                else:
+                    a = np.ascontiguousarray(w, np.float32)
+                    ctx._check(lib().scmoe_mla_set_weight_host(ctx.handle, h, i, _ptr(a)))
+            if self.precision:
+                ctx._check(lib().scmoe_mla_set_precision(ctx.handle, h, int(self.precision)))
+        except Exception:
+            lib().scmoe_mla_destroy(ctx.handle, h)
+            raise
+        self._dev = (ctx, h, self.precision)
         return h
 
     def __del__(self):

@@ -174,13 +174,24 @@ class DeviceLayer:
             int(renormalize), arr(idxs), arr(gatess), arr(cnts), arr(outs)))
 
     def close(self):
+        """Free the device router and bank (also done when the object dies
+        while its context is still open)."""
         L = lib()
+        if not self.ctx.handle:  # closed context: its handles can no longer be used
+            self.bank = self.router = _P()
+            return
         if self.bank:
             L.scmoe_bank_destroy(self.ctx.handle, self.bank)
             self.bank = _P()
         if self.router:
             L.scmoe_router_destroy(self.ctx.handle, self.router)
             self.router = _P()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class DenseFFN:
@@ -197,14 +208,20 @@ class DenseFFN:
         self.bank = _P()
         ctx._check(L.scmoe_bank_create(ctx.handle, 1, d, inter, PREC_BF16, 1,
                                        int(GammaMode.Off), C.byref(self.bank)))
-        if w_in is not None:
-            import numpy as np
-            wi = np.ascontiguousarray(w_in, np.float32)
-            wo = np.ascontiguousarray(w_out, np.float32)
-            ctx._check(L.scmoe_bank_set_expert_host(ctx.handle, self.bank, 0,
-                                                    wi.ctypes.data_as(_P), wo.ctypes.data_as(_P)))
-        else:
-            ctx._check(L.scmoe_bank_init_uniform(ctx.handle, self.bank, seed, stream0, 1.0 / d))
+        try:
+            if w_in is not None:
+                import numpy as np
+                wi = np.ascontiguousarray(w_in, np.float32)
+                wo = np.ascontiguousarray(w_out, np.float32)
+                ctx._check(L.scmoe_bank_set_expert_host(ctx.handle, self.bank, 0,
+                                                        wi.ctypes.data_as(_P),
+                                                        wo.ctypes.data_as(_P)))
+            else:
+                ctx._check(L.scmoe_bank_init_uniform(ctx.handle, self.bank, seed, stream0,
+                                                     1.0 / d))
+        except Exception:
+            self.close()
+            raise
 
     def forward(self, a1: int, gain: Optional[int], tokens: int, out: int,
                 ctx: Optional[Context] = None):
@@ -213,6 +230,12 @@ class DenseFFN:
         c._check(lib().scmoe_dense_ffn(c.handle, self.bank, a1, gain, tokens, out))
 
     def close(self):
-        if self.bank:
+        if self.bank and self.ctx.handle:
             lib().scmoe_bank_destroy(self.ctx.handle, self.bank)
-            self.bank = _P()
+        self.bank = _P()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -17,14 +17,27 @@
 using namespace scmoe;
 
 namespace scmoe {
+// Raises a kernel's dynamic shared-memory limit on this device to at least
+// `bytes` (remembering the largest value set, so a later, larger request for
+// the same kernel raises it again).
 void ensure_max_dynamic_smem(const void* kernel, int bytes, int device) {
+    struct Set {
+        const void* kernel;
+        int device, bytes;
+    };
     static std::mutex mu;
-    static std::vector<std::pair<const void*, int>> done;
+    static std::vector<Set> done;
     std::lock_guard<std::mutex> lock(mu);
-    for (const auto& kv : done)
-        if (kv.first == kernel && kv.second == device) return;
+    for (auto& s : done)
+        if (s.kernel == kernel && s.device == device) {
+            if (bytes <= s.bytes) return;
+            SCMOE_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            bytes));
+            s.bytes = bytes;
+            return;
+        }
     SCMOE_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    done.emplace_back(kernel, device);
+    done.push_back(Set{kernel, device, bytes});
 }
 }  // namespace scmoe
 
@@ -110,14 +123,19 @@ void require_ctx(scmoe_ctx* c) {
     SCMOE_CUDA(cudaSetDevice(c->device));
 }
 
-int tile_rows_for(const scmoe_bank* b) {
-    // single-GPU path: 192-token tiles (or SCMOE_TILE_ROWS=128 / 256)
+int tile_rows_for(const scmoe_ctx* c, const scmoe_bank* b, size_t T, size_t K) {
+    // single-GPU bf16 path: 192-token tiles (or SCMOE_TILE_ROWS=128 / 256)
     static const int v = [] {
         const char* e = getenv("SCMOE_TILE_ROWS");
         const int x = e ? atoi(e) : 192;
         return x == 128 || x == 256 ? x : 192;
     }();
-    return b->precision == SCMOE_PREC_BF16 ? v : 64;
+    if (b->precision == SCMOE_PREC_BF16) return v;
+    // exact fp32: 64-row tiles when they give every SM >= 4 CTAs, else 16-row
+    // tiles so a small batch (config A: ~85 rows per expert) spreads over the
+    // SMs instead of running 48 long CTAs (the chains, hence the bits, do not
+    // depend on the tiling)
+    return seq_gemm_tile_rows(T * K, b->inter, c->num_sms);
 }
 
 // The MoE block is split into a front half (permutation, and the row gather
@@ -132,7 +150,7 @@ void moe_front(scmoe_ctx* c, scmoe_bank* b, const float* x, const __nv_bfloat16*
     PermResult pr;
     {
         ProfScope _p(c, "permute");
-        pr = launch_permute(c, idx, T, K, n_ffn, E, tile_rows_for(b));
+        pr = launch_permute(c, idx, T, K, n_ffn, E, tile_rows_for(c, b, T, K));
     }
     static_assert(sizeof(PermResult) <= sizeof(ws.pr_blob), "perm blob");
     memcpy(ws.pr_blob, &pr, sizeof(pr));
@@ -169,11 +187,11 @@ void moe_back(scmoe_ctx* c, scmoe_bank* b, const float* x, size_t T, const uint3
             {
                 ProfScope _p(c, "expert_gemm1_f32");
                 launch_seq_gemm(c, x, d, pr.row_token, b->w_in32, I, d * I, h, I, d, I, /*silu=*/1,
-                                pr.tiles, pr.n_tiles, pr.max_tiles, 64);
+                                pr.tiles, pr.n_tiles, pr.max_tiles, tile_rows_for(c, b, T, K));
             }
             ProfScope _p(c, "expert_gemm2_f32");
             launch_seq_gemm(c, h, I, nullptr, b->w_out32, d, I * d, y, d, I, d, /*silu=*/0,
-                            pr.tiles, pr.n_tiles, pr.max_tiles, 64);
+                            pr.tiles, pr.n_tiles, pr.max_tiles, tile_rows_for(c, b, T, K));
         }
         if (comb) {
             ProfScope _p(c, "combine");
@@ -190,17 +208,17 @@ void moe_back(scmoe_ctx* c, scmoe_bank* b, const float* x, size_t T, const uint3
                 launch_grouped_gemm_bf16(c, b->w1t, n_ffn, I, d,
                                          ws.hmoe_bf16.get<__nv_bfloat16>(T * d), T, pr.row_token,
                                          h, /*silu=*/1, pr.tiles, pr.n_tiles, pr.max_tiles,
-                                         tile_rows_for(b));
+                                         tile_rows_for(c, b, T, K));
             } else {
                 ProfScope _p(c, "gemm1_tcgen05");
                 launch_grouped_gemm_bf16(c, b->w1t, n_ffn, I, d,
                                          ws.xp.get<__nv_bfloat16>(T * K * d + 1), T * K, nullptr,
                                          h, /*silu=*/1, pr.tiles, pr.n_tiles, pr.max_tiles,
-                                         tile_rows_for(b));
+                                         tile_rows_for(c, b, T, K));
             }
             ProfScope _p(c, "gemm2_tcgen05");
             launch_grouped_gemm_bf16(c, b->w2t, n_ffn, d, I, h, T * K, nullptr, y, /*silu=*/0,
-                                     pr.tiles, pr.n_tiles, pr.max_tiles, tile_rows_for(b));
+                                     pr.tiles, pr.n_tiles, pr.max_tiles, tile_rows_for(c, b, T, K));
         }
         if (comb) {
             ProfScope _p(c, "combine");
@@ -221,8 +239,9 @@ void moe_forward_dev(scmoe_ctx* c, scmoe_bank* b, const float* x, const __nv_bfl
 
 // router.hpp:136 logits = mm(x, W_r).  Kernel choice: the full-width slab
 // kernel (1 CTA/SM, single wave) when the batch fills the GPU; the lean
-// kernel inside pipelined calls (it co-resides with the grouped GEMM); the
-// 64/16-row tiled kernel otherwise (small batches, E > 768).
+// kernel inside pipelined calls (it co-resides with the grouped GEMM); one
+// thread per logit for small batches (config A); the 64/16-row tiled kernel
+// otherwise (E > 768).
 void route_logits(scmoe_ctx* c, scmoe_router* r, const float* x, size_t T, float* logits) {
     const size_t E = r->E();
     int v = c->router_variant;
@@ -230,11 +249,14 @@ void route_logits(scmoe_ctx* c, scmoe_router* r, const float* x, size_t T, float
     if (v == 1 && !router_slab_ok(T, r->d, E, 0)) v = 0;
     if (v == 4 && !router_tma_ok(T, r->d, E, 0)) v = 0;
     if (v == 5 && !router_corun_ok(T, r->d, E)) v = 0;
+    if (v == 6 && !router_small_ok(0, r->d, E, c->num_sms)) v = 0;
     if (v == 0) {
         if (c->overlapped && router_corun_ok(T, r->d, E) && T >= 512)
             v = 5;
         else if (router_tma_ok(T, r->d, E, c->num_sms))
             v = 4;
+        else if (router_small_ok(T, r->d, E, c->num_sms))
+            v = 6;
         else
             v = 3;
     }
@@ -247,6 +269,8 @@ void route_logits(scmoe_ctx* c, scmoe_router* r, const float* x, size_t T, float
         launch_router_slab(c, x, r->w, logits, T, r->d, E);
     } else if (v == 2) {
         launch_router_lean(c, x, r->w, logits, T, r->d, E);
+    } else if (v == 6) {
+        launch_router_small(c, x, r->w, logits, T, r->d, E);
     } else {
         const int tr = seq_gemm_tile_rows(T, E, c->num_sms);
         const size_t ntile = ceil_div(T, tr);
@@ -318,6 +342,7 @@ int scmoe_ctx_create(int device, scmoe_ctx** out) {
                 : sv == "tiled" ? 3
                 : sv == "tma"   ? 4
                 : sv == "corun" ? 5
+                : sv == "small" ? 6
                                 : 0;
         }
         SCMOE_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));

@@ -271,6 +271,9 @@ void launch_router_corun(scmoe_ctx* c, const float* X, const float* W, float* lo
 bool router_slab_ok(size_t T, size_t K, size_t E, int num_sms);
 // Router projection sized to co-reside with the grouped GEMM (28-token slabs).
 bool router_lean_ok(size_t K, size_t E);
+bool router_small_ok(size_t T, size_t K, size_t E, int num_sms);
+void launch_router_small(scmoe_ctx* c, const float* X, const float* W, float* logits, size_t T,
+                         size_t K, size_t E);
 void launch_router_lean(scmoe_ctx* c, const float* X, const float* W, float* logits, size_t T,
                         size_t K, size_t E);
 void launch_router_slab(scmoe_ctx* c, const float* X, const float* W, float* logits, size_t T,

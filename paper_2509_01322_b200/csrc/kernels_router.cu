@@ -569,6 +569,65 @@ void launch_router_lean(scmoe_ctx* c, const float* X, const float* W, float* log
     SCMOE_LAUNCH_CHECK(c);
 }
 
+// Small batches (config A: 512 tokens x 12 experts): one thread per logit,
+// the reference chain c = 0; c = fl(c + fl(x_k * w_k)) in k order (router.hpp:136,
+// tensor.hpp:95-112).  A CTA stages W (K x E) and its kSmallTok token rows in
+// shared memory once; its E x kSmallTok threads then run their chains out of
+// shared memory (x broadcast across a token's experts, W contiguous across
+// the experts), k unrolled so the loads run ahead of the add chain.
+constexpr int kSmallTok = 8;
+
+__global__ void router_small_kernel(const float* __restrict__ X, const float* __restrict__ W,
+                                    float* __restrict__ logits, int T, int K, int E) {
+    extern __shared__ float rs_smem[];
+    float* ws = rs_smem;            // [K][E]
+    float* xs = rs_smem + K * E;    // [kSmallTok][K]
+    const int t0 = blockIdx.x * kSmallTok;
+    const int nt = min(kSmallTok, T - t0);
+    for (int i = threadIdx.x; i < K * E; i += blockDim.x) ws[i] = W[i];
+    for (int i = threadIdx.x; i < nt * K; i += blockDim.x) xs[i] = X[(size_t)t0 * K + i];
+    __syncthreads();
+    const int tl = threadIdx.x / E, e = threadIdx.x % E;
+    if (tl >= nt) return;
+    const float* x = xs + tl * K;
+    float c = 0.f;
+    int k = 0;
+    for (; k + 8 <= K; k += 8) {
+        float xv[8], wv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            xv[u] = x[k + u];
+            wv[u] = ws[(k + u) * E + e];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) c = __fadd_rn(c, __fmul_rn(xv[u], wv[u]));
+    }
+    for (; k < K; ++k) c = __fadd_rn(c, __fmul_rn(x[k], ws[k * E + e]));
+    logits[(size_t)(t0 + tl) * E + e] = c;
+}
+
+static size_t router_small_smem(size_t K, size_t E) { return (K * E + kSmallTok * K) * sizeof(float); }
+
+bool router_small_ok(size_t T, size_t K, size_t E, int num_sms) {
+    // one logit per thread pays when the 16-row seq-GEMM tiles would leave most
+    // SMs idle (fewer than ~4 tiles per SM); a CTA's E x 8 threads and its
+    // staged W (K x E) must stay small
+    return E * kSmallTok <= 1024 && router_small_smem(K, E) <= 96 * 1024 &&
+           (T + 15) / 16 < (size_t)num_sms * 4;
+}
+
+void launch_router_small(scmoe_ctx* c, const float* X, const float* W, float* logits, size_t T,
+                         size_t K, size_t E) {
+    const size_t smem = router_small_smem(K, E);
+    SCMOE_CHECK_ARG(smem <= 200 * 1024 && E * kSmallTok <= 1024, SCMOE_ERR_CONFIG,
+                    "router: small-batch kernel needs K*E + 8*K floats of shared memory");
+    ensure_max_dynamic_smem(reinterpret_cast<const void*>(router_small_kernel), (int)smem,
+                            c->device);
+    router_small_kernel<<<(unsigned)ceil_div(T, (size_t)kSmallTok), (unsigned)(E * kSmallTok), smem,
+                          c->stream>>>(X, W, logits, (int)T, (int)K, (int)E);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
 bool router_slab_ok(size_t T, size_t K, size_t E, int num_sms) {
     // full-width slab needs E <= 768, E and K multiples of 4 (float4 rows), and
     // enough tokens to fill most SMs (otherwise the 16/64-row tiles spread better)

@@ -76,7 +76,7 @@ print("ok")
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
-@pytest.mark.parametrize("variant", ["tma", "corun", "slab", "lean", "tiled"])
+@pytest.mark.parametrize("variant", ["tma", "corun", "slab", "lean", "tiled", "small"])
 def test_router_kernel_variants_edge_values(variant):
     """Subnormal products and sums, exact zeros, signed zeros, a ragged last
     slab and a partial expert width (E = 60 < 768): every router kernel (the

@@ -217,6 +217,75 @@ __global__ void __launch_bounds__(kTB) perm_hist_multi_kernel(
             }
 }
 
+// Small batches (T <= 1024 tokens, E <= 64 experts): the three passes in one
+// CTA of 1024 threads (one token each), the same results -- per-expert token
+// bitmask ranks (tokens ascending, blocks.hpp:349-359), expert counts, FFN
+// bases, equal-width token tiles, slot positions and row tokens.
+constexpr int kSmallPermT = 1024, kSmallPermE = 64;
+
+__global__ void __launch_bounds__(1024) perm_small_kernel(
+    const uint32_t* __restrict__ idx, int T, int K, int E, int n_ffn, int tile_rows,
+    int* __restrict__ expert_count, int* __restrict__ expert_base, TokenTile* __restrict__ tiles,
+    int* __restrict__ n_tiles, int* __restrict__ slot_pos, int* __restrict__ row_token,
+    int* __restrict__ dev_status) {
+    constexpr int W = kSmallPermT / 32;
+    __shared__ uint32_t masks[kSmallPermE * W];
+    __shared__ int cnt_s[kSmallPermE], base_s[kSmallPermE + 1];
+    const int t = threadIdx.x, word = t >> 5;
+    const uint32_t bit = 1u << (t & 31);
+    for (int i = t; i < E * W; i += blockDim.x) masks[i] = 0;
+    __syncthreads();
+    if (t < T)
+        for (int s = 0; s < K; ++s) {
+            const uint32_t e = idx[(size_t)t * K + s];
+            if (e >= (uint32_t)E) {
+                atomicExch(dev_status, DEV_ERR_INDEX_RANGE);
+                continue;
+            }
+            atomicOr(&masks[e * W + word], bit);
+        }
+    __syncthreads();
+    for (int e = t; e < E; e += blockDim.x) {
+        int n = 0;
+        for (int w = 0; w < W; ++w) n += __popc(masks[e * W + w]);
+        cnt_s[e] = n;
+        expert_count[e] = n;
+    }
+    __syncthreads();
+    if (t == 0) {  // FFN bases and the tile list (n_ffn <= 64: serial is cheap)
+        int row = 0, nt_all = 0;
+        for (int e = 0; e < n_ffn; ++e) {
+            base_s[e] = row;
+            expert_base[e] = row;
+            const int cnt = cnt_s[e];
+            const int nt = (cnt + tile_rows - 1) / tile_rows;
+            const int step = nt > 1 ? min(tile_rows, ((cnt + nt - 1) / nt + 15) & ~15) : tile_rows;
+            for (int r = 0, k = 0; r < cnt; r += step, ++k)
+                tiles[nt_all++] = TokenTile{e, row + r, min(step, cnt - r), (k << 16) | nt};
+            row += cnt;
+        }
+        base_s[n_ffn] = row;
+        expert_base[n_ffn] = row;
+        *n_tiles = nt_all;
+    }
+    __syncthreads();
+    if (t < T)
+        for (int s = 0; s < K; ++s) {
+            const size_t i = (size_t)t * K + s;
+            const uint32_t e = idx[i];
+            if (e >= (uint32_t)n_ffn) {
+                slot_pos[i] = -1;
+                continue;
+            }
+            const uint32_t* m = masks + e * W;
+            int r = __popc(m[word] & (bit - 1u));
+            for (int w = 0; w < word; ++w) r += __popc(m[w]);
+            const int pos = base_s[e] + r;
+            slot_pos[i] = pos;
+            row_token[pos] = t;
+        }
+}
+
 PermResult launch_permute(scmoe_ctx* c, const uint32_t* idx, size_t T, size_t K, size_t n_ffn,
                           size_t E, int tile_rows, bool multi, const int* T_dev) {
     Workspace& ws = c->ws;
@@ -232,6 +301,13 @@ PermResult launch_permute(scmoe_ctx* c, const uint32_t* idx, size_t T, size_t K,
     pr.max_tiles = ceil_div(T * K, tile_rows) + n_ffn;
     pr.tiles = ws.tiles.get<TokenTile>(pr.max_tiles);
     pr.n_tiles = ws.n_tiles.get<int>(1);
+    if (!multi && !T_dev && T > 0 && T <= (size_t)kSmallPermT && E <= (size_t)kSmallPermE) {
+        perm_small_kernel<<<1, kSmallPermT, 0, c->stream>>>(
+            idx, (int)T, (int)K, (int)E, (int)n_ffn, tile_rows, pr.expert_count, pr.expert_base,
+            pr.tiles, pr.n_tiles, pr.slot_pos, pr.row_token, c->dev_status);
+        SCMOE_LAUNCH_CHECK(c);
+        return pr;
+    }
     const size_t smem = E * kMaskWords * sizeof(uint32_t);
     SCMOE_CHECK_ARG(smem <= 200 * 1024, SCMOE_ERR_CONFIG, "permute: too many experts");
     if (smem > 48 * 1024)

@@ -340,6 +340,31 @@ def test_moe_forward_bf16_tensor_cores(scmoe, shape):
     assert err < 5e-3  # expected ~1e-3 (SURVEY.md 8c measured 7.4e-4)
 
 
+@pytest.mark.parametrize("T,n,z,k", [(333, 16, 8, 4), (1024, 48, 16, 6), (1, 8, 4, 2),
+                                     (1025, 16, 8, 4), (4000, 64, 32, 8)])
+def test_permutation_matches_oracle(scmoe, T, n, z, k):
+    """moe_block's permutation (blocks.hpp:349-359) on the device -- the one-CTA
+    path for small batches (T <= 1024, E <= 64) and the three-pass path --
+    equals the oracle: per-expert slot counts and each slot's rank in its
+    expert's token list."""
+    import torch
+    P = scmoe
+    rng = np.random.default_rng(T + n)
+    idx = np.stack([rng.permutation(n + z)[:k] for _ in range(T)]).astype(np.uint32).reshape(-1)
+    ctx = P.default_context()
+    idx_d = torch.from_numpy(idx.view(np.int32)).cuda()
+    cnt_d = torch.empty(n + z, dtype=torch.int32, device="cuda")
+    row_d = torch.empty(T * k, dtype=torch.int32, device="cuda")
+    ctx._check(P.lib().scmoe_permutation(ctx.handle, idx_d.data_ptr(), T, k, n, z,
+                                         cnt_d.data_ptr(), row_d.data_ptr()))
+    ctx.synchronize()
+    counts = np.empty(n + z, np.uint64)
+    slot_row = np.empty(T * k, np.int32)
+    O.orc().orc_permutation(ptr(idx), T, k, n, z, ptr(counts), ptr(slot_row))
+    assert (cnt_d.cpu().numpy().astype(np.uint64) == counts).all()
+    assert (row_d.cpu().numpy() == slot_row).all()
+
+
 @pytest.mark.parametrize("case", ["one_expert", "zero_only", "single_token", "max_skew"])
 def test_moe_forward_bf16_skewed_routing(scmoe, case):
     """Routing extremes on the tcgen05 path: every token on one expert (many

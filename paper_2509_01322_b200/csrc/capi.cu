@@ -290,15 +290,23 @@ void layer_front(scmoe_ctx* c, scmoe_router* r, scmoe_bank* b, const float* a1, 
     float* hmoe = ws.hmoe.get<float>(T * d);
     __nv_bfloat16* hb =
         b->precision == SCMOE_PREC_BF16 ? ws.hmoe_bf16.get<__nv_bfloat16>(T * d) : nullptr;
-    {
-        ProfScope _p(c, "rmsnorm");
-        launch_rmsnorm(c, a1, gain, T, d, 1e-6f, hmoe, hb);
-    }
-    float* logits = ws.logits.get<float>(T * E);
-    route_logits(c, r, hmoe, T, logits);
-    {
-        ProfScope _p(c, "softmax_topk");
-        launch_softmax_topk(c, logits, T, E, K, r->n_ffn, r->b, idx, gates, ffn_count, nullptr);
+    if (c->router_variant == 0 && !c->overlapped && front_small_ok(T, d, E, K, c->num_sms)) {
+        // small batches: rmsnorm + router + softmax / top-K in one launch
+        ProfScope _p(c, "front_small");
+        launch_front_small(c, a1, gain, T, d, 1e-6f, r->w, E, K, r->n_ffn, r->b, hmoe, hb, idx,
+                           gates, ffn_count);
+    } else {
+        {
+            ProfScope _p(c, "rmsnorm");
+            launch_rmsnorm(c, a1, gain, T, d, 1e-6f, hmoe, hb);
+        }
+        float* logits = ws.logits.get<float>(T * E);
+        route_logits(c, r, hmoe, T, logits);
+        {
+            ProfScope _p(c, "softmax_topk");
+            launch_softmax_topk(c, logits, T, E, K, r->n_ffn, r->b, idx, gates, ffn_count,
+                                nullptr);
+        }
     }
     moe_front(c, b, hmoe, hb, T, idx, K, r->n_zero);
 }

@@ -272,6 +272,11 @@ bool router_slab_ok(size_t T, size_t K, size_t E, int num_sms);
 // Router projection sized to co-reside with the grouped GEMM (28-token slabs).
 bool router_lean_ok(size_t K, size_t E);
 bool router_small_ok(size_t T, size_t K, size_t E, int num_sms);
+bool front_small_ok(size_t T, size_t d, size_t E, size_t K, int num_sms);
+void launch_front_small(scmoe_ctx* c, const float* a1, const float* gain, size_t T, size_t d,
+                        float eps, const float* W, size_t E, size_t K, size_t n_ffn,
+                        const double* bias, float* hmoe, __nv_bfloat16* hb, uint32_t* idx,
+                        double* gates, uint32_t* ffn_count);
 void launch_router_small(scmoe_ctx* c, const float* X, const float* W, float* logits, size_t T,
                          size_t K, size_t E);
 void launch_router_lean(scmoe_ctx* c, const float* X, const float* W, float* logits, size_t T,

@@ -926,6 +926,140 @@ __global__ void __launch_bounds__(256) softmax_topk_kernel(
     if (lane == 0) ffn_out[t] = ffn;
 }
 
+// ---------------------------------------------------------------------------
+// Small batches (config A): the whole front of the layer in one launch --
+// rmsnorm (graph.hpp:322-335), router logits (router.hpp:136), softmax and
+// biased top-K (tensor.hpp:174-192, router.hpp:90-130) -- for E <= 32 experts.
+// A CTA owns kFrontTok tokens: their rows and W sit in shared memory; one
+// thread per row runs the sequential sum of squares, every thread scales,
+// one thread per logit runs its chain, one warp per token (lane = expert)
+// does softmax and selection.  Every step is the arithmetic of the separate
+// kernels (rmsnorm_kernel, router_small_kernel, softmax_topk_kernel), so the
+// results are identical bit for bit.
+// ---------------------------------------------------------------------------
+constexpr int kFrontTok = 8;
+
+__global__ void __launch_bounds__(256) front_small_kernel(
+    const float* __restrict__ a1, const float* __restrict__ gain, int T, int d, float eps,
+    const float* __restrict__ W, int E, int K, int n_ffn, const double* __restrict__ bias,
+    float* __restrict__ hmoe, __nv_bfloat16* __restrict__ hb, uint32_t* __restrict__ idx_out,
+    double* __restrict__ gates_out, uint32_t* __restrict__ ffn_out) {
+    extern __shared__ __align__(16) float fs_smem[];
+    float* xs = fs_smem;                       // [kFrontTok][d]
+    float* ws = xs + kFrontTok * d;            // [d][E]
+    float* lg = ws + d * E;                    // [kFrontTok][32] logits, then probabilities
+    float* inv = lg + kFrontTok * 32;          // [kFrontTok]
+    __shared__ uint64_t exp_tab[32];
+    const int tid = threadIdx.x;
+    if (tid < 32) exp_tab[tid] = scmoe_exp2f_tab_dev[tid];
+    const int t0 = blockIdx.x * kFrontTok;
+    const int nt = min(kFrontTok, T - t0);
+    for (int i = tid; i < d * E; i += blockDim.x) ws[i] = W[i];
+    for (int i = tid; i < nt * d; i += blockDim.x) xs[i] = a1[(size_t)t0 * d + i];
+    __syncthreads();
+    // rmsnorm: the reference's sequential sum of squares, one thread per row
+    if (tid < nt) {
+        const float* x = xs + tid * d;
+        float s2 = 0.0f;
+        for (int j = 0; j < d; ++j) s2 = __fadd_rn(s2, __fmul_rn(x[j], x[j]));
+        inv[tid] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(s2, (float)d), eps)));
+    }
+    __syncthreads();
+    for (int i = tid; i < nt * d; i += blockDim.x) {
+        const int r = i / d, j = i % d;
+        const float v = __fmul_rn(__fmul_rn(xs[i], inv[r]), gain ? gain[j] : 1.0f);
+        xs[i] = v;
+        hmoe[(size_t)t0 * d + i] = v;
+        if (hb) hb[(size_t)t0 * d + i] = __float2bfloat16_rn(v);
+    }
+    __syncthreads();
+    // router logits: one chain per (token, expert), k ascending
+    if (tid < nt * E) {
+        const int r = tid / E, e = tid % E;
+        const float* x = xs + r * d;
+        float c = 0.f;
+        for (int k = 0; k < d; ++k) c = __fadd_rn(c, __fmul_rn(x[k], ws[k * E + e]));
+        lg[r * 32 + e] = c;
+    }
+    __syncthreads();
+    // softmax + biased top-K: warp w = token w, lane = expert
+    const int warp = tid >> 5, lane = tid & 31;
+    if (warp >= nt) return;
+    const int t = t0 + warp;
+    float* row = lg + warp * 32;
+    float mx = -FLT_MAX;
+    if (lane < E) mx = row[lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float other = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = other > mx ? other : mx;
+    }
+    float p = 0.f;
+    if (lane < E) p = scmoe_expf_smem(__fsub_rn(row[lane], mx), exp_tab);
+    __syncwarp();
+    if (lane < E) row[lane] = p;
+    __syncwarp();
+    float sum = 0.0f;
+    if (lane == 0)
+        for (int j = 0; j < E; ++j) sum = __fadd_rn(sum, row[j]);
+    sum = __shfl_sync(0xffffffffu, sum, 0);
+    const float q = lane < E ? __fdiv_rn(p, sum) : 0.f;
+    const double bj = (lane < E && bias) ? bias[lane] : 0.0;
+    bool taken = lane >= E;
+    uint32_t ffn = 0;
+    for (int s = 0; s < K; ++s) {
+        double best_s = 0.0;
+        int best_i = INT_MAX;
+        float best_q = 0.f;
+        if (!taken) {
+            best_s = __dadd_rn((double)q, bj);
+            best_i = lane;
+            best_q = q;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double os = __shfl_xor_sync(0xffffffffu, best_s, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, best_i, o);
+            const float oq = __shfl_xor_sync(0xffffffffu, best_q, o);
+            if (oi != INT_MAX && (best_i == INT_MAX || better(os, oi, best_s, best_i))) {
+                best_s = os;
+                best_i = oi;
+                best_q = oq;
+            }
+        }
+        if (lane == best_i) taken = true;
+        if (lane == 0) {
+            idx_out[(size_t)t * K + s] = (uint32_t)best_i;
+            gates_out[(size_t)t * K + s] = (double)best_q;
+        }
+        ffn += best_i < n_ffn ? 1u : 0u;
+    }
+    if (lane == 0) ffn_out[t] = ffn;
+}
+
+static size_t front_small_smem(size_t d, size_t E) {
+    return (kFrontTok * d + d * E + kFrontTok * 32 + kFrontTok) * sizeof(float);
+}
+
+bool front_small_ok(size_t T, size_t d, size_t E, size_t K, int num_sms) {
+    return E <= 32 && K <= E && front_small_smem(d, E) <= 96 * 1024 &&
+           (T + 15) / 16 < (size_t)num_sms * 4;
+}
+
+void launch_front_small(scmoe_ctx* c, const float* a1, const float* gain, size_t T, size_t d,
+                        float eps, const float* W, size_t E, size_t K, size_t n_ffn,
+                        const double* bias, float* hmoe, __nv_bfloat16* hb, uint32_t* idx,
+                        double* gates, uint32_t* ffn_count) {
+    if (T == 0) return;
+    const size_t smem = front_small_smem(d, E);
+    ensure_max_dynamic_smem(reinterpret_cast<const void*>(front_small_kernel), (int)smem,
+                            c->device);
+    front_small_kernel<<<(unsigned)ceil_div(T, (size_t)kFrontTok), 256, smem, c->stream>>>(
+        a1, gain, (int)T, (int)d, eps, W, (int)E, (int)K, (int)n_ffn, bias, hmoe, hb, idx, gates,
+        ffn_count);
+    SCMOE_LAUNCH_CHECK(c);
+}
+
 template <typename S, bool kFromLogits>
 static void launch_topk_impl(scmoe_ctx* c, const S* in, size_t T, size_t E, size_t K,
                              size_t n_ffn, const double* bias, uint32_t* idx, double* gates,

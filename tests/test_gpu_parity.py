@@ -309,6 +309,40 @@ def test_layer_forward_exact(scmoe):
     assert (bits32(out) == bits32(want)).all()
 
 
+@pytest.mark.parametrize("T,n,z,k", [(131, 20, 12, 6), (40, 8, 4, 8), (333, 16, 8, 4)])
+def test_layer_forward_small_front_edge_values(scmoe, T, n, z, k):
+    """The fused small-batch front (rmsnorm + router + softmax / top-K in one
+    launch, E <= 32) on edge values -- subnormal products, signed zeros, an
+    all-zero row, large rows, non-zero biases with ties, K up to E - 4 --
+    bit-exact against the reference composition."""
+    P = scmoe
+    d, ke, I = 256, max(1, k // 2), 64
+    a1 = O.normal_f32(O.stream_seed(61, T), T * d).reshape(T, d)
+    a3 = O.normal_f32(O.stream_seed(62, T), T * d).reshape(T, d)
+    a1[::3] *= np.float32(2.0 ** -66)
+    a1[5 % T] = 0.0
+    a1[7 % T, ::2] = -0.0
+    a1[9 % T] *= np.float32(2.0 ** 40)
+    gain = (O.uniform_f32(63, d, 0.05) + np.float32(1.0)).astype(np.float32)
+    bias = np.zeros(n + z)
+    bias[:n] = np.round(np.random.default_rng(T).uniform(-0.02, 0.02, n), 3)  # ties
+    st = make_router(P, d, n, z, k, ke, bias=bias)
+    w_in, w_out = make_bank_arrays(n, d, I, 64)
+    bank = P.ExpertBank(w_in, w_out)
+    out, dg = P.scmoe_layer_forward(a1, a3, gain, st, bank)
+    idx = np.empty(T * k, np.uint32)
+    g = np.empty(T * k)
+    c = np.empty(T, np.uint32)
+    want = np.empty((T, d), np.float32)
+    rc = O.orc().orc_scmoe_layer_f32(ptr(a1), ptr(a3), ptr(gain), T, d, ptr(st.w), n, z, k, ke,
+                                     0.0, ptr(st.b), O.ptr_array(w_in), O.ptr_array(w_out), I,
+                                     1.0, 1.0, 0, ptr(idx), ptr(g), ptr(c), ptr(want))
+    assert rc == 0
+    assert (dg.indices == idx).all() and (dg.ffn_count == c).all()
+    assert (dg.gates.view(np.uint64) == g.view(np.uint64)).all()
+    assert (bits32(out) == bits32(want)).all()
+
+
 def test_empty_batch_is_a_noop(scmoe):
     P = scmoe
     st = make_router(P, 256, 8, 4, 2, 1)

@@ -961,6 +961,7 @@ __global__ void __launch_bounds__(256) front_small_kernel(
     if (tid < nt) {
         const float* x = xs + tid * d;
         float s2 = 0.0f;
+#pragma unroll 8
         for (int j = 0; j < d; ++j) s2 = __fadd_rn(s2, __fmul_rn(x[j], x[j]));
         inv[tid] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(s2, (float)d), eps)));
     }
@@ -978,6 +979,7 @@ __global__ void __launch_bounds__(256) front_small_kernel(
         const int r = tid / E, e = tid % E;
         const float* x = xs + r * d;
         float c = 0.f;
+#pragma unroll 8
         for (int k = 0; k < d; ++k) c = __fadd_rn(c, __fmul_rn(x[k], ws[k * E + e]));
         lg[r * 32 + e] = c;
     }

@@ -387,6 +387,7 @@ int scmoe_ctx_destroy(scmoe_ctx* c) {
         cudaStreamDestroy(c->s_d2h);
         for (int i = 0; i < 2; ++i) {
             cudaEventDestroy(c->ev_in[i]);
+            cudaEventDestroy(c->ev_in_a1[i]);
             cudaEventDestroy(c->ev_done[i]);
             cudaEventDestroy(c->ev_out[i]);
         }
@@ -1137,6 +1138,7 @@ int scmoe_layer_forward_host_batches(scmoe_ctx* c, scmoe_router* r, scmoe_bank* 
             SCMOE_CUDA(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
             for (int i = 0; i < 2; ++i) {
                 SCMOE_CUDA(cudaEventCreateWithFlags(&c->ev_in[i], cudaEventDisableTiming));
+                SCMOE_CUDA(cudaEventCreateWithFlags(&c->ev_in_a1[i], cudaEventDisableTiming));
                 SCMOE_CUDA(cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming));
                 SCMOE_CUDA(cudaEventCreateWithFlags(&c->ev_out[i], cudaEventDisableTiming));
             }
@@ -1167,15 +1169,21 @@ int scmoe_layer_forward_host_batches(scmoe_ctx* c, scmoe_router* r, scmoe_bank* 
             SCMOE_CUDA(cudaStreamWaitEvent(c->s_h2d, c->ev_done[s], 0));
             SCMOE_CUDA(cudaMemcpyAsync(da1, a1[i], T * d * sizeof(float), cudaMemcpyHostToDevice,
                                        c->s_h2d));
+            SCMOE_CUDA(cudaEventRecord(c->ev_in_a1[s], c->s_h2d));
             if (da3)
                 SCMOE_CUDA(cudaMemcpyAsync(da3, a3[i], T * d * sizeof(float),
                                            cudaMemcpyHostToDevice, c->s_h2d));
             SCMOE_CUDA(cudaEventRecord(c->ev_in[s], c->s_h2d));
             // compute(i): needs its inputs, and the slot's outputs drained by D2H(i-2)
-            SCMOE_CUDA(cudaStreamWaitEvent(comp, c->ev_in[s], 0));
+            // the front half needs a1 only: a3 (the residual) is still in flight
+            SCMOE_CUDA(cudaStreamWaitEvent(comp, c->ev_in_a1[s], 0));
             SCMOE_CUDA(cudaStreamWaitEvent(comp, c->ev_out[s], 0));
             layer_front(c, r, b, da1, dg, T, di, dgt, dc);
-            moe_back(c, b, c->ws.hmoe.get<float>(T * d), T, di, dgt, K, renorm, da3, dout);
+            moe_back(c, b, c->ws.hmoe.get<float>(T * d), T, di, dgt, K, renorm, nullptr, nullptr,
+                     /*phase=*/1);  // expert FFN
+            SCMOE_CUDA(cudaStreamWaitEvent(comp, c->ev_in[s], 0));  // a3 for the combine
+            moe_back(c, b, c->ws.hmoe.get<float>(T * d), T, di, dgt, K, renorm, da3, dout,
+                     /*phase=*/2);
             SCMOE_CUDA(cudaEventRecord(c->ev_done[s], comp));
             // D2H(i)
             SCMOE_CUDA(cudaStreamWaitEvent(c->s_d2h, c->ev_done[s], 0));

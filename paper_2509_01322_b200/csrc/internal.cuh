@@ -155,6 +155,7 @@ struct scmoe_ctx {
     // host-batch pipeline (scmoe_layer_forward_host_batches): copy streams,
     // per-slot events and double-buffered device I/O
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_in_a1[2] = {nullptr, nullptr};  // host tier: a1 landed (a3 may follow)
     cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr},
                 ev_out[2] = {nullptr, nullptr};
     DevBuf io[2][7];
